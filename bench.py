@@ -1,0 +1,302 @@
+#!/usr/bin/env python3
+"""Benchmark: aggregate decode tokens/s of colocated LLMs on B200 + the
+paged-attention kernel's HBM roofline fraction (BASELINE.json metric).
+
+Workload (BASELINE config 2): LLaMA-7B + LLaMA-13B (random-init weights)
+colocated on one B200 over ONE unified head-wise KV pool sized like the
+reference's (180 GiB mesh, 10% activation reserve, sim_engine.cpp:172-186).
+Each model holds a decode batch of B requests with ShareGPT-shaped lengths
+(lognormal mean 161 prompt / 338 output, sigma 0.8, workload.hpp:21) caught
+mid-generation. One step = one ADBS decode round (scheduler.cpp:90-117):
+BlockPool.alloc(+1 token) for every member of both models, then both decode
+jobs run concurrently on their own partition streams (full 32/40-layer
+forward: tcgen05 GEMMs, RoPE+KV append, head-wise paged attention, LM head,
+greedy argmax). Tokens per step = 2B.
+
+N GPUs (torchrun): every rank serves its own independent 7B+13B unit (units
+share nothing, sim_engine.hpp:74-80) -> weak scaling, no collective on the
+data path; timing is the max over ranks.
+
+--impl reference: the CPU port of the same decode step (oracle/numerics_ref.c:
+bf16 GEMVs + paged attention, all host threads) on a bounded sample (one layer
+of each model, scaled to the full step), printed as the reference arm.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import math
+import os
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+GIB = 1 << 30
+MESH_BYTES = int(180 * GIB)
+RESERVE = 0.1
+
+
+def peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            p = json.load(f)
+        return float(p["hbm_gbs"]), "measured"
+    except Exception:
+        return 6650.0, "fallback"
+
+
+def pool_blocks(specs):
+    weights = sum(s.weight_bytes for s in specs)
+    reserve = round(RESERVE * MESH_BYTES)
+    return (MESH_BYTES - weights - reserve) // 4096
+
+
+def sample_batch(rng, B, extra_steps):
+    """ShareGPT-shaped requests mid-generation: (prompt, output, steps_done)."""
+    import numpy as np
+    mu_p = math.log(161.0) - 0.32
+    mu_o = math.log(338.0) - 0.32
+    out = []
+    while len(out) < B:
+        p = max(1, int(round(rng.lognormal(mu_p, 0.8))))
+        o = max(1, int(round(rng.lognormal(mu_o, 0.8))))
+        if o < extra_steps + 2 or p + o > 4000:
+            continue
+        done = int(rng.integers(0, o - extra_steps - 1))
+        out.append((p, o, done))
+    return out
+
+
+class Clocks:
+    def __init__(self, index: int):
+        self.proc = None
+        self.path = os.path.join(ROOT, "gpurun_out", f"clocks_{index}.csv")
+        try:
+            os.makedirs(os.path.dirname(self.path), exist_ok=True)
+            q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+                 "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+                 "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+            self.f = open(self.path, "w")
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(index), f"--query-gpu={q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.proc = None
+
+    def stop(self):
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        self.proc.wait()
+        self.f.close()
+        sm, smax, reasons = [], None, set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in open(self.path):
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                smax = float(parts[2])
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        sm.sort()
+        med = sm[len(sm) // 2] if sm else None
+        return {"sm_mhz": med, "sm_max_mhz": smax, "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ------------------------------------------------------------------ our arm
+
+def run_ours(args, rank, world, local_rank):
+    import numpy as np
+    import torch
+
+    import paper_2404_02015_b200 as mux
+
+    torch.cuda.set_device(local_rank)
+    specs = [mux.spec(m) for m in args.models.split(",")]
+    B = args.batch
+    steps_total = args.warmup + args.steps + args.e2e_steps + 2
+    rng = np.random.default_rng(1000 + rank)
+    batches = [sample_batch(rng, B, steps_total) for _ in specs]
+    need = 0
+    for s, reqs in zip(specs, batches):
+        for p, o, d in reqs:
+            need += mux.blocks_for_tokens(s, 16, p + d + steps_total + 1)
+    logical = pool_blocks(specs)
+    assert need <= logical, "batch exceeds the unified pool"
+    max_ctx = max(p + d + steps_total + 1 for reqs in batches for p, o, d in reqs)
+    unit = mux.Unit(specs, pool_blocks=logical, device=local_rank, device_pool_blocks=need + 4096,
+                    max_batch=B, max_prefill_tokens=256, max_ctx=max_ctx + 16, max_slots=2 * B + 16,
+                    init_seed=1 + rank, init_std=0.02, partitions=len(specs) + 1)
+    unit.init_kv(seed=7 + rank, std=1.0)
+    pool = unit.pool
+    ids = []
+    for li, reqs in enumerate(batches):
+        rids = []
+        for k, (p, o, d) in enumerate(reqs):
+            rid = 10_000 * li + k
+            assert pool.admit(li, rid, p, p + o - 1).ok
+            if d:
+                assert pool.alloc(li, rid, d, False).ok
+            rids.append(rid)
+        ids.append(rids)
+    ids_c = [unit._ids(r) for r in ids]
+    ctx0 = [sum(pool.request_tokens(li, r) for r in ids[li]) for li in range(len(specs))]
+
+    def step(tokens=None, outs=None):
+        # one ADBS decode round: +1 token per member (BlockPool), then the jobs
+        for li in range(len(specs)):
+            for rid in ids[li]:
+                r = pool.alloc(li, rid, 1, False)
+                if not r.ok:
+                    raise RuntimeError("pool exhausted")
+            unit.decode(li, ids[li], tokens=None if tokens is None else tokens[li],
+                        out=None if outs is None else outs[li], partition=1 + li, ids_c=ids_c[li])
+
+    for _ in range(args.warmup):
+        step()
+    unit.sync()
+    if world > 1:
+        torch.distributed.barrier()
+    clocks = Clocks(local_rank)
+    unit.attn_timing(True)
+    launches0 = unit.launches()
+    unit.sync()
+    for li in range(len(specs)):
+        unit.record(1 + li, 2 * li)
+    for _ in range(args.steps):
+        step()
+    for li in range(len(specs)):
+        unit.record(1 + li, 2 * li + 1)
+    unit.sync()
+    # span from the first partition's start to the last partition's end
+    ms = max(unit.elapsed_ms(0, 2 * li + 1) for li in range(len(specs)))
+    launches = unit.launches() - launches0
+    attn_ms, attn_n, attn_bytes = unit.attn_time()
+    unit.attn_timing(False)
+    clk = clocks.stop()
+
+    # e2e: host token ids in (pinned) -> jobs -> next tokens out (pinned), each
+    # step waits for its result before the next, as a serving loop does.
+    pinned_in = [torch.zeros(B, dtype=torch.int32).pin_memory().numpy() for _ in specs]
+    pinned_out = [torch.zeros(B, dtype=torch.int32).pin_memory().numpy() for _ in specs]
+    unit.sync()
+    t0 = time.perf_counter()
+    for i in range(args.e2e_steps):
+        step(tokens=pinned_in, outs=pinned_out)
+        unit.sync()  # the step's result is on the host before the next step is issued
+        for li in range(len(specs)):
+            pinned_in[li][:] = pinned_out[li]
+    # wall clock of the serving loop through the public API (host timer)
+    e2e_ms = (time.perf_counter() - t0) * 1e3 / max(1, args.e2e_steps)
+
+    # step roofline: weights + KV bytes of both jobs per step
+    kv_tok = [s.kv_bytes_per_token() for s in specs]
+    bytes_step = 0.0
+    for li, s in enumerate(specs):
+        ctx_mid = ctx0[li] + B * (args.warmup + args.steps / 2 + 1)
+        bytes_step += s.weight_bytes + ctx_mid * kv_tok[li]
+    unit.close()
+    result = {
+        "ms": ms, "tokens": len(specs) * B * args.steps, "launches": launches,
+        "attn_ms": attn_ms, "attn_n": attn_n, "attn_bytes": attn_bytes, "clocks": clk,
+        "e2e_ms": e2e_ms, "bytes_step": bytes_step,
+    }
+    return result
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--batch", type=int, default=128, help="decode members per model")
+    ap.add_argument("--models", default="7b,13b")
+    ap.add_argument("--e2e-steps", type=int, default=4)
+    args = ap.parse_args()
+
+    rank = int(os.environ.get("RANK", "0"))
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+
+    if args.impl == "reference":
+        if rank != 0:
+            return
+        from bench_cpu import reference_arm
+        print(json.dumps(reference_arm(args)), flush=True)
+        return
+
+    import torch
+    if world > 1:
+        torch.distributed.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+    r = run_ours(args, rank, world, local_rank)
+    ms = r["ms"]
+    tokens = r["tokens"]
+    if world > 1:
+        t = torch.tensor([ms, r["e2e_ms"]], dtype=torch.float64, device="cuda")
+        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
+        ms, e2e_ms = t.tolist()
+        tokens *= world
+    else:
+        e2e_ms = r["e2e_ms"]
+    hbm, peak_kind = peaks()
+    achieved = r["attn_bytes"] / (r["attn_ms"] / 1e3) / 1e9 if r["attn_ms"] > 0 else 0.0
+    value = tokens / (ms / 1e3)
+    per_step_tokens = tokens / args.steps
+    cpu = None
+    if rank == 0 and world == 1:
+        from bench_cpu import cpu_baseline
+        cpu = cpu_baseline(args)
+    if rank == 0:
+        # whole-job roofline: every rank streams its own weights + KV per step
+        step_roof = per_step_tokens / (r["bytes_step"] / (hbm * 1e9)) if r["bytes_step"] else None
+        line = {
+            "metric": "aggregate decode tokens/s across colocated LLMs; paged-attn HBM GB/s vs peak",
+            "value": round(value, 1),
+            "unit": "tokens/s",
+            "n_gpus": world,
+            "steps": args.steps,
+            "warmup": args.warmup,
+            "ms_per_step": round(ms / args.steps, 4),
+            "higher_is_better": True,
+            "scaling": "weak",
+            "vs_baseline": None,
+            "dtype": "bf16",
+            "data": "synthetic (random-init weights, ShareGPT-shaped lognormal lengths, random KV)",
+            "config": {
+                "workload": "cfg2: LLaMA-7B + LLaMA-13B colocated per B200, one ADBS decode round per step",
+                "models": args.models, "decode_batch_per_model": args.batch,
+                "pool_blocks": pool_blocks([__import__("paper_2404_02015_b200").spec(m) for m in args.models.split(",")]),
+                "l2": "inputs larger than L2 (39.5 GB weights + KV per step)",
+                "parallelism": f"{world} independent units (dp{world})",
+            },
+            "e2e": {"value": round(per_step_tokens / (e2e_ms / 1e3), 1) if e2e_ms else None,
+                    "unit": "tokens/s", "h2d_bytes_per_step": int(per_step_tokens * 4),
+                    "d2h_bytes_per_step": int(per_step_tokens * 4)},
+            "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
+                         "frac": round(achieved / hbm, 4), "traffic": None,
+                         "kernel": "decode_attention_kernel (K1, per-launch CUDA events)",
+                         "peak_source": peak_kind, "launches_timed": r["attn_n"],
+                         "bytes_per_launch": round(r["attn_bytes"] / max(1, r["attn_n"]))},
+            "step_roofline": {"tokens_per_s_at_peak": round(step_roof, 1) if step_roof else None,
+                              "frac": round(value / step_roof, 4) if step_roof else None},
+            "cpu_baseline": cpu,
+            "gpu_launches": r["launches"] * world,
+            "clocks": r["clocks"],
+        }
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        torch.distributed.barrier()
+        torch.distributed.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

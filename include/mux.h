@@ -1,0 +1,257 @@
+/*
+ * mux.h -- C ABI of the B200-native MuxServe hot path (libmux.so).
+ *
+ * Plain C: pointers, sizes and status codes only; no C++ or torch types cross
+ * it. Every entry point names the reference interface it replaces
+ * (/root/reference/proj/...). The reference has no FFI of its own (its API is
+ * C++), so this is the surface a foreign host (ctypes, cgo,
+ * JNI) binds; INTEGRATION.md shows the bindings.
+ *
+ * Status codes mirror the reference's exception classes:
+ *   MUX_OK             success
+ *   MUX_EINVAL   (1)   std::invalid_argument / std::domain_error / ConfigError
+ *   MUX_EINFEAS  (2)   InfeasibleError          (/root/reference/proj/tools/muxsim.cpp:51-53)
+ *   MUX_EINTERNAL(3)   std::logic_error and everything else (incl. CUDA errors)
+ * mux_last_error() returns the message of the last failure on this thread
+ * (the reference's what() text where one exists).
+ *
+ * Device pointers are raw CUDA pointers on the unit's device; host pointers
+ * are borrowed for the duration of the call. Calls are stream-ordered on the
+ * partition they name; mux_unit_sync() waits for all of them.
+ */
+#ifndef MUX_H_
+#define MUX_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#if defined(__GNUC__)
+#define MUX_API __attribute__((visibility("default")))
+#else
+#define MUX_API
+#endif
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define MUX_OK 0
+#define MUX_EINVAL 1
+#define MUX_EINFEAS 2
+#define MUX_EINTERNAL 3
+
+/* AllocResult.error (kv_manager.hpp:32-39): 0 = None (ok), 1 = Pool, 2 = Quota. */
+#define MUX_ALLOC_OK 0
+#define MUX_ALLOC_POOL 1
+#define MUX_ALLOC_QUOTA 2
+
+MUX_API const char* mux_last_error(void);
+MUX_API const char* mux_version(void);
+
+/* ---- geometry and quotas --------------------------------------------- */
+
+/* blocks_for_tokens (kv_manager.hpp:28-29, kv_manager.cpp:30-35). */
+MUX_API int mux_blocks_for_tokens(int num_layers, int num_heads, int block_tokens, int64_t tokens,
+                          int64_t* out);
+
+/* init_token_block_quota (kv_manager.hpp:117-119, kv_manager.cpp:222-280). */
+MUX_API int mux_init_token_block_quota(int n, const double* rate, const double* blocks_per_token,
+                               const double* mean_request_tokens, int64_t kv_blocks,
+                               double floor_frac, int64_t* out_quotas);
+
+/* adapt_quota (kv_manager.hpp:132-135, kv_manager.cpp:282-323). */
+MUX_API int mux_adapt_quota(int n, const double* utilizations, const int64_t* quotas,
+                    int64_t floor_blocks, double low_mark, double high_mark, double step_frac,
+                    int64_t* out_quotas);
+
+/* ---- unified head-wise block pool (BlockPool, kv_manager.hpp:48-105) ---- */
+
+typedef struct mux_pool mux_pool;
+
+/* BlockPool(total_blocks) (kv_manager.hpp:50). physical != 0 also assigns
+ * physical 4 KiB head-block ids (the B200 extension). */
+MUX_API int mux_pool_create(int64_t total_blocks, int physical, mux_pool** out);
+MUX_API void mux_pool_destroy(mux_pool* pool);
+/* register_llm (kv_manager.hpp:53). */
+MUX_API int mux_pool_register_llm(mux_pool* pool, int llm, int num_layers, int num_heads, int head_dim,
+                          int bytes_per_element, int block_tokens);
+/* admit (kv_manager.hpp:59-60); *result = MUX_ALLOC_*. */
+MUX_API int mux_pool_admit(mux_pool* pool, int llm, int64_t request_id, int64_t prompt_tokens,
+                   int64_t total_tokens, int* result);
+/* alloc (kv_manager.hpp:65). */
+MUX_API int mux_pool_alloc(mux_pool* pool, int llm, int64_t request_id, int64_t add_tokens,
+                   int enforce_quota, int* result);
+/* free_request (kv_manager.hpp:69). */
+MUX_API int mux_pool_free_request(mux_pool* pool, int llm, int64_t request_id);
+/* set_quota / quota / used / committed / request_tokens (kv_manager.hpp:71-79). */
+MUX_API int mux_pool_set_quota(mux_pool* pool, int llm, int64_t blocks);
+MUX_API int mux_pool_llm_stats(const mux_pool* pool, int llm, int64_t* quota, int64_t* used,
+                       int64_t* committed);
+MUX_API int mux_pool_request_tokens(const mux_pool* pool, int llm, int64_t request_id, int64_t* tokens);
+/* free_blocks / total_blocks / committed_total (kv_manager.hpp:80-83). */
+MUX_API int mux_pool_totals(const mux_pool* pool, int64_t* free_blocks, int64_t* total_blocks,
+                    int64_t* committed_total);
+/* check_conservation (kv_manager.hpp:87). */
+MUX_API int mux_pool_check(const mux_pool* pool);
+/* Physical block table of one request: [rows][layer][head][K/V] int32. */
+MUX_API int mux_pool_block_table(const mux_pool* pool, int llm, int64_t request_id, int32_t* out,
+                         int64_t capacity, int64_t* n_out);
+MUX_API int mux_pool_slot(const mux_pool* pool, int llm, int64_t request_id, int* slot);
+
+/* ---- engine: run_simulation (sim_engine.hpp:81-83) -------------------- */
+
+typedef struct {
+  const char* name;
+  int num_layers, num_heads, head_dim, hidden_size;
+  int64_t weight_bytes;
+  int bytes_per_element;
+  double rate, mean_prompt_tokens, mean_output_tokens;  /* LlmEntry (placement.hpp:38-43) */
+  /* B200 execution (ignored when priced): FFN width and vocabulary. */
+  int ffn, vocab;
+} mux_llm_entry;
+
+typedef struct {
+  int unit;           /* index into the placement's unit list */
+  int llm;            /* index into the entries array */
+  int tp_degree;
+  double num_sm;
+} mux_placed_llm;
+
+typedef struct {
+  int num_nodes, gpus_per_node;
+  int64_t gpu_memory_bytes;
+  int n_units;
+  const int* unit_mesh_size;   /* [n_units] gpus per mesh (tp) */
+  int n_placed;
+  const mux_placed_llm* placed;
+  /* LatencyProfile (cost_model.hpp:33-50); NULL fields use the defaults. */
+  const double* profile;       /* 7 doubles in declaration order, or NULL */
+  /* EngineParams (sim_engine.hpp:15-28) */
+  int scheduler;               /* 0 ADBS, 1 FCFS, 2 round-robin */
+  double kappa, quota_period_s;
+  int64_t token_budget;
+  int block_tokens;
+  double warmup_s, decode_sm, prefill_min_sm, activation_reserve_frac, quota_floor_frac;
+} mux_sim_config;
+
+typedef struct {
+  int64_t id;
+  int llm;                     /* entry index */
+  double arrival_s;
+  int prompt_len, output_len;
+} mux_request;
+
+typedef struct {
+  int64_t id;
+  int llm;
+  double arrival_s, first_token_s, done_s;
+  int prompt_len, output_len;
+} mux_record;
+
+/* Priced run (the reference simulator's semantics, bit-identical). */
+MUX_API int mux_simulate(const mux_sim_config* cfg, int n_entries, const mux_llm_entry* entries,
+                 int n_requests, const mux_request* trace, mux_record* records_out);
+
+/* ---- kernels (device pointers; stream = cudaStream_t or NULL) --------- */
+
+/* K1: head-wise paged decode attention for one layer (the work priced by
+ * the c_ctx term of decode_step_latency, cost_model.cpp:85-94).
+ * q [B][H][128] bf16, pool [blocks][16][128] bf16, rowrec [*][L*H*2] int32,
+ * rowlist [slots][max_rows] int32, slots/ctx [B] int32, out [B][H][128]
+ * (fp32 if out_fp32 else bf16). kv_splits = 0 picks automatically. */
+MUX_API int mux_decode_attention_headwise(const void* q, const void* pool, const int32_t* rowrec,
+                                  const int32_t* rowlist, const int32_t* slots,
+                                  const int32_t* ctx, int B, int H, int num_layers, int layer,
+                                  int max_rows, int max_ctx, void* out, int out_fp32,
+                                  int kv_splits, void* workspace, size_t workspace_bytes,
+                                  void* stream);
+
+/* K2: RoPE + KV append (the device side of BlockPool::alloc's new token,
+ * scheduler.cpp:105). qkv [T][3][H][128] bf16; q_out [T][H][128] (nullable). */
+MUX_API int mux_kv_append(const void* qkv, void* q_out, void* pool, const int32_t* rowrec,
+                  const int32_t* rowlist, const int32_t* tok_slot, const int32_t* tok_pos,
+                  const float* rope_table, int rope_positions, int T, int H, int num_layers,
+                  int layer, int max_rows, void* stream);
+/* RoPE table [positions][64][(cos,sin)] fp32, theta 10000, head_dim 128. */
+MUX_API int mux_rope_table(int positions, float* out);
+
+/* K4: D[M x N] = X[M x K] * W[N x K]^T on tcgen05 (bf16 in, fp32 acc).
+ * epilogue: 0 bf16 store, 1 fp32 split-K partials [splits][M][N],
+ * 2 SiLU(gate)*up over interleaved rows -> bf16 [M][N/2], 3 fp32 store. */
+MUX_API int mux_gemm_bf16(const void* x, const void* w, int M, int N, int K, void* out, int epilogue,
+                  int splits, void* stream);
+
+/* ---- device unit: one GPU, its KV pool and colocated models ---------- */
+
+typedef struct mux_unit mux_unit;
+
+typedef struct {
+  int device;
+  int n_llms;
+  const mux_llm_entry* llms;
+  int64_t pool_blocks;          /* logical pool (count semantics) */
+  int64_t device_pool_blocks;   /* physically allocated head-blocks (0 = pool_blocks) */
+  int max_batch;                /* decode members per job */
+  int max_prefill_tokens;       /* prompt tokens per prefill job */
+  int max_ctx;                  /* longest request (tokens) */
+  int max_slots;                /* live requests per model */
+  uint64_t init_seed;           /* random N(0, init_std) weights; 0 = leave for set_tensor */
+  float init_std;
+  int partitions;               /* concurrent job streams */
+} mux_unit_config;
+
+MUX_API int mux_unit_create(const mux_unit_config* cfg, mux_unit** out);
+MUX_API void mux_unit_destroy(mux_unit* unit);
+/* The unit's block pool (owned by the unit; do not destroy). */
+MUX_API mux_pool* mux_unit_pool(mux_unit* unit);
+/* Upload / read one weight tensor in device layout:
+ *  embed, lm_head [vocab][hidden] bf16; final_norm [hidden] fp32;
+ *  per layer: wqkv [3*H*128][hidden], wo [hidden][H*128],
+ *  wgu [2*ffn][hidden] rows interleaved (gate_0, up_0, gate_1, ...),
+ *  wdown [hidden][ffn] bf16; attn_norm, ffn_norm [hidden] fp32. */
+MUX_API int mux_unit_set_tensor(mux_unit* unit, int llm, const char* name, int layer, const void* host,
+                        size_t bytes);
+MUX_API int mux_unit_get_tensor(mux_unit* unit, int llm, const char* name, int layer, void* host,
+                        size_t bytes);
+/* Fill the whole KV pool with N(0, std) bf16 (benchmarks). */
+MUX_API int mux_unit_init_kv(mux_unit* unit, uint64_t seed, float std);
+/* Device pointers for tests: pool, rowrec/rowlist/last_tok of a model. */
+MUX_API int mux_unit_device_ptrs(mux_unit* unit, int llm, void** pool, void** rowrec, void** rowlist,
+                         int* max_rows, int* row_width);
+/* Prefill job (sim_engine.cpp:308 launch of a Prefill JobPlan): requests must
+ * be admitted in the unit pool; tokens = concatenated prompts (host);
+ * out_tokens (host, nullable) receives each request's first token. */
+MUX_API int mux_unit_prefill(mux_unit* unit, int llm, int n, const int64_t* request_ids,
+                     const int32_t* tokens, int32_t* out_tokens, int partition);
+/* Decode job: every member already grew by one token in the pool (the ADBS
+ * decode round, scheduler.cpp:105). tokens (host, nullable) = input tokens;
+ * NULL uses each request's last generated token (device resident). */
+MUX_API int mux_unit_decode(mux_unit* unit, int llm, int n, const int64_t* request_ids,
+                    const int32_t* tokens, int32_t* out_tokens, int partition);
+MUX_API int mux_unit_sync(mux_unit* unit);
+/* Device-side timing: record event `slot` (0..63) on a partition stream;
+ * elapsed milliseconds between two recorded slots (synchronises). */
+MUX_API int mux_unit_record(mux_unit* unit, int partition, int slot);
+MUX_API int mux_unit_elapsed(mux_unit* unit, int slot_a, int slot_b, float* ms);
+/* Per-launch decode-attention timing (CUDA events around every K1 launch):
+ * enable, then read the summed kernel milliseconds and launch count. */
+MUX_API int mux_unit_attn_timing(mux_unit* unit, int enable);
+MUX_API int mux_unit_attn_time(mux_unit* unit, double* total_ms, int64_t* launches, double* bytes);
+/* Kernel launches issued by this unit so far (all libmux kernels). */
+MUX_API int64_t mux_unit_launches(mux_unit* unit);
+
+/* Lockstep run: the engine's decisions are those of mux_simulate (oracle
+ * timing), and every launched job executes on the unit's GPU. Synthetic
+ * prompt tokens come from (seed, request id). tokens_out (nullable) receives
+ * all generated tokens, request-major in trace order; each request writes
+ * output_len tokens. Single-unit placements only; entries[i] must describe
+ * the unit's model i (rates and mean lengths seed the ADBS quotas). */
+MUX_API int mux_unit_run_lockstep(mux_unit* unit, const mux_sim_config* cfg, int n_entries,
+                          const mux_llm_entry* entries, int n_requests, const mux_request* trace,
+                          uint64_t prompt_seed, mux_record* records_out, int32_t* tokens_out);
+
+#ifdef __cplusplus
+}
+#endif
+
+#endif /* MUX_H_ */

@@ -1,0 +1,721 @@
+// C ABI (include/mux.h): exception -> status mapping, handles, and the
+// lockstep JobExecutor that runs the engine's JobPlans on the GPU.
+#include "../../include/mux.h"
+
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <deque>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <unordered_map>
+#include <vector>
+
+#include "device/runtime.h"
+#include "kernels/kernels.h"
+#include "mux/engine.hpp"
+#include "mux/kv.hpp"
+
+using muxsim::BlockPool;
+
+struct mux_pool {
+  BlockPool* bp = nullptr;
+  std::unique_ptr<BlockPool> owned;
+  std::deque<muxsim::LLMSpec> specs;  // stable addresses for register_llm
+};
+
+namespace {
+
+thread_local std::string g_err;
+
+template <typename F>
+int guarded(F&& f) {
+  try {
+    f();
+    return MUX_OK;
+  } catch (const muxsim::InfeasibleError& e) {
+    g_err = e.what();
+    return MUX_EINFEAS;
+  } catch (const std::invalid_argument& e) {
+    g_err = e.what();
+    return MUX_EINVAL;
+  } catch (const std::domain_error& e) {
+    g_err = e.what();
+    return MUX_EINVAL;
+  } catch (const std::exception& e) {
+    g_err = e.what();
+    return MUX_EINTERNAL;
+  } catch (...) {
+    g_err = "unknown error";
+    return MUX_EINTERNAL;
+  }
+}
+
+void require(bool ok, const char* msg) {
+  if (!ok) throw std::invalid_argument(msg);
+}
+
+int alloc_code(const muxsim::AllocResult& r) {
+  if (r.ok) return MUX_ALLOC_OK;
+  return r.error == muxsim::AllocError::Quota ? MUX_ALLOC_QUOTA : MUX_ALLOC_POOL;
+}
+
+muxsim::LLMSpec spec_of(const mux_llm_entry& e) {
+  muxsim::LLMSpec s;
+  s.name = e.name ? e.name : "";
+  s.num_layers = e.num_layers;
+  s.num_heads = e.num_heads;
+  s.head_dim = e.head_dim;
+  s.hidden_size = e.hidden_size;
+  s.weight_bytes = e.weight_bytes;
+  s.bytes_per_element = e.bytes_per_element;
+  return s;
+}
+
+struct SimInputs {
+  muxsim::Cluster cluster;
+  muxsim::PlacementResult placement;
+  std::vector<muxsim::LlmEntry> entries;
+  std::vector<muxsim::Request> trace;
+  muxsim::LatencyProfile prof;
+  muxsim::EngineParams params;
+};
+
+SimInputs build_inputs(const mux_sim_config* c, int n_entries, const mux_llm_entry* entries, int n_req,
+                       const mux_request* trace) {
+  require(c != nullptr && entries != nullptr && (n_req == 0 || trace != nullptr), "null argument");
+  SimInputs in;
+  in.cluster.num_nodes = c->num_nodes;
+  in.cluster.gpus_per_node = c->gpus_per_node;
+  in.cluster.gpu_memory_bytes = c->gpu_memory_bytes;
+  for (int i = 0; i < n_entries; ++i) {
+    muxsim::LlmEntry e;
+    e.spec = spec_of(entries[i]);
+    e.rate = entries[i].rate;
+    e.mean_prompt_tokens = entries[i].mean_prompt_tokens;
+    e.mean_output_tokens = entries[i].mean_output_tokens;
+    in.entries.push_back(e);
+  }
+  in.placement.backend = "greedy";
+  int gpu = 0;
+  for (int u = 0; u < c->n_units; ++u) {
+    muxsim::LLMUnit lu;
+    lu.mesh.node = 0;
+    for (int g = 0; g < c->unit_mesh_size[u]; ++g) lu.mesh.gpu_ids.push_back(gpu++);
+    in.placement.units.push_back(lu);
+  }
+  for (int i = 0; i < c->n_placed; ++i) {
+    const mux_placed_llm& p = c->placed[i];
+    require(p.unit >= 0 && p.unit < c->n_units && p.llm >= 0 && p.llm < n_entries, "bad placement");
+    muxsim::PlacedLlm pl;
+    pl.llm = p.llm;
+    pl.candidate.tp_degree = p.tp_degree;
+    pl.candidate.num_sm = p.num_sm;
+    in.placement.units[p.unit].llms.push_back(pl);
+  }
+  for (int i = 0; i < n_req; ++i) {
+    require(trace[i].llm >= 0 && trace[i].llm < n_entries, "trace llm out of range");
+    muxsim::Request r;
+    r.id = trace[i].id;
+    r.llm = in.entries[trace[i].llm].spec.name;
+    r.arrival_s = trace[i].arrival_s;
+    r.prompt_len = trace[i].prompt_len;
+    r.output_len = trace[i].output_len;
+    in.trace.push_back(r);
+  }
+  if (c->profile) {
+    const double* p = c->profile;
+    in.prof.prefill_ms_per_token = p[0];
+    in.prof.decode_base_ms = p[1];
+    in.prof.decode_ctx_ms_per_token = p[2];
+    in.prof.tp_efficiency = p[3];
+    in.prof.sm_saturation_point = p[4];
+    in.prof.batch_knee = p[5];
+    in.prof.reference_scale = p[6];
+  }
+  in.params.scheduler = static_cast<muxsim::SchedKind>(c->scheduler);
+  in.params.kappa = c->kappa;
+  in.params.quota_period_s = c->quota_period_s;
+  in.params.token_budget = c->token_budget;
+  in.params.block_tokens = c->block_tokens;
+  in.params.warmup_s = c->warmup_s;
+  in.params.decode_sm = c->decode_sm;
+  in.params.prefill_min_sm = c->prefill_min_sm;
+  in.params.activation_reserve_frac = c->activation_reserve_frac;
+  in.params.quota_floor_frac = c->quota_floor_frac;
+  return in;
+}
+
+void export_records(const muxsim::SimResult& res, const SimInputs& in, mux_record* out) {
+  if (out == nullptr) return;
+  std::unordered_map<std::string, int> idx;
+  for (size_t i = 0; i < in.entries.size(); ++i) idx[in.entries[i].spec.name] = static_cast<int>(i);
+  for (size_t i = 0; i < res.records.size(); ++i) {
+    const muxsim::RequestRecord& r = res.records[i];
+    out[i] = {r.id, idx[r.llm], r.arrival_s, r.first_token_s, r.done_s, r.prompt_len, r.output_len};
+  }
+}
+
+uint64_t mix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+}  // namespace
+
+// -------------------------------------------------------------------- unit
+
+struct mux_unit {
+  std::unique_ptr<mux::Runtime> rt;
+  std::deque<muxsim::LLMSpec> specs;
+  std::vector<std::unique_ptr<mux::Llama>> models;
+  mux_pool pool;
+  std::vector<cudaStream_t> streams;
+  std::vector<std::unique_ptr<mux::Workspace>> ws;
+  cudaEvent_t ev[64] = {};
+  bool timing = false;
+  mux::AttnTimer timer;
+  int max_batch = 0;
+  int max_prefill = 0;
+  ~mux_unit() {
+    if (rt) cudaDeviceSynchronize();
+    ws.clear();
+    for (cudaStream_t s : streams) cudaStreamDestroy(s);
+    for (cudaEvent_t e : ev)
+      if (e) cudaEventDestroy(e);
+  }
+  cudaStream_t stream(int p) {
+    if (p < 0 || p >= static_cast<int>(streams.size())) throw std::invalid_argument("bad partition");
+    return streams[p];
+  }
+  mux::Llama& model(int llm) {
+    if (llm < 0 || llm >= static_cast<int>(models.size())) throw std::invalid_argument("bad llm index");
+    return *models[llm];
+  }
+};
+
+namespace {
+
+// Lockstep executor: JobPlans decided by the engine (oracle timing) run on
+// the unit's GPU; completion is consumed only after the device finished.
+class GpuExecutor : public muxsim::JobExecutor {
+ public:
+  GpuExecutor(mux_unit* u, uint64_t prompt_seed, const std::vector<muxsim::Request>& trace)
+      : u_(u), seed_(prompt_seed) {
+    for (size_t i = 0; i < trace.size(); ++i) row_of_id_[trace[i].id] = static_cast<int>(i);
+    tokens_.resize(trace.size());
+    check(cudaEventCreateWithFlags(&tables_ready_, cudaEventDisableTiming));
+  }
+  ~GpuExecutor() override {
+    for (auto& kv : jobs_) cudaEventDestroy(kv.second.done);
+    cudaEventDestroy(tables_ready_);
+  }
+
+  void attach_unit(int, const std::vector<const muxsim::LLMSpec*>& specs, BlockPool& pool) override {
+    if (specs.size() != u_->models.size()) throw std::invalid_argument("lockstep: model count mismatch");
+    for (size_t i = 0; i < specs.size(); ++i) {
+      const mux::ModelDims& d = u_->models[i]->dims();
+      if (specs[i]->num_layers != d.layers || specs[i]->num_heads != d.heads)
+        throw std::invalid_argument("lockstep: model " + specs[i]->name + " does not match the unit");
+    }
+    if (pool.total_blocks() > INT32_MAX) throw std::invalid_argument("lockstep: pool too large");
+  }
+
+  void begin_pass(int, BlockPool& pool) override {
+    cudaStream_t s0 = u_->streams[0];
+    for (int i = 0; i < static_cast<int>(u_->models.size()); ++i)
+      u_->rt->upload_rows(pool, i, *u_->models[i], s0);
+    check(cudaEventRecord(tables_ready_, s0));
+    for (size_t p = 1; p < u_->streams.size(); ++p) check(cudaStreamWaitEvent(u_->streams[p], tables_ready_, 0));
+  }
+
+  void launch(const muxsim::JobLaunch& j) override {
+    const muxsim::UnitState& st = *j.state;
+    const int P = static_cast<int>(u_->streams.size());
+    const int part = j.kind == muxsim::JobKind::Prefill || P == 1 ? 0 : 1 + (j.llm % (P - 1));
+    cudaStream_t s = u_->streams[part];
+    mux::Llama& m = *u_->models[j.llm];
+    mux::Workspace& ws = *u_->ws[part];
+    const int n = static_cast<int>(j.members->size());
+    Job job;
+    job.members = *j.members;
+    job.out = std::make_unique<mux::PinnedMem>(static_cast<size_t>(n) * 4);
+    std::vector<int32_t> slots(n), aux(n);
+    for (int i = 0; i < n; ++i) {
+      const int rid = (*j.members)[i];
+      slots[i] = j.pool->slot_of(j.llm, rid);
+      if (j.kind == muxsim::JobKind::Prefill) {
+        aux[i] = st.requests[rid].prompt_len;
+      } else {
+        aux[i] = static_cast<int32_t>(j.pool->request_tokens(j.llm, rid));
+      }
+    }
+    if (j.kind == muxsim::JobKind::Prefill) {
+      std::vector<int32_t> toks;
+      for (int i = 0; i < n; ++i) {
+        const muxsim::UnitRequest& r = st.requests[(*j.members)[i]];
+        for (int p = 0; p < r.prompt_len; ++p)
+          toks.push_back(static_cast<int32_t>(mix64(seed_ ^ mix64(static_cast<uint64_t>(r.global_id) * 131071u + p)) %
+                                              static_cast<uint64_t>(m.dims().vocab)));
+      }
+      u_->rt->prefill(m, ws, n, slots.data(), aux.data(), toks.data(), job.out->as<int32_t>(), s);
+    } else {
+      u_->rt->decode(m, ws, n, slots.data(), aux.data(), nullptr, job.out->as<int32_t>(), s,
+                     u_->timing ? &u_->timer : nullptr);
+    }
+    check(cudaEventCreateWithFlags(&job.done, cudaEventDisableTiming));
+    check(cudaEventRecord(job.done, s));
+    job.llm = j.llm;
+    job.global_ids.resize(n);
+    for (int i = 0; i < n; ++i) job.global_ids[i] = st.requests[(*j.members)[i]].global_id;
+    jobs_.emplace(j.job_id, std::move(job));
+  }
+
+  void retire(int, std::int64_t job_id) override {
+    auto it = jobs_.find(job_id);
+    if (it == jobs_.end()) throw std::logic_error("lockstep: retire of unknown job");
+    Job& job = it->second;
+    check(cudaEventSynchronize(job.done));
+    const int32_t* out = job.out->as<int32_t>();
+    for (size_t i = 0; i < job.global_ids.size(); ++i) {
+      auto r = row_of_id_.find(job.global_ids[i]);
+      if (r != row_of_id_.end()) tokens_[r->second].push_back(out[i]);
+    }
+    cudaEventDestroy(job.done);
+    jobs_.erase(it);
+  }
+
+  void detach_unit(int) override { check(cudaDeviceSynchronize()); }
+
+  const std::vector<std::vector<int32_t>>& tokens() const { return tokens_; }
+
+ private:
+  struct Job {
+    int llm = -1;
+    std::vector<int> members;
+    std::vector<int64_t> global_ids;
+    std::unique_ptr<mux::PinnedMem> out;
+    cudaEvent_t done = nullptr;
+  };
+  static void check(cudaError_t e) { mux::check_cuda(e, "lockstep executor"); }
+  mux_unit* u_;
+  uint64_t seed_;
+  std::unordered_map<int64_t, int> row_of_id_;
+  std::vector<std::vector<int32_t>> tokens_;
+  std::unordered_map<int64_t, Job> jobs_;
+  cudaEvent_t tables_ready_ = nullptr;
+};
+
+}  // namespace
+
+extern "C" {
+
+const char* mux_last_error(void) { return g_err.c_str(); }
+const char* mux_version(void) { return "mux-b200 0.1 (sm_100a)"; }
+
+int mux_blocks_for_tokens(int num_layers, int num_heads, int block_tokens, int64_t tokens, int64_t* out) {
+  return guarded([&] {
+    muxsim::LLMSpec s;
+    s.num_layers = num_layers;
+    s.num_heads = num_heads;
+    *out = muxsim::blocks_for_tokens(s, block_tokens, tokens);
+  });
+}
+
+int mux_init_token_block_quota(int n, const double* rate, const double* bpt, const double* mean_tokens,
+                               int64_t kv_blocks, double floor_frac, int64_t* out) {
+  return guarded([&] {
+    std::vector<muxsim::QuotaInput> in(n);
+    for (int i = 0; i < n; ++i) in[i] = {rate[i], bpt[i], mean_tokens[i]};
+    std::vector<int64_t> q = muxsim::init_token_block_quota(in, kv_blocks, floor_frac);
+    std::copy(q.begin(), q.end(), out);
+  });
+}
+
+int mux_adapt_quota(int n, const double* util, const int64_t* quotas, int64_t floor_blocks, double low,
+                    double high, double step, int64_t* out) {
+  return guarded([&] {
+    muxsim::QuotaAdaptParams p{low, high, step};
+    std::vector<int64_t> q = muxsim::adapt_quota(std::vector<double>(util, util + n),
+                                                 std::vector<int64_t>(quotas, quotas + n), floor_blocks, p);
+    std::copy(q.begin(), q.end(), out);
+  });
+}
+
+int mux_pool_create(int64_t total_blocks, int physical, mux_pool** out) {
+  return guarded([&] {
+    auto p = std::make_unique<mux_pool>();
+    p->owned = std::make_unique<BlockPool>(total_blocks);
+    p->bp = p->owned.get();
+    if (physical) p->bp->enable_physical();
+    *out = p.release();
+  });
+}
+
+void mux_pool_destroy(mux_pool* pool) { delete pool; }
+
+int mux_pool_register_llm(mux_pool* pool, int llm, int layers, int heads, int head_dim, int bpe, int block_tokens) {
+  return guarded([&] {
+    muxsim::LLMSpec s;
+    s.name = "llm" + std::to_string(llm);
+    s.num_layers = layers;
+    s.num_heads = heads;
+    s.head_dim = head_dim;
+    s.hidden_size = heads * head_dim;
+    s.weight_bytes = 1;
+    s.bytes_per_element = bpe;
+    pool->specs.push_back(s);
+    pool->bp->register_llm(llm, &pool->specs.back(), block_tokens);
+  });
+}
+
+int mux_pool_admit(mux_pool* pool, int llm, int64_t rid, int64_t prompt, int64_t total, int* result) {
+  return guarded([&] { *result = alloc_code(pool->bp->admit(llm, rid, prompt, total)); });
+}
+
+int mux_pool_alloc(mux_pool* pool, int llm, int64_t rid, int64_t add, int enforce, int* result) {
+  return guarded([&] { *result = alloc_code(pool->bp->alloc(llm, rid, add, enforce != 0)); });
+}
+
+int mux_pool_free_request(mux_pool* pool, int llm, int64_t rid) {
+  return guarded([&] { pool->bp->free_request(llm, rid); });
+}
+
+int mux_pool_set_quota(mux_pool* pool, int llm, int64_t blocks) {
+  return guarded([&] { pool->bp->set_quota(llm, blocks); });
+}
+
+int mux_pool_llm_stats(const mux_pool* pool, int llm, int64_t* quota, int64_t* used, int64_t* committed) {
+  return guarded([&] {
+    if (quota) *quota = pool->bp->quota(llm);
+    if (used) *used = pool->bp->used(llm);
+    if (committed) *committed = pool->bp->committed(llm);
+  });
+}
+
+int mux_pool_request_tokens(const mux_pool* pool, int llm, int64_t rid, int64_t* tokens) {
+  return guarded([&] { *tokens = pool->bp->request_tokens(llm, rid); });
+}
+
+int mux_pool_totals(const mux_pool* pool, int64_t* free_blocks, int64_t* total, int64_t* committed) {
+  return guarded([&] {
+    if (free_blocks) *free_blocks = pool->bp->free_blocks();
+    if (total) *total = pool->bp->total_blocks();
+    if (committed) *committed = pool->bp->committed_total();
+  });
+}
+
+int mux_pool_check(const mux_pool* pool) {
+  return guarded([&] { pool->bp->check_conservation(); });
+}
+
+int mux_pool_block_table(const mux_pool* pool, int llm, int64_t rid, int32_t* out, int64_t cap, int64_t* n_out) {
+  return guarded([&] {
+    if (!pool->bp->physical()) throw std::logic_error("block pool: physical ids are disabled");
+    std::vector<int32_t> t = pool->bp->block_table(llm, rid);
+    *n_out = static_cast<int64_t>(t.size());
+    if (out) std::copy_n(t.begin(), std::min<int64_t>(cap, *n_out), out);
+  });
+}
+
+int mux_pool_slot(const mux_pool* pool, int llm, int64_t rid, int* slot) {
+  return guarded([&] { *slot = pool->bp->slot_of(llm, rid); });
+}
+
+int mux_simulate(const mux_sim_config* cfg, int n_entries, const mux_llm_entry* entries, int n_requests,
+                 const mux_request* trace, mux_record* records_out) {
+  return guarded([&] {
+    SimInputs in = build_inputs(cfg, n_entries, entries, n_requests, trace);
+    muxsim::SimResult res = muxsim::run_simulation(in.cluster, in.placement, in.entries, in.trace, in.prof, in.params);
+    export_records(res, in, records_out);
+  });
+}
+
+int mux_decode_attention_headwise(const void* q, const void* pool, const int32_t* rowrec, const int32_t* rowlist,
+                                  const int32_t* slots, const int32_t* ctx, int B, int H, int num_layers,
+                                  int layer, int max_rows, int max_ctx, void* out, int out_fp32, int kv_splits,
+                                  void* workspace, size_t workspace_bytes, void* stream) {
+  return guarded([&] {
+    require(H > 0 && B >= 0 && layer >= 0 && layer < num_layers, "decode attention: bad shape");
+    mux::DecodeAttnArgs a{};
+    a.q = q;
+    a.pool = pool;
+    a.rowrec = rowrec;
+    a.rowlist = rowlist;
+    a.slots = slots;
+    a.ctx = ctx;
+    a.out = out;
+    a.B = B;
+    a.H = H;
+    a.layer = layer;
+    a.max_rows = max_rows;
+    a.row_width = 2 * num_layers * H;
+    const int rows = std::max(1, (max_ctx + 15) / 16);
+    int splits = kv_splits > 0 ? kv_splits : 1;
+    while ((rows + splits - 1) / splits > mux::decode_attention_max_rows_per_split()) splits *= 2;
+    a.splits = splits;
+    a.rows_per_split = (rows + splits - 1) / splits;
+    if (splits > 1) {
+      const size_t need = static_cast<size_t>(B) * H * splits * (128 + 2) * 4;
+      require(workspace != nullptr && workspace_bytes >= need, "decode attention: workspace too small");
+      a.part_o = static_cast<float*>(workspace);
+      a.part_ml = a.part_o + static_cast<size_t>(B) * H * splits * 128;
+    }
+    a.scale_log2 = 1.4426950408889634f / std::sqrt(128.f);
+    mux::check_cuda(mux::decode_attention(a, out_fp32 != 0, static_cast<cudaStream_t>(stream)), "decode_attention");
+  });
+}
+
+int mux_kv_append(const void* qkv, void* q_out, void* pool, const int32_t* rowrec, const int32_t* rowlist,
+                  const int32_t* tok_slot, const int32_t* tok_pos, const float* rope, int rope_positions, int T,
+                  int H, int num_layers, int layer, int max_rows, void* stream) {
+  return guarded([&] {
+    mux::AppendArgs a{};
+    a.qkv = qkv;
+    a.q_out = q_out;
+    a.pool = pool;
+    a.rowrec = rowrec;
+    a.rowlist = rowlist;
+    a.tok_slot = tok_slot;
+    a.tok_pos = tok_pos;
+    a.rope = rope;
+    a.T = T;
+    a.H = H;
+    a.layer = layer;
+    a.max_rows = max_rows;
+    a.row_width = 2 * num_layers * H;
+    a.rope_positions = rope_positions;
+    mux::check_cuda(mux::kv_append(a, static_cast<cudaStream_t>(stream)), "kv_append");
+  });
+}
+
+int mux_rope_table(int positions, float* out) {
+  return guarded([&] {
+    for (int p = 0; p < positions; ++p)
+      for (int i = 0; i < 64; ++i) {
+        const double inv_freq = 1.0 / std::pow(10000.0, 2.0 * i / 128.0);
+        const double ang = static_cast<double>(p) * inv_freq;
+        out[static_cast<size_t>(p) * 128 + 2 * i] = static_cast<float>(std::cos(ang));
+        out[static_cast<size_t>(p) * 128 + 2 * i + 1] = static_cast<float>(std::sin(ang));
+      }
+  });
+}
+
+int mux_gemm_bf16(const void* x, const void* w, int M, int N, int K, void* out, int epilogue, int splits,
+                  void* stream) {
+  return guarded([&] {
+    require(M > 0 && N > 0 && K > 0 && K % 8 == 0, "gemm: bad shape");
+    alignas(64) unsigned char tw[128], tx[128];
+    int n_tile = std::max(16, std::min(256, ((M + 15) / 16) * 16));
+    if (!mux::make_tmap_bf16(tw, w, N, K, static_cast<uint64_t>(K) * 2, 128) ||
+        !mux::make_tmap_bf16(tx, x, M, K, static_cast<uint64_t>(K) * 2, n_tile))
+      throw std::runtime_error("gemm: tensor map encode failed");
+    mux::GemmArgs g{};
+    g.tmap_w = tw;
+    g.tmap_x = tx;
+    g.out = out;
+    g.M = M;
+    g.N = N;
+    g.K = K;
+    g.ldo = epilogue == 2 ? N / 2 : N;
+    g.splits = splits;
+    g.epi = static_cast<mux::Epilogue>(epilogue);
+    mux::check_cuda(mux::gemm_bf16_tn(g, static_cast<cudaStream_t>(stream)), "gemm");
+  });
+}
+
+int mux_unit_create(const mux_unit_config* cfg, mux_unit** out) {
+  return guarded([&] {
+    require(cfg != nullptr && cfg->n_llms > 0 && cfg->llms != nullptr, "unit: bad config");
+    auto u = std::make_unique<mux_unit>();
+    const int64_t dev_blocks = cfg->device_pool_blocks > 0 ? std::min(cfg->device_pool_blocks, cfg->pool_blocks)
+                                                           : cfg->pool_blocks;
+    const int max_ctx = std::max(cfg->max_ctx, 16);
+    u->rt = std::make_unique<mux::Runtime>(cfg->device, dev_blocks, max_ctx + 16);
+    u->pool.owned = std::make_unique<BlockPool>(cfg->pool_blocks);
+    u->pool.bp = u->pool.owned.get();
+    u->pool.bp->enable_physical();
+    u->max_batch = std::max(1, cfg->max_batch);
+    u->max_prefill = std::max(16, cfg->max_prefill_tokens);
+    const int max_rows = (max_ctx + 15) / 16;
+    int hid = 0, qkv = 0, ffn = 0, vocab = 0, heads = 0;
+    for (int i = 0; i < cfg->n_llms; ++i) {
+      const mux_llm_entry& e = cfg->llms[i];
+      u->specs.push_back(spec_of(e));
+      u->pool.bp->register_llm(i, &u->specs.back(), 16);
+      mux::ModelDims d;
+      d.name = u->specs.back().name;
+      d.layers = e.num_layers;
+      d.heads = e.num_heads;
+      d.head_dim = e.head_dim;
+      d.hidden = e.hidden_size;
+      d.ffn = e.ffn;
+      d.vocab = e.vocab;
+      const int64_t row_blocks = 2ll * e.num_layers * e.num_heads;
+      const int64_t max_rowrecs = std::max<int64_t>(1, cfg->pool_blocks / row_blocks);
+      const int slots = cfg->max_slots > 0 ? cfg->max_slots : static_cast<int>(std::min<int64_t>(max_rowrecs, 1 << 20));
+      u->models.push_back(std::make_unique<mux::Llama>(d, slots, max_rows, max_rowrecs));
+      if (cfg->init_seed != 0) u->models.back()->init_random(cfg->init_seed + 7919ull * i, cfg->init_std, nullptr);
+      hid = std::max(hid, d.hidden);
+      qkv = std::max(qkv, 3 * d.heads * 128);
+      ffn = std::max(ffn, d.ffn);
+      vocab = std::max(vocab, d.vocab);
+      heads = std::max(heads, d.heads);
+    }
+    const int P = std::max(1, cfg->partitions);
+    for (int p = 0; p < P; ++p) {
+      cudaStream_t s;
+      mux::check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+      u->streams.push_back(s);
+      const int max_tok = std::max(u->max_prefill, u->max_batch);
+      u->ws.push_back(std::make_unique<mux::Workspace>(max_tok, std::max(u->max_batch, 256), hid, qkv, ffn, vocab,
+                                                       heads, 16, u->max_batch));
+    }
+    for (auto& e : u->ev) mux::check_cuda(cudaEventCreate(&e), "event");
+    mux::check_cuda(cudaDeviceSynchronize(), "unit create");
+    *out = u.release();
+  });
+}
+
+void mux_unit_destroy(mux_unit* unit) { delete unit; }
+
+mux_pool* mux_unit_pool(mux_unit* unit) { return unit ? &unit->pool : nullptr; }
+
+int mux_unit_set_tensor(mux_unit* u, int llm, const char* name, int layer, const void* host, size_t bytes) {
+  return guarded([&] {
+    if (!u->model(llm).set_tensor(name, layer, host, bytes, u->streams[0]))
+      throw std::invalid_argument(std::string("set_tensor: unknown tensor or size mismatch: ") + name);
+  });
+}
+
+int mux_unit_get_tensor(mux_unit* u, int llm, const char* name, int layer, void* host, size_t bytes) {
+  return guarded([&] {
+    if (!u->model(llm).get_tensor(name, layer, host, bytes, u->streams[0]))
+      throw std::invalid_argument(std::string("get_tensor: unknown tensor or size mismatch: ") + name);
+  });
+}
+
+int mux_unit_init_kv(mux_unit* u, uint64_t seed, float std) {
+  return guarded([&] {
+    mux::check_cuda(mux::init_normal_bf16(u->rt->pool(), u->rt->pool_blocks() * 2048, seed, std, u->streams[0]),
+                    "init kv");
+    u->rt->count_launch();
+    mux::check_cuda(cudaStreamSynchronize(u->streams[0]), "init kv sync");
+  });
+}
+
+int mux_unit_device_ptrs(mux_unit* u, int llm, void** pool, void** rowrec, void** rowlist, int* max_rows,
+                         int* row_width) {
+  return guarded([&] {
+    mux::Llama& m = u->model(llm);
+    if (pool) *pool = u->rt->pool();
+    if (rowrec) *rowrec = m.rowrec.p;
+    if (rowlist) *rowlist = m.rowlist.p;
+    if (max_rows) *max_rows = m.max_rows();
+    if (row_width) *row_width = m.row_width();
+  });
+}
+
+int mux_unit_prefill(mux_unit* u, int llm, int n, const int64_t* rids, const int32_t* tokens, int32_t* out_tokens,
+                     int partition) {
+  return guarded([&] {
+    mux::Llama& m = u->model(llm);
+    cudaStream_t s = u->stream(partition);
+    u->rt->upload_rows(*u->pool.bp, llm, m, s);
+    std::vector<int32_t> slots(n), lens(n);
+    for (int i = 0; i < n; ++i) {
+      slots[i] = u->pool.bp->slot_of(llm, rids[i]);
+      lens[i] = static_cast<int32_t>(u->pool.bp->request_tokens(llm, rids[i]));
+      require(slots[i] >= 0 && lens[i] > 0, "prefill: request not admitted");
+    }
+    u->rt->prefill(m, *u->ws[partition], n, slots.data(), lens.data(), tokens, out_tokens, s);
+  });
+}
+
+int mux_unit_decode(mux_unit* u, int llm, int n, const int64_t* rids, const int32_t* tokens, int32_t* out_tokens,
+                    int partition) {
+  return guarded([&] {
+    mux::Llama& m = u->model(llm);
+    cudaStream_t s = u->stream(partition);
+    u->rt->upload_rows(*u->pool.bp, llm, m, s);
+    std::vector<int32_t> slots(n), ctx(n);
+    for (int i = 0; i < n; ++i) {
+      slots[i] = u->pool.bp->slot_of(llm, rids[i]);
+      ctx[i] = static_cast<int32_t>(u->pool.bp->request_tokens(llm, rids[i]));
+      require(slots[i] >= 0 && ctx[i] > 0, "decode: request has no cached tokens");
+    }
+    u->rt->decode(m, *u->ws[partition], n, slots.data(), ctx.data(), tokens, out_tokens, s,
+                  u->timing ? &u->timer : nullptr);
+  });
+}
+
+int mux_unit_sync(mux_unit* u) {
+  return guarded([&] { mux::check_cuda(cudaDeviceSynchronize(), "sync"); });
+}
+
+int mux_unit_record(mux_unit* u, int partition, int slot) {
+  return guarded([&] {
+    require(slot >= 0 && slot < 64, "event slot out of range");
+    mux::check_cuda(cudaEventRecord(u->ev[slot], u->stream(partition)), "record");
+  });
+}
+
+int mux_unit_elapsed(mux_unit* u, int a, int b, float* ms) {
+  return guarded([&] {
+    require(a >= 0 && a < 64 && b >= 0 && b < 64, "event slot out of range");
+    mux::check_cuda(cudaEventSynchronize(u->ev[b]), "elapsed sync");
+    mux::check_cuda(cudaEventElapsedTime(ms, u->ev[a], u->ev[b]), "elapsed");
+  });
+}
+
+int mux_unit_attn_timing(mux_unit* u, int enable) {
+  return guarded([&] {
+    u->timer.harvest();
+    u->timing = enable != 0;
+    u->timer.total_ms = 0.0;
+    u->timer.bytes = 0.0;
+    u->timer.launches = 0;
+  });
+}
+
+int mux_unit_attn_time(mux_unit* u, double* total_ms, int64_t* launches, double* bytes) {
+  return guarded([&] {
+    u->timer.harvest();
+    if (total_ms) *total_ms = u->timer.total_ms;
+    if (launches) *launches = u->timer.launches;
+    if (bytes) *bytes = u->timer.bytes;
+  });
+}
+
+int64_t mux_unit_launches(mux_unit* u) { return u ? u->rt->launches() : -1; }
+
+int mux_unit_run_lockstep(mux_unit* u, const mux_sim_config* cfg, int n_entries, const mux_llm_entry* entries,
+                          int n_requests, const mux_request* trace, uint64_t prompt_seed, mux_record* records_out,
+                          int32_t* tokens_out) {
+  return guarded([&] {
+    require(cfg->n_units == 1, "lockstep: single-unit placements only");
+    require(n_entries == static_cast<int>(u->models.size()), "lockstep: entries must describe the unit's models");
+    SimInputs in = build_inputs(cfg, n_entries, entries, n_requests, trace);
+    GpuExecutor exec(u, prompt_seed, in.trace);
+    muxsim::SimResult res =
+        muxsim::run_simulation(in.cluster, in.placement, in.entries, in.trace, in.prof, in.params, &exec);
+    export_records(res, in, records_out);
+    if (tokens_out) {
+      size_t off = 0;
+      for (int i = 0; i < n_requests; ++i) {
+        const auto& t = exec.tokens()[i];
+        if (static_cast<int>(t.size()) != trace[i].output_len)
+          throw std::logic_error("lockstep: request " + std::to_string(trace[i].id) + " produced " +
+                                 std::to_string(t.size()) + " tokens, expected " + std::to_string(trace[i].output_len));
+        std::copy(t.begin(), t.end(), tokens_out + off);
+        off += t.size();
+      }
+    }
+  });
+}
+
+}  // extern "C"

@@ -1,0 +1,569 @@
+// B200 device runtime: KV pool, LLaMA weights/tables, job forwards.
+#include "runtime.h"
+
+#include <cuda.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstring>
+#include <stdexcept>
+#include <string>
+
+#include "../kernels/kernels.h"
+
+namespace mux {
+
+void check_cuda(cudaError_t e, const char* what) {
+  if (e != cudaSuccess)
+    throw std::runtime_error(std::string("cuda error in ") + what + ": " + cudaGetErrorString(e));
+}
+
+DevMem::DevMem(size_t n) : bytes(n) {
+  if (n > 0) check_cuda(cudaMalloc(&p, n), "cudaMalloc");
+}
+DevMem::~DevMem() {
+  if (p) cudaFree(p);
+}
+DevMem& DevMem::operator=(DevMem&& o) noexcept {
+  if (this != &o) {
+    if (p) cudaFree(p);
+    p = o.p;
+    bytes = o.bytes;
+    o.p = nullptr;
+    o.bytes = 0;
+  }
+  return *this;
+}
+PinnedMem::PinnedMem(size_t n) : bytes(n) {
+  if (n > 0) check_cuda(cudaMallocHost(&p, n), "cudaMallocHost");
+}
+PinnedMem::~PinnedMem() {
+  if (p) cudaFreeHost(p);
+}
+
+namespace {
+
+constexpr int kEpiStoreBf16 = 0, kEpiPartial = 1, kEpiSilu = 2, kEpiStoreF32 = 3;
+
+__global__ void gather_last_tok(const int32_t* last_tok, const int32_t* slots, int32_t* tokens, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) tokens[i] = last_tok[slots[i]];
+}
+
+__global__ void scatter_last_tok(int32_t* last_tok, const int32_t* slots, const int32_t* tokens, int n) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) last_tok[slots[i]] = tokens[i];
+}
+
+int gemm_n_tile(int M) {
+  int n = ((M + 15) / 16) * 16;
+  return std::max(16, std::min(256, n));
+}
+
+}  // namespace
+
+// ------------------------------------------------------------------ Llama
+
+Llama::Llama(const ModelDims& d, int max_slots, int max_rows, int64_t max_rowrecs)
+    : d_(d), max_slots_(max_slots), max_rows_(max_rows), max_rowrecs_(max_rowrecs) {
+  if (d.head_dim != 128) throw std::invalid_argument("llama: head_dim must be 128");
+  if (d.hidden % 64 != 0 || d.ffn % 64 != 0) throw std::invalid_argument("llama: hidden/ffn must be multiples of 64");
+  const size_t hid = d.hidden, ffn = d.ffn, V = d.vocab, qkv = 3ull * d.heads * 128, att = 1ull * d.heads * 128;
+  embed = DevMem(V * hid * 2);
+  lm_head = DevMem(V * hid * 2);
+  final_norm = DevMem(hid * 4);
+  for (int l = 0; l < d.layers; ++l) {
+    wqkv.emplace_back(qkv * hid * 2);
+    wo.emplace_back(hid * att * 2);
+    wgu.emplace_back(2 * ffn * hid * 2);
+    wdown.emplace_back(hid * ffn * 2);
+    attn_norm.emplace_back(hid * 4);
+    ffn_norm.emplace_back(hid * 4);
+  }
+  rowrec = DevMem(static_cast<size_t>(max_rowrecs) * row_width() * 4);
+  rowlist = DevMem(static_cast<size_t>(max_slots) * max_rows * 4);
+  last_tok = DevMem(static_cast<size_t>(max_slots) * 4);
+  check_cuda(cudaMemset(rowlist.p, 0, rowlist.bytes), "memset rowlist");
+  check_cuda(cudaMemset(last_tok.p, 0, last_tok.bytes), "memset last_tok");
+  build_tmaps();
+}
+
+int64_t Llama::weight_bytes() const {
+  int64_t t = embed.bytes + lm_head.bytes;
+  for (int l = 0; l < d_.layers; ++l) t += wqkv[l].bytes + wo[l].bytes + wgu[l].bytes + wdown[l].bytes;
+  return t;
+}
+
+void Llama::build_tmaps() {
+  const int hid = d_.hidden, ffn = d_.ffn, att = d_.heads * 128;
+  tm_qkv.resize(d_.layers);
+  tm_o.resize(d_.layers);
+  tm_gu.resize(d_.layers);
+  tm_down.resize(d_.layers);
+  for (int l = 0; l < d_.layers; ++l) {
+    bool ok = make_tmap_bf16(tm_qkv[l].raw, wqkv[l].p, qkv_cols(), hid, hid * 2ull, 128) &&
+              make_tmap_bf16(tm_o[l].raw, wo[l].p, hid, att, att * 2ull, 128) &&
+              make_tmap_bf16(tm_gu[l].raw, wgu[l].p, 2ull * ffn, hid, hid * 2ull, 128) &&
+              make_tmap_bf16(tm_down[l].raw, wdown[l].p, hid, ffn, ffn * 2ull, 128);
+    if (!ok) throw std::runtime_error("llama: tensor map encode failed");
+  }
+  if (!make_tmap_bf16(tm_lm.raw, lm_head.p, d_.vocab, hid, hid * 2ull, 128))
+    throw std::runtime_error("llama: tensor map encode failed (lm_head)");
+}
+
+void Llama::init_random(uint64_t seed, float std, cudaStream_t s) {
+  uint64_t k = seed * 0x100000001B3ull;
+  auto init = [&](DevMem& m) { check_cuda(init_normal_bf16(m.p, m.bytes / 2, ++k, std, s), "init"); };
+  auto ones = [&](DevMem& m) { check_cuda(fill_f32(m.as<float>(), m.bytes / 4, 1.f, s), "fill"); };
+  init(embed);
+  init(lm_head);
+  ones(final_norm);
+  for (int l = 0; l < d_.layers; ++l) {
+    init(wqkv[l]);
+    init(wo[l]);
+    init(wgu[l]);
+    init(wdown[l]);
+    ones(attn_norm[l]);
+    ones(ffn_norm[l]);
+  }
+}
+
+DevMem* Llama::tensor(const std::string& name, int layer, size_t* bytes) {
+  DevMem* m = nullptr;
+  auto per_layer = [&](std::vector<DevMem>& v) -> DevMem* {
+    return layer >= 0 && layer < d_.layers ? &v[layer] : nullptr;
+  };
+  if (name == "embed") m = &embed;
+  else if (name == "lm_head") m = &lm_head;
+  else if (name == "final_norm") m = &final_norm;
+  else if (name == "wqkv") m = per_layer(wqkv);
+  else if (name == "wo") m = per_layer(wo);
+  else if (name == "wgu") m = per_layer(wgu);
+  else if (name == "wdown") m = per_layer(wdown);
+  else if (name == "attn_norm") m = per_layer(attn_norm);
+  else if (name == "ffn_norm") m = per_layer(ffn_norm);
+  if (m && bytes) *bytes = m->bytes;
+  return m;
+}
+
+bool Llama::set_tensor(const std::string& name, int layer, const void* host, size_t bytes, cudaStream_t s) {
+  size_t want = 0;
+  DevMem* m = tensor(name, layer, &want);
+  if (!m || want != bytes) return false;
+  check_cuda(cudaMemcpyAsync(m->p, host, bytes, cudaMemcpyHostToDevice, s), "set_tensor");
+  check_cuda(cudaStreamSynchronize(s), "set_tensor sync");
+  return true;
+}
+
+bool Llama::get_tensor(const std::string& name, int layer, void* host, size_t bytes, cudaStream_t s) const {
+  size_t want = 0;
+  DevMem* m = const_cast<Llama*>(this)->tensor(name, layer, &want);
+  if (!m || want != bytes) return false;
+  check_cuda(cudaMemcpyAsync(host, m->p, bytes, cudaMemcpyDeviceToHost, s), "get_tensor");
+  check_cuda(cudaStreamSynchronize(s), "get_tensor sync");
+  return true;
+}
+
+// -------------------------------------------------------------- Workspace
+
+Workspace::Workspace(int max_tok, int max_batch_rows, int hidden, int qkv_cols, int ffn, int vocab,
+                     int heads, int max_splits, int max_decode_batch)
+    : max_tokens(max_tok), max_hidden(hidden), max_qkv(qkv_cols), max_ffn(ffn), max_vocab(vocab),
+      max_heads(heads) {
+  const size_t T = std::max(max_tok, 16);
+  max_part_rows = static_cast<int>(std::max<size_t>(T, static_cast<size_t>(max_splits) * max_decode_batch));
+  // Activation buffers get >= 256 rows so any n_tile box stays in bounds.
+  const size_t Tp = std::max<size_t>(T, 256);
+  resid = DevMem(Tp * hidden * 4);
+  xn = DevMem(Tp * hidden * 2);
+  qkv = DevMem(Tp * qkv_cols * 2);
+  q = DevMem(Tp * heads * 128 * 2);
+  attn = DevMem(Tp * heads * 128 * 2);
+  act = DevMem(Tp * ffn * 2);
+  parts = DevMem(static_cast<size_t>(max_part_rows) * hidden * 4);
+  const size_t rows_out = std::max<size_t>(max_batch_rows, 256);
+  logits = DevMem(rows_out * vocab * 4);
+  xlast = DevMem(rows_out * hidden * 2);
+  const size_t kv_splits = 16;
+  attn_part_o = DevMem(static_cast<size_t>(max_decode_batch) * heads * kv_splits * 128 * 4);
+  attn_part_ml = DevMem(static_cast<size_t>(max_decode_batch) * heads * kv_splits * 2 * 4);
+  // ints: tokens[T] slots[T] ctx[T] tok_slot[T] tok_pos[T] seq_start[T+1] out_tok[T] last_rows[T]
+  const size_t n_ints = 8 * T + 8;
+  ints = DevMem(n_ints * 4);
+  for (int i = 0; i < 2; ++i) {
+    new (&host_ints[i]) PinnedMem(n_ints * 4);
+    check_cuda(cudaEventCreateWithFlags(&staged[i], cudaEventDisableTiming), "event");
+  }
+  int32_t* b = ints.as<int32_t>();
+  tokens = b;
+  slots = b + T;
+  ctx = b + 2 * T;
+  tok_slot = b + 3 * T;
+  tok_pos = b + 4 * T;
+  seq_start = b + 5 * T;
+  out_tok = b + 6 * T + 1;
+  last_rows = b + 7 * T + 1;
+}
+
+cudaEvent_t AttnTimer::get() {
+  if (!spare.empty()) {
+    cudaEvent_t e = spare.back();
+    spare.pop_back();
+    return e;
+  }
+  cudaEvent_t e;
+  check_cuda(cudaEventCreate(&e), "event");
+  return e;
+}
+
+void AttnTimer::harvest() {
+  for (auto& pr : pending) {
+    check_cuda(cudaEventSynchronize(pr.second), "timer sync");
+    float ms = 0.f;
+    check_cuda(cudaEventElapsedTime(&ms, pr.first, pr.second), "timer elapsed");
+    total_ms += ms;
+    launches += 1;
+    spare.push_back(pr.first);
+    spare.push_back(pr.second);
+  }
+  pending.clear();
+  bytes += pending_bytes;
+  pending_bytes = 0.0;
+}
+
+AttnTimer::~AttnTimer() {
+  for (cudaEvent_t e : spare) cudaEventDestroy(e);
+  for (auto& pr : pending) {
+    cudaEventDestroy(pr.first);
+    cudaEventDestroy(pr.second);
+  }
+}
+
+Workspace::~Workspace() {
+  for (int i = 0; i < 2; ++i)
+    if (staged[i]) cudaEventDestroy(staged[i]);
+}
+
+int32_t* Workspace::stage_begin() {
+  check_cuda(cudaEventSynchronize(staged[cur]), "stage wait");
+  return host_ints[cur].as<int32_t>();
+}
+
+void Workspace::stage_commit(size_t n_ints, cudaStream_t stream) {
+  check_cuda(cudaMemcpyAsync(ints.p, host_ints[cur].p, n_ints * 4, cudaMemcpyHostToDevice, stream),
+             "meta copy");
+  check_cuda(cudaEventRecord(staged[cur], stream), "stage record");
+  cur ^= 1;
+}
+
+// ---------------------------------------------------------------- Runtime
+
+Runtime::Runtime(int device, int64_t pool_blocks, int max_pos)
+    : device_(device), pool_blocks_(pool_blocks), max_pos_(max_pos) {
+  check_cuda(cudaSetDevice(device), "cudaSetDevice");
+  check_cuda(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device), "sm count");
+  pool_ = DevMem(static_cast<size_t>(pool_blocks) * 4096);
+  // RoPE table [max_pos][64][(cos, sin)], computed in double, stored fp32.
+  std::vector<float> tab(static_cast<size_t>(max_pos) * 128);
+  for (int p = 0; p < max_pos; ++p) {
+    for (int i = 0; i < 64; ++i) {
+      const double inv_freq = 1.0 / std::pow(10000.0, 2.0 * i / 128.0);
+      const double ang = static_cast<double>(p) * inv_freq;
+      tab[static_cast<size_t>(p) * 128 + 2 * i] = static_cast<float>(std::cos(ang));
+      tab[static_cast<size_t>(p) * 128 + 2 * i + 1] = static_cast<float>(std::sin(ang));
+    }
+  }
+  rope_ = DevMem(tab.size() * 4);
+  check_cuda(cudaMemcpy(rope_.p, tab.data(), tab.size() * 4, cudaMemcpyHostToDevice), "rope upload");
+}
+
+Runtime::~Runtime() {
+  for (StageSlot& s : ring_)
+    if (s.done) cudaEventDestroy(s.done);
+}
+
+const void* Runtime::act_tmap(const void* base, int rows, int cols, int box_rows) {
+  auto key = std::make_tuple(base, rows, cols, box_rows);
+  auto it = tmaps_.find(key);
+  if (it != tmaps_.end()) return it->second.data();
+  std::vector<unsigned char> raw(128 + 64);
+  // CUtensorMap must be 64-byte aligned; std::vector data is 16-aligned, so
+  // keep an aligned copy inside the buffer.
+  unsigned char* aligned = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(raw.data()) + 63) & ~uintptr_t(63));
+  if (!make_tmap_bf16(aligned, base, rows, cols, static_cast<uint64_t>(cols) * 2, box_rows))
+    throw std::runtime_error("act tensor map encode failed");
+  std::vector<unsigned char> stored(aligned, aligned + 128);
+  auto ins = tmaps_.emplace(key, std::move(stored));
+  return ins.first->second.data();
+}
+
+int Runtime::pick_splits(int tiles, int kb_total) const {
+  if (tiles >= num_sms_) return 1;
+  int s = (num_sms_ + tiles - 1) / tiles;
+  s = std::min(s, std::max(1, kb_total / 4));
+  return std::max(1, std::min(s, 16));
+}
+
+void Runtime::gemm(const void* tmap_w, const void* x, int M, int N, int K, void* out, int ldo, int epi,
+                   int splits, cudaStream_t stream) {
+  // The X map is viewed over max(M, 256) rows: buffers are sized for it and
+  // rows past M are never stored.
+  const int rows = std::max(M, 256);
+  const void* tx = act_tmap(x, rows, K, gemm_n_tile(M));
+  GemmArgs g{};
+  g.tmap_w = tmap_w;
+  g.tmap_x = tx;
+  g.out = out;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.ldo = ldo;
+  g.splits = splits;
+  g.epi = static_cast<Epilogue>(epi);
+  check_cuda(gemm_bf16_tn(g, stream), "gemm");
+  launches_ += 1;
+}
+
+void Runtime::upload_rows(muxsim::BlockPool& bp, int llm, Llama& m, cudaStream_t stream) {
+  std::vector<muxsim::RowDelta>& pend = bp.pending_rows(llm);
+  if (pend.empty()) return;
+  const int W = m.row_width();
+  if (W != bp.row_width(llm)) throw std::logic_error("upload_rows: row width mismatch");
+  const size_t n = pend.size();
+  const size_t need = n * (3 + static_cast<size_t>(W)) * 4;
+  StageSlot& slot = ring_[ring_next_];
+  ring_next_ = (ring_next_ + 1) % 4;
+  if (slot.done == nullptr) check_cuda(cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming), "event");
+  // The slot's previous copy + scatter must be complete before it is reused.
+  check_cuda(cudaEventSynchronize(slot.done), "stage wait");
+  if (need > slot.cap) {
+    size_t cap = std::max(need, slot.cap * 2);
+    slot.dev = DevMem(cap);
+    slot.host = std::make_unique<PinnedMem>(cap);
+    slot.cap = cap;
+  }
+  int32_t* meta = slot.host->as<int32_t>();
+  int32_t* ids = meta + 3 * n;
+  for (size_t i = 0; i < n; ++i) {
+    const muxsim::RowDelta& d = pend[i];
+    if (d.slot >= m.max_slots() || d.row >= m.max_rows() || d.rowrec >= m.max_rowrecs())
+      throw std::runtime_error("upload_rows: device table capacity exceeded (slot " +
+                               std::to_string(d.slot) + ", row " + std::to_string(d.row) + ")");
+    meta[3 * i] = d.slot;
+    meta[3 * i + 1] = d.row;
+    meta[3 * i + 2] = d.rowrec;
+    const int32_t* src = bp.row_ids(llm, d.rowrec);
+    for (int j = 0; j < W; ++j) {
+      if (src[j] >= pool_blocks_) throw std::runtime_error("upload_rows: block id beyond the device pool");
+      ids[i * W + j] = src[j];
+    }
+  }
+  check_cuda(cudaMemcpyAsync(slot.dev.p, slot.host->p, need, cudaMemcpyHostToDevice, stream), "stage copy");
+  TableUpdateArgs t{};
+  t.meta = slot.dev.as<int32_t>();
+  t.ids = slot.dev.as<int32_t>() + 3 * n;
+  t.rowrec = m.rowrec.as<int32_t>();
+  t.rowlist = m.rowlist.as<int32_t>();
+  t.n = static_cast<int>(n);
+  t.row_width = W;
+  t.max_rows = m.max_rows();
+  check_cuda(table_update(t, stream), "table_update");
+  launches_ += 1;
+  check_cuda(cudaEventRecord(slot.done, stream), "stage record");
+  pend.clear();
+}
+
+void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, const int32_t* ctx_host,
+                     const int32_t* tokens_host, int32_t* out_host, cudaStream_t stream,
+                     AttnTimer* timer) {
+  if (n <= 0) return;
+  if (n > ws.max_tokens) throw std::invalid_argument("decode: batch exceeds workspace");
+  const ModelDims& d = m.dims();
+  const int T = std::max(ws.max_tokens, 16);
+  int32_t* h = ws.stage_begin();
+  for (int i = 0; i < n; ++i) {
+    h[T + i] = slots_host[i];
+    h[2 * T + i] = ctx_host[i];
+    h[4 * T + i] = ctx_host[i] - 1;
+    if (tokens_host) h[i] = tokens_host[i];
+  }
+  ws.stage_commit(5 * static_cast<size_t>(T), stream);
+  if (!tokens_host) {
+    gather_last_tok<<<(n + 127) / 128, 128, 0, stream>>>(m.last_tok.as<int32_t>(), ws.slots, ws.tokens, n);
+    launches_ += 1;
+  }
+
+  const int hid = d.hidden, H = d.heads, L = d.layers;
+  check_cuda(embed_rmsnorm(m.embed.p, ws.tokens, m.attn_norm[0].as<float>(), ws.resid.as<float>(), ws.xn.p,
+                           n, hid, d.norm_eps, stream), "embed");
+  launches_ += 1;
+  const int kb_att = (H * 128 + 63) / 64, kb_ffn = (d.ffn + 63) / 64;
+  const int tiles_hid = (hid + 127) / 128;
+  const int split_o = pick_splits(tiles_hid, kb_att);
+  const int split_d = pick_splits(tiles_hid, kb_ffn);
+  DecodeAttnArgs at{};
+  at.q = ws.q.p;
+  at.pool = pool_.p;
+  at.rowrec = m.rowrec.as<int32_t>();
+  at.rowlist = m.rowlist.as<int32_t>();
+  at.slots = ws.slots;
+  at.ctx = ws.ctx;
+  at.out = ws.attn.p;
+  at.part_o = ws.attn_part_o.as<float>();
+  at.part_ml = ws.attn_part_ml.as<float>();
+  at.B = n;
+  at.H = H;
+  at.max_rows = m.max_rows();
+  at.row_width = m.row_width();
+  int max_ctx = 0;
+  for (int i = 0; i < n; ++i) max_ctx = std::max(max_ctx, ctx_host[i]);
+  const int max_rows_req = (max_ctx + 15) / 16;
+  // KV splits: enough CTAs to fill the GPU a few times over.
+  int splits = 1;
+  while (splits < 16 && n * H * splits < 4 * num_sms_ && (max_rows_req + splits * 2 - 1) / (splits * 2) >= 4) splits *= 2;
+  while ((max_rows_req + splits - 1) / splits > decode_attention_max_rows_per_split()) splits *= 2;
+  at.splits = splits;
+  at.rows_per_split = std::max(1, (max_rows_req + splits - 1) / splits);
+  at.scale_log2 = 1.4426950408889634f / std::sqrt(128.f);
+  // Algorithmic bytes of one K1 launch: K+V of every cached token, q in, o out.
+  double attn_bytes = 0.0;
+  for (int i = 0; i < n; ++i) attn_bytes += static_cast<double>(ctx_host[i]) * H * 128 * 2 * 2;
+  attn_bytes += static_cast<double>(n) * H * 128 * 2 * 2;
+
+  AppendArgs ap{};
+  ap.qkv = ws.qkv.p;
+  ap.q_out = ws.q.p;
+  ap.pool = pool_.p;
+  ap.rowrec = m.rowrec.as<int32_t>();
+  ap.rowlist = m.rowlist.as<int32_t>();
+  ap.tok_slot = ws.slots;
+  ap.tok_pos = ws.tok_pos;
+  ap.rope = rope_.as<float>();
+  ap.T = n;
+  ap.H = H;
+  ap.max_rows = m.max_rows();
+  ap.row_width = m.row_width();
+  ap.rope_positions = max_pos_;
+
+  for (int l = 0; l < L; ++l) {
+    gemm(m.tm_qkv[l].raw, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, 1, stream);
+    ap.layer = l;
+    check_cuda(kv_append(ap, stream), "kv_append");
+    launches_ += 1;
+    at.layer = l;
+    cudaEvent_t e0 = nullptr, e1 = nullptr;
+    if (timer) {
+      e0 = timer->get();
+      e1 = timer->get();
+      check_cuda(cudaEventRecord(e0, stream), "timer");
+    }
+    check_cuda(decode_attention(at, false, stream), "decode_attention");
+    launches_ += at.splits > 1 ? 2 : 1;
+    if (timer) {
+      check_cuda(cudaEventRecord(e1, stream), "timer");
+      timer->pending.emplace_back(e0, e1);
+      timer->pending_bytes += attn_bytes;
+    }
+    gemm(m.tm_o[l].raw, ws.attn.p, n, hid, H * 128, ws.parts.p, hid, kEpiPartial, split_o, stream);
+    check_cuda(reduce_residual_rmsnorm(ws.parts.as<float>(), split_o, ws.resid.as<float>(),
+                                       m.ffn_norm[l].as<float>(), ws.xn.p, n, hid, d.norm_eps, stream), "reduce");
+    launches_ += 1;
+    gemm(m.tm_gu[l].raw, ws.xn.p, n, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, 1, stream);
+    gemm(m.tm_down[l].raw, ws.act.p, n, hid, d.ffn, ws.parts.p, hid, kEpiPartial, split_d, stream);
+    const float* next_norm = l + 1 < L ? m.attn_norm[l + 1].as<float>() : m.final_norm.as<float>();
+    check_cuda(reduce_residual_rmsnorm(ws.parts.as<float>(), split_d, ws.resid.as<float>(), next_norm,
+                                       ws.xn.p, n, hid, d.norm_eps, stream), "reduce");
+    launches_ += 1;
+  }
+  gemm(m.tm_lm.raw, ws.xn.p, n, d.vocab, hid, ws.logits.p, d.vocab, kEpiStoreF32, 1, stream);
+  check_cuda(argmax_rows(ws.logits.as<float>(), n, d.vocab, ws.out_tok, stream), "argmax");
+  scatter_last_tok<<<(n + 127) / 128, 128, 0, stream>>>(m.last_tok.as<int32_t>(), ws.slots, ws.out_tok, n);
+  launches_ += 2;
+  if (out_host)
+    check_cuda(cudaMemcpyAsync(out_host, ws.out_tok, n * 4, cudaMemcpyDeviceToHost, stream), "out copy");
+}
+
+void Runtime::prefill(Llama& m, Workspace& ws, int n, const int32_t* slots_host, const int32_t* lens_host,
+                      const int32_t* tokens_host, int32_t* out_host, cudaStream_t stream) {
+  if (n <= 0) return;
+  const ModelDims& d = m.dims();
+  int T = 0;
+  for (int i = 0; i < n; ++i) T += lens_host[i];
+  if (T > ws.max_tokens) throw std::invalid_argument("prefill: tokens exceed workspace");
+  const int cap = std::max(ws.max_tokens, 16);
+  int32_t* h = ws.stage_begin();
+  int t = 0;
+  for (int i = 0; i < n; ++i) {
+    h[cap + i] = slots_host[i];
+    h[5 * cap + i] = t;
+    for (int p = 0; p < lens_host[i]; ++p, ++t) {
+      h[t] = tokens_host[t];
+      h[3 * cap + t] = slots_host[i];
+      h[4 * cap + t] = p;
+    }
+    h[7 * cap + 1 + i] = t - 1;
+  }
+  h[5 * cap + n] = T;
+  ws.stage_commit(8 * static_cast<size_t>(cap) + 8, stream);
+
+  const int hid = d.hidden, H = d.heads, L = d.layers;
+  check_cuda(embed_rmsnorm(m.embed.p, ws.tokens, m.attn_norm[0].as<float>(), ws.resid.as<float>(), ws.xn.p,
+                           T, hid, d.norm_eps, stream), "embed");
+  launches_ += 1;
+  const int kb_att = (H * 128 + 63) / 64, kb_ffn = (d.ffn + 63) / 64;
+  const int tiles_hid = ((hid + 127) / 128) * ((T + 255) / 256);
+  const int split_o = std::min(pick_splits(tiles_hid, kb_att), std::max(1, ws.max_part_rows / T));
+  const int split_d = std::min(pick_splits(tiles_hid, kb_ffn), std::max(1, ws.max_part_rows / T));
+  AppendArgs ap{};
+  ap.qkv = ws.qkv.p;
+  ap.q_out = ws.q.p;
+  ap.pool = pool_.p;
+  ap.rowrec = m.rowrec.as<int32_t>();
+  ap.rowlist = m.rowlist.as<int32_t>();
+  ap.tok_slot = ws.tok_slot;
+  ap.tok_pos = ws.tok_pos;
+  ap.rope = rope_.as<float>();
+  ap.T = T;
+  ap.H = H;
+  ap.max_rows = m.max_rows();
+  ap.row_width = m.row_width();
+  ap.rope_positions = max_pos_;
+  PrefillAttnArgs pa{};
+  pa.q = ws.q.p;
+  pa.qkv = ws.qkv.p;
+  pa.out = ws.attn.p;
+  pa.seq_start = ws.seq_start;
+  pa.nseq = n;
+  pa.H = H;
+  pa.T = T;
+  pa.scale_log2 = 1.4426950408889634f / std::sqrt(128.f);
+  for (int l = 0; l < L; ++l) {
+    gemm(m.tm_qkv[l].raw, ws.xn.p, T, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, 1, stream);
+    ap.layer = l;
+    check_cuda(kv_append(ap, stream), "kv_append");
+    launches_ += 1;
+    check_cuda(prefill_attention(pa, stream), "prefill_attention");
+    launches_ += 1;
+    gemm(m.tm_o[l].raw, ws.attn.p, T, hid, H * 128, ws.parts.p, hid, kEpiPartial, split_o, stream);
+    check_cuda(reduce_residual_rmsnorm(ws.parts.as<float>(), split_o, ws.resid.as<float>(),
+                                       m.ffn_norm[l].as<float>(), ws.xn.p, T, hid, d.norm_eps, stream), "reduce");
+    launches_ += 1;
+    gemm(m.tm_gu[l].raw, ws.xn.p, T, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, 1, stream);
+    gemm(m.tm_down[l].raw, ws.act.p, T, hid, d.ffn, ws.parts.p, hid, kEpiPartial, split_d, stream);
+    const float* next_norm = l + 1 < L ? m.attn_norm[l + 1].as<float>() : m.final_norm.as<float>();
+    check_cuda(reduce_residual_rmsnorm(ws.parts.as<float>(), split_d, ws.resid.as<float>(), next_norm,
+                                       ws.xn.p, T, hid, d.norm_eps, stream), "reduce");
+    launches_ += 1;
+  }
+  check_cuda(gather_rows_bf16(ws.xn.p, ws.last_rows, ws.xlast.p, n, hid, stream), "gather");
+  launches_ += 1;
+  gemm(m.tm_lm.raw, ws.xlast.p, n, d.vocab, hid, ws.logits.p, d.vocab, kEpiStoreF32, 1, stream);
+  check_cuda(argmax_rows(ws.logits.as<float>(), n, d.vocab, ws.out_tok, stream), "argmax");
+  scatter_last_tok<<<(n + 127) / 128, 128, 0, stream>>>(m.last_tok.as<int32_t>(), ws.slots, ws.out_tok, n);
+  launches_ += 2;
+  if (out_host)
+    check_cuda(cudaMemcpyAsync(out_host, ws.out_tok, n * 4, cudaMemcpyDeviceToHost, stream), "out copy");
+}
+
+}  // namespace mux

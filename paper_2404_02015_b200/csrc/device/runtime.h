@@ -1,0 +1,180 @@
+// B200 device runtime: the unified KV block pool in HBM, per-model LLaMA
+// weights and device block tables, per-partition workspaces, and the
+// prefill / decode job forwards that UnitSim::launch
+// (/root/reference/proj/src/sim_engine.cpp:308-330) only priced.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <map>
+#include <memory>
+#include <string>
+#include <tuple>
+#include <vector>
+
+#include "mux/kv.hpp"
+
+namespace mux {
+
+struct ModelDims {
+  std::string name;
+  int layers = 0;
+  int heads = 0;
+  int head_dim = 128;
+  int hidden = 0;
+  int ffn = 0;
+  int vocab = 32000;
+  float norm_eps = 1e-5f;
+  float rope_theta = 10000.f;
+};
+
+// Device buffer (cudaMalloc), owned.
+struct DevMem {
+  void* p = nullptr;
+  size_t bytes = 0;
+  DevMem() = default;
+  explicit DevMem(size_t n);
+  ~DevMem();
+  DevMem(const DevMem&) = delete;
+  DevMem& operator=(const DevMem&) = delete;
+  DevMem(DevMem&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+  DevMem& operator=(DevMem&& o) noexcept;
+  template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+struct PinnedMem {
+  void* p = nullptr;
+  size_t bytes = 0;
+  PinnedMem() = default;
+  explicit PinnedMem(size_t n);
+  ~PinnedMem();
+  PinnedMem(const PinnedMem&) = delete;
+  PinnedMem& operator=(const PinnedMem&) = delete;
+  template <typename T> T* as() const { return static_cast<T*>(p); }
+};
+
+// One colocated LLaMA model: weights + its block tables in HBM.
+class Llama {
+ public:
+  Llama(const ModelDims& d, int max_slots, int max_rows, int64_t max_rowrecs);
+  const ModelDims& dims() const { return d_; }
+  int row_width() const { return 2 * d_.layers * d_.heads; }
+  int qkv_cols() const { return 3 * d_.heads * d_.head_dim; }
+  int max_slots() const { return max_slots_; }
+  int max_rows() const { return max_rows_; }
+  int64_t max_rowrecs() const { return max_rowrecs_; }
+  int64_t weight_bytes() const;
+  void init_random(uint64_t seed, float std, cudaStream_t s);
+  // Upload one tensor from host in device layout (see capi docs). Returns false on bad name/size.
+  bool set_tensor(const std::string& name, int layer, const void* host, size_t bytes, cudaStream_t s);
+  bool get_tensor(const std::string& name, int layer, void* host, size_t bytes, cudaStream_t s) const;
+
+  // weights (bf16 unless noted)
+  DevMem embed, lm_head, final_norm;                 // final_norm fp32
+  std::vector<DevMem> wqkv, wo, wgu, wdown;          // per layer
+  std::vector<DevMem> attn_norm, ffn_norm;           // fp32
+  // tensor maps (CUtensorMap, 128 bytes each), box = 128 W rows
+  struct TMap { alignas(64) unsigned char raw[128]; };
+  std::vector<TMap> tm_qkv, tm_o, tm_gu, tm_down;
+  TMap tm_lm;
+  // device block tables
+  DevMem rowrec;    // [max_rowrecs][row_width] int32
+  DevMem rowlist;   // [max_slots][max_rows] int32
+  DevMem last_tok;  // [max_slots] int32: most recent token of each slot
+
+ private:
+  void build_tmaps();
+  DevMem* tensor(const std::string& name, int layer, size_t* bytes);
+  ModelDims d_;
+  int max_slots_, max_rows_;
+  int64_t max_rowrecs_;
+};
+
+// Per-partition scratch for one running job.
+struct Workspace {
+  int max_tokens = 0;    // prefill token budget or max decode batch
+  int max_hidden = 0, max_qkv = 0, max_ffn = 0, max_vocab = 0, max_heads = 0;
+  int max_part_rows = 0; // splits * tokens for split-K partials
+  DevMem resid, xn, qkv, q, attn, act, parts, logits, ints, attn_part_o, attn_part_ml, xlast;
+  PinnedMem host_ints[2];  // double-buffered staging for per-job metadata
+  cudaEvent_t staged[2] = {nullptr, nullptr};
+  int cur = 0;
+  // Next staging buffer: waits until the copy that last used it completed.
+  int32_t* stage_begin();
+  // Enqueue the copy of the first n_ints of the staging buffer and flip.
+  void stage_commit(size_t n_ints, cudaStream_t stream);
+  ~Workspace();
+  // int32 views into `ints`
+  int32_t *tokens, *slots, *ctx, *tok_slot, *tok_pos, *seq_start, *out_tok, *last_rows;
+  Workspace(int max_tokens, int max_batch_rows, int hidden, int qkv, int ffn, int vocab, int heads,
+            int max_splits, int max_decode_batch);
+};
+
+// Per-launch K1 timing: an event pair around every decode-attention launch.
+struct AttnTimer {
+  std::vector<cudaEvent_t> spare;
+  std::vector<std::pair<cudaEvent_t, cudaEvent_t>> pending;
+  double total_ms = 0.0;
+  double bytes = 0.0;
+  int64_t launches = 0;
+  double pending_bytes = 0.0;
+  cudaEvent_t get();
+  void harvest();  // synchronises pending pairs and accumulates
+  ~AttnTimer();
+};
+
+class Runtime {
+ public:
+  Runtime(int device, int64_t pool_blocks, int max_pos);
+  ~Runtime();
+  int device() const { return device_; }
+  int64_t pool_blocks() const { return pool_blocks_; }
+  void* pool() const { return pool_.p; }
+  const float* rope() const { return rope_.as<float>(); }
+  int rope_positions() const { return max_pos_; }
+  int num_sms() const { return num_sms_; }
+  int64_t launches() const { return launches_; }
+  void count_launch(int64_t n = 1) { launches_ += n; }
+
+  // Cached tensor map for an activation buffer viewed as rows x cols bf16.
+  const void* act_tmap(const void* base, int rows, int cols, int box_rows);
+
+  // Block-table maintenance: copy pending rows of `llm` (host pool) to the
+  // model's device tables on `stream` (through pinned staging).
+  void upload_rows(muxsim::BlockPool& pool, int llm, Llama& m, cudaStream_t stream);
+
+  // Jobs. Members are (slot, ctx) pairs; ctx = cached tokens incl. the new one.
+  void decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, const int32_t* ctx_host,
+              const int32_t* tokens_host /*nullable: use last_tok*/, int32_t* out_host /*nullable*/,
+              cudaStream_t stream, AttnTimer* timer = nullptr);
+  void prefill(Llama& m, Workspace& ws, int n, const int32_t* slots_host, const int32_t* lens_host,
+               const int32_t* tokens_host, int32_t* out_host /*nullable*/, cudaStream_t stream);
+
+  // Decode-forward building blocks, exposed for tests/bench.
+  int pick_splits(int tiles, int kb_total) const;
+  void gemm(const void* tmap_w, const void* x, int M, int N, int K, void* out, int ldo, int epi,
+            int splits, cudaStream_t stream);
+
+ private:
+  int device_;
+  int num_sms_;
+  int64_t pool_blocks_;
+  int max_pos_;
+  int64_t launches_ = 0;
+  DevMem pool_;
+  DevMem rope_;
+  struct StageSlot {
+    DevMem dev;
+    std::unique_ptr<PinnedMem> host;
+    cudaEvent_t done = nullptr;
+    size_t cap = 0;
+  };
+  StageSlot ring_[4];
+  int ring_next_ = 0;
+  std::map<std::tuple<const void*, int, int, int>, std::vector<unsigned char>> tmaps_;
+};
+
+void check_cuda(cudaError_t e, const char* what);
+
+}  // namespace mux

@@ -1,0 +1,262 @@
+// K5: the small LLaMA ops around the GEMMs, fused where a pass over the
+// activations is needed anyway: embedding + RMSNorm, split-K reduction +
+// residual add + RMSNorm, row argmax (greedy sampling), row gather, a
+// causal varlen prefill attention (CUDA cores, v1), and deterministic weight
+// initialisation. All HBM-bound; one CTA per token row.
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace mux {
+namespace {
+
+constexpr int kRowThreads = 256;
+
+__device__ __forceinline__ float block_sum(float v, float* scratch) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) scratch[warp] = v;
+  __syncthreads();
+  float t = 0.f;
+  const int nw = blockDim.x >> 5;
+  for (int w = 0; w < nw; ++w) t += scratch[w];
+  __syncthreads();
+  return t;
+}
+
+// y = x * rsqrt(mean(x^2) + eps) * w, rounded to bf16. x lives in resid (fp32).
+__device__ void rmsnorm_row(const float* x, const float* w, __nv_bfloat16* y, int hidden, float eps,
+                            float* scratch) {
+  float ss = 0.f;
+  for (int i = threadIdx.x; i < hidden; i += blockDim.x) ss = fmaf(x[i], x[i], ss);
+  const float tot = block_sum(ss, scratch);
+  const float inv = rsqrtf(tot / static_cast<float>(hidden) + eps);
+  for (int i = threadIdx.x; i < hidden; i += blockDim.x) y[i] = __float2bfloat16_rn(x[i] * inv * w[i]);
+}
+
+__global__ void __launch_bounds__(kRowThreads) embed_rmsnorm_kernel(
+    const __nv_bfloat16* emb, const int32_t* tokens, const float* norm_w, float* resid,
+    __nv_bfloat16* xn, int hidden, float eps) {
+  __shared__ float scratch[32];
+  const int t = blockIdx.x;
+  const int64_t tok = tokens[t];
+  const __nv_bfloat16* e = emb + tok * hidden;
+  float* x = resid + static_cast<int64_t>(t) * hidden;
+  for (int i = threadIdx.x; i < hidden; i += blockDim.x) x[i] = __bfloat162float(e[i]);
+  __syncthreads();
+  rmsnorm_row(x, norm_w, xn + static_cast<int64_t>(t) * hidden, hidden, eps, scratch);
+}
+
+__global__ void __launch_bounds__(kRowThreads) reduce_residual_rmsnorm_kernel(
+    const float* parts, int splits, int T, float* resid, const float* norm_w, __nv_bfloat16* xn,
+    int hidden, float eps) {
+  __shared__ float scratch[32];
+  const int t = blockIdx.x;
+  float* x = resid + static_cast<int64_t>(t) * hidden;
+  const int64_t plane = static_cast<int64_t>(T) * hidden;
+  for (int i = threadIdx.x; i < hidden; i += blockDim.x) {
+    float acc = x[i];
+    for (int s = 0; s < splits; ++s) acc += parts[s * plane + static_cast<int64_t>(t) * hidden + i];
+    x[i] = acc;
+  }
+  __syncthreads();
+  if (xn != nullptr) rmsnorm_row(x, norm_w, xn + static_cast<int64_t>(t) * hidden, hidden, eps, scratch);
+}
+
+__global__ void __launch_bounds__(kRowThreads) argmax_kernel(const float* logits, int V, int32_t* out) {
+  __shared__ float sv[32];
+  __shared__ int si[32];
+  const float* row = logits + static_cast<int64_t>(blockIdx.x) * V;
+  float best = -INFINITY;
+  int bi = 0x7fffffff;
+  for (int i = threadIdx.x; i < V; i += blockDim.x) {
+    const float v = row[i];
+    if (v > best || (v == best && i < bi)) {
+      best = v;
+      bi = i;
+    }
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    const float ov = __shfl_xor_sync(0xffffffffu, best, o);
+    const int oi = __shfl_xor_sync(0xffffffffu, bi, o);
+    if (ov > best || (ov == best && oi < bi)) {
+      best = ov;
+      bi = oi;
+    }
+  }
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  if (lane == 0) {
+    sv[warp] = best;
+    si[warp] = bi;
+  }
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float b0 = sv[0];
+    int i0 = si[0];
+    for (int w = 1; w < (blockDim.x >> 5); ++w)
+      if (sv[w] > b0 || (sv[w] == b0 && si[w] < i0)) {
+        b0 = sv[w];
+        i0 = si[w];
+      }
+    out[blockIdx.x] = i0;
+  }
+}
+
+__global__ void gather_rows_kernel(const uint4* src, const int32_t* idx, uint4* dst, int vec_per_row) {
+  const int r = blockIdx.x;
+  const int64_t s = static_cast<int64_t>(idx[r]) * vec_per_row;
+  const int64_t d = static_cast<int64_t>(r) * vec_per_row;
+  for (int i = threadIdx.x; i < vec_per_row; i += blockDim.x) dst[d + i] = src[s + i];
+}
+
+// One warp per (query token, head); keys in chunks of 32 (lane = key for the
+// scores, lane = 4 dims for the P.V accumulation), online softmax in fp32.
+__global__ void __launch_bounds__(128) prefill_attention_kernel(const PrefillAttnArgs a) {
+  __shared__ float qs[4][128];
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int gw = blockIdx.x * 4 + warp;
+  if (gw >= a.T * a.H) return;
+  const int t = gw / a.H;
+  const int h = gw % a.H;
+  // Which sequence owns token t.
+  int lo = 0, hi = a.nseq;
+  while (hi - lo > 1) {
+    const int mid = (lo + hi) >> 1;
+    if (a.seq_start[mid] <= t) lo = mid; else hi = mid;
+  }
+  const int s0 = a.seq_start[lo];
+  const __nv_bfloat16* q = reinterpret_cast<const __nv_bfloat16*>(a.q);
+  const __nv_bfloat16* qkv = reinterpret_cast<const __nv_bfloat16*>(a.qkv);
+  for (int d = lane; d < 128; d += 32)
+    qs[warp][d] = __bfloat162float(q[(static_cast<int64_t>(t) * a.H + h) * 128 + d]) * a.scale_log2;
+  __syncwarp();
+  const int64_t tok_stride = static_cast<int64_t>(3) * a.H * 128;
+  float m = -INFINITY, l = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
+  for (int k0 = s0; k0 <= t; k0 += 32) {
+    const int key = k0 + lane;
+    float sc = -INFINITY;
+    if (key <= t) {
+      const uint4* kr = reinterpret_cast<const uint4*>(qkv + key * tok_stride + (a.H + h) * 128);
+      float dot = 0.f;
+#pragma unroll 4
+      for (int v = 0; v < 16; ++v) {
+        const uint4 w = kr[v];
+        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          dot = fmaf(qs[warp][v * 8 + 2 * k], bf16_lo(ws[k]), dot);
+          dot = fmaf(qs[warp][v * 8 + 2 * k + 1], bf16_hi(ws[k]), dot);
+        }
+      }
+      sc = dot;
+    }
+    float mb = sc;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, o));
+    const float mn = fmaxf(m, mb);
+    const float alpha = exp2f(m - mn);
+    const float p = key <= t ? exp2f(sc - mn) : 0.f;
+    float ps = p;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
+    l = l * alpha + ps;
+    m = mn;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) acc[k] *= alpha;
+    const int nk = min(32, t - k0 + 1);
+    for (int j = 0; j < nk; ++j) {
+      const float pj = __shfl_sync(0xffffffffu, p, j);
+      const uint2 vv = *reinterpret_cast<const uint2*>(qkv + (k0 + j) * tok_stride + (2 * a.H + h) * 128 + lane * 4);
+      acc[0] = fmaf(pj, bf16_lo(vv.x), acc[0]);
+      acc[1] = fmaf(pj, bf16_hi(vv.x), acc[1]);
+      acc[2] = fmaf(pj, bf16_lo(vv.y), acc[2]);
+      acc[3] = fmaf(pj, bf16_hi(vv.y), acc[3]);
+    }
+  }
+  const float inv = 1.f / l;
+  __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(a.out) + (static_cast<int64_t>(t) * a.H + h) * 128 + lane * 4;
+  *reinterpret_cast<uint2*>(o) = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv),
+                                            pack_bf16(acc[2] * inv, acc[3] * inv));
+}
+
+__device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+__global__ void init_normal_kernel(__nv_bfloat16* dst, int64_t n, uint64_t seed, float std) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) {
+    const uint64_t r = splitmix64(seed ^ splitmix64(static_cast<uint64_t>(i)));
+    const float u1 = (static_cast<float>(r >> 40) + 0.5f) * (1.0f / 16777216.0f);
+    const float u2 = static_cast<float>((r >> 16) & 0xFFFFFF) * (1.0f / 16777216.0f);
+    const float z = sqrtf(-2.f * __logf(u1)) * __cosf(6.28318530718f * u2);
+    dst[i] = __float2bfloat16_rn(z * std);
+  }
+}
+
+__global__ void fill_kernel(float* dst, int64_t n, float v) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < n; i += stride) dst[i] = v;
+}
+
+}  // namespace
+
+cudaError_t embed_rmsnorm(const void* emb, const int32_t* tokens, const float* norm_w, float* resid,
+                          void* xn, int T, int hidden, float eps, cudaStream_t stream) {
+  if (T <= 0) return cudaSuccess;
+  embed_rmsnorm_kernel<<<T, kRowThreads, 0, stream>>>(
+      reinterpret_cast<const __nv_bfloat16*>(emb), tokens, norm_w, resid,
+      reinterpret_cast<__nv_bfloat16*>(xn), hidden, eps);
+  return cudaGetLastError();
+}
+
+cudaError_t reduce_residual_rmsnorm(const float* parts, int splits, float* resid, const float* norm_w,
+                                    void* xn, int T, int hidden, float eps, cudaStream_t stream) {
+  if (T <= 0) return cudaSuccess;
+  reduce_residual_rmsnorm_kernel<<<T, kRowThreads, 0, stream>>>(
+      parts, splits, T, resid, norm_w, reinterpret_cast<__nv_bfloat16*>(xn), hidden, eps);
+  return cudaGetLastError();
+}
+
+cudaError_t argmax_rows(const float* logits, int T, int V, int32_t* out, cudaStream_t stream) {
+  if (T <= 0) return cudaSuccess;
+  argmax_kernel<<<T, kRowThreads, 0, stream>>>(logits, V, out);
+  return cudaGetLastError();
+}
+
+cudaError_t gather_rows_bf16(const void* src, const int32_t* idx, void* dst, int n, int cols,
+                             cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  gather_rows_kernel<<<n, 128, 0, stream>>>(reinterpret_cast<const uint4*>(src), idx,
+                                            reinterpret_cast<uint4*>(dst), cols / 8);
+  return cudaGetLastError();
+}
+
+cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
+  if (a.T <= 0) return cudaSuccess;
+  const int warps = a.T * a.H;
+  prefill_attention_kernel<<<(warps + 3) / 4, 128, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t init_normal_bf16(void* dst, int64_t n, uint64_t seed, float std, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  init_normal_kernel<<<148 * 8, 256, 0, stream>>>(reinterpret_cast<__nv_bfloat16*>(dst), n, seed, std);
+  return cudaGetLastError();
+}
+
+cudaError_t fill_f32(float* dst, int64_t n, float v, cudaStream_t stream) {
+  if (n <= 0) return cudaSuccess;
+  fill_kernel<<<148 * 4, 256, 0, stream>>>(dst, n, v);
+  return cudaGetLastError();
+}
+
+}  // namespace mux

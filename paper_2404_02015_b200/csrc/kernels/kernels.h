@@ -1,0 +1,105 @@
+// Launch interfaces of the sm_100a kernels (host-callable, stream-ordered).
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace mux {
+
+// ---- K1 decode attention -------------------------------------------------
+struct DecodeAttnArgs {
+  const void* q;            // [B][H][128] bf16 (already RoPE-rotated)
+  const void* pool;         // [n_blocks][16][128] bf16
+  const int32_t* rowrec;    // [n_rowrec][L*H*2]
+  const int32_t* rowlist;   // [slots][max_rows]
+  const int32_t* slots;     // [B] device-table slot of each member
+  const int32_t* ctx;       // [B] cached tokens incl. the one appended this step
+  void* out;                // [B][H][128] bf16 or fp32
+  float* part_o;            // [B][H][splits][128] (splits > 1)
+  float* part_ml;           // [B][H][splits][2]   (splits > 1)
+  int B, H, layer, max_rows, row_width;
+  int splits, rows_per_split;
+  float scale_log2;         // log2(e) / sqrt(128)
+};
+cudaError_t decode_attention(const DecodeAttnArgs& a, bool fp32_out, cudaStream_t stream);
+int decode_attention_max_rows_per_split();
+
+// ---- K2 KV append (+ RoPE) and block-table maintenance --------------------
+struct AppendArgs {
+  const void* qkv;          // [T][3][H][128] bf16 (q | k | v per token)
+  void* q_out;              // [T][H][128] bf16 rotated q (may be null)
+  void* pool;               // [n_blocks][16][128] bf16
+  const int32_t* rowrec;
+  const int32_t* rowlist;
+  const int32_t* tok_slot;  // [T] slot of the request owning the token
+  const int32_t* tok_pos;   // [T] position of the token in its request
+  const float* rope;        // [max_pos][64][2] (cos, sin)
+  int T, H, layer, max_rows, row_width;
+  int rope_positions;
+};
+cudaError_t kv_append(const AppendArgs& a, cudaStream_t stream);
+
+// Scatter freshly allocated rows into the device block tables:
+//   rowrec[rec[i]][:] = ids[i][:], rowlist[slot[i]][row[i]] = rec[i]
+struct TableUpdateArgs {
+  const int32_t* meta;      // [n][3] (slot, row, rowrec)
+  const int32_t* ids;       // [n][row_width]
+  int32_t* rowrec;
+  int32_t* rowlist;
+  int n, row_width, max_rows;
+};
+cudaError_t table_update(const TableUpdateArgs& a, cudaStream_t stream);
+
+// ---- K4 tcgen05 GEMM: D[M x N] = X[M x K] * W[N x K]^T -------------------
+// Weight-stationary tiling: every CTA owns 128 rows of W (one UMMA M=128
+// tile) and up to 256 activation rows (UMMA N), so decode batches (M <= 256)
+// stream each weight byte exactly once.
+enum class Epilogue : int {
+  kStoreBf16 = 0,   // out bf16 [M][ldo]
+  kPartialF32 = 1,  // out fp32 [split][M][ldo] (split-K partial sums)
+  kSiluMulBf16 = 2, // W rows interleaved (gate, up) pairs: out bf16 [M][N/2]
+  kStoreF32 = 3,    // out fp32 [M][ldo]
+};
+struct GemmArgs {
+  const void* tmap_w;       // CUtensorMap* (host memory, passed by value)
+  const void* tmap_x;
+  void* out;
+  int M, N, K;
+  int ldo;
+  int splits;               // split-K factor (kPartialF32 only)
+  Epilogue epi;
+};
+cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream);
+// Encode a 2-D bf16 tensor map (rows x cols, cols contiguous) with a
+// box of box_rows x 64 and 128-byte swizzle. Returns false on failure.
+bool make_tmap_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t cols,
+                    uint64_t row_stride_bytes, uint32_t box_rows);
+
+// ---- K5 small fused ops ---------------------------------------------------
+cudaError_t embed_rmsnorm(const void* emb, const int32_t* tokens, const float* norm_w,
+                          float* resid, void* xn, int T, int hidden, float eps,
+                          cudaStream_t stream);
+// resid[t] += sum_s parts[s][t]; xn[t] = rmsnorm(resid[t]) * w (bf16)
+cudaError_t reduce_residual_rmsnorm(const float* parts, int splits, float* resid,
+                                    const float* norm_w, void* xn, int T, int hidden, float eps,
+                                    cudaStream_t stream);
+// Row argmax of fp32 logits; writes token ids (lowest index on ties).
+cudaError_t argmax_rows(const float* logits, int T, int V, int32_t* out, cudaStream_t stream);
+// Gather rows: dst[i] = src[idx[i]] (bf16 rows of `cols`).
+cudaError_t gather_rows_bf16(const void* src, const int32_t* idx, void* dst, int n, int cols,
+                             cudaStream_t stream);
+// Causal varlen prefill attention over the fresh q/k/v (fp32 math).
+struct PrefillAttnArgs {
+  const void* q;            // [T][H][128] bf16 rotated
+  const void* qkv;          // [T][3][H][128] bf16 (k rotated in-place by kv_append)
+  void* out;                // [T][H][128] bf16
+  const int32_t* seq_start; // [nseq + 1]
+  int nseq, H, T;
+  float scale_log2;
+};
+cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream);
+// Deterministic N(0, std) init of a bf16 buffer from (seed, index).
+cudaError_t init_normal_bf16(void* dst, int64_t n, uint64_t seed, float std, cudaStream_t stream);
+cudaError_t fill_f32(float* dst, int64_t n, float v, cudaStream_t stream);
+
+}  // namespace mux

@@ -1,0 +1,127 @@
+// K2: KV append with block allocation.
+//
+// Replaces the device side of BlockPool::alloc(llm, rid, +1) / admit's prompt
+// rows (/root/reference/proj/src/scheduler.cpp:105, kv_manager.cpp:87-120):
+// the host pool decides which 4 KiB head-blocks a new 16-token row gets
+// (csrc/host/kv.cpp), table_update scatters those ids into the device block
+// tables, and kv_append writes each token's K (after RoPE) and V into slot
+// pos % 16 of its (layer, head) blocks. One warp per (token, head); lane =
+// 4 dims (8-byte loads/stores, 256 B per warp per block row).
+#include <cstdint>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include "kernels.h"
+#include "ptx.cuh"
+
+namespace mux {
+namespace {
+
+constexpr int kDim = 128;
+
+__device__ __forceinline__ void unpack4(uint2 v, float (&x)[4]) {
+  x[0] = bf16_lo(v.x);
+  x[1] = bf16_hi(v.x);
+  x[2] = bf16_lo(v.y);
+  x[3] = bf16_hi(v.y);
+}
+
+__device__ __forceinline__ uint2 pack4(const float (&x)[4]) {
+  return make_uint2(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]));
+}
+
+// rotate_half RoPE on 4 dims held by this lane; partner dims live in lane^16.
+// Explicit _rn intrinsics: no FMA contraction, so the CPU oracle's float32
+// arithmetic reproduces it bit for bit.
+__device__ __forceinline__ void rope4(float (&x)[4], const float* cs, int lane) {
+  float other[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) other[k] = __shfl_xor_sync(0xffffffffu, x[k], 16);
+  const int f0 = (lane & 15) * 4;
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    const float c = cs[2 * (f0 + k)];
+    const float s = cs[2 * (f0 + k) + 1];
+    if (lane < 16) {
+      x[k] = __fsub_rn(__fmul_rn(x[k], c), __fmul_rn(other[k], s));
+    } else {
+      x[k] = __fadd_rn(__fmul_rn(x[k], c), __fmul_rn(other[k], s));
+    }
+  }
+}
+
+__global__ void __launch_bounds__(256) kv_append_kernel(const AppendArgs a) {
+  const int warp_global = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (warp_global >= a.T * a.H) return;
+  const int t = warp_global / a.H;
+  const int h = warp_global % a.H;
+  const int pos = a.tok_pos[t];
+  const int slot = a.tok_slot[t];
+
+  const int64_t tok_base = static_cast<int64_t>(t) * 3 * a.H * kDim;
+  const __nv_bfloat16* qkv = reinterpret_cast<const __nv_bfloat16*>(a.qkv);
+  const uint2 qv = *reinterpret_cast<const uint2*>(qkv + tok_base + (0 * a.H + h) * kDim + lane * 4);
+  const uint2 kv = *reinterpret_cast<const uint2*>(qkv + tok_base + (1 * a.H + h) * kDim + lane * 4);
+  const uint2 vv = *reinterpret_cast<const uint2*>(qkv + tok_base + (2 * a.H + h) * kDim + lane * 4);
+  float q[4], k[4];
+  unpack4(qv, q);
+  unpack4(kv, k);
+  const float* cs = a.rope + static_cast<int64_t>(min(pos, a.rope_positions - 1)) * 128;
+  rope4(q, cs, lane);
+  rope4(k, cs, lane);
+  const uint2 kr = pack4(k);
+  if (a.q_out != nullptr) {
+    __nv_bfloat16* qo = reinterpret_cast<__nv_bfloat16*>(a.q_out);
+    *reinterpret_cast<uint2*>(qo + (static_cast<int64_t>(t) * a.H + h) * kDim + lane * 4) = pack4(q);
+    // Rotated k back in place too, for the prefill attention that reads it.
+    __nv_bfloat16* qkv_w = const_cast<__nv_bfloat16*>(qkv);
+    *reinterpret_cast<uint2*>(qkv_w + tok_base + (1 * a.H + h) * kDim + lane * 4) = kr;
+  }
+
+  const int row = pos >> 4;
+  const int in_blk = pos & 15;
+  const int rr = a.rowlist[static_cast<int64_t>(slot) * a.max_rows + row];
+  const int32_t* rec = a.rowrec + static_cast<int64_t>(rr) * a.row_width + (a.layer * a.H + h) * 2;
+  const int kid = rec[0];
+  const int vid = rec[1];
+  uint8_t* pool = reinterpret_cast<uint8_t*>(a.pool);
+  const int64_t off = static_cast<int64_t>(in_blk) * 256 + lane * 8;
+  *reinterpret_cast<uint2*>(pool + static_cast<int64_t>(kid) * 4096 + off) = kr;
+  *reinterpret_cast<uint2*>(pool + static_cast<int64_t>(vid) * 4096 + off) = vv;
+}
+
+__global__ void __launch_bounds__(256) table_update_kernel(const TableUpdateArgs a) {
+  const int i = blockIdx.x;
+  const int slot = a.meta[3 * i + 0];
+  const int row = a.meta[3 * i + 1];
+  const int rec = a.meta[3 * i + 2];
+  const int4* src = reinterpret_cast<const int4*>(a.ids + static_cast<int64_t>(i) * a.row_width);
+  int32_t* dst32 = a.rowrec + static_cast<int64_t>(rec) * a.row_width;
+  if ((a.row_width & 3) == 0) {
+    int4* dst = reinterpret_cast<int4*>(dst32);
+    for (int j = threadIdx.x; j < a.row_width / 4; j += blockDim.x) dst[j] = src[j];
+  } else {
+    const int32_t* s32 = a.ids + static_cast<int64_t>(i) * a.row_width;
+    for (int j = threadIdx.x; j < a.row_width; j += blockDim.x) dst32[j] = s32[j];
+  }
+  if (threadIdx.x == 0) a.rowlist[static_cast<int64_t>(slot) * a.max_rows + row] = rec;
+}
+
+}  // namespace
+
+cudaError_t kv_append(const AppendArgs& a, cudaStream_t stream) {
+  if (a.T <= 0) return cudaSuccess;
+  const int warps = a.T * a.H;
+  const int blocks = (warps + 7) / 8;
+  kv_append_kernel<<<blocks, 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+cudaError_t table_update(const TableUpdateArgs& a, cudaStream_t stream) {
+  if (a.n <= 0) return cudaSuccess;
+  table_update_kernel<<<a.n, 256, 0, stream>>>(a);
+  return cudaGetLastError();
+}
+
+}  // namespace mux

@@ -1,0 +1,448 @@
+"""Host-side mirror of the reference hot-path API over the C ABI.
+
+Names, argument meaning and error behaviour follow the reference C++ API
+(/root/reference/proj/include/muxsim/kv_manager.hpp, scheduler.hpp,
+sim_engine.hpp); everything executes in libmux.so. The device unit
+(:class:`Unit`) is the B200 extension: the KV pool in HBM, colocated LLaMA
+models and the prefill/decode jobs that ``UnitSim::launch``
+(/root/reference/proj/src/sim_engine.cpp:308-330) only priced.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass, field
+from typing import Iterable, Sequence
+
+from ._lib import (ALLOC_OK, ALLOC_POOL, ALLOC_QUOTA, LlmEntry as _CEntry, PlacedLlm, Record,
+                   Request as _CRequest, SimConfig, UnitConfig, check, lib)
+
+# ----------------------------------------------------------------- model specs
+
+
+@dataclass(frozen=True)
+class LLMSpec:
+    """cost_model.hpp:11-21 plus the FFN width / vocabulary a real forward needs
+    (the reference catalog has neither)."""
+    name: str
+    num_layers: int
+    num_heads: int
+    head_dim: int = 128
+    hidden_size: int = 0
+    weight_bytes: int = 1
+    bytes_per_element: int = 2
+    ffn: int = 0
+    vocab: int = 32000
+
+    def kv_bytes_per_token(self) -> float:
+        return 2.0 * self.num_layers * self.num_heads * self.head_dim * self.bytes_per_element
+
+
+# Reference catalog (config.cpp:12-22) extended with LLaMA-1 FFN sizes and vocab.
+CATALOG = {
+    "7b": LLMSpec("7b", 32, 32, 128, 4096, int(13.5e9), 2, 11008, 32000),
+    "13b": LLMSpec("13b", 40, 40, 128, 5120, int(26e9), 2, 13824, 32000),
+    "30b": LLMSpec("30b", 60, 52, 128, 6656, int(65e9), 2, 17920, 32000),
+    "65b": LLMSpec("65b", 80, 64, 128, 8192, int(130e9), 2, 22016, 32000),
+    # BASELINE config 1 (SURVEY.md Appendix B "Tiny"), head_dim 128 so that
+    # block bytes agree with the big models (sim_engine.cpp:180-184).
+    "tiny-a": LLMSpec("tiny-a", 2, 4, 128, 512, 8_000_000, 2, 1024, 512),
+    "tiny-b": LLMSpec("tiny-b", 4, 2, 128, 256, 4_000_000, 2, 512, 512),
+}
+
+
+def spec(name: str, alias: str | None = None) -> LLMSpec:
+    s = CATALOG[name]
+    if alias:
+        s = LLMSpec(alias, *[getattr(s, f) for f in
+                             ("num_layers", "num_heads", "head_dim", "hidden_size", "weight_bytes",
+                              "bytes_per_element", "ffn", "vocab")])
+    return s
+
+
+def _c_entry(s: LLMSpec, rate=0.0, mean_prompt=1.0, mean_output=1.0, keep=None) -> _CEntry:
+    name = s.name.encode()
+    if keep is not None:
+        keep.append(name)
+    return _CEntry(name, s.num_layers, s.num_heads, s.head_dim, s.hidden_size, s.weight_bytes,
+                   s.bytes_per_element, rate, mean_prompt, mean_output, s.ffn, s.vocab)
+
+
+# -------------------------------------------------------------- geometry/quota
+
+def blocks_for_tokens(s: LLMSpec, block_tokens: int, tokens: int) -> int:
+    out = C.c_int64()
+    check(lib.mux_blocks_for_tokens(s.num_layers, s.num_heads, block_tokens, tokens, C.byref(out)))
+    return out.value
+
+
+def blocks_per_token(s: LLMSpec, block_tokens: int) -> float:
+    return 2.0 * s.num_layers * s.num_heads / block_tokens
+
+
+@dataclass
+class QuotaInput:
+    rate: float = 0.0
+    blocks_per_token: float = 0.0
+    mean_request_tokens: float = 0.0
+
+
+def init_token_block_quota(llms: Sequence[QuotaInput], kv_blocks: int, floor_frac: float = 0.02):
+    n = len(llms)
+    arr = C.c_double * max(n, 1)
+    out = (C.c_int64 * max(n, 1))()
+    check(lib.mux_init_token_block_quota(n, arr(*[q.rate for q in llms]),
+                                         arr(*[q.blocks_per_token for q in llms]),
+                                         arr(*[q.mean_request_tokens for q in llms]),
+                                         kv_blocks, floor_frac, out))
+    return list(out[:n])
+
+
+def adapt_quota(utilizations: Sequence[float], quotas: Sequence[int], floor_blocks: int,
+                low_mark=0.5, high_mark=0.9, step_frac=0.1):
+    n = len(quotas)
+    out = (C.c_int64 * max(n, 1))()
+    check(lib.mux_adapt_quota(n, (C.c_double * max(n, 1))(*utilizations),
+                              (C.c_int64 * max(n, 1))(*quotas), floor_blocks, low_mark, high_mark,
+                              step_frac, out))
+    return list(out[:n])
+
+
+# ------------------------------------------------------------------- BlockPool
+
+@dataclass
+class AllocResult:
+    ok: bool
+    error: str  # "none" | "pool" | "quota"
+
+
+_ERR = {ALLOC_OK: "none", ALLOC_POOL: "pool", ALLOC_QUOTA: "quota"}
+
+
+class BlockPool:
+    """kv_manager.hpp:48-105 over the C ABI, with physical head-block ids."""
+
+    def __init__(self, total_blocks: int, physical: bool = True, _handle=None):
+        self._owned = _handle is None
+        if _handle is None:
+            h = C.c_void_p()
+            check(lib.mux_pool_create(total_blocks, 1 if physical else 0, C.byref(h)))
+            _handle = h.value
+        self._h = _handle
+
+    def __del__(self):
+        if getattr(self, "_owned", False) and getattr(self, "_h", None):
+            lib.mux_pool_destroy(self._h)
+            self._h = None
+
+    def register_llm(self, llm: int, s: LLMSpec, block_tokens: int = 16):
+        check(lib.mux_pool_register_llm(self._h, llm, s.num_layers, s.num_heads, s.head_dim,
+                                        s.bytes_per_element, block_tokens))
+
+    def admit(self, llm, request_id, prompt_tokens, total_tokens) -> AllocResult:
+        r = C.c_int()
+        check(lib.mux_pool_admit(self._h, llm, request_id, prompt_tokens, total_tokens, C.byref(r)))
+        return AllocResult(r.value == ALLOC_OK, _ERR[r.value])
+
+    def alloc(self, llm, request_id, add_tokens, enforce_quota) -> AllocResult:
+        r = C.c_int()
+        check(lib.mux_pool_alloc(self._h, llm, request_id, add_tokens, 1 if enforce_quota else 0,
+                                 C.byref(r)))
+        return AllocResult(r.value == ALLOC_OK, _ERR[r.value])
+
+    def free_request(self, llm, request_id):
+        check(lib.mux_pool_free_request(self._h, llm, request_id))
+
+    def set_quota(self, llm, blocks):
+        check(lib.mux_pool_set_quota(self._h, llm, blocks))
+
+    def _stats(self, llm):
+        q, u, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib.mux_pool_llm_stats(self._h, llm, C.byref(q), C.byref(u), C.byref(c)))
+        return q.value, u.value, c.value
+
+    def quota(self, llm):
+        return self._stats(llm)[0]
+
+    def used(self, llm):
+        return self._stats(llm)[1]
+
+    def committed(self, llm):
+        return self._stats(llm)[2]
+
+    def request_tokens(self, llm, request_id):
+        t = C.c_int64()
+        check(lib.mux_pool_request_tokens(self._h, llm, request_id, C.byref(t)))
+        return t.value
+
+    def _totals(self):
+        f, t, c = C.c_int64(), C.c_int64(), C.c_int64()
+        check(lib.mux_pool_totals(self._h, C.byref(f), C.byref(t), C.byref(c)))
+        return f.value, t.value, c.value
+
+    def free_blocks(self):
+        return self._totals()[0]
+
+    def total_blocks(self):
+        return self._totals()[1]
+
+    def committed_total(self):
+        return self._totals()[2]
+
+    def total_used(self):
+        f, t, _ = self._totals()
+        return t - f
+
+    def check_conservation(self):
+        check(lib.mux_pool_check(self._h))
+
+    def block_table(self, llm, request_id) -> list[int]:
+        n = C.c_int64()
+        check(lib.mux_pool_block_table(self._h, llm, request_id, None, 0, C.byref(n)))
+        buf = (C.c_int32 * max(n.value, 1))()
+        check(lib.mux_pool_block_table(self._h, llm, request_id, buf, n.value, C.byref(n)))
+        return list(buf[:n.value])
+
+    def slot(self, llm, request_id) -> int:
+        s = C.c_int()
+        check(lib.mux_pool_slot(self._h, llm, request_id, C.byref(s)))
+        return s.value
+
+
+# ------------------------------------------------------------------ simulate
+
+@dataclass
+class TraceRequest:
+    id: int
+    llm: int            # index into the entries
+    arrival_s: float
+    prompt_len: int
+    output_len: int
+
+
+@dataclass
+class EngineParams:
+    """sim_engine.hpp:15-28 defaults."""
+    scheduler: int = 0  # 0 ADBS, 1 FCFS, 2 round-robin
+    kappa: float = 0.1
+    quota_period_s: float = 10.0
+    token_budget: int = 4096
+    block_tokens: int = 16
+    warmup_s: float = 0.0
+    decode_sm: float = 0.5
+    prefill_min_sm: float = 0.3
+    activation_reserve_frac: float = 0.1
+    quota_floor_frac: float = 0.02
+
+
+@dataclass
+class Entry:
+    spec: LLMSpec
+    rate: float = 0.0
+    mean_prompt_tokens: float = 1.0
+    mean_output_tokens: float = 1.0
+
+
+@dataclass
+class Placement:
+    """Units (mesh sizes) and which entries each serves."""
+    mesh_sizes: list[int]
+    members: list[list[int]]                 # per unit: entry indices
+    num_sm: float = 0.5
+
+
+@dataclass
+class _Built:
+    cfg: SimConfig
+    keep: list = field(default_factory=list)
+
+
+def _build_config(gpu_memory_bytes: int, num_gpus: int, placement: Placement, params: EngineParams,
+                  profile: Sequence[float] | None) -> _Built:
+    keep = []
+    sizes = (C.c_int * len(placement.mesh_sizes))(*placement.mesh_sizes)
+    placed_list = [PlacedLlm(u, e, placement.mesh_sizes[u], placement.num_sm)
+                   for u, mem in enumerate(placement.members) for e in mem]
+    placed = (PlacedLlm * max(len(placed_list), 1))(*placed_list)
+    prof = None if profile is None else (C.c_double * 7)(*profile)
+    keep += [sizes, placed, prof]
+    cfg = SimConfig(1, num_gpus, gpu_memory_bytes, len(placement.mesh_sizes), sizes, len(placed_list),
+                    placed, prof, params.scheduler, params.kappa, params.quota_period_s,
+                    params.token_budget, params.block_tokens, params.warmup_s, params.decode_sm,
+                    params.prefill_min_sm, params.activation_reserve_frac, params.quota_floor_frac)
+    return _Built(cfg, keep)
+
+
+def _c_entries(entries: Sequence[Entry], keep):
+    arr = (_CEntry * len(entries))(*[_c_entry(e.spec, e.rate, e.mean_prompt_tokens,
+                                             e.mean_output_tokens, keep) for e in entries])
+    keep.append(arr)
+    return arr
+
+
+def _c_trace(trace: Sequence[TraceRequest]):
+    return (_CRequest * max(len(trace), 1))(*[_CRequest(r.id, r.llm, r.arrival_s, r.prompt_len,
+                                                        r.output_len) for r in trace])
+
+
+def simulate(entries: Sequence[Entry], trace: Sequence[TraceRequest], placement: Placement,
+             gpu_memory_bytes: int, params: EngineParams | None = None,
+             profile: Sequence[float] | None = None) -> list[Record]:
+    """run_simulation (sim_engine.cpp:370-413), priced. Records sorted by id."""
+    params = params or EngineParams()
+    b = _build_config(gpu_memory_bytes, sum(placement.mesh_sizes), placement, params, profile)
+    ents = _c_entries(entries, b.keep)
+    recs = (Record * max(len(trace), 1))()
+    check(lib.mux_simulate(C.byref(b.cfg), len(entries), ents, len(trace), _c_trace(trace), recs))
+    return list(recs[:len(trace)])
+
+
+# ---------------------------------------------------------------------- Unit
+
+def _ptr(x) -> int | None:
+    if x is None:
+        return None
+    if hasattr(x, "data_ptr"):
+        return x.data_ptr()
+    return int(x)
+
+
+class Unit:
+    """One GPU: the unified KV pool in HBM plus colocated LLaMA models."""
+
+    def __init__(self, specs: Sequence[LLMSpec], pool_blocks: int, device: int = 0,
+                 device_pool_blocks: int = 0, max_batch: int = 256, max_prefill_tokens: int = 4096,
+                 max_ctx: int = 4096, max_slots: int = 0, init_seed: int = 0,
+                 init_std: float = 0.02, partitions: int = 2):
+        self.specs = list(specs)
+        self._keep = []
+        ents = (_CEntry * len(specs))(*[_c_entry(s, keep=self._keep) for s in specs])
+        self._keep.append(ents)
+        cfg = UnitConfig(device, len(specs), ents, pool_blocks, device_pool_blocks, max_batch,
+                         max_prefill_tokens, max_ctx, max_slots, init_seed, init_std, partitions)
+        h = C.c_void_p()
+        check(lib.mux_unit_create(C.byref(cfg), C.byref(h)))
+        self._h = h.value
+        self.pool = BlockPool(0, _handle=lib.mux_unit_pool(self._h))
+
+    def close(self):
+        if getattr(self, "_h", None):
+            lib.mux_unit_destroy(self._h)
+            self._h = None
+
+    def __del__(self):
+        self.close()
+
+    def set_tensor(self, llm: int, name: str, layer: int, host_array) -> None:
+        """host_array: a contiguous numpy array in device layout (see mux.h)."""
+        check(lib.mux_unit_set_tensor(self._h, llm, name.encode(), layer,
+                                      host_array.ctypes.data, host_array.nbytes))
+
+    def get_tensor(self, llm: int, name: str, layer: int, host_array) -> None:
+        check(lib.mux_unit_get_tensor(self._h, llm, name.encode(), layer,
+                                      host_array.ctypes.data, host_array.nbytes))
+
+    def init_kv(self, seed: int = 1, std: float = 1.0):
+        check(lib.mux_unit_init_kv(self._h, seed, std))
+
+    def device_ptrs(self, llm: int):
+        pool, rr, rl = C.c_void_p(), C.c_void_p(), C.c_void_p()
+        mr, rw = C.c_int(), C.c_int()
+        check(lib.mux_unit_device_ptrs(self._h, llm, C.byref(pool), C.byref(rr), C.byref(rl),
+                                       C.byref(mr), C.byref(rw)))
+        return pool.value, rr.value, rl.value, mr.value, rw.value
+
+    @staticmethod
+    def _ids(request_ids):
+        return (C.c_int64 * len(request_ids))(*request_ids)
+
+    def prefill(self, llm: int, request_ids: Sequence[int], tokens, out=None, partition: int = 0):
+        """tokens: int32 numpy array (concatenated prompts); out: int32 numpy or None."""
+        check(lib.mux_unit_prefill(self._h, llm, len(request_ids), self._ids(request_ids),
+                                   tokens.ctypes.data_as(C.POINTER(C.c_int32)),
+                                   None if out is None else out.ctypes.data_as(C.POINTER(C.c_int32)),
+                                   partition))
+
+    def decode(self, llm: int, request_ids: Sequence[int], tokens=None, out=None, partition: int = 0,
+               ids_c=None):
+        ids = ids_c if ids_c is not None else self._ids(request_ids)
+        check(lib.mux_unit_decode(
+            self._h, llm, len(request_ids), ids,
+            None if tokens is None else tokens.ctypes.data_as(C.POINTER(C.c_int32)),
+            None if out is None else out.ctypes.data_as(C.POINTER(C.c_int32)), partition))
+
+    def sync(self):
+        check(lib.mux_unit_sync(self._h))
+
+    def record(self, partition: int, slot: int):
+        check(lib.mux_unit_record(self._h, partition, slot))
+
+    def elapsed_ms(self, a: int, b: int) -> float:
+        ms = C.c_float()
+        check(lib.mux_unit_elapsed(self._h, a, b, C.byref(ms)))
+        return ms.value
+
+    def attn_timing(self, enable: bool):
+        check(lib.mux_unit_attn_timing(self._h, 1 if enable else 0))
+
+    def attn_time(self):
+        ms, n, by = C.c_double(), C.c_int64(), C.c_double()
+        check(lib.mux_unit_attn_time(self._h, C.byref(ms), C.byref(n), C.byref(by)))
+        return ms.value, n.value, by.value
+
+    def launches(self) -> int:
+        return int(lib.mux_unit_launches(self._h))
+
+    def run_lockstep(self, entries: Sequence[Entry], trace: Sequence[TraceRequest],
+                     gpu_memory_bytes: int, params: EngineParams | None = None,
+                     prompt_seed: int = 11, num_sm: float = 0.5, profile=None):
+        """Engine decisions priced by the oracle model, every job run on this GPU.
+        Returns (records, tokens) with tokens[i] the output of trace[i]."""
+        params = params or EngineParams()
+        placement = Placement([1], [list(range(len(entries)))], num_sm)
+        b = _build_config(gpu_memory_bytes, 1, placement, params, profile)
+        ents = _c_entries(entries, b.keep)
+        recs = (Record * max(len(trace), 1))()
+        total = sum(r.output_len for r in trace)
+        toks = (C.c_int32 * max(total, 1))()
+        check(lib.mux_unit_run_lockstep(self._h, C.byref(b.cfg), len(entries), ents, len(trace),
+                                        _c_trace(trace), prompt_seed, recs, toks))
+        out, off = [], 0
+        for r in trace:
+            out.append(list(toks[off:off + r.output_len]))
+            off += r.output_len
+        return list(recs[:len(trace)]), out
+
+
+# ------------------------------------------------------------ kernel wrappers
+
+def decode_attention_headwise(q, pool_ptr, rowrec_ptr, rowlist_ptr, slots, ctx, num_layers: int,
+                              layer: int, max_rows: int, max_ctx: int, out, kv_splits: int = 0,
+                              workspace=None, stream=None):
+    """K1 for one layer; q/out/slots/ctx are torch CUDA tensors."""
+    B, H = q.shape[0], q.shape[1]
+    ws_bytes = workspace.numel() * workspace.element_size() if workspace is not None else 0
+    check(lib.mux_decode_attention_headwise(
+        _ptr(q), _ptr(pool_ptr), _ptr(rowrec_ptr), _ptr(rowlist_ptr), _ptr(slots), _ptr(ctx), B, H,
+        num_layers, layer, max_rows, max_ctx, _ptr(out), 1 if out.dtype.itemsize == 4 else 0,
+        kv_splits, _ptr(workspace), ws_bytes, _ptr(stream)))
+
+
+def kv_append(qkv, q_out, pool_ptr, rowrec_ptr, rowlist_ptr, tok_slot, tok_pos, rope, T: int, H: int,
+              num_layers: int, layer: int, max_rows: int, stream=None):
+    check(lib.mux_kv_append(_ptr(qkv), _ptr(q_out), _ptr(pool_ptr), _ptr(rowrec_ptr),
+                            _ptr(rowlist_ptr), _ptr(tok_slot), _ptr(tok_pos), _ptr(rope),
+                            rope.shape[0], T, H, num_layers, layer, max_rows, _ptr(stream)))
+
+
+def rope_table(positions: int):
+    import numpy as np
+    out = np.empty((positions, 64, 2), dtype=np.float32)
+    check(lib.mux_rope_table(positions, out.ctypes.data_as(C.POINTER(C.c_float))))
+    return out
+
+
+def gemm_bf16(x, w, out, epilogue: int = 0, splits: int = 1, stream=None):
+    """out = x @ w.T on tcgen05; x [M,K], w [N,K] bf16 CUDA tensors."""
+    M, K = x.shape
+    N = w.shape[0]
+    check(lib.mux_gemm_bf16(_ptr(x), _ptr(w), M, N, K, _ptr(out), epilogue, splits, _ptr(stream)))
