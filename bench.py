@@ -221,6 +221,7 @@ def main():
     ap.add_argument("--batch", type=int, default=128, help="decode members per model")
     ap.add_argument("--models", default="7b,13b")
     ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg (profiling runs)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))
@@ -252,7 +253,7 @@ def main():
     value = tokens / (ms / 1e3)
     per_step_tokens = tokens / args.steps
     cpu = None
-    if rank == 0 and world == 1:
+    if rank == 0 and world == 1 and not args.skip_cpu:
         from bench_cpu import cpu_baseline
         cpu = cpu_baseline(args)
     if rank == 0:

@@ -33,7 +33,8 @@ def f32_to_bf16(x: np.ndarray) -> np.ndarray:
     u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
     r = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
     nan = (u & 0x7F800000) == 0x7F800000
-    r = np.where(nan, (u >> 16) | np.where((u & 0xFFFF) != 0, 0x40, 0), r)
+    quiet = np.where((u & 0xFFFF) != 0, np.uint64(0x40), np.uint64(0))
+    r = np.where(nan, (u >> 16) | quiet, r)
     return r.astype(np.uint16)
 
 

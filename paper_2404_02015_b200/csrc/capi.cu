@@ -547,6 +547,7 @@ int mux_unit_create(const mux_unit_config* cfg, mux_unit** out) {
       const mux_llm_entry& e = cfg->llms[i];
       u->specs.push_back(spec_of(e));
       u->pool.bp->register_llm(i, &u->specs.back(), 16);
+      u->pool.bp->set_quota(i, cfg->pool_blocks);  // no quota until a scheduler sets one
       mux::ModelDims d;
       d.name = u->specs.back().name;
       d.layers = e.num_layers;

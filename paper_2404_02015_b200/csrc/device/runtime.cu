@@ -331,7 +331,8 @@ void Runtime::upload_rows(muxsim::BlockPool& bp, int llm, Llama& m, cudaStream_t
   const int W = m.row_width();
   if (W != bp.row_width(llm)) throw std::logic_error("upload_rows: row width mismatch");
   const size_t n = pend.size();
-  const size_t need = n * (3 + static_cast<size_t>(W)) * 4;
+  const size_t meta_ints = (3 * n + 3) & ~size_t(3);  // keep the id block 16-byte aligned
+  const size_t need = (meta_ints + n * static_cast<size_t>(W)) * 4;
   StageSlot& slot = ring_[ring_next_];
   ring_next_ = (ring_next_ + 1) % 4;
   if (slot.done == nullptr) check_cuda(cudaEventCreateWithFlags(&slot.done, cudaEventDisableTiming), "event");
@@ -344,7 +345,7 @@ void Runtime::upload_rows(muxsim::BlockPool& bp, int llm, Llama& m, cudaStream_t
     slot.cap = cap;
   }
   int32_t* meta = slot.host->as<int32_t>();
-  int32_t* ids = meta + 3 * n;
+  int32_t* ids = meta + meta_ints;
   for (size_t i = 0; i < n; ++i) {
     const muxsim::RowDelta& d = pend[i];
     if (d.slot >= m.max_slots() || d.row >= m.max_rows() || d.rowrec >= m.max_rowrecs())
@@ -362,7 +363,7 @@ void Runtime::upload_rows(muxsim::BlockPool& bp, int llm, Llama& m, cudaStream_t
   check_cuda(cudaMemcpyAsync(slot.dev.p, slot.host->p, need, cudaMemcpyHostToDevice, stream), "stage copy");
   TableUpdateArgs t{};
   t.meta = slot.dev.as<int32_t>();
-  t.ids = slot.dev.as<int32_t>() + 3 * n;
+  t.ids = slot.dev.as<int32_t>() + meta_ints;
   t.rowrec = m.rowrec.as<int32_t>();
   t.rowlist = m.rowlist.as<int32_t>();
   t.n = static_cast<int>(n);

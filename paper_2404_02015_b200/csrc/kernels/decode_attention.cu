@@ -107,8 +107,8 @@ decode_attention_kernel(const DecodeAttnArgs a) {
   const int c = lane & 15;     // dims [8c, 8c+8)
   float q[8];
   {
-    const uint4 qv = *reinterpret_cast<const uint4*>(
-        a.q + (static_cast<int64_t>(b) * a.H + h) * kDim + c * 8);
+    const __nv_bfloat16* qp = reinterpret_cast<const __nv_bfloat16*>(a.q);
+    const uint4 qv = *reinterpret_cast<const uint4*>(qp + (static_cast<int64_t>(b) * a.H + h) * kDim + c * 8);
     const uint32_t w[4] = {qv.x, qv.y, qv.z, qv.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
