@@ -175,11 +175,20 @@ MUX_API int mux_kv_append(const void* qkv, void* q_out, void* pool, const int32_
 /* RoPE table [positions][64][(cos,sin)] fp32, theta 10000, head_dim 128. */
 MUX_API int mux_rope_table(int positions, float* out);
 
-/* K4: D[M x N] = X[M x K] * W[N x K]^T on tcgen05 (bf16 in, fp32 acc).
- * epilogue: 0 bf16 store, 1 fp32 split-K partials [splits][M][N],
+/* K4: D[M x N] = X[M x K] * W[N x K]^T on tcgen05 (bf16 in, fp32 acc),
+ * persistent stream-K over `grid` CTAs (0 = one per SM).
+ * epilogue: 0 bf16 store, 1 fp32 residual add (out += D),
  * 2 SiLU(gate)*up over interleaved rows -> bf16 [M][N/2], 3 fp32 store. */
-MUX_API int mux_gemm_bf16(const void* x, const void* w, int M, int N, int K, void* out, int epilogue,
-                  int splits, void* stream);
+MUX_API int mux_gemm_bf16(const void* x, const void* w, int w_tiled, int M, int N, int K, void* out,
+                  int epilogue, int grid, void* stream);
+/* B200 weight layout for K4: [ceil(N/128)][ceil(K/64)] contiguous, pre-swizzled
+ * 16 KiB UMMA tiles (one bulk copy each). w [N][K] row-major bf16 -> out
+ * (mux_weight_tiled_bytes(N, K) bytes); inverse != 0 converts back. */
+MUX_API int mux_weight_tile(const void* w, int N, int K, void* out, int inverse, void* stream);
+MUX_API int64_t mux_weight_tiled_bytes(int N, int K);
+/* Debug: per-CTA globaltimer stamps of every K4 launch ([grid][4] u64:
+ * start, MMA issue done, epilogue done, exit) into buf; NULL turns it off. */
+MUX_API void mux_debug_gemm_timing(void* buf);
 
 /* ---- device unit: one GPU, its KV pool and colocated models ---------- */
 
@@ -239,6 +248,8 @@ MUX_API int mux_unit_attn_timing(mux_unit* unit, int enable);
 MUX_API int mux_unit_attn_time(mux_unit* unit, double* total_ms, int64_t* launches, double* bytes);
 /* Kernel launches issued by this unit so far (all libmux kernels). */
 MUX_API int64_t mux_unit_launches(mux_unit* unit);
+/* Tuning knobs: "gemm_min_iters" (k-blocks per GEMM CTA, default 24). */
+MUX_API int mux_unit_set_option(mux_unit* unit, const char* key, int64_t value);
 
 /* Lockstep run: the engine's decisions are those of mux_simulate (oracle
  * timing), and every launched job executes on the unit's GPU. Synthetic

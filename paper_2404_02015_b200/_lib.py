@@ -104,7 +104,11 @@ _SIGS = {
     "mux_kv_append": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,
                                 C.c_int, C.c_int, C.c_int, vp]),
     "mux_rope_table": (C.c_int, [C.c_int, P(f32)]),
-    "mux_gemm_bf16": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp]),
+    "mux_gemm_bf16": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp]),
+    "mux_weight_tile": (C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp]),
+    "mux_weight_tiled_bytes": (i64, [C.c_int, C.c_int]),
+    "mux_unit_set_option": (C.c_int, [vp, C.c_char_p, i64]),
+    "mux_debug_gemm_timing": (None, [vp]),
     "mux_unit_create": (C.c_int, [P(UnitConfig), P(vp)]),
     "mux_unit_destroy": (None, [vp]),
     "mux_unit_pool": (vp, [vp]),

@@ -505,24 +505,57 @@ int mux_rope_table(int positions, float* out) {
   });
 }
 
-int mux_gemm_bf16(const void* x, const void* w, int M, int N, int K, void* out, int epilogue, int splits,
+void mux_debug_gemm_timing(void* buf) { mux::gemm_debug_timing(buf); }
+
+int64_t mux_weight_tiled_bytes(int N, int K) { return static_cast<int64_t>(mux::weight_tiled_bytes(N, K)); }
+
+int mux_weight_tile(const void* w, int N, int K, void* out, int inverse, void* stream) {
+  return guarded([&] {
+    require(N > 0 && K > 0 && K % 8 == 0, "weight_tile: bad shape");
+    mux::check_cuda(mux::weight_tile(w, N, K, out, inverse != 0, static_cast<cudaStream_t>(stream)), "weight_tile");
+  });
+}
+
+int mux_gemm_bf16(const void* x, const void* w, int w_tiled, int M, int N, int K, void* out, int epilogue, int grid,
                   void* stream) {
   return guarded([&] {
-    require(M > 0 && N > 0 && K > 0 && K % 8 == 0, "gemm: bad shape");
-    alignas(64) unsigned char tw[128], tx[128];
-    int n_tile = std::max(16, std::min(256, ((M + 15) / 16) * 16));
-    if (!mux::make_tmap_bf16(tw, w, N, K, static_cast<uint64_t>(K) * 2, 128) ||
+    require(M > 0 && N > 0 && K > 0 && K % 8 == 0 && N % 8 == 0, "gemm: bad shape");
+    require(epilogue >= 0 && epilogue <= 3, "gemm: bad epilogue");
+    require(epilogue != 2 || N % 16 == 0, "gemm: SiLU epilogue needs N % 16 == 0");
+    // Process-wide stream-K scratch for direct calls (tests); the runtime
+    // gives every partition its own.
+    static float* partials = nullptr;
+    static int* flags = nullptr;
+    static int epoch = 0;
+    constexpr int kMaxGrid = 1024;
+    if (partials == nullptr) {
+      mux::check_cuda(cudaMalloc(&partials, mux::gemm_partials_floats(kMaxGrid) * 4), "gemm scratch");
+      mux::check_cuda(cudaMalloc(&flags, kMaxGrid * 4), "gemm flags");
+      mux::check_cuda(cudaMemset(flags, 0, kMaxGrid * 4), "gemm flags");
+    }
+    int sms = 148;
+    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    alignas(64) unsigned char tw[128], tx[128], to[128];
+    const int n_tile = mux::gemm_pick_n_tile(M);
+    if ((!w_tiled && !mux::make_tmap_bf16(tw, w, N, K, static_cast<uint64_t>(K) * 2, 128)) ||
         !mux::make_tmap_bf16(tx, x, M, K, static_cast<uint64_t>(K) * 2, n_tile))
       throw std::runtime_error("gemm: tensor map encode failed");
+    const int ldo = epilogue == 2 ? N / 2 : N;
+    if (!mux::make_tmap_gemm_out(to, out, epilogue, M, N, ldo)) throw std::runtime_error("gemm: out map encode failed");
     mux::GemmArgs g{};
-    g.tmap_w = tw;
+    g.tmap_out = to;
+    g.w_tiled = w_tiled ? w : nullptr;
+    g.tmap_w = w_tiled ? nullptr : tw;
     g.tmap_x = tx;
     g.out = out;
+    g.partials = partials;
+    g.flags = flags;
+    g.epoch = ++epoch;
+    g.grid = std::min(kMaxGrid, grid > 0 ? grid : sms);
     g.M = M;
     g.N = N;
     g.K = K;
-    g.ldo = epilogue == 2 ? N / 2 : N;
-    g.splits = splits;
+    g.ldo = ldo;
     g.epi = static_cast<mux::Epilogue>(epilogue);
     mux::check_cuda(mux::gemm_bf16_tn(g, static_cast<cudaStream_t>(stream)), "gemm");
   });
@@ -574,7 +607,7 @@ int mux_unit_create(const mux_unit_config* cfg, mux_unit** out) {
       u->streams.push_back(s);
       const int max_tok = std::max(u->max_prefill, u->max_batch);
       u->ws.push_back(std::make_unique<mux::Workspace>(max_tok, std::max(u->max_batch, 256), hid, qkv, ffn, vocab,
-                                                       heads, 16, u->max_batch));
+                                                       heads, u->max_batch, u->rt->num_sms()));
     }
     for (auto& e : u->ev) mux::check_cuda(cudaEventCreate(&e), "event");
     mux::check_cuda(cudaDeviceSynchronize(), "unit create");
@@ -693,6 +726,14 @@ int mux_unit_attn_time(mux_unit* u, double* total_ms, int64_t* launches, double*
 }
 
 int64_t mux_unit_launches(mux_unit* u) { return u ? u->rt->launches() : -1; }
+
+int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
+  return guarded([&] {
+    const std::string k = key ? key : "";
+    if (k == "gemm_min_iters") u->rt->set_gemm_min_iters(static_cast<int>(value));
+    else throw std::invalid_argument("unknown option: " + k);
+  });
+}
 
 int mux_unit_run_lockstep(mux_unit* u, const mux_sim_config* cfg, int n_entries, const mux_llm_entry* entries,
                           int n_requests, const mux_request* trace, uint64_t prompt_seed, mux_record* records_out,

@@ -43,7 +43,7 @@ PinnedMem::~PinnedMem() {
 
 namespace {
 
-constexpr int kEpiStoreBf16 = 0, kEpiPartial = 1, kEpiSilu = 2, kEpiStoreF32 = 3;
+constexpr int kEpiStoreBf16 = 0, kEpiResidual = 1, kEpiSilu = 2, kEpiStoreF32 = 3;
 
 __global__ void gather_last_tok(const int32_t* last_tok, const int32_t* slots, int32_t* tokens, int n) {
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
@@ -68,47 +68,29 @@ Llama::Llama(const ModelDims& d, int max_slots, int max_rows, int64_t max_rowrec
     : d_(d), max_slots_(max_slots), max_rows_(max_rows), max_rowrecs_(max_rowrecs) {
   if (d.head_dim != 128) throw std::invalid_argument("llama: head_dim must be 128");
   if (d.hidden % 64 != 0 || d.ffn % 64 != 0) throw std::invalid_argument("llama: hidden/ffn must be multiples of 64");
-  const size_t hid = d.hidden, ffn = d.ffn, V = d.vocab, qkv = 3ull * d.heads * 128, att = 1ull * d.heads * 128;
-  embed = DevMem(V * hid * 2);
-  lm_head = DevMem(V * hid * 2);
-  final_norm = DevMem(hid * 4);
+  const int hid = d.hidden, ffn = d.ffn, V = d.vocab, qkv = 3 * d.heads * 128, att = d.heads * 128;
+  embed = DevMem(static_cast<size_t>(V) * hid * 2);  // row-major: gathered by token id
+  lm_head = DevMem(weight_tiled_bytes(V, hid));
+  final_norm = DevMem(static_cast<size_t>(hid) * 4);
   for (int l = 0; l < d.layers; ++l) {
-    wqkv.emplace_back(qkv * hid * 2);
-    wo.emplace_back(hid * att * 2);
-    wgu.emplace_back(2 * ffn * hid * 2);
-    wdown.emplace_back(hid * ffn * 2);
-    attn_norm.emplace_back(hid * 4);
-    ffn_norm.emplace_back(hid * 4);
+    wqkv.emplace_back(weight_tiled_bytes(qkv, hid));
+    wo.emplace_back(weight_tiled_bytes(hid, att));
+    wgu.emplace_back(weight_tiled_bytes(2 * ffn, hid));
+    wdown.emplace_back(weight_tiled_bytes(hid, ffn));
+    attn_norm.emplace_back(static_cast<size_t>(hid) * 4);
+    ffn_norm.emplace_back(static_cast<size_t>(hid) * 4);
   }
   rowrec = DevMem(static_cast<size_t>(max_rowrecs) * row_width() * 4);
   rowlist = DevMem(static_cast<size_t>(max_slots) * max_rows * 4);
   last_tok = DevMem(static_cast<size_t>(max_slots) * 4);
   check_cuda(cudaMemset(rowlist.p, 0, rowlist.bytes), "memset rowlist");
   check_cuda(cudaMemset(last_tok.p, 0, last_tok.bytes), "memset last_tok");
-  build_tmaps();
 }
 
 int64_t Llama::weight_bytes() const {
   int64_t t = embed.bytes + lm_head.bytes;
   for (int l = 0; l < d_.layers; ++l) t += wqkv[l].bytes + wo[l].bytes + wgu[l].bytes + wdown[l].bytes;
   return t;
-}
-
-void Llama::build_tmaps() {
-  const int hid = d_.hidden, ffn = d_.ffn, att = d_.heads * 128;
-  tm_qkv.resize(d_.layers);
-  tm_o.resize(d_.layers);
-  tm_gu.resize(d_.layers);
-  tm_down.resize(d_.layers);
-  for (int l = 0; l < d_.layers; ++l) {
-    bool ok = make_tmap_bf16(tm_qkv[l].raw, wqkv[l].p, qkv_cols(), hid, hid * 2ull, 128) &&
-              make_tmap_bf16(tm_o[l].raw, wo[l].p, hid, att, att * 2ull, 128) &&
-              make_tmap_bf16(tm_gu[l].raw, wgu[l].p, 2ull * ffn, hid, hid * 2ull, 128) &&
-              make_tmap_bf16(tm_down[l].raw, wdown[l].p, hid, ffn, ffn * 2ull, 128);
-    if (!ok) throw std::runtime_error("llama: tensor map encode failed");
-  }
-  if (!make_tmap_bf16(tm_lm.raw, lm_head.p, d_.vocab, hid, hid * 2ull, 128))
-    throw std::runtime_error("llama: tensor map encode failed (lm_head)");
 }
 
 void Llama::init_random(uint64_t seed, float std, cudaStream_t s) {
@@ -128,38 +110,58 @@ void Llama::init_random(uint64_t seed, float std, cudaStream_t s) {
   }
 }
 
-DevMem* Llama::tensor(const std::string& name, int layer, size_t* bytes) {
-  DevMem* m = nullptr;
+DevMem* Llama::tensor(const std::string& name, int layer, int* rows, int* cols, bool* tiled) {
+  const int hid = d_.hidden, ffn = d_.ffn, att = d_.heads * 128;
   auto per_layer = [&](std::vector<DevMem>& v) -> DevMem* {
     return layer >= 0 && layer < d_.layers ? &v[layer] : nullptr;
   };
-  if (name == "embed") m = &embed;
-  else if (name == "lm_head") m = &lm_head;
-  else if (name == "final_norm") m = &final_norm;
-  else if (name == "wqkv") m = per_layer(wqkv);
-  else if (name == "wo") m = per_layer(wo);
-  else if (name == "wgu") m = per_layer(wgu);
-  else if (name == "wdown") m = per_layer(wdown);
-  else if (name == "attn_norm") m = per_layer(attn_norm);
-  else if (name == "ffn_norm") m = per_layer(ffn_norm);
-  if (m && bytes) *bytes = m->bytes;
-  return m;
+  struct Shape { DevMem* m; int r, c; bool t; };
+  Shape sh{nullptr, 0, 0, false};
+  if (name == "embed") sh = {&embed, d_.vocab, hid, false};
+  else if (name == "lm_head") sh = {&lm_head, d_.vocab, hid, true};
+  else if (name == "final_norm") sh = {&final_norm, 1, hid * 2, false};
+  else if (name == "wqkv") sh = {per_layer(wqkv), qkv_cols(), hid, true};
+  else if (name == "wo") sh = {per_layer(wo), hid, att, true};
+  else if (name == "wgu") sh = {per_layer(wgu), 2 * ffn, hid, true};
+  else if (name == "wdown") sh = {per_layer(wdown), hid, ffn, true};
+  else if (name == "attn_norm") sh = {per_layer(attn_norm), 1, hid * 2, false};
+  else if (name == "ffn_norm") sh = {per_layer(ffn_norm), 1, hid * 2, false};
+  *rows = sh.r;
+  *cols = sh.c;  // in bf16 units (fp32 norms count as 2)
+  *tiled = sh.t;
+  return sh.m;
 }
 
 bool Llama::set_tensor(const std::string& name, int layer, const void* host, size_t bytes, cudaStream_t s) {
-  size_t want = 0;
-  DevMem* m = tensor(name, layer, &want);
-  if (!m || want != bytes) return false;
-  check_cuda(cudaMemcpyAsync(m->p, host, bytes, cudaMemcpyHostToDevice, s), "set_tensor");
+  int rows = 0, cols = 0;
+  bool tiled = false;
+  DevMem* m = tensor(name, layer, &rows, &cols, &tiled);
+  if (!m || static_cast<size_t>(rows) * cols * 2 != bytes) return false;
+  if (!tiled) {
+    check_cuda(cudaMemcpyAsync(m->p, host, bytes, cudaMemcpyHostToDevice, s), "set_tensor");
+  } else {
+    DevMem tmp(bytes);
+    check_cuda(cudaMemcpyAsync(tmp.p, host, bytes, cudaMemcpyHostToDevice, s), "set_tensor");
+    check_cuda(weight_tile(tmp.p, rows, cols, m->p, false, s), "weight_tile");
+    check_cuda(cudaStreamSynchronize(s), "set_tensor sync");
+  }
   check_cuda(cudaStreamSynchronize(s), "set_tensor sync");
   return true;
 }
 
 bool Llama::get_tensor(const std::string& name, int layer, void* host, size_t bytes, cudaStream_t s) const {
-  size_t want = 0;
-  DevMem* m = const_cast<Llama*>(this)->tensor(name, layer, &want);
-  if (!m || want != bytes) return false;
-  check_cuda(cudaMemcpyAsync(host, m->p, bytes, cudaMemcpyDeviceToHost, s), "get_tensor");
+  int rows = 0, cols = 0;
+  bool tiled = false;
+  DevMem* m = const_cast<Llama*>(this)->tensor(name, layer, &rows, &cols, &tiled);
+  if (!m || static_cast<size_t>(rows) * cols * 2 != bytes) return false;
+  if (!tiled) {
+    check_cuda(cudaMemcpyAsync(host, m->p, bytes, cudaMemcpyDeviceToHost, s), "get_tensor");
+  } else {
+    DevMem tmp(bytes);
+    check_cuda(weight_tile(m->p, rows, cols, tmp.p, true, s), "weight_untile");
+    check_cuda(cudaMemcpyAsync(host, tmp.p, bytes, cudaMemcpyDeviceToHost, s), "get_tensor");
+    check_cuda(cudaStreamSynchronize(s), "get_tensor sync");
+  }
   check_cuda(cudaStreamSynchronize(s), "get_tensor sync");
   return true;
 }
@@ -167,11 +169,10 @@ bool Llama::get_tensor(const std::string& name, int layer, void* host, size_t by
 // -------------------------------------------------------------- Workspace
 
 Workspace::Workspace(int max_tok, int max_batch_rows, int hidden, int qkv_cols, int ffn, int vocab,
-                     int heads, int max_splits, int max_decode_batch)
+                     int heads, int max_decode_batch, int grid)
     : max_tokens(max_tok), max_hidden(hidden), max_qkv(qkv_cols), max_ffn(ffn), max_vocab(vocab),
       max_heads(heads) {
   const size_t T = std::max(max_tok, 16);
-  max_part_rows = static_cast<int>(std::max<size_t>(T, static_cast<size_t>(max_splits) * max_decode_batch));
   // Activation buffers get >= 256 rows so any n_tile box stays in bounds.
   const size_t Tp = std::max<size_t>(T, 256);
   resid = DevMem(Tp * hidden * 4);
@@ -180,7 +181,9 @@ Workspace::Workspace(int max_tok, int max_batch_rows, int hidden, int qkv_cols, 
   q = DevMem(Tp * heads * 128 * 2);
   attn = DevMem(Tp * heads * 128 * 2);
   act = DevMem(Tp * ffn * 2);
-  parts = DevMem(static_cast<size_t>(max_part_rows) * hidden * 4);
+  gemm_partials = DevMem(gemm_partials_floats(grid) * 4);
+  gemm_flags = DevMem(static_cast<size_t>(std::max(grid, 1024)) * 4);
+  check_cuda(cudaMemset(gemm_flags.p, 0, gemm_flags.bytes), "memset flags");
   const size_t rows_out = std::max<size_t>(max_batch_rows, 256);
   logits = DevMem(rows_out * vocab * 4);
   xlast = DevMem(rows_out * hidden * 2);
@@ -298,31 +301,42 @@ const void* Runtime::act_tmap(const void* base, int rows, int cols, int box_rows
   return ins.first->second.data();
 }
 
-int Runtime::pick_splits(int tiles, int kb_total) const {
-  if (tiles >= num_sms_) return 1;
-  int s = (num_sms_ + tiles - 1) / tiles;
-  s = std::min(s, std::max(1, kb_total / 4));
-  return std::max(1, std::min(s, 16));
-}
-
-void Runtime::gemm(const void* tmap_w, const void* x, int M, int N, int K, void* out, int ldo, int epi,
-                   int splits, cudaStream_t stream) {
+void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void* out, int ldo, int epi,
+                   Workspace& ws, cudaStream_t stream) {
   // The X map is viewed over max(M, 256) rows: buffers are sized for it and
   // rows past M are never stored.
   const int rows = std::max(M, 256);
   const void* tx = act_tmap(x, rows, K, gemm_n_tile(M));
+  const void* to = out_tmap(out, epi, M, N, ldo);
   GemmArgs g{};
-  g.tmap_w = tmap_w;
+  g.w_tiled = w_tiled;
   g.tmap_x = tx;
+  g.tmap_out = to;
   g.out = out;
+  g.partials = ws.gemm_partials.as<float>();
+  g.flags = ws.gemm_flags.as<int>();
+  g.epoch = ++ws.gemm_epoch;
+  g.grid = num_sms_;
+  g.min_iters = gemm_min_iters_;
   g.M = M;
   g.N = N;
   g.K = K;
   g.ldo = ldo;
-  g.splits = splits;
   g.epi = static_cast<Epilogue>(epi);
   check_cuda(gemm_bf16_tn(g, stream), "gemm");
   launches_ += 1;
+}
+
+const void* Runtime::out_tmap(const void* out, int epi, int M, int N, int ldo) {
+  auto key = std::make_tuple(out, M, N * 8 + epi, ldo);
+  auto it = out_tmaps_.find(key);
+  if (it != out_tmaps_.end()) return it->second.data();
+  std::vector<unsigned char> raw(128 + 64);
+  unsigned char* aligned = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(raw.data()) + 63) & ~uintptr_t(63));
+  if (!make_tmap_gemm_out(aligned, out, epi, M, N, ldo)) throw std::runtime_error("out tensor map encode failed");
+  auto ins = out_tmaps_.emplace(key, std::vector<unsigned char>(aligned, aligned + 128));
+  return ins.first->second.data();
 }
 
 void Runtime::upload_rows(muxsim::BlockPool& bp, int llm, Llama& m, cudaStream_t stream) {
@@ -399,10 +413,6 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   check_cuda(embed_rmsnorm(m.embed.p, ws.tokens, m.attn_norm[0].as<float>(), ws.resid.as<float>(), ws.xn.p,
                            n, hid, d.norm_eps, stream), "embed");
   launches_ += 1;
-  const int kb_att = (H * 128 + 63) / 64, kb_ffn = (d.ffn + 63) / 64;
-  const int tiles_hid = (hid + 127) / 128;
-  const int split_o = pick_splits(tiles_hid, kb_att);
-  const int split_d = pick_splits(tiles_hid, kb_ffn);
   DecodeAttnArgs at{};
   at.q = ws.q.p;
   at.pool = pool_.p;
@@ -448,7 +458,7 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   ap.rope_positions = max_pos_;
 
   for (int l = 0; l < L; ++l) {
-    gemm(m.tm_qkv[l].raw, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, 1, stream);
+    gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
     ap.layer = l;
     check_cuda(kv_append(ap, stream), "kv_append");
     launches_ += 1;
@@ -466,18 +476,17 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
       timer->pending.emplace_back(e0, e1);
       timer->pending_bytes += attn_bytes;
     }
-    gemm(m.tm_o[l].raw, ws.attn.p, n, hid, H * 128, ws.parts.p, hid, kEpiPartial, split_o, stream);
-    check_cuda(reduce_residual_rmsnorm(ws.parts.as<float>(), split_o, ws.resid.as<float>(),
-                                       m.ffn_norm[l].as<float>(), ws.xn.p, n, hid, d.norm_eps, stream), "reduce");
+    gemm(m.wo[l].p, ws.attn.p, n, hid, H * 128, ws.resid.p, hid, kEpiResidual, ws, stream);
+    check_cuda(rmsnorm_rows(ws.resid.as<float>(), m.ffn_norm[l].as<float>(), ws.xn.p, n, hid, d.norm_eps, stream),
+               "rmsnorm");
     launches_ += 1;
-    gemm(m.tm_gu[l].raw, ws.xn.p, n, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, 1, stream);
-    gemm(m.tm_down[l].raw, ws.act.p, n, hid, d.ffn, ws.parts.p, hid, kEpiPartial, split_d, stream);
+    gemm(m.wgu[l].p, ws.xn.p, n, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, ws, stream);
+    gemm(m.wdown[l].p, ws.act.p, n, hid, d.ffn, ws.resid.p, hid, kEpiResidual, ws, stream);
     const float* next_norm = l + 1 < L ? m.attn_norm[l + 1].as<float>() : m.final_norm.as<float>();
-    check_cuda(reduce_residual_rmsnorm(ws.parts.as<float>(), split_d, ws.resid.as<float>(), next_norm,
-                                       ws.xn.p, n, hid, d.norm_eps, stream), "reduce");
+    check_cuda(rmsnorm_rows(ws.resid.as<float>(), next_norm, ws.xn.p, n, hid, d.norm_eps, stream), "rmsnorm");
     launches_ += 1;
   }
-  gemm(m.tm_lm.raw, ws.xn.p, n, d.vocab, hid, ws.logits.p, d.vocab, kEpiStoreF32, 1, stream);
+  gemm(m.lm_head.p, ws.xn.p, n, d.vocab, hid, ws.logits.p, d.vocab, kEpiStoreF32, ws, stream);
   check_cuda(argmax_rows(ws.logits.as<float>(), n, d.vocab, ws.out_tok, stream), "argmax");
   scatter_last_tok<<<(n + 127) / 128, 128, 0, stream>>>(m.last_tok.as<int32_t>(), ws.slots, ws.out_tok, n);
   launches_ += 2;
@@ -512,10 +521,6 @@ void Runtime::prefill(Llama& m, Workspace& ws, int n, const int32_t* slots_host,
   check_cuda(embed_rmsnorm(m.embed.p, ws.tokens, m.attn_norm[0].as<float>(), ws.resid.as<float>(), ws.xn.p,
                            T, hid, d.norm_eps, stream), "embed");
   launches_ += 1;
-  const int kb_att = (H * 128 + 63) / 64, kb_ffn = (d.ffn + 63) / 64;
-  const int tiles_hid = ((hid + 127) / 128) * ((T + 255) / 256);
-  const int split_o = std::min(pick_splits(tiles_hid, kb_att), std::max(1, ws.max_part_rows / T));
-  const int split_d = std::min(pick_splits(tiles_hid, kb_ffn), std::max(1, ws.max_part_rows / T));
   AppendArgs ap{};
   ap.qkv = ws.qkv.p;
   ap.q_out = ws.q.p;
@@ -540,26 +545,25 @@ void Runtime::prefill(Llama& m, Workspace& ws, int n, const int32_t* slots_host,
   pa.T = T;
   pa.scale_log2 = 1.4426950408889634f / std::sqrt(128.f);
   for (int l = 0; l < L; ++l) {
-    gemm(m.tm_qkv[l].raw, ws.xn.p, T, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, 1, stream);
+    gemm(m.wqkv[l].p, ws.xn.p, T, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
     ap.layer = l;
     check_cuda(kv_append(ap, stream), "kv_append");
     launches_ += 1;
     check_cuda(prefill_attention(pa, stream), "prefill_attention");
     launches_ += 1;
-    gemm(m.tm_o[l].raw, ws.attn.p, T, hid, H * 128, ws.parts.p, hid, kEpiPartial, split_o, stream);
-    check_cuda(reduce_residual_rmsnorm(ws.parts.as<float>(), split_o, ws.resid.as<float>(),
-                                       m.ffn_norm[l].as<float>(), ws.xn.p, T, hid, d.norm_eps, stream), "reduce");
+    gemm(m.wo[l].p, ws.attn.p, T, hid, H * 128, ws.resid.p, hid, kEpiResidual, ws, stream);
+    check_cuda(rmsnorm_rows(ws.resid.as<float>(), m.ffn_norm[l].as<float>(), ws.xn.p, T, hid, d.norm_eps, stream),
+               "rmsnorm");
     launches_ += 1;
-    gemm(m.tm_gu[l].raw, ws.xn.p, T, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, 1, stream);
-    gemm(m.tm_down[l].raw, ws.act.p, T, hid, d.ffn, ws.parts.p, hid, kEpiPartial, split_d, stream);
+    gemm(m.wgu[l].p, ws.xn.p, T, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, ws, stream);
+    gemm(m.wdown[l].p, ws.act.p, T, hid, d.ffn, ws.resid.p, hid, kEpiResidual, ws, stream);
     const float* next_norm = l + 1 < L ? m.attn_norm[l + 1].as<float>() : m.final_norm.as<float>();
-    check_cuda(reduce_residual_rmsnorm(ws.parts.as<float>(), split_d, ws.resid.as<float>(), next_norm,
-                                       ws.xn.p, T, hid, d.norm_eps, stream), "reduce");
+    check_cuda(rmsnorm_rows(ws.resid.as<float>(), next_norm, ws.xn.p, T, hid, d.norm_eps, stream), "rmsnorm");
     launches_ += 1;
   }
   check_cuda(gather_rows_bf16(ws.xn.p, ws.last_rows, ws.xlast.p, n, hid, stream), "gather");
   launches_ += 1;
-  gemm(m.tm_lm.raw, ws.xlast.p, n, d.vocab, hid, ws.logits.p, d.vocab, kEpiStoreF32, 1, stream);
+  gemm(m.lm_head.p, ws.xlast.p, n, d.vocab, hid, ws.logits.p, d.vocab, kEpiStoreF32, ws, stream);
   check_cuda(argmax_rows(ws.logits.as<float>(), n, d.vocab, ws.out_tok, stream), "argmax");
   scatter_last_tok<<<(n + 127) / 128, 128, 0, stream>>>(m.last_tok.as<int32_t>(), ws.slots, ws.out_tok, n);
   launches_ += 2;

@@ -74,18 +74,16 @@ class Llama {
   DevMem embed, lm_head, final_norm;                 // final_norm fp32
   std::vector<DevMem> wqkv, wo, wgu, wdown;          // per layer
   std::vector<DevMem> attn_norm, ffn_norm;           // fp32
-  // tensor maps (CUtensorMap, 128 bytes each), box = 128 W rows
-  struct TMap { alignas(64) unsigned char raw[128]; };
-  std::vector<TMap> tm_qkv, tm_o, tm_gu, tm_down;
-  TMap tm_lm;
+  // GEMM weights (lm_head, wqkv, wo, wgu, wdown) live in the B200 tiled
+  // layout of weight_tile(): contiguous pre-swizzled 16 KiB UMMA tiles.
   // device block tables
   DevMem rowrec;    // [max_rowrecs][row_width] int32
   DevMem rowlist;   // [max_slots][max_rows] int32
   DevMem last_tok;  // [max_slots] int32: most recent token of each slot
 
  private:
-  void build_tmaps();
-  DevMem* tensor(const std::string& name, int layer, size_t* bytes);
+  // (rows, cols) of a named tensor; tiled = stored in the GEMM tile layout.
+  DevMem* tensor(const std::string& name, int layer, int* rows, int* cols, bool* tiled);
   ModelDims d_;
   int max_slots_, max_rows_;
   int64_t max_rowrecs_;
@@ -95,8 +93,9 @@ class Llama {
 struct Workspace {
   int max_tokens = 0;    // prefill token budget or max decode batch
   int max_hidden = 0, max_qkv = 0, max_ffn = 0, max_vocab = 0, max_heads = 0;
-  int max_part_rows = 0; // splits * tokens for split-K partials
-  DevMem resid, xn, qkv, q, attn, act, parts, logits, ints, attn_part_o, attn_part_ml, xlast;
+  DevMem resid, xn, qkv, q, attn, act, logits, ints, attn_part_o, attn_part_ml, xlast;
+  DevMem gemm_partials, gemm_flags;  // stream-K fixup scratch of this partition's GEMMs
+  int gemm_epoch = 0;
   PinnedMem host_ints[2];  // double-buffered staging for per-job metadata
   cudaEvent_t staged[2] = {nullptr, nullptr};
   int cur = 0;
@@ -108,7 +107,7 @@ struct Workspace {
   // int32 views into `ints`
   int32_t *tokens, *slots, *ctx, *tok_slot, *tok_pos, *seq_start, *out_tok, *last_rows;
   Workspace(int max_tokens, int max_batch_rows, int hidden, int qkv, int ffn, int vocab, int heads,
-            int max_splits, int max_decode_batch);
+            int max_decode_batch, int grid);
 };
 
 // Per-launch K1 timing: an event pair around every decode-attention launch.
@@ -135,10 +134,13 @@ class Runtime {
   int rope_positions() const { return max_pos_; }
   int num_sms() const { return num_sms_; }
   int64_t launches() const { return launches_; }
+  void set_gemm_min_iters(int v) { gemm_min_iters_ = v; }
   void count_launch(int64_t n = 1) { launches_ += n; }
 
   // Cached tensor map for an activation buffer viewed as rows x cols bf16.
   const void* act_tmap(const void* base, int rows, int cols, int box_rows);
+  // Cached store map of a GEMM output (exact M rows: TMA clips the tail).
+  const void* out_tmap(const void* out, int epi, int M, int N, int ldo);
 
   // Block-table maintenance: copy pending rows of `llm` (host pool) to the
   // model's device tables on `stream` (through pinned staging).
@@ -152,9 +154,8 @@ class Runtime {
                const int32_t* tokens_host, int32_t* out_host /*nullable*/, cudaStream_t stream);
 
   // Decode-forward building blocks, exposed for tests/bench.
-  int pick_splits(int tiles, int kb_total) const;
-  void gemm(const void* tmap_w, const void* x, int M, int N, int K, void* out, int ldo, int epi,
-            int splits, cudaStream_t stream);
+  void gemm(const void* w_tiled, const void* x, int M, int N, int K, void* out, int ldo, int epi,
+            Workspace& ws, cudaStream_t stream);
 
  private:
   int device_;
@@ -162,6 +163,7 @@ class Runtime {
   int64_t pool_blocks_;
   int max_pos_;
   int64_t launches_ = 0;
+  int gemm_min_iters_ = 24;
   DevMem pool_;
   DevMem rope_;
   struct StageSlot {
@@ -173,6 +175,7 @@ class Runtime {
   StageSlot ring_[4];
   int ring_next_ = 0;
   std::map<std::tuple<const void*, int, int, int>, std::vector<unsigned char>> tmaps_;
+  std::map<std::tuple<const void*, int, int, int>, std::vector<unsigned char>> out_tmaps_;
 };
 
 void check_cuda(cudaError_t e, const char* what);

@@ -51,20 +51,34 @@ __global__ void __launch_bounds__(kRowThreads) embed_rmsnorm_kernel(
   rmsnorm_row(x, norm_w, xn + static_cast<int64_t>(t) * hidden, hidden, eps, scratch);
 }
 
-__global__ void __launch_bounds__(kRowThreads) reduce_residual_rmsnorm_kernel(
-    const float* parts, int splits, int T, float* resid, const float* norm_w, __nv_bfloat16* xn,
-    int hidden, float eps) {
+// One CTA per row, float4 loads kept in registers between the two passes.
+template <int kVec>
+__global__ void __launch_bounds__(kRowThreads) rmsnorm_rows_kernel(const float* resid, const float* norm_w,
+                                                                   __nv_bfloat16* xn, int hidden, float eps) {
   __shared__ float scratch[32];
   const int t = blockIdx.x;
-  float* x = resid + static_cast<int64_t>(t) * hidden;
-  const int64_t plane = static_cast<int64_t>(T) * hidden;
-  for (int i = threadIdx.x; i < hidden; i += blockDim.x) {
-    float acc = x[i];
-    for (int s = 0; s < splits; ++s) acc += parts[s * plane + static_cast<int64_t>(t) * hidden + i];
-    x[i] = acc;
+  const float4* x = reinterpret_cast<const float4*>(resid + static_cast<int64_t>(t) * hidden);
+  const float4* w = reinterpret_cast<const float4*>(norm_w);
+  const int n4 = hidden / 4;
+  float4 v[kVec];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kVec; ++k) {
+    const int i = threadIdx.x + k * kRowThreads;
+    v[k] = i < n4 ? x[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+    ss = fmaf(v[k].x, v[k].x, fmaf(v[k].y, v[k].y, fmaf(v[k].z, v[k].z, fmaf(v[k].w, v[k].w, ss))));
   }
-  __syncthreads();
-  if (xn != nullptr) rmsnorm_row(x, norm_w, xn + static_cast<int64_t>(t) * hidden, hidden, eps, scratch);
+  const float inv = rsqrtf(block_sum(ss, scratch) / static_cast<float>(hidden) + eps);
+  uint2* y = reinterpret_cast<uint2*>(xn + static_cast<int64_t>(t) * hidden);
+#pragma unroll
+  for (int k = 0; k < kVec; ++k) {
+    const int i = threadIdx.x + k * kRowThreads;
+    if (i < n4) {
+      const float4 g = w[i];
+      y[i] = make_uint2(pack_bf16(v[k].x * inv * g.x, v[k].y * inv * g.y),
+                        pack_bf16(v[k].z * inv * g.z, v[k].w * inv * g.w));
+    }
+  }
 }
 
 __global__ void __launch_bounds__(kRowThreads) argmax_kernel(const float* logits, int V, int32_t* out) {
@@ -72,7 +86,7 @@ __global__ void __launch_bounds__(kRowThreads) argmax_kernel(const float* logits
   __shared__ int si[32];
   const float* row = logits + static_cast<int64_t>(blockIdx.x) * V;
   float best = -INFINITY;
-  int bi = 0x7fffffff;
+  int bi = V;  // sentinel above any index; NaN logits never win
   for (int i = threadIdx.x; i < V; i += blockDim.x) {
     const float v = row[i];
     if (v > best || (v == best && i < bi)) {
@@ -103,7 +117,7 @@ __global__ void __launch_bounds__(kRowThreads) argmax_kernel(const float* logits
         b0 = sv[w];
         i0 = si[w];
       }
-    out[blockIdx.x] = i0;
+    out[blockIdx.x] = i0 < V ? i0 : 0;
   }
 }
 
@@ -218,11 +232,16 @@ cudaError_t embed_rmsnorm(const void* emb, const int32_t* tokens, const float* n
   return cudaGetLastError();
 }
 
-cudaError_t reduce_residual_rmsnorm(const float* parts, int splits, float* resid, const float* norm_w,
-                                    void* xn, int T, int hidden, float eps, cudaStream_t stream) {
+cudaError_t rmsnorm_rows(const float* resid, const float* norm_w, void* xn, int T, int hidden, float eps,
+                         cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  reduce_residual_rmsnorm_kernel<<<T, kRowThreads, 0, stream>>>(
-      parts, splits, T, resid, norm_w, reinterpret_cast<__nv_bfloat16*>(xn), hidden, eps);
+  if (hidden % 4 != 0 || hidden > 4 * kRowThreads * 16) return cudaErrorInvalidValue;
+  __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(xn);
+  const int per = (hidden / 4 + kRowThreads - 1) / kRowThreads;
+  if (per <= 2) rmsnorm_rows_kernel<2><<<T, kRowThreads, 0, stream>>>(resid, norm_w, y, hidden, eps);
+  else if (per <= 4) rmsnorm_rows_kernel<4><<<T, kRowThreads, 0, stream>>>(resid, norm_w, y, hidden, eps);
+  else if (per <= 8) rmsnorm_rows_kernel<8><<<T, kRowThreads, 0, stream>>>(resid, norm_w, y, hidden, eps);
+  else rmsnorm_rows_kernel<16><<<T, kRowThreads, 0, stream>>>(resid, norm_w, y, hidden, eps);
   return cudaGetLastError();
 }
 

@@ -8,20 +8,35 @@
 //   D[M x N] = X[M x K] * W[N x K]^T      (X activations, W nn.Linear weight)
 //
 // Weight-stationary swap-AB tiling: the UMMA "A" operand is a 128-row slice
-// of W and "B" is up to 256 activation rows, so D^T tiles of 128 x n_tile
-// accumulate in TMEM (fp32). A decode batch (M <= 256) therefore reads each
-// weight byte exactly once -- the HBM-bound regime -- and prefill tiles over
-// tokens. Warp roles: warp 0 = TMA producer (elected lane), warp 1 = MMA
-// issuer (elected lane), warp 2 = TMEM allocator, warps 4..7 = epilogue
-// (tcgen05.ld 32 lanes x 32 columns each). K is pipelined through an
-// S-stage shared-memory ring (SWIZZLE_128B boxes, 64 K-elements per stage)
-// with full/empty mbarriers; tcgen05.commit releases stages.
+// of W and "B" up to 256 activation rows, so D^T tiles of 128 x n_tile
+// accumulate in TMEM (fp32). A decode batch (M <= 256) reads each weight byte
+// exactly once -- the HBM-bound regime -- and prefill tiles over tokens.
+//
+// Persistent stream-K: grid = #SMs; the flattened (tile, k-block) iteration
+// space is cut into equal contiguous ranges, one per CTA, so every SM streams
+// the same number of weight bytes regardless of how many 128-row tiles the
+// projection has (no wave quantisation, no split-K planes). A tile cut
+// between CTAs is finished in-kernel: the CTA holding the tile's first
+// k-segment (it reaches that segment last) adds its partners' fp32 partials
+// in a fixed order -- deterministic -- and applies the real epilogue;
+// partners publish partials with release/acquire flags tagged by a launch
+// epoch. Every CTA publishes at most one partial and only waits on CTAs of
+// higher index that never wait on it, so the scheme cannot deadlock even
+// when the grid is not fully co-resident.
+//
+// Warp roles: warp 0 = TMA producer, warp 1 = MMA issuer (one elected lane),
+// warp 2 = TMEM allocator, warps 4..7 = epilogue. Accumulators are double
+// buffered in TMEM so the epilogue of one segment overlaps the MMAs of the
+// next; operands flow through an S-stage shared-memory ring (SWIZZLE_128B
+// boxes, 64 K-elements per stage, full/empty mbarriers, tcgen05.commit frees
+// a stage).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 #include <cstdint>
+#include <algorithm>
 #include <cstring>
 #include <mutex>
 
@@ -31,52 +46,101 @@
 namespace mux {
 namespace {
 
-constexpr int kBM = 128;          // W rows per CTA (UMMA M)
-constexpr int kBK = 64;           // K per stage (one 128-byte swizzle atom)
+constexpr int kBM = 128;  // W rows per tile (UMMA M)
+constexpr int kBK = 64;   // K per stage (one 128-byte swizzle atom)
 constexpr int kAStageBytes = kBM * kBK * 2;
 constexpr int kThreads = 256;
-constexpr int kSmemBudget = 200 * 1024;
+constexpr int kEpiThreads = 128;
+constexpr int kChunkBytes = 32 * kBM * 4;  // one epilogue chunk: 32 tokens x 128 fp32
+constexpr int kSmemBudget = 224 * 1024;     // A ring + B ring + 2 staging chunks
 
 struct GemmRun {
+  const uint8_t* w_tiled;  // pre-tiled weights (weight_tile), or null -> TMA map
   void* out;
+  float* partials;  // [grid][n_tile][128] fp32
+  int* flags;       // [grid]
+  int epoch;
   int M, N, K, ldo;
-  int n_tile, stages;
-  int kb_total, kb_per_split;
+  int n_tile, stages_a, stages_b;
+  int kb;           // k-blocks per tile
+  int m_tiles;      // ceil(N / 128)
+  int64_t iters;    // tiles * kb
   int epi;
   uint32_t tmem_cols;
+  unsigned long long* timing;  // debug: [grid][4] globaltimer stamps, or null
 };
+
+__device__ __forceinline__ unsigned long long gtimer() {
+  unsigned long long t;
+  asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+  return t;
+}
+
+__device__ __forceinline__ int64_t range_begin(int64_t iters, int c, int grid) {
+  return iters * c / grid;
+}
+
+__device__ __forceinline__ int ld_acquire(const int* p) {
+  int v;
+  asm volatile("ld.acquire.gpu.global.b32 %0, [%1];" : "=r"(v) : "l"(p) : "memory");
+  return v;
+}
+
+__device__ __forceinline__ void st_release(int* p, int v) {
+  asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
+}
+
+__device__ __forceinline__ void epi_bar() {
+  asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+}
 
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
-               const GemmRun r) {
+               const __grid_constant__ CUtensorMap tout, const GemmRun r) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  // 1024-byte alignment for the swizzled stages.
   uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
-  const int S = r.stages;
+  // Separate rings: weights (A, HBM-streamed) run SA stages deep, the small
+  // L2-resident activation tiles (B) only SB, so more weight bytes are in
+  // flight per SM than a shared ring of the same smem would allow.
+  const int SA = r.stages_a, SB = r.stages_b;
   const int b_stage_bytes = r.n_tile * kBK * 2;
   uint8_t* a_st = base;
-  uint8_t* b_st = base + S * kAStageBytes;
-  uint64_t* full = reinterpret_cast<uint64_t*>(b_st + S * b_stage_bytes);
-  uint64_t* empty = full + S;
-  uint64_t* done = empty + S;
-  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(done + 1);
+  uint8_t* b_st = base + SA * kAStageBytes;
+  uint8_t* stage_out = b_st + SB * b_stage_bytes;  // 2 x 16 KiB epilogue staging
+  uint64_t* full_a = reinterpret_cast<uint64_t*>(stage_out + 2 * kChunkBytes);
+  uint64_t* empty_a = full_a + SA;
+  uint64_t* full_b = empty_a + SA;
+  uint64_t* empty_b = full_b + SB;
+  uint64_t* tm_full = empty_b + SB;  // [2]
+  uint64_t* tm_empty = tm_full + 2;  // [2]
+  uint64_t* pbar = tm_empty + 2;     // fixer's partial prefetch
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pbar + 1);
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int m_blk = blockIdx.x;
-  const int n_blk = blockIdx.y;
-  const int split = blockIdx.z;
-  const int kb0 = split * r.kb_per_split;
-  const int nk = min(r.kb_total, kb0 + r.kb_per_split) - kb0;
+  const int c = blockIdx.x;
+  const int G = gridDim.x;
+  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 16 + 0] = gtimer();
+  const int64_t it0 = range_begin(r.iters, c, G);
+  const int64_t it1 = range_begin(r.iters, c + 1, G);
 
   if (warp == 0 && lane == 0) {
-    prefetch_tmap(&tw);
+    if (r.w_tiled == nullptr) prefetch_tmap(&tw);
     prefetch_tmap(&tx);
-    for (int s = 0; s < S; ++s) {
-      mbar_init(&full[s], 1);
-      mbar_init(&empty[s], 1);
+    prefetch_tmap(&tout);
+    for (int s = 0; s < SA; ++s) {
+      mbar_init(&full_a[s], 1);
+      mbar_init(&empty_a[s], 1);
     }
-    mbar_init(done, 1);
+    for (int s = 0; s < SB; ++s) {
+      mbar_init(&full_b[s], 1);
+      mbar_init(&empty_b[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&tm_full[b], 1);
+      mbar_init(&tm_empty[b], kEpiThreads / 32);
+    }
+    mbar_init(pbar, 1);
     fence_barrier_init();
   }
   if (warp == 2) tmem_alloc_dyn(tmem_slot, r.tmem_cols);
@@ -85,90 +149,225 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
 
-  if (warp == 0) {
+  if (warp == 0 || warp == 3) {
+    // ------------------------------------------------ TMA producers
+    // warp 0 streams the weight tiles, warp 3 the activation tiles.
     if (elect_one()) {
-      const uint64_t pol_w = policy_evict_first();  // weights: streamed once per step
-      const uint64_t pol_x = policy_evict_last();   // activations: re-read by every CTA
-      const uint32_t bytes = kAStageBytes + b_stage_bytes;
-      for (int i = 0; i < nk; ++i) {
-        const int s = i % S;
-        if (i >= S) mbar_wait(&empty[s], ((i / S) - 1) & 1);
-        mbar_arrive_expect_tx(&full[s], bytes);
-        const int kc = (kb0 + i) * kBK;
-        tma_load_2d(a_st + s * kAStageBytes, &tw, &full[s], kc, m_blk * kBM, pol_w);
-        tma_load_2d(b_st + s * b_stage_bytes, &tx, &full[s], kc, n_blk * r.n_tile, pol_x);
+      const bool is_a = warp == 0;
+      const uint64_t pol = is_a ? policy_evict_first()   // weights: streamed once per step
+                                : policy_evict_last();   // activations: re-read by every CTA
+      const int SS = is_a ? SA : SB;
+      uint64_t* fb = is_a ? full_a : full_b;
+      uint64_t* eb = is_a ? empty_a : empty_b;
+      const uint32_t bytes = is_a ? kAStageBytes : b_stage_bytes;
+      int i = 0;
+      for (int64_t it = it0; it < it1; ++it, ++i) {
+        const int64_t t = it / r.kb;
+        const int kbi = static_cast<int>(it - t * r.kb);
+        const int s = i % SS;
+        if (i >= SS) mbar_wait(&eb[s], ((i / SS) - 1) & 1);
+        mbar_arrive_expect_tx(&fb[s], bytes);
+        if (is_a) {
+          const int m = static_cast<int>(t % r.m_tiles);
+          if (r.w_tiled != nullptr) {
+            // one contiguous, pre-swizzled 16 KiB UMMA tile: a single bulk copy
+            const uint8_t* src = r.w_tiled + (static_cast<int64_t>(m) * r.kb + kbi) * kAStageBytes;
+            bulk_g2s_stream(a_st + s * kAStageBytes, src, kAStageBytes, &fb[s], pol);
+          } else {
+            tma_load_2d(a_st + s * kAStageBytes, &tw, &fb[s], kbi * kBK, m * kBM, pol);
+          }
+        } else {
+          const int nt = static_cast<int>(t / r.m_tiles);
+          tma_load_2d(b_st + s * b_stage_bytes, &tx, &fb[s], kbi * kBK, nt * r.n_tile, pol);
+        }
       }
     }
   } else if (warp == 1) {
+    // ------------------------------------------------------ MMA issuer
     const uint32_t idesc = umma_idesc_bf16(kBM, r.n_tile);
-    for (int i = 0; i < nk; ++i) {
-      const int s = i % S;
-      mbar_wait(&full[s], (i / S) & 1);
+    int i = 0, seg = 0;
+    int64_t it = it0;
+    while (it < it1) {
+      const int64_t t = it / r.kb;
+      const int64_t seg_begin = it;
+      const int64_t seg_end = min(it1, (t + 1) * r.kb);
+      const int b = seg & 1;
+      if (seg >= 2) mbar_wait(&tm_empty[b], ((seg >> 1) - 1) & 1);
       tc_fence_after();
-      if (elect_one()) {
-        const uint32_t a_addr = smem_u32(a_st + s * kAStageBytes);
-        const uint32_t b_addr = smem_u32(b_st + s * b_stage_bytes);
+      const uint32_t acc = tmem + static_cast<uint32_t>(b * r.n_tile);
+      for (; it < seg_end; ++it, ++i) {
+        const int sa = i % SA, sb = i % SB;
+        mbar_wait(&full_a[sa], (i / SA) & 1);
+        mbar_wait(&full_b[sb], (i / SB) & 1);
+        tc_fence_after();
+        if (elect_one()) {
+          const uint32_t a_addr = smem_u32(a_st + sa * kAStageBytes);
+          const uint32_t b_addr = smem_u32(b_st + sb * b_stage_bytes);
 #pragma unroll
-        for (int kk = 0; kk < kBK / 16; ++kk) {
-          // Advance along K inside the swizzle atom: 16 bf16 = 32 bytes.
-          umma_bf16(tmem, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32),
-                    idesc, (i | kk) != 0 ? 1u : 0u);
+          for (int kk = 0; kk < kBK / 16; ++kk) {
+            // Advance along K inside the swizzle atom: 16 bf16 = 32 bytes.
+            umma_bf16(acc, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
+                      (it != seg_begin || kk != 0) ? 1u : 0u);
+          }
+          umma_commit(&empty_a[sa]);
+          umma_commit(&empty_b[sb]);
+          if (it == seg_end - 1) umma_commit(&tm_full[b]);
         }
-        umma_commit(&empty[s]);
-        if (i == nk - 1) umma_commit(done);
+        __syncwarp();
       }
-      __syncwarp();
+      ++seg;
     }
-    if (nk <= 0 && elect_one()) mbar_arrive(done);
+    if (r.timing != nullptr && lane == 0) r.timing[c * 16 + 1] = gtimer();
   } else if (warp >= 4) {
+    // ------------------------------------------------------ epilogue
+    // Each chunk (32 tokens of the tile) goes TMEM -> registers -> a 16 KiB
+    // shared staging buffer -> global by asynchronous bulk copies issued by
+    // one leader thread, so no thread ever waits on a global store.
     const int q = warp - 4;  // TMEM lane quarter this warp may access
-    mbar_wait(done, 0);
-    tc_fence_after();
-    const int feat = m_blk * kBM + q * 32 + lane;  // W row = output column
-    const int tok0 = n_blk * r.n_tile;
-    for (int c = 0; c < r.n_tile; c += 32) {
-      float v[32];
-      if (nk > 0) {
-        tmem_ld_32x32b_x32(tmem + (static_cast<uint32_t>(q * 32) << 16) + c, v);
-      } else {
-#pragma unroll
-        for (int j = 0; j < 32; ++j) v[j] = 0.f;
+    const int etid = threadIdx.x - 128;
+    const int fl = q * 32 + lane;  // feature row of this thread inside the tile
+    const bool leader = etid == 0;
+    const bool residual = r.epi == static_cast<int>(Epilogue::kResidualAddF32);
+    int seg = 0, sbuf = 0;
+    uint32_t pphase = 0;
+    int64_t it = it0;
+    while (it < it1) {
+      const int64_t t = it / r.kb;
+      const int64_t tile_lo = t * r.kb, tile_hi = tile_lo + r.kb;
+      const int64_t seg_end = min(it1, tile_hi);
+      // Residual adds need no fixup: every piece reduce-adds into the fp32
+      // residual stream (order of the <= few pieces is not fixed). Other
+      // epilogues are nonlinear or rounding, so pieces are summed first.
+      const bool first = residual || it == tile_lo;
+      const bool last = residual || seg_end == tile_hi;
+      const int b = seg & 1;
+      const int m = static_cast<int>(t % r.m_tiles);
+      const int nt = static_cast<int>(t / r.m_tiles);
+      const int tok0 = nt * r.n_tile;
+      const int nchunk = (r.n_tile + 31) / 32;
+      int n_part = 0;
+      const float* pstage = reinterpret_cast<const float*>(a_st);  // idle A ring at the last segment
+      if (first && !last) {
+        // Fixer (always this CTA's last segment): wait for the partners of
+        // this tile, then bulk-prefetch all their chunks into the A ring.
+        int p_hi = c + 1;
+        while (p_hi < G && range_begin(r.iters, p_hi, G) < tile_hi) ++p_hi;
+        n_part = p_hi - (c + 1);
+        if (leader)
+          for (int p = c + 1; p < p_hi; ++p)
+            while (ld_acquire(r.flags + p) != r.epoch) __nanosleep(32);
       }
-      const int jmax = min(32, min(r.n_tile - c, r.M - (tok0 + c)));
-      if (r.epi == static_cast<int>(Epilogue::kStoreBf16)) {
-        if (feat < r.N) {
-          __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(r.out);
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < jmax) o[static_cast<int64_t>(tok0 + c + j) * r.ldo + feat] = __float2bfloat16_rn(v[j]);
+      mbar_wait(&tm_full[b], (seg >> 1) & 1);
+      tc_fence_after();
+      if (n_part > 0) {
+        // All MMAs of this CTA are complete, so the A ring is idle now.
+        if (leader) {
+          mbar_arrive_expect_tx(pbar, static_cast<uint32_t>(n_part * nchunk * kChunkBytes));
+          for (int pi = 0; pi < n_part; ++pi)
+            for (int k = 0; k < nchunk; ++k)
+              bulk_g2s(a_st + (pi * nchunk + k) * kChunkBytes,
+                       r.partials + (static_cast<int64_t>(c + 1 + pi) * 8 + k) * (kChunkBytes / 4), kChunkBytes, pbar);
         }
-      } else if (r.epi == static_cast<int>(Epilogue::kPartialF32) ||
-                 r.epi == static_cast<int>(Epilogue::kStoreF32)) {
-        if (feat < r.N) {
-          float* o = reinterpret_cast<float*>(r.out) + static_cast<int64_t>(split) * r.M * r.ldo;
-#pragma unroll
-          for (int j = 0; j < 32; ++j)
-            if (j < jmax) o[static_cast<int64_t>(tok0 + c + j) * r.ldo + feat] = v[j];
+        mbar_wait(pbar, pphase);
+        pphase ^= 1;
+      }
+      const uint32_t acc = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * r.n_tile);
+      for (int k = 0; k < nchunk; ++k) {
+        const int cc = k * 32;
+        float v[32];
+        tmem_ld_32x32b_x32(acc + cc, v);
+        if (k == nchunk - 1) {  // accumulators consumed: hand TMEM back
+          tc_fence_before();
+          __syncwarp();
+          if (lane == 0) mbar_arrive(&tm_empty[b]);
         }
-      } else {  // kSiluMulBf16: even row = gate_i, odd row = up_i
-        __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(r.out);
+        for (int pi = 0; pi < n_part; ++pi) {  // partner order = CTA order: deterministic
+          const float* src = pstage + (pi * nchunk + k) * (kChunkBytes / 4) + fl;
 #pragma unroll
-        for (int j = 0; j < 32; ++j) {
-          const float up = __shfl_xor_sync(0xffffffffu, v[j], 1);
-          if ((lane & 1) == 0 && j < jmax && feat < r.N) {
+          for (int j = 0; j < 32; ++j) v[j] += src[j * kBM];
+        }
+        // Staging buffer: wait until the bulk group that last read it is done.
+        if (leader) bulk_wait_read<1>();
+        epi_bar();
+        uint8_t* st = stage_out + sbuf * kChunkBytes;
+        const bool fp32_rows = !first || residual || r.epi == static_cast<int>(Epilogue::kStoreF32);
+        if (fp32_rows) {
+          float* sf = reinterpret_cast<float*>(st);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sf[j * kBM + fl] = v[j];
+        } else if (r.epi == static_cast<int>(Epilogue::kStoreBf16)) {
+          __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(st);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) sh[j * kBM + fl] = __float2bfloat16_rn(v[j]);
+        } else {  // kSiluMulBf16: even row = gate_i, odd row = up_i -> act[:, i]
+          __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(st);
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float up = __shfl_xor_sync(0xffffffffu, v[j], 1);
             const float g = v[j];
-            const float act = g / (1.f + __expf(-g)) * up;
-            o[static_cast<int64_t>(tok0 + c + j) * r.ldo + (feat >> 1)] = __float2bfloat16_rn(act);
+            if ((lane & 1) == 0) sh[j * (kBM / 2) + (fl >> 1)] = __float2bfloat16_rn(g / (1.f + __expf(-g)) * up);
           }
         }
+        fence_async_smem();
+        epi_bar();
+        if (leader) {
+          if (!first) {
+            // partner: publish the whole chunk (fixed slot of this CTA)
+            bulk_s2g(r.partials + (static_cast<int64_t>(c) * 8 + k) * (kChunkBytes / 4), st, kChunkBytes);
+          } else if (residual) {
+            tma_reduce_add_2d(&tout, st, m * kBM, tok0 + cc);  // rows >= M are clipped by TMA
+          } else if (r.epi == static_cast<int>(Epilogue::kSiluMulBf16)) {
+            tma_store_2d(&tout, st, m * (kBM / 2), tok0 + cc);
+          } else {
+            tma_store_2d(&tout, st, m * kBM, tok0 + cc);
+          }
+          bulk_commit();
+        }
+        sbuf ^= 1;
       }
+      if (!first && leader) {  // publish: partial writes complete, then the flag
+        bulk_wait<0>();
+        __threadfence();
+        st_release(r.flags + c, r.epoch);
+      }
+      it = seg_end;
+      ++seg;
     }
+    if (leader) bulk_wait<0>();  // staging smem must outlive its bulk reads
+    if (r.timing != nullptr && threadIdx.x == 128) r.timing[c * 16 + 2] = gtimer();
   }
   tc_fence_before();
   __syncthreads();
+  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 16 + 3] = gtimer();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, r.tmem_cols);
+  }
+}
+
+// Row-major [N][K] bf16 -> [m_tile][k_block][128 rows][128 B] with the
+// 128-byte swizzle applied (16-B chunk c of row r stored at chunk c ^ (r & 7)),
+// i.e. exactly the shared-memory image a SWIZZLE_128B TMA box would produce.
+// Rows / columns past N / K are zero. One thread per 16-byte chunk.
+__global__ void weight_tile_kernel(const uint4* __restrict__ src, uint4* __restrict__ dst, int N, int K,
+                                   int kb, int64_t chunks, bool inverse) {
+  const int64_t stride = static_cast<int64_t>(gridDim.x) * blockDim.x;
+  for (int64_t i = blockIdx.x * static_cast<int64_t>(blockDim.x) + threadIdx.x; i < chunks; i += stride) {
+    const int c = static_cast<int>(i & 7);
+    const int64_t rest = i >> 3;
+    const int r = static_cast<int>(rest & 127);
+    const int64_t tile = rest >> 7;
+    const int kbi = static_cast<int>(tile % kb);
+    const int64_t m = tile / kb;
+    const int64_t row = m * kBM + r;
+    const int64_t col = static_cast<int64_t>(kbi) * kBK + c * 8;
+    const int64_t d = (tile * 128 + r) * 8 + (c ^ (r & 7));
+    const bool in = row < N && col < K;
+    if (!inverse) {
+      dst[d] = in ? src[(row * K + col) / 8] : make_uint4(0, 0, 0, 0);
+    } else if (in) {
+      dst[(row * K + col) / 8] = src[d];
+    }
   }
 }
 
@@ -208,6 +407,29 @@ bool make_tmap_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t co
   return res == CUDA_SUCCESS;
 }
 
+bool make_tmap_2d(void* tmap_out, const void* base, bool fp32, uint64_t rows, uint64_t cols,
+                  uint64_t row_stride_bytes, uint32_t box_rows, uint32_t box_cols) {
+  auto fn = encode_fn();
+  if (fn == nullptr) return false;
+  cuuint64_t dims[2] = {cols, rows};
+  cuuint64_t strides[1] = {row_stride_bytes};
+  cuuint32_t box[2] = {box_cols, box_rows};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult res = fn(reinterpret_cast<CUtensorMap*>(tmap_out),
+                    fp32 ? CU_TENSOR_MAP_DATA_TYPE_FLOAT32 : CU_TENSOR_MAP_DATA_TYPE_BFLOAT16, 2,
+                    const_cast<void*>(base), dims, strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                    CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_NONE, CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return res == CUDA_SUCCESS;
+}
+
+bool make_tmap_gemm_out(void* tmap_out, const void* out, int epi, int M, int N, int ldo) {
+  const bool fp32 = epi == static_cast<int>(Epilogue::kResidualAddF32) || epi == static_cast<int>(Epilogue::kStoreF32);
+  const bool silu = epi == static_cast<int>(Epilogue::kSiluMulBf16);
+  const uint64_t cols = silu ? static_cast<uint64_t>(N / 2) : static_cast<uint64_t>(N);
+  const uint64_t stride = static_cast<uint64_t>(ldo) * (fp32 ? 4 : 2);
+  return make_tmap_2d(tmap_out, out, fp32, static_cast<uint64_t>(M), cols, stride, 32, silu ? kBM / 2 : kBM);
+}
+
 int gemm_pick_n_tile(int M) {
   int n = ((M + 15) / 16) * 16;
   if (n > 256) n = 256;
@@ -215,37 +437,83 @@ int gemm_pick_n_tile(int M) {
   return n;
 }
 
+size_t gemm_partials_floats(int max_grid) { return static_cast<size_t>(max_grid) * 8 * (kChunkBytes / 4); }
+
+size_t weight_tiled_bytes(int N, int K) {
+  return static_cast<size_t>((N + kBM - 1) / kBM) * ((K + kBK - 1) / kBK) * kAStageBytes;
+}
+
+cudaError_t weight_tile(const void* src, int N, int K, void* dst, bool inverse, cudaStream_t stream) {
+  if (K % 8 != 0) return cudaErrorInvalidValue;
+  const int kb = (K + kBK - 1) / kBK;
+  const int64_t chunks = static_cast<int64_t>(weight_tiled_bytes(N, K)) / 16;
+  const int blocks = static_cast<int>(std::min<int64_t>((chunks + 255) / 256, 148 * 16));
+  if (!inverse)
+    weight_tile_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const uint4*>(src),
+                                                   reinterpret_cast<uint4*>(dst), N, K, kb, chunks, false);
+  else
+    weight_tile_kernel<<<blocks, 256, 0, stream>>>(reinterpret_cast<const uint4*>(src),
+                                                   reinterpret_cast<uint4*>(dst), N, K, kb, chunks, true);
+  return cudaGetLastError();
+}
+
+static unsigned long long* g_debug_timing = nullptr;
+void gemm_debug_timing(void* buf) { g_debug_timing = static_cast<unsigned long long*>(buf); }
+
 cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   if (a.M <= 0 || a.N <= 0) return cudaSuccess;
   // tmap_x must have been encoded with box rows == gemm_pick_n_tile(M).
   GemmRun r{};
+  r.w_tiled = static_cast<const uint8_t*>(a.w_tiled);
+  r.timing = g_debug_timing;
   r.out = a.out;
+  r.partials = a.partials;
+  r.flags = a.flags;
+  r.epoch = a.epoch;
   r.M = a.M;
   r.N = a.N;
   r.K = a.K;
   r.ldo = a.ldo;
   r.n_tile = gemm_pick_n_tile(a.M);
-  const int stage_bytes = kAStageBytes + r.n_tile * kBK * 2;
-  r.stages = kSmemBudget / stage_bytes;
-  if (r.stages > 8) r.stages = 8;
-  r.kb_total = (a.K + kBK - 1) / kBK;
-  const int splits = a.epi == Epilogue::kPartialF32 ? (a.splits < 1 ? 1 : a.splits) : 1;
-  r.kb_per_split = (r.kb_total + splits - 1) / splits;
+  const int b_stage = r.n_tile * kBK * 2;
+  r.stages_b = r.n_tile > 128 ? 2 : 3;
+  r.stages_a = (kSmemBudget - r.stages_b * b_stage - 2 * kChunkBytes) / kAStageBytes;
+  if (r.stages_a > 10) r.stages_a = 10;
+  // The fixer prefetches up to 2 partners x ceil(n_tile/32) chunks into the A ring.
+  r.kb = (a.K + kBK - 1) / kBK;
+  r.m_tiles = (a.N + kBM - 1) / kBM;
+  const int n_tiles_tok = (a.M + r.n_tile - 1) / r.n_tile;
+  r.iters = static_cast<int64_t>(r.m_tiles) * n_tiles_tok * r.kb;
   r.epi = static_cast<int>(a.epi);
-  r.tmem_cols = pow2_cols(r.n_tile);
-  const size_t smem = 1024 + static_cast<size_t>(r.stages) * stage_bytes + (2 * r.stages + 1) * 8 + 16;
+  r.tmem_cols = pow2_cols(r.n_tile + (r.n_tile > 32 ? r.n_tile : 32));
+  int grid = a.grid > 0 ? a.grid : 148;
+  // Enough k-blocks per CTA that the fixed per-CTA cost and the fixup
+  // partials stay small next to the weight bytes it streams.
+  const int64_t min_iters = a.min_iters > 0 ? a.min_iters : 1;
+  if (static_cast<int64_t>(grid) * min_iters > r.iters) grid = static_cast<int>(std::max<int64_t>(1, r.iters / min_iters));
+  // Non-residual epilogues sum pieces in a fixer: keep every tile in <= 3
+  // pieces (<= 2 partners) so their chunks fit the idle A ring.
+  if (r.epi != static_cast<int>(Epilogue::kResidualAddF32)) {
+    const int nchunk = (r.n_tile + 31) / 32;
+    const int max_partners = (r.stages_a * kAStageBytes) / (nchunk * kChunkBytes);
+    // a range of R iterations lets a tile meet at most ceil(kb / R) + 1 ranges
+    const int64_t need_r = (r.kb + max_partners - 1) / std::max(1, max_partners);
+    if (static_cast<int64_t>(grid) * need_r > r.iters) grid = static_cast<int>(std::max<int64_t>(1, r.iters / need_r));
+  }
+  const size_t smem = 1024 + static_cast<size_t>(r.stages_a) * kAStageBytes + static_cast<size_t>(r.stages_b) * b_stage +
+                      2 * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16;
   static bool configured = false;
   if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         232448);
+    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
     if (e != cudaSuccess) return e;
     configured = true;
   }
-  CUtensorMap tw, tx;
-  std::memcpy(&tw, a.tmap_w, sizeof(CUtensorMap));
+  CUtensorMap tw, tx, to;
+  if (a.tmap_w != nullptr) std::memcpy(&tw, a.tmap_w, sizeof(CUtensorMap));
+  else std::memset(&tw, 0, sizeof(CUtensorMap));
   std::memcpy(&tx, a.tmap_x, sizeof(CUtensorMap));
-  dim3 grid((a.N + kBM - 1) / kBM, (a.M + r.n_tile - 1) / r.n_tile, splits);
-  gemm_tn_kernel<<<grid, kThreads, smem, stream>>>(tw, tx, r);
+  std::memcpy(&to, a.tmap_out, sizeof(CUtensorMap));
+  gemm_tn_kernel<<<grid, kThreads, smem, stream>>>(tw, tx, to, r);
   return cudaGetLastError();
 }
 

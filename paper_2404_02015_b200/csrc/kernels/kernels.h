@@ -55,21 +55,35 @@ cudaError_t table_update(const TableUpdateArgs& a, cudaStream_t stream);
 // tile) and up to 256 activation rows (UMMA N), so decode batches (M <= 256)
 // stream each weight byte exactly once.
 enum class Epilogue : int {
-  kStoreBf16 = 0,   // out bf16 [M][ldo]
-  kPartialF32 = 1,  // out fp32 [split][M][ldo] (split-K partial sums)
-  kSiluMulBf16 = 2, // W rows interleaved (gate, up) pairs: out bf16 [M][N/2]
-  kStoreF32 = 3,    // out fp32 [M][ldo]
+  kStoreBf16 = 0,      // out bf16 [M][ldo]
+  kResidualAddF32 = 1, // out fp32 [M][ldo] += D (the residual stream; single owner per element)
+  kSiluMulBf16 = 2,    // W rows interleaved (gate, up) pairs: out bf16 [M][N/2]
+  kStoreF32 = 3,       // out fp32 [M][ldo]
 };
 struct GemmArgs {
-  const void* tmap_w;       // CUtensorMap* (host memory, passed by value)
-  const void* tmap_x;
+  const void* w_tiled;      // weights in weight_tile() layout (preferred), or null
+  const void* tmap_w;       // else: CUtensorMap* over row-major W (host memory)
+  const void* tmap_x;       // box rows must equal gemm_pick_n_tile(M)
+  const void* tmap_out;     // make_tmap_gemm_out(): box 32 tokens x 128 (SiLU: 64) features
   void* out;
+  float* partials;          // stream-K fixup scratch: gemm_partials_floats(grid) floats
+  int* flags;               // [grid] ints, zero-initialised once
+  int epoch;                // distinct (> 0) for every launch sharing `flags`
+  int grid;                 // persistent CTAs (#SMs)
+  int min_iters;            // cap the grid so every CTA gets >= min_iters k-blocks (0 = no cap)
   int M, N, K;
   int ldo;
-  int splits;               // split-K factor (kPartialF32 only)
   Epilogue epi;
 };
 cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream);
+int gemm_pick_n_tile(int M);
+bool make_tmap_gemm_out(void* tmap_out, const void* out, int epi, int M, int N, int ldo);
+// B200 weight layout: [ceil(N/128)][ceil(K/64)] contiguous 16 KiB UMMA tiles,
+// pre-swizzled (SWIZZLE_128B), zero-padded. inverse=true converts back.
+size_t weight_tiled_bytes(int N, int K);
+cudaError_t weight_tile(const void* src, int N, int K, void* dst, bool inverse, cudaStream_t stream);
+size_t gemm_partials_floats(int max_grid);
+void gemm_debug_timing(void* buf);  // [grid][4] u64 globaltimer stamps per CTA, null = off
 // Encode a 2-D bf16 tensor map (rows x cols, cols contiguous) with a
 // box of box_rows x 64 and 128-byte swizzle. Returns false on failure.
 bool make_tmap_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t cols,
@@ -79,10 +93,9 @@ bool make_tmap_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t co
 cudaError_t embed_rmsnorm(const void* emb, const int32_t* tokens, const float* norm_w,
                           float* resid, void* xn, int T, int hidden, float eps,
                           cudaStream_t stream);
-// resid[t] += sum_s parts[s][t]; xn[t] = rmsnorm(resid[t]) * w (bf16)
-cudaError_t reduce_residual_rmsnorm(const float* parts, int splits, float* resid,
-                                    const float* norm_w, void* xn, int T, int hidden, float eps,
-                                    cudaStream_t stream);
+// xn[t] = bf16(resid[t] * rsqrt(mean(resid[t]^2) + eps) * w)
+cudaError_t rmsnorm_rows(const float* resid, const float* norm_w, void* xn, int T, int hidden, float eps,
+                         cudaStream_t stream);
 // Row argmax of fp32 logits; writes token ids (lowest index on ties).
 cudaError_t argmax_rows(const float* logits, int T, int V, int32_t* out, cudaStream_t stream);
 // Gather rows: dst[i] = src[idx[i]] (bf16 rows of `cols`).

@@ -392,6 +392,9 @@ class Unit:
     def launches(self) -> int:
         return int(lib.mux_unit_launches(self._h))
 
+    def set_option(self, key: str, value: int):
+        check(lib.mux_unit_set_option(self._h, key.encode(), value))
+
     def run_lockstep(self, entries: Sequence[Entry], trace: Sequence[TraceRequest],
                      gpu_memory_bytes: int, params: EngineParams | None = None,
                      prompt_seed: int = 11, num_sm: float = 0.5, profile=None):
@@ -441,8 +444,21 @@ def rope_table(positions: int):
     return out
 
 
-def gemm_bf16(x, w, out, epilogue: int = 0, splits: int = 1, stream=None):
-    """out = x @ w.T on tcgen05; x [M,K], w [N,K] bf16 CUDA tensors."""
+def gemm_bf16(x, w, out, epilogue: int = 0, grid: int = 0, stream=None, w_tiled=None):
+    """x @ w.T on tcgen05 (x [M,K], w [N,K] bf16 CUDA tensors). epilogue: 0 store
+    bf16, 1 out += (fp32), 2 SiLU(gate)*up of interleaved rows, 3 store fp32.
+    w_tiled: the same weights in weight_tile() layout (streamed by bulk copy)."""
     M, K = x.shape
     N = w.shape[0]
-    check(lib.mux_gemm_bf16(_ptr(x), _ptr(w), M, N, K, _ptr(out), epilogue, splits, _ptr(stream)))
+    src = w if w_tiled is None else w_tiled
+    check(lib.mux_gemm_bf16(_ptr(x), _ptr(src), 0 if w_tiled is None else 1, M, N, K, _ptr(out), epilogue,
+                            grid, _ptr(stream)))
+
+
+def weight_tile(w, stream=None):
+    """Row-major [N,K] bf16 CUDA tensor -> uint8 tensor in the B200 tile layout."""
+    import torch
+    N, K = w.shape
+    out = torch.empty(int(lib.mux_weight_tiled_bytes(N, K)), dtype=torch.uint8, device=w.device)
+    check(lib.mux_weight_tile(_ptr(w), N, K, _ptr(out), 0, _ptr(stream)))
+    return out

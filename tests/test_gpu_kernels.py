@@ -160,13 +160,54 @@ def test_gemm_tcgen05(cuda, M, N, K):
     mux.gemm_bf16(x, w, out32, epilogue=3)
     out16 = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
     mux.gemm_bf16(x, w, out16, epilogue=0)
-    splits = 3
-    parts = torch.empty(splits, M, N, dtype=torch.float32, device="cuda")
-    mux.gemm_bf16(x, w, parts, epilogue=1, splits=splits)
+    resid0 = torch.randn(M, N, generator=g, device="cuda")
+    resid = resid0.clone()
+    mux.gemm_bf16(x, w, resid, epilogue=1)
+    # odd grids exercise tiles split across many CTAs (stream-K fixups)
+    out_g = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    mux.gemm_bf16(x, w, out_g, epilogue=3, grid=37)
+    out_g2 = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    mux.gemm_bf16(x, w, out_g2, epilogue=3, grid=1000)
     torch.cuda.synchronize()
     assert (out32 - ref).abs().max().item() <= 1e-4 * scale + 1e-6
     assert (out16.float() - ref).abs().max().item() <= 8e-3 * scale
-    assert (parts.sum(0) - ref).abs().max().item() <= 1e-4 * scale + 1e-6
+    assert (resid - resid0 - ref).abs().max().item() <= 1e-4 * scale + 1e-5
+    assert (out_g - ref).abs().max().item() <= 1e-4 * scale + 1e-6
+    assert (out_g2 - ref).abs().max().item() <= 1e-4 * scale + 1e-6
+
+
+@pytest.mark.parametrize("M,N,K", [(1, 256, 512), (64, 384, 200), (128, 1000, 576), (300, 640, 1024)])
+def test_gemm_tiled_weights(cuda, M, N, K):
+    """Weights in the B200 tile layout (bulk-copied 16 KiB UMMA tiles) give the
+    same result as the TMA path; the tile transform round-trips exactly."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(M + N + K)
+    x = torch.randn(M, K, generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(N, K, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
+    wt = mux.weight_tile(w)
+    back = torch.empty_like(w)
+    mux._lib.check(mux.lib.mux_weight_tile(wt.data_ptr(), N, K, back.data_ptr(), 1, None))
+    a = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    b = torch.empty(M, N, dtype=torch.float32, device="cuda")
+    mux.gemm_bf16(x, w, a, epilogue=3)
+    mux.gemm_bf16(x, w, b, epilogue=3, w_tiled=wt)
+    torch.cuda.synchronize()
+    assert torch.equal(back, w)
+    assert torch.equal(a, b)
+
+
+def test_gemm_deterministic(cuda):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(9)
+    x = torch.randn(128, 4096, generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(4096, 4096, generator=g, device="cuda") * 0.02).to(torch.bfloat16)
+    outs = []
+    for _ in range(3):
+        o = torch.empty(128, 4096, dtype=torch.float32, device="cuda")
+        mux.gemm_bf16(x, w, o, epilogue=3)
+        outs.append(o)
+    torch.cuda.synchronize()
+    assert torch.equal(outs[0], outs[1]) and torch.equal(outs[1], outs[2])
 
 
 @pytest.mark.parametrize("M", [3, 64, 300])
