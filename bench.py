@@ -122,7 +122,7 @@ def run_ours(args, rank, world, local_rank):
     torch.cuda.set_device(local_rank)
     specs = [mux.spec(m) for m in args.models.split(",")]
     B = args.batch
-    steps_total = args.warmup + args.steps + args.e2e_steps + 2
+    steps_total = args.warmup + args.steps + args.e2e_steps + args.attn_steps + 2
     rng = np.random.default_rng(1000 + rank)
     batches = [sample_batch(rng, B, steps_total) for _ in specs]
     need = 0
@@ -135,6 +135,7 @@ def run_ours(args, rank, world, local_rank):
     unit = mux.Unit(specs, pool_blocks=logical, device=local_rank, device_pool_blocks=need + 4096,
                     max_batch=B, max_prefill_tokens=256, max_ctx=max_ctx + 16, max_slots=2 * B + 16,
                     init_seed=1 + rank, init_std=0.02, partitions=len(specs) + 1)
+    unit.set_option("pdl", args.pdl)
     unit.init_kv(seed=7 + rank, std=1.0)
     pool = unit.pool
     ids = []
@@ -158,7 +159,8 @@ def run_ours(args, rank, world, local_rank):
                 if not r.ok:
                     raise RuntimeError("pool exhausted")
             unit.decode(li, ids[li], tokens=None if tokens is None else tokens[li],
-                        out=None if outs is None else outs[li], partition=1 + li, ids_c=ids_c[li])
+                        out=None if outs is None else outs[li], partition=1 + (0 if args.serial else li),
+                        ids_c=ids_c[li])
 
     for _ in range(args.warmup):
         step()
@@ -166,7 +168,6 @@ def run_ours(args, rank, world, local_rank):
     if world > 1:
         torch.distributed.barrier()
     clocks = Clocks(local_rank)
-    unit.attn_timing(True)
     launches0 = unit.launches()
     unit.sync()
     for li in range(len(specs)):
@@ -179,9 +180,17 @@ def run_ours(args, rank, world, local_rank):
     # span from the first partition's start to the last partition's end
     ms = max(unit.elapsed_ms(0, 2 * li + 1) for li in range(len(specs)))
     launches = unit.launches() - launches0
+    clk = clocks.stop()
+
+    # K1 roofline: CUDA events around every decode-attention launch, on its
+    # stream, over separate steps (events between kernels would break the
+    # PDL overlap inside the timed region above).
+    unit.attn_timing(True)
+    for _ in range(args.attn_steps):
+        step()
+    unit.sync()
     attn_ms, attn_n, attn_bytes = unit.attn_time()
     unit.attn_timing(False)
-    clk = clocks.stop()
 
     # e2e: host token ids in (pinned) -> jobs -> next tokens out (pinned), each
     # step waits for its result before the next, as a serving loop does.
@@ -221,6 +230,9 @@ def main():
     ap.add_argument("--batch", type=int, default=128, help="decode members per model")
     ap.add_argument("--models", default="7b,13b")
     ap.add_argument("--e2e-steps", type=int, default=4)
+    ap.add_argument("--attn-steps", type=int, default=2, help="steps with per-launch K1 events")
+    ap.add_argument("--serial", action="store_true", help="run the colocated decode jobs on one stream")
+    ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch between job kernels")
     ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg (profiling runs)")
     args = ap.parse_args()
 

@@ -248,7 +248,8 @@ MUX_API int mux_unit_attn_timing(mux_unit* unit, int enable);
 MUX_API int mux_unit_attn_time(mux_unit* unit, double* total_ms, int64_t* launches, double* bytes);
 /* Kernel launches issued by this unit so far (all libmux kernels). */
 MUX_API int64_t mux_unit_launches(mux_unit* unit);
-/* Tuning knobs: "gemm_min_iters" (k-blocks per GEMM CTA, default 24). */
+/* Tuning knobs: "gemm_min_iters" (k-blocks per GEMM CTA, default 24);
+ * "pdl" (programmatic dependent launch between job kernels, default 1). */
 MUX_API int mux_unit_set_option(mux_unit* unit, const char* key, int64_t value);
 
 /* Lockstep run: the engine's decisions are those of mux_simulate (oracle

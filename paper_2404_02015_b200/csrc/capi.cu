@@ -15,6 +15,7 @@
 
 #include "device/runtime.h"
 #include "kernels/kernels.h"
+#include "kernels/launch.cuh"
 #include "mux/engine.hpp"
 #include "mux/kv.hpp"
 
@@ -731,6 +732,7 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
   return guarded([&] {
     const std::string k = key ? key : "";
     if (k == "gemm_min_iters") u->rt->set_gemm_min_iters(static_cast<int>(value));
+    else if (k == "pdl") mux::pdl_enabled() = value != 0;
     else throw std::invalid_argument("unknown option: " + k);
   });
 }

@@ -10,8 +10,15 @@
 #include <string>
 
 #include "../kernels/kernels.h"
+#include "../kernels/launch.cuh"
+#include "../kernels/ptx.cuh"
 
 namespace mux {
+
+bool& pdl_enabled() {
+  static bool on = true;
+  return on;
+}
 
 void check_cuda(cudaError_t e, const char* what) {
   if (e != cudaSuccess)
@@ -46,11 +53,15 @@ namespace {
 constexpr int kEpiStoreBf16 = 0, kEpiResidual = 1, kEpiSilu = 2, kEpiStoreF32 = 3;
 
 __global__ void gather_last_tok(const int32_t* last_tok, const int32_t* slots, int32_t* tokens, int n) {
+  grid_dep_wait();
+  grid_dep_launch();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) tokens[i] = last_tok[slots[i]];
 }
 
 __global__ void scatter_last_tok(int32_t* last_tok, const int32_t* slots, const int32_t* tokens, int n) {
+  grid_dep_wait();
+  grid_dep_launch();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) last_tok[slots[i]] = tokens[i];
 }
@@ -403,9 +414,15 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
     h[4 * T + i] = ctx_host[i] - 1;
     if (tokens_host) h[i] = tokens_host[i];
   }
+  // K1 visits members longest-context first (LPT): the ragged tail of the
+  // launch is then made of the shortest requests.
+  int32_t* order = h + 3 * T;
+  for (int i = 0; i < n; ++i) order[i] = i;
+  std::stable_sort(order, order + n, [&](int32_t x, int32_t y) { return ctx_host[x] > ctx_host[y]; });
   ws.stage_commit(5 * static_cast<size_t>(T), stream);
   if (!tokens_host) {
-    gather_last_tok<<<(n + 127) / 128, 128, 0, stream>>>(m.last_tok.as<int32_t>(), ws.slots, ws.tokens, n);
+    check_cuda(launch(gather_last_tok, dim3((n + 127) / 128), dim3(128), 0, stream, m.last_tok.as<int32_t>(),
+                      ws.slots, ws.tokens, n), "gather_last_tok");
     launches_ += 1;
   }
 
@@ -420,6 +437,7 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   at.rowlist = m.rowlist.as<int32_t>();
   at.slots = ws.slots;
   at.ctx = ws.ctx;
+  at.order = ws.tok_slot;  // staged above
   at.out = ws.attn.p;
   at.part_o = ws.attn_part_o.as<float>();
   at.part_ml = ws.attn_part_ml.as<float>();
@@ -488,7 +506,8 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   }
   gemm(m.lm_head.p, ws.xn.p, n, d.vocab, hid, ws.logits.p, d.vocab, kEpiStoreF32, ws, stream);
   check_cuda(argmax_rows(ws.logits.as<float>(), n, d.vocab, ws.out_tok, stream), "argmax");
-  scatter_last_tok<<<(n + 127) / 128, 128, 0, stream>>>(m.last_tok.as<int32_t>(), ws.slots, ws.out_tok, n);
+  check_cuda(launch(scatter_last_tok, dim3((n + 127) / 128), dim3(128), 0, stream, m.last_tok.as<int32_t>(),
+                    ws.slots, ws.out_tok, n), "scatter_last_tok");
   launches_ += 2;
   if (out_host)
     check_cuda(cudaMemcpyAsync(out_host, ws.out_tok, n * 4, cudaMemcpyDeviceToHost, stream), "out copy");
@@ -565,7 +584,8 @@ void Runtime::prefill(Llama& m, Workspace& ws, int n, const int32_t* slots_host,
   launches_ += 1;
   gemm(m.lm_head.p, ws.xlast.p, n, d.vocab, hid, ws.logits.p, d.vocab, kEpiStoreF32, ws, stream);
   check_cuda(argmax_rows(ws.logits.as<float>(), n, d.vocab, ws.out_tok, stream), "argmax");
-  scatter_last_tok<<<(n + 127) / 128, 128, 0, stream>>>(m.last_tok.as<int32_t>(), ws.slots, ws.out_tok, n);
+  check_cuda(launch(scatter_last_tok, dim3((n + 127) / 128), dim3(128), 0, stream, m.last_tok.as<int32_t>(),
+                    ws.slots, ws.out_tok, n), "scatter_last_tok");
   launches_ += 2;
   if (out_host)
     check_cuda(cudaMemcpyAsync(out_host, ws.out_tok, n * 4, cudaMemcpyDeviceToHost, stream), "out copy");

@@ -25,6 +25,7 @@
 
 #include "ptx.cuh"
 #include "kernels.h"
+#include "launch.cuh"
 
 namespace mux {
 namespace {
@@ -55,7 +56,8 @@ decode_attention_kernel(const DecodeAttnArgs a) {
 
   const int split = blockIdx.x;
   const int h = blockIdx.y;
-  const int b = blockIdx.z;
+  // Longest-first order (host sorted by ctx) so the ragged tail is short.
+  const int b = a.order != nullptr ? a.order[blockIdx.z] : blockIdx.z;
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
 
@@ -73,6 +75,8 @@ decode_attention_kernel(const DecodeAttnArgs a) {
     fence_barrier_init();
   }
   __syncthreads();
+  grid_dep_wait();    // q / pool / tables come from the kernels before
+  grid_dep_launch();
 
   if (warp == kConsumerWarps) {
     // ---------------- producer warp: resolve ids, then stream K/V blocks
@@ -259,6 +263,8 @@ decode_attention_kernel(const DecodeAttnArgs a) {
 // Merge KV splits: O = sum_s O_s L_s 2^(M_s - M) / sum_s L_s 2^(M_s - M).
 template <typename OutT>
 __global__ void __launch_bounds__(128) decode_attention_combine(const DecodeAttnArgs a) {
+  grid_dep_wait();
+  grid_dep_launch();
   const int64_t bh = blockIdx.x;
   const int d = threadIdx.x;
   const float* pml = a.part_ml + bh * a.splits * 2;
@@ -294,11 +300,10 @@ cudaError_t launch_decode(const DecodeAttnArgs& a, cudaStream_t stream) {
     configured = true;
   }
   dim3 grid(a.splits, a.H, a.B);
-  decode_attention_kernel<S, OutT><<<grid, kThreads, smem, stream>>>(a);
-  if (a.splits > 1) {
-    decode_attention_combine<OutT><<<a.B * a.H, 128, 0, stream>>>(a);
-  }
-  return cudaGetLastError();
+  cudaError_t e = launch(decode_attention_kernel<S, OutT>, grid, dim3(kThreads), smem, stream, a);
+  if (e == cudaSuccess && a.splits > 1)
+    e = launch(decode_attention_combine<OutT>, dim3(a.B * a.H), dim3(128), 0, stream, a);
+  return e;
 }
 
 }  // namespace

@@ -9,6 +9,7 @@
 
 #include "kernels.h"
 #include "ptx.cuh"
+#include "launch.cuh"
 
 namespace mux {
 namespace {
@@ -42,6 +43,8 @@ __global__ void __launch_bounds__(kRowThreads) embed_rmsnorm_kernel(
     const __nv_bfloat16* emb, const int32_t* tokens, const float* norm_w, float* resid,
     __nv_bfloat16* xn, int hidden, float eps) {
   __shared__ float scratch[32];
+  grid_dep_wait();
+  grid_dep_launch();
   const int t = blockIdx.x;
   const int64_t tok = tokens[t];
   const __nv_bfloat16* e = emb + tok * hidden;
@@ -56,6 +59,8 @@ template <int kVec>
 __global__ void __launch_bounds__(kRowThreads) rmsnorm_rows_kernel(const float* resid, const float* norm_w,
                                                                    __nv_bfloat16* xn, int hidden, float eps) {
   __shared__ float scratch[32];
+  grid_dep_wait();
+  grid_dep_launch();
   const int t = blockIdx.x;
   const float4* x = reinterpret_cast<const float4*>(resid + static_cast<int64_t>(t) * hidden);
   const float4* w = reinterpret_cast<const float4*>(norm_w);
@@ -84,6 +89,8 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_rows_kernel(const float* 
 __global__ void __launch_bounds__(kRowThreads) argmax_kernel(const float* logits, int V, int32_t* out) {
   __shared__ float sv[32];
   __shared__ int si[32];
+  grid_dep_wait();
+  grid_dep_launch();
   const float* row = logits + static_cast<int64_t>(blockIdx.x) * V;
   float best = -INFINITY;
   int bi = V;  // sentinel above any index; NaN logits never win
@@ -122,6 +129,8 @@ __global__ void __launch_bounds__(kRowThreads) argmax_kernel(const float* logits
 }
 
 __global__ void gather_rows_kernel(const uint4* src, const int32_t* idx, uint4* dst, int vec_per_row) {
+  grid_dep_wait();
+  grid_dep_launch();
   const int r = blockIdx.x;
   const int64_t s = static_cast<int64_t>(idx[r]) * vec_per_row;
   const int64_t d = static_cast<int64_t>(r) * vec_per_row;
@@ -132,6 +141,8 @@ __global__ void gather_rows_kernel(const uint4* src, const int32_t* idx, uint4* 
 // scores, lane = 4 dims for the P.V accumulation), online softmax in fp32.
 __global__ void __launch_bounds__(128) prefill_attention_kernel(const PrefillAttnArgs a) {
   __shared__ float qs[4][128];
+  grid_dep_wait();
+  grid_dep_launch();
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   const int gw = blockIdx.x * 4 + warp;
   if (gw >= a.T * a.H) return;
@@ -226,10 +237,9 @@ __global__ void fill_kernel(float* dst, int64_t n, float v) {
 cudaError_t embed_rmsnorm(const void* emb, const int32_t* tokens, const float* norm_w, float* resid,
                           void* xn, int T, int hidden, float eps, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  embed_rmsnorm_kernel<<<T, kRowThreads, 0, stream>>>(
-      reinterpret_cast<const __nv_bfloat16*>(emb), tokens, norm_w, resid,
-      reinterpret_cast<__nv_bfloat16*>(xn), hidden, eps);
-  return cudaGetLastError();
+  return launch(embed_rmsnorm_kernel, dim3(T), dim3(kRowThreads), 0, stream,
+                reinterpret_cast<const __nv_bfloat16*>(emb), tokens, norm_w, resid,
+                reinterpret_cast<__nv_bfloat16*>(xn), hidden, eps);
 }
 
 cudaError_t rmsnorm_rows(const float* resid, const float* norm_w, void* xn, int T, int hidden, float eps,
@@ -238,32 +248,27 @@ cudaError_t rmsnorm_rows(const float* resid, const float* norm_w, void* xn, int 
   if (hidden % 4 != 0 || hidden > 4 * kRowThreads * 16) return cudaErrorInvalidValue;
   __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(xn);
   const int per = (hidden / 4 + kRowThreads - 1) / kRowThreads;
-  if (per <= 2) rmsnorm_rows_kernel<2><<<T, kRowThreads, 0, stream>>>(resid, norm_w, y, hidden, eps);
-  else if (per <= 4) rmsnorm_rows_kernel<4><<<T, kRowThreads, 0, stream>>>(resid, norm_w, y, hidden, eps);
-  else if (per <= 8) rmsnorm_rows_kernel<8><<<T, kRowThreads, 0, stream>>>(resid, norm_w, y, hidden, eps);
-  else rmsnorm_rows_kernel<16><<<T, kRowThreads, 0, stream>>>(resid, norm_w, y, hidden, eps);
-  return cudaGetLastError();
+  auto k = per <= 2 ? rmsnorm_rows_kernel<2> : per <= 4 ? rmsnorm_rows_kernel<4>
+         : per <= 8 ? rmsnorm_rows_kernel<8> : rmsnorm_rows_kernel<16>;
+  return launch(k, dim3(T), dim3(kRowThreads), 0, stream, resid, norm_w, y, hidden, eps);
 }
 
 cudaError_t argmax_rows(const float* logits, int T, int V, int32_t* out, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
-  argmax_kernel<<<T, kRowThreads, 0, stream>>>(logits, V, out);
-  return cudaGetLastError();
+  return launch(argmax_kernel, dim3(T), dim3(kRowThreads), 0, stream, logits, V, out);
 }
 
 cudaError_t gather_rows_bf16(const void* src, const int32_t* idx, void* dst, int n, int cols,
                              cudaStream_t stream) {
   if (n <= 0) return cudaSuccess;
-  gather_rows_kernel<<<n, 128, 0, stream>>>(reinterpret_cast<const uint4*>(src), idx,
-                                            reinterpret_cast<uint4*>(dst), cols / 8);
-  return cudaGetLastError();
+  return launch(gather_rows_kernel, dim3(n), dim3(128), 0, stream, reinterpret_cast<const uint4*>(src), idx,
+                reinterpret_cast<uint4*>(dst), cols / 8);
 }
 
 cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
   if (a.T <= 0) return cudaSuccess;
   const int warps = a.T * a.H;
-  prefill_attention_kernel<<<(warps + 3) / 4, 128, 0, stream>>>(a);
-  return cudaGetLastError();
+  return launch(prefill_attention_kernel, dim3((warps + 3) / 4), dim3(128), 0, stream, a);
 }
 
 cudaError_t init_normal_bf16(void* dst, int64_t n, uint64_t seed, float std, cudaStream_t stream) {

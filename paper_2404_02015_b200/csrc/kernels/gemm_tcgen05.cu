@@ -37,11 +37,13 @@
 
 #include <cstdint>
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
 #include "kernels.h"
 #include "ptx.cuh"
+#include "launch.cuh"
 
 namespace mux {
 namespace {
@@ -98,7 +100,9 @@ __global__ void __launch_bounds__(kThreads, 1)
 gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
                const __grid_constant__ CUtensorMap tout, const GemmRun r) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
-  uint8_t* base = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  // 1 KiB-aligned carve-up; pointer arithmetic on smem_raw itself keeps the
+  // shared address space visible to the compiler (STS/LDS, not generic ST/LD).
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   // Separate rings: weights (A, HBM-streamed) run SA stages deep, the small
   // L2-resident activation tiles (B) only SB, so more weight bytes are in
   // flight per SM than a shared ring of the same smem would allow.
@@ -120,7 +124,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x;
   const int G = gridDim.x;
-  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 16 + 0] = gtimer();
+  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 32 + 0] = gtimer();
   const int64_t it0 = range_begin(r.iters, c, G);
   const int64_t it1 = range_begin(r.iters, c + 1, G);
 
@@ -148,12 +152,16 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (threadIdx.x == 0) grid_dep_launch();
 
   if (warp == 0 || warp == 3) {
     // ------------------------------------------------ TMA producers
     // warp 0 streams the weight tiles, warp 3 the activation tiles.
     if (elect_one()) {
       const bool is_a = warp == 0;
+      // Weights do not depend on earlier kernels: warp 0 starts streaming
+      // them while the predecessor drains (PDL); activations must wait.
+      if (!is_a) grid_dep_wait();
       const uint64_t pol = is_a ? policy_evict_first()   // weights: streamed once per step
                                 : policy_evict_last();   // activations: re-read by every CTA
       const int SS = is_a ? SA : SB;
@@ -198,7 +206,9 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       for (; it < seg_end; ++it, ++i) {
         const int sa = i % SA, sb = i % SB;
         mbar_wait(&full_a[sa], (i / SA) & 1);
+        if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 32 + 4] = gtimer();
         mbar_wait(&full_b[sb], (i / SB) & 1);
+        if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 32 + 5] = gtimer();
         tc_fence_after();
         if (elect_one()) {
           const uint32_t a_addr = smem_u32(a_st + sa * kAStageBytes);
@@ -217,12 +227,13 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       }
       ++seg;
     }
-    if (r.timing != nullptr && lane == 0) r.timing[c * 16 + 1] = gtimer();
+    if (r.timing != nullptr && lane == 0) r.timing[c * 32 + 1] = gtimer();
   } else if (warp >= 4) {
     // ------------------------------------------------------ epilogue
     // Each chunk (32 tokens of the tile) goes TMEM -> registers -> a 16 KiB
     // shared staging buffer -> global by asynchronous bulk copies issued by
     // one leader thread, so no thread ever waits on a global store.
+    grid_dep_wait();  // partials / flags / out may still be in use by the predecessor
     const int q = warp - 4;  // TMEM lane quarter this warp may access
     const int etid = threadIdx.x - 128;
     const int fl = q * 32 + lane;  // feature row of this thread inside the tile
@@ -256,12 +267,15 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         if (leader)
           for (int p = c + 1; p < p_hi; ++p)
             while (ld_acquire(r.flags + p) != r.epoch) __nanosleep(32);
+        if (leader && r.timing != nullptr) r.timing[c * 32 + 6] = gtimer();
       }
       mbar_wait(&tm_full[b], (seg >> 1) & 1);
       tc_fence_after();
+      if (leader && r.timing != nullptr && seg < 4) r.timing[c * 32 + 9 + seg] = gtimer();
       if (n_part > 0) {
         // All MMAs of this CTA are complete, so the A ring is idle now.
         if (leader) {
+          asm volatile("fence.proxy.async.global;" ::: "memory");
           mbar_arrive_expect_tx(pbar, static_cast<uint32_t>(n_part * nchunk * kChunkBytes));
           for (int pi = 0; pi < n_part; ++pi)
             for (int k = 0; k < nchunk; ++k)
@@ -270,12 +284,15 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         }
         mbar_wait(pbar, pphase);
         pphase ^= 1;
+        if (leader && r.timing != nullptr) r.timing[c * 32 + 7] = gtimer();
       }
       const uint32_t acc = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * r.n_tile);
       for (int k = 0; k < nchunk; ++k) {
         const int cc = k * 32;
         float v[32];
         tmem_ld_32x32b_x32(acc + cc, v);
+        const bool stamp = leader && r.timing != nullptr && seg_end == it1 && k < 4;
+        if (stamp) r.timing[c * 32 + 20 + k] = gtimer();
         if (k == nchunk - 1) {  // accumulators consumed: hand TMEM back
           tc_fence_before();
           __syncwarp();
@@ -289,24 +306,37 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         // Staging buffer: wait until the bulk group that last read it is done.
         if (leader) bulk_wait_read<1>();
         epi_bar();
+        if (stamp) r.timing[c * 32 + 24 + k] = gtimer();
         uint8_t* st = stage_out + sbuf * kChunkBytes;
-        const bool fp32_rows = !first || residual || r.epi == static_cast<int>(Epilogue::kStoreF32);
+        const bool silu = first && r.epi == static_cast<int>(Epilogue::kSiluMulBf16);
+        const bool fp32_rows = !first || residual || silu || r.epi == static_cast<int>(Epilogue::kStoreF32);
         if (fp32_rows) {
           float* sf = reinterpret_cast<float*>(st);
 #pragma unroll
           for (int j = 0; j < 32; ++j) sf[j * kBM + fl] = v[j];
-        } else if (r.epi == static_cast<int>(Epilogue::kStoreBf16)) {
+        } else {  // kStoreBf16
           __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(st);
 #pragma unroll
           for (int j = 0; j < 32; ++j) sh[j * kBM + fl] = __float2bfloat16_rn(v[j]);
-        } else {  // kSiluMulBf16: even row = gate_i, odd row = up_i -> act[:, i]
-          __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(st);
+        }
+        if (silu) {
+          // kSiluMulBf16: feature rows come in (gate_i, up_i) pairs. The fp32
+          // chunk is staged first; each thread then turns 16 adjacent pairs of
+          // one token into 16 bf16 act[token][i] (no shuffles, all ILP).
+          epi_bar();
+          const float4* sf4 = reinterpret_cast<const float4*>(st) + (etid >> 2) * (kBM / 4) + (etid & 3) * 8;
+          uint32_t packed[8];
 #pragma unroll
-          for (int j = 0; j < 32; ++j) {
-            const float up = __shfl_xor_sync(0xffffffffu, v[j], 1);
-            const float g = v[j];
-            if ((lane & 1) == 0) sh[j * (kBM / 2) + (fl >> 1)] = __float2bfloat16_rn(g / (1.f + __expf(-g)) * up);
+          for (int q2 = 0; q2 < 8; ++q2) {
+            const float4 gu = sf4[q2];  // gate, up, gate, up
+            const float s0 = gu.x * rcp_approx(1.f + __expf(-gu.x));
+            const float s1 = gu.z * rcp_approx(1.f + __expf(-gu.z));
+            packed[q2] = pack_bf16(s0 * gu.y, s1 * gu.w);
           }
+          epi_bar();
+          uint4* dst = reinterpret_cast<uint4*>(st + (etid >> 2) * kBM + (etid & 3) * 32);
+          dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
+          dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
         }
         fence_async_smem();
         epi_bar();
@@ -316,29 +346,36 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             bulk_s2g(r.partials + (static_cast<int64_t>(c) * 8 + k) * (kChunkBytes / 4), st, kChunkBytes);
           } else if (residual) {
             tma_reduce_add_2d(&tout, st, m * kBM, tok0 + cc);  // rows >= M are clipped by TMA
-          } else if (r.epi == static_cast<int>(Epilogue::kSiluMulBf16)) {
+          } else if (silu) {
             tma_store_2d(&tout, st, m * (kBM / 2), tok0 + cc);
           } else {
             tma_store_2d(&tout, st, m * kBM, tok0 + cc);
           }
           bulk_commit();
+          if (stamp) r.timing[c * 32 + 28 + k] = gtimer();
         }
         sbuf ^= 1;
       }
-      if (!first && leader) {  // publish: partial writes complete, then the flag
-        bulk_wait<0>();
-        __threadfence();
-        st_release(r.flags + c, r.epoch);
+      if (!first && leader) {  // publish: partial bulk writes complete, then the flag
+        {
+          bulk_wait<0>();
+          asm volatile("fence.acq_rel.gpu;" ::: "memory");
+          st_release(r.flags + c, r.epoch);
+        }
+        if (leader && r.timing != nullptr) r.timing[c * 32 + 8] = gtimer();
       }
+      if (leader && r.timing != nullptr && seg < 4) r.timing[c * 32 + 16 + seg] = gtimer();
       it = seg_end;
       ++seg;
     }
     if (leader) bulk_wait<0>();  // staging smem must outlive its bulk reads
-    if (r.timing != nullptr && threadIdx.x == 128) r.timing[c * 16 + 2] = gtimer();
+    if (r.timing != nullptr && threadIdx.x == 128) r.timing[c * 32 + 2] = gtimer();
   }
   tc_fence_before();
   __syncthreads();
-  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 16 + 3] = gtimer();
+  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 32 + 3] = gtimer();
+  if (r.timing != nullptr && threadIdx.x == 128) r.timing[c * 32 + 13] = gtimer();
+  if (r.timing != nullptr && threadIdx.x == 32) r.timing[c * 32 + 14] = gtimer();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, r.tmem_cols);
@@ -477,8 +514,13 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   r.n_tile = gemm_pick_n_tile(a.M);
   const int b_stage = r.n_tile * kBK * 2;
   r.stages_b = r.n_tile > 128 ? 2 : 3;
+  // Debug overrides for pipeline-depth sweeps (scripts/gemm_micro.py).
+  static const int env_sb = getenv("MUX_GEMM_SB") ? atoi(getenv("MUX_GEMM_SB")) : 0;
+  static const int env_sa = getenv("MUX_GEMM_SA") ? atoi(getenv("MUX_GEMM_SA")) : 0;
+  if (env_sb > 0) r.stages_b = env_sb;
   r.stages_a = (kSmemBudget - r.stages_b * b_stage - 2 * kChunkBytes) / kAStageBytes;
   if (r.stages_a > 10) r.stages_a = 10;
+  if (env_sa > 0 && env_sa < r.stages_a) r.stages_a = env_sa;
   // The fixer prefetches up to 2 partners x ceil(n_tile/32) chunks into the A ring.
   r.kb = (a.K + kBK - 1) / kBK;
   r.m_tiles = (a.N + kBM - 1) / kBM;
@@ -513,8 +555,7 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   else std::memset(&tw, 0, sizeof(CUtensorMap));
   std::memcpy(&tx, a.tmap_x, sizeof(CUtensorMap));
   std::memcpy(&to, a.tmap_out, sizeof(CUtensorMap));
-  gemm_tn_kernel<<<grid, kThreads, smem, stream>>>(tw, tx, to, r);
-  return cudaGetLastError();
+  return launch(gemm_tn_kernel, dim3(grid), dim3(kThreads), smem, stream, tw, tx, to, r);
 }
 
 }  // namespace mux

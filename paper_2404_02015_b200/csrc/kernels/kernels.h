@@ -14,6 +14,7 @@ struct DecodeAttnArgs {
   const int32_t* rowlist;   // [slots][max_rows]
   const int32_t* slots;     // [B] device-table slot of each member
   const int32_t* ctx;       // [B] cached tokens incl. the one appended this step
+  const int32_t* order;     // [B] CTA z -> member (longest ctx first), or null
   void* out;                // [B][H][128] bf16 or fp32
   float* part_o;            // [B][H][splits][128] (splits > 1)
   float* part_ml;           // [B][H][splits][2]   (splits > 1)

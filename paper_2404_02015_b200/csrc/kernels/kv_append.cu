@@ -13,6 +13,7 @@
 
 #include "kernels.h"
 #include "ptx.cuh"
+#include "launch.cuh"
 
 namespace mux {
 namespace {
@@ -51,6 +52,8 @@ __device__ __forceinline__ void rope4(float (&x)[4], const float* cs, int lane) 
 }
 
 __global__ void __launch_bounds__(256) kv_append_kernel(const AppendArgs a) {
+  grid_dep_wait();
+  grid_dep_launch();
   const int warp_global = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
   if (warp_global >= a.T * a.H) return;
@@ -92,6 +95,8 @@ __global__ void __launch_bounds__(256) kv_append_kernel(const AppendArgs a) {
 }
 
 __global__ void __launch_bounds__(256) table_update_kernel(const TableUpdateArgs a) {
+  grid_dep_wait();
+  grid_dep_launch();
   const int i = blockIdx.x;
   const int slot = a.meta[3 * i + 0];
   const int row = a.meta[3 * i + 1];
@@ -114,14 +119,12 @@ cudaError_t kv_append(const AppendArgs& a, cudaStream_t stream) {
   if (a.T <= 0) return cudaSuccess;
   const int warps = a.T * a.H;
   const int blocks = (warps + 7) / 8;
-  kv_append_kernel<<<blocks, 256, 0, stream>>>(a);
-  return cudaGetLastError();
+  return launch(kv_append_kernel, dim3(blocks), dim3(256), 0, stream, a);
 }
 
 cudaError_t table_update(const TableUpdateArgs& a, cudaStream_t stream) {
   if (a.n <= 0) return cudaSuccess;
-  table_update_kernel<<<a.n, 256, 0, stream>>>(a);
-  return cudaGetLastError();
+  return launch(table_update_kernel, dim3(a.n), dim3(256), 0, stream, a);
 }
 
 }  // namespace mux

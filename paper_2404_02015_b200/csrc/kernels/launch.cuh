@@ -1,0 +1,32 @@
+// Host launcher: every kernel of a prefill/decode job goes through launch(),
+// which sets programmatic stream serialization (PDL) unless disabled, so a
+// kernel's prologue -- and the GEMM's weight streaming, which does not depend
+// on the previous kernel -- overlaps the tail of its predecessor.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <utility>
+
+namespace mux {
+
+// Process-wide switch (default on); "pdl" option of mux_unit_set_option.
+bool& pdl_enabled();
+
+template <typename... P, typename... A>
+inline cudaError_t launch(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
+                          A&&... args) {
+  cudaLaunchAttribute attr[1];
+  attr[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+  attr[0].val.programmaticStreamSerializationAllowed = 1;
+  cudaLaunchConfig_t cfg{};
+  cfg.gridDim = grid;
+  cfg.blockDim = block;
+  cfg.dynamicSmemBytes = smem;
+  cfg.stream = stream;
+  cfg.attrs = attr;
+  cfg.numAttrs = pdl_enabled() ? 1 : 0;
+  return cudaLaunchKernelEx(&cfg, kernel, std::forward<A>(args)...);
+}
+
+}  // namespace mux

@@ -1,4 +1,9 @@
-"""Per-CTA globaltimer timeline of single K4 launches (debug)."""
+"""Per-CTA globaltimer timeline of single K4 launches (debug).
+
+Stamps (kernel, [grid][32] u64): 0 start, 4 first A stage landed, 5 first B
+stage landed, 1 MMA issue done, 9+s TMEM full for segment s (s<4),
+6 fixer: partner flags seen, 7 fixer: partials landed, 8 partner published,
+2 epilogue done, 3 exit."""
 import sys
 
 import torch
@@ -6,30 +11,41 @@ import torch
 sys.path.insert(0, ".")
 import paper_2404_02015_b200 as mux  # noqa: E402
 
-shapes = {"o7": (4096, 4096, 1), "qkv7": (12288, 4096, 0), "gu13": (27648, 5120, 0), "down7": (4096, 11008, 1), "lm": (32000, 4096, 3), "gu7s": (22016, 4096, 2)}
-M = 128
-buf = torch.zeros(1024 * 16, dtype=torch.int64, device="cuda")
+shapes = {"o13": (5120, 5120, 1), "qkv13": (15360, 5120, 0), "down13": (5120, 13824, 1), "gu13": (27648, 5120, 2)}
+M = int(sys.argv[1]) if len(sys.argv) > 1 else 128
+buf = torch.zeros(1024 * 32, dtype=torch.int64, device="cuda")
+names = {0: "start", 4: "A0", 5: "B0", 9: "seg0", 10: "seg1", 11: "seg2", 6: "fixflag", 7: "fixdata",
+         8: "publish", 1: "mma_done", 2: "epi_done", 3: "exit", 13: "exit128", 14: "exit32",
+         16: "end0", 17: "end1", 18: "end2"}
 for name, (N, K, epi) in shapes.items():
-    for grid in (148, 128, 32):
-        x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
-        w = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
-        wt = mux.weight_tile(w)
-        out = torch.zeros(M, N, device="cuda", dtype=torch.float32 if epi == 1 else torch.bfloat16)
-        for _ in range(2):
-            mux.gemm_bf16(x, w, out, epilogue=epi, grid=grid, w_tiled=wt)
-        torch.cuda.synchronize()
-        buf.zero_()
-        mux.lib.mux_debug_gemm_timing(buf.data_ptr())
+    grid = 148
+    x = torch.randn(M, K, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(N, K, device="cuda") * 0.02).to(torch.bfloat16)
+    wt = mux.weight_tile(w)
+    out = torch.zeros(M, N // 2 if epi == 2 else N, device="cuda", dtype=torch.float32 if epi == 1 else torch.bfloat16)
+    for _ in range(2):
         mux.gemm_bf16(x, w, out, epilogue=epi, grid=grid, w_tiled=wt)
-        torch.cuda.synchronize()
-        mux.lib.mux_debug_gemm_timing(None)
-        raw = buf.view(-1, 16)[:grid].cpu().double()
-        t0 = raw[:, 0].min()
-        t = (raw - t0) / 1e3  # us
+    torch.cuda.synchronize()
+    buf.zero_()
+    mux.lib.mux_debug_gemm_timing(buf.data_ptr())
+    mux.gemm_bf16(x, w, out, epilogue=epi, grid=grid, w_tiled=wt)
+    torch.cuda.synchronize()
+    mux.lib.mux_debug_gemm_timing(None)
+    raw = buf.view(-1, 32)[:grid].cpu().double()
+    t0 = raw[:, 0].min()
+    t = (raw - t0) / 1e3  # us
+    parts = []
+    for k, nm in names.items():
+        v = t[:, k][raw[:, k] > 0]
+        if len(v):
+            parts.append(f"{nm} {v.min():.1f}/{v.median():.1f}/{v.max():.1f}")
+    print(f"{name:6s} {N * K * 2 / 1e6:.0f}MB | " + " | ".join(parts), flush=True)
 
-        def st(col):
-            v = t[:, col][raw[:, col] > 0]
-            return f"med {v.median():6.2f} max {v.max():6.2f}" if len(v) else "   -   "
-        print(f"{name:6s} g{grid:3d} mma-issued {st(1)} | first tm_full {st(4)} | partner published {st(7)} | "
-              f"fixer waited {st(5)} | fixer adds done {st(6)} | epi done {st(2)}", flush=True)
-        print("   fixer chunk stamps (begin,end) med: " + " ".join(f"{t[:, k][raw[:, k] > 0].median():6.2f}" for k in range(8, 16) if (raw[:, k] > 0).any()))
+if len(sys.argv) > 2:  # per-CTA dump of the last shape
+    cols = [1, 7] + [20, 24, 28, 21, 25, 29, 22, 26, 30, 23, 27, 31] + [2]
+    names.update({20 + k: f"ld{k}" for k in range(4)})
+    names.update({24 + k: f"bar{k}" for k in range(4)})
+    names.update({28 + k: f"st{k}" for k in range(4)})
+    print("cta " + " ".join(f"{names[k]:>8s}" for k in cols))
+    for c in range(0, grid, max(1, grid // 24)):
+        print(f"{c:3d} " + " ".join(f"{t[c, k]:8.1f}" if raw[c, k] > 0 else "       -" for k in cols))
