@@ -172,6 +172,12 @@ MUX_API int mux_kv_append(const void* qkv, void* q_out, void* pool, const int32_
                   const int32_t* rowlist, const int32_t* tok_slot, const int32_t* tok_pos,
                   const float* rope_table, int rope_positions, int T, int H, int num_layers,
                   int layer, int max_rows, void* stream);
+/* K3: causal varlen prefill attention (the attention term of prefill_latency,
+ * cost_model.cpp:75-83) on tcgen05. q [T][H][128] bf16 (rotated), qkv
+ * [T][3][H][128] bf16 (k rotated), out [T][H][128] bf16; seq_lens (host)
+ * split the T tokens into nseq prompts. Synchronises the stream. */
+MUX_API int mux_prefill_attention(const void* q, const void* qkv, void* out, const int32_t* seq_lens, int nseq,
+                                  int H, void* stream);
 /* RoPE table [positions][64][(cos,sin)] fp32, theta 10000, head_dim 128. */
 MUX_API int mux_rope_table(int positions, float* out);
 

@@ -166,3 +166,29 @@ class RefLlama:
             nw = self.attn_norm[l + 1] if l + 1 < d.layers else self.final_norm
             xn = rmsnorm_bf16(x, nw)
         return (xn[-1] @ self.lm_head.T).astype(np.float32)
+
+
+def prefill_attention_ref(q, k, v, seq_lens):
+    """Causal varlen attention of each prompt (K3's contract), fp64.
+
+    q, k, v: [T, H, 128] float arrays (the bf16 values the kernel reads, k and
+    q already rotated); seq_lens split the T tokens into prompts. Context
+    semantics follow the reference's prefill job: every prompt token attends
+    to the prompt tokens up to itself (cost_model.cpp:75-83 prices exactly
+    this causal pass)."""
+    T, H, D = q.shape
+    out = np.zeros((T, H, D), np.float64)
+    scale = 1.0 / math.sqrt(D)
+    s0 = 0
+    for n in seq_lens:
+        qs = q[s0:s0 + n].astype(np.float64).transpose(1, 0, 2)  # [H, n, D]
+        ks = k[s0:s0 + n].astype(np.float64).transpose(1, 2, 0)  # [H, D, n]
+        vs = v[s0:s0 + n].astype(np.float64).transpose(1, 0, 2)  # [H, n, D]
+        s = np.matmul(qs, ks) * scale
+        s = np.where(np.tril(np.ones((n, n), bool))[None], s, -np.inf)
+        s -= s.max(axis=-1, keepdims=True)
+        p = np.exp(s)
+        p /= p.sum(axis=-1, keepdims=True)
+        out[s0:s0 + n] = np.matmul(p, vs).transpose(1, 0, 2)
+        s0 += n
+    return out

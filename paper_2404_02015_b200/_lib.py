@@ -101,6 +101,7 @@ _SIGS = {
     "mux_decode_attention_headwise": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,
                                                 C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int,
                                                 vp, sz, vp]),
+    "mux_prefill_attention": (C.c_int, [vp, vp, vp, P(i32), C.c_int, C.c_int, vp]),
     "mux_kv_append": (C.c_int, [vp, vp, vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,
                                 C.c_int, C.c_int, C.c_int, vp]),
     "mux_rope_table": (C.c_int, [C.c_int, P(f32)]),

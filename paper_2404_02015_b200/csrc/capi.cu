@@ -471,6 +471,50 @@ int mux_decode_attention_headwise(const void* q, const void* pool, const int32_t
   });
 }
 
+int mux_prefill_attention(const void* q, const void* qkv, void* out, const int32_t* seq_lens, int nseq, int H,
+                          void* stream) {
+  return guarded([&] {
+    require(nseq > 0 && H > 0 && seq_lens != nullptr, "prefill attention: bad shape");
+    std::vector<int32_t> meta(nseq + 1, 0);
+    int T = 0, max_qt = 0;
+    for (int i = 0; i < nseq; ++i) {
+      require(seq_lens[i] > 0, "prefill attention: empty sequence");
+      meta[i] = T;
+      T += seq_lens[i];
+      max_qt = std::max(max_qt, (seq_lens[i] - 1) / 128);
+    }
+    meta[nseq] = T;
+    require(nseq < 65536 && max_qt < 65536, "prefill attention: too many sequences");
+    for (int qt = max_qt; qt >= 0; --qt)
+      for (int i = 0; i < nseq; ++i)
+        if (qt * 128 < seq_lens[i]) meta.push_back((i << 16) | qt);
+    const int n_tiles = static_cast<int>(meta.size()) - (nseq + 1);
+    cudaStream_t s = static_cast<cudaStream_t>(stream);
+    static mux::DevMem& d = *new mux::DevMem();  // grows; the call synchronises before returning
+    if (d.bytes < meta.size() * 4) d = mux::DevMem(std::max<size_t>(meta.size() * 4, 1 << 16));
+    mux::check_cuda(cudaMemcpyAsync(d.p, meta.data(), meta.size() * 4, cudaMemcpyHostToDevice, s), "meta");
+    alignas(64) unsigned char tq[128], tkv[128];
+    if (!mux::make_tmap_bf16(tq, q, T, static_cast<uint64_t>(H) * 128, static_cast<uint64_t>(H) * 256, 128) ||
+        !mux::make_tmap_bf16(tkv, qkv, T, static_cast<uint64_t>(3 * H) * 128, static_cast<uint64_t>(3 * H) * 256, 128))
+      throw std::runtime_error("prefill attention: tensor map encode failed");
+    mux::PrefillAttnArgs a{};
+    a.q = q;
+    a.qkv = qkv;
+    a.out = out;
+    a.seq_start = d.as<int32_t>();
+    a.tiles = d.as<int32_t>() + nseq + 1;
+    a.tmap_q = tq;
+    a.tmap_qkv = tkv;
+    a.n_tiles = n_tiles;
+    a.nseq = nseq;
+    a.H = H;
+    a.T = T;
+    a.scale_log2 = 1.4426950408889634f / std::sqrt(128.f);
+    mux::check_cuda(mux::prefill_attention(a, s), "prefill_attention");
+    mux::check_cuda(cudaStreamSynchronize(s), "prefill_attention sync");
+  });
+}
+
 int mux_kv_append(const void* qkv, void* q_out, void* pool, const int32_t* rowrec, const int32_t* rowlist,
                   const int32_t* tok_slot, const int32_t* tok_pos, const float* rope, int rope_positions, int T,
                   int H, int num_layers, int layer, int max_rows, void* stream) {

@@ -534,6 +534,14 @@ void Runtime::prefill(Llama& m, Workspace& ws, int n, const int32_t* slots_host,
     h[7 * cap + 1 + i] = t - 1;
   }
   h[5 * cap + n] = T;
+  // K3 work list: (sequence, 128-query tile), longest causal row first.
+  int n_tiles = 0;
+  int32_t* tiles = h + 2 * cap;
+  int max_qt = 0;
+  for (int i = 0; i < n; ++i) max_qt = std::max(max_qt, (lens_host[i] - 1) / 128);
+  for (int qt = max_qt; qt >= 0; --qt)
+    for (int i = 0; i < n; ++i)
+      if (qt * 128 < lens_host[i]) tiles[n_tiles++] = (i << 16) | qt;
   ws.stage_commit(8 * static_cast<size_t>(cap) + 8, stream);
 
   const int hid = d.hidden, H = d.heads, L = d.layers;
@@ -559,6 +567,11 @@ void Runtime::prefill(Llama& m, Workspace& ws, int n, const int32_t* slots_host,
   pa.qkv = ws.qkv.p;
   pa.out = ws.attn.p;
   pa.seq_start = ws.seq_start;
+  pa.tiles = ws.ctx;  // staged above
+  const int view_rows = std::max(cap, 256);
+  pa.tmap_q = act_tmap(ws.q.p, view_rows, H * 128, 128);
+  pa.tmap_qkv = act_tmap(ws.qkv.p, view_rows, 3 * H * 128, 128);
+  pa.n_tiles = n_tiles;
   pa.nseq = n;
   pa.H = H;
   pa.T = T;

@@ -1,7 +1,6 @@
 // K5: the small LLaMA ops around the GEMMs, fused where a pass over the
-// activations is needed anyway: embedding + RMSNorm, split-K reduction +
-// residual add + RMSNorm, row argmax (greedy sampling), row gather, a
-// causal varlen prefill attention (CUDA cores, v1), and deterministic weight
+// activations is needed anyway: embedding + RMSNorm, residual RMSNorm, row
+// argmax (greedy sampling), row gather, and deterministic weight
 // initialisation. All HBM-bound; one CTA per token row.
 #include <cstdint>
 #include <cuda_bf16.h>
@@ -137,78 +136,6 @@ __global__ void gather_rows_kernel(const uint4* src, const int32_t* idx, uint4* 
   for (int i = threadIdx.x; i < vec_per_row; i += blockDim.x) dst[d + i] = src[s + i];
 }
 
-// One warp per (query token, head); keys in chunks of 32 (lane = key for the
-// scores, lane = 4 dims for the P.V accumulation), online softmax in fp32.
-__global__ void __launch_bounds__(128) prefill_attention_kernel(const PrefillAttnArgs a) {
-  __shared__ float qs[4][128];
-  grid_dep_wait();
-  grid_dep_launch();
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int gw = blockIdx.x * 4 + warp;
-  if (gw >= a.T * a.H) return;
-  const int t = gw / a.H;
-  const int h = gw % a.H;
-  // Which sequence owns token t.
-  int lo = 0, hi = a.nseq;
-  while (hi - lo > 1) {
-    const int mid = (lo + hi) >> 1;
-    if (a.seq_start[mid] <= t) lo = mid; else hi = mid;
-  }
-  const int s0 = a.seq_start[lo];
-  const __nv_bfloat16* q = reinterpret_cast<const __nv_bfloat16*>(a.q);
-  const __nv_bfloat16* qkv = reinterpret_cast<const __nv_bfloat16*>(a.qkv);
-  for (int d = lane; d < 128; d += 32)
-    qs[warp][d] = __bfloat162float(q[(static_cast<int64_t>(t) * a.H + h) * 128 + d]) * a.scale_log2;
-  __syncwarp();
-  const int64_t tok_stride = static_cast<int64_t>(3) * a.H * 128;
-  float m = -INFINITY, l = 0.f, acc[4] = {0.f, 0.f, 0.f, 0.f};
-  for (int k0 = s0; k0 <= t; k0 += 32) {
-    const int key = k0 + lane;
-    float sc = -INFINITY;
-    if (key <= t) {
-      const uint4* kr = reinterpret_cast<const uint4*>(qkv + key * tok_stride + (a.H + h) * 128);
-      float dot = 0.f;
-#pragma unroll 4
-      for (int v = 0; v < 16; ++v) {
-        const uint4 w = kr[v];
-        const uint32_t ws[4] = {w.x, w.y, w.z, w.w};
-#pragma unroll
-        for (int k = 0; k < 4; ++k) {
-          dot = fmaf(qs[warp][v * 8 + 2 * k], bf16_lo(ws[k]), dot);
-          dot = fmaf(qs[warp][v * 8 + 2 * k + 1], bf16_hi(ws[k]), dot);
-        }
-      }
-      sc = dot;
-    }
-    float mb = sc;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) mb = fmaxf(mb, __shfl_xor_sync(0xffffffffu, mb, o));
-    const float mn = fmaxf(m, mb);
-    const float alpha = exp2f(m - mn);
-    const float p = key <= t ? exp2f(sc - mn) : 0.f;
-    float ps = p;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) ps += __shfl_xor_sync(0xffffffffu, ps, o);
-    l = l * alpha + ps;
-    m = mn;
-#pragma unroll
-    for (int k = 0; k < 4; ++k) acc[k] *= alpha;
-    const int nk = min(32, t - k0 + 1);
-    for (int j = 0; j < nk; ++j) {
-      const float pj = __shfl_sync(0xffffffffu, p, j);
-      const uint2 vv = *reinterpret_cast<const uint2*>(qkv + (k0 + j) * tok_stride + (2 * a.H + h) * 128 + lane * 4);
-      acc[0] = fmaf(pj, bf16_lo(vv.x), acc[0]);
-      acc[1] = fmaf(pj, bf16_hi(vv.x), acc[1]);
-      acc[2] = fmaf(pj, bf16_lo(vv.y), acc[2]);
-      acc[3] = fmaf(pj, bf16_hi(vv.y), acc[3]);
-    }
-  }
-  const float inv = 1.f / l;
-  __nv_bfloat16* o = reinterpret_cast<__nv_bfloat16*>(a.out) + (static_cast<int64_t>(t) * a.H + h) * 128 + lane * 4;
-  *reinterpret_cast<uint2*>(o) = make_uint2(pack_bf16(acc[0] * inv, acc[1] * inv),
-                                            pack_bf16(acc[2] * inv, acc[3] * inv));
-}
-
 __device__ __forceinline__ uint64_t splitmix64(uint64_t x) {
   x += 0x9E3779B97F4A7C15ull;
   x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
@@ -263,12 +190,6 @@ cudaError_t gather_rows_bf16(const void* src, const int32_t* idx, void* dst, int
   if (n <= 0) return cudaSuccess;
   return launch(gather_rows_kernel, dim3(n), dim3(128), 0, stream, reinterpret_cast<const uint4*>(src), idx,
                 reinterpret_cast<uint4*>(dst), cols / 8);
-}
-
-cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
-  if (a.T <= 0) return cudaSuccess;
-  const int warps = a.T * a.H;
-  return launch(prefill_attention_kernel, dim3((warps + 3) / 4), dim3(128), 0, stream, a);
 }
 
 cudaError_t init_normal_bf16(void* dst, int64_t n, uint64_t seed, float std, cudaStream_t stream) {

@@ -102,16 +102,20 @@ cudaError_t argmax_rows(const float* logits, int T, int V, int32_t* out, cudaStr
 // Gather rows: dst[i] = src[idx[i]] (bf16 rows of `cols`).
 cudaError_t gather_rows_bf16(const void* src, const int32_t* idx, void* dst, int n, int cols,
                              cudaStream_t stream);
-// Causal varlen prefill attention over the fresh q/k/v (fp32 math).
+// ---- K3 causal varlen prefill attention (tcgen05 flash attention) ---------
 struct PrefillAttnArgs {
   const void* q;            // [T][H][128] bf16 rotated
   const void* qkv;          // [T][3][H][128] bf16 (k rotated in-place by kv_append)
   void* out;                // [T][H][128] bf16
   const int32_t* seq_start; // [nseq + 1]
-  int nseq, H, T;
+  const int32_t* tiles;     // [n_tiles] (seq << 16) | q_tile, heaviest (largest q_tile) first
+  const void* tmap_q;       // make_tmap_bf16(q, T, H*128, .., box_rows 128)   (host memory)
+  const void* tmap_qkv;     // make_tmap_bf16(qkv, T, 3*H*128, .., box_rows 128)
+  int n_tiles, nseq, H, T;
   float scale_log2;
 };
 cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream);
+size_t prefill_attention_smem();
 // Deterministic N(0, std) init of a bf16 buffer from (seed, index).
 cudaError_t init_normal_bf16(void* dst, int64_t n, uint64_t seed, float std, cudaStream_t stream);
 cudaError_t fill_f32(float* dst, int64_t n, float v, cudaStream_t stream);

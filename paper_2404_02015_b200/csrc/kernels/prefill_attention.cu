@@ -1,0 +1,293 @@
+// K3: causal varlen prefill attention on the 5th-generation tensor cores.
+//
+// Work it replaces: the attention part of prefill_latency
+// (/root/reference/proj/src/cost_model.cpp:75-83) -- causal softmax(q k^T /
+// sqrt(128)) v over every prompt of a prefill job, head_dim 128, after
+// kv_append has rotated q and k (RoPE) and written k/v into the head-blocks
+// (the K/V read here are the same bytes, straight from the QKV GEMM output).
+//
+// One CTA = (128-query tile of one sequence, head). Flash-attention over
+// 128-key tiles with both contractions on tcgen05:
+//   S_j = Q K_j^T      UMMA 128x128x128, A = Q (smem, K-major), B = K_j (smem,
+//                      K-major), fp32 accumulator in TMEM (double-buffered so
+//                      S_{j+1} is computed while the softmax reads S_j)
+//   O_j = P_j V_j      UMMA 128x128x128, A = P_j (bf16, written to smem by the
+//                      softmax in the canonical SW128 K-major image), B = V_j
+//                      (smem, MN-major: the same TMA box as K, other descriptor)
+// Warp 4 = TMA producer + MMA issuer (one elected lane); warps 0-3 = softmax,
+// thread i owns query row i (TMEM lane i): online max/sum in fp32, causal +
+// sequence-end masking. The output accumulates in TMEM across key tiles; when
+// a row's max moves, its O row is rescaled in place (tcgen05.ld/st) before
+// the next P V is issued.
+// K/V tiles stream through a 2-stage TMA ring (SWIZZLE_128B boxes of 64 dims
+// x 128 tokens over the [T][3][H][128] QKV buffer).
+// FLOPs per (sequence of length n, head): 4 * 128 * n * (n + 1) / 2 (causal).
+#include <cuda.h>
+#include <cuda_bf16.h>
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstring>
+
+#include "kernels.h"
+#include "launch.cuh"
+#include "ptx.cuh"
+
+namespace mux {
+namespace {
+
+constexpr int kTile = 128;                   // queries per CTA, keys per KV tile
+constexpr int kHalfBytes = kTile * 64 * 2;   // one 64-dim SW128 half of a tile: 16 KiB
+constexpr int kTileBytes = 2 * kHalfBytes;   // 128 x 128 bf16
+constexpr int kStages = 2;
+constexpr int kThreads = 160;                // 4 softmax warps + 1 TMA/MMA warp
+constexpr uint32_t kTmemCols = 512;          // S0 [0,128) S1 [128,256) O [256,384)
+constexpr size_t kSmemBytes = 1024 + kTileBytes /*Q*/ + kStages * 2 * kTileBytes /*K,V*/ +
+                              kTileBytes /*P*/ + 256 /*barriers*/;
+
+struct Bars {
+  uint64_t q_full;
+  uint64_t kv_full[kStages];
+  uint64_t kv_empty[kStages];
+  uint64_t s_full[2];
+  uint64_t s_empty[2];
+  uint64_t p_full;
+  uint64_t o_full;
+  uint32_t tmem;
+};
+
+// MN-major SW128 descriptor (B = V: N = head dims contiguous, K = keys):
+// 8-key groups 1024 B apart (SBO), the second 64-dim half 16 KiB away (LBO).
+__device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr) {
+  uint64_t d = 0;
+  d |= static_cast<uint64_t>((smem_addr >> 4) & 0x3FFF);
+  d |= static_cast<uint64_t>(kHalfBytes >> 4) << 16;  // LBO: next 64-wide MN atom column
+  d |= static_cast<uint64_t>(1024 >> 4) << 32;        // SBO: next 8-row group along K
+  d |= static_cast<uint64_t>(1) << 46;
+  d |= static_cast<uint64_t>(2) << 61;
+  return d;
+}
+
+__global__ void __launch_bounds__(kThreads, 1)
+prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv,
+                         const PrefillAttnArgs a) {
+  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
+  uint8_t* q_s = base;
+  uint8_t* kv_s = q_s + kTileBytes;                 // [stage][K|V][2 halves]
+  uint8_t* p_s = kv_s + kStages * 2 * kTileBytes;   // [2 halves][128 rows][128 B]
+  Bars& bar = *reinterpret_cast<Bars*>(p_s + kTileBytes);
+
+  const int h = blockIdx.x;
+  const int tile = a.tiles[blockIdx.y];
+  const int seq = tile >> 16, qt = tile & 0xFFFF;
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    mbar_init(&bar.q_full, 1);
+    for (int s = 0; s < kStages; ++s) {
+      mbar_init(&bar.kv_full[s], 1);
+      mbar_init(&bar.kv_empty[s], 1);
+    }
+    for (int s = 0; s < 2; ++s) {
+      mbar_init(&bar.s_full[s], 1);
+      mbar_init(&bar.s_empty[s], 4);
+    }
+    mbar_init(&bar.p_full, 4);
+    mbar_init(&bar.o_full, 1);
+    fence_barrier_init();
+  }
+  if (warp == 0) tmem_alloc<kTmemCols>(&bar.tmem);
+  tc_fence_before();
+  __syncthreads();
+  tc_fence_after();
+  grid_dep_wait();  // q / k / v come from kv_append and the QKV GEMM
+  if (threadIdx.x == 0) grid_dep_launch();
+  const uint32_t tmem = bar.tmem;
+
+  const int s0 = a.seq_start[seq];
+  const int len = a.seq_start[seq + 1] - s0;
+  const int q0 = qt * kTile;                // sequence-local index of query row 0
+  const int n_kv = qt + 1;                  // causal: key tiles 0..qt
+
+  if (warp == 4) {
+    if (elect_one()) {
+      // ---------------- TMA producer + MMA issuer
+      const uint64_t pol_q = policy_evict_first();
+      const uint64_t pol_kv = policy_evict_last();  // re-read by the other q tiles of this head
+      mbar_arrive_expect_tx(&bar.q_full, kTileBytes);
+      for (int hh = 0; hh < 2; ++hh)
+        tma_load_2d(q_s + hh * kHalfBytes, &tq, &bar.q_full, h * 128 + hh * 64, s0 + q0, pol_q);
+      auto load_kv = [&](int j) {
+        const int st = j % kStages;
+        if (j >= kStages) mbar_wait(&bar.kv_empty[st], ((j / kStages) - 1) & 1);
+        uint8_t* dst = kv_s + st * 2 * kTileBytes;
+        mbar_arrive_expect_tx(&bar.kv_full[st], 2 * kTileBytes);
+        for (int hh = 0; hh < 2; ++hh) {
+          tma_load_2d(dst + hh * kHalfBytes, &tkv, &bar.kv_full[st], (a.H + h) * 128 + hh * 64,
+                      s0 + j * kTile, pol_kv);
+          tma_load_2d(dst + kTileBytes + hh * kHalfBytes, &tkv, &bar.kv_full[st],
+                      (2 * a.H + h) * 128 + hh * 64, s0 + j * kTile, pol_kv);
+        }
+      };
+      const uint32_t idesc_qk = umma_idesc_bf16(kTile, kTile);
+      const uint32_t idesc_pv = umma_idesc_bf16(kTile, 128) | (1u << 16);  // B (V) MN-major
+      const uint32_t q_addr = smem_u32(q_s), p_addr = smem_u32(p_s);
+      auto issue_qk = [&](int j) {
+        const int st = j % kStages, sb = j & 1;
+        mbar_wait(&bar.kv_full[st], (j / kStages) & 1);
+        if (j >= 2) mbar_wait(&bar.s_empty[sb], ((j >> 1) - 1) & 1);
+        tc_fence_after();
+        const uint32_t k_addr = smem_u32(kv_s + st * 2 * kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
+          umma_bf16(tmem + sb * kTile, umma_desc_sw128(q_addr + off), umma_desc_sw128(k_addr + off), idesc_qk,
+                    kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&bar.s_full[sb]);
+      };
+      load_kv(0);
+      if (n_kv > 1) load_kv(1);
+      mbar_wait(&bar.q_full, 0);
+      issue_qk(0);
+      for (int j = 0; j < n_kv; ++j) {
+        if (j + 1 < n_kv) issue_qk(j + 1);
+        // O_j = P_j V_j once the softmax has written P_j
+        mbar_wait(&bar.p_full, j & 1);
+        tc_fence_after();
+        const int st = j % kStages;
+        const uint32_t v_addr = smem_u32(kv_s + st * 2 * kTileBytes + kTileBytes);
+#pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          umma_bf16(tmem + 2 * kTile, umma_desc_sw128(p_addr + (kk >> 2) * kHalfBytes + (kk & 3) * 32),
+                    umma_desc_sw128_mn(v_addr + kk * 2048), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+        }
+        umma_commit(&bar.o_full);
+        umma_commit(&bar.kv_empty[st]);
+        if (j + kStages < n_kv) load_kv(j + kStages);
+      }
+    }
+    __syncwarp();
+  } else {
+    // ---------------- softmax warps: thread = query row
+    const int row = warp * 32 + lane;
+    const int qi = q0 + row;               // sequence-local query index
+    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    float m_run = -INFINITY, l_run = 0.f;
+    uint8_t* p_row = p_s + row * 128;
+    const uint32_t o_addr = tmem + lane_base + 2 * kTile;
+    for (int j = 0; j < n_kv; ++j) {
+      const int sb = j & 1;
+      mbar_wait(&bar.s_full[sb], (j >> 1) & 1);
+      tc_fence_after();
+      const uint32_t s_addr = tmem + lane_base + sb * kTile;
+      const int kmax = min(qi, len - 1) - j * kTile;  // keys [0, kmax] of this tile are visible
+      // pass 1: row max
+      float mx = -INFINITY;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float v[32];
+        tmem_ld_32x32b_x32(s_addr + c * 32, v);
+#pragma unroll
+        for (int i = 0; i < 32; ++i)
+          if (c * 32 + i <= kmax) mx = fmaxf(mx, v[i]);
+      }
+      const float m_new = fmaxf(m_run, mx * a.scale_log2);
+      const float m_use = m_new == -INFINITY ? 0.f : m_new;
+      const float alpha = exp2f(m_run - m_use);
+      if (j > 0) {
+        // P_{j-1} V_{j-1} complete: the P buffer is free and O may be rescaled
+        mbar_wait(&bar.o_full, (j - 1) & 1);
+        tc_fence_after();
+        if (!__all_sync(0xffffffffu, alpha == 1.f)) {
+#pragma unroll 1
+          for (int c = 0; c < 4; ++c) {
+            float v[32];
+            tmem_ld_32x32b_x32(o_addr + c * 32, v);
+#pragma unroll
+            for (int i = 0; i < 32; ++i) v[i] *= alpha;
+            tmem_st_32x32b_x32(o_addr + c * 32, v);
+          }
+        }
+      }
+      // pass 2: P = exp2(s - m) -> bf16 in the SW128 K-major image
+      float psum = 0.f;
+#pragma unroll
+      for (int c = 0; c < 4; ++c) {
+        float v[32];
+        tmem_ld_32x32b_x32(s_addr + c * 32, v);
+        uint32_t pk[16];
+#pragma unroll
+        for (int i = 0; i < 32; i += 2) {
+          const float p0 = c * 32 + i <= kmax ? exp2f(fmaf(v[i], a.scale_log2, -m_use)) : 0.f;
+          const float p1 = c * 32 + i + 1 <= kmax ? exp2f(fmaf(v[i + 1], a.scale_log2, -m_use)) : 0.f;
+          psum += p0 + p1;
+          pk[i >> 1] = pack_bf16(p0, p1);
+        }
+        // keys [32c, 32c+32): half c/2, 16-byte chunks (c%2)*4 .. +4
+        uint8_t* half = p_row + (c >> 1) * kHalfBytes;
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+          const int chunk = (c & 1) * 4 + u;
+          *reinterpret_cast<uint4*>(half + ((chunk ^ (row & 7)) << 4)) =
+              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+        }
+      }
+      l_run = l_run * alpha + psum;
+      m_run = m_new;
+      tc_fence_before();
+      fence_async_smem();  // P (generic writes) -> the tensor core (async proxy)
+      __syncwarp();
+      if (lane == 0) {
+        mbar_arrive(&bar.s_empty[sb]);
+        mbar_arrive(&bar.p_full);
+      }
+    }
+    mbar_wait(&bar.o_full, (n_kv - 1) & 1);
+    tc_fence_after();
+    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) +
+                                          (static_cast<int64_t>(s0 + qi) * a.H + h) * 128);
+#pragma unroll
+    for (int c = 0; c < 4; ++c) {
+      float v[32];
+      tmem_ld_32x32b_x32(o_addr + c * 32, v);  // all lanes: .sync.aligned
+      if (qi < len) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u)
+          dst[c * 4 + u] = make_uint4(pack_bf16(v[8 * u] * inv, v[8 * u + 1] * inv),
+                                      pack_bf16(v[8 * u + 2] * inv, v[8 * u + 3] * inv),
+                                      pack_bf16(v[8 * u + 4] * inv, v[8 * u + 5] * inv),
+                                      pack_bf16(v[8 * u + 6] * inv, v[8 * u + 7] * inv));
+      }
+    }
+  }
+  tc_fence_before();
+  __syncthreads();
+  if (warp == 0) {
+    tc_fence_after();
+    tmem_dealloc(tmem, kTmemCols);
+  }
+}
+
+}  // namespace
+
+size_t prefill_attention_smem() { return kSmemBytes; }
+
+cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
+  if (a.T <= 0 || a.n_tiles <= 0) return cudaSuccess;
+  static bool configured = false;
+  if (!configured) {
+    cudaError_t e = cudaFuncSetAttribute(prefill_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                         static_cast<int>(kSmemBytes));
+    if (e != cudaSuccess) return e;
+    configured = true;
+  }
+  CUtensorMap tq, tkv;
+  std::memcpy(&tq, a.tmap_q, sizeof(CUtensorMap));
+  std::memcpy(&tkv, a.tmap_qkv, sizeof(CUtensorMap));
+  return launch(prefill_attention_kernel, dim3(a.H, a.n_tiles), dim3(kThreads), kSmemBytes, stream, tq, tkv, a);
+}
+
+}  // namespace mux

@@ -430,6 +430,14 @@ def decode_attention_headwise(q, pool_ptr, rowrec_ptr, rowlist_ptr, slots, ctx, 
         kv_splits, _ptr(workspace), ws_bytes, _ptr(stream)))
 
 
+def prefill_attention(q, qkv, out, seq_lens, stream=None):
+    """K3 (tcgen05): causal attention of each prompt; q/qkv/out torch CUDA bf16
+    tensors [T,H,128] / [T,3,H,128] / [T,H,128]; seq_lens host ints."""
+    lens = (C.c_int32 * len(seq_lens))(*seq_lens)
+    check(lib.mux_prefill_attention(_ptr(q), _ptr(qkv), _ptr(out), lens, len(seq_lens), q.shape[1],
+                                    _ptr(stream)))
+
+
 def kv_append(qkv, q_out, pool_ptr, rowrec_ptr, rowlist_ptr, tok_slot, tok_pos, rope, T: int, H: int,
               num_layers: int, layer: int, max_rows: int, stream=None):
     check(lib.mux_kv_append(_ptr(qkv), _ptr(q_out), _ptr(pool_ptr), _ptr(rowrec_ptr),
