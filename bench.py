@@ -134,7 +134,8 @@ def run_ours(args, rank, world, local_rank):
     max_ctx = max(p + d + steps_total + 1 for reqs in batches for p, o, d in reqs)
     unit = mux.Unit(specs, pool_blocks=logical, device=local_rank, device_pool_blocks=need + 4096,
                     max_batch=B, max_prefill_tokens=256, max_ctx=max_ctx + 16, max_slots=2 * B + 16,
-                    init_seed=1 + rank, init_std=0.02, partitions=len(specs) + 1)
+                    init_seed=1 + rank, init_std=0.02, partitions=len(specs) + 1,
+                    partition_sms=[0] + args.partition_sms if args.partition_sms else None)
     unit.set_option("pdl", args.pdl)
     unit.init_kv(seed=7 + rank, std=1.0)
     pool = unit.pool
@@ -231,6 +232,8 @@ def main():
     ap.add_argument("--models", default="7b,13b")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--attn-steps", type=int, default=2, help="steps with per-launch K1 events")
+    ap.add_argument("--partition-sms", type=lambda s: [int(x) for x in s.split(",")], default=None,
+                    help="green-context SMs of each model's decode partition, e.g. 72,72")
     ap.add_argument("--serial", action="store_true", help="run the colocated decode jobs on one stream")
     ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch between job kernels")
     ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg (profiling runs)")

@@ -213,6 +213,12 @@ typedef struct {
   uint64_t init_seed;           /* random N(0, init_std) weights; 0 = leave for set_tensor */
   float init_std;
   int partitions;               /* concurrent job streams */
+  /* SM partitions (P1, the spatial multiplexing of scheduler.cpp:50-54 /
+   * sim_engine.cpp:16-18): partition_sms[p] > 0 gives partition p its own
+   * green context with that many SMs (rounded up to the hardware granule),
+   * carved disjointly in order; <= 0 or a NULL array = a plain stream over
+   * all SMs. Kernels size their persistent grids to their partition. */
+  const int* partition_sms;
 } mux_unit_config;
 
 MUX_API int mux_unit_create(const mux_unit_config* cfg, mux_unit** out);
@@ -252,6 +258,11 @@ MUX_API int mux_unit_elapsed(mux_unit* unit, int slot_a, int slot_b, float* ms);
  * enable, then read the summed kernel milliseconds and launch count. */
 MUX_API int mux_unit_attn_timing(mux_unit* unit, int enable);
 MUX_API int mux_unit_attn_time(mux_unit* unit, double* total_ms, int64_t* launches, double* bytes);
+/* SMs of a partition (its green context's, or the device's). */
+MUX_API int mux_unit_partition_sms(mux_unit* unit, int partition, int* sms);
+/* Debug: launch `blocks` CTAs on a partition and record each CTA's %smid
+ * into out (host, [blocks]); synchronises. Proves partition disjointness. */
+MUX_API int mux_unit_probe_smids(mux_unit* unit, int partition, int blocks, int* out);
 /* Kernel launches issued by this unit so far (all libmux kernels). */
 MUX_API int64_t mux_unit_launches(mux_unit* unit);
 /* Tuning knobs: "gemm_min_iters" (k-blocks per GEMM CTA, default 24);

@@ -75,7 +75,8 @@ class UnitConfig(C.Structure):
     _fields_ = [("device", C.c_int), ("n_llms", C.c_int), ("llms", P(LlmEntry)),
                 ("pool_blocks", i64), ("device_pool_blocks", i64), ("max_batch", C.c_int),
                 ("max_prefill_tokens", C.c_int), ("max_ctx", C.c_int), ("max_slots", C.c_int),
-                ("init_seed", u64), ("init_std", f32), ("partitions", C.c_int)]
+                ("init_seed", u64), ("init_std", f32), ("partitions", C.c_int),
+                ("partition_sms", P(C.c_int))]
 
 
 _SIGS = {
@@ -108,6 +109,8 @@ _SIGS = {
     "mux_gemm_bf16": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp]),
     "mux_weight_tile": (C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp]),
     "mux_weight_tiled_bytes": (i64, [C.c_int, C.c_int]),
+    "mux_unit_partition_sms": (C.c_int, [vp, C.c_int, P(C.c_int)]),
+    "mux_unit_probe_smids": (C.c_int, [vp, C.c_int, C.c_int, P(C.c_int)]),
     "mux_unit_set_option": (C.c_int, [vp, C.c_char_p, i64]),
     "mux_debug_gemm_timing": (None, [vp]),
     "mux_unit_create": (C.c_int, [P(UnitConfig), P(vp)]),

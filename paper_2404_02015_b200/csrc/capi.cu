@@ -2,6 +2,7 @@
 // lockstep JobExecutor that runs the engine's JobPlans on the GPU.
 #include "../../include/mux.h"
 
+#include <cuda.h>
 #include <cuda_runtime.h>
 
 #include <algorithm>
@@ -20,6 +21,48 @@
 #include "mux/kv.hpp"
 
 using muxsim::BlockPool;
+
+namespace {
+void check_cu(CUresult r, const char* what) {
+  if (r != CUDA_SUCCESS)
+    throw std::runtime_error(std::string("cuda driver error in ") + what + ": CUresult " + std::to_string(r));
+}
+
+// Driver entry points, resolved through the runtime so libmux.so loads on a
+// host without libcuda (the CPU test suite only needs the control plane).
+template <typename F>
+F driver_fn(const char* name) {
+  void* p = nullptr;
+  cudaDriverEntryPointQueryResult q;
+  if (cudaGetDriverEntryPoint(name, &p, cudaEnableDefault, &q) != cudaSuccess || q != cudaDriverEntryPointSuccess)
+    throw std::runtime_error(std::string("driver entry point unavailable: ") + name);
+  return reinterpret_cast<F>(p);
+}
+struct GreenApi {
+  decltype(&cuDeviceGet) device_get = driver_fn<decltype(&cuDeviceGet)>("cuDeviceGet");
+  decltype(&cuDeviceGetDevResource) get_resource = driver_fn<decltype(&cuDeviceGetDevResource)>("cuDeviceGetDevResource");
+  decltype(&cuDevSmResourceSplitByCount) split =
+      driver_fn<decltype(&cuDevSmResourceSplitByCount)>("cuDevSmResourceSplitByCount");
+  decltype(&cuDevResourceGenerateDesc) gen_desc = driver_fn<decltype(&cuDevResourceGenerateDesc)>("cuDevResourceGenerateDesc");
+  decltype(&cuGreenCtxCreate) create = driver_fn<decltype(&cuGreenCtxCreate)>("cuGreenCtxCreate");
+  decltype(&cuGreenCtxStreamCreate) stream_create = driver_fn<decltype(&cuGreenCtxStreamCreate)>("cuGreenCtxStreamCreate");
+  decltype(&cuGreenCtxDestroy) destroy = driver_fn<decltype(&cuGreenCtxDestroy)>("cuGreenCtxDestroy");
+};
+GreenApi& green_api() {
+  static GreenApi* api = new GreenApi();
+  return *api;
+}
+
+// Each CTA records the SM it ran on (and lingers so the grid spreads out).
+__global__ void probe_smid_kernel(int* out) {
+  unsigned smid;
+  asm volatile("mov.u32 %0, %%smid;" : "=r"(smid));
+  const long long t0 = clock64();
+  while (clock64() - t0 < 200000) {
+  }
+  if (threadIdx.x == 0) out[blockIdx.x] = static_cast<int>(smid);
+}
+}  // namespace
 
 struct mux_pool {
   BlockPool* bp = nullptr;
@@ -176,6 +219,8 @@ struct mux_unit {
   std::vector<std::unique_ptr<mux::Llama>> models;
   mux_pool pool;
   std::vector<cudaStream_t> streams;
+  std::vector<CUgreenCtx> green;  // one per SM-partitioned stream (nullptr = whole device)
+  std::vector<int> sms;           // SMs each partition may use
   std::vector<std::unique_ptr<mux::Workspace>> ws;
   cudaEvent_t ev[64] = {};
   bool timing = false;
@@ -186,6 +231,8 @@ struct mux_unit {
     if (rt) cudaDeviceSynchronize();
     ws.clear();
     for (cudaStream_t s : streams) cudaStreamDestroy(s);
+    for (CUgreenCtx g : green)
+      if (g) green_api().destroy(g);
     for (cudaEvent_t e : ev)
       if (e) cudaEventDestroy(e);
   }
@@ -646,13 +693,77 @@ int mux_unit_create(const mux_unit_config* cfg, mux_unit** out) {
       heads = std::max(heads, d.heads);
     }
     const int P = std::max(1, cfg->partitions);
+    // Green-context SM partitions: the device's SMs are split once into
+    // 8-SM granules (the sm_100 partition granularity; on B200 that yields
+    // 15 symmetric granules = 120 SMs plus a 28-SM remainder outside the
+    // symmetric set); partition p takes the next ceil(want/8) granules, the
+    // remainder joins the first partition that runs out of granules (else the
+    // last green partition), so partitions are disjoint by construction.
+    std::vector<CUdevResource> granules;
+    CUdevResource remainder{};
+    bool remainder_free = false;
+    size_t next_granule = 0;
+    int last_green = -1;
+    if (cfg->partition_sms != nullptr) {
+      bool any = false;
+      for (int p = 0; p < P; ++p) any = any || cfg->partition_sms[p] > 0;
+      if (any) {
+        GreenApi& ga = green_api();
+        CUdevice dev = 0;
+        CUdevResource all{};
+        check_cu(ga.device_get(&dev, cfg->device), "cuDeviceGet");
+        check_cu(ga.get_resource(dev, &all, CU_DEV_RESOURCE_TYPE_SM), "cuDeviceGetDevResource");
+        unsigned int nb = 0;
+        check_cu(ga.split(nullptr, &nb, &all, nullptr, 0, 8), "cuDevSmResourceSplitByCount(query)");
+        granules.resize(nb);
+        check_cu(ga.split(granules.data(), &nb, &all, &remainder, 0, 8), "cuDevSmResourceSplitByCount");
+        granules.resize(nb);
+        remainder_free = remainder.sm.smCount > 0;
+        for (int p = 0; p < P; ++p)
+          if (cfg->partition_sms[p] > 0) last_green = p;
+      }
+    }
     for (int p = 0; p < P; ++p) {
+      const int want = cfg->partition_sms ? cfg->partition_sms[p] : 0;
       cudaStream_t s;
-      mux::check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+      CUgreenCtx g = nullptr;
+      int sms = u->rt->num_sms();
+      if (want > 0) {
+        GreenApi& ga = green_api();
+        int take = 0, got = 0;
+        while (got < want && next_granule + take < granules.size()) got += granules[next_granule + take++].sm.smCount;
+        std::vector<CUdevResource> parts(granules.begin() + next_granule, granules.begin() + next_granule + take);
+        if (remainder_free && (got < want || p == last_green)) {
+          parts.push_back(remainder);
+          got += remainder.sm.smCount;
+          remainder_free = false;
+        }
+        if (got < want) {
+          std::string sizes;
+          for (const CUdevResource& r : granules) sizes += " " + std::to_string(r.sm.smCount);
+          throw std::invalid_argument("partition_sms: not enough SMs left for partition " + std::to_string(p) +
+                                      " (granules:" + sizes + ")");
+        }
+        CUdevResourceDesc desc;
+        check_cu(ga.gen_desc(&desc, parts.data(), static_cast<unsigned>(parts.size())), "cuDevResourceGenerateDesc");
+        next_granule += take;
+        CUdevice dev = 0;
+        check_cu(ga.device_get(&dev, cfg->device), "cuDeviceGet");
+        check_cu(ga.create(&g, desc, dev, CU_GREEN_CTX_DEFAULT_STREAM), "cuGreenCtxCreate");
+        CUstream cs;
+        check_cu(ga.stream_create(&cs, g, CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate");
+        s = reinterpret_cast<cudaStream_t>(cs);
+        sms = got;
+      } else {
+        mux::check_cuda(cudaStreamCreateWithFlags(&s, cudaStreamNonBlocking), "stream");
+      }
       u->streams.push_back(s);
+      u->green.push_back(g);
+      u->sms.push_back(sms);
       const int max_tok = std::max(u->max_prefill, u->max_batch);
       u->ws.push_back(std::make_unique<mux::Workspace>(max_tok, std::max(u->max_batch, 256), hid, qkv, ffn, vocab,
                                                        heads, u->max_batch, u->rt->num_sms()));
+      u->ws.back()->sms = sms;
     }
     for (auto& e : u->ev) mux::check_cuda(cudaEventCreate(&e), "event");
     mux::check_cuda(cudaDeviceSynchronize(), "unit create");
@@ -771,6 +882,25 @@ int mux_unit_attn_time(mux_unit* u, double* total_ms, int64_t* launches, double*
 }
 
 int64_t mux_unit_launches(mux_unit* u) { return u ? u->rt->launches() : -1; }
+
+int mux_unit_partition_sms(mux_unit* u, int partition, int* sms) {
+  return guarded([&] {
+    u->stream(partition);
+    *sms = u->sms[partition];
+  });
+}
+
+int mux_unit_probe_smids(mux_unit* u, int partition, int blocks, int* out) {
+  return guarded([&] {
+    require(blocks > 0, "probe: blocks must be positive");
+    cudaStream_t s = u->stream(partition);
+    mux::DevMem d(static_cast<size_t>(blocks) * 4);
+    probe_smid_kernel<<<blocks, 32, 0, s>>>(d.as<int>());
+    mux::check_cuda(cudaGetLastError(), "probe");
+    mux::check_cuda(cudaMemcpyAsync(out, d.p, static_cast<size_t>(blocks) * 4, cudaMemcpyDeviceToHost, s), "probe copy");
+    mux::check_cuda(cudaStreamSynchronize(s), "probe sync");
+  });
+}
 
 int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
   return guarded([&] {

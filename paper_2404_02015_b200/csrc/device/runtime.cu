@@ -327,7 +327,7 @@ void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void
   g.partials = ws.gemm_partials.as<float>();
   g.flags = ws.gemm_flags.as<int>();
   g.epoch = ++ws.gemm_epoch;
-  g.grid = num_sms_;
+  g.grid = ws.sms;  // persistent grid = the partition's SMs
   g.min_iters = gemm_min_iters_;
   g.M = M;
   g.N = N;
@@ -450,7 +450,7 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   const int max_rows_req = (max_ctx + 15) / 16;
   // KV splits: enough CTAs to fill the GPU a few times over.
   int splits = 1;
-  while (splits < 16 && n * H * splits < 4 * num_sms_ && (max_rows_req + splits * 2 - 1) / (splits * 2) >= 4) splits *= 2;
+  while (splits < 16 && n * H * splits < 4 * ws.sms && (max_rows_req + splits * 2 - 1) / (splits * 2) >= 4) splits *= 2;
   while ((max_rows_req + splits - 1) / splits > decode_attention_max_rows_per_split()) splits *= 2;
   at.splits = splits;
   at.rows_per_split = std::max(1, (max_rows_req + splits - 1) / splits);

@@ -96,6 +96,7 @@ struct Workspace {
   DevMem resid, xn, qkv, q, attn, act, logits, ints, attn_part_o, attn_part_ml, xlast;
   DevMem gemm_partials, gemm_flags;  // stream-K fixup scratch of this partition's GEMMs
   int gemm_epoch = 0;
+  int sms = 148;           // SMs of the partition this workspace's jobs run on
   PinnedMem host_ints[2];  // double-buffered staging for per-job metadata
   cudaEvent_t staged[2] = {nullptr, nullptr};
   int cur = 0;

@@ -312,13 +312,21 @@ class Unit:
     def __init__(self, specs: Sequence[LLMSpec], pool_blocks: int, device: int = 0,
                  device_pool_blocks: int = 0, max_batch: int = 256, max_prefill_tokens: int = 4096,
                  max_ctx: int = 4096, max_slots: int = 0, init_seed: int = 0,
-                 init_std: float = 0.02, partitions: int = 2):
+                 init_std: float = 0.02, partitions: int = 2, partition_sms: Sequence[int] | None = None):
+        """partition_sms[p] > 0 puts partition p on its own green context of
+        that many SMs (the SM share a JobPlan's sm_demand asks for)."""
         self.specs = list(specs)
         self._keep = []
         ents = (_CEntry * len(specs))(*[_c_entry(s, keep=self._keep) for s in specs])
         self._keep.append(ents)
+        psms = None
+        if partition_sms is not None:
+            if len(partition_sms) != partitions:
+                raise ValueError("partition_sms needs one entry per partition")
+            psms = (C.c_int * partitions)(*partition_sms)
+            self._keep.append(psms)
         cfg = UnitConfig(device, len(specs), ents, pool_blocks, device_pool_blocks, max_batch,
-                         max_prefill_tokens, max_ctx, max_slots, init_seed, init_std, partitions)
+                         max_prefill_tokens, max_ctx, max_slots, init_seed, init_std, partitions, psms)
         h = C.c_void_p()
         check(lib.mux_unit_create(C.byref(cfg), C.byref(h)))
         self._h = h.value
@@ -388,6 +396,16 @@ class Unit:
         ms, n, by = C.c_double(), C.c_int64(), C.c_double()
         check(lib.mux_unit_attn_time(self._h, C.byref(ms), C.byref(n), C.byref(by)))
         return ms.value, n.value, by.value
+
+    def partition_sms(self, partition: int) -> int:
+        v = C.c_int()
+        check(lib.mux_unit_partition_sms(self._h, partition, C.byref(v)))
+        return v.value
+
+    def probe_smids(self, partition: int, blocks: int):
+        out = (C.c_int * blocks)()
+        check(lib.mux_unit_probe_smids(self._h, partition, blocks, out))
+        return list(out)
 
     def launches(self) -> int:
         return int(lib.mux_unit_launches(self._h))

@@ -168,3 +168,62 @@ def lockstep_prompt(seed, rid, n, vocab):
         return x ^ (x >> 31)
 
     return np.array([mix(seed ^ mix((rid * 131071 + p) & M)) % vocab for p in range(n)], np.int32)
+
+
+@pytest.fixture(scope="module")
+def green_unit(cuda):
+    """Config 1 with SM partitions: partition 1 and 2 are disjoint green
+    contexts (the ADBS decode share decode_sm = 0.5 of 148 SMs, rounded to the
+    8-SM granule), partition 0 is the whole device."""
+    specs = [mux.spec("tiny-a"), mux.spec("tiny-b")]
+    unit = mux.Unit(specs, pool_blocks=232999, device_pool_blocks=232999, max_batch=64,
+                    max_prefill_tokens=1024, max_ctx=1024, partitions=3, partition_sms=[0, 72, 64])
+    weights = [load_weights(unit, i, s, 200 + i) for i, s in enumerate(specs)]
+    rope = llama_ref.rope_table(1024 + 16)
+    refs = [llama_ref.RefLlama(dims_of(s), w, rope) for s, w in zip(specs, weights)]
+    yield unit, specs, refs
+    unit.close()
+
+
+def test_green_partitions_are_disjoint_sm_sets(green_unit):
+    unit = green_unit[0]
+    s1, s2 = unit.partition_sms(1), unit.partition_sms(2)
+    assert s1 >= 72 and s2 >= 64 and s1 + s2 <= unit.partition_sms(0)
+    ids1, ids2 = set(unit.probe_smids(1, 4 * s1)), set(unit.probe_smids(2, 4 * s2))
+    assert ids1.isdisjoint(ids2)
+    assert len(ids1) <= s1 and len(ids2) <= s2
+    assert len(set(unit.probe_smids(0, 4 * unit.partition_sms(0)))) > s1  # partition 0 spans the device
+
+
+def test_colocated_decode_on_green_partitions(green_unit):
+    """Both models prefill and decode concurrently, each on its own SM
+    partition (spatial multiplexing, PAPER §4); tokens match the oracle."""
+    unit, specs, refs = green_unit
+    rng = np.random.default_rng(11)
+    jobs = []
+    for llm in (0, 1):
+        rids = [70000 + 100 * llm + i for i in range(6)]
+        lens = rng.integers(1, 200, len(rids)).tolist()
+        for rid, n in zip(rids, lens):
+            assert unit.pool.admit(llm, rid, n, n + 10).ok
+        prompts = [rng.integers(0, specs[llm].vocab, n).astype(np.int32) for n in lens]
+        first = np.zeros(len(rids), np.int32)
+        unit.prefill(llm, rids, np.concatenate(prompts), first, partition=llm + 1)
+        jobs.append((llm, rids, prompts, first))
+    unit.sync()
+    gens = [[[int(t)] for t in j[3]] for j in jobs]
+    outs = [np.zeros(6, np.int32), np.zeros(6, np.int32)]
+    for _ in range(10):
+        for llm, rids, _, _ in jobs:
+            for rid in rids:
+                assert unit.pool.alloc(llm, rid, 1, False).ok
+            unit.decode(llm, rids, out=outs[llm], partition=llm + 1)
+        unit.sync()
+        for llm in (0, 1):
+            for i, t in enumerate(outs[llm]):
+                gens[llm][i].append(int(t))
+    for (llm, rids, prompts, _), gen in zip(jobs, gens):
+        for i in range(len(rids)):
+            check_tokens(refs[llm], prompts[i], gen[i])
+        for rid in rids:
+            unit.pool.free_request(llm, rid)
