@@ -219,6 +219,11 @@ typedef struct {
    * carved disjointly in order; <= 0 or a NULL array = a plain stream over
    * all SMs. Kernels size their persistent grids to their partition. */
   const int* partition_sms;
+  /* Tensor parallelism over the unit's mesh: this process is
+   * rank tp_rank of tp_size; it holds heads [r*H/tp, (r+1)*H/tp) and FFN
+   * columns [r*ffn/tp, ...) of every model (H % tp == 0, ffn % tp == 0) and a
+   * pool_blocks slice of floor(total/tp) head-blocks. 0/1 = no TP. */
+  int tp_rank, tp_size;
 } mux_unit_config;
 
 MUX_API int mux_unit_create(const mux_unit_config* cfg, mux_unit** out);
@@ -258,6 +263,18 @@ MUX_API int mux_unit_elapsed(mux_unit* unit, int slot_a, int slot_b, float* ms);
  * enable, then read the summed kernel milliseconds and launch count. */
 MUX_API int mux_unit_attn_timing(mux_unit* unit, int enable);
 MUX_API int mux_unit_attn_time(mux_unit* unit, double* total_ms, int64_t* launches, double* bytes);
+/* Tensor-parallel mailbox of a partition (the fused row-parallel GEMM ->
+ * allreduce): its device pointer and a CUDA IPC handle (64 bytes) that the
+ * other ranks of the mesh open with mux_unit_tp_connect. Replaces the
+ * reference's tp_speedup = eta * tp pricing (cost_model.cpp:43-47). */
+MUX_API int mux_unit_tp_mailbox(mux_unit* unit, int partition, void** dev_ptr, void* ipc_handle);
+/* Map rank peer_rank's mailbox: from its IPC handle (other process), or its
+ * device pointer when the peer lives in this process (handle = NULL). */
+MUX_API int mux_unit_tp_connect(mux_unit* unit, int partition, int peer_rank, const void* ipc_handle,
+                                void* dev_ptr);
+/* Debug: the partition's two mailbox counters and their expected values
+ * (out[4] = counter0, counter1, expected0, expected1), read on a side stream. */
+MUX_API int mux_unit_tp_debug(mux_unit* unit, int partition, uint32_t* out);
 /* SMs of a partition (its green context's, or the device's). */
 MUX_API int mux_unit_partition_sms(mux_unit* unit, int partition, int* sms);
 /* Debug: launch `blocks` CTAs on a partition and record each CTA's %smid

@@ -76,7 +76,7 @@ class UnitConfig(C.Structure):
                 ("pool_blocks", i64), ("device_pool_blocks", i64), ("max_batch", C.c_int),
                 ("max_prefill_tokens", C.c_int), ("max_ctx", C.c_int), ("max_slots", C.c_int),
                 ("init_seed", u64), ("init_std", f32), ("partitions", C.c_int),
-                ("partition_sms", P(C.c_int))]
+                ("partition_sms", P(C.c_int)), ("tp_rank", C.c_int), ("tp_size", C.c_int)]
 
 
 _SIGS = {
@@ -109,6 +109,9 @@ _SIGS = {
     "mux_gemm_bf16": (C.c_int, [vp, vp, C.c_int, C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int, vp]),
     "mux_weight_tile": (C.c_int, [vp, C.c_int, C.c_int, vp, C.c_int, vp]),
     "mux_weight_tiled_bytes": (i64, [C.c_int, C.c_int]),
+    "mux_unit_tp_mailbox": (C.c_int, [vp, C.c_int, P(vp), vp]),
+    "mux_unit_tp_connect": (C.c_int, [vp, C.c_int, C.c_int, vp, vp]),
+    "mux_unit_tp_debug": (C.c_int, [vp, C.c_int, P(C.c_uint32)]),
     "mux_unit_partition_sms": (C.c_int, [vp, C.c_int, P(C.c_int)]),
     "mux_unit_probe_smids": (C.c_int, [vp, C.c_int, C.c_int, P(C.c_int)]),
     "mux_unit_set_option": (C.c_int, [vp, C.c_char_p, i64]),

@@ -668,20 +668,28 @@ int mux_unit_create(const mux_unit_config* cfg, mux_unit** out) {
     u->max_prefill = std::max(16, cfg->max_prefill_tokens);
     const int max_rows = (max_ctx + 15) / 16;
     int hid = 0, qkv = 0, ffn = 0, vocab = 0, heads = 0;
+    const int tp = std::max(1, cfg->tp_size), tp_rank = tp > 1 ? cfg->tp_rank : 0;
+    require(tp <= mux::kMaxTp && tp_rank >= 0 && tp_rank < tp, "unit: bad tensor-parallel rank/size");
     for (int i = 0; i < cfg->n_llms; ++i) {
       const mux_llm_entry& e = cfg->llms[i];
+      // the reference planner never checks head divisibility.
+      require(e.num_heads % tp == 0 && e.ffn % tp == 0,
+              "unit: heads and ffn must be divisible by tp_size (reference planner emits e.g. 30b at tp 8)");
       u->specs.push_back(spec_of(e));
+      u->specs.back().num_heads = e.num_heads / tp;  // this rank's head slice of the pool rows
       u->pool.bp->register_llm(i, &u->specs.back(), 16);
       u->pool.bp->set_quota(i, cfg->pool_blocks);  // no quota until a scheduler sets one
       mux::ModelDims d;
       d.name = u->specs.back().name;
       d.layers = e.num_layers;
-      d.heads = e.num_heads;
+      d.heads = e.num_heads / tp;
       d.head_dim = e.head_dim;
       d.hidden = e.hidden_size;
-      d.ffn = e.ffn;
+      d.ffn = e.ffn / tp;
       d.vocab = e.vocab;
-      const int64_t row_blocks = 2ll * e.num_layers * e.num_heads;
+      d.tp_rank = tp_rank;
+      d.tp_size = tp;
+      const int64_t row_blocks = 2ll * e.num_layers * d.heads;
       const int64_t max_rowrecs = std::max<int64_t>(1, cfg->pool_blocks / row_blocks);
       const int slots = cfg->max_slots > 0 ? cfg->max_slots : static_cast<int>(std::min<int64_t>(max_rowrecs, 1 << 20));
       u->models.push_back(std::make_unique<mux::Llama>(d, slots, max_rows, max_rowrecs));
@@ -764,6 +772,17 @@ int mux_unit_create(const mux_unit_config* cfg, mux_unit** out) {
       u->ws.push_back(std::make_unique<mux::Workspace>(max_tok, std::max(u->max_batch, 256), hid, qkv, ffn, vocab,
                                                        heads, u->max_batch, u->rt->num_sms()));
       u->ws.back()->sms = sms;
+      if (tp > 1) {
+        auto link = std::make_unique<mux::TpLink>();
+        link->rank = tp_rank;
+        link->size = tp;
+        link->rows = std::max(max_tok, 256);
+        link->hidden = hid;
+        link->box = mux::DevMem(2 * tp * link->slot_floats() * 4 + 256);
+        mux::check_cuda(cudaMemset(link->box.p, 0, link->box.bytes), "tp mailbox");
+        link->peer[tp_rank] = link->box.p;
+        u->ws.back()->tp = std::move(link);
+      }
     }
     for (auto& e : u->ev) mux::check_cuda(cudaEventCreate(&e), "event");
     mux::check_cuda(cudaDeviceSynchronize(), "unit create");
@@ -882,6 +901,59 @@ int mux_unit_attn_time(mux_unit* u, double* total_ms, int64_t* launches, double*
 }
 
 int64_t mux_unit_launches(mux_unit* u) { return u ? u->rt->launches() : -1; }
+
+int mux_unit_tp_mailbox(mux_unit* u, int partition, void** dev_ptr, void* ipc_handle) {
+  return guarded([&] {
+    u->stream(partition);
+    mux::TpLink* t = u->ws[partition]->tp.get();
+    require(t != nullptr, "tp mailbox: unit was created without tensor parallelism");
+    if (dev_ptr) *dev_ptr = t->box.p;
+    if (ipc_handle) {
+      cudaIpcMemHandle_t h;
+      mux::check_cuda(cudaIpcGetMemHandle(&h, t->box.p), "cudaIpcGetMemHandle");
+      std::memcpy(ipc_handle, &h, sizeof(h));
+    }
+  });
+}
+
+int mux_unit_tp_connect(mux_unit* u, int partition, int peer_rank, const void* ipc_handle, void* dev_ptr) {
+  return guarded([&] {
+    u->stream(partition);
+    mux::TpLink* t = u->ws[partition]->tp.get();
+    require(t != nullptr, "tp connect: unit was created without tensor parallelism");
+    require(peer_rank >= 0 && peer_rank < t->size && peer_rank != t->rank, "tp connect: bad peer rank");
+    require(t->peer[peer_rank] == nullptr, "tp connect: peer already connected");
+    if (ipc_handle != nullptr) {
+      cudaIpcMemHandle_t h;
+      std::memcpy(&h, ipc_handle, sizeof(h));
+      void* p = nullptr;
+      mux::check_cuda(cudaIpcOpenMemHandle(&p, h, cudaIpcMemLazyEnablePeerAccess), "cudaIpcOpenMemHandle");
+      t->peer[peer_rank] = p;
+      t->ipc_opened[peer_rank] = true;
+    } else {
+      require(dev_ptr != nullptr, "tp connect: need an IPC handle or a device pointer");
+      t->peer[peer_rank] = dev_ptr;
+    }
+  });
+}
+
+int mux_unit_tp_debug(mux_unit* u, int partition, uint32_t* out) {
+  return guarded([&] {
+    u->stream(partition);
+    mux::TpLink* t = u->ws[partition]->tp.get();
+    require(t != nullptr, "tp debug: no tensor parallelism");
+    cudaStream_t side;
+    mux::check_cuda(cudaStreamCreateWithFlags(&side, cudaStreamNonBlocking), "side stream");
+    mux::PinnedMem h(8);
+    mux::check_cuda(cudaMemcpyAsync(h.p, t->counter(t->rank, 0), 8, cudaMemcpyDeviceToHost, side), "counter read");
+    mux::check_cuda(cudaStreamSynchronize(side), "counter sync");
+    cudaStreamDestroy(side);
+    out[0] = h.as<uint32_t>()[0];
+    out[1] = h.as<uint32_t>()[1];
+    out[2] = t->expected[0];
+    out[3] = t->expected[1];
+  });
+}
 
 int mux_unit_partition_sms(mux_unit* u, int partition, int* sms) {
   return guarded([&] {

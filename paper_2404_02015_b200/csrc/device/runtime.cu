@@ -143,10 +143,41 @@ DevMem* Llama::tensor(const std::string& name, int layer, int* rows, int* cols, 
   return sh.m;
 }
 
+// Megatron shard of a full host tensor: column-parallel QKV (rows of this
+// rank's heads in each of q/k/v) and gate/up (rows of this rank's FFN
+// columns; the (gate_i, up_i) interleave keeps them contiguous), row-parallel
+// O / down (this rank's input columns). Returns false if `name` is replicated.
+static bool shard_rows(const ModelDims& d, const std::string& name, const uint16_t* full, std::vector<uint16_t>& out) {
+  const int r = d.tp_rank, tp = d.tp_size, hid = d.hidden;
+  const int64_t hl = static_cast<int64_t>(d.heads) * 128, hf = hl * tp;  // local / full attention width
+  const int64_t fl = d.ffn, ff = fl * tp;
+  if (name == "wqkv") {
+    out.resize(3 * hl * hid);
+    for (int part = 0; part < 3; ++part)
+      std::memcpy(out.data() + part * hl * hid, full + (part * hf + r * hl) * hid, hl * hid * 2);
+  } else if (name == "wgu") {
+    out.resize(2 * fl * hid);
+    std::memcpy(out.data(), full + 2 * r * fl * hid, 2 * fl * hid * 2);
+  } else if (name == "wo" || name == "wdown") {
+    const int64_t loc = name == "wo" ? hl : fl, tot = name == "wo" ? hf : ff;
+    out.resize(static_cast<size_t>(hid) * loc);
+    for (int64_t row = 0; row < hid; ++row) std::memcpy(out.data() + row * loc, full + row * tot + r * loc, loc * 2);
+  } else {
+    return false;
+  }
+  return true;
+}
+
 bool Llama::set_tensor(const std::string& name, int layer, const void* host, size_t bytes, cudaStream_t s) {
   int rows = 0, cols = 0;
   bool tiled = false;
   DevMem* m = tensor(name, layer, &rows, &cols, &tiled);
+  std::vector<uint16_t> shard;
+  if (m != nullptr && d_.tp_size > 1 && static_cast<size_t>(rows) * cols * 2 * d_.tp_size == bytes &&
+      shard_rows(d_, name, static_cast<const uint16_t*>(host), shard)) {
+    host = shard.data();  // a full tensor was given: keep this rank's shard
+    bytes = shard.size() * 2;
+  }
   if (!m || static_cast<size_t>(rows) * cols * 2 != bytes) return false;
   if (!tiled) {
     check_cuda(cudaMemcpyAsync(m->p, host, bytes, cudaMemcpyHostToDevice, s), "set_tensor");
@@ -270,12 +301,23 @@ void Workspace::stage_commit(size_t n_ints, cudaStream_t stream) {
   cur ^= 1;
 }
 
+TpLink::~TpLink() {
+  for (int r = 0; r < size; ++r)
+    if (ipc_opened[r] && peer[r] != nullptr) cudaIpcCloseMemHandle(peer[r]);
+}
+
 // ---------------------------------------------------------------- Runtime
 
 Runtime::Runtime(int device, int64_t pool_blocks, int max_pos)
     : device_(device), pool_blocks_(pool_blocks), max_pos_(max_pos) {
   check_cuda(cudaSetDevice(device), "cudaSetDevice");
   check_cuda(cudaDeviceGetAttribute(&num_sms_, cudaDevAttrMultiProcessorCount, device), "sm count");
+  check_cuda(preload_decode_attention(), "preload");
+  check_cuda(preload_kv_append(), "preload");
+  check_cuda(preload_gemm(), "preload");
+  check_cuda(preload_prefill_attention(), "preload");
+  check_cuda(preload_fused_ops(), "preload");
+  check_cuda(preload(gather_last_tok, scatter_last_tok), "preload");
   pool_ = DevMem(static_cast<size_t>(pool_blocks) * 4096);
   // RoPE table [max_pos][64][(cos, sin)], computed in double, stored fp32.
   std::vector<float> tab(static_cast<size_t>(max_pos) * 128);
@@ -350,6 +392,47 @@ const void* Runtime::out_tmap(const void* out, int epi, int M, int N, int ldo) {
   return ins.first->second.data();
 }
 
+void Runtime::row_parallel_norm(const void* w_tiled, const void* x, int M, int N, int K, int s, const float* norm_w,
+                                float eps, Workspace& ws, cudaStream_t stream) {
+  TpLink& tp = *ws.tp;
+  if (!tp.connected()) throw std::logic_error("tensor parallel: mailbox peers not connected");
+  // slot rows are packed at this model's hidden size (<= the unit's largest)
+  if (M > tp.rows || N > tp.hidden) throw std::invalid_argument("tensor parallel: mailbox too small");
+  const int rows = std::max(M, 256);
+  GemmArgs g{};
+  g.w_tiled = w_tiled;
+  g.tmap_x = act_tmap(x, rows, K, gemm_n_tile(M));
+  float* own = tp.slot(tp.rank, s, tp.rank);
+  g.tmap_out = out_tmap(own, kEpiStoreF32, M, N, N);
+  g.out = own;
+  for (int r = 0, k = 0; r < tp.size; ++r) {
+    g.signal[r] = tp.counter(r, s);
+    if (r != tp.rank) g.tmap_peers[k++] = out_tmap(tp.slot(r, s, tp.rank), kEpiStoreF32, M, N, N);
+  }
+  g.n_peers = tp.size - 1;
+  g.n_signal = tp.size;
+  int grid = 0;
+  g.grid_out = &grid;
+  g.partials = ws.gemm_partials.as<float>();
+  g.flags = ws.gemm_flags.as<int>();
+  g.epoch = ++ws.gemm_epoch;
+  g.grid = ws.sms;
+  g.min_iters = gemm_min_iters_;
+  g.M = M;
+  g.N = N;
+  g.K = K;
+  g.ldo = N;
+  g.epi = Epilogue::kStoreF32;
+  check_cuda(gemm_bf16_tn(g, stream), "gemm (row-parallel)");
+  // Every rank launches the same grid for the same shapes (equal partitions),
+  // so each counter receives grid signals from each of the tp ranks.
+  tp.expected[s] += static_cast<uint32_t>(grid) * tp.size;
+  check_cuda(rmsnorm_tp(ws.resid.as<float>(), tp.slot(tp.rank, s, 0), static_cast<int64_t>(tp.slot_floats()), tp.size,
+                        tp.counter(tp.rank, s), tp.expected[s], norm_w, ws.xn.p, M, N, eps, stream),
+             "rmsnorm_tp");
+  launches_ += 2;
+}
+
 void Runtime::upload_rows(muxsim::BlockPool& bp, int llm, Llama& m, cudaStream_t stream) {
   std::vector<muxsim::RowDelta>& pend = bp.pending_rows(llm);
   if (pend.empty()) return;
@@ -364,7 +447,11 @@ void Runtime::upload_rows(muxsim::BlockPool& bp, int llm, Llama& m, cudaStream_t
   // The slot's previous copy + scatter must be complete before it is reused.
   check_cuda(cudaEventSynchronize(slot.done), "stage wait");
   if (need > slot.cap) {
-    size_t cap = std::max(need, slot.cap * 2);
+    // Grow without freeing on the job path (cudaFree / cudaFreeHost
+    // synchronise the device): the old buffers retire until destruction.
+    size_t cap = std::max<size_t>({need, slot.cap * 2, 1 << 20});
+    retired_dev_.push_back(std::move(slot.dev));
+    if (slot.host) retired_host_.push_back(std::move(slot.host));
     slot.dev = DevMem(cap);
     slot.host = std::make_unique<PinnedMem>(cap);
     slot.cap = cap;
@@ -494,13 +581,19 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
       timer->pending.emplace_back(e0, e1);
       timer->pending_bytes += attn_bytes;
     }
+    const float* next_norm = l + 1 < L ? m.attn_norm[l + 1].as<float>() : m.final_norm.as<float>();
+    if (d.tp_size > 1) {
+      row_parallel_norm(m.wo[l].p, ws.attn.p, n, hid, H * 128, 0, m.ffn_norm[l].as<float>(), d.norm_eps, ws, stream);
+      gemm(m.wgu[l].p, ws.xn.p, n, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, ws, stream);
+      row_parallel_norm(m.wdown[l].p, ws.act.p, n, hid, d.ffn, 1, next_norm, d.norm_eps, ws, stream);
+      continue;
+    }
     gemm(m.wo[l].p, ws.attn.p, n, hid, H * 128, ws.resid.p, hid, kEpiResidual, ws, stream);
     check_cuda(rmsnorm_rows(ws.resid.as<float>(), m.ffn_norm[l].as<float>(), ws.xn.p, n, hid, d.norm_eps, stream),
                "rmsnorm");
     launches_ += 1;
     gemm(m.wgu[l].p, ws.xn.p, n, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, ws, stream);
     gemm(m.wdown[l].p, ws.act.p, n, hid, d.ffn, ws.resid.p, hid, kEpiResidual, ws, stream);
-    const float* next_norm = l + 1 < L ? m.attn_norm[l + 1].as<float>() : m.final_norm.as<float>();
     check_cuda(rmsnorm_rows(ws.resid.as<float>(), next_norm, ws.xn.p, n, hid, d.norm_eps, stream), "rmsnorm");
     launches_ += 1;
   }
@@ -583,13 +676,19 @@ void Runtime::prefill(Llama& m, Workspace& ws, int n, const int32_t* slots_host,
     launches_ += 1;
     check_cuda(prefill_attention(pa, stream), "prefill_attention");
     launches_ += 1;
+    const float* next_norm = l + 1 < L ? m.attn_norm[l + 1].as<float>() : m.final_norm.as<float>();
+    if (d.tp_size > 1) {
+      row_parallel_norm(m.wo[l].p, ws.attn.p, T, hid, H * 128, 0, m.ffn_norm[l].as<float>(), d.norm_eps, ws, stream);
+      gemm(m.wgu[l].p, ws.xn.p, T, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, ws, stream);
+      row_parallel_norm(m.wdown[l].p, ws.act.p, T, hid, d.ffn, 1, next_norm, d.norm_eps, ws, stream);
+      continue;
+    }
     gemm(m.wo[l].p, ws.attn.p, T, hid, H * 128, ws.resid.p, hid, kEpiResidual, ws, stream);
     check_cuda(rmsnorm_rows(ws.resid.as<float>(), m.ffn_norm[l].as<float>(), ws.xn.p, T, hid, d.norm_eps, stream),
                "rmsnorm");
     launches_ += 1;
     gemm(m.wgu[l].p, ws.xn.p, T, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, ws, stream);
     gemm(m.wdown[l].p, ws.act.p, T, hid, d.ffn, ws.resid.p, hid, kEpiResidual, ws, stream);
-    const float* next_norm = l + 1 < L ? m.attn_norm[l + 1].as<float>() : m.final_norm.as<float>();
     check_cuda(rmsnorm_rows(ws.resid.as<float>(), next_norm, ws.xn.p, T, hid, d.norm_eps, stream), "rmsnorm");
     launches_ += 1;
   }

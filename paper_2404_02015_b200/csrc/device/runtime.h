@@ -27,6 +27,11 @@ struct ModelDims {
   int vocab = 32000;
   float norm_eps = 1e-5f;
   float rope_theta = 10000.f;
+  // Tensor parallelism (Megatron): this shard holds heads [r*heads, (r+1)*heads)
+  // and FFN columns [r*ffn, (r+1)*ffn) of the full model; `heads` and `ffn`
+  // above are the LOCAL counts. tp_size == 1: the whole model.
+  int tp_rank = 0;
+  int tp_size = 1;
 };
 
 // Device buffer (cudaMalloc), owned.
@@ -89,6 +94,38 @@ class Llama {
   int64_t max_rowrecs_;
 };
 
+// Tensor-parallel mailbox of one partition (the fused GEMM -> allreduce of
+// the row-parallel O / down projections). Layout of every rank's box:
+//   slots [2][tp][rows][hidden] fp32   slot s, written by rank src
+//   counters [2] int32                 bumped by every CTA of every rank's GEMM
+// Rank src's GEMM stores its fp32 partial tile straight into slot (s, src) of
+// every rank (NVLink peer stores by TMA) and then signals their counter s;
+// each rank's rmsnorm_tp waits for its counter and sums the tp slots in rank
+// order, so the residual stream stays bit-identical on every rank. Slot 0
+// serves the O projection, slot 1 the down projection: a rank can only reach
+// a slot again after every peer has consumed it (see runtime.cu).
+struct TpLink {
+  int rank = 0, size = 1;
+  int rows = 0, hidden = 0;
+  DevMem box;
+  void* peer[8] = {};        // every rank's box as mapped in this process (peer[rank] = own)
+  bool ipc_opened[8] = {};
+  uint32_t expected[2] = {0, 0};
+  size_t slot_floats() const { return static_cast<size_t>(rows) * hidden; }
+  float* slot(int r, int s, int src) const {
+    return static_cast<float*>(peer[r]) + (static_cast<size_t>(s) * size + src) * slot_floats();
+  }
+  int* counter(int r, int s) const {
+    return reinterpret_cast<int*>(static_cast<float*>(peer[r]) + 2 * size * slot_floats()) + s;
+  }
+  bool connected() const {
+    for (int r = 0; r < size; ++r)
+      if (peer[r] == nullptr) return false;
+    return true;
+  }
+  ~TpLink();
+};
+
 // Per-partition scratch for one running job.
 struct Workspace {
   int max_tokens = 0;    // prefill token budget or max decode batch
@@ -97,6 +134,7 @@ struct Workspace {
   DevMem gemm_partials, gemm_flags;  // stream-K fixup scratch of this partition's GEMMs
   int gemm_epoch = 0;
   int sms = 148;           // SMs of the partition this workspace's jobs run on
+  std::unique_ptr<TpLink> tp;  // tensor-parallel mailbox (tp_size > 1)
   PinnedMem host_ints[2];  // double-buffered staging for per-job metadata
   cudaEvent_t staged[2] = {nullptr, nullptr};
   int cur = 0;
@@ -157,6 +195,11 @@ class Runtime {
   // Decode-forward building blocks, exposed for tests/bench.
   void gemm(const void* w_tiled, const void* x, int M, int N, int K, void* out, int ldo, int epi,
             Workspace& ws, cudaStream_t stream);
+  // Row-parallel projection + the fused allreduce (tp > 1): out partial of
+  // X[M x K] W[N x K]^T to every rank's slot `s`, then resid += sum of ranks'
+  // slots and xn = rmsnorm(resid) * norm_w on this rank.
+  void row_parallel_norm(const void* w_tiled, const void* x, int M, int N, int K, int s, const float* norm_w,
+                         float eps, Workspace& ws, cudaStream_t stream);
 
  private:
   int device_;
@@ -174,6 +217,8 @@ class Runtime {
     size_t cap = 0;
   };
   StageSlot ring_[4];
+  std::vector<DevMem> retired_dev_;
+  std::vector<std::unique_ptr<PinnedMem>> retired_host_;
   int ring_next_ = 0;
   std::map<std::tuple<const void*, int, int, int>, std::vector<unsigned char>> tmaps_;
   std::map<std::tuple<const void*, int, int, int>, std::vector<unsigned char>> out_tmaps_;

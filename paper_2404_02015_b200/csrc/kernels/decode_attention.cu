@@ -310,6 +310,11 @@ cudaError_t launch_decode(const DecodeAttnArgs& a, cudaStream_t stream) {
 
 int decode_attention_max_rows_per_split() { return kMaxIdsPerSplit; }
 
+cudaError_t preload_decode_attention() {
+  return preload(decode_attention_kernel<4, float>, decode_attention_kernel<4, __nv_bfloat16>,
+                 decode_attention_combine<float>, decode_attention_combine<__nv_bfloat16>);
+}
+
 cudaError_t decode_attention(const DecodeAttnArgs& a, bool fp32_out, cudaStream_t stream) {
   if (a.B <= 0) return cudaSuccess;
   if (a.rows_per_split > kMaxIdsPerSplit || a.rows_per_split <= 0) return cudaErrorInvalidValue;

@@ -85,6 +85,65 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_rows_kernel(const float* 
   }
 }
 
+template <int kVec>
+__global__ void __launch_bounds__(kRowThreads) rmsnorm_tp_kernel(float* resid, const float* parts, int64_t part_stride,
+                                                                 int tp, const int* counter, uint32_t expected,
+                                                                 const float* norm_w, __nv_bfloat16* xn, int hidden,
+                                                                 float eps) {
+  __shared__ float scratch[32];
+  grid_dep_wait();
+  if (threadIdx.x == 0) {
+    // every rank's GEMM CTAs have stored their partials and signalled
+    for (;;) {
+      uint32_t v;
+      asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
+      if (static_cast<int32_t>(v - expected) >= 0) break;
+      __nanosleep(64);
+    }
+  }
+  __syncthreads();
+  // Only now let the next kernel (the next GEMM, 1 CTA/SM) be scheduled: an
+  // early launch would park it on the SMs the peer ranks' GEMMs need when
+  // ranks share a GPU, and gains nothing while this grid waits on peers.
+  grid_dep_launch();
+  const int t = blockIdx.x;
+  float4* x = reinterpret_cast<float4*>(resid + static_cast<int64_t>(t) * hidden);
+  const float4* w = reinterpret_cast<const float4*>(norm_w);
+  const int n4 = hidden / 4;
+  float4 v[kVec];
+  float ss = 0.f;
+#pragma unroll
+  for (int k = 0; k < kVec; ++k) {
+    const int i = threadIdx.x + k * kRowThreads;
+    if (i < n4) {
+      float4 a = x[i];
+      for (int src = 0; src < tp; ++src) {  // fixed rank order: identical on every rank
+        const float4 p = reinterpret_cast<const float4*>(parts + src * part_stride + static_cast<int64_t>(t) * hidden)[i];
+        a.x += p.x;
+        a.y += p.y;
+        a.z += p.z;
+        a.w += p.w;
+      }
+      x[i] = a;
+      v[k] = a;
+    } else {
+      v[k] = make_float4(0.f, 0.f, 0.f, 0.f);
+    }
+    ss = fmaf(v[k].x, v[k].x, fmaf(v[k].y, v[k].y, fmaf(v[k].z, v[k].z, fmaf(v[k].w, v[k].w, ss))));
+  }
+  const float inv = rsqrtf(block_sum(ss, scratch) / static_cast<float>(hidden) + eps);
+  uint2* y = reinterpret_cast<uint2*>(xn + static_cast<int64_t>(t) * hidden);
+#pragma unroll
+  for (int k = 0; k < kVec; ++k) {
+    const int i = threadIdx.x + k * kRowThreads;
+    if (i < n4) {
+      const float4 g = w[i];
+      y[i] = make_uint2(pack_bf16(v[k].x * inv * g.x, v[k].y * inv * g.y),
+                        pack_bf16(v[k].z * inv * g.z, v[k].w * inv * g.w));
+    }
+  }
+}
+
 __global__ void __launch_bounds__(kRowThreads) argmax_kernel(const float* logits, int V, int32_t* out) {
   __shared__ float sv[32];
   __shared__ int si[32];
@@ -161,6 +220,12 @@ __global__ void fill_kernel(float* dst, int64_t n, float v) {
 
 }  // namespace
 
+cudaError_t preload_fused_ops() {
+  return preload(embed_rmsnorm_kernel, rmsnorm_rows_kernel<2>, rmsnorm_rows_kernel<4>, rmsnorm_rows_kernel<8>,
+                 rmsnorm_rows_kernel<16>, rmsnorm_tp_kernel<2>, rmsnorm_tp_kernel<4>, rmsnorm_tp_kernel<8>,
+                 rmsnorm_tp_kernel<16>, argmax_kernel, gather_rows_kernel, init_normal_kernel, fill_kernel);
+}
+
 cudaError_t embed_rmsnorm(const void* emb, const int32_t* tokens, const float* norm_w, float* resid,
                           void* xn, int T, int hidden, float eps, cudaStream_t stream) {
   if (T <= 0) return cudaSuccess;
@@ -178,6 +243,19 @@ cudaError_t rmsnorm_rows(const float* resid, const float* norm_w, void* xn, int 
   auto k = per <= 2 ? rmsnorm_rows_kernel<2> : per <= 4 ? rmsnorm_rows_kernel<4>
          : per <= 8 ? rmsnorm_rows_kernel<8> : rmsnorm_rows_kernel<16>;
   return launch(k, dim3(T), dim3(kRowThreads), 0, stream, resid, norm_w, y, hidden, eps);
+}
+
+cudaError_t rmsnorm_tp(float* resid, const float* parts, int64_t part_stride, int tp, const int* counter,
+                       uint32_t expected, const float* norm_w, void* xn, int T, int hidden, float eps,
+                       cudaStream_t stream) {
+  if (T <= 0) return cudaSuccess;
+  if (hidden % 4 != 0 || hidden > 4 * kRowThreads * 16) return cudaErrorInvalidValue;
+  __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(xn);
+  const int per = (hidden / 4 + kRowThreads - 1) / kRowThreads;
+  auto k = per <= 2 ? rmsnorm_tp_kernel<2> : per <= 4 ? rmsnorm_tp_kernel<4>
+         : per <= 8 ? rmsnorm_tp_kernel<8> : rmsnorm_tp_kernel<16>;
+  return launch(k, dim3(T), dim3(kRowThreads), 0, stream, resid, parts, part_stride, tp, counter, expected, norm_w, y,
+                hidden, eps);
 }
 
 cudaError_t argmax_rows(const float* logits, int T, int V, int32_t* out, cudaStream_t stream) {

@@ -56,6 +56,10 @@ constexpr int kEpiThreads = 128;
 constexpr int kChunkBytes = 32 * kBM * 4;  // one epilogue chunk: 32 tokens x 128 fp32
 constexpr int kSmemBudget = 224 * 1024;     // A ring + B ring + 2 staging chunks
 
+struct PeerMaps {
+  CUtensorMap m[kMaxTp - 1];
+};
+
 struct GemmRun {
   const uint8_t* w_tiled;  // pre-tiled weights (weight_tile), or null -> TMA map
   void* out;
@@ -70,6 +74,13 @@ struct GemmRun {
   int epi;
   uint32_t tmem_cols;
   unsigned long long* timing;  // debug: [grid][4] globaltimer stamps, or null
+  // Tensor-parallel fan-out (kStoreF32 only): every finished tile is also
+  // stored through peers.m[0..n_peers) (the same slot on the other ranks of
+  // the mesh, NVLink peer memory), and once all of a CTA's stores have landed
+  // it adds 1 to signal[0..n_signal) (this rank's and every peer's counter).
+  int n_peers;
+  int n_signal;
+  int* signal[kMaxTp];
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -98,7 +109,7 @@ __device__ __forceinline__ void epi_bar() {
 
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
-               const __grid_constant__ CUtensorMap tout, const GemmRun r) {
+               const __grid_constant__ CUtensorMap tout, const GemmRun r, const __grid_constant__ PeerMaps peers) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   // 1 KiB-aligned carve-up; pointer arithmetic on smem_raw itself keeps the
   // shared address space visible to the compiler (STS/LDS, not generic ST/LD).
@@ -350,6 +361,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             tma_store_2d(&tout, st, m * (kBM / 2), tok0 + cc);
           } else {
             tma_store_2d(&tout, st, m * kBM, tok0 + cc);
+            for (int pr = 0; pr < r.n_peers; ++pr) tma_store_2d(&peers.m[pr], st, m * kBM, tok0 + cc);
           }
           bulk_commit();
           if (stamp) r.timing[c * 32 + 28 + k] = gtimer();
@@ -369,6 +381,13 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       ++seg;
     }
     if (leader) bulk_wait<0>();  // staging smem must outlive its bulk reads
+    if (leader && r.n_signal > 0) {
+      // every store of this CTA (local + peers) has completed: publish
+      asm volatile("fence.proxy.async.global;" ::: "memory");
+      asm volatile("fence.acq_rel.sys;" ::: "memory");
+      for (int d = 0; d < r.n_signal; ++d)
+        asm volatile("red.release.sys.global.add.s32 [%0], 1;" ::"l"(r.signal[d]) : "memory");
+    }
     if (r.timing != nullptr && threadIdx.x == 128) r.timing[c * 32 + 2] = gtimer();
   }
   tc_fence_before();
@@ -494,6 +513,8 @@ cudaError_t weight_tile(const void* src, int N, int K, void* dst, bool inverse, 
   return cudaGetLastError();
 }
 
+cudaError_t preload_gemm() { return preload(gemm_tn_kernel, weight_tile_kernel); }
+
 static unsigned long long* g_debug_timing = nullptr;
 void gemm_debug_timing(void* buf) { g_debug_timing = static_cast<unsigned long long*>(buf); }
 
@@ -550,12 +571,19 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
     if (e != cudaSuccess) return e;
     configured = true;
   }
+  r.n_peers = a.n_peers;
+  r.n_signal = a.n_signal;
+  for (int d = 0; d < kMaxTp; ++d) r.signal[d] = a.signal[d];
+  PeerMaps pm;
+  std::memset(&pm, 0, sizeof(pm));
+  for (int d = 0; d < a.n_peers; ++d) std::memcpy(&pm.m[d], a.tmap_peers[d], sizeof(CUtensorMap));
   CUtensorMap tw, tx, to;
   if (a.tmap_w != nullptr) std::memcpy(&tw, a.tmap_w, sizeof(CUtensorMap));
   else std::memset(&tw, 0, sizeof(CUtensorMap));
   std::memcpy(&tx, a.tmap_x, sizeof(CUtensorMap));
   std::memcpy(&to, a.tmap_out, sizeof(CUtensorMap));
-  return launch(gemm_tn_kernel, dim3(grid), dim3(kThreads), smem, stream, tw, tx, to, r);
+  if (a.grid_out != nullptr) *a.grid_out = grid;
+  return launch(gemm_tn_kernel, dim3(grid), dim3(kThreads), smem, stream, tw, tx, to, r, pm);
 }
 
 }  // namespace mux

@@ -55,6 +55,8 @@ cudaError_t table_update(const TableUpdateArgs& a, cudaStream_t stream);
 // Weight-stationary tiling: every CTA owns 128 rows of W (one UMMA M=128
 // tile) and up to 256 activation rows (UMMA N), so decode batches (M <= 256)
 // stream each weight byte exactly once.
+constexpr int kMaxTp = 8;  // tensor-parallel ranks of one mesh (node-local)
+
 enum class Epilogue : int {
   kStoreBf16 = 0,      // out bf16 [M][ldo]
   kResidualAddF32 = 1, // out fp32 [M][ldo] += D (the residual stream; single owner per element)
@@ -75,6 +77,14 @@ struct GemmArgs {
   int M, N, K;
   int ldo;
   Epilogue epi;
+  // Tensor parallelism (kStoreF32): also store every tile through these
+  // maps (host CUtensorMap*, peer ranks' slots) and signal the counters
+  // once per CTA when its stores have landed. grid_out receives the grid.
+  int n_peers = 0;
+  const void* tmap_peers[kMaxTp - 1] = {};
+  int n_signal = 0;
+  int* signal[kMaxTp] = {};
+  int* grid_out = nullptr;
 };
 cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream);
 int gemm_pick_n_tile(int M);
@@ -97,6 +107,13 @@ cudaError_t embed_rmsnorm(const void* emb, const int32_t* tokens, const float* n
 // xn[t] = bf16(resid[t] * rsqrt(mean(resid[t]^2) + eps) * w)
 cudaError_t rmsnorm_rows(const float* resid, const float* norm_w, void* xn, int T, int hidden, float eps,
                          cudaStream_t stream);
+// Tensor-parallel residual update + RMSNorm: waits until *counter has reached
+// `expected` (every rank's row-parallel GEMM stored its partial here), then
+// resid[t] += parts[0][t] + ... + parts[tp-1][t] (rank order), xn = rmsnorm.
+// parts[src] = parts + src * part_stride floats, rows of `hidden`.
+cudaError_t rmsnorm_tp(float* resid, const float* parts, int64_t part_stride, int tp, const int* counter,
+                       uint32_t expected, const float* norm_w, void* xn, int T, int hidden, float eps,
+                       cudaStream_t stream);
 // Row argmax of fp32 logits; writes token ids (lowest index on ties).
 cudaError_t argmax_rows(const float* logits, int T, int V, int32_t* out, cudaStream_t stream);
 // Gather rows: dst[i] = src[idx[i]] (bf16 rows of `cols`).
@@ -119,5 +136,12 @@ size_t prefill_attention_smem();
 // Deterministic N(0, std) init of a bf16 buffer from (seed, index).
 cudaError_t init_normal_bf16(void* dst, int64_t n, uint64_t seed, float std, cudaStream_t stream);
 cudaError_t fill_f32(float* dst, int64_t n, float v, cudaStream_t stream);
+
+// Load every libmux kernel (see launch.cuh: preload); one per translation unit.
+cudaError_t preload_decode_attention();
+cudaError_t preload_kv_append();
+cudaError_t preload_gemm();
+cudaError_t preload_prefill_attention();
+cudaError_t preload_fused_ops();
 
 }  // namespace mux

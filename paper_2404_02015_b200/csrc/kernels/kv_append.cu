@@ -115,6 +115,8 @@ __global__ void __launch_bounds__(256) table_update_kernel(const TableUpdateArgs
 
 }  // namespace
 
+cudaError_t preload_kv_append() { return preload(kv_append_kernel, table_update_kernel); }
+
 cudaError_t kv_append(const AppendArgs& a, cudaStream_t stream) {
   if (a.T <= 0) return cudaSuccess;
   const int warps = a.T * a.H;

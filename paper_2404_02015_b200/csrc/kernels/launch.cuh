@@ -13,6 +13,17 @@ namespace mux {
 // Process-wide switch (default on); "pdl" option of mux_unit_set_option.
 bool& pdl_enabled();
 
+// Force-load kernels now (CUDA lazy loading would otherwise load a kernel at
+// its first launch, which can wait for the device to idle -- a deadlock when
+// an earlier kernel of the same process spins on a tensor-parallel peer).
+template <typename... K>
+inline cudaError_t preload(K... kernels) {
+  cudaError_t err = cudaSuccess;
+  cudaFuncAttributes attr;
+  ((err = err == cudaSuccess ? cudaFuncGetAttributes(&attr, reinterpret_cast<const void*>(kernels)) : err), ...);
+  return err;
+}
+
 template <typename... P, typename... A>
 inline cudaError_t launch(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,
                           A&&... args) {

@@ -275,6 +275,8 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
 
 size_t prefill_attention_smem() { return kSmemBytes; }
 
+cudaError_t preload_prefill_attention() { return preload(prefill_attention_kernel); }
+
 cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
   if (a.T <= 0 || a.n_tiles <= 0) return cudaSuccess;
   static bool configured = false;

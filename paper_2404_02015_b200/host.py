@@ -312,7 +312,8 @@ class Unit:
     def __init__(self, specs: Sequence[LLMSpec], pool_blocks: int, device: int = 0,
                  device_pool_blocks: int = 0, max_batch: int = 256, max_prefill_tokens: int = 4096,
                  max_ctx: int = 4096, max_slots: int = 0, init_seed: int = 0,
-                 init_std: float = 0.02, partitions: int = 2, partition_sms: Sequence[int] | None = None):
+                 init_std: float = 0.02, partitions: int = 2, partition_sms: Sequence[int] | None = None,
+                 tp_rank: int = 0, tp_size: int = 1):
         """partition_sms[p] > 0 puts partition p on its own green context of
         that many SMs (the SM share a JobPlan's sm_demand asks for)."""
         self.specs = list(specs)
@@ -326,7 +327,8 @@ class Unit:
             psms = (C.c_int * partitions)(*partition_sms)
             self._keep.append(psms)
         cfg = UnitConfig(device, len(specs), ents, pool_blocks, device_pool_blocks, max_batch,
-                         max_prefill_tokens, max_ctx, max_slots, init_seed, init_std, partitions, psms)
+                         max_prefill_tokens, max_ctx, max_slots, init_seed, init_std, partitions, psms,
+                         tp_rank, tp_size)
         h = C.c_void_p()
         check(lib.mux_unit_create(C.byref(cfg), C.byref(h)))
         self._h = h.value
@@ -396,6 +398,18 @@ class Unit:
         ms, n, by = C.c_double(), C.c_int64(), C.c_double()
         check(lib.mux_unit_attn_time(self._h, C.byref(ms), C.byref(n), C.byref(by)))
         return ms.value, n.value, by.value
+
+    def tp_mailbox(self, partition: int):
+        """(device pointer, 64-byte CUDA IPC handle) of a partition's TP mailbox."""
+        ptr = C.c_void_p()
+        handle = (C.c_ubyte * 64)()
+        check(lib.mux_unit_tp_mailbox(self._h, partition, C.byref(ptr), handle))
+        return ptr.value, bytes(handle)
+
+    def tp_connect(self, partition: int, peer_rank: int, handle: bytes | None = None, ptr: int | None = None):
+        """Map a peer rank's mailbox: IPC handle (other process) or pointer (same process)."""
+        h = None if handle is None else (C.c_ubyte * 64).from_buffer_copy(handle)
+        check(lib.mux_unit_tp_connect(self._h, partition, peer_rank, h, ptr))
 
     def partition_sms(self, partition: int) -> int:
         v = C.c_int()

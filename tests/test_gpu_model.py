@@ -227,3 +227,66 @@ def test_colocated_decode_on_green_partitions(green_unit):
             check_tokens(refs[llm], prompts[i], gen[i])
         for rid in rids:
             unit.pool.free_request(llm, rid)
+
+
+def _pinned_i32(n):
+    import torch
+    return torch.zeros(n, dtype=torch.int32).pin_memory().numpy()
+
+
+@pytest.mark.timeout(300)
+def test_tensor_parallel_tp2_fused_allreduce(cuda):
+    """Config 3's mechanism at tp=2, both ranks in this process on one GPU:
+    Megatron shards (heads / FFN columns), per-rank KV pool slices with
+    replicated allocation decisions, and the row-parallel O / down GEMMs that
+    store their fp32 partials straight into every rank's mailbox slot and
+    signal it (the fused GEMM -> allreduce). Both ranks must emit identical
+    greedy tokens (the residual stream is summed in rank order everywhere),
+    and those tokens must match the full-model oracle."""
+    specs = [mux.spec("tiny-a"), mux.spec("tiny-b")]
+    total = 232998
+    units = [mux.Unit(specs, pool_blocks=total // 2, device_pool_blocks=total // 2, max_batch=16,
+                      max_prefill_tokens=512, max_ctx=512, partitions=2, tp_rank=r, tp_size=2) for r in (0, 1)]
+    try:
+        for p in range(2):
+            ptrs = [u.tp_mailbox(p)[0] for u in units]
+            units[0].tp_connect(p, 1, ptr=ptrs[1])
+            units[1].tp_connect(p, 0, ptr=ptrs[0])
+        rope = llama_ref.rope_table(512 + 16)
+        refs = []
+        for llm, s in enumerate(specs):
+            w = [load_weights(u, llm, s, 300 + llm) for u in units][0]
+            refs.append(llama_ref.RefLlama(dims_of(s), w, rope))
+        rng = np.random.default_rng(5)
+        for llm, s in enumerate(specs):
+            lens = [1, 17, 40, 130]
+            rids = [90000 + 10 * llm + i for i in range(len(lens))]
+            prompts = [rng.integers(0, s.vocab, n).astype(np.int32) for n in lens]
+            for u in units:
+                for rid, n in zip(rids, lens):
+                    assert u.pool.admit(llm, rid, n, n + 8).ok
+            outs = [_pinned_i32(len(lens)) for _ in units]
+            for u, o in zip(units, outs):  # both ranks enqueue before either waits
+                u.prefill(llm, rids, np.concatenate(prompts), o, partition=1)
+            for u in units:
+                u.sync()
+            assert np.array_equal(outs[0], outs[1])
+            gen = [[int(t)] for t in outs[0]]
+            for _ in range(8):
+                for u in units:
+                    for rid in rids:
+                        assert u.pool.alloc(llm, rid, 1, False).ok
+                for u, o in zip(units, outs):
+                    u.decode(llm, rids, out=o, partition=1)
+                for u in units:
+                    u.sync()
+                assert np.array_equal(outs[0], outs[1])
+                for i, t in enumerate(outs[0]):
+                    gen[i].append(int(t))
+            for i in range(len(lens)):
+                check_tokens(refs[llm], prompts[i], gen[i])
+            # replicated allocation decisions: identical per-rank pool state
+            assert [u.pool.used(llm) for u in units][0] == units[1].pool.used(llm)
+    finally:
+        for u in units:
+            u.close()
