@@ -48,6 +48,15 @@ def peaks():
         return 6650.0, "fallback"
 
 
+def k1_traffic():
+    """DRAM bytes of one K1 launch from the committed ncu capture (profiles/)."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "r01_k1_traffic.json")) as f:
+            return json.load(f)
+    except Exception:
+        return None
+
+
 def pool_blocks(specs):
     weights = sum(s.weight_bytes for s in specs)
     reserve = round(RESERVE * MESH_BYTES)
@@ -298,7 +307,9 @@ def main():
                     "unit": "tokens/s", "h2d_bytes_per_step": int(per_step_tokens * 4),
                     "d2h_bytes_per_step": int(per_step_tokens * 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(achieved / hbm, 4), "traffic": None,
+                         "frac": round(achieved / hbm, 4),
+                         "traffic": (k1_traffic() or {}).get("dram_bytes"),
+                         "traffic_note": (k1_traffic() or {}).get("capture"),
                          "kernel": "decode_attention_kernel (K1, per-launch CUDA events)",
                          "peak_source": peak_kind, "launches_timed": r["attn_n"],
                          "bytes_per_launch": round(r["attn_bytes"] / max(1, r["attn_n"]))},

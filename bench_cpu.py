@@ -116,14 +116,23 @@ def _ref_sim():
         return {"error": str(e)}
 
 
-def cpu_baseline(args):
+def cpu_baseline(args, min_seconds: float = 10.0):
+    """Repeats the one-layer sample until >= min_seconds of CPU work (bounded
+    sample of the same workload), reports the mean full-step estimate."""
     models = args.models.split(",")
     smp = StepSample(models, args.batch)
-    est, sampled = smp.run()
+    ests, sampled, reps = [], 0.0, 0
+    t0 = time.perf_counter()
+    while time.perf_counter() - t0 < min_seconds or reps < 2:
+        est, s = smp.run()
+        ests.append(est)
+        sampled += s
+        reps += 1
+    est = sum(ests) / len(ests)
     tokens = len(models) * args.batch
     return {"value": round(tokens / est, 3), "unit": "tokens/s", "cores": smp.threads, "kind": "port",
-            "sample": f"1 layer + LM head of each of {models} at decode batch {args.batch} "
-                      f"(ShareGPT contexts), scaled by layer count; {sampled:.1f} s sampled",
+            "sample": f"{reps} x (1 layer + LM head of each of {models}) at decode batch {args.batch} "
+                      f"(ShareGPT contexts), scaled by layer count; {sampled:.1f} s of CPU work sampled",
             "reference_sim": _ref_sim()}
 
 

@@ -4,6 +4,7 @@
 #include <cuda.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cmath>
 #include <cstring>
 #include <stdexcept>
@@ -562,7 +563,22 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   ap.row_width = m.row_width();
   ap.rope_positions = max_pos_;
 
-  for (int l = 0; l < L; ++l) {
+  // Profiling aid (MUX_DEBUG_SKIP bitmask; results are garbage when set):
+  // 1 kv_append, 2 rmsnorm, 4 K1, 8 qkv, 16 o, 32 gate-up, 64 down.
+  static const int skip = getenv("MUX_DEBUG_SKIP") ? atoi(getenv("MUX_DEBUG_SKIP")) : 0;
+  for (int l = 0; l < L && skip != 0; ++l) {
+    if (!(skip & 8)) gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
+    ap.layer = l;
+    if (!(skip & 1)) check_cuda(kv_append(ap, stream), "kv_append");
+    at.layer = l;
+    if (!(skip & 4)) check_cuda(decode_attention(at, false, stream), "decode_attention");
+    if (!(skip & 16)) gemm(m.wo[l].p, ws.attn.p, n, hid, H * 128, ws.resid.p, hid, kEpiResidual, ws, stream);
+    if (!(skip & 2)) check_cuda(rmsnorm_rows(ws.resid.as<float>(), m.ffn_norm[l].as<float>(), ws.xn.p, n, hid, d.norm_eps, stream), "rmsnorm");
+    if (!(skip & 32)) gemm(m.wgu[l].p, ws.xn.p, n, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, ws, stream);
+    if (!(skip & 64)) gemm(m.wdown[l].p, ws.act.p, n, hid, d.ffn, ws.resid.p, hid, kEpiResidual, ws, stream);
+    if (!(skip & 2)) check_cuda(rmsnorm_rows(ws.resid.as<float>(), m.ffn_norm[l].as<float>(), ws.xn.p, n, hid, d.norm_eps, stream), "rmsnorm");
+  }
+  for (int l = 0; l < L && skip == 0; ++l) {
     gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
     ap.layer = l;
     check_cuda(kv_append(ap, stream), "kv_append");

@@ -78,6 +78,8 @@ struct GemmRun {
   // stored through peers.m[0..n_peers) (the same slot on the other ranks of
   // the mesh, NVLink peer memory), and once all of a CTA's stores have landed
   // it adds 1 to signal[0..n_signal) (this rank's and every peer's counter).
+  int a_split;      // bulk copies per weight stage (1, 2, 4)
+  int dbg_nomma;    // debug (MUX_GEMM_NOMMA): stream operands without MMAs
   int n_peers;
   int n_signal;
   int* signal[kMaxTp];
@@ -173,31 +175,46 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       // Weights do not depend on earlier kernels: warp 0 starts streaming
       // them while the predecessor drains (PDL); activations must wait.
       if (!is_a) grid_dep_wait();
+      if (!is_a && r.dbg_nomma >= 2) return;  // debug: weights only
       const uint64_t pol = is_a ? policy_evict_first()   // weights: streamed once per step
                                 : policy_evict_last();   // activations: re-read by every CTA
       const int SS = is_a ? SA : SB;
       uint64_t* fb = is_a ? full_a : full_b;
       uint64_t* eb = is_a ? empty_a : empty_b;
       const uint32_t bytes = is_a ? kAStageBytes : b_stage_bytes;
-      int i = 0;
-      for (int64_t it = it0; it < it1; ++it, ++i) {
-        const int64_t t = it / r.kb;
-        const int kbi = static_cast<int>(it - t * r.kb);
-        const int s = i % SS;
-        if (i >= SS) mbar_wait(&eb[s], ((i / SS) - 1) & 1);
+      // Incremental (tile, k-block, stage) counters: no 64-bit division or
+      // modulo in the issue loop (a per-iteration int64 divide is a ~100-
+      // instruction subroutine call on the critical path of every stage).
+      const int t0 = static_cast<int>(it0 / r.kb);
+      int kbi = static_cast<int>(it0 - static_cast<int64_t>(t0) * r.kb);
+      int m = t0 % r.m_tiles, nt = t0 / r.m_tiles;
+      int s = 0, round = 0;
+      for (int64_t it = it0; it < it1; ++it) {
+        if (round > 0) mbar_wait(&eb[s], (round - 1) & 1);
         mbar_arrive_expect_tx(&fb[s], bytes);
         if (is_a) {
-          const int m = static_cast<int>(t % r.m_tiles);
           if (r.w_tiled != nullptr) {
-            // one contiguous, pre-swizzled 16 KiB UMMA tile: a single bulk copy
+            // one contiguous, pre-swizzled 16 KiB UMMA tile: a_split bulk copies
             const uint8_t* src = r.w_tiled + (static_cast<int64_t>(m) * r.kb + kbi) * kAStageBytes;
-            bulk_g2s_stream(a_st + s * kAStageBytes, src, kAStageBytes, &fb[s], pol);
+            const uint32_t piece = kAStageBytes / r.a_split;
+            for (int pc = 0; pc < r.a_split; ++pc)
+              bulk_g2s_stream(a_st + s * kAStageBytes + pc * piece, src + pc * piece, piece, &fb[s], pol);
           } else {
             tma_load_2d(a_st + s * kAStageBytes, &tw, &fb[s], kbi * kBK, m * kBM, pol);
           }
         } else {
-          const int nt = static_cast<int>(t / r.m_tiles);
           tma_load_2d(b_st + s * b_stage_bytes, &tx, &fb[s], kbi * kBK, nt * r.n_tile, pol);
+        }
+        if (++s == SS) {
+          s = 0;
+          ++round;
+        }
+        if (++kbi == r.kb) {
+          kbi = 0;
+          if (++m == r.m_tiles) {
+            m = 0;
+            ++nt;
+          }
         }
       }
     }
@@ -205,6 +222,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     // ------------------------------------------------------ MMA issuer
     const uint32_t idesc = umma_idesc_bf16(kBM, r.n_tile);
     int i = 0, seg = 0;
+    int sa = 0, ra = 0, sb = 0, rb = 0;  // ring slots and their round parities
     int64_t it = it0;
     while (it < it1) {
       const int64_t t = it / r.kb;
@@ -215,10 +233,9 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       tc_fence_after();
       const uint32_t acc = tmem + static_cast<uint32_t>(b * r.n_tile);
       for (; it < seg_end; ++it, ++i) {
-        const int sa = i % SA, sb = i % SB;
-        mbar_wait(&full_a[sa], (i / SA) & 1);
+        mbar_wait(&full_a[sa], ra & 1);
         if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 32 + 4] = gtimer();
-        mbar_wait(&full_b[sb], (i / SB) & 1);
+        if (r.dbg_nomma < 2) mbar_wait(&full_b[sb], rb & 1);
         if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 32 + 5] = gtimer();
         tc_fence_after();
         if (elect_one()) {
@@ -226,15 +243,30 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           const uint32_t b_addr = smem_u32(b_st + sb * b_stage_bytes);
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
+            if (r.dbg_nomma) break;
             // Advance along K inside the swizzle atom: 16 bf16 = 32 bytes.
             umma_bf16(acc, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
                       (it != seg_begin || kk != 0) ? 1u : 0u);
           }
-          umma_commit(&empty_a[sa]);
-          umma_commit(&empty_b[sb]);
-          if (it == seg_end - 1) umma_commit(&tm_full[b]);
+          if (r.dbg_nomma) {  // debug: pure streaming rate (results are garbage)
+            mbar_arrive(&empty_a[sa]);
+            if (r.dbg_nomma < 2) mbar_arrive(&empty_b[sb]);
+            if (it == seg_end - 1) mbar_arrive(&tm_full[b]);
+          } else {
+            umma_commit(&empty_a[sa]);
+            umma_commit(&empty_b[sb]);
+            if (it == seg_end - 1) umma_commit(&tm_full[b]);
+          }
         }
         __syncwarp();
+        if (++sa == SA) {
+          sa = 0;
+          ++ra;
+        }
+        if (++sb == SB) {
+          sb = 0;
+          ++rb;
+        }
       }
       ++seg;
     }
@@ -539,6 +571,10 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   static const int env_sb = getenv("MUX_GEMM_SB") ? atoi(getenv("MUX_GEMM_SB")) : 0;
   static const int env_sa = getenv("MUX_GEMM_SA") ? atoi(getenv("MUX_GEMM_SA")) : 0;
   if (env_sb > 0) r.stages_b = env_sb;
+  static const int env_split = getenv("MUX_GEMM_ASPLIT") ? atoi(getenv("MUX_GEMM_ASPLIT")) : 1;
+  r.a_split = (env_split == 2 || env_split == 4 || env_split == 8) ? env_split : 1;
+  static const int env_nomma = getenv("MUX_GEMM_NOMMA") ? atoi(getenv("MUX_GEMM_NOMMA")) : 0;
+  r.dbg_nomma = env_nomma;
   r.stages_a = (kSmemBudget - r.stages_b * b_stage - 2 * kChunkBytes) / kAStageBytes;
   if (r.stages_a > 10) r.stages_a = 10;
   if (env_sa > 0 && env_sa < r.stages_a) r.stages_a = env_sa;
@@ -552,7 +588,11 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   int grid = a.grid > 0 ? a.grid : 148;
   // Enough k-blocks per CTA that the fixed per-CTA cost and the fixup
   // partials stay small next to the weight bytes it streams.
-  const int64_t min_iters = a.min_iters > 0 ? a.min_iters : 1;
+  int64_t min_iters = a.min_iters > 0 ? a.min_iters : 1;
+  // Residual epilogues reduce-add their pieces (no fixup): keep the whole
+  // machine streaming even for small projections (O of 7B: 2048 k-blocks).
+  static const int env_rmin = getenv("MUX_GEMM_RES_MIN_ITERS") ? atoi(getenv("MUX_GEMM_RES_MIN_ITERS")) : 8;
+  if (a.epi == Epilogue::kResidualAddF32) min_iters = std::min<int64_t>(min_iters, env_rmin);
   if (static_cast<int64_t>(grid) * min_iters > r.iters) grid = static_cast<int>(std::max<int64_t>(1, r.iters / min_iters));
   // Non-residual epilogues sum pieces in a fixer: keep every tile in <= 3
   // pieces (<= 2 partners) so their chunks fit the idle A ring.

@@ -17,12 +17,17 @@ print(" ".join(out), flush=True)
 
 if __name__ == "__main__":
     M = int(sys.argv[1]) if len(sys.argv) > 1 else 128
-    configs = [(0, 0)] + [tuple(map(int, c.split(","))) for c in sys.argv[2:]]
-    for sa, sb in configs:
+    configs = [(0, 0, 1)] + [tuple(map(int, c.split(","))) for c in sys.argv[2:]]
+    for cfg in configs:
+        sa, sb = cfg[0], cfg[1]
+        split = cfg[2] if len(cfg) > 2 else 1
         env = dict(os.environ)
+        env["MUX_GEMM_ASPLIT"] = str(split)
+        if len(cfg) > 3:
+            env["MUX_GEMM_NOMMA"] = str(cfg[3])
         if sa:
             env["MUX_GEMM_SA"] = str(sa)
         if sb:
             env["MUX_GEMM_SB"] = str(sb)
         r = subprocess.run([sys.executable, "-c", CODE, str(M)], env=env, capture_output=True, text=True)
-        print(f"M={M} SA={sa} SB={sb}: {r.stdout.strip()} {r.stderr.strip()[-300:]}", flush=True)
+        print(f"M={M} SA={sa} SB={sb} split={split}: {r.stdout.strip()} {r.stderr.strip()[-300:]}", flush=True)
