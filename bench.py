@@ -146,6 +146,7 @@ def run_ours(args, rank, world, local_rank):
                     init_seed=1 + rank, init_std=0.02, partitions=len(specs) + 1,
                     partition_sms=[0] + args.partition_sms if args.partition_sms else None)
     unit.set_option("pdl", args.pdl)
+    unit.set_option("chain", args.chain)
     unit.init_kv(seed=7 + rank, std=1.0)
     pool = unit.pool
     ids = []
@@ -244,6 +245,7 @@ def main():
     ap.add_argument("--partition-sms", type=lambda s: [int(x) for x in s.split(",")], default=None,
                     help="green-context SMs of each model's decode partition, e.g. 72,72")
     ap.add_argument("--serial", action="store_true", help="run the colocated decode jobs on one stream")
+    ap.add_argument("--chain", type=int, default=0, help="fused persistent layer chain for decode (experimental)")
     ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch between job kernels")
     ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg (profiling runs)")
     args = ap.parse_args()

@@ -597,6 +597,10 @@ int mux_rope_table(int positions, float* out) {
   });
 }
 
+void mux_debug_chain_timing(void* buf) { mux::chain_debug_timing(buf); }
+
+int mux_debug_chain_coop_pdl(void) { return mux::chain_coop_pdl() ? 1 : 0; }
+
 void mux_debug_gemm_timing(void* buf) { mux::gemm_debug_timing(buf); }
 
 int64_t mux_weight_tiled_bytes(int N, int K) { return static_cast<int64_t>(mux::weight_tiled_bytes(N, K)); }
@@ -979,6 +983,7 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
     const std::string k = key ? key : "";
     if (k == "gemm_min_iters") u->rt->set_gemm_min_iters(static_cast<int>(value));
     else if (k == "pdl") mux::pdl_enabled() = value != 0;
+    else if (k == "chain") u->rt->set_chain(value != 0);
     else throw std::invalid_argument("unknown option: " + k);
   });
 }

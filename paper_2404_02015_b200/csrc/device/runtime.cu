@@ -225,6 +225,13 @@ Workspace::Workspace(int max_tok, int max_batch_rows, int hidden, int qkv_cols, 
   attn = DevMem(Tp * heads * 128 * 2);
   act = DevMem(Tp * ffn * 2);
   gemm_partials = DevMem(gemm_partials_floats(grid) * 4);
+  const size_t chain_rows = std::max(max_batch_rows, 16);
+  gu32 = DevMem(chain_rows * 2 * ffn * 4);
+  qkv32 = DevMem(chain_rows * qkv_cols * 4);
+  chain_bar = DevMem(256);
+  check_cuda(cudaMemset(gu32.p, 0, gu32.bytes), "memset gu32");
+  check_cuda(cudaMemset(qkv32.p, 0, qkv32.bytes), "memset qkv32");
+  check_cuda(cudaMemset(chain_bar.p, 0, chain_bar.bytes), "memset chain bar");
   gemm_flags = DevMem(static_cast<size_t>(std::max(grid, 1024)) * 4);
   check_cuda(cudaMemset(gemm_flags.p, 0, gemm_flags.bytes), "memset flags");
   const size_t rows_out = std::max<size_t>(max_batch_rows, 256);
@@ -318,6 +325,7 @@ Runtime::Runtime(int device, int64_t pool_blocks, int max_pos)
   check_cuda(preload_gemm(), "preload");
   check_cuda(preload_prefill_attention(), "preload");
   check_cuda(preload_fused_ops(), "preload");
+  check_cuda(preload_layer_chain(), "preload");
   check_cuda(preload(gather_last_tok, scatter_last_tok), "preload");
   pool_ = DevMem(static_cast<size_t>(pool_blocks) * 4096);
   // RoPE table [max_pos][64][(cos, sin)], computed in double, stored fp32.
@@ -563,22 +571,83 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   ap.row_width = m.row_width();
   ap.rope_positions = max_pos_;
 
-  // Profiling aid (MUX_DEBUG_SKIP bitmask; results are garbage when set):
-  // 1 kv_append, 2 rmsnorm, 4 K1, 8 qkv, 16 o, 32 gate-up, 64 down.
-  static const int skip = getenv("MUX_DEBUG_SKIP") ? atoi(getenv("MUX_DEBUG_SKIP")) : 0;
-  for (int l = 0; l < L && skip != 0; ++l) {
-    if (!(skip & 8)) gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
-    ap.layer = l;
-    if (!(skip & 1)) check_cuda(kv_append(ap, stream), "kv_append");
-    at.layer = l;
-    if (!(skip & 4)) check_cuda(decode_attention(at, false, stream), "decode_attention");
-    if (!(skip & 16)) gemm(m.wo[l].p, ws.attn.p, n, hid, H * 128, ws.resid.p, hid, kEpiResidual, ws, stream);
-    if (!(skip & 2)) check_cuda(rmsnorm_rows(ws.resid.as<float>(), m.ffn_norm[l].as<float>(), ws.xn.p, n, hid, d.norm_eps, stream), "rmsnorm");
-    if (!(skip & 32)) gemm(m.wgu[l].p, ws.xn.p, n, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, ws, stream);
-    if (!(skip & 64)) gemm(m.wdown[l].p, ws.act.p, n, hid, d.ffn, ws.resid.p, hid, kEpiResidual, ws, stream);
-    if (!(skip & 2)) check_cuda(rmsnorm_rows(ws.resid.as<float>(), m.ffn_norm[l].as<float>(), ws.xn.p, n, hid, d.norm_eps, stream), "rmsnorm");
+  // Fused path (single rank, decode batch <= 256): per layer one K1 launch
+  // and one persistent layer-chain launch (layer_chain.cu).
+  if (chain_enabled_ && d.tp_size == 1 && n <= 256) {
+    auto job = [&](const DevMem& w, int N, int K, int post, const float* norm_w, const void* x, void* out,
+                   ChainArgs& c) {
+      const int j = c.n_jobs++;
+      c.job[j] = ChainJob{};
+      c.job[j].w = w.as<uint8_t>();
+      c.job[j].N = N;
+      c.job[j].K = K;
+      c.job[j].post = post;
+      c.job[j].norm_w = norm_w;
+      c.tmap_x[j] = act_tmap(x, std::max(n, 256), K, gemm_n_tile(n));
+      c.tmap_out[j] = out_tmap(out, kEpiResidual, n, N, N);
+    };
+    ChainArgs base{};
+    base.M = n;
+    base.grid = ws.sms;
+    base.bar = ws.chain_bar.as<unsigned>();
+    ChainPost& p = base.post;
+    p.resid = ws.resid.as<float>();
+    p.xn = ws.xn.as<__nv_bfloat16>();
+    p.hidden = hid;
+    p.eps = d.norm_eps;
+    p.gu32 = ws.gu32.as<float>();
+    p.act = ws.act.as<__nv_bfloat16>();
+    p.ffn = d.ffn;
+    p.qkv32 = ws.qkv32.as<float>();
+    p.q = ws.q.as<__nv_bfloat16>();
+    p.heads = H;
+    p.slots = ws.slots;
+    p.ctx = ws.ctx;
+    p.rope = rope_.as<float>();
+    p.rope_positions = max_pos_;
+    p.pool = pool_.p;
+    p.rowlist = m.rowlist.as<int32_t>();
+    p.rowrec = m.rowrec.as<int32_t>();
+    p.row_width = m.row_width();
+    p.max_rows = m.max_rows();
+    auto run = [&](ChainArgs& c) {
+      c.bar_base = ws.chain_base;
+      check_cuda(layer_chain(c, stream), "layer_chain");
+      ws.chain_base += 2u * static_cast<unsigned>(c.n_jobs) * static_cast<unsigned>(c.grid);
+      launches_ += 1;
+    };
+    {  // layer 0's QKV + RoPE + KV append
+      ChainArgs c = base;
+      c.post.layer = 0;
+      job(m.wqkv[0], m.qkv_cols(), hid, kPostQkvAppend, nullptr, ws.xn.p, ws.qkv32.p, c);
+      run(c);
+    }
+    for (int l = 0; l < L; ++l) {
+      at.layer = l;
+      cudaEvent_t e0 = nullptr, e1 = nullptr;
+      if (timer) {
+        e0 = timer->get();
+        e1 = timer->get();
+        check_cuda(cudaEventRecord(e0, stream), "timer");
+      }
+      check_cuda(decode_attention(at, false, stream), "decode_attention");
+      launches_ += at.splits > 1 ? 2 : 1;
+      if (timer) {
+        check_cuda(cudaEventRecord(e1, stream), "timer");
+        timer->pending.emplace_back(e0, e1);
+        timer->pending_bytes += attn_bytes;
+      }
+      const float* next_norm = l + 1 < L ? m.attn_norm[l + 1].as<float>() : m.final_norm.as<float>();
+      ChainArgs c = base;
+      c.post.layer = l + 1;
+      job(m.wo[l], hid, H * 128, kPostNorm, m.ffn_norm[l].as<float>(), ws.attn.p, ws.resid.p, c);
+      job(m.wgu[l], 2 * d.ffn, hid, kPostSilu, nullptr, ws.xn.p, ws.gu32.p, c);
+      job(m.wdown[l], hid, d.ffn, kPostNorm, next_norm, ws.act.p, ws.resid.p, c);
+      if (l + 1 < L) job(m.wqkv[l + 1], m.qkv_cols(), hid, kPostQkvAppend, nullptr, ws.xn.p, ws.qkv32.p, c);
+      run(c);
+    }
   }
-  for (int l = 0; l < L && skip == 0; ++l) {
+  for (int l = 0; l < L && !(chain_enabled_ && d.tp_size == 1 && n <= 256); ++l) {
     gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
     ap.layer = l;
     check_cuda(kv_append(ap, stream), "kv_append");

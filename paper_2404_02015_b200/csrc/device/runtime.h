@@ -135,6 +135,10 @@ struct Workspace {
   int gemm_epoch = 0;
   int sms = 148;           // SMs of the partition this workspace's jobs run on
   std::unique_ptr<TpLink> tp;  // tensor-parallel mailbox (tp_size > 1)
+  // fused layer chain: fp32 reduce-add targets (kept zero between uses) and
+  // the grid-barrier counter with its running base
+  DevMem gu32, qkv32, chain_bar;
+  unsigned chain_base = 0;
   PinnedMem host_ints[2];  // double-buffered staging for per-job metadata
   cudaEvent_t staged[2] = {nullptr, nullptr};
   int cur = 0;
@@ -174,6 +178,7 @@ class Runtime {
   int num_sms() const { return num_sms_; }
   int64_t launches() const { return launches_; }
   void set_gemm_min_iters(int v) { gemm_min_iters_ = v; }
+  void set_chain(bool on) { chain_enabled_ = on; }
   void count_launch(int64_t n = 1) { launches_ += n; }
 
   // Cached tensor map for an activation buffer viewed as rows x cols bf16.
@@ -208,6 +213,7 @@ class Runtime {
   int max_pos_;
   int64_t launches_ = 0;
   int gemm_min_iters_ = 24;
+  bool chain_enabled_ = false;  // measured slower than separate launches so far
   DevMem pool_;
   DevMem rope_;
   struct StageSlot {

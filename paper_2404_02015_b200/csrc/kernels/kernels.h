@@ -2,6 +2,7 @@
 #pragma once
 
 #include <cstdint>
+#include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
 namespace mux {
@@ -100,6 +101,42 @@ void gemm_debug_timing(void* buf);  // [grid][4] u64 globaltimer stamps per CTA,
 bool make_tmap_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t cols,
                     uint64_t row_stride_bytes, uint32_t box_rows);
 
+// ---- fused decode layer chain (layer_chain.cu) -----------------------------
+// The projections of a decode layer between two attention launches in one
+// persistent cooperative tcgen05 kernel; every job reduce-adds fp32 into its
+// output, then an element-wise step runs on all CTAs after a grid barrier.
+constexpr int kChainMaxJobs = 6;
+enum ChainPostKind : int { kPostNone = 0, kPostNorm = 1, kPostSilu = 2, kPostQkvAppend = 3 };
+struct ChainJob {
+  const uint8_t* w;        // weights in weight_tile() layout
+  int N, K;                // D[M x N] += X[M x K] W[N x K]^T
+  int post;                // ChainPostKind, run after this job
+  const float* norm_w;     // kPostNorm: RMSNorm weight
+  int kb, m_tiles;         // filled by layer_chain()
+  int64_t iters;
+};
+struct ChainPost {
+  float* resid; __nv_bfloat16* xn; int hidden; float eps;   // norm: resid -> xn
+  float* gu32; __nv_bfloat16* act; int ffn;                  // silu: gu32 [M][2ffn] -> act [M][ffn]
+  float* qkv32; __nv_bfloat16* q; int heads;                 // qkv: qkv32 [M][3][H][128] -> q, pool
+  const int32_t* slots; const int32_t* ctx;                  // per member: table slot, ctx incl. new token
+  const float* rope; int rope_positions;
+  void* pool; const int32_t* rowlist; const int32_t* rowrec; int row_width, max_rows, layer;
+};
+struct ChainArgs {
+  int n_jobs;
+  ChainJob job[kChainMaxJobs];
+  const void* tmap_x[kChainMaxJobs];    // B operand maps (bf16, box rows = gemm_pick_n_tile(M))
+  const void* tmap_out[kChainMaxJobs];  // fp32 reduce-add maps (make_tmap_gemm_out, residual epilogue)
+  int M, grid;
+  unsigned* bar;                        // grid-barrier counter (monotonic)
+  unsigned bar_base;                    // its value before this launch; the launch adds 2 * n_jobs * grid
+  ChainPost post;
+};
+cudaError_t layer_chain(const ChainArgs& a, cudaStream_t stream);
+void chain_debug_timing(void* buf);  // [grid][64] u64 globaltimer stamps of every launch, null = off
+bool chain_coop_pdl();               // false once the driver refused cooperative + PDL together
+
 // ---- K5 small fused ops ---------------------------------------------------
 cudaError_t embed_rmsnorm(const void* emb, const int32_t* tokens, const float* norm_w,
                           float* resid, void* xn, int T, int hidden, float eps,
@@ -143,5 +180,6 @@ cudaError_t preload_kv_append();
 cudaError_t preload_gemm();
 cudaError_t preload_prefill_attention();
 cudaError_t preload_fused_ops();
+cudaError_t preload_layer_chain();
 
 }  // namespace mux

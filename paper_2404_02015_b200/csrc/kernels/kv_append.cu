@@ -14,42 +14,12 @@
 #include "kernels.h"
 #include "ptx.cuh"
 #include "launch.cuh"
+#include "rope.cuh"
 
 namespace mux {
 namespace {
 
 constexpr int kDim = 128;
-
-__device__ __forceinline__ void unpack4(uint2 v, float (&x)[4]) {
-  x[0] = bf16_lo(v.x);
-  x[1] = bf16_hi(v.x);
-  x[2] = bf16_lo(v.y);
-  x[3] = bf16_hi(v.y);
-}
-
-__device__ __forceinline__ uint2 pack4(const float (&x)[4]) {
-  return make_uint2(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]));
-}
-
-// rotate_half RoPE on 4 dims held by this lane; partner dims live in lane^16.
-// Explicit _rn intrinsics: no FMA contraction, so the CPU oracle's float32
-// arithmetic reproduces it bit for bit.
-__device__ __forceinline__ void rope4(float (&x)[4], const float* cs, int lane) {
-  float other[4];
-#pragma unroll
-  for (int k = 0; k < 4; ++k) other[k] = __shfl_xor_sync(0xffffffffu, x[k], 16);
-  const int f0 = (lane & 15) * 4;
-#pragma unroll
-  for (int k = 0; k < 4; ++k) {
-    const float c = cs[2 * (f0 + k)];
-    const float s = cs[2 * (f0 + k) + 1];
-    if (lane < 16) {
-      x[k] = __fsub_rn(__fmul_rn(x[k], c), __fmul_rn(other[k], s));
-    } else {
-      x[k] = __fadd_rn(__fmul_rn(x[k], c), __fmul_rn(other[k], s));
-    }
-  }
-}
 
 __global__ void __launch_bounds__(256) kv_append_kernel(const AppendArgs a) {
   grid_dep_wait();

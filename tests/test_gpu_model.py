@@ -290,3 +290,38 @@ def test_tensor_parallel_tp2_fused_allreduce(cuda):
     finally:
         for u in units:
             u.close()
+
+
+def test_decode_fused_layer_chain_matches_oracle(tiny_unit):
+    """The experimental fused decode path (one persistent cooperative
+    layer-chain launch per layer: O, gate-up, down, next QKV with RMSNorm,
+    SiLU and RoPE + KV append between grid barriers) keeps greedy-token
+    parity with the oracle."""
+    unit, specs, refs = tiny_unit
+    unit.set_option("chain", 1)
+    try:
+        for llm in (0, 1):
+            rng = np.random.default_rng(40 + llm)
+            lens = [3, 16, 33, 90]
+            rids = [30000 + 100 * llm + i for i in range(len(lens))]
+            for rid, n in zip(rids, lens):
+                assert unit.pool.admit(llm, rid, n, n + 12).ok
+            prompts = [rng.integers(0, specs[llm].vocab, n).astype(np.int32) for n in lens]
+            first = np.zeros(len(lens), np.int32)
+            unit.prefill(llm, rids, np.concatenate(prompts), first, partition=0)
+            unit.sync()
+            gen = [[int(t)] for t in first]
+            out = np.zeros(len(lens), np.int32)
+            for _ in range(12):
+                for rid in rids:
+                    assert unit.pool.alloc(llm, rid, 1, False).ok
+                unit.decode(llm, rids, out=out, partition=1)
+                unit.sync()
+                for i, t in enumerate(out):
+                    gen[i].append(int(t))
+            for i in range(len(lens)):
+                check_tokens(refs[llm], prompts[i], gen[i])
+            for rid in rids:
+                unit.pool.free_request(llm, rid)
+    finally:
+        unit.set_option("chain", 0)
