@@ -14,9 +14,10 @@
 //   O_j = P_j V_j      UMMA 128x128x128, A = P_j (bf16, written to smem by the
 //                      softmax in the canonical SW128 K-major image), B = V_j
 //                      (smem, MN-major: the same TMA box as K, other descriptor)
-// Warp 4 = TMA producer + MMA issuer (one elected lane); warps 0-3 = softmax,
-// thread i owns query row i (TMEM lane i): online max/sum in fp32, causal +
-// sequence-end masking. The output accumulates in TMEM across key tiles; when
+// Warp 8 = TMA producer + MMA issuer (one elected lane); warps 0-7 = softmax,
+// two warps per TMEM lane quarter, a thread owns half (64 keys / 64 output
+// dims) of one query row: online max/sum in fp32, causal + sequence-end
+// masking. The output accumulates in TMEM across key tiles; when
 // a row's max moves, its O row is rescaled in place (tcgen05.ld/st) before
 // the next P V is issued.
 // K/V tiles stream through a 2-stage TMA ring (SWIZZLE_128B boxes of 64 dims
@@ -40,20 +41,26 @@ constexpr int kTile = 128;                   // queries per CTA, keys per KV til
 constexpr int kHalfBytes = kTile * 64 * 2;   // one 64-dim SW128 half of a tile: 16 KiB
 constexpr int kTileBytes = 2 * kHalfBytes;   // 128 x 128 bf16
 constexpr int kStages = 2;
-constexpr int kThreads = 160;                // 4 softmax warps + 1 TMA/MMA warp
+constexpr int kSoftmaxWarps = 8;             // 2 per TMEM lane quarter: each owns 64 of a row's 128 keys
+constexpr int kThreads = (kSoftmaxWarps + 1) * 32;  // + 1 TMA/MMA warp
 constexpr uint32_t kTmemCols = 512;          // S0 [0,128) S1 [128,256) O [256,384)
 constexpr size_t kSmemBytes = 1024 + kTileBytes /*Q*/ + kStages * 2 * kTileBytes /*K,V*/ +
-                              kTileBytes /*P*/ + 256 /*barriers*/;
+                              kTileBytes /*P*/ + 256 /*barriers*/ + 4 * 2 * 128 * 4 /*row exchange*/;
 
 struct Bars {
   uint64_t q_full;
-  uint64_t kv_full[kStages];
-  uint64_t kv_empty[kStages];
+  uint64_t k_full[kStages];
+  uint64_t k_empty[kStages];
+  uint64_t v_full[kStages];
+  uint64_t v_empty[kStages];
   uint64_t s_full[2];
   uint64_t s_empty[2];
   uint64_t p_full;
   uint64_t o_full;
   uint32_t tmem;
+  uint32_t pad[3];
+  float mx[2][2][128];  // [tile parity][key half][row]: partial row maxima
+  float ls[2][128];     // [key half][row]: partial row sums (end)
 };
 
 // MN-major SW128 descriptor (B = V: N = head dims contiguous, K = keys):
@@ -86,14 +93,16 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
   if (threadIdx.x == 0) {
     mbar_init(&bar.q_full, 1);
     for (int s = 0; s < kStages; ++s) {
-      mbar_init(&bar.kv_full[s], 1);
-      mbar_init(&bar.kv_empty[s], 1);
+      mbar_init(&bar.k_full[s], 1);
+      mbar_init(&bar.k_empty[s], 1);
+      mbar_init(&bar.v_full[s], 1);
+      mbar_init(&bar.v_empty[s], 1);
     }
     for (int s = 0; s < 2; ++s) {
       mbar_init(&bar.s_full[s], 1);
-      mbar_init(&bar.s_empty[s], 4);
+      mbar_init(&bar.s_empty[s], kSoftmaxWarps);
     }
-    mbar_init(&bar.p_full, 4);
+    mbar_init(&bar.p_full, kSoftmaxWarps);
     mbar_init(&bar.o_full, 1);
     fence_barrier_init();
   }
@@ -110,7 +119,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
   const int q0 = qt * kTile;                // sequence-local index of query row 0
   const int n_kv = qt + 1;                  // causal: key tiles 0..qt
 
-  if (warp == 4) {
+  if (warp == kSoftmaxWarps) {
     if (elect_one()) {
       // ---------------- TMA producer + MMA issuer
       const uint64_t pol_q = policy_evict_first();
@@ -118,24 +127,32 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
       mbar_arrive_expect_tx(&bar.q_full, kTileBytes);
       for (int hh = 0; hh < 2; ++hh)
         tma_load_2d(q_s + hh * kHalfBytes, &tq, &bar.q_full, h * 128 + hh * 64, s0 + q0, pol_q);
-      auto load_kv = [&](int j) {
+      // K and V of a tile have separate ring slots and barriers: K_j's slot
+      // frees when S_j = Q K_j^T completes (early), V_j's when P_j V_j does,
+      // so the next K load never waits behind a P V.
+      auto load_k = [&](int j) {
         const int st = j % kStages;
-        if (j >= kStages) mbar_wait(&bar.kv_empty[st], ((j / kStages) - 1) & 1);
+        if (j >= kStages) mbar_wait(&bar.k_empty[st], ((j / kStages) - 1) & 1);
         uint8_t* dst = kv_s + st * 2 * kTileBytes;
-        mbar_arrive_expect_tx(&bar.kv_full[st], 2 * kTileBytes);
-        for (int hh = 0; hh < 2; ++hh) {
-          tma_load_2d(dst + hh * kHalfBytes, &tkv, &bar.kv_full[st], (a.H + h) * 128 + hh * 64,
-                      s0 + j * kTile, pol_kv);
-          tma_load_2d(dst + kTileBytes + hh * kHalfBytes, &tkv, &bar.kv_full[st],
-                      (2 * a.H + h) * 128 + hh * 64, s0 + j * kTile, pol_kv);
-        }
+        mbar_arrive_expect_tx(&bar.k_full[st], kTileBytes);
+        for (int hh = 0; hh < 2; ++hh)
+          tma_load_2d(dst + hh * kHalfBytes, &tkv, &bar.k_full[st], (a.H + h) * 128 + hh * 64, s0 + j * kTile, pol_kv);
+      };
+      auto load_v = [&](int j) {
+        const int st = j % kStages;
+        if (j >= kStages) mbar_wait(&bar.v_empty[st], ((j / kStages) - 1) & 1);
+        uint8_t* dst = kv_s + st * 2 * kTileBytes + kTileBytes;
+        mbar_arrive_expect_tx(&bar.v_full[st], kTileBytes);
+        for (int hh = 0; hh < 2; ++hh)
+          tma_load_2d(dst + hh * kHalfBytes, &tkv, &bar.v_full[st], (2 * a.H + h) * 128 + hh * 64, s0 + j * kTile,
+                      pol_kv);
       };
       const uint32_t idesc_qk = umma_idesc_bf16(kTile, kTile);
       const uint32_t idesc_pv = umma_idesc_bf16(kTile, 128) | (1u << 16);  // B (V) MN-major
       const uint32_t q_addr = smem_u32(q_s), p_addr = smem_u32(p_s);
       auto issue_qk = [&](int j) {
         const int st = j % kStages, sb = j & 1;
-        mbar_wait(&bar.kv_full[st], (j / kStages) & 1);
+        mbar_wait(&bar.k_full[st], (j / kStages) & 1);
         if (j >= 2) mbar_wait(&bar.s_empty[sb], ((j >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(kv_s + st * 2 * kTileBytes);
@@ -146,17 +163,24 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
                     kk > 0 ? 1u : 0u);
         }
         umma_commit(&bar.s_full[sb]);
+        umma_commit(&bar.k_empty[st]);
       };
-      load_kv(0);
-      if (n_kv > 1) load_kv(1);
+      load_k(0);
+      load_v(0);
+      if (n_kv > 1) {
+        load_k(1);
+        load_v(1);
+      }
       mbar_wait(&bar.q_full, 0);
       issue_qk(0);
       for (int j = 0; j < n_kv; ++j) {
         if (j + 1 < n_kv) issue_qk(j + 1);
+        if (j + 1 < n_kv && j + 1 >= kStages) load_v(j + 1);  // waits for P_{j-1} V_{j-1}
         // O_j = P_j V_j once the softmax has written P_j
         mbar_wait(&bar.p_full, j & 1);
-        tc_fence_after();
         const int st = j % kStages;
+        mbar_wait(&bar.v_full[st], (j / kStages) & 1);
+        tc_fence_after();
         const uint32_t v_addr = smem_u32(kv_s + st * 2 * kTileBytes + kTileBytes);
 #pragma unroll
         for (int kk = 0; kk < 8; ++kk) {
@@ -164,35 +188,43 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
                     umma_desc_sw128_mn(v_addr + kk * 2048), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
         }
         umma_commit(&bar.o_full);
-        umma_commit(&bar.kv_empty[st]);
-        if (j + kStages < n_kv) load_kv(j + kStages);
+        umma_commit(&bar.v_empty[st]);
+        if (j + kStages < n_kv) load_k(j + kStages);  // S_j done long ago: no stall
       }
     }
     __syncwarp();
   } else {
-    // ---------------- softmax warps: thread = query row
-    const int row = warp * 32 + lane;
+    // ---------------- softmax warps: thread = (query row, key half)
+    // Warps w and w+4 share TMEM lane quarter w%4 (rows 32*(w%4)..+31) and
+    // split the 128 keys of a tile (and the 128 output dims) in halves; the
+    // row max is exchanged through smem once per tile (double-buffered by
+    // tile parity, so one barrier per tile), the row sums once at the end.
+    const int quarter = warp & 3, hf = warp >> 2;
+    const int row = quarter * 32 + lane;
     const int qi = q0 + row;               // sequence-local query index
-    const uint32_t lane_base = static_cast<uint32_t>(warp * 32) << 16;
+    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     float m_run = -INFINITY, l_run = 0.f;
-    uint8_t* p_row = p_s + row * 128;
-    const uint32_t o_addr = tmem + lane_base + 2 * kTile;
+    uint8_t* p_row = p_s + hf * kHalfBytes + row * 128;
+    const uint32_t o_addr = tmem + lane_base + 2 * kTile + hf * 64;
     for (int j = 0; j < n_kv; ++j) {
       const int sb = j & 1;
       mbar_wait(&bar.s_full[sb], (j >> 1) & 1);
       tc_fence_after();
-      const uint32_t s_addr = tmem + lane_base + sb * kTile;
-      const int kmax = min(qi, len - 1) - j * kTile;  // keys [0, kmax] of this tile are visible
-      // pass 1: row max
+      const uint32_t s_addr = tmem + lane_base + sb * kTile + hf * 64;
+      const int kmax = min(qi, len - 1) - j * kTile - hf * 64;  // keys [0, kmax] of this half are visible
+      // pass 1: partial row max over this half, exchanged with the partner warp
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         float v[32];
         tmem_ld_32x32b_x32(s_addr + c * 32, v);
 #pragma unroll
         for (int i = 0; i < 32; ++i)
           if (c * 32 + i <= kmax) mx = fmaxf(mx, v[i]);
       }
+      bar.mx[j & 1][hf][row] = mx;
+      asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
+      mx = fmaxf(mx, bar.mx[j & 1][hf ^ 1][row]);
       const float m_new = fmaxf(m_run, mx * a.scale_log2);
       const float m_use = m_new == -INFINITY ? 0.f : m_new;
       const float alpha = exp2f(m_run - m_use);
@@ -202,7 +234,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         tc_fence_after();
         if (!__all_sync(0xffffffffu, alpha == 1.f)) {
 #pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
+          for (int c = 0; c < 2; ++c) {
             float v[32];
             tmem_ld_32x32b_x32(o_addr + c * 32, v);
 #pragma unroll
@@ -211,10 +243,10 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
           }
         }
       }
-      // pass 2: P = exp2(s - m) -> bf16 in the SW128 K-major image
+      // pass 2: P = exp2(s - m) -> bf16 in the SW128 K-major image (this half's 64 keys)
       float psum = 0.f;
 #pragma unroll
-      for (int c = 0; c < 4; ++c) {
+      for (int c = 0; c < 2; ++c) {
         float v[32];
         tmem_ld_32x32b_x32(s_addr + c * 32, v);
         uint32_t pk[16];
@@ -225,12 +257,11 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
           psum += p0 + p1;
           pk[i >> 1] = pack_bf16(p0, p1);
         }
-        // keys [32c, 32c+32): half c/2, 16-byte chunks (c%2)*4 .. +4
-        uint8_t* half = p_row + (c >> 1) * kHalfBytes;
+        // keys [64hf + 32c, +32): 16-byte chunks c*4 .. +4 of this half's row
 #pragma unroll
         for (int u = 0; u < 4; ++u) {
-          const int chunk = (c & 1) * 4 + u;
-          *reinterpret_cast<uint4*>(half + ((chunk ^ (row & 7)) << 4)) =
+          const int chunk = c * 4 + u;
+          *reinterpret_cast<uint4*>(p_row + ((chunk ^ (row & 7)) << 4)) =
               make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
         }
       }
@@ -244,13 +275,16 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         mbar_arrive(&bar.p_full);
       }
     }
+    bar.ls[hf][row] = l_run;
+    asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
+    const float l_tot = l_run + bar.ls[hf ^ 1][row];
     mbar_wait(&bar.o_full, (n_kv - 1) & 1);
     tc_fence_after();
-    const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
+    const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) +
-                                          (static_cast<int64_t>(s0 + qi) * a.H + h) * 128);
+                                          (static_cast<int64_t>(s0 + qi) * a.H + h) * 128 + hf * 64);
 #pragma unroll
-    for (int c = 0; c < 4; ++c) {
+    for (int c = 0; c < 2; ++c) {
       float v[32];
       tmem_ld_32x32b_x32(o_addr + c * 32, v);  // all lanes: .sync.aligned
       if (qi < len) {
