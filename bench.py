@@ -245,6 +245,8 @@ def main():
     ap.add_argument("--partition-sms", type=lambda s: [int(x) for x in s.split(",")], default=None,
                     help="green-context SMs of each model's decode partition, e.g. 72,72")
     ap.add_argument("--serial", action="store_true", help="run the colocated decode jobs on one stream")
+    ap.add_argument("--serve-horizon", type=float, default=3.0,
+                    help="seconds of Poisson arrivals for the auxiliary measured serving run (0 = skip)")
     ap.add_argument("--chain", type=int, default=0, help="fused persistent layer chain for decode (experimental)")
     ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch between job kernels")
     ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg (profiling runs)")
@@ -282,6 +284,16 @@ def main():
     if rank == 0 and world == 1 and not args.skip_cpu:
         from bench_cpu import cpu_baseline
         cpu = cpu_baseline(args)
+    serving = None
+    if rank == 0 and world == 1 and args.serve_horizon > 0:
+        # the whole serving loop (ADBS engine, prefill + decode jobs, measured
+        # device time) on the same two models: auxiliary, not the headline
+        try:
+            import serve
+            serving = serve.serve(args.models.split(","), (120.0, 60.0)[:len(args.models.split(","))],
+                                  args.serve_horizon, seed=3, device=local_rank)
+        except Exception as e:  # pragma: no cover - reported, never fatal for the headline
+            serving = {"error": f"{type(e).__name__}: {e}"}
     if rank == 0:
         # whole-job roofline: every rank streams its own weights + KV per step
         step_roof = per_step_tokens / (r["bytes_step"] / (hbm * 1e9)) if r["bytes_step"] else None
@@ -318,6 +330,7 @@ def main():
             "step_roofline": {"tokens_per_s_at_peak": round(step_roof, 1) if step_roof else None,
                               "frac": round(value / step_roof, 4) if step_roof else None},
             "cpu_baseline": cpu,
+            "serving": serving,
             "gpu_launches": r["launches"] * world,
             "clocks": r["clocks"],
         }

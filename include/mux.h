@@ -302,6 +302,15 @@ MUX_API int mux_unit_run_lockstep(mux_unit* unit, const mux_sim_config* cfg, int
                           const mux_llm_entry* entries, int n_requests, const mux_request* trace,
                           uint64_t prompt_seed, mux_record* records_out, int32_t* tokens_out);
 
+/* Measured run: the same engine and ADBS decisions process,
+ * but every job's completion time is its measured device time (CUDA events
+ * from the start of its scheduling pass, the pass's jobs running concurrently
+ * on their partitions) instead of the pricing model's. Records then carry
+ * real TTFT / latency; throughput = tokens / last done time. */
+MUX_API int mux_unit_run_measured(mux_unit* unit, const mux_sim_config* cfg, int n_entries,
+                                  const mux_llm_entry* entries, int n_requests, const mux_request* trace,
+                                  uint64_t prompt_seed, mux_record* records_out, int32_t* tokens_out);
+
 #ifdef __cplusplus
 }
 #endif

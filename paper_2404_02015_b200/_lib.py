@@ -135,6 +135,8 @@ _SIGS = {
     "mux_unit_launches": (i64, [vp]),
     "mux_unit_run_lockstep": (C.c_int, [vp, P(SimConfig), C.c_int, P(LlmEntry), C.c_int,
                                         P(Request), u64, P(Record), P(i32)]),
+    "mux_unit_run_measured": (C.c_int, [vp, P(SimConfig), C.c_int, P(LlmEntry), C.c_int,
+                                        P(Request), u64, P(Record), P(i32)]),
 }
 
 

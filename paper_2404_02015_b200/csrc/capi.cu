@@ -252,15 +252,30 @@ namespace {
 // the unit's GPU; completion is consumed only after the device finished.
 class GpuExecutor : public muxsim::JobExecutor {
  public:
-  GpuExecutor(mux_unit* u, uint64_t prompt_seed, const std::vector<muxsim::Request>& trace)
-      : u_(u), seed_(prompt_seed) {
+  GpuExecutor(mux_unit* u, uint64_t prompt_seed, const std::vector<muxsim::Request>& trace, bool measured = false)
+      : u_(u), seed_(prompt_seed), measured_(measured) {
     for (size_t i = 0; i < trace.size(); ++i) row_of_id_[trace[i].id] = static_cast<int>(i);
     tokens_.resize(trace.size());
     check(cudaEventCreateWithFlags(&tables_ready_, cudaEventDisableTiming));
+    check(cudaEventCreate(&pass_start_));
   }
   ~GpuExecutor() override {
     for (auto& kv : jobs_) cudaEventDestroy(kv.second.done);
     cudaEventDestroy(tables_ready_);
+    cudaEventDestroy(pass_start_);
+  }
+
+  bool measured() const override { return measured_; }
+
+  // Device time from the start of the pass (its block-table upload included)
+  // to the end of this job, waiting for it.
+  double measure(int, std::int64_t job_id) override {
+    auto it = jobs_.find(job_id);
+    if (it == jobs_.end()) throw std::logic_error("measured: unknown job");
+    check(cudaEventSynchronize(it->second.done));
+    float ms = 0.f;
+    check(cudaEventElapsedTime(&ms, pass_start_, it->second.done));
+    return static_cast<double>(ms);
   }
 
   void attach_unit(int, const std::vector<const muxsim::LLMSpec*>& specs, BlockPool& pool) override {
@@ -275,6 +290,7 @@ class GpuExecutor : public muxsim::JobExecutor {
 
   void begin_pass(int, BlockPool& pool) override {
     cudaStream_t s0 = u_->streams[0];
+    if (measured_) check(cudaEventRecord(pass_start_, s0));
     for (int i = 0; i < static_cast<int>(u_->models.size()); ++i)
       u_->rt->upload_rows(pool, i, *u_->models[i], s0);
     check(cudaEventRecord(tables_ready_, s0));
@@ -315,7 +331,7 @@ class GpuExecutor : public muxsim::JobExecutor {
       u_->rt->decode(m, ws, n, slots.data(), aux.data(), nullptr, job.out->as<int32_t>(), s,
                      u_->timing ? &u_->timer : nullptr);
     }
-    check(cudaEventCreateWithFlags(&job.done, cudaEventDisableTiming));
+    check(cudaEventCreateWithFlags(&job.done, measured_ ? cudaEventDefault : cudaEventDisableTiming));
     check(cudaEventRecord(job.done, s));
     job.llm = j.llm;
     job.global_ids.resize(n);
@@ -352,6 +368,8 @@ class GpuExecutor : public muxsim::JobExecutor {
   static void check(cudaError_t e) { mux::check_cuda(e, "lockstep executor"); }
   mux_unit* u_;
   uint64_t seed_;
+  bool measured_ = false;
+  cudaEvent_t pass_start_ = nullptr;
   std::unordered_map<int64_t, int> row_of_id_;
   std::vector<std::vector<int32_t>> tokens_;
   std::unordered_map<int64_t, Job> jobs_;
@@ -988,14 +1006,15 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
   });
 }
 
-int mux_unit_run_lockstep(mux_unit* u, const mux_sim_config* cfg, int n_entries, const mux_llm_entry* entries,
-                          int n_requests, const mux_request* trace, uint64_t prompt_seed, mux_record* records_out,
-                          int32_t* tokens_out) {
+namespace {
+int run_unit(mux_unit* u, const mux_sim_config* cfg, int n_entries, const mux_llm_entry* entries, int n_requests,
+             const mux_request* trace, uint64_t prompt_seed, mux_record* records_out, int32_t* tokens_out,
+             bool measured) {
   return guarded([&] {
     require(cfg->n_units == 1, "lockstep: single-unit placements only");
     require(n_entries == static_cast<int>(u->models.size()), "lockstep: entries must describe the unit's models");
     SimInputs in = build_inputs(cfg, n_entries, entries, n_requests, trace);
-    GpuExecutor exec(u, prompt_seed, in.trace);
+    GpuExecutor exec(u, prompt_seed, in.trace, measured);
     muxsim::SimResult res =
         muxsim::run_simulation(in.cluster, in.placement, in.entries, in.trace, in.prof, in.params, &exec);
     export_records(res, in, records_out);
@@ -1011,6 +1030,19 @@ int mux_unit_run_lockstep(mux_unit* u, const mux_sim_config* cfg, int n_entries,
       }
     }
   });
+}
+}  // namespace
+
+int mux_unit_run_lockstep(mux_unit* u, const mux_sim_config* cfg, int n_entries, const mux_llm_entry* entries,
+                          int n_requests, const mux_request* trace, uint64_t prompt_seed, mux_record* records_out,
+                          int32_t* tokens_out) {
+  return run_unit(u, cfg, n_entries, entries, n_requests, trace, prompt_seed, records_out, tokens_out, false);
+}
+
+int mux_unit_run_measured(mux_unit* u, const mux_sim_config* cfg, int n_entries, const mux_llm_entry* entries,
+                          int n_requests, const mux_request* trace, uint64_t prompt_seed, mux_record* records_out,
+                          int32_t* tokens_out) {
+  return run_unit(u, cfg, n_entries, entries, n_requests, trace, prompt_seed, records_out, tokens_out, true);
 }
 
 }  // extern "C"

@@ -103,6 +103,11 @@ class JobExecutor {
   // executor must make sure the job's device work has finished.
   virtual void retire(int unit, std::int64_t job_id) = 0;
   virtual void detach_unit(int unit) = 0;
+  // Measured mode: job durations come from the device instead
+  // of the pricing model. After all launches of a scheduling pass the engine
+  // asks for each job's measured milliseconds (the executor waits for it).
+  virtual bool measured() const { return false; }
+  virtual double measure(int unit, std::int64_t job_id) { (void)unit; (void)job_id; return 0.0; }
 };
 
 SimResult run_simulation(const Cluster& cluster, const PlacementResult& placement,

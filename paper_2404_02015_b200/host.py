@@ -429,8 +429,9 @@ class Unit:
 
     def run_lockstep(self, entries: Sequence[Entry], trace: Sequence[TraceRequest],
                      gpu_memory_bytes: int, params: EngineParams | None = None,
-                     prompt_seed: int = 11, num_sm: float = 0.5, profile=None):
-        """Engine decisions priced by the oracle model, every job run on this GPU.
+                     prompt_seed: int = 11, num_sm: float = 0.5, profile=None, measured: bool = False):
+        """Engine decisions priced by the oracle model, every job run on this GPU
+        (measured=True: job durations are the measured device times instead).
         Returns (records, tokens) with tokens[i] the output of trace[i]."""
         params = params or EngineParams()
         placement = Placement([1], [list(range(len(entries)))], num_sm)
@@ -439,8 +440,8 @@ class Unit:
         recs = (Record * max(len(trace), 1))()
         total = sum(r.output_len for r in trace)
         toks = (C.c_int32 * max(total, 1))()
-        check(lib.mux_unit_run_lockstep(self._h, C.byref(b.cfg), len(entries), ents, len(trace),
-                                        _c_trace(trace), prompt_seed, recs, toks))
+        fn = lib.mux_unit_run_measured if measured else lib.mux_unit_run_lockstep
+        check(fn(self._h, C.byref(b.cfg), len(entries), ents, len(trace), _c_trace(trace), prompt_seed, recs, toks))
         out, off = [], 0
         for r in trace:
             out.append(list(toks[off:off + r.output_len]))

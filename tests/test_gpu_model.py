@@ -325,3 +325,30 @@ def test_decode_fused_layer_chain_matches_oracle(tiny_unit):
                 unit.pool.free_request(llm, rid)
     finally:
         unit.set_option("chain", 0)
+
+
+def test_measured_engine_runs_config1_on_device_time(tiny_unit):
+    """Measured mode: the same engine and ADBS passes, but every
+    job completes at its measured device time. All requests finish, record
+    timestamps are ordered, the run is much faster than the priced model's
+    request latencies are device times (not the priced model's), and every
+    token still passes the oracle check."""
+    unit, specs, refs = tiny_unit
+    with open(os.path.join(GOLDEN, "sim_cfg1_tiny.json")) as f:
+        g = json.load(f)
+    names = [s.name for s in specs]
+    entries = [mux.Entry(specs[names.index(n)], rate, mp, mo) for (n, L, H, hid, wb, rate, mp, mo) in g["entries"]]
+    trace = [mux.TraceRequest(i, names.index(llm), a, p, min(o, 24)) for (i, llm, a, p, o) in g["trace"]
+             if a < 10.0]
+    recs, tokens = unit.run_lockstep(entries, trace, g["gpu_memory_bytes"], prompt_seed=11, measured=True)
+    priced = mux.simulate(entries, trace, mux.Placement([1], [[0, 1]]), g["gpu_memory_bytes"])
+    assert len(recs) == len(trace)
+    assert all(r.arrival_s <= r.first_token_s <= r.done_s for r in recs)
+    assert all(len(t) == r.output_len for t, r in zip(tokens, trace))
+    # latencies are measured device times: positive, bounded, and not the priced ones
+    lat = [r.done_s - r.arrival_s for r in recs]
+    assert all(0 < x < 5.0 for x in lat)
+    assert [r.done_s for r in recs] != [r.done_s for r in priced]
+    for r, toks in list(zip(trace, tokens))[:8]:
+        prompt = lockstep_prompt(11, r.id, r.prompt_len, specs[r.llm].vocab)
+        check_tokens(refs[r.llm], prompt, toks)
