@@ -194,14 +194,17 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop()
 
     # K1 roofline: CUDA events around every decode-attention launch, on its
-    # stream, over separate steps (events between kernels would break the
-    # PDL overlap inside the timed region above).
+    # stream, over separate steps of the same workload (both models' jobs
+    # still concurrent). PDL is off for these steps: with it, the event pair
+    # around a K1 launch would also span the kernel's programmatic overlap.
+    unit.set_option("pdl", 0)
     unit.attn_timing(True)
     for _ in range(args.attn_steps):
         step()
     unit.sync()
     attn_ms, attn_n, attn_bytes = unit.attn_time()
     unit.attn_timing(False)
+    unit.set_option("pdl", args.pdl)
 
     # e2e: host token ids in (pinned) -> jobs -> next tokens out (pinned), each
     # step waits for its result before the next, as a serving loop does.
