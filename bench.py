@@ -128,7 +128,9 @@ def run_ours(args, rank, world, local_rank):
 
     import paper_2404_02015_b200 as mux
 
-    torch.cuda.set_device(local_rank)
+    device = local_rank if torch.cuda.device_count() > local_rank else 0
+    torch.cuda.set_device(device)
+    local_rank = device
     specs = [mux.spec(m) for m in args.models.split(",")]
     B = args.batch
     steps_total = args.warmup + args.steps + args.e2e_steps + args.attn_steps + 2
@@ -268,17 +270,16 @@ def main():
 
     import torch
     if world > 1:
-        torch.distributed.init_process_group("nccl" if torch.cuda.is_available() else "gloo")
+        # one GPU per rank -> NCCL; MUX_DIST_BACKEND=gloo lets several ranks
+        # share one GPU (a test of this multi-rank path, not a measurement)
+        backend = os.environ.get("MUX_DIST_BACKEND") or ("nccl" if torch.cuda.is_available() else "gloo")
+        if backend == "nccl":
+            torch.cuda.set_device(local_rank)
+        torch.distributed.init_process_group(backend)
     r = run_ours(args, rank, world, local_rank)
-    ms = r["ms"]
-    tokens = r["tokens"]
-    if world > 1:
-        t = torch.tensor([ms, r["e2e_ms"]], dtype=torch.float64, device="cuda")
-        torch.distributed.all_reduce(t, op=torch.distributed.ReduceOp.MAX)
-        ms, e2e_ms = t.tolist()
-        tokens *= world
-    else:
-        e2e_ms = r["e2e_ms"]
+    tokens = r["tokens"] * world
+    from paper_2404_02015_b200 import mesh
+    ms, e2e_ms = mesh.max_over_ranks([r["ms"], r["e2e_ms"]])  # the job ends with its slowest rank
     hbm, peak_kind = peaks()
     achieved = r["attn_bytes"] / (r["attn_ms"] / 1e3) / 1e9 if r["attn_ms"] > 0 else 0.0
     value = tokens / (ms / 1e3)
