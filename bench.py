@@ -149,6 +149,7 @@ def run_ours(args, rank, world, local_rank):
                     partition_sms=[0] + args.partition_sms if args.partition_sms else None)
     unit.set_option("pdl", args.pdl)
     unit.set_option("chain", args.chain)
+    unit.set_option("fuse_qkv", args.fuse_qkv)
     unit.init_kv(seed=7 + rank, std=1.0)
     pool = unit.pool
     ids = []
@@ -252,6 +253,7 @@ def main():
     ap.add_argument("--serial", action="store_true", help="run the colocated decode jobs on one stream")
     ap.add_argument("--serve-horizon", type=float, default=3.0,
                     help="seconds of Poisson arrivals for the auxiliary measured serving run (0 = skip)")
+    ap.add_argument("--fuse-qkv", type=int, default=0, help="RoPE + KV append in the QKV GEMM epilogue (experimental)")
     ap.add_argument("--chain", type=int, default=0, help="fused persistent layer chain for decode (experimental)")
     ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch between job kernels")
     ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg (profiling runs)")

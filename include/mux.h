@@ -289,7 +289,9 @@ MUX_API int64_t mux_unit_launches(mux_unit* unit);
 /* Tuning knobs: "gemm_min_iters" (k-blocks per GEMM CTA, default 24);
  * "pdl" (programmatic dependent launch between job kernels, default 1);
  * "chain" (decode layers as one fused persistent layer-chain launch plus
- * K1, default 0 = one launch per projection / element-wise step). */
+ * K1, default 0 = one launch per projection / element-wise step);
+ * "fuse_qkv" (RoPE + KV append in the QKV GEMM epilogue, default 0: the
+ * epilogue on the critical path costs more than the separate kv_append). */
 MUX_API int mux_unit_set_option(mux_unit* unit, const char* key, int64_t value);
 
 /* Lockstep run: the engine's decisions are those of mux_simulate (oracle

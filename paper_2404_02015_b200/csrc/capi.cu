@@ -1002,6 +1002,7 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
     if (k == "gemm_min_iters") u->rt->set_gemm_min_iters(static_cast<int>(value));
     else if (k == "pdl") mux::pdl_enabled() = value != 0;
     else if (k == "chain") u->rt->set_chain(value != 0);
+    else if (k == "fuse_qkv") u->rt->set_fuse_qkv(value != 0);
     else throw std::invalid_argument("unknown option: " + k);
   });
 }

@@ -51,7 +51,7 @@ PinnedMem::~PinnedMem() {
 
 namespace {
 
-constexpr int kEpiStoreBf16 = 0, kEpiResidual = 1, kEpiSilu = 2, kEpiStoreF32 = 3;
+constexpr int kEpiStoreBf16 = 0, kEpiResidual = 1, kEpiSilu = 2, kEpiStoreF32 = 3, kEpiQkvRope = 4;
 
 __global__ void gather_last_tok(const int32_t* last_tok, const int32_t* slots, int32_t* tokens, int n) {
   grid_dep_wait();
@@ -65,6 +65,24 @@ __global__ void scatter_last_tok(int32_t* last_tok, const int32_t* slots, const 
   grid_dep_launch();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) last_tok[slots[i]] = tokens[i];
+}
+
+// The fused QKV epilogue reads exactly the tables kv_append would.
+QkvRopeArgs qkv_rope_args(const AppendArgs& ap) {
+  QkvRopeArgs q{};
+  q.q_out = ap.q_out;
+  q.pool = ap.pool;
+  q.rowrec = ap.rowrec;
+  q.rowlist = ap.rowlist;
+  q.tok_slot = ap.tok_slot;
+  q.tok_pos = ap.tok_pos;
+  q.rope = ap.rope;
+  q.rope_positions = ap.rope_positions;
+  q.H = ap.H;
+  q.layer = ap.layer;
+  q.row_width = ap.row_width;
+  q.max_rows = ap.max_rows;
+  return q;
 }
 
 int gemm_n_tile(int M) {
@@ -364,7 +382,7 @@ const void* Runtime::act_tmap(const void* base, int rows, int cols, int box_rows
 }
 
 void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void* out, int ldo, int epi,
-                   Workspace& ws, cudaStream_t stream) {
+                   Workspace& ws, cudaStream_t stream, const QkvRopeArgs* qkv) {
   // The X map is viewed over max(M, 256) rows: buffers are sized for it and
   // rows past M are never stored.
   const int rows = std::max(M, 256);
@@ -385,6 +403,7 @@ void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void
   g.K = K;
   g.ldo = ldo;
   g.epi = static_cast<Epilogue>(epi);
+  if (qkv != nullptr) g.qkv = *qkv;
   check_cuda(gemm_bf16_tn(g, stream), "gemm");
   launches_ += 1;
 }
@@ -648,10 +667,15 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
     }
   }
   for (int l = 0; l < L && !(chain_enabled_ && d.tp_size == 1 && n <= 256); ++l) {
-    gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
     ap.layer = l;
-    check_cuda(kv_append(ap, stream), "kv_append");
-    launches_ += 1;
+    if (fuse_qkv_) {
+      const QkvRopeArgs qr = qkv_rope_args(ap);
+      gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiQkvRope, ws, stream, &qr);
+    } else {
+      gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
+      check_cuda(kv_append(ap, stream), "kv_append");
+      launches_ += 1;
+    }
     at.layer = l;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
     if (timer) {
@@ -755,10 +779,15 @@ void Runtime::prefill(Llama& m, Workspace& ws, int n, const int32_t* slots_host,
   pa.T = T;
   pa.scale_log2 = 1.4426950408889634f / std::sqrt(128.f);
   for (int l = 0; l < L; ++l) {
-    gemm(m.wqkv[l].p, ws.xn.p, T, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
     ap.layer = l;
-    check_cuda(kv_append(ap, stream), "kv_append");
-    launches_ += 1;
+    if (fuse_qkv_) {
+      const QkvRopeArgs qr = qkv_rope_args(ap);
+      gemm(m.wqkv[l].p, ws.xn.p, T, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiQkvRope, ws, stream, &qr);
+    } else {
+      gemm(m.wqkv[l].p, ws.xn.p, T, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
+      check_cuda(kv_append(ap, stream), "kv_append");
+      launches_ += 1;
+    }
     check_cuda(prefill_attention(pa, stream), "prefill_attention");
     launches_ += 1;
     const float* next_norm = l + 1 < L ? m.attn_norm[l + 1].as<float>() : m.final_norm.as<float>();

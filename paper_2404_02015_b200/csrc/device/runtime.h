@@ -14,6 +14,7 @@
 #include <vector>
 
 #include "mux/kv.hpp"
+#include "../kernels/kernels.h"
 
 namespace mux {
 
@@ -179,6 +180,7 @@ class Runtime {
   int64_t launches() const { return launches_; }
   void set_gemm_min_iters(int v) { gemm_min_iters_ = v; }
   void set_chain(bool on) { chain_enabled_ = on; }
+  void set_fuse_qkv(bool on) { fuse_qkv_ = on; }
   void count_launch(int64_t n = 1) { launches_ += n; }
 
   // Cached tensor map for an activation buffer viewed as rows x cols bf16.
@@ -199,7 +201,7 @@ class Runtime {
 
   // Decode-forward building blocks, exposed for tests/bench.
   void gemm(const void* w_tiled, const void* x, int M, int N, int K, void* out, int ldo, int epi,
-            Workspace& ws, cudaStream_t stream);
+            Workspace& ws, cudaStream_t stream, const QkvRopeArgs* qkv = nullptr);
   // Row-parallel projection + the fused allreduce (tp > 1): out partial of
   // X[M x K] W[N x K]^T to every rank's slot `s`, then resid += sum of ranks'
   // slots and xn = rmsnorm(resid) * norm_w on this rank.
@@ -213,7 +215,8 @@ class Runtime {
   int max_pos_;
   int64_t launches_ = 0;
   int gemm_min_iters_ = 24;
-  bool chain_enabled_ = false;  // measured slower than separate launches so far
+  bool chain_enabled_ = false;
+  bool fuse_qkv_ = false;  // K2 in the QKV GEMM epilogue (kQkvRope): measured slower than kv_append  // measured slower than separate launches so far
   DevMem pool_;
   DevMem rope_;
   struct StageSlot {

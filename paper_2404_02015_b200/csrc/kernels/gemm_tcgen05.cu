@@ -54,7 +54,7 @@ constexpr int kAStageBytes = kBM * kBK * 2;
 constexpr int kThreads = 256;
 constexpr int kEpiThreads = 128;
 constexpr int kChunkBytes = 32 * kBM * 4;  // one epilogue chunk: 32 tokens x 128 fp32
-constexpr int kSmemBudget = 224 * 1024;     // A ring + B ring + 2 staging chunks
+constexpr int kSmemBudget = 222 * 1024;     // A ring + B ring + 2 staging chunks (+ 2 KiB QKV metadata)
 
 struct PeerMaps {
   CUtensorMap m[kMaxTp - 1];
@@ -78,6 +78,7 @@ struct GemmRun {
   // stored through peers.m[0..n_peers) (the same slot on the other ranks of
   // the mesh, NVLink peer memory), and once all of a CTA's stores have landed
   // it adds 1 to signal[0..n_signal) (this rank's and every peer's counter).
+  QkvRopeArgs qr;   // kQkvRope
   int a_split;      // bulk copies per weight stage (1, 2, 4)
   int dbg_nomma;    // debug (MUX_GEMM_NOMMA): stream operands without MMAs
   int n_peers;
@@ -132,6 +133,8 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   uint64_t* tm_empty = tm_full + 2;  // [2]
   uint64_t* pbar = tm_empty + 2;     // fixer's partial prefetch
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pbar + 1);
+  int* meta_pos = reinterpret_cast<int*>(tmem_slot + 4);  // kQkvRope: [256] token positions
+  int* meta_id = meta_pos + 256;                          //            [256] K or V block ids
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -312,6 +315,24 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             while (ld_acquire(r.flags + p) != r.epoch) __nanosleep(32);
         if (leader && r.timing != nullptr) r.timing[c * 32 + 6] = gtimer();
       }
+      const bool rope = first && r.epi == static_cast<int>(Epilogue::kQkvRope);
+      const int part = m / max(1, r.qr.H), head = m % max(1, r.qr.H);  // kQkvRope: q/k/v and head of the tile
+      if (rope) {
+        // token positions and K/V block ids of this tile's tokens, fetched
+        // while the MMAs still run (read after the staging barrier below)
+        for (int i = etid; i < r.n_tile; i += kEpiThreads) {
+          const int tt = tok0 + i;
+          if (tt < r.M) {
+            const int pos = r.qr.tok_pos[tt];
+            meta_pos[i] = pos;
+            if (part > 0) {
+              const int rr = r.qr.rowlist[static_cast<int64_t>(r.qr.tok_slot[tt]) * r.qr.max_rows + (pos >> 4)];
+              meta_id[i] = r.qr.rowrec[static_cast<int64_t>(rr) * r.qr.row_width + (r.qr.layer * r.qr.H + head) * 2 +
+                                       (part - 1)];
+            }
+          }
+        }
+      }
       mbar_wait(&tm_full[b], (seg >> 1) & 1);
       tc_fence_after();
       if (leader && r.timing != nullptr && seg < 4) r.timing[c * 32 + 9 + seg] = gtimer();
@@ -380,6 +401,50 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           uint4* dst = reinterpret_cast<uint4*>(st + (etid >> 2) * kBM + (etid & 3) * 32);
           dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
           dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
+        }
+        if (rope) {
+          // K2 fused: thread = (token jj of the chunk, dims [d0, d0+16) and
+          // their rotate_half partners d0+64..); the same _rn arithmetic as
+          // kv_append, on the same bf16-rounded values.
+          epi_bar();
+          const int jj = etid >> 2, d0 = (etid & 3) * 16;
+          const int tt = tok0 + cc + jj;
+          if (tt < r.M) {
+            __nv_bfloat16* rowp = reinterpret_cast<__nv_bfloat16*>(st) + jj * kBM;
+            uint4 lo4[2] = {reinterpret_cast<uint4*>(rowp + d0)[0], reinterpret_cast<uint4*>(rowp + d0)[1]};
+            uint4 hi4[2] = {reinterpret_cast<uint4*>(rowp + 64 + d0)[0], reinterpret_cast<uint4*>(rowp + 64 + d0)[1]};
+            const int pos = meta_pos[cc + jj];
+            if (part < 2) {
+              const float* cs = r.qr.rope + static_cast<int64_t>(min(pos, r.qr.rope_positions - 1)) * 128;
+              uint32_t* lw = reinterpret_cast<uint32_t*>(lo4);
+              uint32_t* hw = reinterpret_cast<uint32_t*>(hi4);
+#pragma unroll
+              for (int i = 0; i < 8; ++i) {
+                const float l0 = bf16_lo(lw[i]), l1 = bf16_hi(lw[i]), h0 = bf16_lo(hw[i]), h1 = bf16_hi(hw[i]);
+                const float c0 = cs[2 * (d0 + 2 * i)], s0 = cs[2 * (d0 + 2 * i) + 1];
+                const float c1 = cs[2 * (d0 + 2 * i + 1)], s1 = cs[2 * (d0 + 2 * i + 1) + 1];
+                lw[i] = pack_bf16(__fsub_rn(__fmul_rn(l0, c0), __fmul_rn(h0, s0)),
+                                  __fsub_rn(__fmul_rn(l1, c1), __fmul_rn(h1, s1)));
+                hw[i] = pack_bf16(__fadd_rn(__fmul_rn(h0, c0), __fmul_rn(l0, s0)),
+                                  __fadd_rn(__fmul_rn(h1, c1), __fmul_rn(l1, s1)));
+              }
+              reinterpret_cast<uint4*>(rowp + d0)[0] = lo4[0];
+              reinterpret_cast<uint4*>(rowp + d0)[1] = lo4[1];
+              reinterpret_cast<uint4*>(rowp + 64 + d0)[0] = hi4[0];
+              reinterpret_cast<uint4*>(rowp + 64 + d0)[1] = hi4[1];
+            }
+            __nv_bfloat16* dst;
+            if (part == 0) {
+              dst = reinterpret_cast<__nv_bfloat16*>(r.qr.q_out) + (static_cast<int64_t>(tt) * r.qr.H + head) * 128;
+            } else {
+              dst = reinterpret_cast<__nv_bfloat16*>(static_cast<uint8_t*>(r.qr.pool) +
+                                                     static_cast<int64_t>(meta_id[cc + jj]) * 4096 + (pos & 15) * 256);
+            }
+            reinterpret_cast<uint4*>(dst + d0)[0] = lo4[0];
+            reinterpret_cast<uint4*>(dst + d0)[1] = lo4[1];
+            reinterpret_cast<uint4*>(dst + 64 + d0)[0] = hi4[0];
+            reinterpret_cast<uint4*>(dst + 64 + d0)[1] = hi4[1];
+          }
         }
         fence_async_smem();
         epi_bar();
@@ -584,6 +649,7 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   const int n_tiles_tok = (a.M + r.n_tile - 1) / r.n_tile;
   r.iters = static_cast<int64_t>(r.m_tiles) * n_tiles_tok * r.kb;
   r.epi = static_cast<int>(a.epi);
+  r.qr = a.qkv;
   r.tmem_cols = pow2_cols(r.n_tile + (r.n_tile > 32 ? r.n_tile : 32));
   int grid = a.grid > 0 ? a.grid : 148;
   // Enough k-blocks per CTA that the fixed per-CTA cost and the fixup
@@ -604,7 +670,7 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
     if (static_cast<int64_t>(grid) * need_r > r.iters) grid = static_cast<int>(std::max<int64_t>(1, r.iters / need_r));
   }
   const size_t smem = 1024 + static_cast<size_t>(r.stages_a) * kAStageBytes + static_cast<size_t>(r.stages_b) * b_stage +
-                      2 * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16;
+                      2 * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16 + 2 * 256 * 4;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);

@@ -63,6 +63,19 @@ enum class Epilogue : int {
   kResidualAddF32 = 1, // out fp32 [M][ldo] += D (the residual stream; single owner per element)
   kSiluMulBf16 = 2,    // W rows interleaved (gate, up) pairs: out bf16 [M][N/2]
   kStoreF32 = 3,       // out fp32 [M][ldo]
+  kQkvRope = 4,        // K2 fused into the QKV projection: out bf16 [M][3][H][128] with q and k
+                       // rotated (RoPE), rotated q -> q_out, the token's K/V -> its head-blocks
+};
+// Tables of the fused QKV epilogue (kQkvRope): what kv_append would read.
+struct QkvRopeArgs {
+  void* q_out;              // [M][H][128] bf16 rotated q
+  void* pool;               // [n_blocks][16][128] bf16
+  const int32_t* rowrec;
+  const int32_t* rowlist;
+  const int32_t* tok_slot;  // [M] table slot of each token's request
+  const int32_t* tok_pos;   // [M] position of the token in its request
+  const float* rope;        // [rope_positions][64][2]
+  int rope_positions, H, layer, row_width, max_rows;
 };
 struct GemmArgs {
   const void* w_tiled;      // weights in weight_tile() layout (preferred), or null
@@ -78,6 +91,7 @@ struct GemmArgs {
   int M, N, K;
   int ldo;
   Epilogue epi;
+  QkvRopeArgs qkv;          // kQkvRope only
   // Tensor parallelism (kStoreF32): also store every tile through these
   // maps (host CUtensorMap*, peer ranks' slots) and signal the counters
   // once per CTA when its stores have landed. grid_out receives the grid.

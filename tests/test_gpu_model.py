@@ -352,3 +352,38 @@ def test_measured_engine_runs_config1_on_device_time(tiny_unit):
     for r, toks in list(zip(trace, tokens))[:8]:
         prompt = lockstep_prompt(11, r.id, r.prompt_len, specs[r.llm].vocab)
         check_tokens(refs[r.llm], prompt, toks)
+
+
+def test_fused_qkv_epilogue_is_bit_identical_to_kv_append(tiny_unit):
+    """K2 fused into the QKV GEMM epilogue (option "fuse_qkv") against the
+    separate kv_append kernel (default): same bf16 rounding and _rn RoPE arithmetic, so the same
+    prefill + decode produce identical tokens."""
+    unit, specs, refs = tiny_unit
+    rng = np.random.default_rng(77)
+    lens = [1, 15, 16, 17, 64, 200]
+    prompts = [rng.integers(0, specs[0].vocab, n).astype(np.int32) for n in lens]
+    runs = []
+    for fused, base in ((1, 61000), (0, 62000)):
+        unit.set_option("fuse_qkv", fused)
+        rids = [base + i for i in range(len(lens))]
+        for rid, n in zip(rids, lens):
+            assert unit.pool.admit(0, rid, n, n + 10).ok
+        first = np.zeros(len(lens), np.int32)
+        unit.prefill(0, rids, np.concatenate(prompts), first, partition=0)
+        unit.sync()
+        gen = [[int(t)] for t in first]
+        out = np.zeros(len(lens), np.int32)
+        for _ in range(10):
+            for rid in rids:
+                assert unit.pool.alloc(0, rid, 1, False).ok
+            unit.decode(0, rids, out=out, partition=1)
+            unit.sync()
+            for i, t in enumerate(out):
+                gen[i].append(int(t))
+        for rid in rids:
+            unit.pool.free_request(0, rid)
+        runs.append(gen)
+    unit.set_option("fuse_qkv", 0)
+    assert runs[0] == runs[1]
+    for i in range(len(lens)):
+        check_tokens(refs[0], prompts[i], runs[0][i])
