@@ -54,7 +54,7 @@ constexpr int kAStageBytes = kBM * kBK * 2;
 constexpr int kThreads = 256;
 constexpr int kEpiThreads = 128;
 constexpr int kChunkBytes = 32 * kBM * 4;  // one epilogue chunk: 32 tokens x 128 fp32
-constexpr int kSmemBudget = 222 * 1024;     // A ring + B ring + 2 staging chunks (+ 2 KiB QKV metadata)
+constexpr int kSmemBudget = 224 * 1024;     // A ring + B ring + 2 staging chunks
 
 struct PeerMaps {
   CUtensorMap m[kMaxTp - 1];
@@ -640,7 +640,8 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   r.a_split = (env_split == 2 || env_split == 4 || env_split == 8) ? env_split : 1;
   static const int env_nomma = getenv("MUX_GEMM_NOMMA") ? atoi(getenv("MUX_GEMM_NOMMA")) : 0;
   r.dbg_nomma = env_nomma;
-  r.stages_a = (kSmemBudget - r.stages_b * b_stage - 2 * kChunkBytes) / kAStageBytes;
+  const int meta_bytes = a.epi == Epilogue::kQkvRope ? 2 * 256 * 4 : 0;  // token positions + block ids
+  r.stages_a = (kSmemBudget - meta_bytes - r.stages_b * b_stage - 2 * kChunkBytes) / kAStageBytes;
   if (r.stages_a > 10) r.stages_a = 10;
   if (env_sa > 0 && env_sa < r.stages_a) r.stages_a = env_sa;
   // The fixer prefetches up to 2 partners x ceil(n_tile/32) chunks into the A ring.
@@ -670,7 +671,7 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
     if (static_cast<int64_t>(grid) * need_r > r.iters) grid = static_cast<int>(std::max<int64_t>(1, r.iters / need_r));
   }
   const size_t smem = 1024 + static_cast<size_t>(r.stages_a) * kAStageBytes + static_cast<size_t>(r.stages_b) * b_stage +
-                      2 * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16 + 2 * 256 * 4;
+                      2 * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16 + meta_bytes;
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);

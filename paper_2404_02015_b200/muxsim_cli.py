@@ -1,0 +1,80 @@
+"""`muxsim simulate` drop-in:
+
+    python -m paper_2404_02015_b200.muxsim_cli -c cfg.json -p plan.json -t trace.csv -o out/ \\
+        [--engine priced|lockstep|measured]
+
+Reads the reference's config / plan.json / trace.csv and writes records.csv
+in the reference's format (/root/reference/proj/src/commands.cpp:265-298,
+74-87). Engines:
+  priced    the reference's event loop and pricing model in libmux.so
+            (CPU; records byte-identical to `muxsim simulate`)
+  lockstep  the same decisions, every job executed on this GPU (random-init
+            weights, synthetic prompt tokens); records identical to priced
+  measured  job completions at measured device time (real serving latencies)
+The GPU engines serve single-unit, single-GPU plans (one B200).
+Exit codes follow the reference CLI (muxsim.cpp:51-63): 1 config error,
+2 infeasible, 3 anything else.
+"""
+from __future__ import annotations
+
+import argparse
+import os
+import sys
+
+from . import wire
+from ._lib import Infeasible, InvalidArgument
+from .host import Unit, simulate
+
+
+def run(cfg_path: str, plan_path: str, trace_path: str, out_dir: str, engine: str = "priced") -> list:
+    exp = wire.load_config(cfg_path)
+    placement = wire.load_plan(plan_path, exp.names)
+    trace = wire.load_trace(trace_path, exp.names)
+    if engine == "priced":
+        recs = simulate(exp.entries, trace, placement, exp.gpu_memory_bytes, exp.params, exp.profile)
+    else:
+        if len(placement.mesh_sizes) != 1 or placement.mesh_sizes[0] != 1:
+            raise wire.ConfigError("GPU engines serve a single-unit, single-GPU plan")
+        specs = [exp.entries[i].spec for i in placement.members[0]]
+        weights = sum(s.weight_bytes for s in specs)
+        logical = (exp.gpu_memory_bytes - weights - round(exp.params.activation_reserve_frac * exp.gpu_memory_bytes)) // 4096
+        longest = max((r.prompt_len + r.output_len for r in trace), default=16)
+        unit = Unit(specs, pool_blocks=logical, device_pool_blocks=min(logical, 20_000_000), max_batch=512,
+                    max_prefill_tokens=max(exp.params.token_budget, longest), max_ctx=longest + 16,
+                    max_slots=len(trace) + 8, init_seed=1, init_std=0.02, partitions=len(specs) + 1)
+        try:
+            recs, _ = unit.run_lockstep([exp.entries[i] for i in placement.members[0]], trace,
+                                        exp.gpu_memory_bytes, exp.params, profile=exp.profile,
+                                        measured=engine == "measured")
+        finally:
+            unit.close()
+    os.makedirs(out_dir, exist_ok=True)
+    wire.write_records_csv(os.path.join(out_dir, "records.csv"), recs, exp.names)
+    return recs
+
+
+def main(argv=None) -> int:
+    ap = argparse.ArgumentParser(prog="simulate", description=__doc__.split("\n")[0])
+    ap.add_argument("-c", "--config", required=True)
+    ap.add_argument("-p", "--plan", required=True)
+    ap.add_argument("-t", "--trace", required=True)
+    ap.add_argument("-o", "--output", default="out")
+    ap.add_argument("--engine", choices=["priced", "lockstep", "measured"], default="priced")
+    a = ap.parse_args(argv)
+    try:
+        recs = run(a.config, a.plan, a.trace, a.output, a.engine)
+    except (wire.ConfigError, InvalidArgument) as e:
+        print(f"error: {e}", file=sys.stderr)
+        return 1
+    except Infeasible as e:
+        print(f"infeasible: {e}", file=sys.stderr)
+        return 2
+    except Exception as e:  # noqa: BLE001 - the reference maps everything else to 3
+        print(f"error: {e}", file=sys.stderr)
+        return 3
+    print(f"engine {a.engine}: {len(recs)} requests; wrote {a.output}/records.csv")
+    return 0
+
+
+if __name__ == "__main__":
+    sys.exit(main())

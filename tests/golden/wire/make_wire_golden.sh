@@ -1,0 +1,14 @@
+#!/bin/bash
+# Regenerate the wire-format goldens with the UNMODIFIED reference CLI
+# (oracle/_ref/muxsim, built by `make -C oracle`): trace.csv from
+# gen-workload, records.csv from simulate with the hand-written plans.
+set -euo pipefail
+cd "$(dirname "$0")"
+MUX=../../../oracle/_ref/muxsim
+for c in pair mesh; do
+  $MUX gen-workload -c cfg_$c.json -o trace_$c.csv > /dev/null
+  rm -rf out_$c
+  $MUX simulate -c cfg_$c.json -p plan_$c.json -t trace_$c.csv -o out_$c > /dev/null
+  mv out_$c/records.csv records_$c.csv
+  rm -rf out_$c
+done

@@ -387,3 +387,25 @@ def test_fused_qkv_epilogue_is_bit_identical_to_kv_append(tiny_unit):
     assert runs[0] == runs[1]
     for i in range(len(lens)):
         check_tokens(refs[0], prompts[i], runs[0][i])
+
+
+@pytest.mark.timeout(600)
+def test_muxsim_cli_lockstep_on_gpu_matches_reference_records(cuda, tmp_path):
+    """The drop-in CLI with every job executed on the B200 (7B + 13B, lockstep
+    engine): records.csv byte-identical to the unmodified reference CLI's on
+    the same config / plan / trace (first 40 requests of the golden trace)."""
+    from paper_2404_02015_b200 import muxsim_cli, wire
+    g = os.path.join(GOLDEN, "wire")
+    with open(os.path.join(g, "trace_pair.csv")) as f:
+        lines = f.read().splitlines()
+    trace = tmp_path / "trace.csv"
+    trace.write_text("\n".join(lines[:41]) + "\n")
+    priced, gpu = tmp_path / "priced", tmp_path / "gpu"
+    args = ["-c", os.path.join(g, "cfg_pair.json"), "-p", os.path.join(g, "plan_pair.json"), "-t", str(trace)]
+    assert muxsim_cli.main(args + ["-o", str(priced)]) == 0
+    assert muxsim_cli.main(args + ["-o", str(gpu), "--engine", "lockstep"]) == 0
+    assert (gpu / "records.csv").read_bytes() == (priced / "records.csv").read_bytes()
+    assert muxsim_cli.main(args + ["-o", str(tmp_path / "m"), "--engine", "measured"]) == 0
+    exp = wire.load_config(os.path.join(g, "cfg_pair.json"))
+    assert len((tmp_path / "m" / "records.csv").read_text().splitlines()) == 41
+    assert exp.names == ["chat-7b", "chat-13b"]
