@@ -50,13 +50,21 @@ def make_trace(models, rates, horizon_s, seed, max_len=2048):
     return reqs
 
 
-def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, device=0, partition_sms=None):
+def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, device=0, partition_sms=None,
+          scheduler="adbs", gpu_memory_gib=180.0, lengths=None):
+    """lengths: optional per-model (prompt, output) constants (contention runs)."""
     import paper_2404_02015_b200 as mux
-    specs = [mux.spec(m) for m in model_names]
+    specs = [mux.spec(m, f"{m}.{i}") for i, m in enumerate(model_names)]  # distinct names per unit
     raw = make_trace(specs, rates, horizon_s, seed)
+    if lengths is not None:
+        raw = [(t, llm, lengths[llm][0], lengths[llm][1]) for t, llm, _, _ in raw]
     trace = [mux.TraceRequest(i, llm, t, p, o) for i, (t, llm, p, o) in enumerate(raw)]
-    entries = [mux.Entry(s, rate, 161.0, 338.0) for s, rate in zip(specs, rates)]
-    gpu_mem = 180 * GIB
+    if lengths is None:
+        entries = [mux.Entry(s, rate, 161.0, 338.0) for s, rate in zip(specs, rates)]
+    else:
+        entries = [mux.Entry(s, rate, float(p), float(o)) for s, rate, (p, o) in zip(specs, rates, lengths)]
+    gpu_mem = int(gpu_memory_gib * GIB)
+    params = mux.EngineParams(scheduler={"adbs": 0, "fcfs": 1, "rr": 2}[scheduler])
     weights = sum(s.weight_bytes for s in specs)
     logical = (gpu_mem - weights - round(0.1 * gpu_mem)) // 4096
     unit = mux.Unit(specs, pool_blocks=logical, device=device, device_pool_blocks=min(logical, 20_000_000),
@@ -66,7 +74,7 @@ def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, 
     try:
         unit.init_kv(seed=5, std=1.0)
         t0 = time.perf_counter()
-        recs, _ = unit.run_lockstep(entries, trace, gpu_mem, measured=True)
+        recs, _ = unit.run_lockstep(entries, trace, gpu_mem, params, measured=True)
         wall = time.perf_counter() - t0
     finally:
         unit.close()
@@ -84,7 +92,8 @@ def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, 
         "ttft_ms": {"mean": round(1e3 * sum(ttft) / len(ttft), 2), "p99": round(1e3 * p99(ttft), 2)},
         "tpot_ms": {"mean": round(1e3 * sum(tpot) / len(tpot), 3), "p99": round(1e3 * p99(tpot), 3)},
         "workload": {"models": list(model_names), "rates_rps": list(rates), "horizon_s": horizon_s, "seed": seed,
-                     "lengths": "ShareGPT lognormal 161/338 sigma 0.8", "scheduler": "ADBS",
+                     "lengths": "ShareGPT lognormal 161/338 sigma 0.8" if lengths is None else lengths,
+                     "scheduler": scheduler, "gpu_memory_gib": gpu_memory_gib,
                      "partition_sms": partition_sms},
         "host_wall_s": round(wall, 2),
     }
@@ -97,11 +106,16 @@ def main():
     ap.add_argument("--horizon", type=float, default=8.0)
     ap.add_argument("--seed", type=int, default=3)
     ap.add_argument("--partition-sms", type=lambda s: [int(x) for x in s.split(",")], default=None)
+    ap.add_argument("--scheduler", choices=["adbs", "fcfs", "rr"], default="adbs")
+    ap.add_argument("--gpu-memory-gib", type=float, default=180.0)
+    ap.add_argument("--lengths", default=None, help="per-model constant prompt:output, e.g. 128:384,64:64")
     args = ap.parse_args()
     models = args.models.split(",")
     rates = [float(x) for x in args.rates.split(",")]
     psms = [0] + args.partition_sms if args.partition_sms else None
-    print(json.dumps(serve(models, rates, args.horizon, args.seed, partition_sms=psms)), flush=True)
+    lengths = None if args.lengths is None else [tuple(int(x) for x in m.split(":")) for m in args.lengths.split(",")]
+    print(json.dumps(serve(models, rates, args.horizon, args.seed, partition_sms=psms, scheduler=args.scheduler,
+                           gpu_memory_gib=args.gpu_memory_gib, lengths=lengths)), flush=True)
 
 
 if __name__ == "__main__":
