@@ -71,6 +71,13 @@ struct GemmRun {
   int kb;           // k-blocks per tile
   int m_tiles;      // ceil(N / 128)
   int64_t iters;    // tiles * kb
+  // Prefill schedule (several token tiles): n_dp data-parallel rounds of
+  // whole tiles (tile j*G + c), raster-grouped group_m weight tiles wide so
+  // the tiles in flight share their weight and activation k-slices in L2,
+  // then stream-K over the remaining sk_iters. Decode: n_dp = 0, group_m =
+  // 0, sk_iters = iters (pure stream-K).
+  int n_dp, group_m, n_tok_tiles;
+  int64_t sk_iters;
   int epi;
   uint32_t tmem_cols;
   unsigned long long* timing;  // debug: [grid][4] globaltimer stamps, or null
@@ -94,6 +101,53 @@ __device__ __forceinline__ unsigned long long gtimer() {
 
 __device__ __forceinline__ int64_t range_begin(int64_t iters, int c, int grid) {
   return iters * c / grid;
+}
+
+// The work of one CTA as a sequence of segments: (tile, k-block range); the
+// same sequence is walked by the producers, the MMA issuer and the epilogue.
+struct SegGen {
+  int64_t sk, sk_end;
+  int j;
+  __device__ SegGen(const GemmRun& r, int c, int G)
+      : sk(range_begin(r.sk_iters, c, G)), sk_end(range_begin(r.sk_iters, c + 1, G)), j(0) {}
+  // tile (m, nt), k-blocks [kb0, kb1); sk: stream-K piece of the tile whose
+  // stream-K iterations are [lo, lo + kb)
+  __device__ bool next(const GemmRun& r, int c, int G, int& m, int& nt, int& kb0, int& kb1, bool& skp, int64_t& lo) {
+    int64_t tile;
+    if (j < r.n_dp) {
+      tile = static_cast<int64_t>(j) * G + c;
+      ++j;
+      kb0 = 0;
+      kb1 = r.kb;
+      skp = false;
+      lo = 0;
+    } else {
+      if (sk >= sk_end) return false;
+      const int64_t st = sk / r.kb;
+      lo = st * r.kb;
+      kb0 = static_cast<int>(sk - lo);
+      const int64_t e = min(sk_end, lo + r.kb);
+      kb1 = static_cast<int>(e - lo);
+      sk = e;
+      skp = true;
+      tile = static_cast<int64_t>(r.n_dp) * G + st;
+    }
+    if (r.group_m <= 0) {
+      m = static_cast<int>(tile % r.m_tiles);
+      nt = static_cast<int>(tile / r.m_tiles);
+    } else {
+      const int64_t per = static_cast<int64_t>(r.group_m) * r.n_tok_tiles;
+      const int64_t g = tile / per, in = tile - g * per;
+      const int gm = min(r.group_m, r.m_tiles - static_cast<int>(g) * r.group_m);  // last group may be narrower
+      m = static_cast<int>(g) * r.group_m + static_cast<int>(in % gm);
+      nt = static_cast<int>(in / gm);
+    }
+    return true;
+  }
+};
+
+__device__ __forceinline__ bool sg_has_more(const SegGen& sg, const GemmRun& r) {
+  return sg.j < r.n_dp || sg.sk < sg.sk_end;
 }
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
@@ -141,8 +195,6 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   const int c = blockIdx.x;
   const int G = gridDim.x;
   if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 32 + 0] = gtimer();
-  const int64_t it0 = range_begin(r.iters, c, G);
-  const int64_t it1 = range_begin(r.iters, c + 1, G);
 
   if (warp == 0 && lane == 0) {
     if (r.w_tiled == nullptr) prefetch_tmap(&tw);
@@ -185,38 +237,33 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       uint64_t* fb = is_a ? full_a : full_b;
       uint64_t* eb = is_a ? empty_a : empty_b;
       const uint32_t bytes = is_a ? kAStageBytes : b_stage_bytes;
-      // Incremental (tile, k-block, stage) counters: no 64-bit division or
-      // modulo in the issue loop (a per-iteration int64 divide is a ~100-
-      // instruction subroutine call on the critical path of every stage).
-      const int t0 = static_cast<int>(it0 / r.kb);
-      int kbi = static_cast<int>(it0 - static_cast<int64_t>(t0) * r.kb);
-      int m = t0 % r.m_tiles, nt = t0 / r.m_tiles;
+      // Segments (tile, k-block range) with incremental stage counters: no
+      // 64-bit division in the issue loop.
+      SegGen sg(r, c, G);
+      int m, nt, kb0, kb1;
+      bool skp;
+      int64_t lo;
       int s = 0, round = 0;
-      for (int64_t it = it0; it < it1; ++it) {
-        if (round > 0) mbar_wait(&eb[s], (round - 1) & 1);
-        mbar_arrive_expect_tx(&fb[s], bytes);
-        if (is_a) {
-          if (r.w_tiled != nullptr) {
-            // one contiguous, pre-swizzled 16 KiB UMMA tile: a_split bulk copies
-            const uint8_t* src = r.w_tiled + (static_cast<int64_t>(m) * r.kb + kbi) * kAStageBytes;
-            const uint32_t piece = kAStageBytes / r.a_split;
-            for (int pc = 0; pc < r.a_split; ++pc)
-              bulk_g2s_stream(a_st + s * kAStageBytes + pc * piece, src + pc * piece, piece, &fb[s], pol);
+      while (sg.next(r, c, G, m, nt, kb0, kb1, skp, lo)) {
+        for (int kbi = kb0; kbi < kb1; ++kbi) {
+          if (round > 0) mbar_wait(&eb[s], (round - 1) & 1);
+          mbar_arrive_expect_tx(&fb[s], bytes);
+          if (is_a) {
+            if (r.w_tiled != nullptr) {
+              // one contiguous, pre-swizzled 16 KiB UMMA tile: a_split bulk copies
+              const uint8_t* src = r.w_tiled + (static_cast<int64_t>(m) * r.kb + kbi) * kAStageBytes;
+              const uint32_t piece = kAStageBytes / r.a_split;
+              for (int pc = 0; pc < r.a_split; ++pc)
+                bulk_g2s_stream(a_st + s * kAStageBytes + pc * piece, src + pc * piece, piece, &fb[s], pol);
+            } else {
+              tma_load_2d(a_st + s * kAStageBytes, &tw, &fb[s], kbi * kBK, m * kBM, pol);
+            }
           } else {
-            tma_load_2d(a_st + s * kAStageBytes, &tw, &fb[s], kbi * kBK, m * kBM, pol);
+            tma_load_2d(b_st + s * b_stage_bytes, &tx, &fb[s], kbi * kBK, nt * r.n_tile, pol);
           }
-        } else {
-          tma_load_2d(b_st + s * b_stage_bytes, &tx, &fb[s], kbi * kBK, nt * r.n_tile, pol);
-        }
-        if (++s == SS) {
-          s = 0;
-          ++round;
-        }
-        if (++kbi == r.kb) {
-          kbi = 0;
-          if (++m == r.m_tiles) {
-            m = 0;
-            ++nt;
+          if (++s == SS) {
+            s = 0;
+            ++round;
           }
         }
       }
@@ -226,16 +273,16 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     const uint32_t idesc = umma_idesc_bf16(kBM, r.n_tile);
     int i = 0, seg = 0;
     int sa = 0, ra = 0, sb = 0, rb = 0;  // ring slots and their round parities
-    int64_t it = it0;
-    while (it < it1) {
-      const int64_t t = it / r.kb;
-      const int64_t seg_begin = it;
-      const int64_t seg_end = min(it1, (t + 1) * r.kb);
+    SegGen sg(r, c, G);
+    int m, nt, kb0, kb1;
+    bool skp;
+    int64_t lo;
+    while (sg.next(r, c, G, m, nt, kb0, kb1, skp, lo)) {
       const int b = seg & 1;
       if (seg >= 2) mbar_wait(&tm_empty[b], ((seg >> 1) - 1) & 1);
       tc_fence_after();
       const uint32_t acc = tmem + static_cast<uint32_t>(b * r.n_tile);
-      for (; it < seg_end; ++it, ++i) {
+      for (int kbi = kb0; kbi < kb1; ++kbi, ++i) {
         mbar_wait(&full_a[sa], ra & 1);
         if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 32 + 4] = gtimer();
         if (r.dbg_nomma < 2) mbar_wait(&full_b[sb], rb & 1);
@@ -249,16 +296,16 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             if (r.dbg_nomma) break;
             // Advance along K inside the swizzle atom: 16 bf16 = 32 bytes.
             umma_bf16(acc, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
-                      (it != seg_begin || kk != 0) ? 1u : 0u);
+                      (kbi != kb0 || kk != 0) ? 1u : 0u);
           }
           if (r.dbg_nomma) {  // debug: pure streaming rate (results are garbage)
             mbar_arrive(&empty_a[sa]);
             if (r.dbg_nomma < 2) mbar_arrive(&empty_b[sb]);
-            if (it == seg_end - 1) mbar_arrive(&tm_full[b]);
+            if (kbi == kb1 - 1) mbar_arrive(&tm_full[b]);
           } else {
             umma_commit(&empty_a[sa]);
             umma_commit(&empty_b[sb]);
-            if (it == seg_end - 1) umma_commit(&tm_full[b]);
+            if (kbi == kb1 - 1) umma_commit(&tm_full[b]);
           }
         }
         __syncwarp();
@@ -287,19 +334,20 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     const bool residual = r.epi == static_cast<int>(Epilogue::kResidualAddF32);
     int seg = 0, sbuf = 0;
     uint32_t pphase = 0;
-    int64_t it = it0;
-    while (it < it1) {
-      const int64_t t = it / r.kb;
-      const int64_t tile_lo = t * r.kb, tile_hi = tile_lo + r.kb;
-      const int64_t seg_end = min(it1, tile_hi);
-      // Residual adds need no fixup: every piece reduce-adds into the fp32
-      // residual stream (order of the <= few pieces is not fixed). Other
-      // epilogues are nonlinear or rounding, so pieces are summed first.
-      const bool first = residual || it == tile_lo;
-      const bool last = residual || seg_end == tile_hi;
+    SegGen sg(r, c, G);
+    int m, nt, kb0, kb1;
+    bool skp;
+    int64_t tile_lo;
+    while (sg.next(r, c, G, m, nt, kb0, kb1, skp, tile_lo)) {
+      const int64_t tile_hi = tile_lo + r.kb;  // stream-K iterations of this tile (skp)
+      const bool seg_last = !sg_has_more(sg, r);
+      // Whole (data-parallel) tiles need no fixup; residual adds neither:
+      // every piece reduce-adds into the fp32 residual stream (order of the
+      // <= few pieces is not fixed). Other epilogues are nonlinear or
+      // rounding, so stream-K pieces are summed first.
+      const bool first = residual || !skp || kb0 == 0;
+      const bool last = residual || !skp || kb1 == r.kb;
       const int b = seg & 1;
-      const int m = static_cast<int>(t % r.m_tiles);
-      const int nt = static_cast<int>(t / r.m_tiles);
       const int tok0 = nt * r.n_tile;
       const int nchunk = (r.n_tile + 31) / 32;
       int n_part = 0;
@@ -308,7 +356,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         // Fixer (always this CTA's last segment): wait for the partners of
         // this tile, then bulk-prefetch all their chunks into the A ring.
         int p_hi = c + 1;
-        while (p_hi < G && range_begin(r.iters, p_hi, G) < tile_hi) ++p_hi;
+        while (p_hi < G && range_begin(r.sk_iters, p_hi, G) < tile_hi) ++p_hi;
         n_part = p_hi - (c + 1);
         if (leader)
           for (int p = c + 1; p < p_hi; ++p)
@@ -355,7 +403,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         const int cc = k * 32;
         float v[32];
         tmem_ld_32x32b_x32(acc + cc, v);
-        const bool stamp = leader && r.timing != nullptr && seg_end == it1 && k < 4;
+        const bool stamp = leader && r.timing != nullptr && seg_last && k < 4;
         if (stamp) r.timing[c * 32 + 20 + k] = gtimer();
         if (k == nchunk - 1) {  // accumulators consumed: hand TMEM back
           tc_fence_before();
@@ -474,7 +522,6 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         if (leader && r.timing != nullptr) r.timing[c * 32 + 8] = gtimer();
       }
       if (leader && r.timing != nullptr && seg < 4) r.timing[c * 32 + 16 + seg] = gtimer();
-      it = seg_end;
       ++seg;
     }
     if (leader) bulk_wait<0>();  // staging smem must outlive its bulk reads
@@ -651,6 +698,7 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   r.iters = static_cast<int64_t>(r.m_tiles) * n_tiles_tok * r.kb;
   r.epi = static_cast<int>(a.epi);
   r.qr = a.qkv;
+  r.n_tok_tiles = n_tiles_tok;
   r.tmem_cols = pow2_cols(r.n_tile + (r.n_tile > 32 ? r.n_tile : 32));
   int grid = a.grid > 0 ? a.grid : 148;
   // Enough k-blocks per CTA that the fixed per-CTA cost and the fixup
@@ -670,6 +718,19 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
     const int64_t need_r = (r.kb + max_partners - 1) / std::max(1, max_partners);
     if (static_cast<int64_t>(grid) * need_r > r.iters) grid = static_cast<int>(std::max<int64_t>(1, r.iters / need_r));
   }
+  // Schedule: decode (one token tile) = pure stream-K; prefill = grouped
+  // data-parallel rounds + stream-K over the last 1-2 waves of tiles (so
+  // every stream-K range spans >= one tile's k-blocks: <= 2 partners).
+  static const int env_group = getenv("MUX_GEMM_GROUP_M") ? atoi(getenv("MUX_GEMM_GROUP_M")) : 8;
+  const int64_t tiles = static_cast<int64_t>(r.m_tiles) * n_tiles_tok;
+  if (n_tiles_tok > 1 && env_group > 0) {
+    r.n_dp = static_cast<int>(std::max<int64_t>(0, tiles / grid - 1));
+    r.group_m = env_group;
+  } else {
+    r.n_dp = 0;
+    r.group_m = 0;
+  }
+  r.sk_iters = (tiles - static_cast<int64_t>(r.n_dp) * grid) * r.kb;
   const size_t smem = 1024 + static_cast<size_t>(r.stages_a) * kAStageBytes + static_cast<size_t>(r.stages_b) * b_stage +
                       2 * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16 + meta_bytes;
   static bool configured = false;
