@@ -9,7 +9,8 @@ Each model holds a decode batch of B requests with ShareGPT-shaped lengths
 (lognormal mean 161 prompt / 338 output, sigma 0.8, workload.hpp:21) caught
 mid-generation. One step = one ADBS decode round (scheduler.cpp:90-117):
 BlockPool.alloc(+1 token) for every member of both models, then both decode
-jobs run concurrently on their own partition streams (full 32/40-layer
+jobs run concurrently, each on its own green-context SM partition sized by
+its share of the round's HBM bytes (byte_share_partitions; full 32/40-layer
 forward: tcgen05 GEMMs, RoPE+KV append, head-wise paged attention, LM head,
 greedy argmax). Tokens per step = 2B.
 
@@ -95,6 +96,22 @@ class Clocks:
         except Exception:
             self.proc = None
 
+    def wait_started(self, timeout_s: float = 5.0):
+        """Wait for nvidia-smi's first (idle) sample; samples up to here are
+        dropped by stop(), so the reported clocks are the ones under load."""
+        self.skip = 0
+        if self.proc is None:
+            return
+        t0 = time.time()
+        while time.time() - t0 < timeout_s:
+            self.f.flush()
+            with open(self.path) as f:
+                n = sum(1 for _ in f)
+            if n:
+                self.skip = n
+                return
+            time.sleep(0.02)
+
     def stop(self):
         if self.proc is None:
             return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
@@ -103,7 +120,9 @@ class Clocks:
         self.f.close()
         sm, smax, reasons = [], None, set()
         names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
-        for line in open(self.path):
+        for i, line in enumerate(open(self.path)):
+            if i < getattr(self, "skip", 0):
+                continue
             parts = [x.strip() for x in line.split(",")]
             if len(parts) < 9:
                 continue
@@ -143,13 +162,24 @@ def run_ours(args, rank, world, local_rank):
     logical = pool_blocks(specs)
     assert need <= logical, "batch exceeds the unified pool"
     max_ctx = max(p + d + steps_total + 1 for reqs in batches for p, o, d in reqs)
+    if args.partition_sms == "auto" and len(specs) == 1:
+        psms = None
+    elif args.partition_sms == "auto":
+        ctx = [sum(p + d for p, o, d in reqs) for reqs in batches]
+        psms = mux.byte_share_partitions(specs, ctx, torch.cuda.get_device_properties(device).multi_processor_count)
+    elif args.partition_sms in ("none", "", None):
+        psms = None
+    else:
+        psms = [int(x) for x in args.partition_sms.split(",")]
+    args.partition_resolved = psms
     unit = mux.Unit(specs, pool_blocks=logical, device=local_rank, device_pool_blocks=need + 4096,
                     max_batch=B, max_prefill_tokens=256, max_ctx=max_ctx + 16, max_slots=2 * B + 16,
                     init_seed=1 + rank, init_std=0.02, partitions=len(specs) + 1,
-                    partition_sms=[0] + args.partition_sms if args.partition_sms else None)
+                    partition_sms=[0] + psms if psms else None)
     unit.set_option("pdl", args.pdl)
     unit.set_option("chain", args.chain)
     unit.set_option("fuse_qkv", args.fuse_qkv)
+    unit.set_option("l2_next", args.l2_next)
     unit.init_kv(seed=7 + rank, std=1.0)
     pool = unit.pool
     ids = []
@@ -165,7 +195,7 @@ def run_ours(args, rank, world, local_rank):
     ids_c = [unit._ids(r) for r in ids]
     ctx0 = [sum(pool.request_tokens(li, r) for r in ids[li]) for li in range(len(specs))]
 
-    def step(tokens=None, outs=None):
+    def step(tokens=None, outs=None, whole_gpu=False):
         # one ADBS decode round: +1 token per member (BlockPool), then the jobs
         for li in range(len(specs)):
             for rid in ids[li]:
@@ -173,15 +203,18 @@ def run_ours(args, rank, world, local_rank):
                 if not r.ok:
                     raise RuntimeError("pool exhausted")
             unit.decode(li, ids[li], tokens=None if tokens is None else tokens[li],
-                        out=None if outs is None else outs[li], partition=1 + (0 if args.serial else li),
+                        out=None if outs is None else outs[li], partition=0 if whole_gpu else 1 + (0 if args.serial else li),
                         ids_c=ids_c[li])
 
+    # clocks are sampled from the warm-up on (the timed region alone is only
+    # a few hundred ms): idle samples before the first step are dropped
+    clocks = Clocks(local_rank)
+    clocks.wait_started()
     for _ in range(args.warmup):
         step()
     unit.sync()
     if world > 1:
         torch.distributed.barrier()
-    clocks = Clocks(local_rank)
     launches0 = unit.launches()
     unit.sync()
     for li in range(len(specs)):
@@ -197,13 +230,15 @@ def run_ours(args, rank, world, local_rank):
     clk = clocks.stop()
 
     # K1 roofline: CUDA events around every decode-attention launch, on its
-    # stream, over separate steps of the same workload (both models' jobs
-    # still concurrent). PDL is off for these steps: with it, the event pair
-    # around a K1 launch would also span the kernel's programmatic overlap.
+    # stream, over separate steps of the same workload. The kernel is timed
+    # alone on the whole GPU (both jobs on partition 0, the ungreened stream):
+    # on a green partition it only owns that partition's share of HBM. PDL is
+    # off for these steps: with it, the event pair around a K1 launch would
+    # also span the kernel's programmatic overlap.
     unit.set_option("pdl", 0)
     unit.attn_timing(True)
     for _ in range(args.attn_steps):
-        step()
+        step(whole_gpu=True)
     unit.sync()
     attn_ms, attn_n, attn_bytes = unit.attn_time()
     unit.attn_timing(False)
@@ -229,11 +264,13 @@ def run_ours(args, rank, world, local_rank):
     for li, s in enumerate(specs):
         ctx_mid = ctx0[li] + B * (args.warmup + args.steps / 2 + 1)
         bytes_step += s.weight_bytes + ctx_mid * kv_tok[li]
+    unit_sms = [unit.partition_sms(1 + li) for li in range(len(specs))]
     unit.close()
     result = {
         "ms": ms, "tokens": len(specs) * B * args.steps, "launches": launches,
         "attn_ms": attn_ms, "attn_n": attn_n, "attn_bytes": attn_bytes, "clocks": clk,
         "e2e_ms": e2e_ms, "bytes_step": bytes_step,
+        "partition_sms": [unit_sms[li] for li in range(len(specs))] if psms else None,
     }
     return result
 
@@ -241,20 +278,23 @@ def run_ours(args, rank, world, local_rank):
 def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--gpus", type=int, default=1)
-    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--steps", type=int, default=20)
     ap.add_argument("--warmup", type=int, default=3)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=128, help="decode members per model")
     ap.add_argument("--models", default="7b,13b")
     ap.add_argument("--e2e-steps", type=int, default=4)
     ap.add_argument("--attn-steps", type=int, default=2, help="steps with per-launch K1 events")
-    ap.add_argument("--partition-sms", type=lambda s: [int(x) for x in s.split(",")], default=None,
-                    help="green-context SMs of each model's decode partition, e.g. 72,72")
+    ap.add_argument("--partition-sms", default="auto",
+                    help="green-context SMs of each model's decode partition: 'auto' (shares of the per-round "
+                         "HBM bytes, byte_share_partitions), 'none' (every job on the whole GPU), or e.g. 56,88")
     ap.add_argument("--serial", action="store_true", help="run the colocated decode jobs on one stream")
     ap.add_argument("--serve-horizon", type=float, default=3.0,
                     help="seconds of Poisson arrivals for the auxiliary measured serving run (0 = skip)")
     ap.add_argument("--fuse-qkv", type=int, default=0, help="RoPE + KV append in the QKV GEMM epilogue (experimental)")
     ap.add_argument("--chain", type=int, default=0, help="fused persistent layer chain for decode (experimental)")
+    ap.add_argument("--l2-next", type=int, default=0,
+                    help="16 KiB weight tiles per CTA of the next decode GEMM prefetched into L2 (0 = off)")
     ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch between job kernels")
     ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg (profiling runs)")
     args = ap.parse_args()
@@ -322,6 +362,7 @@ def main():
                 "pool_blocks": pool_blocks([__import__("paper_2404_02015_b200").spec(m) for m in args.models.split(",")]),
                 "l2": "inputs larger than L2 (39.5 GB weights + KV per step)",
                 "parallelism": f"{world} independent units (dp{world})",
+                "partition_sms": r["partition_sms"],
             },
             "e2e": {"value": round(per_step_tokens / (e2e_ms / 1e3), 1) if e2e_ms else None,
                     "unit": "tokens/s", "h2d_bytes_per_step": int(per_step_tokens * 4),
@@ -330,7 +371,7 @@ def main():
                          "frac": round(achieved / hbm, 4),
                          "traffic": (k1_traffic() or {}).get("dram_bytes"),
                          "traffic_note": (k1_traffic() or {}).get("capture"),
-                         "kernel": "decode_attention_kernel (K1, per-launch CUDA events)",
+                         "kernel": "decode_attention_kernel (K1, per-launch CUDA events, timed alone on the whole GPU)",
                          "peak_source": peak_kind, "launches_timed": r["attn_n"],
                          "bytes_per_launch": round(r["attn_bytes"] / max(1, r["attn_n"]))},
             "step_roofline": {"tokens_per_s_at_peak": round(step_roof, 1) if step_roof else None,

@@ -6,7 +6,7 @@ reference's C++ API (see host.py and include/mux.h).
 """
 from ._lib import LIB_PATH, MuxError, header_symbols, lib  # noqa: F401
 from .host import (CATALOG, AllocResult, BlockPool, EngineParams, Entry, LLMSpec, Placement,  # noqa: F401
-                   QuotaInput, TraceRequest, Unit, adapt_quota, blocks_for_tokens, blocks_per_token,
+                   QuotaInput, TraceRequest, Unit, adapt_quota, blocks_for_tokens, blocks_per_token, byte_share_partitions,
                    decode_attention_headwise, gemm_bf16, init_token_block_quota, kv_append,
                    prefill_attention,
                    rope_table, simulate, spec, weight_tile)

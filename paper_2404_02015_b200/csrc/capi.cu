@@ -1003,6 +1003,7 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
     else if (k == "pdl") mux::pdl_enabled() = value != 0;
     else if (k == "chain") u->rt->set_chain(value != 0);
     else if (k == "fuse_qkv") u->rt->set_fuse_qkv(value != 0);
+    else if (k == "l2_next") u->rt->set_l2_next(static_cast<int>(value));
     else throw std::invalid_argument("unknown option: " + k);
   });
 }

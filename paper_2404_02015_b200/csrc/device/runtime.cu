@@ -382,7 +382,7 @@ const void* Runtime::act_tmap(const void* base, int rows, int cols, int box_rows
 }
 
 void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void* out, int ldo, int epi,
-                   Workspace& ws, cudaStream_t stream, const QkvRopeArgs* qkv) {
+                   Workspace& ws, cudaStream_t stream, const QkvRopeArgs* qkv, const NextGemm* next) {
   // The X map is viewed over max(M, 256) rows: buffers are sized for it and
   // rows past M are never stored.
   const int rows = std::max(M, 256);
@@ -404,6 +404,13 @@ void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void
   g.ldo = ldo;
   g.epi = static_cast<Epilogue>(epi);
   if (qkv != nullptr) g.qkv = *qkv;
+  if (next != nullptr && next->w != nullptr && l2_next_ > 0) {
+    g.next_w = next->w;
+    g.next_N = next->N;
+    g.next_K = next->K;
+    g.next_epi = static_cast<Epilogue>(next->epi);
+    g.pf_stages = l2_next_;
+  }
   check_cuda(gemm_bf16_tn(g, stream), "gemm");
   launches_ += 1;
 }
@@ -668,11 +675,18 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   }
   for (int l = 0; l < L && !(chain_enabled_ && d.tp_size == 1 && n <= 256); ++l) {
     ap.layer = l;
+    // next GEMM on this stream after each projection (L2 prefetch targets)
+    const NextGemm nx_o{m.wo[l].p, hid, H * 128, kEpiResidual};
+    const NextGemm nx_gu{m.wgu[l].p, 2 * d.ffn, hid, kEpiSilu};
+    const NextGemm nx_down{m.wdown[l].p, hid, d.ffn, kEpiResidual};
+    const NextGemm nx_qkv = l + 1 < L ? NextGemm{m.wqkv[l + 1].p, m.qkv_cols(), hid, kEpiStoreBf16}
+                                      : NextGemm{m.lm_head.p, d.vocab, hid, kEpiStoreF32};
     if (fuse_qkv_) {
       const QkvRopeArgs qr = qkv_rope_args(ap);
       gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiQkvRope, ws, stream, &qr);
     } else {
-      gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
+      gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream, nullptr,
+           &nx_o);
       check_cuda(kv_append(ap, stream), "kv_append");
       launches_ += 1;
     }
@@ -697,12 +711,12 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
       row_parallel_norm(m.wdown[l].p, ws.act.p, n, hid, d.ffn, 1, next_norm, d.norm_eps, ws, stream);
       continue;
     }
-    gemm(m.wo[l].p, ws.attn.p, n, hid, H * 128, ws.resid.p, hid, kEpiResidual, ws, stream);
+    gemm(m.wo[l].p, ws.attn.p, n, hid, H * 128, ws.resid.p, hid, kEpiResidual, ws, stream, nullptr, &nx_gu);
     check_cuda(rmsnorm_rows(ws.resid.as<float>(), m.ffn_norm[l].as<float>(), ws.xn.p, n, hid, d.norm_eps, stream),
                "rmsnorm");
     launches_ += 1;
-    gemm(m.wgu[l].p, ws.xn.p, n, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, ws, stream);
-    gemm(m.wdown[l].p, ws.act.p, n, hid, d.ffn, ws.resid.p, hid, kEpiResidual, ws, stream);
+    gemm(m.wgu[l].p, ws.xn.p, n, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, ws, stream, nullptr, &nx_down);
+    gemm(m.wdown[l].p, ws.act.p, n, hid, d.ffn, ws.resid.p, hid, kEpiResidual, ws, stream, nullptr, &nx_qkv);
     check_cuda(rmsnorm_rows(ws.resid.as<float>(), next_norm, ws.xn.p, n, hid, d.norm_eps, stream), "rmsnorm");
     launches_ += 1;
   }

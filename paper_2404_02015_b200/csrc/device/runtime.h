@@ -181,6 +181,7 @@ class Runtime {
   void set_gemm_min_iters(int v) { gemm_min_iters_ = v; }
   void set_chain(bool on) { chain_enabled_ = on; }
   void set_fuse_qkv(bool on) { fuse_qkv_ = on; }
+  void set_l2_next(int stages) { l2_next_ = stages; }
   void count_launch(int64_t n = 1) { launches_ += n; }
 
   // Cached tensor map for an activation buffer viewed as rows x cols bf16.
@@ -200,8 +201,14 @@ class Runtime {
                const int32_t* tokens_host, int32_t* out_host /*nullable*/, cudaStream_t stream);
 
   // Decode-forward building blocks, exposed for tests/bench.
+  // The next GEMM on the same stream (decode chains): its first weight tiles
+  // are prefetched into L2 during this launch's tail (l2_next option).
+  struct NextGemm {
+    const void* w = nullptr;
+    int N = 0, K = 0, epi = 0;
+  };
   void gemm(const void* w_tiled, const void* x, int M, int N, int K, void* out, int ldo, int epi,
-            Workspace& ws, cudaStream_t stream, const QkvRopeArgs* qkv = nullptr);
+            Workspace& ws, cudaStream_t stream, const QkvRopeArgs* qkv = nullptr, const NextGemm* next = nullptr);
   // Row-parallel projection + the fused allreduce (tp > 1): out partial of
   // X[M x K] W[N x K]^T to every rank's slot `s`, then resid += sum of ranks'
   // slots and xn = rmsnorm(resid) * norm_w on this rank.
@@ -216,7 +223,8 @@ class Runtime {
   int64_t launches_ = 0;
   int gemm_min_iters_ = 24;
   bool chain_enabled_ = false;
-  bool fuse_qkv_ = false;  // K2 in the QKV GEMM epilogue (kQkvRope): measured slower than kv_append  // measured slower than separate launches so far
+  bool fuse_qkv_ = false;  // K2 in the QKV GEMM epilogue (kQkvRope): measured slower than kv_append
+  int l2_next_ = 0;        // tiles per CTA of the next decode GEMM prefetched into L2 (0 = off)
   DevMem pool_;
   DevMem rope_;
   struct StageSlot {

@@ -87,10 +87,19 @@ struct GemmRun {
   // it adds 1 to signal[0..n_signal) (this rank's and every peer's counter).
   QkvRopeArgs qr;   // kQkvRope
   int a_split;      // bulk copies per weight stage (1, 2, 4)
+  int n_stg;        // epilogue staging buffers (1 or 2)
   int dbg_nomma;    // debug (MUX_GEMM_NOMMA): stream operands without MMAs
   int n_peers;
   int n_signal;
   int* signal[kMaxTp];
+  // Cross-launch L2 prefetch: once this CTA has issued its last weight load,
+  // it prefetches the first pf_stages tiles of its range in the NEXT decode
+  // GEMM of the chain (same flattened [m][kb] tile layout, contiguous), so
+  // HBM keeps streaming through this launch's tail and the next one's head.
+  const uint8_t* next_w;
+  int next_grid;
+  int pf_stages;
+  int64_t next_iters;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -179,7 +188,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   uint8_t* a_st = base;
   uint8_t* b_st = base + SA * kAStageBytes;
   uint8_t* stage_out = b_st + SB * b_stage_bytes;  // 2 x 16 KiB epilogue staging
-  uint64_t* full_a = reinterpret_cast<uint64_t*>(stage_out + 2 * kChunkBytes);
+  uint64_t* full_a = reinterpret_cast<uint64_t*>(stage_out + r.n_stg * kChunkBytes);
   uint64_t* empty_a = full_a + SA;
   uint64_t* full_b = empty_a + SA;
   uint64_t* empty_b = full_b + SB;
@@ -220,6 +229,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
+  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 32 + 15] = gtimer();
   if (threadIdx.x == 0) grid_dep_launch();
 
   if (warp == 0 || warp == 3) {
@@ -244,6 +254,13 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       bool skp;
       int64_t lo;
       int s = 0, round = 0;
+      int64_t issued = 0, pf_at = -1;
+      if (is_a && r.next_w != nullptr && c < r.next_grid) {
+        // start the prefetch when ~SA stages of this range remain
+        const int64_t mine = range_begin(r.sk_iters, c + 1, G) - range_begin(r.sk_iters, c, G) +
+                             static_cast<int64_t>(r.n_dp) * r.kb;
+        pf_at = mine > SA ? mine - SA : 0;
+      }
       while (sg.next(r, c, G, m, nt, kb0, kb1, skp, lo)) {
         for (int kbi = kb0; kbi < kb1; ++kbi) {
           if (round > 0) mbar_wait(&eb[s], (round - 1) & 1);
@@ -260,6 +277,12 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             }
           } else {
             tma_load_2d(b_st + s * b_stage_bytes, &tx, &fb[s], kbi * kBK, nt * r.n_tile, pol);
+          }
+          if (is_a && round == 0 && s == 0 && r.timing != nullptr) r.timing[c * 32 + 19] = gtimer();
+          if (issued++ == pf_at) {
+            const int64_t b0 = range_begin(r.next_iters, c, r.next_grid);
+            const int64_t b1 = min(range_begin(r.next_iters, c + 1, r.next_grid), b0 + r.pf_stages);
+            for (int64_t t = b0; t < b1; ++t) prefetch_l2(r.next_w + t * kAStageBytes, kAStageBytes);
           }
           if (++s == SS) {
             s = 0;
@@ -416,7 +439,10 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           for (int j = 0; j < 32; ++j) v[j] += src[j * kBM];
         }
         // Staging buffer: wait until the bulk group that last read it is done.
-        if (leader) bulk_wait_read<1>();
+        if (leader) {
+          if (r.n_stg == 2) bulk_wait_read<1>();
+          else bulk_wait_read<0>();
+        }
         epi_bar();
         if (stamp) r.timing[c * 32 + 24 + k] = gtimer();
         uint8_t* st = stage_out + sbuf * kChunkBytes;
@@ -511,7 +537,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           bulk_commit();
           if (stamp) r.timing[c * 32 + 28 + k] = gtimer();
         }
-        sbuf ^= 1;
+        if (r.n_stg == 2) sbuf ^= 1;
       }
       if (!first && leader) {  // publish: partial bulk writes complete, then the flag
         {
@@ -534,6 +560,10 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     }
     if (r.timing != nullptr && threadIdx.x == 128) r.timing[c * 32 + 2] = gtimer();
   }
+  // Reconverge the role warps (elected producer / MMA lanes) before the
+  // block barrier: a diverged warp would arrive early and let warp 2 free
+  // TMEM while the epilogue still reads it.
+  __syncwarp();
   tc_fence_before();
   __syncthreads();
   if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 32 + 3] = gtimer();
@@ -662,10 +692,8 @@ cudaError_t preload_gemm() { return preload(gemm_tn_kernel, weight_tile_kernel);
 static unsigned long long* g_debug_timing = nullptr;
 void gemm_debug_timing(void* buf) { g_debug_timing = static_cast<unsigned long long*>(buf); }
 
-cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
-  if (a.M <= 0 || a.N <= 0) return cudaSuccess;
-  // tmap_x must have been encoded with box rows == gemm_pick_n_tile(M).
-  GemmRun r{};
+// Tiling, pipeline depths, grid and schedule of one launch (no side effects).
+static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out) {
   r.w_tiled = static_cast<const uint8_t*>(a.w_tiled);
   r.timing = g_debug_timing;
   r.out = a.out;
@@ -688,9 +716,12 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   static const int env_nomma = getenv("MUX_GEMM_NOMMA") ? atoi(getenv("MUX_GEMM_NOMMA")) : 0;
   r.dbg_nomma = env_nomma;
   const int meta_bytes = a.epi == Epilogue::kQkvRope ? 2 * 256 * 4 : 0;  // token positions + block ids
-  r.stages_a = (kSmemBudget - meta_bytes - r.stages_b * b_stage - 2 * kChunkBytes) / kAStageBytes;
-  if (r.stages_a > 10) r.stages_a = 10;
-  if (env_sa > 0 && env_sa < r.stages_a) r.stages_a = env_sa;
+  static const int env_stg = getenv("MUX_GEMM_STG") ? atoi(getenv("MUX_GEMM_STG")) : 2;
+  static const int env_budget = getenv("MUX_GEMM_SMEM_KB") ? atoi(getenv("MUX_GEMM_SMEM_KB")) * 1024 : kSmemBudget;
+  r.n_stg = env_stg == 1 ? 1 : 2;
+  r.stages_a = (env_budget - meta_bytes - r.stages_b * b_stage - r.n_stg * kChunkBytes) / kAStageBytes;
+  if (env_sa > 0) r.stages_a = std::min(env_sa, r.stages_a);
+  else if (r.stages_a > 10) r.stages_a = 10;
   // The fixer prefetches up to 2 partners x ceil(n_tile/32) chunks into the A ring.
   r.kb = (a.K + kBK - 1) / kBK;
   r.m_tiles = (a.N + kBM - 1) / kBM;
@@ -731,8 +762,33 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
     r.group_m = 0;
   }
   r.sk_iters = (tiles - static_cast<int64_t>(r.n_dp) * grid) * r.kb;
-  const size_t smem = 1024 + static_cast<size_t>(r.stages_a) * kAStageBytes + static_cast<size_t>(r.stages_b) * b_stage +
-                      2 * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16 + meta_bytes;
+  smem_out = 1024 + static_cast<size_t>(r.stages_a) * kAStageBytes + static_cast<size_t>(r.stages_b) * b_stage +
+             r.n_stg * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16 + meta_bytes;
+  grid_out = grid;
+}
+
+cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
+  if (a.M <= 0 || a.N <= 0) return cudaSuccess;
+  // tmap_x must have been encoded with box rows == gemm_pick_n_tile(M).
+  GemmRun r{};
+  int grid = 0;
+  size_t smem = 0;
+  plan(a, r, grid, smem);
+  if (a.next_w != nullptr && a.pf_stages > 0 && r.n_tok_tiles == 1) {
+    // the next decode GEMM of the chain: same tokens, same partition
+    GemmArgs na = a;
+    na.N = a.next_N;
+    na.K = a.next_K;
+    na.epi = a.next_epi;
+    GemmRun nr{};
+    int ngrid = 0;
+    size_t nsmem = 0;
+    plan(na, nr, ngrid, nsmem);
+    r.next_w = static_cast<const uint8_t*>(a.next_w);
+    r.next_grid = ngrid;
+    r.next_iters = nr.sk_iters;
+    r.pf_stages = a.pf_stages;
+  }
   static bool configured = false;
   if (!configured) {
     cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);

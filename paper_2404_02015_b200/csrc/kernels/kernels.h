@@ -100,6 +100,13 @@ struct GemmArgs {
   int n_signal = 0;
   int* signal[kMaxTp] = {};
   int* grid_out = nullptr;
+  // Decode chains: the weights (weight_tile layout) and shape of the NEXT
+  // GEMM on this stream; each CTA prefetches the first pf_stages 16 KiB tiles
+  // of its range there into L2 once its own weight loads are issued.
+  const void* next_w = nullptr;
+  int next_N = 0, next_K = 0;
+  Epilogue next_epi = Epilogue::kStoreBf16;
+  int pf_stages = 0;
 };
 cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream);
 int gemm_pick_n_tile(int M);

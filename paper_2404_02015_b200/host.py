@@ -306,6 +306,31 @@ def _ptr(x) -> int | None:
     return int(x)
 
 
+def byte_share_partitions(specs: Sequence[LLMSpec], ctx_tokens: Sequence[int], total_sms: int = 148,
+                          granule: int = 8) -> list[int]:
+    """SMs of each colocated decode job's green partition, proportional to the
+    HBM bytes the job streams per round (its weights + the K/V of its members'
+    contexts): decode is HBM-bound, so equal per-SM bandwidth demand lets the
+    jobs finish their rounds together. The reference expresses the same split
+    as a JobPlan's sm_demand share (scheduler.cpp:50-54, sim_engine.cpp:16-18).
+    Shares are whole 8-SM granules (the sm_100 green-context granularity),
+    largest-remainder rounded; the unit's leftover SMs join the last
+    partition (Unit creation does that)."""
+    bytes_ = [s.weight_bytes + c * s.kv_bytes_per_token() for s, c in zip(specs, ctx_tokens)]
+    n = len(specs)
+    units = total_sms // granule
+    if n == 0 or units < n:
+        raise ValueError("not enough SM granules for one partition per job")
+    tot = sum(bytes_)
+    exact = [b / tot * units for b in bytes_]
+    share = [max(1, int(e)) for e in exact]
+    while sum(share) > units:
+        share[max(range(n), key=lambda i: share[i] - exact[i])] -= 1
+    for i in sorted(range(n), key=lambda i: share[i] - exact[i])[: units - sum(share)]:
+        share[i] += 1
+    return [g * granule for g in share]
+
+
 class Unit:
     """One GPU: the unified KV pool in HBM plus colocated LLaMA models."""
 
