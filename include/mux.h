@@ -152,6 +152,41 @@ typedef struct {
 MUX_API int mux_simulate(const mux_sim_config* cfg, int n_entries, const mux_llm_entry* entries,
                  int n_requests, const mux_request* trace, mux_record* records_out);
 
+/* Priced run plus the per-unit pool statistics behind the reference's
+ * poolstats.json / metrics.json "units" (sim_engine.hpp:48-71,
+ * commands.cpp:89-121). Release with mux_sim_stats_destroy. */
+typedef struct mux_sim_stats mux_sim_stats;
+typedef struct {
+  int unit;
+  int64_t total_blocks;
+  int n_llms;
+  int64_t n_samples;
+} mux_unit_stats;
+typedef struct {
+  int llm;                     /* entry index */
+  double rate, avg_used_blocks;
+  int64_t final_quota_blocks;
+  double resource_usage;
+} mux_unit_llm_stats;
+typedef struct {
+  double t_s;
+  int llm;                     /* entry index */
+  int64_t used_blocks, quota_blocks;
+} mux_pool_sample;
+MUX_API int mux_simulate_stats(const mux_sim_config* cfg, int n_entries, const mux_llm_entry* entries,
+                               int n_requests, const mux_request* trace, mux_record* records_out,
+                               mux_sim_stats** stats_out);
+MUX_API int mux_sim_stats_units(const mux_sim_stats* stats, int* n_units);
+MUX_API int mux_sim_stats_unit(const mux_sim_stats* stats, int unit, mux_unit_stats* out);
+MUX_API int mux_sim_stats_llms(const mux_sim_stats* stats, int unit, mux_unit_llm_stats* out /* [n_llms] */);
+MUX_API int mux_sim_stats_samples(const mux_sim_stats* stats, int unit, mux_pool_sample* out /* [n_samples] */);
+MUX_API void mux_sim_stats_destroy(mux_sim_stats* stats);
+
+/* slo_reference_latency_ms (metrics.cpp:21-27): the unloaded latency a
+ * request's SLO is a multiple of. profile: 7 doubles or NULL (defaults). */
+MUX_API int mux_slo_reference_latency_ms(const mux_llm_entry* entry, const double* profile, int tp_degree,
+                                         int prompt_len, int output_len, double* out_ms);
+
 /* ---- kernels (device pointers; stream = cudaStream_t or NULL) --------- */
 
 /* K1: head-wise paged decode attention for one layer (the work priced by
@@ -309,6 +344,9 @@ MUX_API int mux_unit_run_lockstep(mux_unit* unit, const mux_sim_config* cfg, int
  * from the start of its scheduling pass, the pass's jobs running concurrently
  * on their partitions) instead of the pricing model's. Records then carry
  * real TTFT / latency; throughput = tokens / last done time. */
+/* Pool statistics (poolstats.json) of the unit's last lockstep / measured
+ * run; release with mux_sim_stats_destroy. */
+MUX_API int mux_unit_last_stats(mux_unit* unit, mux_sim_stats** out);
 MUX_API int mux_unit_run_measured(mux_unit* unit, const mux_sim_config* cfg, int n_entries,
                                   const mux_llm_entry* entries, int n_requests, const mux_request* trace,
                                   uint64_t prompt_seed, mux_record* records_out, int32_t* tokens_out);

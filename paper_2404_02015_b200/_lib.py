@@ -71,6 +71,19 @@ class Record(C.Structure):
                 ("done_s", f64), ("prompt_len", C.c_int), ("output_len", C.c_int)]
 
 
+class UnitStats(C.Structure):
+    _fields_ = [("unit", C.c_int), ("total_blocks", i64), ("n_llms", C.c_int), ("n_samples", i64)]
+
+
+class UnitLlmStats(C.Structure):
+    _fields_ = [("llm", C.c_int), ("rate", f64), ("avg_used_blocks", f64), ("final_quota_blocks", i64),
+                ("resource_usage", f64)]
+
+
+class PoolSample(C.Structure):
+    _fields_ = [("t_s", f64), ("llm", C.c_int), ("used_blocks", i64), ("quota_blocks", i64)]
+
+
 class UnitConfig(C.Structure):
     _fields_ = [("device", C.c_int), ("n_llms", C.c_int), ("llms", P(LlmEntry)),
                 ("pool_blocks", i64), ("device_pool_blocks", i64), ("max_batch", C.c_int),
@@ -99,6 +112,14 @@ _SIGS = {
     "mux_pool_block_table": (C.c_int, [vp, C.c_int, i64, P(i32), i64, P(i64)]),
     "mux_pool_slot": (C.c_int, [vp, C.c_int, i64, P(C.c_int)]),
     "mux_simulate": (C.c_int, [P(SimConfig), C.c_int, P(LlmEntry), C.c_int, P(Request), P(Record)]),
+    "mux_simulate_stats": (C.c_int, [P(SimConfig), C.c_int, P(LlmEntry), C.c_int, P(Request), P(Record),
+                                     P(vp)]),
+    "mux_sim_stats_units": (C.c_int, [vp, P(C.c_int)]),
+    "mux_sim_stats_unit": (C.c_int, [vp, C.c_int, P(UnitStats)]),
+    "mux_sim_stats_llms": (C.c_int, [vp, C.c_int, P(UnitLlmStats)]),
+    "mux_sim_stats_samples": (C.c_int, [vp, C.c_int, P(PoolSample)]),
+    "mux_sim_stats_destroy": (None, [vp]),
+    "mux_slo_reference_latency_ms": (C.c_int, [P(LlmEntry), P(f64), C.c_int, C.c_int, C.c_int, P(f64)]),
     "mux_decode_attention_headwise": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,
                                                 C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int,
                                                 vp, sz, vp]),
@@ -133,6 +154,7 @@ _SIGS = {
     "mux_unit_attn_timing": (C.c_int, [vp, C.c_int]),
     "mux_unit_attn_time": (C.c_int, [vp, P(f64), P(i64), P(f64)]),
     "mux_unit_launches": (i64, [vp]),
+    "mux_unit_last_stats": (C.c_int, [vp, P(vp)]),
     "mux_unit_run_lockstep": (C.c_int, [vp, P(SimConfig), C.c_int, P(LlmEntry), C.c_int,
                                         P(Request), u64, P(Record), P(i32)]),
     "mux_unit_run_measured": (C.c_int, [vp, P(SimConfig), C.c_int, P(LlmEntry), C.c_int,

@@ -211,9 +211,16 @@ uint64_t mix64(uint64_t x) {
 
 }  // namespace
 
+// Pool statistics of a run (SimResult.units) behind poolstats.json.
+struct mux_sim_stats {
+  std::vector<muxsim::UnitStats> units;
+  std::unordered_map<std::string, int> idx;  // model name -> entry index
+};
+
 // -------------------------------------------------------------------- unit
 
 struct mux_unit {
+  std::unique_ptr<mux_sim_stats> last_stats;  // of the last lockstep / measured run
   std::unique_ptr<mux::Runtime> rt;
   std::deque<muxsim::LLMSpec> specs;
   std::vector<std::unique_ptr<mux::Llama>> models;
@@ -498,6 +505,90 @@ int mux_simulate(const mux_sim_config* cfg, int n_entries, const mux_llm_entry* 
     SimInputs in = build_inputs(cfg, n_entries, entries, n_requests, trace);
     muxsim::SimResult res = muxsim::run_simulation(in.cluster, in.placement, in.entries, in.trace, in.prof, in.params);
     export_records(res, in, records_out);
+  });
+}
+
+int mux_simulate_stats(const mux_sim_config* cfg, int n_entries, const mux_llm_entry* entries, int n_requests,
+                       const mux_request* trace, mux_record* records_out, mux_sim_stats** stats_out) {
+  return guarded([&] {
+    require(stats_out != nullptr, "null argument");
+    *stats_out = nullptr;
+    SimInputs in = build_inputs(cfg, n_entries, entries, n_requests, trace);
+    muxsim::SimResult res = muxsim::run_simulation(in.cluster, in.placement, in.entries, in.trace, in.prof, in.params);
+    export_records(res, in, records_out);
+    auto st = std::make_unique<mux_sim_stats>();
+    for (size_t i = 0; i < in.entries.size(); ++i) st->idx[in.entries[i].spec.name] = static_cast<int>(i);
+    st->units = std::move(res.units);
+    *stats_out = st.release();
+  });
+}
+
+void mux_sim_stats_destroy(mux_sim_stats* st) { delete st; }
+
+int mux_sim_stats_units(const mux_sim_stats* st, int* n_units) {
+  return guarded([&] {
+    require(st != nullptr && n_units != nullptr, "null argument");
+    *n_units = static_cast<int>(st->units.size());
+  });
+}
+
+int mux_sim_stats_unit(const mux_sim_stats* st, int u, mux_unit_stats* out) {
+  return guarded([&] {
+    require(st != nullptr && out != nullptr, "null argument");
+    require(u >= 0 && u < static_cast<int>(st->units.size()), "unit out of range");
+    const muxsim::UnitStats& us = st->units[u];
+    out->unit = us.unit;
+    out->total_blocks = us.total_blocks;
+    out->n_llms = static_cast<int>(us.llms.size());
+    out->n_samples = static_cast<int64_t>(us.samples.size());
+  });
+}
+
+int mux_sim_stats_llms(const mux_sim_stats* st, int u, mux_unit_llm_stats* out) {
+  return guarded([&] {
+    require(st != nullptr && out != nullptr, "null argument");
+    require(u >= 0 && u < static_cast<int>(st->units.size()), "unit out of range");
+    const muxsim::UnitStats& us = st->units[u];
+    for (size_t i = 0; i < us.llms.size(); ++i) {
+      const muxsim::UnitLlmStats& m = us.llms[i];
+      out[i] = {st->idx.at(m.llm), m.rate, m.avg_used_blocks, m.final_quota_blocks, m.resource_usage};
+    }
+  });
+}
+
+int mux_sim_stats_samples(const mux_sim_stats* st, int u, mux_pool_sample* out) {
+  return guarded([&] {
+    require(st != nullptr && out != nullptr, "null argument");
+    require(u >= 0 && u < static_cast<int>(st->units.size()), "unit out of range");
+    const muxsim::UnitStats& us = st->units[u];
+    for (size_t i = 0; i < us.samples.size(); ++i) {
+      const muxsim::PoolSample& p = us.samples[i];
+      out[i] = {p.t_s, st->idx.at(p.llm), p.used_blocks, p.quota_blocks};
+    }
+  });
+}
+
+int mux_slo_reference_latency_ms(const mux_llm_entry* entry, const double* profile, int tp_degree, int prompt_len,
+                                 int output_len, double* out_ms) {
+  return guarded([&] {
+    require(entry != nullptr && out_ms != nullptr, "null argument");
+    const muxsim::LLMSpec spec = spec_of(*entry);
+    muxsim::LatencyProfile prof;
+    if (profile) {
+      prof.prefill_ms_per_token = profile[0];
+      prof.decode_base_ms = profile[1];
+      prof.decode_ctx_ms_per_token = profile[2];
+      prof.tp_efficiency = profile[3];
+      prof.sm_saturation_point = profile[4];
+      prof.batch_knee = profile[5];
+      prof.reference_scale = profile[6];
+    }
+    // metrics.cpp:21-27: one prefill over the prompt + output_len-1 decode
+    // steps, context growing by one token per step, whole SM budget
+    muxsim::ExecConfig cfg{tp_degree, 1.0};
+    double t = muxsim::prefill_latency(spec, prof, cfg, 1, prompt_len);
+    for (int k = 1; k < output_len; ++k) t += muxsim::decode_step_latency(spec, prof, cfg, 1, prompt_len + k);
+    *out_ms = t;
   });
 }
 
@@ -1020,6 +1111,9 @@ int run_unit(mux_unit* u, const mux_sim_config* cfg, int n_entries, const mux_ll
     muxsim::SimResult res =
         muxsim::run_simulation(in.cluster, in.placement, in.entries, in.trace, in.prof, in.params, &exec);
     export_records(res, in, records_out);
+    u->last_stats = std::make_unique<mux_sim_stats>();
+    for (size_t i = 0; i < in.entries.size(); ++i) u->last_stats->idx[in.entries[i].spec.name] = static_cast<int>(i);
+    u->last_stats->units = res.units;
     if (tokens_out) {
       size_t off = 0;
       for (int i = 0; i < n_requests; ++i) {
@@ -1045,6 +1139,14 @@ int mux_unit_run_measured(mux_unit* u, const mux_sim_config* cfg, int n_entries,
                           int n_requests, const mux_request* trace, uint64_t prompt_seed, mux_record* records_out,
                           int32_t* tokens_out) {
   return run_unit(u, cfg, n_entries, entries, n_requests, trace, prompt_seed, records_out, tokens_out, true);
+}
+
+int mux_unit_last_stats(mux_unit* u, mux_sim_stats** out) {
+  return guarded([&] {
+    require(u != nullptr && out != nullptr, "null argument");
+    require(u->last_stats != nullptr, "no lockstep / measured run yet");
+    *out = new mux_sim_stats(*u->last_stats);
+  });
 }
 
 }  // extern "C"

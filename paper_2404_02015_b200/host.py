@@ -15,6 +15,7 @@ from typing import Iterable, Sequence
 
 from ._lib import (ALLOC_OK, ALLOC_POOL, ALLOC_QUOTA, LlmEntry as _CEntry, PlacedLlm, Record,
                    Request as _CRequest, SimConfig, UnitConfig, check, lib)
+from ._lib import PoolSample as _PoolSample, UnitLlmStats as _UnitLlmStats, UnitStats as _UnitStats
 
 # ----------------------------------------------------------------- model specs
 
@@ -248,6 +249,7 @@ class Placement:
     mesh_sizes: list[int]
     members: list[list[int]]                 # per unit: entry indices
     num_sm: float = 0.5
+    tp_degree: dict = field(default_factory=dict)  # entry index -> plan tp_degree (metrics' placed_tp)
 
 
 @dataclass
@@ -284,16 +286,76 @@ def _c_trace(trace: Sequence[TraceRequest]):
                                                         r.output_len) for r in trace])
 
 
+@dataclass
+class UnitLlmStat:
+    """UnitLlmStats (sim_engine.hpp:57-63); llm = entry index."""
+    llm: int
+    rate: float
+    avg_used_blocks: float
+    final_quota_blocks: int
+    resource_usage: float
+
+
+@dataclass
+class UnitStat:
+    """UnitStats (sim_engine.hpp:65-70): pool statistics of one unit;
+    samples are (t_s, llm entry index, used_blocks, quota_blocks)."""
+    unit: int
+    total_blocks: int
+    llms: list
+    samples: list
+
+
 def simulate(entries: Sequence[Entry], trace: Sequence[TraceRequest], placement: Placement,
              gpu_memory_bytes: int, params: EngineParams | None = None,
-             profile: Sequence[float] | None = None) -> list[Record]:
-    """run_simulation (sim_engine.cpp:370-413), priced. Records sorted by id."""
+             profile: Sequence[float] | None = None, stats: bool = False):
+    """run_simulation (sim_engine.cpp:370-413), priced. Records sorted by id;
+    with stats=True returns (records, [UnitStat]) -- SimResult.units."""
     params = params or EngineParams()
     b = _build_config(gpu_memory_bytes, sum(placement.mesh_sizes), placement, params, profile)
     ents = _c_entries(entries, b.keep)
     recs = (Record * max(len(trace), 1))()
-    check(lib.mux_simulate(C.byref(b.cfg), len(entries), ents, len(trace), _c_trace(trace), recs))
-    return list(recs[:len(trace)])
+    if not stats:
+        check(lib.mux_simulate(C.byref(b.cfg), len(entries), ents, len(trace), _c_trace(trace), recs))
+        return list(recs[:len(trace)])
+    h = C.c_void_p()
+    check(lib.mux_simulate_stats(C.byref(b.cfg), len(entries), ents, len(trace), _c_trace(trace), recs,
+                                 C.byref(h)))
+    units = _read_stats(h)
+    return list(recs[:len(trace)]), units
+
+
+def _read_stats(h) -> list:
+    """Copy a mux_sim_stats handle into UnitStat objects and release it."""
+    try:
+        n = C.c_int()
+        check(lib.mux_sim_stats_units(h, C.byref(n)))
+        units = []
+        for u in range(n.value):
+            us = _UnitStats()
+            check(lib.mux_sim_stats_unit(h, u, C.byref(us)))
+            ll = (_UnitLlmStats * max(us.n_llms, 1))()
+            check(lib.mux_sim_stats_llms(h, u, ll))
+            ps = (_PoolSample * max(us.n_samples, 1))()
+            check(lib.mux_sim_stats_samples(h, u, ps))
+            units.append(UnitStat(us.unit, us.total_blocks,
+                                  [UnitLlmStat(m.llm, m.rate, m.avg_used_blocks, m.final_quota_blocks,
+                                               m.resource_usage) for m in ll[:us.n_llms]],
+                                  [(p.t_s, p.llm, p.used_blocks, p.quota_blocks) for p in ps[:us.n_samples]]))
+        return units
+    finally:
+        lib.mux_sim_stats_destroy(h)
+
+
+def slo_reference_latency_ms(s: LLMSpec, profile: Sequence[float] | None, tp_degree: int, prompt_len: int,
+                             output_len: int) -> float:
+    """metrics.cpp:21-27 (cost model in libmux.so)."""
+    keep = []
+    e = _c_entry(s, keep=keep)
+    prof = None if profile is None else (C.c_double * 7)(*profile)
+    out = C.c_double()
+    check(lib.mux_slo_reference_latency_ms(C.byref(e), prof, tp_degree, prompt_len, output_len, C.byref(out)))
+    return out.value
 
 
 # ---------------------------------------------------------------------- Unit
@@ -435,6 +497,12 @@ class Unit:
         """Map a peer rank's mailbox: IPC handle (other process) or pointer (same process)."""
         h = None if handle is None else (C.c_ubyte * 64).from_buffer_copy(handle)
         check(lib.mux_unit_tp_connect(self._h, partition, peer_rank, h, ptr))
+
+    def last_stats(self) -> list:
+        """Pool statistics (SimResult.units) of the last run_lockstep / measured run."""
+        h = C.c_void_p()
+        check(lib.mux_unit_last_stats(self._h, C.byref(h)))
+        return _read_stats(h)
 
     def partition_sms(self, partition: int) -> int:
         v = C.c_int()

@@ -3,9 +3,10 @@
     python -m paper_2404_02015_b200.muxsim_cli -c cfg.json -p plan.json -t trace.csv -o out/ \\
         [--engine priced|lockstep|measured]
 
-Reads the reference's config / plan.json / trace.csv and writes records.csv
-in the reference's format (/root/reference/proj/src/commands.cpp:265-298,
-74-87). Engines:
+Reads the reference's config / plan.json / trace.csv and writes records.csv,
+metrics.json and poolstats.json in the reference's formats
+(/root/reference/proj/src/commands.cpp:265-298, 74-121; metrics.cpp:40-167).
+Engines:
   priced    the reference's event loop and pricing model in libmux.so
             (CPU; records byte-identical to `muxsim simulate`)
   lockstep  the same decisions, every job executed on this GPU (random-init
@@ -31,7 +32,8 @@ def run(cfg_path: str, plan_path: str, trace_path: str, out_dir: str, engine: st
     placement = wire.load_plan(plan_path, exp.names)
     trace = wire.load_trace(trace_path, exp.names)
     if engine == "priced":
-        recs = simulate(exp.entries, trace, placement, exp.gpu_memory_bytes, exp.params, exp.profile)
+        recs, units = simulate(exp.entries, trace, placement, exp.gpu_memory_bytes, exp.params, exp.profile,
+                               stats=True)
     else:
         if len(placement.mesh_sizes) != 1 or placement.mesh_sizes[0] != 1:
             raise wire.ConfigError("GPU engines serve a single-unit, single-GPU plan")
@@ -46,10 +48,21 @@ def run(cfg_path: str, plan_path: str, trace_path: str, out_dir: str, engine: st
             recs, _ = unit.run_lockstep([exp.entries[i] for i in placement.members[0]], trace,
                                         exp.gpu_memory_bytes, exp.params, profile=exp.profile,
                                         measured=engine == "measured")
+            units = unit.last_stats()
+            mem = placement.members[0]  # unit-local entry index -> config entry index
+            for u in units:
+                for m in u.llms:
+                    m.llm = mem[m.llm]
+                u.samples = [(t, mem[li], used, q) for t, li, used, q in u.samples]
         finally:
             unit.close()
+    report = wire.compute_metrics(recs, exp, placement)
     os.makedirs(out_dir, exist_ok=True)
     wire.write_records_csv(os.path.join(out_dir, "records.csv"), recs, exp.names)
+    with open(os.path.join(out_dir, "metrics.json"), "w") as f:
+        f.write(wire.metrics_json(report, exp, units))
+    with open(os.path.join(out_dir, "poolstats.json"), "w") as f:
+        f.write(wire.poolstats_json(units, exp.names))
     return recs
 
 
@@ -72,7 +85,7 @@ def main(argv=None) -> int:
     except Exception as e:  # noqa: BLE001 - the reference maps everything else to 3
         print(f"error: {e}", file=sys.stderr)
         return 3
-    print(f"engine {a.engine}: {len(recs)} requests; wrote {a.output}/records.csv")
+    print(f"engine {a.engine}: {len(recs)} requests; wrote {a.output}/records.csv, metrics.json, poolstats.json")
     return 0
 
 

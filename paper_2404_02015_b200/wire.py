@@ -9,6 +9,9 @@ Format sources (reference, read-only):
   plan.json     /root/reference/proj/src/commands.cpp:165-217 placement_from_json
   trace.csv     /root/reference/proj/src/workload.cpp:138-215 save/load_trace
   records.csv   /root/reference/proj/src/commands.cpp:74-87 write_records_csv
+  metrics.json  /root/reference/proj/src/metrics.cpp:40-167 compute_metrics /
+                report_to_json (nlohmann ordered_json dump(2))
+  poolstats.json /root/reference/proj/src/commands.cpp:89-121 poolstats_json
   rates         /root/reference/proj/src/workload.cpp:78-86 gen_rates
 The engine itself is libmux.so (priced: mux_simulate, bit-identical to the
 reference; lockstep / measured: a GPU unit).
@@ -16,9 +19,10 @@ reference; lockstep / measured: a GPU unit).
 from __future__ import annotations
 
 import json
+import math
 from dataclasses import dataclass, field
 
-from .host import CATALOG, EngineParams, Entry, LLMSpec, Placement, TraceRequest
+from .host import CATALOG, EngineParams, Entry, LLMSpec, Placement, TraceRequest, slo_reference_latency_ms
 
 GIB = 1 << 30
 
@@ -42,9 +46,11 @@ class Experiment:
     entries: list[Entry]
     params: EngineParams
     profile: list[float]
-    horizon_s: float = 0.0
+    horizon_s: float = 60.0
     seed: int = 0
     extra: dict = field(default_factory=dict)
+    slo_scales: list = field(default_factory=lambda: [1.0, 2.0, 4.0, 8.0, 16.0])  # config.hpp:61
+    slo_reference_tp_one: bool = False                                           # config.hpp:60
 
 
 def _mean_len(d, what):
@@ -120,8 +126,17 @@ def load_config(path: str, catalog: dict[str, LLMSpec] | None = None) -> Experim
             setattr(p, k, int(sim[k]))
     if "decode_sm" not in sim:
         p.decode_sm = prof[PROFILE_KEYS.index("sm_saturation_point")]
-    return Experiment(num_nodes, gpn, mem, names, entries, p, prof, float(wl.get("horizon_s", 0.0)),
-                      int(wl.get("seed", 0)), {"root": root})
+    exp = Experiment(num_nodes, gpn, mem, names, entries, p, prof, float(wl.get("horizon_s", 60.0)),
+                     int(wl.get("seed", 0)), {"root": root})
+    if exp.horizon_s <= 0.0:
+        raise ConfigError("workload.horizon_s must be positive")
+    scales = (root.get("metrics") or {}).get("slo_scales")
+    if scales is not None:
+        if not isinstance(scales, list) or not scales or any(float(x) <= 0.0 for x in scales):
+            raise ConfigError("metrics.slo_scales must be a non-empty list of positive numbers")
+        exp.slo_scales = [float(x) for x in scales]
+    exp.slo_reference_tp_one = bool(sim.get("slo_reference_tp_one", False))
+    return exp
 
 
 def load_plan(path: str, names: list[str]) -> Placement:
@@ -133,7 +148,7 @@ def load_plan(path: str, names: list[str]) -> Placement:
             raise ConfigError(f"plan: invalid JSON: {e}") from None
     if not isinstance(root, dict) or not isinstance(root.get("units"), list):
         raise ConfigError("plan: expected an object with a 'units' array")
-    sizes, members = [], []
+    sizes, members, tp = [], [], {}
     for u in root["units"]:
         if not isinstance(u, dict) or not isinstance(u.get("gpu_ids"), list):
             raise ConfigError("plan: each unit needs a gpu_ids array")
@@ -143,8 +158,9 @@ def load_plan(path: str, names: list[str]) -> Placement:
             if m.get("name") not in names:
                 raise ConfigError(f"plan: model '{m.get('name')}' is not in the config")
             mem.append(names.index(m["name"]))
+            tp[names.index(m["name"])] = int(m.get("tp_degree", len(u["gpu_ids"])))  # commands.cpp:205
         members.append(mem)
-    return Placement(sizes, members)
+    return Placement(sizes, members, tp_degree=tp)
 
 
 def load_trace(path: str, names: list[str]) -> list[TraceRequest]:
@@ -192,3 +208,154 @@ def write_records_csv(path: str, records, names: list[str]) -> None:
             tpot = (r.done_s - r.first_token_s) / (r.output_len - 1) if r.output_len > 1 else 0.0
             f.write(b"%d,%s,%.9f,%.9f,%.9f,%.9f\n" % (r.id, names[r.llm].encode(), r.arrival_s, ttft, tpot,
                                                    r.done_s))
+
+
+# ------------------------------------------------------------ metrics.json
+
+def _dump(obj) -> str:
+    """nlohmann::ordered_json::dump(2) + newline: insertion-ordered keys,
+    2-space indent, shortest round-trip doubles (integral ones as "2.0"),
+    fixed notation below 1e15 and exponent form (1e-05, 1e+15) outside
+    [1e-4, 1e15) -- Python's repr differs only in [1e15, 1e16)."""
+    def num(x: float) -> str:
+        if math.isnan(x) or math.isinf(x):
+            return "null"
+        if x == 0.0:
+            return "-0.0" if math.copysign(1.0, x) < 0 else "0.0"
+        # shortest round-trip digits (as nlohmann's grisu2 to_chars), value = digits * 10^k
+        sign = "-" if x < 0 else ""
+        mant, _, exp = ("%r" % abs(x)).partition("e")
+        ip, _, fp = mant.partition(".")
+        digits = (ip + fp).lstrip("0")
+        k = (int(exp) if exp else 0) - len(fp)
+        stripped = digits.rstrip("0")
+        k += len(digits) - len(stripped)
+        digits = stripped
+        n = k + len(digits)
+        if k >= 0 and n <= 15:
+            return sign + digits + "0" * k + ".0"
+        if 0 < n <= 15:
+            return sign + digits[:n] + "." + digits[n:]
+        if -4 < n <= 0:
+            return sign + "0." + "0" * (-n) + digits
+        e = n - 1
+        m = digits[0] + ("." + digits[1:] if len(digits) > 1 else "")
+        return sign + m + "e" + ("-" if e < 0 else "+") + "%02d" % abs(e)
+
+    def enc(o, ind):
+        pad, pad2 = "  " * ind, "  " * (ind + 1)
+        if isinstance(o, dict):
+            if not o:
+                return "{}"
+            return "{\n" + ",\n".join(f"{pad2}{json.dumps(k)}: {enc(v, ind + 1)}" for k, v in o.items()) + "\n" + pad + "}"
+        if isinstance(o, list):
+            if not o:
+                return "[]"
+            return "[\n" + ",\n".join(pad2 + enc(v, ind + 1) for v in o) + "\n" + pad + "]"
+        if isinstance(o, bool):
+            return "true" if o else "false"
+        if isinstance(o, int):
+            return str(o)
+        if isinstance(o, float):
+            return num(o)
+        if isinstance(o, str):
+            return json.dumps(o)
+        raise TypeError(type(o))
+    return enc(obj, 0) + "\n"
+
+
+def _percentile(values, p):
+    """metrics.cpp:12-19, nearest rank: sorted[ceil(p*n)-1]."""
+    v = sorted(values)
+    return v[math.ceil(p * len(v)) - 1]
+
+
+def compute_metrics(records, exp: Experiment, placement: Placement) -> dict:
+    """metrics.cpp:40-113 over the engine's records (any engine: priced,
+    lockstep or measured). Returns the report as plain values."""
+    if exp.horizon_s <= 0.0:
+        raise ConfigError("horizon must be positive")
+    scales = exp.slo_scales
+    total_rate = sum(e.rate for e in exp.entries)
+    overall_met, overall_total = [0] * len(scales), 0
+    report = {"aggregated_throughput_rps": 0.0, "llms": []}
+    for li, (name, e) in enumerate(zip(exp.names, exp.entries)):
+        if li not in placement.tp_degree:
+            raise ConfigError(f"plan does not place model '{name}'")  # commands.cpp:66-68
+        tp_ref = 1 if exp.slo_reference_tp_one else placement.tp_degree[li]
+        ttft, tpot, lat = [], [], []
+        met, total, completed = [0] * len(scales), 0, 0
+        for r in records:
+            if r.llm != li:
+                continue
+            total += 1
+            if r.done_s <= exp.horizon_s:
+                completed += 1
+            ttft.append(r.first_token_s - r.arrival_s)
+            if r.output_len > 1:
+                tpot.append((r.done_s - r.first_token_s) / float(r.output_len - 1))
+            e2e = r.done_s - r.arrival_s
+            lat.append(e2e / float(r.output_len))
+            ref_s = slo_reference_latency_ms(e.spec, exp.profile, tp_ref, r.prompt_len, r.output_len) / 1000.0
+            for si, sc in enumerate(scales):
+                if e2e <= sc * ref_s * (1.0 + 1e-9):
+                    met[si] += 1
+
+        def mean(v):
+            s = 0.0
+            for x in v:
+                s += x
+            return s / len(v) if v else 0.0
+
+        def p99(v):
+            return _percentile(v, 0.99) if v else 0.0
+        m = {"name": name, "rate": e.rate, "completed": completed, "throughput_rps": completed / exp.horizon_s,
+             "mean_ttft_s": mean(ttft), "p99_ttft_s": p99(ttft), "mean_tpot_s": mean(tpot), "p99_tpot_s": p99(tpot),
+             "mean_latency_s": mean(lat), "p99_latency_s": p99(lat),
+             "slo_attainment": [met[si] / total if total else 0.0 for si in range(len(scales))]}
+        for si in range(len(scales)):
+            overall_met[si] += met[si]
+        overall_total += total
+        weight = e.rate / total_rate if total_rate > 0.0 else 0.0
+        report["aggregated_throughput_rps"] += weight * m["throughput_rps"]
+        report["llms"].append(m)
+    report["overall_slo"] = [overall_met[si] / overall_total if overall_total else 0.0 for si in range(len(scales))]
+    return report
+
+
+def _max_resource_gap(units) -> float:
+    """metrics.cpp:115-124."""
+    rs = [m.resource_usage for u in units for m in u.llms if m.rate > 0.0]
+    gap = 0.0
+    for i in range(len(rs)):
+        for j in range(i + 1, len(rs)):
+            gap = max(gap, abs(rs[i] - rs[j]))
+    return gap
+
+
+def _unit_models(u, names):
+    return [{"name": names[m.llm], "rate_rps": m.rate, "avg_used_blocks": m.avg_used_blocks,
+             "final_quota_blocks": m.final_quota_blocks, "resource_usage": m.resource_usage} for m in u.llms]
+
+
+def metrics_json(report: dict, exp: Experiment, units) -> str:
+    """report_to_json (metrics.cpp:126-167)."""
+    j = {"horizon_s": exp.horizon_s, "aggregated_throughput_rps": report["aggregated_throughput_rps"],
+         "slo_scales": list(exp.slo_scales), "overall_slo_attainment": report["overall_slo"],
+         "max_resource_gap": _max_resource_gap(units),
+         "models": [{"name": m["name"], "rate_rps": m["rate"], "completed": m["completed"],
+                     "throughput_rps": m["throughput_rps"], "mean_ttft_s": m["mean_ttft_s"],
+                     "p99_ttft_s": m["p99_ttft_s"], "mean_tpot_s": m["mean_tpot_s"], "p99_tpot_s": m["p99_tpot_s"],
+                     "mean_latency_s": m["mean_latency_s"], "p99_latency_s": m["p99_latency_s"],
+                     "slo_attainment": m["slo_attainment"]} for m in report["llms"]],
+         "units": [{"unit": u.unit, "total_blocks": u.total_blocks, "models": _unit_models(u, exp.names)}
+                   for u in units]}
+    return _dump(j)
+
+
+def poolstats_json(units, names: list[str]) -> str:
+    """poolstats_json (commands.cpp:89-121)."""
+    j = {"units": [{"unit": u.unit, "total_blocks": u.total_blocks, "models": _unit_models(u, names),
+                    "samples": [{"t_s": t, "llm": names[li], "used_blocks": used, "quota_blocks": quota}
+                                for t, li, used, quota in u.samples]} for u in units]}
+    return _dump(j)

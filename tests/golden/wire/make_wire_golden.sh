@@ -10,5 +10,7 @@ for c in pair mesh; do
   rm -rf out_$c
   $MUX simulate -c cfg_$c.json -p plan_$c.json -t trace_$c.csv -o out_$c > /dev/null
   mv out_$c/records.csv records_$c.csv
+  mv out_$c/metrics.json metrics_$c.json
+  mv out_$c/poolstats.json poolstats_$c.json
   rm -rf out_$c
 done

@@ -390,9 +390,10 @@ def test_fused_qkv_epilogue_is_bit_identical_to_kv_append(tiny_unit):
 
 
 @pytest.mark.timeout(600)
-def test_muxsim_cli_lockstep_on_gpu_matches_reference_records(cuda, tmp_path):
+def test_muxsim_cli_lockstep_on_gpu_matches_reference_outputs(cuda, tmp_path):
     """The drop-in CLI with every job executed on the B200 (7B + 13B, lockstep
-    engine): records.csv byte-identical to the unmodified reference CLI's on
+    engine): records.csv / metrics.json / poolstats.json byte-identical to the
+    priced run (itself byte-identical to the unmodified reference CLI) on
     the same config / plan / trace (first 40 requests of the golden trace)."""
     from paper_2404_02015_b200 import muxsim_cli, wire
     g = os.path.join(GOLDEN, "wire")
@@ -404,8 +405,13 @@ def test_muxsim_cli_lockstep_on_gpu_matches_reference_records(cuda, tmp_path):
     args = ["-c", os.path.join(g, "cfg_pair.json"), "-p", os.path.join(g, "plan_pair.json"), "-t", str(trace)]
     assert muxsim_cli.main(args + ["-o", str(priced)]) == 0
     assert muxsim_cli.main(args + ["-o", str(gpu), "--engine", "lockstep"]) == 0
-    assert (gpu / "records.csv").read_bytes() == (priced / "records.csv").read_bytes()
+    for name in ("records.csv", "metrics.json", "poolstats.json"):  # C8: lockstep == priced, byte for byte
+        assert (gpu / name).read_bytes() == (priced / name).read_bytes(), name
     assert muxsim_cli.main(args + ["-o", str(tmp_path / "m"), "--engine", "measured"]) == 0
+    import json
+    mj = json.loads((tmp_path / "m" / "metrics.json").read_text())
+    assert list(mj) == list(json.loads((priced / "metrics.json").read_text()))
+    assert [m["name"] for m in mj["models"]] == ["chat-7b", "chat-13b"]
     exp = wire.load_config(os.path.join(g, "cfg_pair.json"))
     assert len((tmp_path / "m" / "records.csv").read_text().splitlines()) == 41
     assert exp.names == ["chat-7b", "chat-13b"]

@@ -1,7 +1,7 @@
 """Drop-in `muxsim simulate`: the reference's config /
-plan.json / trace.csv in, records.csv out, byte-identical to the unmodified
-reference CLI on the same inputs (goldens in tests/golden/wire, made by
-make_wire_golden.sh with oracle/_ref/muxsim)."""
+plan.json / trace.csv in, records.csv / metrics.json / poolstats.json out,
+byte-identical to the unmodified reference CLI on the same inputs (goldens in
+tests/golden/wire, made by make_wire_golden.sh with oracle/_ref/muxsim)."""
 import os
 
 import pytest
@@ -12,13 +12,29 @@ G = os.path.join(os.path.dirname(__file__), "golden", "wire")
 
 
 @pytest.mark.parametrize("case", ["pair", "mesh"])
-def test_priced_records_csv_byte_identical_to_reference(case, tmp_path):
+def test_priced_outputs_byte_identical_to_reference(case, tmp_path):
     out = tmp_path / "out"
     rc = simulate.main(["-c", os.path.join(G, f"cfg_{case}.json"), "-p", os.path.join(G, f"plan_{case}.json"),
                         "-t", os.path.join(G, f"trace_{case}.csv"), "-o", str(out)])
     assert rc == 0
-    with open(out / "records.csv", "rb") as f, open(os.path.join(G, f"records_{case}.csv"), "rb") as g:
-        assert f.read() == g.read()
+    for name, golden in (("records.csv", f"records_{case}.csv"), ("metrics.json", f"metrics_{case}.json"),
+                         ("poolstats.json", f"poolstats_{case}.json")):
+        with open(out / name, "rb") as f, open(os.path.join(G, golden), "rb") as g:
+            assert f.read() == g.read(), name
+
+
+def test_nlohmann_number_format():
+    # nlohmann::json dump: shortest round-trip digits, exponent form outside [1e-4, 1e15)
+    cases = {0.0: "0.0", 2.0: "2.0", 0.1: "0.1", 1e-4: "0.0001", 1e-5: "1e-05", 1e15: "1e+15",
+             1.5e15: "1.5e+15", 123456789.125: "123456789.125", -2.5e-7: "-2.5e-07", 1e22: "1e+22"}
+    for x, want in cases.items():
+        assert wire._dump(x) == want + "\n", x
+    assert wire._dump({"a": [], "b": [1, 2.0], "c": "x"}) == '{\n  "a": [],\n  "b": [\n    1,\n    2.0\n  ],\n  "c": "x"\n}\n'
+
+
+def test_percentile_nearest_rank():
+    assert wire._percentile([3.0, 1.0, 2.0], 0.99) == 3.0
+    assert wire._percentile(list(range(100)), 0.5) == 49
 
 
 def test_trace_round_trip(tmp_path):
