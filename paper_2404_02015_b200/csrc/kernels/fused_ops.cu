@@ -58,12 +58,20 @@ template <int kVec>
 __global__ void __launch_bounds__(kRowThreads) rmsnorm_rows_kernel(const float* resid, const float* norm_w,
                                                                    __nv_bfloat16* xn, int hidden, float eps) {
   __shared__ float scratch[32];
+  const int n4 = hidden / 4;
+  // The norm weights do not depend on the predecessor: fetch them before the
+  // dependency wait, so only the residual read sits on the critical path.
+  const float4* w = reinterpret_cast<const float4*>(norm_w);
+  float4 g[kVec];
+#pragma unroll
+  for (int k = 0; k < kVec; ++k) {
+    const int i = threadIdx.x + k * kRowThreads;
+    g[k] = i < n4 ? w[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   grid_dep_wait();
   grid_dep_launch();
   const int t = blockIdx.x;
   const float4* x = reinterpret_cast<const float4*>(resid + static_cast<int64_t>(t) * hidden);
-  const float4* w = reinterpret_cast<const float4*>(norm_w);
-  const int n4 = hidden / 4;
   float4 v[kVec];
   float ss = 0.f;
 #pragma unroll
@@ -77,11 +85,9 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_rows_kernel(const float* 
 #pragma unroll
   for (int k = 0; k < kVec; ++k) {
     const int i = threadIdx.x + k * kRowThreads;
-    if (i < n4) {
-      const float4 g = w[i];
-      y[i] = make_uint2(pack_bf16(v[k].x * inv * g.x, v[k].y * inv * g.y),
-                        pack_bf16(v[k].z * inv * g.z, v[k].w * inv * g.w));
-    }
+    if (i < n4)
+      y[i] = make_uint2(pack_bf16(v[k].x * inv * g[k].x, v[k].y * inv * g[k].y),
+                        pack_bf16(v[k].z * inv * g[k].z, v[k].w * inv * g[k].w));
   }
 }
 

@@ -108,8 +108,11 @@ __device__ __forceinline__ unsigned long long gtimer() {
   return t;
 }
 
+// 32-bit index math: the host guarantees iters * grid < 2^32 (plan()), and a
+// 64-bit division is a ~100-instruction call that sat on the producer's path
+// to its first weight load.
 __device__ __forceinline__ int64_t range_begin(int64_t iters, int c, int grid) {
-  return iters * c / grid;
+  return static_cast<int64_t>(static_cast<uint32_t>(iters) * static_cast<uint32_t>(c) / static_cast<uint32_t>(grid));
 }
 
 // The work of one CTA as a sequence of segments: (tile, k-block range); the
@@ -132,7 +135,7 @@ struct SegGen {
       lo = 0;
     } else {
       if (sk >= sk_end) return false;
-      const int64_t st = sk / r.kb;
+      const int64_t st = static_cast<uint32_t>(sk) / static_cast<uint32_t>(r.kb);
       lo = st * r.kb;
       kb0 = static_cast<int>(sk - lo);
       const int64_t e = min(sk_end, lo + r.kb);
@@ -142,14 +145,16 @@ struct SegGen {
       tile = static_cast<int64_t>(r.n_dp) * G + st;
     }
     if (r.group_m <= 0) {
-      m = static_cast<int>(tile % r.m_tiles);
-      nt = static_cast<int>(tile / r.m_tiles);
+      const uint32_t t32 = static_cast<uint32_t>(tile), mt = static_cast<uint32_t>(r.m_tiles);
+      nt = static_cast<int>(t32 / mt);
+      m = static_cast<int>(t32 - static_cast<uint32_t>(nt) * mt);
     } else {
       const int64_t per = static_cast<int64_t>(r.group_m) * r.n_tok_tiles;
-      const int64_t g = tile / per, in = tile - g * per;
+      const uint32_t g = static_cast<uint32_t>(tile) / static_cast<uint32_t>(per);
+      const uint32_t in = static_cast<uint32_t>(tile) - g * static_cast<uint32_t>(per);
       const int gm = min(r.group_m, r.m_tiles - static_cast<int>(g) * r.group_m);  // last group may be narrower
-      m = static_cast<int>(g) * r.group_m + static_cast<int>(in % gm);
-      nt = static_cast<int>(in / gm);
+      nt = static_cast<int>(in / static_cast<uint32_t>(gm));
+      m = static_cast<int>(g) * r.group_m + static_cast<int>(in - static_cast<uint32_t>(nt) * static_cast<uint32_t>(gm));
     }
     return true;
   }
@@ -774,6 +779,8 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   int grid = 0;
   size_t smem = 0;
   plan(a, r, grid, smem);
+  // device index math is 32-bit (range_begin): iters * (grid + 1) must fit
+  if (static_cast<uint64_t>(r.iters) * static_cast<uint64_t>(grid + 1) >= (1ull << 32)) return cudaErrorInvalidValue;
   if (a.next_w != nullptr && a.pf_stages > 0 && r.n_tok_tiles == 1) {
     // the next decode GEMM of the chain: same tokens, same partition
     GemmArgs na = a;
@@ -784,6 +791,7 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
     int ngrid = 0;
     size_t nsmem = 0;
     plan(na, nr, ngrid, nsmem);
+    if (static_cast<uint64_t>(nr.iters) * static_cast<uint64_t>(ngrid + 1) >= (1ull << 32)) return cudaErrorInvalidValue;
     r.next_w = static_cast<const uint8_t*>(a.next_w);
     r.next_grid = ngrid;
     r.next_iters = nr.sk_iters;
