@@ -75,11 +75,13 @@ decode_attention_kernel(const DecodeAttnArgs a) {
     fence_barrier_init();
   }
   __syncthreads();
-  grid_dep_wait();    // q / pool / tables come from the kernels before
-  grid_dep_launch();
 
   if (warp == kConsumerWarps) {
-    // ---------------- producer warp: resolve ids, then stream K/V blocks
+    // ---------------- producer warp: resolve ids, then stream K/V blocks.
+    // The tables, contexts and every row but the one holding this step's
+    // new token (written by the K2 launch just before) are fixed before the
+    // job: the ids and the first S stages of older rows are issued before
+    // the PDL dependency wait, overlapping the predecessor's tail.
     const int slot = a.slots[b];
     const int32_t* rl = a.rowlist + static_cast<int64_t>(slot) * a.max_rows;
     const int col = (a.layer * a.H + h) * 2;
@@ -89,22 +91,27 @@ decode_attention_kernel(const DecodeAttnArgs a) {
       sm.ids[i] = make_int2(__ldg(rec), __ldg(rec + 1));
     }
     __syncwarp();
-    if (lane == 0) {
-      const uint64_t pol = policy_evict_first();
-      const uint8_t* pool = reinterpret_cast<const uint8_t*>(a.pool);
-      for (int i = 0; i < n; ++i) {
-        const int s = i % S;
-        if (i >= S) mbar_wait(&sm.empty[s], ((i / S) - 1) & 1);
-        const int2 id = sm.ids[i];
-        mbar_arrive_expect_tx(&sm.full[s], 2 * kBlockBytes);
-        bulk_g2s_stream(sm.kv[s][0], pool + static_cast<int64_t>(id.x) * kBlockBytes, kBlockBytes,
-                        &sm.full[s], pol);
-        bulk_g2s_stream(sm.kv[s][1], pool + static_cast<int64_t>(id.y) * kBlockBytes, kBlockBytes,
-                        &sm.full[s], pol);
-      }
-    }
+    const int n_early = min(min(n, S), max(0, nrows_total - 1 - r0));
+    const uint64_t pol = policy_evict_first();
+    const uint8_t* pool = reinterpret_cast<const uint8_t*>(a.pool);
+    auto issue = [&](int i) {
+      const int s = i % S;
+      if (i >= S) mbar_wait(&sm.empty[s], ((i / S) - 1) & 1);
+      const int2 id = sm.ids[i];
+      mbar_arrive_expect_tx(&sm.full[s], 2 * kBlockBytes);
+      bulk_g2s_stream(sm.kv[s][0], pool + static_cast<int64_t>(id.x) * kBlockBytes, kBlockBytes, &sm.full[s], pol);
+      bulk_g2s_stream(sm.kv[s][1], pool + static_cast<int64_t>(id.y) * kBlockBytes, kBlockBytes, &sm.full[s], pol);
+    };
+    if (lane == 0)
+      for (int i = 0; i < n_early; ++i) issue(i);
+    grid_dep_wait();  // the new token's K/V (K2) and q
+    grid_dep_launch();
+    if (lane == 0)
+      for (int i = n_early; i < n; ++i) issue(i);
     return;
   }
+  grid_dep_wait();  // q comes from K2
+  grid_dep_launch();
 
   // ---------------- consumer warps
   const int half = lane >> 4;  // token parity handled by this half-warp

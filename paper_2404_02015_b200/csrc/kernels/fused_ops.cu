@@ -158,12 +158,36 @@ __global__ void __launch_bounds__(kRowThreads) argmax_kernel(const float* logits
   const float* row = logits + static_cast<int64_t>(blockIdx.x) * V;
   float best = -INFINITY;
   int bi = V;  // sentinel above any index; NaN logits never win
-  for (int i = threadIdx.x; i < V; i += blockDim.x) {
-    const float v = row[i];
+  auto take = [&](float v, int i) {
     if (v > best || (v == best && i < bi)) {
       best = v;
       bi = i;
     }
+  };
+  if ((V & 3) == 0 && (reinterpret_cast<uintptr_t>(row) & 15) == 0) {
+    // 128-bit loads, kUnroll of them in flight per thread (a scalar loop
+    // keeps one load in flight and is latency-bound: 63 us for 32000 logits)
+    constexpr int kUnroll = 8;
+    const float4* r4 = reinterpret_cast<const float4*>(row);
+    const int n4 = V >> 2;
+    for (int base = threadIdx.x; base < n4; base += kUnroll * kRowThreads) {
+      float4 v[kUnroll];
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int j = base + u * kRowThreads;
+        v[u] = j < n4 ? r4[j] : make_float4(-INFINITY, -INFINITY, -INFINITY, -INFINITY);
+      }
+#pragma unroll
+      for (int u = 0; u < kUnroll; ++u) {
+        const int i = 4 * (base + u * kRowThreads);
+        take(v[u].x, i);
+        take(v[u].y, i + 1);
+        take(v[u].z, i + 2);
+        take(v[u].w, i + 3);
+      }
+    }
+  } else {
+    for (int i = threadIdx.x; i < V; i += blockDim.x) take(row[i], i);
   }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) {

@@ -22,15 +22,33 @@ namespace {
 constexpr int kDim = 128;
 
 __global__ void __launch_bounds__(256) kv_append_kernel(const AppendArgs a) {
-  grid_dep_wait();
-  grid_dep_launch();
   const int warp_global = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   const int lane = threadIdx.x & 31;
-  if (warp_global >= a.T * a.H) return;
-  const int t = warp_global / a.H;
-  const int h = warp_global % a.H;
-  const int pos = a.tok_pos[t];
-  const int slot = a.tok_slot[t];
+  const bool active = warp_global < a.T * a.H;
+  // Everything but the QKV output is fixed before this job's kernels run
+  // (token positions / slots staged by the host, block tables by
+  // table_update, the RoPE table): resolve the destination blocks and this
+  // lane's (cos, sin) before the PDL dependency wait, so only the qkv read
+  // sits between the QKV GEMM and the K/V stores.
+  int t = 0, h = 0, pos = 0, kid = 0, vid = 0;
+  float4 cs8[2] = {};
+  if (active) {
+    t = warp_global / a.H;
+    h = warp_global - t * a.H;
+    pos = a.tok_pos[t];
+    const int slot = a.tok_slot[t];
+    const int rr = a.rowlist[static_cast<int64_t>(slot) * a.max_rows + (pos >> 4)];
+    const int32_t* rec = a.rowrec + static_cast<int64_t>(rr) * a.row_width + (a.layer * a.H + h) * 2;
+    kid = rec[0];
+    vid = rec[1];
+    const float4* cs = reinterpret_cast<const float4*>(a.rope + static_cast<int64_t>(min(pos, a.rope_positions - 1)) * 128);
+    const int f0 = (lane & 15) * 4;  // dims f0..f0+3 -> floats 2*f0 .. 2*f0+7
+    cs8[0] = cs[f0 / 2];
+    cs8[1] = cs[f0 / 2 + 1];
+  }
+  grid_dep_wait();
+  grid_dep_launch();
+  if (!active) return;
 
   const int64_t tok_base = static_cast<int64_t>(t) * 3 * a.H * kDim;
   const __nv_bfloat16* qkv = reinterpret_cast<const __nv_bfloat16*>(a.qkv);
@@ -40,9 +58,8 @@ __global__ void __launch_bounds__(256) kv_append_kernel(const AppendArgs a) {
   float q[4], k[4];
   unpack4(qv, q);
   unpack4(kv, k);
-  const float* cs = a.rope + static_cast<int64_t>(min(pos, a.rope_positions - 1)) * 128;
-  rope4(q, cs, lane);
-  rope4(k, cs, lane);
+  rope4_pre(q, cs8, lane);
+  rope4_pre(k, cs8, lane);
   const uint2 kr = pack4(k);
   if (a.q_out != nullptr) {
     __nv_bfloat16* qo = reinterpret_cast<__nv_bfloat16*>(a.q_out);
@@ -51,15 +68,8 @@ __global__ void __launch_bounds__(256) kv_append_kernel(const AppendArgs a) {
     __nv_bfloat16* qkv_w = const_cast<__nv_bfloat16*>(qkv);
     *reinterpret_cast<uint2*>(qkv_w + tok_base + (1 * a.H + h) * kDim + lane * 4) = kr;
   }
-
-  const int row = pos >> 4;
-  const int in_blk = pos & 15;
-  const int rr = a.rowlist[static_cast<int64_t>(slot) * a.max_rows + row];
-  const int32_t* rec = a.rowrec + static_cast<int64_t>(rr) * a.row_width + (a.layer * a.H + h) * 2;
-  const int kid = rec[0];
-  const int vid = rec[1];
   uint8_t* pool = reinterpret_cast<uint8_t*>(a.pool);
-  const int64_t off = static_cast<int64_t>(in_blk) * 256 + lane * 8;
+  const int64_t off = static_cast<int64_t>(pos & 15) * 256 + lane * 8;
   *reinterpret_cast<uint2*>(pool + static_cast<int64_t>(kid) * 4096 + off) = kr;
   *reinterpret_cast<uint2*>(pool + static_cast<int64_t>(vid) * 4096 + off) = vv;
 }

@@ -41,4 +41,22 @@ static __device__ __forceinline__ void rope4(float (&x)[4], const float* cs, int
   }
 }
 
+// Same rotation with this lane's (cos, sin) pairs already in registers:
+// cs8 = cs[2*f0 .. 2*f0+7], f0 = (lane & 15) * 4 (two 16-byte loads).
+static __device__ __forceinline__ void rope4_pre(float (&x)[4], const float4 (&cs8)[2], int lane) {
+  float other[4];
+#pragma unroll
+  for (int k = 0; k < 4; ++k) other[k] = __shfl_xor_sync(0xffffffffu, x[k], 16);
+  const float c[4] = {cs8[0].x, cs8[0].z, cs8[1].x, cs8[1].z};
+  const float s[4] = {cs8[0].y, cs8[0].w, cs8[1].y, cs8[1].w};
+#pragma unroll
+  for (int k = 0; k < 4; ++k) {
+    if (lane < 16) {
+      x[k] = __fsub_rn(__fmul_rn(x[k], c[k]), __fmul_rn(other[k], s[k]));
+    } else {
+      x[k] = __fadd_rn(__fmul_rn(x[k], c[k]), __fmul_rn(other[k], s[k]));
+    }
+  }
+}
+
 }  // namespace mux
