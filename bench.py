@@ -371,6 +371,7 @@ def main():
                          "frac": round(achieved / hbm, 4),
                          "traffic": (k1_traffic() or {}).get("dram_bytes"),
                          "traffic_note": (k1_traffic() or {}).get("capture"),
+                         "traffic_algorithmic_bytes": (k1_traffic() or {}).get("algorithmic_bytes"),
                          "kernel": "decode_attention_kernel (K1, per-launch CUDA events, timed alone on the whole GPU)",
                          "peak_source": peak_kind, "launches_timed": r["attn_n"],
                          "bytes_per_launch": round(r["attn_bytes"] / max(1, r["attn_n"]))},
