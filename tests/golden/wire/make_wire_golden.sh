@@ -5,8 +5,12 @@
 set -euo pipefail
 cd "$(dirname "$0")"
 MUX=../../../oracle/_ref/muxsim
-for c in pair mesh; do
-  $MUX gen-workload -c cfg_$c.json -o trace_$c.csv > /dev/null
+# b200prof: the pair config with the B200-measured LatencyProfile
+# (profiles/r01_b200_profile_7b.json); its plan comes from the reference's own planner.
+$MUX plan -c cfg_b200prof.json -o plan_b200prof.json > /dev/null
+cp trace_pair.csv trace_b200prof.csv
+for c in pair mesh b200prof; do
+  [ $c = b200prof ] || $MUX gen-workload -c cfg_$c.json -o trace_$c.csv > /dev/null
   rm -rf out_$c
   $MUX simulate -c cfg_$c.json -p plan_$c.json -t trace_$c.csv -o out_$c > /dev/null
   mv out_$c/records.csv records_$c.csv

@@ -11,7 +11,7 @@ from paper_2404_02015_b200 import muxsim_cli as simulate, wire
 G = os.path.join(os.path.dirname(__file__), "golden", "wire")
 
 
-@pytest.mark.parametrize("case", ["pair", "mesh"])
+@pytest.mark.parametrize("case", ["pair", "mesh", "b200prof"])
 def test_priced_outputs_byte_identical_to_reference(case, tmp_path):
     out = tmp_path / "out"
     rc = simulate.main(["-c", os.path.join(G, f"cfg_{case}.json"), "-p", os.path.join(G, f"plan_{case}.json"),
