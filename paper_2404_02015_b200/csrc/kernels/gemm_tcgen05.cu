@@ -208,7 +208,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x;
   const int G = gridDim.x;
-  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 32 + 0] = gtimer();
+  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 64 + 0] = gtimer();
 
   if (warp == 0 && lane == 0) {
     if (r.w_tiled == nullptr) prefetch_tmap(&tw);
@@ -234,7 +234,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 32 + 15] = gtimer();
+  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 64 + 15] = gtimer();
   if (threadIdx.x == 0) grid_dep_launch();
 
   if (warp == 0 || warp == 3) {
@@ -242,6 +242,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     // warp 0 streams the weight tiles, warp 3 the activation tiles.
     if (elect_one()) {
       const bool is_a = warp == 0;
+      if (is_a && r.timing != nullptr) r.timing[c * 64 + 32] = gtimer();
       // Weights do not depend on earlier kernels: warp 0 starts streaming
       // them while the predecessor drains (PDL); activations must wait.
       if (!is_a) grid_dep_wait();
@@ -254,11 +255,13 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       const uint32_t bytes = is_a ? kAStageBytes : b_stage_bytes;
       // Segments (tile, k-block range) with incremental stage counters: no
       // 64-bit division in the issue loop.
+      if (is_a && r.timing != nullptr) r.timing[c * 64 + 33] = gtimer();
       SegGen sg(r, c, G);
       int m, nt, kb0, kb1;
       bool skp;
       int64_t lo;
       int s = 0, round = 0;
+      if (is_a && r.timing != nullptr) r.timing[c * 64 + 34] = gtimer();
       int64_t issued = 0, pf_at = -1;
       if (is_a && r.next_w != nullptr && c < r.next_grid) {
         // start the prefetch when ~SA stages of this range remain
@@ -269,7 +272,9 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       while (sg.next(r, c, G, m, nt, kb0, kb1, skp, lo)) {
         for (int kbi = kb0; kbi < kb1; ++kbi) {
           if (round > 0) mbar_wait(&eb[s], (round - 1) & 1);
+          if (is_a && round == 0 && s == 0 && r.timing != nullptr) r.timing[c * 64 + 35] = gtimer();
           mbar_arrive_expect_tx(&fb[s], bytes);
+          if (is_a && round == 0 && s == 0 && r.timing != nullptr) r.timing[c * 64 + 36] = gtimer();
           if (is_a) {
             if (r.w_tiled != nullptr) {
               // one contiguous, pre-swizzled 16 KiB UMMA tile: a_split bulk copies
@@ -283,7 +288,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           } else {
             tma_load_2d(b_st + s * b_stage_bytes, &tx, &fb[s], kbi * kBK, nt * r.n_tile, pol);
           }
-          if (is_a && round == 0 && s == 0 && r.timing != nullptr) r.timing[c * 32 + 19] = gtimer();
+          if (is_a && round == 0 && s == 0 && r.timing != nullptr) r.timing[c * 64 + 19] = gtimer();
           if (issued++ == pf_at) {
             const int64_t b0 = range_begin(r.next_iters, c, r.next_grid);
             const int64_t b1 = min(range_begin(r.next_iters, c + 1, r.next_grid), b0 + r.pf_stages);
@@ -312,9 +317,9 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       const uint32_t acc = tmem + static_cast<uint32_t>(b * r.n_tile);
       for (int kbi = kb0; kbi < kb1; ++kbi, ++i) {
         mbar_wait(&full_a[sa], ra & 1);
-        if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 32 + 4] = gtimer();
+        if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 64 + 4] = gtimer();
         if (r.dbg_nomma < 2) mbar_wait(&full_b[sb], rb & 1);
-        if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 32 + 5] = gtimer();
+        if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 64 + 5] = gtimer();
         tc_fence_after();
         if (elect_one()) {
           const uint32_t a_addr = smem_u32(a_st + sa * kAStageBytes);
@@ -348,7 +353,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       }
       ++seg;
     }
-    if (r.timing != nullptr && lane == 0) r.timing[c * 32 + 1] = gtimer();
+    if (r.timing != nullptr && lane == 0) r.timing[c * 64 + 1] = gtimer();
   } else if (warp >= 4) {
     // ------------------------------------------------------ epilogue
     // Each chunk (32 tokens of the tile) goes TMEM -> registers -> a 16 KiB
@@ -389,7 +394,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         if (leader)
           for (int p = c + 1; p < p_hi; ++p)
             while (ld_acquire(r.flags + p) != r.epoch) __nanosleep(32);
-        if (leader && r.timing != nullptr) r.timing[c * 32 + 6] = gtimer();
+        if (leader && r.timing != nullptr) r.timing[c * 64 + 6] = gtimer();
       }
       const bool rope = first && r.epi == static_cast<int>(Epilogue::kQkvRope);
       const int part = m / max(1, r.qr.H), head = m % max(1, r.qr.H);  // kQkvRope: q/k/v and head of the tile
@@ -411,7 +416,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       }
       mbar_wait(&tm_full[b], (seg >> 1) & 1);
       tc_fence_after();
-      if (leader && r.timing != nullptr && seg < 4) r.timing[c * 32 + 9 + seg] = gtimer();
+      if (leader && r.timing != nullptr && seg < 4) r.timing[c * 64 + 9 + seg] = gtimer();
       if (n_part > 0) {
         // All MMAs of this CTA are complete, so the A ring is idle now.
         if (leader) {
@@ -424,7 +429,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         }
         mbar_wait(pbar, pphase);
         pphase ^= 1;
-        if (leader && r.timing != nullptr) r.timing[c * 32 + 7] = gtimer();
+        if (leader && r.timing != nullptr) r.timing[c * 64 + 7] = gtimer();
       }
       const uint32_t acc = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * r.n_tile);
       for (int k = 0; k < nchunk; ++k) {
@@ -432,7 +437,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         float v[32];
         tmem_ld_32x32b_x32(acc + cc, v);
         const bool stamp = leader && r.timing != nullptr && seg_last && k < 4;
-        if (stamp) r.timing[c * 32 + 20 + k] = gtimer();
+        if (stamp) r.timing[c * 64 + 20 + k] = gtimer();
         if (k == nchunk - 1) {  // accumulators consumed: hand TMEM back
           tc_fence_before();
           __syncwarp();
@@ -449,7 +454,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           else bulk_wait_read<0>();
         }
         epi_bar();
-        if (stamp) r.timing[c * 32 + 24 + k] = gtimer();
+        if (stamp) r.timing[c * 64 + 24 + k] = gtimer();
         uint8_t* st = stage_out + sbuf * kChunkBytes;
         const bool silu = first && r.epi == static_cast<int>(Epilogue::kSiluMulBf16);
         const bool fp32_rows = !first || residual || silu || r.epi == static_cast<int>(Epilogue::kStoreF32);
@@ -540,7 +545,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             for (int pr = 0; pr < r.n_peers; ++pr) tma_store_2d(&peers.m[pr], st, m * kBM, tok0 + cc);
           }
           bulk_commit();
-          if (stamp) r.timing[c * 32 + 28 + k] = gtimer();
+          if (stamp) r.timing[c * 64 + 28 + k] = gtimer();
         }
         if (r.n_stg == 2) sbuf ^= 1;
       }
@@ -550,9 +555,9 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
           st_release(r.flags + c, r.epoch);
         }
-        if (leader && r.timing != nullptr) r.timing[c * 32 + 8] = gtimer();
+        if (leader && r.timing != nullptr) r.timing[c * 64 + 8] = gtimer();
       }
-      if (leader && r.timing != nullptr && seg < 4) r.timing[c * 32 + 16 + seg] = gtimer();
+      if (leader && r.timing != nullptr && seg < 4) r.timing[c * 64 + 16 + seg] = gtimer();
       ++seg;
     }
     if (leader) bulk_wait<0>();  // staging smem must outlive its bulk reads
@@ -563,7 +568,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       for (int d = 0; d < r.n_signal; ++d)
         asm volatile("red.release.sys.global.add.s32 [%0], 1;" ::"l"(r.signal[d]) : "memory");
     }
-    if (r.timing != nullptr && threadIdx.x == 128) r.timing[c * 32 + 2] = gtimer();
+    if (r.timing != nullptr && threadIdx.x == 128) r.timing[c * 64 + 2] = gtimer();
   }
   // Reconverge the role warps (elected producer / MMA lanes) before the
   // block barrier: a diverged warp would arrive early and let warp 2 free
@@ -571,9 +576,9 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   __syncwarp();
   tc_fence_before();
   __syncthreads();
-  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 32 + 3] = gtimer();
-  if (r.timing != nullptr && threadIdx.x == 128) r.timing[c * 32 + 13] = gtimer();
-  if (r.timing != nullptr && threadIdx.x == 32) r.timing[c * 32 + 14] = gtimer();
+  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 64 + 3] = gtimer();
+  if (r.timing != nullptr && threadIdx.x == 128) r.timing[c * 64 + 13] = gtimer();
+  if (r.timing != nullptr && threadIdx.x == 32) r.timing[c * 64 + 14] = gtimer();
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, r.tmem_cols);

@@ -116,7 +116,7 @@ bool make_tmap_gemm_out(void* tmap_out, const void* out, int epi, int M, int N, 
 size_t weight_tiled_bytes(int N, int K);
 cudaError_t weight_tile(const void* src, int N, int K, void* dst, bool inverse, cudaStream_t stream);
 size_t gemm_partials_floats(int max_grid);
-void gemm_debug_timing(void* buf);  // [grid][4] u64 globaltimer stamps per CTA, null = off
+void gemm_debug_timing(void* buf);  // [grid][64] u64 globaltimer stamps per CTA, null = off
 // Encode a 2-D bf16 tensor map (rows x cols, cols contiguous) with a
 // box of box_rows x 64 and 128-byte swizzle. Returns false on failure.
 bool make_tmap_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t cols,

@@ -13,8 +13,8 @@ import paper_2404_02015_b200 as mux  # noqa: E402
 
 shapes = {"o13": (5120, 5120, 1), "qkv13": (15360, 5120, 0), "down13": (5120, 13824, 1), "gu13": (27648, 5120, 2)}
 M = int(sys.argv[1]) if len(sys.argv) > 1 else 128
-buf = torch.zeros(1024 * 32, dtype=torch.int64, device="cuda")
-names = {0: "start", 15: "synced", 19: "A0issued", 4: "A0", 5: "B0", 9: "seg0", 10: "seg1", 11: "seg2", 6: "fixflag", 7: "fixdata",
+buf = torch.zeros(1024 * 64, dtype=torch.int64, device="cuda")
+names = {0: "start", 15: "synced", 32: "elected", 33: "policy", 34: "seggen", 35: "preexp", 36: "expect", 19: "A0issued", 4: "A0", 5: "B0", 9: "seg0", 10: "seg1", 11: "seg2", 6: "fixflag", 7: "fixdata",
          8: "publish", 1: "mma_done", 2: "epi_done", 3: "exit", 13: "exit128", 14: "exit32",
          16: "end0", 17: "end1", 18: "end2"}
 for name, (N, K, epi) in shapes.items():
@@ -31,7 +31,7 @@ for name, (N, K, epi) in shapes.items():
     mux.gemm_bf16(x, w, out, epilogue=epi, grid=grid, w_tiled=wt)
     torch.cuda.synchronize()
     mux.lib.mux_debug_gemm_timing(None)
-    raw = buf.view(-1, 32)[:grid].cpu().double()
+    raw = buf.view(-1, 64)[:grid].cpu().double()
     t0 = raw[:, 0].min()
     t = (raw - t0) / 1e3  # us
     parts = []
