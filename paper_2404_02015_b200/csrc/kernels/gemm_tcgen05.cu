@@ -89,6 +89,7 @@ struct GemmRun {
   int a_split;      // bulk copies per weight stage (1, 2, 4)
   int n_stg;        // epilogue staging buffers (1 or 2)
   int dbg_nomma;    // debug (MUX_GEMM_NOMMA): stream operands without MMAs
+  int dbg_bres;     // debug (MUX_GEMM_BRES): load only the first SB activation stages, reuse them
   int n_peers;
   int n_signal;
   int* signal[kMaxTp];
@@ -271,6 +272,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       }
       while (sg.next(r, c, G, m, nt, kb0, kb1, skp, lo)) {
         for (int kbi = kb0; kbi < kb1; ++kbi) {
+          if (!is_a && r.dbg_bres && round > 0) break;  // debug: resident activations
           if (round > 0) mbar_wait(&eb[s], (round - 1) & 1);
           if (is_a && round == 0 && s == 0 && r.timing != nullptr) r.timing[c * 64 + 35] = gtimer();
           mbar_arrive_expect_tx(&fb[s], bytes);
@@ -318,7 +320,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       for (int kbi = kb0; kbi < kb1; ++kbi, ++i) {
         mbar_wait(&full_a[sa], ra & 1);
         if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 64 + 4] = gtimer();
-        if (r.dbg_nomma < 2) mbar_wait(&full_b[sb], rb & 1);
+        if (r.dbg_nomma < 2 && !(r.dbg_bres && rb > 0)) mbar_wait(&full_b[sb], rb & 1);
         if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 64 + 5] = gtimer();
         tc_fence_after();
         if (elect_one()) {
@@ -337,7 +339,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             if (kbi == kb1 - 1) mbar_arrive(&tm_full[b]);
           } else {
             umma_commit(&empty_a[sa]);
-            umma_commit(&empty_b[sb]);
+            if (!r.dbg_bres) umma_commit(&empty_b[sb]);
             if (kbi == kb1 - 1) umma_commit(&tm_full[b]);
           }
         }
@@ -725,6 +727,8 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   r.a_split = (env_split == 2 || env_split == 4 || env_split == 8) ? env_split : 1;
   static const int env_nomma = getenv("MUX_GEMM_NOMMA") ? atoi(getenv("MUX_GEMM_NOMMA")) : 0;
   r.dbg_nomma = env_nomma;
+  static const int env_bres = getenv("MUX_GEMM_BRES") ? atoi(getenv("MUX_GEMM_BRES")) : 0;
+  r.dbg_bres = env_bres;
   const int meta_bytes = a.epi == Epilogue::kQkvRope ? 2 * 256 * 4 : 0;  // token positions + block ids
   static const int env_stg = getenv("MUX_GEMM_STG") ? atoi(getenv("MUX_GEMM_STG")) : 2;
   static const int env_budget = getenv("MUX_GEMM_SMEM_KB") ? atoi(getenv("MUX_GEMM_SMEM_KB")) * 1024 : kSmemBudget;

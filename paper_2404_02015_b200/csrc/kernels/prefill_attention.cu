@@ -212,57 +212,59 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
       tc_fence_after();
       const uint32_t s_addr = tmem + lane_base + sb * kTile + hf * 64;
       const int kmax = min(qi, len - 1) - j * kTile - hf * 64;  // keys [0, kmax] of this half are visible
-      // pass 1: partial row max over this half, exchanged with the partner warp
+      // S read once (64 keys of this half into registers); the S buffer is
+      // handed back right away so Q K_{j+2}^T can start.
+      float v[64];
+      tmem_ld_32x32b_x32(s_addr, *reinterpret_cast<float(*)[32]>(v));
+      tmem_ld_32x32b_x32(s_addr + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+      tc_fence_before();
+      __syncwarp();
+      if (lane == 0) mbar_arrive(&bar.s_empty[sb]);
+      // partial row max over this half, exchanged with the partner warp
       float mx = -INFINITY;
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        float v[32];
-        tmem_ld_32x32b_x32(s_addr + c * 32, v);
-#pragma unroll
-        for (int i = 0; i < 32; ++i)
-          if (c * 32 + i <= kmax) mx = fmaxf(mx, v[i]);
-      }
+      for (int i = 0; i < 64; ++i)
+        if (i <= kmax) mx = fmaxf(mx, v[i]);
       bar.mx[j & 1][hf][row] = mx;
       asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
       mx = fmaxf(mx, bar.mx[j & 1][hf ^ 1][row]);
-      const float m_new = fmaxf(m_run, mx * a.scale_log2);
+      // Lazy rescaling: the running max only moves (and O is rescaled) when
+      // the tile's max exceeds it by more than 2^8; otherwise P = exp2(s - m)
+      // stays <= 256 under the stale max, and l / O share that max, so the
+      // final O / l is unchanged.
+      const float m_tile = mx * a.scale_log2;
+      const bool move = m_tile > m_run + 8.f;
+      const float m_new = move ? m_tile : m_run;
       const float m_use = m_new == -INFINITY ? 0.f : m_new;
-      const float alpha = exp2f(m_run - m_use);
+      const float alpha = move ? exp2f(m_run - m_use) : 1.f;
+      // P = exp2(s - m) -> packed bf16 in registers while P_{j-1} V_{j-1} runs
+      float psum = 0.f;
+      uint32_t pk[32];
+#pragma unroll
+      for (int i = 0; i < 64; i += 2) {
+        const float p0 = i <= kmax ? exp2f(fmaf(v[i], a.scale_log2, -m_use)) : 0.f;
+        const float p1 = i + 1 <= kmax ? exp2f(fmaf(v[i + 1], a.scale_log2, -m_use)) : 0.f;
+        psum += p0 + p1;
+        pk[i >> 1] = pack_bf16(p0, p1);
+      }
       if (j > 0) {
         // P_{j-1} V_{j-1} complete: the P buffer is free and O may be rescaled
         mbar_wait(&bar.o_full, (j - 1) & 1);
         tc_fence_after();
-        if (!__all_sync(0xffffffffu, alpha == 1.f)) {
-#pragma unroll 1
-          for (int c = 0; c < 2; ++c) {
-            float v[32];
-            tmem_ld_32x32b_x32(o_addr + c * 32, v);
-#pragma unroll
-            for (int i = 0; i < 32; ++i) v[i] *= alpha;
-            tmem_st_32x32b_x32(o_addr + c * 32, v);
-          }
-        }
       }
-      // pass 2: P = exp2(s - m) -> bf16 in the SW128 K-major image (this half's 64 keys)
-      float psum = 0.f;
+      // keys [64hf + 8chunk, +8) in the SW128 K-major image of this half's row
 #pragma unroll
-      for (int c = 0; c < 2; ++c) {
-        float v[32];
-        tmem_ld_32x32b_x32(s_addr + c * 32, v);
-        uint32_t pk[16];
+      for (int chunk = 0; chunk < 8; ++chunk)
+        *reinterpret_cast<uint4*>(p_row + ((chunk ^ (row & 7)) << 4)) =
+            make_uint4(pk[4 * chunk], pk[4 * chunk + 1], pk[4 * chunk + 2], pk[4 * chunk + 3]);
+      if (j > 0 && __any_sync(0xffffffffu, move)) {
+#pragma unroll 1
+        for (int c = 0; c < 2; ++c) {
+          float o[32];
+          tmem_ld_32x32b_x32(o_addr + c * 32, o);
 #pragma unroll
-        for (int i = 0; i < 32; i += 2) {
-          const float p0 = c * 32 + i <= kmax ? exp2f(fmaf(v[i], a.scale_log2, -m_use)) : 0.f;
-          const float p1 = c * 32 + i + 1 <= kmax ? exp2f(fmaf(v[i + 1], a.scale_log2, -m_use)) : 0.f;
-          psum += p0 + p1;
-          pk[i >> 1] = pack_bf16(p0, p1);
-        }
-        // keys [64hf + 32c, +32): 16-byte chunks c*4 .. +4 of this half's row
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-          const int chunk = c * 4 + u;
-          *reinterpret_cast<uint4*>(p_row + ((chunk ^ (row & 7)) << 4)) =
-              make_uint4(pk[4 * u], pk[4 * u + 1], pk[4 * u + 2], pk[4 * u + 3]);
+          for (int i = 0; i < 32; ++i) o[i] *= alpha;
+          tmem_st_32x32b_x32(o_addr + c * 32, o);
         }
       }
       l_run = l_run * alpha + psum;
@@ -270,10 +272,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
       tc_fence_before();
       fence_async_smem();  // P (generic writes) -> the tensor core (async proxy)
       __syncwarp();
-      if (lane == 0) {
-        mbar_arrive(&bar.s_empty[sb]);
-        mbar_arrive(&bar.p_full);
-      }
+      if (lane == 0) mbar_arrive(&bar.p_full);
     }
     bar.ls[hf][row] = l_run;
     asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
