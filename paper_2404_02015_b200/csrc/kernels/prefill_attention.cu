@@ -175,6 +175,11 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
       issue_qk(0);
       for (int j = 0; j < n_kv; ++j) {
         if (j + 1 < n_kv) issue_qk(j + 1);
+        // K_{j+2} goes into S_j's K slot as soon as S_j is done (issued one
+        // iteration ago): a full iteration ahead of Q K_{j+2}^T, instead of
+        // right before it (the MMA thread used to stall on that load before
+        // it could issue the next P V).
+        if (j + kStages < n_kv) load_k(j + kStages);
         if (j + 1 < n_kv && j + 1 >= kStages) load_v(j + 1);  // waits for P_{j-1} V_{j-1}
         // O_j = P_j V_j once the softmax has written P_j
         mbar_wait(&bar.p_full, j & 1);
@@ -189,7 +194,6 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         }
         umma_commit(&bar.o_full);
         umma_commit(&bar.v_empty[st]);
-        if (j + kStages < n_kv) load_k(j + kStages);  // S_j done long ago: no stall
       }
     }
     __syncwarp();
@@ -221,10 +225,18 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar.s_empty[sb]);
       // partial row max over this half, exchanged with the partner warp
+      // Tiles below the diagonal and inside the sequence need no masking:
+      // the fast path is 3-input max, paired FMA, bare MUFU.EX2, paired add.
+      const bool full = kmax >= 63;
       float mx = -INFINITY;
+      if (full) {
 #pragma unroll
-      for (int i = 0; i < 64; ++i)
-        if (i <= kmax) mx = fmaxf(mx, v[i]);
+        for (int i = 0; i < 64; i += 2) mx = fmax3(mx, v[i], v[i + 1]);
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; ++i)
+          if (i <= kmax) mx = fmaxf(mx, v[i]);
+      }
       bar.mx[j & 1][hf][row] = mx;
       asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
       mx = fmaxf(mx, bar.mx[j & 1][hf ^ 1][row]);
@@ -240,12 +252,25 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
       // P = exp2(s - m) -> packed bf16 in registers while P_{j-1} V_{j-1} runs
       float psum = 0.f;
       uint32_t pk[32];
+      if (full) {
+        float s0 = 0.f, s1 = 0.f;
 #pragma unroll
-      for (int i = 0; i < 64; i += 2) {
-        const float p0 = i <= kmax ? exp2f(fmaf(v[i], a.scale_log2, -m_use)) : 0.f;
-        const float p1 = i + 1 <= kmax ? exp2f(fmaf(v[i + 1], a.scale_log2, -m_use)) : 0.f;
-        psum += p0 + p1;
-        pk[i >> 1] = pack_bf16(p0, p1);
+        for (int i = 0; i < 64; i += 2) {
+          float x0, x1;
+          ffma2(x0, x1, v[i], v[i + 1], a.scale_log2, a.scale_log2, -m_use, -m_use);
+          const float p0 = ex2_ftz(x0), p1 = ex2_ftz(x1);
+          fadd2(s0, s1, p0, p1);
+          pk[i >> 1] = pack_bf16(p0, p1);
+        }
+        psum = s0 + s1;
+      } else {
+#pragma unroll
+        for (int i = 0; i < 64; i += 2) {
+          const float p0 = i <= kmax ? exp2f(fmaf(v[i], a.scale_log2, -m_use)) : 0.f;
+          const float p1 = i + 1 <= kmax ? exp2f(fmaf(v[i + 1], a.scale_log2, -m_use)) : 0.f;
+          psum += p0 + p1;
+          pk[i >> 1] = pack_bf16(p0, p1);
+        }
       }
       if (j > 0) {
         // P_{j-1} V_{j-1} complete: the P buffer is free and O may be rescaled
