@@ -221,6 +221,7 @@ struct mux_sim_stats {
 
 struct mux_unit {
   std::unique_ptr<mux_sim_stats> last_stats;  // of the last lockstep / measured run
+  bool prefill_on_partition = false;          // option: prefill jobs on their model's partition
   std::unique_ptr<mux::Runtime> rt;
   std::deque<muxsim::LLMSpec> specs;
   std::vector<std::unique_ptr<mux::Llama>> models;
@@ -307,7 +308,12 @@ class GpuExecutor : public muxsim::JobExecutor {
   void launch(const muxsim::JobLaunch& j) override {
     const muxsim::UnitState& st = *j.state;
     const int P = static_cast<int>(u_->streams.size());
-    const int part = j.kind == muxsim::JobKind::Prefill || P == 1 ? 0 : 1 + (j.llm % (P - 1));
+    // Decode jobs run on their model's partition. Prefill jobs run on the
+    // ungreened stream 0 (all SMs) unless prefill_on_partition is set: then
+    // every job of a model stays inside its green partition (stream 0's
+    // kernels may otherwise occupy the SMs of the other model's partition).
+    const bool own = j.kind != muxsim::JobKind::Prefill || u_->prefill_on_partition;
+    const int part = !own || P == 1 ? 0 : 1 + (j.llm % (P - 1));
     cudaStream_t s = u_->streams[part];
     mux::Llama& m = *u_->models[j.llm];
     mux::Workspace& ws = *u_->ws[part];
@@ -1095,6 +1101,7 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
     else if (k == "chain") u->rt->set_chain(value != 0);
     else if (k == "fuse_qkv") u->rt->set_fuse_qkv(value != 0);
     else if (k == "l2_next") u->rt->set_l2_next(static_cast<int>(value));
+    else if (k == "prefill_on_partition") u->prefill_on_partition = value != 0;
     else throw std::invalid_argument("unknown option: " + k);
   });
 }

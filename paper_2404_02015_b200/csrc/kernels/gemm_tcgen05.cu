@@ -562,7 +562,13 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       if (leader && r.timing != nullptr && seg < 4) r.timing[c * 64 + 16 + seg] = gtimer();
       ++seg;
     }
-    if (leader) bulk_wait<0>();  // staging smem must outlive its bulk reads
+    // Staging smem must outlive the bulk stores' reads of it; completion of
+    // the writes themselves is only needed before a signal to the TP peers
+    // (dependent kernels see them through grid completion).
+    if (leader) {
+      if (r.n_signal > 0) bulk_wait<0>();
+      else bulk_wait_read<0>();
+    }
     if (leader && r.n_signal > 0) {
       // every store of this CTA (local + peers) has completed: publish
       asm volatile("fence.proxy.async.global;" ::: "memory");

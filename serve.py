@@ -51,7 +51,7 @@ def make_trace(models, rates, horizon_s, seed, max_len=2048):
 
 
 def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, device=0, partition_sms=None,
-          scheduler="adbs", gpu_memory_gib=180.0, lengths=None):
+          scheduler="adbs", gpu_memory_gib=180.0, lengths=None, prefill_on_partition=False):
     """lengths: optional per-model (prompt, output) constants (contention runs)."""
     import paper_2404_02015_b200 as mux
     specs = [mux.spec(m, f"{m}.{i}") for i, m in enumerate(model_names)]  # distinct names per unit
@@ -72,6 +72,7 @@ def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, 
                     init_seed=1, init_std=0.02, partitions=len(specs) + 1,
                     partition_sms=partition_sms)
     try:
+        unit.set_option("prefill_on_partition", int(prefill_on_partition))
         unit.init_kv(seed=5, std=1.0)
         t0 = time.perf_counter()
         recs, _ = unit.run_lockstep(entries, trace, gpu_mem, params, measured=True)
@@ -94,7 +95,7 @@ def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, 
         "workload": {"models": list(model_names), "rates_rps": list(rates), "horizon_s": horizon_s, "seed": seed,
                      "lengths": "ShareGPT lognormal 161/338 sigma 0.8" if lengths is None else lengths,
                      "scheduler": scheduler, "gpu_memory_gib": gpu_memory_gib,
-                     "partition_sms": partition_sms},
+                     "partition_sms": partition_sms, "prefill_on_partition": prefill_on_partition},
         "host_wall_s": round(wall, 2),
     }
 
@@ -106,6 +107,8 @@ def main():
     ap.add_argument("--horizon", type=float, default=8.0)
     ap.add_argument("--seed", type=int, default=3)
     ap.add_argument("--partition-sms", type=lambda s: [int(x) for x in s.split(",")], default=None)
+    ap.add_argument("--prefill-on-partition", type=int, default=0,
+                    help="run each model's prefill jobs on its own green partition too")
     ap.add_argument("--scheduler", choices=["adbs", "fcfs", "rr"], default="adbs")
     ap.add_argument("--gpu-memory-gib", type=float, default=180.0)
     ap.add_argument("--lengths", default=None, help="per-model constant prompt:output, e.g. 128:384,64:64")
@@ -115,7 +118,8 @@ def main():
     psms = [0] + args.partition_sms if args.partition_sms else None
     lengths = None if args.lengths is None else [tuple(int(x) for x in m.split(":")) for m in args.lengths.split(",")]
     print(json.dumps(serve(models, rates, args.horizon, args.seed, partition_sms=psms, scheduler=args.scheduler,
-                           gpu_memory_gib=args.gpu_memory_gib, lengths=lengths)), flush=True)
+                           gpu_memory_gib=args.gpu_memory_gib, lengths=lengths,
+                           prefill_on_partition=bool(args.prefill_on_partition))), flush=True)
 
 
 if __name__ == "__main__":
