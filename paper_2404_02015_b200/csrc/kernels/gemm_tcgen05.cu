@@ -51,8 +51,9 @@ namespace {
 constexpr int kBM = 128;  // W rows per tile (UMMA M)
 constexpr int kBK = 64;   // K per stage (one 128-byte swizzle atom)
 constexpr int kAStageBytes = kBM * kBK * 2;
-constexpr int kThreads = 256;
-constexpr int kEpiThreads = 128;
+constexpr int kThreads = 384;               // warps 0-3 roles, warps 4-11 two epilogue groups
+constexpr int kEpiThreads = 128;            // one epilogue group: a warp per TMEM lane quarter
+constexpr int kEpiGroups = 2;
 constexpr int kChunkBytes = 32 * kBM * 4;  // one epilogue chunk: 32 tokens x 128 fp32
 constexpr int kSmemBudget = 224 * 1024;     // A ring + B ring + 2 staging chunks
 
@@ -175,8 +176,12 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-__device__ __forceinline__ void epi_bar() {
-  asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+// Named barriers: 1 + g for epilogue group g, 3 for both groups.
+__device__ __forceinline__ void epi_bar(int g) {
+  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kEpiThreads) : "memory");
+}
+__device__ __forceinline__ void epi_bar_all() {
+  asm volatile("bar.sync 3, %0;" ::"n"(kEpiGroups * kEpiThreads) : "memory");
 }
 
 __global__ void __launch_bounds__(kThreads, 1)
@@ -225,7 +230,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     }
     for (int b = 0; b < 2; ++b) {
       mbar_init(&tm_full[b], 1);
-      mbar_init(&tm_empty[b], kEpiThreads / 32);
+      mbar_init(&tm_empty[b], kEpiGroups * kEpiThreads / 32);
     }
     mbar_init(pbar, 1);
     fence_barrier_init();
@@ -360,19 +365,26 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     // ------------------------------------------------------ epilogue
     // Each chunk (32 tokens of the tile) goes TMEM -> registers -> a 16 KiB
     // shared staging buffer -> global by asynchronous bulk copies issued by
-    // one leader thread, so no thread ever waits on a global store.
+    // one leader thread, so no thread ever waits on a global store. Two
+    // groups of four warps (one warp per TMEM lane quarter each) take the
+    // even and odd chunks, each with its own staging buffer and leader: the
+    // epilogue of the last segment -- on the launch's critical path -- runs
+    // two chunks at a time.
     grid_dep_wait();  // partials / flags / out may still be in use by the predecessor
-    const int q = warp - 4;  // TMEM lane quarter this warp may access
-    const int etid = threadIdx.x - 128;
+    const int eg = (warp - 4) >> 2;  // epilogue group
+    const int q = warp & 3;          // TMEM lane quarter this warp may access (warp id % 4)
+    const int etid = (threadIdx.x - 128) & (kEpiThreads - 1);
     const int fl = q * 32 + lane;  // feature row of this thread inside the tile
     const bool leader = etid == 0;
+    const bool lead0 = leader && eg == 0;
     const bool residual = r.epi == static_cast<int>(Epilogue::kResidualAddF32);
-    int seg = 0, sbuf = 0;
+    int seg = 0;
     uint32_t pphase = 0;
     SegGen sg(r, c, G);
     int m, nt, kb0, kb1;
     bool skp;
     int64_t tile_lo;
+    uint8_t* st = stage_out + eg * kChunkBytes;  // this group's staging buffer
     while (sg.next(r, c, G, m, nt, kb0, kb1, skp, tile_lo)) {
       const int64_t tile_hi = tile_lo + r.kb;  // stream-K iterations of this tile (skp)
       const bool seg_last = !sg_has_more(sg, r);
@@ -393,16 +405,18 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         int p_hi = c + 1;
         while (p_hi < G && range_begin(r.sk_iters, p_hi, G) < tile_hi) ++p_hi;
         n_part = p_hi - (c + 1);
-        if (leader)
+        if (lead0)
           for (int p = c + 1; p < p_hi; ++p)
             while (ld_acquire(r.flags + p) != r.epoch) __nanosleep(32);
-        if (leader && r.timing != nullptr) r.timing[c * 64 + 6] = gtimer();
+        if (lead0 && r.timing != nullptr) r.timing[c * 64 + 6] = gtimer();
       }
       const bool rope = first && r.epi == static_cast<int>(Epilogue::kQkvRope);
       const int part = m / max(1, r.qr.H), head = m % max(1, r.qr.H);  // kQkvRope: q/k/v and head of the tile
       if (rope) {
         // token positions and K/V block ids of this tile's tokens, fetched
-        // while the MMAs still run (read after the staging barrier below)
+        // while the MMAs still run (read after the staging barrier below);
+        // both groups must have left the previous segment's tables first
+        epi_bar_all();
         for (int i = etid; i < r.n_tile; i += kEpiThreads) {
           const int tt = tok0 + i;
           if (tt < r.M) {
@@ -418,10 +432,15 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       }
       mbar_wait(&tm_full[b], (seg >> 1) & 1);
       tc_fence_after();
-      if (leader && r.timing != nullptr && seg < 4) r.timing[c * 64 + 9 + seg] = gtimer();
+      if (lead0 && r.timing != nullptr && seg < 4) r.timing[c * 64 + 9 + seg] = gtimer();
+      if (eg >= nchunk) {  // no chunk for this group (n_tile <= 32): hand TMEM back now
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&tm_empty[b]);
+      }
       if (n_part > 0) {
         // All MMAs of this CTA are complete, so the A ring is idle now.
-        if (leader) {
+        if (lead0) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
           mbar_arrive_expect_tx(pbar, static_cast<uint32_t>(n_part * nchunk * kChunkBytes));
           for (int pi = 0; pi < n_part; ++pi)
@@ -431,16 +450,16 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         }
         mbar_wait(pbar, pphase);
         pphase ^= 1;
-        if (leader && r.timing != nullptr) r.timing[c * 64 + 7] = gtimer();
+        if (lead0 && r.timing != nullptr) r.timing[c * 64 + 7] = gtimer();
       }
       const uint32_t acc = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * r.n_tile);
-      for (int k = 0; k < nchunk; ++k) {
+      for (int k = eg; k < nchunk; k += kEpiGroups) {
         const int cc = k * 32;
         float v[32];
         tmem_ld_32x32b_x32(acc + cc, v);
-        const bool stamp = leader && r.timing != nullptr && seg_last && k < 4;
+        const bool stamp = lead0 && r.timing != nullptr && seg_last && k < 4;
         if (stamp) r.timing[c * 64 + 20 + k] = gtimer();
-        if (k == nchunk - 1) {  // accumulators consumed: hand TMEM back
+        if (k + kEpiGroups >= nchunk) {  // this group's accumulators consumed: hand TMEM back
           tc_fence_before();
           __syncwarp();
           if (lane == 0) mbar_arrive(&tm_empty[b]);
@@ -451,13 +470,9 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           for (int j = 0; j < 32; ++j) v[j] += src[j * kBM];
         }
         // Staging buffer: wait until the bulk group that last read it is done.
-        if (leader) {
-          if (r.n_stg == 2) bulk_wait_read<1>();
-          else bulk_wait_read<0>();
-        }
-        epi_bar();
+        if (leader) bulk_wait_read<0>();
+        epi_bar(eg);
         if (stamp) r.timing[c * 64 + 24 + k] = gtimer();
-        uint8_t* st = stage_out + sbuf * kChunkBytes;
         const bool silu = first && r.epi == static_cast<int>(Epilogue::kSiluMulBf16);
         const bool fp32_rows = !first || residual || silu || r.epi == static_cast<int>(Epilogue::kStoreF32);
         if (fp32_rows) {
@@ -473,7 +488,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           // kSiluMulBf16: feature rows come in (gate_i, up_i) pairs. The fp32
           // chunk is staged first; each thread then turns 16 adjacent pairs of
           // one token into 16 bf16 act[token][i] (no shuffles, all ILP).
-          epi_bar();
+          epi_bar(eg);
           const float4* sf4 = reinterpret_cast<const float4*>(st) + (etid >> 2) * (kBM / 4) + (etid & 3) * 8;
           uint32_t packed[8];
 #pragma unroll
@@ -483,7 +498,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
             const float s1 = gu.z * rcp_approx(1.f + __expf(-gu.z));
             packed[q2] = pack_bf16(s0 * gu.y, s1 * gu.w);
           }
-          epi_bar();
+          epi_bar(eg);
           uint4* dst = reinterpret_cast<uint4*>(st + (etid >> 2) * kBM + (etid & 3) * 32);
           dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
           dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
@@ -492,7 +507,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           // K2 fused: thread = (token jj of the chunk, dims [d0, d0+16) and
           // their rotate_half partners d0+64..); the same _rn arithmetic as
           // kv_append, on the same bf16-rounded values.
-          epi_bar();
+          epi_bar(eg);
           const int jj = etid >> 2, d0 = (etid & 3) * 16;
           const int tt = tok0 + cc + jj;
           if (tt < r.M) {
@@ -533,7 +548,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           }
         }
         fence_async_smem();
-        epi_bar();
+        epi_bar(eg);
         if (leader) {
           if (!first) {
             // partner: publish the whole chunk (fixed slot of this CTA)
@@ -549,17 +564,17 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           bulk_commit();
           if (stamp) r.timing[c * 64 + 28 + k] = gtimer();
         }
-        if (r.n_stg == 2) sbuf ^= 1;
       }
-      if (!first && leader) {  // publish: partial bulk writes complete, then the flag
-        {
-          bulk_wait<0>();
+      if (!first) {  // publish: both groups' partial bulk writes complete, then the flag
+        if (leader) bulk_wait<0>();
+        epi_bar_all();
+        if (lead0) {
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
           st_release(r.flags + c, r.epoch);
+          if (r.timing != nullptr) r.timing[c * 64 + 8] = gtimer();
         }
-        if (leader && r.timing != nullptr) r.timing[c * 64 + 8] = gtimer();
       }
-      if (leader && r.timing != nullptr && seg < 4) r.timing[c * 64 + 16 + seg] = gtimer();
+      if (lead0 && r.timing != nullptr && seg < 4) r.timing[c * 64 + 16 + seg] = gtimer();
       ++seg;
     }
     // Staging smem must outlive the bulk stores' reads of it; completion of
@@ -569,7 +584,8 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       if (r.n_signal > 0) bulk_wait<0>();
       else bulk_wait_read<0>();
     }
-    if (leader && r.n_signal > 0) {
+    if (r.n_signal > 0) epi_bar_all();  // both groups' stores have landed
+    if (lead0 && r.n_signal > 0) {
       // every store of this CTA (local + peers) has completed: publish
       asm volatile("fence.proxy.async.global;" ::: "memory");
       asm volatile("fence.acq_rel.sys;" ::: "memory");
@@ -738,7 +754,8 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   const int meta_bytes = a.epi == Epilogue::kQkvRope ? 2 * 256 * 4 : 0;  // token positions + block ids
   static const int env_stg = getenv("MUX_GEMM_STG") ? atoi(getenv("MUX_GEMM_STG")) : 2;
   static const int env_budget = getenv("MUX_GEMM_SMEM_KB") ? atoi(getenv("MUX_GEMM_SMEM_KB")) * 1024 : kSmemBudget;
-  r.n_stg = env_stg == 1 ? 1 : 2;
+  r.n_stg = 2;  // one staging buffer per epilogue group
+  (void)env_stg;
   r.stages_a = (env_budget - meta_bytes - r.stages_b * b_stage - r.n_stg * kChunkBytes) / kAStageBytes;
   if (env_sa > 0) r.stages_a = std::min(env_sa, r.stages_a);
   else if (r.stages_a > 10) r.stages_a = 10;
