@@ -94,13 +94,18 @@ decode_attention_kernel(const DecodeAttnArgs a) {
     const int n_early = min(min(n, S), max(0, nrows_total - 1 - r0));
     const uint64_t pol = policy_evict_first();
     const uint8_t* pool = reinterpret_cast<const uint8_t*>(a.pool);
+    // The request's last row holds only ctx - 16*(rows-1) valid tokens: copy
+    // just those (256 B each); the consumers mask the rest by `valid` and
+    // skip their V rows, so the stale smem tail is never used.
+    const uint32_t last_bytes = static_cast<uint32_t>(ctx - (nrows_total - 1) * kBlockTok) * (kBlockBytes / kBlockTok);
     auto issue = [&](int i) {
       const int s = i % S;
       if (i >= S) mbar_wait(&sm.empty[s], ((i / S) - 1) & 1);
       const int2 id = sm.ids[i];
-      mbar_arrive_expect_tx(&sm.full[s], 2 * kBlockBytes);
-      bulk_g2s_stream(sm.kv[s][0], pool + static_cast<int64_t>(id.x) * kBlockBytes, kBlockBytes, &sm.full[s], pol);
-      bulk_g2s_stream(sm.kv[s][1], pool + static_cast<int64_t>(id.y) * kBlockBytes, kBlockBytes, &sm.full[s], pol);
+      const uint32_t bytes = r0 + i == nrows_total - 1 ? last_bytes : kBlockBytes;
+      mbar_arrive_expect_tx(&sm.full[s], 2 * bytes);
+      bulk_g2s_stream(sm.kv[s][0], pool + static_cast<int64_t>(id.x) * kBlockBytes, bytes, &sm.full[s], pol);
+      bulk_g2s_stream(sm.kv[s][1], pool + static_cast<int64_t>(id.y) * kBlockBytes, bytes, &sm.full[s], pol);
     };
     if (lane == 0)
       for (int i = 0; i < n_early; ++i) issue(i);
