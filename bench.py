@@ -368,7 +368,7 @@ def main():
                     "unit": "tokens/s", "h2d_bytes_per_step": int(per_step_tokens * 4),
                     "d2h_bytes_per_step": int(per_step_tokens * 4)},
             "roofline": {"bound": "hbm", "achieved": round(achieved, 1), "peak": hbm, "unit": "GB/s",
-                         "frac": round(achieved / hbm, 4),
+                         "frac": round(achieved / hbm, 4), "frac_nominal_8tbs": round(achieved / 8000.0, 4),
                          "traffic": (k1_traffic() or {}).get("dram_bytes"),
                          "traffic_note": (k1_traffic() or {}).get("capture"),
                          "traffic_algorithmic_bytes": (k1_traffic() or {}).get("algorithmic_bytes"),
@@ -376,7 +376,8 @@ def main():
                          "peak_source": peak_kind, "launches_timed": r["attn_n"],
                          "bytes_per_launch": round(r["attn_bytes"] / max(1, r["attn_n"]))},
             "step_roofline": {"tokens_per_s_at_peak": round(step_roof, 1) if step_roof else None,
-                              "frac": round(value / step_roof, 4) if step_roof else None},
+                              "frac": round(value / step_roof, 4) if step_roof else None,
+                              "frac_nominal_8tbs": round(value / (step_roof * 8000.0 / hbm), 4) if step_roof else None},
             "cpu_baseline": cpu,
             "serving": serving,
             "gpu_launches": r["launches"] * world,
