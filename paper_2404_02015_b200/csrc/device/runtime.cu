@@ -258,6 +258,8 @@ Workspace::Workspace(int max_tok, int max_batch_rows, int hidden, int qkv_cols, 
   const size_t kv_splits = 16;
   attn_part_o = DevMem(static_cast<size_t>(max_decode_batch) * heads * kv_splits * 128 * 4);
   attn_part_ml = DevMem(static_cast<size_t>(max_decode_batch) * heads * kv_splits * 2 * 4);
+  attn_split_count = DevMem(static_cast<size_t>(max_decode_batch) * heads * 4);
+  check_cuda(cudaMemset(attn_split_count.p, 0, attn_split_count.bytes), "memset split counters");
   // ints: tokens[T] slots[T] ctx[T] tok_slot[T] tok_pos[T] seq_start[T+1] out_tok[T] last_rows[T]
   const size_t n_ints = 8 * T + 8;
   ints = DevMem(n_ints * 4);
@@ -563,6 +565,7 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   at.out = ws.attn.p;
   at.part_o = ws.attn_part_o.as<float>();
   at.part_ml = ws.attn_part_ml.as<float>();
+  at.split_count = ws.attn_split_count.as<int>();  // the last split of each (member, head) merges
   at.B = n;
   at.H = H;
   at.max_rows = m.max_rows();
@@ -572,7 +575,8 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   const int max_rows_req = (max_ctx + 15) / 16;
   // KV splits: enough CTAs to fill the GPU a few times over.
   int splits = 1;
-  while (splits < 16 && n * H * splits < 4 * ws.sms && (max_rows_req + splits * 2 - 1) / (splits * 2) >= 4) splits *= 2;
+  // (the last split merges in-kernel, so small batches can afford ~2 rows per split)
+  while (splits < 16 && n * H * splits < 4 * ws.sms && (max_rows_req + splits * 2 - 1) / (splits * 2) >= 2) splits *= 2;
   while ((max_rows_req + splits - 1) / splits > decode_attention_max_rows_per_split()) splits *= 2;
   at.splits = splits;
   at.rows_per_split = std::max(1, (max_rows_req + splits - 1) / splits);
@@ -657,7 +661,7 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
         check_cuda(cudaEventRecord(e0, stream), "timer");
       }
       check_cuda(decode_attention(at, false, stream), "decode_attention");
-      launches_ += at.splits > 1 ? 2 : 1;
+      launches_ += 1;
       if (timer) {
         check_cuda(cudaEventRecord(e1, stream), "timer");
         timer->pending.emplace_back(e0, e1);
@@ -698,7 +702,7 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
       check_cuda(cudaEventRecord(e0, stream), "timer");
     }
     check_cuda(decode_attention(at, false, stream), "decode_attention");
-    launches_ += at.splits > 1 ? 2 : 1;
+    launches_ += 1;
     if (timer) {
       check_cuda(cudaEventRecord(e1, stream), "timer");
       timer->pending.emplace_back(e0, e1);

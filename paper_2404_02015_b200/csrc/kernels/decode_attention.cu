@@ -46,6 +46,7 @@ struct __align__(128) AttnSmem {
   float red_m[kConsumerWarps];
   float red_l[kConsumerWarps];
   float red_o[kConsumerWarps][kDim];
+  int last;  // this CTA is the last split of its (member, head) to finish
 };
 
 template <int S, typename OutT>
@@ -269,6 +270,37 @@ decode_attention_kernel(const DecodeAttnArgs a) {
       pml[0] = M;
       pml[1] = L;
     }
+    if (a.split_count != nullptr) {
+      // The last split of this (member, head) to finish merges all of them
+      // (threadfence-reduction pattern): no second launch on the critical path.
+      __threadfence();
+      asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+      if (d == 0) sm.last = atomicAdd(a.split_count + bh, 1) == a.splits - 1;
+      asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32) : "memory");
+      if (sm.last) {
+        __threadfence();
+        const float* pml = a.part_ml + bh * a.splits * 2;
+        float Mx = -INFINITY;
+        for (int s2 = 0; s2 < a.splits; ++s2)
+          if (__ldcg(pml + 2 * s2 + 1) > 0.f) Mx = fmaxf(Mx, __ldcg(pml + 2 * s2));
+        float Lt = 0.f, Ot = 0.f;
+        for (int s2 = 0; s2 < a.splits; ++s2) {
+          const float l = __ldcg(pml + 2 * s2 + 1);
+          if (l <= 0.f) continue;
+          const float f = exp2f(__ldcg(pml + 2 * s2) - Mx) * l;
+          Lt += f;
+          Ot = fmaf(__ldcg(a.part_o + (bh * a.splits + s2) * kDim + d), f, Ot);
+        }
+        const float val = Lt > 0.f ? Ot / Lt : 0.f;
+        OutT* out = reinterpret_cast<OutT*>(a.out);
+        if constexpr (sizeof(OutT) == 4) {
+          out[bh * kDim + d] = val;
+        } else {
+          out[bh * kDim + d] = __float2bfloat16_rn(val);
+        }
+        if (d == 0) a.split_count[bh] = 0;  // ready for the next launch
+      }
+    }
   }
 }
 
@@ -313,7 +345,7 @@ cudaError_t launch_decode(const DecodeAttnArgs& a, cudaStream_t stream) {
   }
   dim3 grid(a.splits, a.H, a.B);
   cudaError_t e = launch(decode_attention_kernel<S, OutT>, grid, dim3(kThreads), smem, stream, a);
-  if (e == cudaSuccess && a.splits > 1)
+  if (e == cudaSuccess && a.splits > 1 && a.split_count == nullptr)
     e = launch(decode_attention_combine<OutT>, dim3(a.B * a.H), dim3(128), 0, stream, a);
   return e;
 }

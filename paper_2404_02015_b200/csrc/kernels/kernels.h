@@ -19,6 +19,7 @@ struct DecodeAttnArgs {
   void* out;                // [B][H][128] bf16 or fp32
   float* part_o;            // [B][H][splits][128] (splits > 1)
   float* part_ml;           // [B][H][splits][2]   (splits > 1)
+  int* split_count;         // [B][H] zeroed: the last split CTA merges in-kernel (null: combine launch)
   int B, H, layer, max_rows, row_width;
   int splits, rows_per_split;
   float scale_log2;         // log2(e) / sqrt(128)
