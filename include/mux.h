@@ -81,6 +81,10 @@ MUX_API int mux_pool_admit(mux_pool* pool, int llm, int64_t request_id, int64_t 
 /* alloc (kv_manager.hpp:65). */
 MUX_API int mux_pool_alloc(mux_pool* pool, int llm, int64_t request_id, int64_t add_tokens,
                    int enforce_quota, int* result);
+/* The same alloc for n members of one decode round (one call instead of n):
+ * results[i] is the AllocResult code of rids[i]; identical to n calls. */
+MUX_API int mux_pool_alloc_n(mux_pool* pool, int llm, int n, const int64_t* request_ids, int64_t add_tokens,
+                             int enforce_quota, int* results);
 /* free_request (kv_manager.hpp:69). */
 MUX_API int mux_pool_free_request(mux_pool* pool, int llm, int64_t request_id);
 /* set_quota / quota / used / committed / request_tokens (kv_manager.hpp:71-79). */

@@ -103,6 +103,7 @@ _SIGS = {
     "mux_pool_register_llm": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int, C.c_int]),
     "mux_pool_admit": (C.c_int, [vp, C.c_int, i64, i64, i64, P(C.c_int)]),
     "mux_pool_alloc": (C.c_int, [vp, C.c_int, i64, i64, C.c_int, P(C.c_int)]),
+    "mux_pool_alloc_n": (C.c_int, [vp, C.c_int, C.c_int, P(i64), i64, C.c_int, P(C.c_int)]),
     "mux_pool_free_request": (C.c_int, [vp, C.c_int, i64]),
     "mux_pool_set_quota": (C.c_int, [vp, C.c_int, i64]),
     "mux_pool_llm_stats": (C.c_int, [vp, C.c_int, P(i64), P(i64), P(i64)]),

@@ -460,6 +460,13 @@ int mux_pool_alloc(mux_pool* pool, int llm, int64_t rid, int64_t add, int enforc
   return guarded([&] { *result = alloc_code(pool->bp->alloc(llm, rid, add, enforce != 0)); });
 }
 
+int mux_pool_alloc_n(mux_pool* pool, int llm, int n, const int64_t* rids, int64_t add, int enforce, int* results) {
+  return guarded([&] {
+    require(n >= 0 && (n == 0 || (rids != nullptr && results != nullptr)), "null argument");
+    for (int i = 0; i < n; ++i) results[i] = alloc_code(pool->bp->alloc(llm, rids[i], add, enforce != 0));
+  });
+}
+
 int mux_pool_free_request(mux_pool* pool, int llm, int64_t rid) {
   return guarded([&] { pool->bp->free_request(llm, rid); });
 }

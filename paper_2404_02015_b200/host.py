@@ -150,6 +150,15 @@ class BlockPool:
                                  C.byref(r)))
         return AllocResult(r.value == ALLOC_OK, _ERR[r.value])
 
+    def alloc_n(self, llm, request_ids, add_tokens, enforce_quota) -> list[AllocResult]:
+        """alloc() for every member of a decode round in one C call;
+        request_ids: a sequence of ints or a ctypes int64 array."""
+        ids = request_ids if isinstance(request_ids, C.Array) else (C.c_int64 * len(request_ids))(*request_ids)
+        n = len(ids)
+        res = (C.c_int * max(n, 1))()
+        check(lib.mux_pool_alloc_n(self._h, llm, n, ids, add_tokens, 1 if enforce_quota else 0, res))
+        return [AllocResult(r == ALLOC_OK, _ERR[r]) for r in res[:n]]
+
     def free_request(self, llm, request_id):
         check(lib.mux_pool_free_request(self._h, llm, request_id))
 
