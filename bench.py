@@ -180,6 +180,7 @@ def run_ours(args, rank, world, local_rank):
     unit.set_option("chain", args.chain)
     unit.set_option("fuse_qkv", args.fuse_qkv)
     unit.set_option("l2_next", args.l2_next)
+    unit.set_option("fuse_norm", args.fuse_norm)
     unit.init_kv(seed=7 + rank, std=1.0)
     pool = unit.pool
     ids = []
@@ -293,6 +294,8 @@ def main():
     ap.add_argument("--chain", type=int, default=0, help="fused persistent layer chain for decode (experimental)")
     ap.add_argument("--l2-next", type=int, default=0,
                     help="16 KiB weight tiles per CTA of the next decode GEMM prefetched into L2 (0 = off)")
+    ap.add_argument("--fuse-norm", type=int, default=0,
+                    help="RMSNorm fused into the residual GEMMs on green partitions (grid barrier)")
     ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch between job kernels")
     ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg (profiling runs)")
     args = ap.parse_args()

@@ -898,6 +898,7 @@ int mux_unit_create(const mux_unit_config* cfg, mux_unit** out) {
       u->ws.push_back(std::make_unique<mux::Workspace>(max_tok, std::max(u->max_batch, 256), hid, qkv, ffn, vocab,
                                                        heads, u->max_batch, u->rt->num_sms()));
       u->ws.back()->sms = sms;
+      u->ws.back()->exclusive = g != nullptr;
       if (tp > 1) {
         auto link = std::make_unique<mux::TpLink>();
         link->rank = tp_rank;
@@ -1109,6 +1110,7 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
     else if (k == "fuse_qkv") u->rt->set_fuse_qkv(value != 0);
     else if (k == "l2_next") u->rt->set_l2_next(static_cast<int>(value));
     else if (k == "prefill_on_partition") u->prefill_on_partition = value != 0;
+    else if (k == "fuse_norm") u->rt->set_fuse_norm(value != 0);
     else throw std::invalid_argument("unknown option: " + k);
   });
 }

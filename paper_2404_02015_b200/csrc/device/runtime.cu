@@ -259,6 +259,8 @@ Workspace::Workspace(int max_tok, int max_batch_rows, int hidden, int qkv_cols, 
   attn_part_o = DevMem(static_cast<size_t>(max_decode_batch) * heads * kv_splits * 128 * 4);
   attn_part_ml = DevMem(static_cast<size_t>(max_decode_batch) * heads * kv_splits * 2 * 4);
   attn_split_count = DevMem(static_cast<size_t>(max_decode_batch) * heads * 4);
+  norm_bar = DevMem(256);
+  check_cuda(cudaMemset(norm_bar.p, 0, norm_bar.bytes), "memset norm barrier");
   check_cuda(cudaMemset(attn_split_count.p, 0, attn_split_count.bytes), "memset split counters");
   // ints: tokens[T] slots[T] ctx[T] tok_slot[T] tok_pos[T] seq_start[T+1] out_tok[T] last_rows[T]
   const size_t n_ints = 8 * T + 8;
@@ -384,7 +386,8 @@ const void* Runtime::act_tmap(const void* base, int rows, int cols, int box_rows
 }
 
 void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void* out, int ldo, int epi,
-                   Workspace& ws, cudaStream_t stream, const QkvRopeArgs* qkv, const NextGemm* next) {
+                   Workspace& ws, cudaStream_t stream, const QkvRopeArgs* qkv, const NextGemm* next,
+                   const float* norm_w, float norm_eps) {
   // The X map is viewed over max(M, 256) rows: buffers are sized for it and
   // rows past M are never stored.
   const int rows = std::max(M, 256);
@@ -413,7 +416,17 @@ void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void
     g.next_epi = static_cast<Epilogue>(next->epi);
     g.pf_stages = l2_next_;
   }
+  int grid = 0;
+  if (norm_w != nullptr) {
+    g.norm_w = norm_w;
+    g.norm_out = ws.xn.p;
+    g.norm_bar = ws.norm_bar.as<unsigned>();
+    g.norm_base = ws.norm_base;
+    g.norm_eps = norm_eps;
+    g.grid_out = &grid;
+  }
   check_cuda(gemm_bf16_tn(g, stream), "gemm");
+  if (norm_w != nullptr) ws.norm_base += static_cast<unsigned>(grid);
   launches_ += 1;
 }
 
@@ -677,6 +690,10 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
       run(c);
     }
   }
+  // Debug (MUX_DEBUG_SKIP bitmask; outputs are garbage, timings are not): the
+  // marginal in-step cost of a kernel class. 1 = K2, 2 = RMSNorm, 4 = K1,
+  // 8 = RMSNorm over one row only (the launch boundary without the work).
+  static const int dbg_skip = getenv("MUX_DEBUG_SKIP") ? atoi(getenv("MUX_DEBUG_SKIP")) : 0;
   for (int l = 0; l < L && !(chain_enabled_ && d.tp_size == 1 && n <= 256); ++l) {
     ap.layer = l;
     // next GEMM on this stream after each projection (L2 prefetch targets)
@@ -691,8 +708,10 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
     } else {
       gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream, nullptr,
            &nx_o);
-      check_cuda(kv_append(ap, stream), "kv_append");
-      launches_ += 1;
+      if (!(dbg_skip & 1)) {
+        check_cuda(kv_append(ap, stream), "kv_append");
+        launches_ += 1;
+      }
     }
     at.layer = l;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -701,8 +720,10 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
       e1 = timer->get();
       check_cuda(cudaEventRecord(e0, stream), "timer");
     }
-    check_cuda(decode_attention(at, false, stream), "decode_attention");
-    launches_ += 1;
+    if (!(dbg_skip & 4)) {
+      check_cuda(decode_attention(at, false, stream), "decode_attention");
+      launches_ += 1;
+    }
     if (timer) {
       check_cuda(cudaEventRecord(e1, stream), "timer");
       timer->pending.emplace_back(e0, e1);
@@ -715,14 +736,25 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
       row_parallel_norm(m.wdown[l].p, ws.act.p, n, hid, d.ffn, 1, next_norm, d.norm_eps, ws, stream);
       continue;
     }
-    gemm(m.wo[l].p, ws.attn.p, n, hid, H * 128, ws.resid.p, hid, kEpiResidual, ws, stream, nullptr, &nx_gu);
-    check_cuda(rmsnorm_rows(ws.resid.as<float>(), m.ffn_norm[l].as<float>(), ws.xn.p, n, hid, d.norm_eps, stream),
-               "rmsnorm");
-    launches_ += 1;
+    // RMSNorm fused into the residual GEMMs when this stream owns its SMs
+    const bool fnorm = fuse_norm_ && ws.exclusive && n <= 256 && !(dbg_skip & 2);
+    gemm(m.wo[l].p, ws.attn.p, n, hid, H * 128, ws.resid.p, hid, kEpiResidual, ws, stream, nullptr, &nx_gu,
+         fnorm ? m.ffn_norm[l].as<float>() : nullptr, d.norm_eps);
+    if (!(dbg_skip & 2) && !fnorm) {
+      check_cuda(rmsnorm_rows(ws.resid.as<float>(), m.ffn_norm[l].as<float>(), ws.xn.p, (dbg_skip & 8) ? 1 : n, hid,
+                              d.norm_eps, stream, ws.sms),
+                 "rmsnorm");
+      launches_ += 1;
+    }
     gemm(m.wgu[l].p, ws.xn.p, n, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, ws, stream, nullptr, &nx_down);
-    gemm(m.wdown[l].p, ws.act.p, n, hid, d.ffn, ws.resid.p, hid, kEpiResidual, ws, stream, nullptr, &nx_qkv);
-    check_cuda(rmsnorm_rows(ws.resid.as<float>(), next_norm, ws.xn.p, n, hid, d.norm_eps, stream), "rmsnorm");
-    launches_ += 1;
+    gemm(m.wdown[l].p, ws.act.p, n, hid, d.ffn, ws.resid.p, hid, kEpiResidual, ws, stream, nullptr, &nx_qkv,
+         fnorm ? next_norm : nullptr, d.norm_eps);
+    if (!(dbg_skip & 2) && !fnorm) {
+      check_cuda(rmsnorm_rows(ws.resid.as<float>(), next_norm, ws.xn.p, (dbg_skip & 8) ? 1 : n, hid, d.norm_eps,
+                              stream, ws.sms),
+                 "rmsnorm");
+      launches_ += 1;
+    }
   }
   gemm(m.lm_head.p, ws.xn.p, n, d.vocab, hid, ws.logits.p, d.vocab, kEpiStoreF32, ws, stream);
   check_cuda(argmax_rows(ws.logits.as<float>(), n, d.vocab, ws.out_tok, stream), "argmax");

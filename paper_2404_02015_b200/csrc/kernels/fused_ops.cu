@@ -2,7 +2,9 @@
 // activations is needed anyway: embedding + RMSNorm, residual RMSNorm, row
 // argmax (greedy sampling), row gather, and deterministic weight
 // initialisation. All HBM-bound; one CTA per token row.
+#include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
@@ -53,41 +55,42 @@ __global__ void __launch_bounds__(kRowThreads) embed_rmsnorm_kernel(
   rmsnorm_row(x, norm_w, xn + static_cast<int64_t>(t) * hidden, hidden, eps, scratch);
 }
 
-// One CTA per row, float4 loads kept in registers between the two passes.
+// Rows strided over at most one CTA per SM of the partition, float4 loads
+// kept in registers between the two passes, norm weights read after the
+// reduction (L2-resident). Few registers (kVec = exact float4s per thread)
+// and no shared memory beyond the reduction scratch: the kernel's CTAs fit
+// beside a GEMM CTA (224 KB smem, 46 K registers), so they are resident
+// before the residual GEMM ends and the next GEMM's CTAs can start their
+// prologue and weight stream while the norm runs (PDL).
 template <int kVec>
 __global__ void __launch_bounds__(kRowThreads) rmsnorm_rows_kernel(const float* resid, const float* norm_w,
-                                                                   __nv_bfloat16* xn, int hidden, float eps) {
+                                                                   __nv_bfloat16* xn, int T, int hidden, float eps) {
   __shared__ float scratch[32];
-  const int n4 = hidden / 4;
-  // The norm weights do not depend on the predecessor: fetch them before the
-  // dependency wait, so only the residual read sits on the critical path.
-  const float4* w = reinterpret_cast<const float4*>(norm_w);
-  float4 g[kVec];
-#pragma unroll
-  for (int k = 0; k < kVec; ++k) {
-    const int i = threadIdx.x + k * kRowThreads;
-    g[k] = i < n4 ? w[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-  }
   grid_dep_wait();
   grid_dep_launch();
-  const int t = blockIdx.x;
-  const float4* x = reinterpret_cast<const float4*>(resid + static_cast<int64_t>(t) * hidden);
-  float4 v[kVec];
-  float ss = 0.f;
+  const int n4 = hidden / 4;
+  const float4* w = reinterpret_cast<const float4*>(norm_w);
+  for (int t = blockIdx.x; t < T; t += gridDim.x) {
+    const float4* x = reinterpret_cast<const float4*>(resid + static_cast<int64_t>(t) * hidden);
+    float4 v[kVec];
+    float ss = 0.f;
 #pragma unroll
-  for (int k = 0; k < kVec; ++k) {
-    const int i = threadIdx.x + k * kRowThreads;
-    v[k] = i < n4 ? x[i] : make_float4(0.f, 0.f, 0.f, 0.f);
-    ss = fmaf(v[k].x, v[k].x, fmaf(v[k].y, v[k].y, fmaf(v[k].z, v[k].z, fmaf(v[k].w, v[k].w, ss))));
-  }
-  const float inv = rsqrtf(block_sum(ss, scratch) / static_cast<float>(hidden) + eps);
-  uint2* y = reinterpret_cast<uint2*>(xn + static_cast<int64_t>(t) * hidden);
+    for (int k = 0; k < kVec; ++k) {
+      const int i = threadIdx.x + k * kRowThreads;
+      v[k] = i < n4 ? x[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+      ss = fmaf(v[k].x, v[k].x, fmaf(v[k].y, v[k].y, fmaf(v[k].z, v[k].z, fmaf(v[k].w, v[k].w, ss))));
+    }
+    const float inv = rsqrtf(block_sum(ss, scratch) / static_cast<float>(hidden) + eps);
+    uint2* y = reinterpret_cast<uint2*>(xn + static_cast<int64_t>(t) * hidden);
 #pragma unroll
-  for (int k = 0; k < kVec; ++k) {
-    const int i = threadIdx.x + k * kRowThreads;
-    if (i < n4)
-      y[i] = make_uint2(pack_bf16(v[k].x * inv * g[k].x, v[k].y * inv * g[k].y),
-                        pack_bf16(v[k].z * inv * g[k].z, v[k].w * inv * g[k].w));
+    for (int k = 0; k < kVec; ++k) {
+      const int i = threadIdx.x + k * kRowThreads;
+      if (i < n4) {
+        const float4 g = w[i];
+        y[i] = make_uint2(pack_bf16(v[k].x * inv * g.x, v[k].y * inv * g.y),
+                          pack_bf16(v[k].z * inv * g.z, v[k].w * inv * g.w));
+      }
+    }
   }
 }
 
@@ -251,7 +254,8 @@ __global__ void fill_kernel(float* dst, int64_t n, float v) {
 }  // namespace
 
 cudaError_t preload_fused_ops() {
-  return preload(embed_rmsnorm_kernel, rmsnorm_rows_kernel<2>, rmsnorm_rows_kernel<4>, rmsnorm_rows_kernel<8>,
+  return preload(embed_rmsnorm_kernel, rmsnorm_rows_kernel<2>, rmsnorm_rows_kernel<4>, rmsnorm_rows_kernel<5>,
+                 rmsnorm_rows_kernel<8>,
                  rmsnorm_rows_kernel<16>, rmsnorm_tp_kernel<2>, rmsnorm_tp_kernel<4>, rmsnorm_tp_kernel<8>,
                  rmsnorm_tp_kernel<16>, argmax_kernel, gather_rows_kernel, init_normal_kernel, fill_kernel);
 }
@@ -265,14 +269,17 @@ cudaError_t embed_rmsnorm(const void* emb, const int32_t* tokens, const float* n
 }
 
 cudaError_t rmsnorm_rows(const float* resid, const float* norm_w, void* xn, int T, int hidden, float eps,
-                         cudaStream_t stream) {
+                         cudaStream_t stream, int max_ctas) {
   if (T <= 0) return cudaSuccess;
   if (hidden % 4 != 0 || hidden > 4 * kRowThreads * 16) return cudaErrorInvalidValue;
   __nv_bfloat16* y = reinterpret_cast<__nv_bfloat16*>(xn);
   const int per = (hidden / 4 + kRowThreads - 1) / kRowThreads;
   auto k = per <= 2 ? rmsnorm_rows_kernel<2> : per <= 4 ? rmsnorm_rows_kernel<4>
-         : per <= 8 ? rmsnorm_rows_kernel<8> : rmsnorm_rows_kernel<16>;
-  return launch(k, dim3(T), dim3(kRowThreads), 0, stream, resid, norm_w, y, hidden, eps);
+         : per <= 5 ? rmsnorm_rows_kernel<5> : per <= 8 ? rmsnorm_rows_kernel<8> : rmsnorm_rows_kernel<16>;
+  static const int env_ctas = getenv("MUX_NORM_CTAS") ? atoi(getenv("MUX_NORM_CTAS")) : -1;  // debug override
+  if (env_ctas >= 0) max_ctas = env_ctas;
+  const int grid = max_ctas > 0 ? std::min(T, max_ctas) : T;
+  return launch(k, dim3(grid), dim3(kRowThreads), 0, stream, resid, norm_w, y, T, hidden, eps);
 }
 
 cudaError_t rmsnorm_tp(float* resid, const float* parts, int64_t part_stride, int tp, const int* counter,

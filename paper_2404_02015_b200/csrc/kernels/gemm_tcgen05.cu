@@ -102,6 +102,12 @@ struct GemmRun {
   int next_grid;
   int pf_stages;
   int64_t next_iters;
+  // fused RMSNorm of the residual rows (see GemmArgs::norm_w)
+  const float* norm_w;
+  __nv_bfloat16* norm_out;
+  unsigned* norm_bar;
+  unsigned norm_target;
+  float norm_eps;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -176,9 +182,12 @@ __device__ __forceinline__ void st_release(int* p, int v) {
   asm volatile("st.release.gpu.global.b32 [%0], %1;" ::"l"(p), "r"(v) : "memory");
 }
 
-// Named barriers: 1 + g for epilogue group g, 3 for both groups.
+// Named barriers: 1 + g for epilogue group g, 3 for both groups. Immediate
+// ids: a register id makes ptxas reserve all 16 barriers, and then no other
+// kernel's CTA (RMSNorm, K2 under PDL) can be co-resident with a GEMM CTA.
 __device__ __forceinline__ void epi_bar(int g) {
-  asm volatile("bar.sync %0, %1;" ::"r"(1 + g), "n"(kEpiThreads) : "memory");
+  if (g == 0) asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+  else asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
 }
 __device__ __forceinline__ void epi_bar_all() {
   asm volatile("bar.sync 3, %0;" ::"n"(kEpiGroups * kEpiThreads) : "memory");
@@ -209,6 +218,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pbar + 1);
   int* meta_pos = reinterpret_cast<int*>(tmem_slot + 4);  // kQkvRope: [256] token positions
   int* meta_id = meta_pos + 256;                          //            [256] K or V block ids
+  float* norm_red = reinterpret_cast<float*>(meta_pos);   // fused RMSNorm (never with kQkvRope): [8]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
@@ -585,6 +595,50 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       else bulk_wait_read<0>();
     }
     if (r.n_signal > 0) epi_bar_all();  // both groups' stores have landed
+    if (r.norm_w != nullptr) {
+      // Fused RMSNorm: wait until every CTA's reduce-adds into the residual
+      // have landed (grid barrier: all CTAs are co-resident on an exclusive
+      // partition), then normalise this CTA's share of the token rows.
+      if (leader) bulk_wait<0>();
+      epi_bar_all();
+      if (lead0) {
+        asm volatile("fence.acq_rel.gpu;" ::: "memory");
+        atomicAdd(r.norm_bar, 1u);
+        while (static_cast<int>(static_cast<unsigned>(ld_acquire(reinterpret_cast<const int*>(r.norm_bar))) -
+                                r.norm_target) < 0)
+          __nanosleep(64);
+      }
+      epi_bar_all();
+      const int nt4 = r.N / 4;  // float4s per row (N = hidden)
+      const int t0 = static_cast<int>(static_cast<int64_t>(r.M) * c / G);
+      const int t1 = static_cast<int>(static_cast<int64_t>(r.M) * (c + 1) / G);
+      const int et = threadIdx.x - 128;  // 0..255 over both groups
+      for (int t = t0; t < t1; ++t) {
+        const float4* x = reinterpret_cast<const float4*>(static_cast<const float*>(r.out) +
+                                                          static_cast<int64_t>(t) * r.ldo);
+        float ss = 0.f;
+        for (int i = et; i < nt4; i += kEpiGroups * kEpiThreads) {
+          const float4 v = __ldcg(x + i);
+          ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
+        if (lane == 0) norm_red[warp - 4] = ss;
+        epi_bar_all();
+        float tot = 0.f;
+#pragma unroll
+        for (int w = 0; w < kEpiGroups * kEpiThreads / 32; ++w) tot += norm_red[w];
+        const float inv = rsqrtf(tot / static_cast<float>(r.N) + r.norm_eps);
+        uint2* y = reinterpret_cast<uint2*>(r.norm_out + static_cast<int64_t>(t) * r.N);
+        const float4* g = reinterpret_cast<const float4*>(r.norm_w);
+        for (int i = et; i < nt4; i += kEpiGroups * kEpiThreads) {
+          const float4 v = __ldcg(x + i);
+          const float4 gw = g[i];
+          y[i] = make_uint2(pack_bf16(v.x * inv * gw.x, v.y * inv * gw.y), pack_bf16(v.z * inv * gw.z, v.w * inv * gw.w));
+        }
+        epi_bar_all();  // norm_red is reused by the next row
+      }
+    }
     if (lead0 && r.n_signal > 0) {
       // every store of this CTA (local + peers) has completed: publish
       asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -800,7 +854,7 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   }
   r.sk_iters = (tiles - static_cast<int64_t>(r.n_dp) * grid) * r.kb;
   smem_out = 1024 + static_cast<size_t>(r.stages_a) * kAStageBytes + static_cast<size_t>(r.stages_b) * b_stage +
-             r.n_stg * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16 + meta_bytes;
+             r.n_stg * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16 + std::max(meta_bytes, 64);
   grid_out = grid;
 }
 
@@ -828,6 +882,16 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
     r.next_grid = ngrid;
     r.next_iters = nr.sk_iters;
     r.pf_stages = a.pf_stages;
+  }
+  if (a.norm_w != nullptr) {
+    // decode residual GEMMs only: one token tile, the whole grid co-resident
+    if (a.epi != Epilogue::kResidualAddF32 || r.n_tok_tiles != 1 || a.norm_bar == nullptr || a.N % 4 != 0)
+      return cudaErrorInvalidValue;
+    r.norm_w = a.norm_w;
+    r.norm_out = static_cast<__nv_bfloat16*>(a.norm_out);
+    r.norm_bar = a.norm_bar;
+    r.norm_target = a.norm_base + static_cast<unsigned>(grid);
+    r.norm_eps = a.norm_eps;
   }
   static bool configured = false;
   if (!configured) {

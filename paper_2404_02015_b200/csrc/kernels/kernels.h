@@ -108,6 +108,17 @@ struct GemmArgs {
   int next_N = 0, next_K = 0;
   Epilogue next_epi = Epilogue::kStoreBf16;
   int pf_stages = 0;
+  // kResidualAddF32 decode only: after every CTA's reduce-adds have landed
+  // (grid barrier on norm_bar: count reaches norm_target), the CTAs normalise
+  // the residual rows (RMSNorm with norm_w, eps) into norm_out bf16 [M][N]:
+  // the RMSNorm launch between two GEMMs disappears. All CTAs of the grid
+  // must be co-resident with no other stream sharing their SMs (a green
+  // partition); norm_target is set from the launch grid (grid_out).
+  const float* norm_w = nullptr;
+  void* norm_out = nullptr;
+  unsigned* norm_bar = nullptr;
+  unsigned norm_base = 0;
+  float norm_eps = 1e-6f;
 };
 cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream);
 int gemm_pick_n_tile(int M);
@@ -165,7 +176,7 @@ cudaError_t embed_rmsnorm(const void* emb, const int32_t* tokens, const float* n
                           cudaStream_t stream);
 // xn[t] = bf16(resid[t] * rsqrt(mean(resid[t]^2) + eps) * w)
 cudaError_t rmsnorm_rows(const float* resid, const float* norm_w, void* xn, int T, int hidden, float eps,
-                         cudaStream_t stream);
+                         cudaStream_t stream, int max_ctas = 0);
 // Tensor-parallel residual update + RMSNorm: waits until *counter has reached
 // `expected` (every rank's row-parallel GEMM stored its partial here), then
 // resid[t] += parts[0][t] + ... + parts[tp-1][t] (rank order), xn = rmsnorm.

@@ -195,11 +195,15 @@ def test_green_partitions_are_disjoint_sm_sets(green_unit):
     assert len(set(unit.probe_smids(0, 4 * unit.partition_sms(0)))) > s1  # partition 0 spans the device
 
 
-def test_colocated_decode_on_green_partitions(green_unit):
+@pytest.mark.parametrize("fuse_norm", [0, 1])
+def test_colocated_decode_on_green_partitions(green_unit, fuse_norm):
     """Both models prefill and decode concurrently, each on its own SM
-    partition (spatial multiplexing, PAPER §4); tokens match the oracle."""
+    partition (spatial multiplexing, PAPER §4); tokens match the oracle.
+    fuse_norm=1: the RMSNorm runs inside the residual GEMMs after a grid
+    barrier (exclusive partitions only)."""
     unit, specs, refs = green_unit
-    rng = np.random.default_rng(11)
+    unit.set_option("fuse_norm", fuse_norm)
+    rng = np.random.default_rng(11 + fuse_norm)
     jobs = []
     for llm in (0, 1):
         rids = [70000 + 100 * llm + i for i in range(6)]
@@ -227,6 +231,7 @@ def test_colocated_decode_on_green_partitions(green_unit):
             check_tokens(refs[llm], prompts[i], gen[i])
         for rid in rids:
             unit.pool.free_request(llm, rid)
+    unit.set_option("fuse_norm", 0)
 
 
 def _pinned_i32(n):
