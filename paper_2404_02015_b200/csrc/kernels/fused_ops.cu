@@ -66,10 +66,17 @@ template <int kVec>
 __global__ void __launch_bounds__(kRowThreads) rmsnorm_rows_kernel(const float* resid, const float* norm_w,
                                                                    __nv_bfloat16* xn, int T, int hidden, float eps) {
   __shared__ float scratch[32];
+  const int n4 = hidden / 4;
+  // norm weights do not depend on the predecessor: in registers before the wait
+  const float4* w = reinterpret_cast<const float4*>(norm_w);
+  float4 g[kVec];
+#pragma unroll
+  for (int k = 0; k < kVec; ++k) {
+    const int i = threadIdx.x + k * kRowThreads;
+    g[k] = i < n4 ? w[i] : make_float4(0.f, 0.f, 0.f, 0.f);
+  }
   grid_dep_wait();
   grid_dep_launch();
-  const int n4 = hidden / 4;
-  const float4* w = reinterpret_cast<const float4*>(norm_w);
   for (int t = blockIdx.x; t < T; t += gridDim.x) {
     const float4* x = reinterpret_cast<const float4*>(resid + static_cast<int64_t>(t) * hidden);
     float4 v[kVec];
@@ -85,11 +92,9 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_rows_kernel(const float* 
 #pragma unroll
     for (int k = 0; k < kVec; ++k) {
       const int i = threadIdx.x + k * kRowThreads;
-      if (i < n4) {
-        const float4 g = w[i];
-        y[i] = make_uint2(pack_bf16(v[k].x * inv * g.x, v[k].y * inv * g.y),
-                          pack_bf16(v[k].z * inv * g.z, v[k].w * inv * g.w));
-      }
+      if (i < n4)
+        y[i] = make_uint2(pack_bf16(v[k].x * inv * g[k].x, v[k].y * inv * g[k].y),
+                          pack_bf16(v[k].z * inv * g[k].z, v[k].w * inv * g[k].w));
     }
   }
 }
