@@ -753,7 +753,7 @@ int mux_gemm_bf16(const void* x, const void* w, int w_tiled, int M, int N, int K
     }
     int sms = 148;
     cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
-    alignas(64) unsigned char tw[128], tx[128], to[128];
+    alignas(64) unsigned char tw[128], tx[128], to[128], tx128[128];
     const int n_tile = mux::gemm_pick_n_tile(M);
     if ((!w_tiled && !mux::make_tmap_bf16(tw, w, N, K, static_cast<uint64_t>(K) * 2, 128)) ||
         !mux::make_tmap_bf16(tx, x, M, K, static_cast<uint64_t>(K) * 2, n_tile))
@@ -765,6 +765,8 @@ int mux_gemm_bf16(const void* x, const void* w, int w_tiled, int M, int N, int K
     g.w_tiled = w_tiled ? w : nullptr;
     g.tmap_w = w_tiled ? nullptr : tw;
     g.tmap_x = tx;
+    // prefill shapes with tiled weights may run on CTA pairs (gemm_2sm.cu)
+    if (w_tiled && M > 256 && mux::make_tmap_bf16(tx128, x, M, K, static_cast<uint64_t>(K) * 2, 128)) g.tmap_x128 = tx128;
     g.out = out;
     g.partials = partials;
     g.flags = flags;

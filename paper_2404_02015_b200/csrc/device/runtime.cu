@@ -345,6 +345,7 @@ Runtime::Runtime(int device, int64_t pool_blocks, int max_pos)
   check_cuda(preload_decode_attention(), "preload");
   check_cuda(preload_kv_append(), "preload");
   check_cuda(preload_gemm(), "preload");
+  check_cuda(preload_gemm_2sm(), "preload");
   check_cuda(preload_prefill_attention(), "preload");
   check_cuda(preload_fused_ops(), "preload");
   check_cuda(preload_layer_chain(), "preload");
@@ -396,6 +397,7 @@ void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void
   GemmArgs g{};
   g.w_tiled = w_tiled;
   g.tmap_x = tx;
+  if (M > 256) g.tmap_x128 = act_tmap(x, rows, K, 128);  // 2-SM prefill path (gemm_2sm.cu)
   g.tmap_out = to;
   g.out = out;
   g.partials = ws.gemm_partials.as<float>();

@@ -860,6 +860,7 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
 
 cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   if (a.M <= 0 || a.N <= 0) return cudaSuccess;
+  if (gemm_2sm_eligible(a)) return gemm_2sm(a, stream);
   // tmap_x must have been encoded with box rows == gemm_pick_n_tile(M).
   GemmRun r{};
   int grid = 0;

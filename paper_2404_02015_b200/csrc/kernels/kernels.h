@@ -82,6 +82,7 @@ struct GemmArgs {
   const void* w_tiled;      // weights in weight_tile() layout (preferred), or null
   const void* tmap_w;       // else: CUtensorMap* over row-major W (host memory)
   const void* tmap_x;       // box rows must equal gemm_pick_n_tile(M)
+  const void* tmap_x128 = nullptr;  // same tensor, box 128 rows: enables the 2-SM prefill path (M > 256)
   const void* tmap_out;     // make_tmap_gemm_out(): box 32 tokens x 128 (SiLU: 64) features
   void* out;
   float* partials;          // stream-K fixup scratch: gemm_partials_floats(grid) floats
@@ -121,6 +122,12 @@ struct GemmArgs {
   float norm_eps = 1e-6f;
 };
 cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream);
+// Prefill GEMMs on CTA pairs (tcgen05 cta_group::2, gemm_2sm.cu); gemm_bf16_tn
+// dispatches there when gemm_2sm_eligible (M > 256, N % 256 == 0, plain
+// store / SiLU / residual / fp32 epilogue, tmap_x128 set; MUX_GEMM_2SM=0 off).
+bool gemm_2sm_eligible(const GemmArgs& a);
+cudaError_t gemm_2sm(const GemmArgs& a, cudaStream_t stream);
+cudaError_t preload_gemm_2sm();
 int gemm_pick_n_tile(int M);
 bool make_tmap_gemm_out(void* tmap_out, const void* out, int epi, int M, int N, int ldo);
 // B200 weight layout: [ceil(N/128)][ceil(K/64)] contiguous 16 KiB UMMA tiles,
@@ -131,6 +138,9 @@ size_t gemm_partials_floats(int max_grid);
 void gemm_debug_timing(void* buf);  // [grid][64] u64 globaltimer stamps per CTA, null = off
 // Encode a 2-D bf16 tensor map (rows x cols, cols contiguous) with a
 // box of box_rows x 64 and 128-byte swizzle. Returns false on failure.
+// Plain 2-D map (no swizzle), box box_rows x box_cols, bf16 or fp32.
+bool make_tmap_2d(void* tmap_out, const void* base, bool fp32, uint64_t rows, uint64_t cols,
+                  uint64_t row_stride_bytes, uint32_t box_rows, uint32_t box_cols);
 bool make_tmap_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t cols,
                     uint64_t row_stride_bytes, uint32_t box_rows);
 

@@ -196,6 +196,43 @@ def test_gemm_tiled_weights(cuda, M, N, K):
     assert torch.equal(a, b)
 
 
+@pytest.mark.parametrize("M,N,K", [(300, 512, 576), (1000, 1024, 1024), (4096, 512, 256), (257, 768, 320)])
+@pytest.mark.parametrize("epi", [0, 1, 2, 3])
+def test_gemm_prefill_cta_pairs(cuda, M, N, K, epi):
+    """Prefill shapes with tiled weights run on CTA pairs (tcgen05
+    cta_group::2, gemm_2sm.cu): every epilogue against an fp32 reference."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + N + K + epi)
+    x = torch.randn(M, K, generator=g, device="cuda").to(torch.bfloat16)
+    w = (torch.randn(N, K, generator=g, device="cuda") * 0.05).to(torch.bfloat16)
+    wt = mux.weight_tile(w)
+    ref = x.float() @ w.float().T
+    scale = ref.abs().max().item()
+    if epi == 0:
+        out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        mux.gemm_bf16(x, w, out, epilogue=0, w_tiled=wt)
+        torch.cuda.synchronize()
+        assert (out.float() - ref).abs().max().item() <= 1e-2 * scale
+    elif epi == 1:
+        resid0 = torch.randn(M, N, generator=g, device="cuda")
+        out = resid0.clone()
+        mux.gemm_bf16(x, w, out, epilogue=1, w_tiled=wt)
+        torch.cuda.synchronize()
+        assert (out - (resid0 + ref)).abs().max().item() <= 1e-4 * scale + 1e-5
+    elif epi == 2:
+        out = torch.empty(M, N // 2, dtype=torch.bfloat16, device="cuda")
+        mux.gemm_bf16(x, w, out, epilogue=2, w_tiled=wt)
+        torch.cuda.synchronize()
+        gate, up = ref[:, 0::2], ref[:, 1::2]
+        want = gate * torch.sigmoid(gate) * up
+        assert (out.float() - want).abs().max().item() <= 2e-2 * want.abs().max().item() + 1e-3
+    else:
+        out = torch.empty(M, N, dtype=torch.float32, device="cuda")
+        mux.gemm_bf16(x, w, out, epilogue=3, w_tiled=wt)
+        torch.cuda.synchronize()
+        assert (out - ref).abs().max().item() <= 1e-4 * scale + 1e-6
+
+
 def test_gemm_deterministic(cuda):
     import torch
     g = torch.Generator(device="cuda").manual_seed(9)
