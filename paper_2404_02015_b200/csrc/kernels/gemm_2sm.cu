@@ -281,7 +281,14 @@ gemm_2sm_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ 
 
 bool gemm_2sm_eligible(const GemmArgs& a) {
   static const int env = getenv("MUX_GEMM_2SM") ? atoi(getenv("MUX_GEMM_2SM")) : 1;
-  return env != 0 && a.tmap_x128 != nullptr && a.w_tiled != nullptr && a.M > 256 && a.N % 256 == 0 &&
+  if (a.N % 256 != 0 || a.M <= 256) return false;
+  // Data-parallel pair tiles: when the last round would leave most pairs idle
+  // (e.g. 80 tiles on 74 pairs), the single-SM stream-K path balances better.
+  const int tiles = (a.N / 256) * ((a.M + kBN - 1) / kBN);
+  const int pairs = std::max(1, std::min(tiles, (a.grid > 0 ? a.grid : 148) / 2));
+  const int rounds = (tiles + pairs - 1) / pairs;
+  if (10 * tiles < 7 * rounds * pairs) return false;
+  return env != 0 && a.tmap_x128 != nullptr && a.w_tiled != nullptr &&
          a.K % 64 == 0 && a.n_peers == 0 && a.n_signal == 0 && a.norm_w == nullptr &&
          (a.epi == Epilogue::kStoreBf16 || a.epi == Epilogue::kSiluMulBf16 || a.epi == Epilogue::kResidualAddF32 ||
           a.epi == Epilogue::kStoreF32) &&
