@@ -88,8 +88,10 @@ def run(B, H, long_ctx=None, sets=4, iters=20, seed=0):
 
     # KV splits as the runtime picks them (device/runtime.cu decode): enough
     # CTAs to fill the GPU a few times over
+    fill = int(os.environ.get("K1_FILL", "4"))  # CTAs per SM the split heuristic aims for
+    min_rows = int(os.environ.get("K1_MIN_ROWS", "2"))
     splits = 1
-    while splits < 16 and B * H * splits < 4 * 148 and (max_rows + splits * 2 - 1) // (splits * 2) >= 4:
+    while splits < 16 and B * H * splits < fill * 148 and (max_rows + splits * 2 - 1) // (splits * 2) >= min_rows:
         splits *= 2
 
     def launch(i):
@@ -116,8 +118,9 @@ if __name__ == "__main__":
     except Exception:
         peak = 6650.0
     print(f"K1 one layer, CUDA events; peak {peak:.0f} GB/s measured, 8000 nominal")
+    Bs = [int(x) for x in os.environ.get("K1_BATCHES", "1,4,16,64,128,196").split(",")]
     for H, name in ((32, "7B"), (40, "13B")):
-        for B in (1, 4, 16, 64, 128, 196):
+        for B in Bs:
             us, gbs, mean_ctx = run(B, H)
             print(f"{name} H={H} B={B:3d} mean ctx {mean_ctx:6.0f}: {us:8.1f} us {gbs:7.0f} GB/s "
                   f"{gbs / peak:6.1%} of measured {gbs / 8000:6.1%} of nominal", flush=True)
