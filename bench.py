@@ -224,7 +224,8 @@ def run_ours(args, rank, world, local_rank):
         unit.record(1 + li, 2 * li + 1)
     unit.sync()
     # span from the first partition's start to the last partition's end
-    ms = max(unit.elapsed_ms(0, 2 * li + 1) for li in range(len(specs)))
+    part_ms = [unit.elapsed_ms(0, 2 * li + 1) for li in range(len(specs))]
+    ms = max(part_ms)
     launches = unit.launches() - launches0
     clk = clocks.stop()
 
@@ -270,6 +271,7 @@ def run_ours(args, rank, world, local_rank):
         "attn_ms": attn_ms, "attn_n": attn_n, "attn_bytes": attn_bytes, "clocks": clk,
         "e2e_ms": e2e_ms, "bytes_step": bytes_step,
         "partition_sms": [unit_sms[li] for li in range(len(specs))] if psms else None,
+        "job_ms_per_step": [round(x / args.steps, 3) for x in part_ms],
     }
     return result
 
@@ -364,6 +366,7 @@ def main():
                 "l2": "inputs larger than L2 (39.5 GB weights + KV per step)",
                 "parallelism": f"{world} independent units (dp{world})",
                 "partition_sms": r["partition_sms"],
+                "job_ms_per_step": r["job_ms_per_step"],
             },
             "e2e": {"value": round(per_step_tokens / (e2e_ms / 1e3), 1) if e2e_ms else None,
                     "unit": "tokens/s", "h2d_bytes_per_step": int(per_step_tokens * 4),
