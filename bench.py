@@ -181,6 +181,7 @@ def run_ours(args, rank, world, local_rank):
     unit.set_option("fuse_qkv", args.fuse_qkv)
     unit.set_option("l2_next", args.l2_next)
     unit.set_option("fuse_norm", args.fuse_norm)
+    unit.set_option("fuse_k2", args.fuse_k2)
     unit.init_kv(seed=7 + rank, std=1.0)
     pool = unit.pool
     ids = []
@@ -296,6 +297,8 @@ def main():
     ap.add_argument("--chain", type=int, default=0, help="fused persistent layer chain for decode (experimental)")
     ap.add_argument("--l2-next", type=int, default=0,
                     help="16 KiB weight tiles per CTA of the next decode GEMM prefetched into L2 (0 = off)")
+    ap.add_argument("--fuse-k2", type=int, default=0,
+                    help="decode: RoPE + KV append inside the paged-attention kernel (no kv_append launch)")
     ap.add_argument("--fuse-norm", type=int, default=0,
                     help="RMSNorm fused into the residual GEMMs on green partitions (grid barrier)")
     ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch between job kernels")

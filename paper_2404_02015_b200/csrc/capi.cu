@@ -1113,6 +1113,7 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
     else if (k == "l2_next") u->rt->set_l2_next(static_cast<int>(value));
     else if (k == "prefill_on_partition") u->prefill_on_partition = value != 0;
     else if (k == "fuse_norm") u->rt->set_fuse_norm(value != 0);
+    else if (k == "fuse_k2") u->rt->set_fuse_k2(value != 0);
     else throw std::invalid_argument("unknown option: " + k);
   });
 }

@@ -581,6 +581,13 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   at.part_o = ws.attn_part_o.as<float>();
   at.part_ml = ws.attn_part_ml.as<float>();
   at.split_count = ws.attn_split_count.as<int>();  // the last split of each (member, head) merges
+  if (fuse_k2_ && !fuse_qkv_ && !(chain_enabled_ && d.tp_size == 1 && n <= 256)) {
+    // K2 inside K1: q / k / v straight from the QKV output (no kv_append launch)
+    at.qkv = ws.qkv.p;
+    at.pool_w = pool_.p;
+    at.rope = rope_.as<float>();
+    at.rope_positions = max_pos_;
+  }
   at.B = n;
   at.H = H;
   at.max_rows = m.max_rows();
@@ -710,7 +717,7 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
     } else {
       gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream, nullptr,
            &nx_o);
-      if (!(dbg_skip & 1)) {
+      if (!(dbg_skip & 1) && !fuse_k2_) {
         check_cuda(kv_append(ap, stream), "kv_append");
         launches_ += 1;
       }

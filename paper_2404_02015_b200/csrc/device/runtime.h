@@ -186,6 +186,7 @@ class Runtime {
   void set_fuse_qkv(bool on) { fuse_qkv_ = on; }
   void set_l2_next(int stages) { l2_next_ = stages; }
   void set_fuse_norm(bool on) { fuse_norm_ = on; }
+  void set_fuse_k2(bool on) { fuse_k2_ = on; }
   void count_launch(int64_t n = 1) { launches_ += n; }
 
   // Cached tensor map for an activation buffer viewed as rows x cols bf16.
@@ -232,6 +233,7 @@ class Runtime {
   bool chain_enabled_ = false;
   bool fuse_qkv_ = false;  // K2 in the QKV GEMM epilogue (kQkvRope): measured slower than kv_append
   int l2_next_ = 0;        // tiles per CTA of the next decode GEMM prefetched into L2 (0 = off)
+  bool fuse_k2_ = false;   // decode: RoPE + KV append inside K1 (no kv_append launch; measured no gain)
   bool fuse_norm_ = false;  // RMSNorm fused into the residual GEMMs on exclusive partitions (measured: no gain)
   DevMem pool_;
   DevMem rope_;

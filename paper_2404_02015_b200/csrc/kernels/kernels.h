@@ -20,6 +20,15 @@ struct DecodeAttnArgs {
   float* part_o;            // [B][H][splits][128] (splits > 1)
   float* part_ml;           // [B][H][splits][2]   (splits > 1)
   int* split_count;         // [B][H] zeroed: the last split CTA merges in-kernel (null: combine launch)
+  // Decode with K2 fused (qkv != null): q, k, v of the step's token come
+  // straight from the QKV GEMM output [B][3][H][128] (not rotated); every
+  // CTA rotates q itself (RoPE at position ctx-1, the _rn arithmetic of
+  // kv_append), the CTA holding the member's last row rotates k, writes k and
+  // v into their head-blocks (pool_w) and patches its staged copy of the row.
+  const void* qkv;
+  void* pool_w;
+  const float* rope;        // [rope_positions][64][2] (cos, sin)
+  int rope_positions;
   int B, H, layer, max_rows, row_width;
   int splits, rows_per_split;
   float scale_log2;         // log2(e) / sqrt(128)

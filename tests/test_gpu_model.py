@@ -359,17 +359,20 @@ def test_measured_engine_runs_config1_on_device_time(tiny_unit):
         check_tokens(refs[r.llm], prompt, toks)
 
 
-def test_fused_qkv_epilogue_is_bit_identical_to_kv_append(tiny_unit):
-    """K2 fused into the QKV GEMM epilogue (option "fuse_qkv") against the
-    separate kv_append kernel (default): same bf16 rounding and _rn RoPE arithmetic, so the same
+@pytest.mark.parametrize("option", ["fuse_qkv", "fuse_k2"])
+def test_fused_qkv_epilogue_is_bit_identical_to_kv_append(tiny_unit, option):
+    """K2 fused into the QKV GEMM epilogue (option "fuse_qkv") or into the
+    decode attention K1 (option "fuse_k2") against the separate
+    kv_append kernel: same bf16 rounding and _rn RoPE arithmetic, so the same
     prefill + decode produce identical tokens."""
     unit, specs, refs = tiny_unit
     rng = np.random.default_rng(77)
     lens = [1, 15, 16, 17, 64, 200]
     prompts = [rng.integers(0, specs[0].vocab, n).astype(np.int32) for n in lens]
     runs = []
+    unit.set_option("fuse_k2", 0)
     for fused, base in ((1, 61000), (0, 62000)):
-        unit.set_option("fuse_qkv", fused)
+        unit.set_option(option, fused)
         rids = [base + i for i in range(len(lens))]
         for rid, n in zip(rids, lens):
             assert unit.pool.admit(0, rid, n, n + 10).ok
@@ -389,6 +392,7 @@ def test_fused_qkv_epilogue_is_bit_identical_to_kv_append(tiny_unit):
             unit.pool.free_request(0, rid)
         runs.append(gen)
     unit.set_option("fuse_qkv", 0)
+    unit.set_option("fuse_k2", 0)
     assert runs[0] == runs[1]
     for i in range(len(lens)):
         check_tokens(refs[0], prompts[i], runs[0][i])
