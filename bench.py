@@ -195,11 +195,16 @@ def run_ours(args, rank, world, local_rank):
             rids.append(rid)
         ids.append(rids)
     ids_c = [unit._ids(r) for r in ids]
+    # jobs are enqueued heaviest first (most bytes per round): the host issues
+    # ~8 launches per layer, and the longest job should not wait behind the
+    # enqueue of the others (matters for the e2e loop, which syncs each step)
+    issue_order = sorted(range(len(specs)), key=lambda li: -(specs[li].weight_bytes + sum(
+        p + d for p, o, d in batches[li]) * specs[li].kv_bytes_per_token()))
     ctx0 = [sum(pool.request_tokens(li, r) for r in ids[li]) for li in range(len(specs))]
 
     def step(tokens=None, outs=None, whole_gpu=False):
         # one ADBS decode round: +1 token per member (BlockPool), then the jobs
-        for li in range(len(specs)):
+        for li in issue_order:
             if not all(r.ok for r in pool.alloc_n(li, ids_c[li], 1, False)):
                 raise RuntimeError("pool exhausted")
             unit.decode(li, ids[li], tokens=None if tokens is None else tokens[li],
