@@ -837,6 +837,7 @@ void Runtime::prefill(Llama& m, Workspace& ws, int n, const int32_t* slots_host,
   pa.H = H;
   pa.T = T;
   pa.scale_log2 = 1.4426950408889634f / std::sqrt(128.f);
+  pa.max_ctas = ws.sms;
   for (int l = 0; l < L; ++l) {
     ap.layer = l;
     if (fuse_qkv_) {

@@ -219,6 +219,7 @@ struct PrefillAttnArgs {
   const void* tmap_qkv;     // make_tmap_bf16(qkv, T, 3*H*128, .., box_rows 128)
   int n_tiles, nseq, H, T;
   float scale_log2;
+  int max_ctas = 0;         // persistent grid (the partition's SMs); 0 = 148
 };
 cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream);
 size_t prefill_attention_smem();

@@ -27,6 +27,7 @@
 #include <cuda_bf16.h>
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <cstdint>
 #include <cstring>
 
@@ -57,6 +58,8 @@ struct Bars {
   uint64_t s_empty[2];
   uint64_t p_full;
   uint64_t o_full;
+  uint64_t q_empty;  // persistent: the item's last Q K^T done, Q buffer reusable
+  uint64_t o_empty;  // persistent: the softmax warps have read the item's O
   uint32_t tmem;
   uint32_t pad[3];
   float mx[2][2][128];  // [tile parity][key half][row]: partial row maxima
@@ -75,6 +78,11 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr) {
   return d;
 }
 
+// Item of round r for CTA c: rounds alternate direction (snake) over the
+// heaviest-first item list, so every CTA gets a mix of long and short causal
+// rows instead of the c-th heaviest of every round.
+__device__ __forceinline__ int snake_item(int r, int c, int G) { return r * G + ((r & 1) ? G - 1 - c : c); }
+
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv,
                          const PrefillAttnArgs a) {
@@ -85,10 +93,12 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
   uint8_t* p_s = kv_s + kStages * 2 * kTileBytes;   // [2 halves][128 rows][128 B]
   Bars& bar = *reinterpret_cast<Bars*>(p_s + kTileBytes);
 
-  const int h = blockIdx.x;
-  const int tile = a.tiles[blockIdx.y];
-  const int seq = tile >> 16, qt = tile & 0xFFFF;
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  // Persistent: CTA c takes one work item per round in snake order over the
+  // heaviest-first list (item = tile index * H + head). TMEM, barriers and the pipeline
+  // counters live across items; the next item's Q / K_0 / V_0 loads and its
+  // first Q K^T overlap the current item's last P V and epilogue.
+  const int n_items = a.n_tiles * a.H;
 
   if (threadIdx.x == 0) {
     mbar_init(&bar.q_full, 1);
@@ -104,6 +114,8 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
     }
     mbar_init(&bar.p_full, kSoftmaxWarps);
     mbar_init(&bar.o_full, 1);
+    mbar_init(&bar.q_empty, 1);
+    mbar_init(&bar.o_empty, kSoftmaxWarps);
     fence_barrier_init();
   }
   if (warp == 0) tmem_alloc<kTmemCols>(&bar.tmem);
@@ -114,46 +126,53 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
   if (threadIdx.x == 0) grid_dep_launch();
   const uint32_t tmem = bar.tmem;
 
-  const int s0 = a.seq_start[seq];
-  const int len = a.seq_start[seq + 1] - s0;
-  const int q0 = qt * kTile;                // sequence-local index of query row 0
-  const int n_kv = qt + 1;                  // causal: key tiles 0..qt
-
   if (warp == kSoftmaxWarps) {
     if (elect_one()) {
       // ---------------- TMA producer + MMA issuer
       const uint64_t pol_q = policy_evict_first();
       const uint64_t pol_kv = policy_evict_last();  // re-read by the other q tiles of this head
+      const uint32_t idesc_qk = umma_idesc_bf16(kTile, kTile);
+      const uint32_t idesc_pv = umma_idesc_bf16(kTile, 128) | (1u << 16);  // B (V) MN-major
+      const uint32_t q_addr = smem_u32(q_s), p_addr = smem_u32(p_s);
+      int jg = 0;  // key tiles issued by this CTA before the current item (global ring / buffer counter)
+      int it = 0;
+      for (int round = 0;; ++round, ++it) {
+      const int item = snake_item(round, blockIdx.x, gridDim.x);
+      if (item >= n_items) break;
+      const int h = item % a.H;
+      const int tile = a.tiles[item / a.H];
+      const int seq = tile >> 16, qt = tile & 0xFFFF;
+      const int s0 = a.seq_start[seq];
+      const int q0 = qt * kTile;
+      const int n_kv = qt + 1;  // causal: key tiles 0..qt
+      if (it > 0) mbar_wait(&bar.q_empty, (it - 1) & 1);  // the previous item's Q K^T are done
       mbar_arrive_expect_tx(&bar.q_full, kTileBytes);
       for (int hh = 0; hh < 2; ++hh)
         tma_load_2d(q_s + hh * kHalfBytes, &tq, &bar.q_full, h * 128 + hh * 64, s0 + q0, pol_q);
       // K and V of a tile have separate ring slots and barriers: K_j's slot
       // frees when S_j = Q K_j^T completes (early), V_j's when P_j V_j does,
-      // so the next K load never waits behind a P V.
+      // so the next K load never waits behind a P V. g = global tile index.
       auto load_k = [&](int j) {
-        const int st = j % kStages;
-        if (j >= kStages) mbar_wait(&bar.k_empty[st], ((j / kStages) - 1) & 1);
+        const int g = jg + j, st = g % kStages;
+        if (g >= kStages) mbar_wait(&bar.k_empty[st], ((g / kStages) - 1) & 1);
         uint8_t* dst = kv_s + st * 2 * kTileBytes;
         mbar_arrive_expect_tx(&bar.k_full[st], kTileBytes);
         for (int hh = 0; hh < 2; ++hh)
           tma_load_2d(dst + hh * kHalfBytes, &tkv, &bar.k_full[st], (a.H + h) * 128 + hh * 64, s0 + j * kTile, pol_kv);
       };
       auto load_v = [&](int j) {
-        const int st = j % kStages;
-        if (j >= kStages) mbar_wait(&bar.v_empty[st], ((j / kStages) - 1) & 1);
+        const int g = jg + j, st = g % kStages;
+        if (g >= kStages) mbar_wait(&bar.v_empty[st], ((g / kStages) - 1) & 1);
         uint8_t* dst = kv_s + st * 2 * kTileBytes + kTileBytes;
         mbar_arrive_expect_tx(&bar.v_full[st], kTileBytes);
         for (int hh = 0; hh < 2; ++hh)
           tma_load_2d(dst + hh * kHalfBytes, &tkv, &bar.v_full[st], (2 * a.H + h) * 128 + hh * 64, s0 + j * kTile,
                       pol_kv);
       };
-      const uint32_t idesc_qk = umma_idesc_bf16(kTile, kTile);
-      const uint32_t idesc_pv = umma_idesc_bf16(kTile, 128) | (1u << 16);  // B (V) MN-major
-      const uint32_t q_addr = smem_u32(q_s), p_addr = smem_u32(p_s);
       auto issue_qk = [&](int j) {
-        const int st = j % kStages, sb = j & 1;
-        mbar_wait(&bar.k_full[st], (j / kStages) & 1);
-        if (j >= 2) mbar_wait(&bar.s_empty[sb], ((j >> 1) - 1) & 1);
+        const int g = jg + j, st = g % kStages, sb = g & 1;
+        mbar_wait(&bar.k_full[st], (g / kStages) & 1);
+        if (g >= 2) mbar_wait(&bar.s_empty[sb], ((g >> 1) - 1) & 1);
         tc_fence_after();
         const uint32_t k_addr = smem_u32(kv_s + st * 2 * kTileBytes);
 #pragma unroll
@@ -171,20 +190,22 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         load_k(1);
         load_v(1);
       }
-      mbar_wait(&bar.q_full, 0);
+      mbar_wait(&bar.q_full, it & 1);
       issue_qk(0);
       for (int j = 0; j < n_kv; ++j) {
+        const int g = jg + j;
         if (j + 1 < n_kv) issue_qk(j + 1);
+        if (j + 1 == n_kv) umma_commit(&bar.q_empty);  // fires once this item's last Q K^T is done
         // K_{j+2} goes into S_j's K slot as soon as S_j is done (issued one
-        // iteration ago): a full iteration ahead of Q K_{j+2}^T, instead of
-        // right before it (the MMA thread used to stall on that load before
-        // it could issue the next P V).
+        // iteration ago): a full iteration ahead of Q K_{j+2}^T.
         if (j + kStages < n_kv) load_k(j + kStages);
         if (j + 1 < n_kv && j + 1 >= kStages) load_v(j + 1);  // waits for P_{j-1} V_{j-1}
+        // the previous item's O must have been read before P_0 V_0 overwrites it
+        if (j == 0 && it > 0) mbar_wait(&bar.o_empty, (it - 1) & 1);
         // O_j = P_j V_j once the softmax has written P_j
-        mbar_wait(&bar.p_full, j & 1);
-        const int st = j % kStages;
-        mbar_wait(&bar.v_full[st], (j / kStages) & 1);
+        mbar_wait(&bar.p_full, g & 1);
+        const int st = g % kStages;
+        mbar_wait(&bar.v_full[st], (g / kStages) & 1);
         tc_fence_after();
         const uint32_t v_addr = smem_u32(kv_s + st * 2 * kTileBytes + kTileBytes);
 #pragma unroll
@@ -194,6 +215,8 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         }
         umma_commit(&bar.o_full);
         umma_commit(&bar.v_empty[st]);
+      }
+      jg += n_kv;
       }
     }
     __syncwarp();
@@ -205,14 +228,26 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
     // tile parity, so one barrier per tile), the row sums once at the end.
     const int quarter = warp & 3, hf = warp >> 2;
     const int row = quarter * 32 + lane;
-    const int qi = q0 + row;               // sequence-local query index
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    float m_run = -INFINITY, l_run = 0.f;
     uint8_t* p_row = p_s + hf * kHalfBytes + row * 128;
     const uint32_t o_addr = tmem + lane_base + 2 * kTile + hf * 64;
+    int jg = 0;
+    for (int round = 0;; ++round) {
+    const int item = snake_item(round, blockIdx.x, gridDim.x);
+    if (item >= n_items) break;
+    const int h = item % a.H;
+    const int tile = a.tiles[item / a.H];
+    const int seq = tile >> 16, qt = tile & 0xFFFF;
+    const int s0 = a.seq_start[seq];
+    const int len = a.seq_start[seq + 1] - s0;
+    const int q0 = qt * kTile;
+    const int n_kv = qt + 1;
+    const int qi = q0 + row;               // sequence-local query index
+    float m_run = -INFINITY, l_run = 0.f;
     for (int j = 0; j < n_kv; ++j) {
-      const int sb = j & 1;
-      mbar_wait(&bar.s_full[sb], (j >> 1) & 1);
+      const int g = jg + j;
+      const int sb = g & 1;
+      mbar_wait(&bar.s_full[sb], (g >> 1) & 1);
       tc_fence_after();
       const uint32_t s_addr = tmem + lane_base + sb * kTile + hf * 64;
       const int kmax = min(qi, len - 1) - j * kTile - hf * 64;  // keys [0, kmax] of this half are visible
@@ -237,9 +272,9 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         for (int i = 0; i < 64; ++i)
           if (i <= kmax) mx = fmaxf(mx, v[i]);
       }
-      bar.mx[j & 1][hf][row] = mx;
+      bar.mx[g & 1][hf][row] = mx;
       asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
-      mx = fmaxf(mx, bar.mx[j & 1][hf ^ 1][row]);
+      mx = fmaxf(mx, bar.mx[g & 1][hf ^ 1][row]);
       // Lazy rescaling: the running max only moves (and O is rescaled) when
       // the tile's max exceeds it by more than 2^8; otherwise P = exp2(s - m)
       // stays <= 256 under the stale max, and l / O share that max, so the
@@ -272,9 +307,10 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
           pk[i >> 1] = pack_bf16(p0, p1);
         }
       }
-      if (j > 0) {
-        // P_{j-1} V_{j-1} complete: the P buffer is free and O may be rescaled
-        mbar_wait(&bar.o_full, (j - 1) & 1);
+      if (g > 0) {
+        // the previous P V (this item's or the previous item's last) is
+        // complete: the P buffer is free and O may be rescaled
+        mbar_wait(&bar.o_full, (g - 1) & 1);
         tc_fence_after();
       }
       // keys [64hf + 8chunk, +8) in the SW128 K-major image of this half's row
@@ -302,7 +338,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
     bar.ls[hf][row] = l_run;
     asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
     const float l_tot = l_run + bar.ls[hf ^ 1][row];
-    mbar_wait(&bar.o_full, (n_kv - 1) & 1);
+    mbar_wait(&bar.o_full, (jg + n_kv - 1) & 1);
     tc_fence_after();
     const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
     uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) +
@@ -319,6 +355,11 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
                                       pack_bf16(v[8 * u + 4] * inv, v[8 * u + 5] * inv),
                                       pack_bf16(v[8 * u + 6] * inv, v[8 * u + 7] * inv));
       }
+    }
+    tc_fence_before();  // O read: the next item's P_0 V_0 may overwrite it
+    __syncwarp();
+    if (lane == 0) mbar_arrive(&bar.o_empty);
+    jg += n_kv;
     }
   }
   tc_fence_before();
@@ -347,7 +388,9 @@ cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
   CUtensorMap tq, tkv;
   std::memcpy(&tq, a.tmap_q, sizeof(CUtensorMap));
   std::memcpy(&tkv, a.tmap_qkv, sizeof(CUtensorMap));
-  return launch(prefill_attention_kernel, dim3(a.H, a.n_tiles), dim3(kThreads), kSmemBytes, stream, tq, tkv, a);
+  const int n_items = a.n_tiles * a.H;
+  const int grid = std::max(1, std::min(n_items, a.max_ctas > 0 ? a.max_ctas : 148));
+  return launch(prefill_attention_kernel, dim3(grid), dim3(kThreads), kSmemBytes, stream, tq, tkv, a);
 }
 
 }  // namespace mux
