@@ -137,86 +137,86 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
       int jg = 0;  // key tiles issued by this CTA before the current item (global ring / buffer counter)
       int it = 0;
       for (int round = 0;; ++round, ++it) {
-      const int item = snake_item(round, blockIdx.x, gridDim.x);
-      if (item >= n_items) break;
-      const int h = item % a.H;
-      const int tile = a.tiles[item / a.H];
-      const int seq = tile >> 16, qt = tile & 0xFFFF;
-      const int s0 = a.seq_start[seq];
-      const int q0 = qt * kTile;
-      const int n_kv = qt + 1;  // causal: key tiles 0..qt
-      if (it > 0) mbar_wait(&bar.q_empty, (it - 1) & 1);  // the previous item's Q K^T are done
-      mbar_arrive_expect_tx(&bar.q_full, kTileBytes);
-      for (int hh = 0; hh < 2; ++hh)
-        tma_load_2d(q_s + hh * kHalfBytes, &tq, &bar.q_full, h * 128 + hh * 64, s0 + q0, pol_q);
-      // K and V of a tile have separate ring slots and barriers: K_j's slot
-      // frees when S_j = Q K_j^T completes (early), V_j's when P_j V_j does,
-      // so the next K load never waits behind a P V. g = global tile index.
-      auto load_k = [&](int j) {
-        const int g = jg + j, st = g % kStages;
-        if (g >= kStages) mbar_wait(&bar.k_empty[st], ((g / kStages) - 1) & 1);
-        uint8_t* dst = kv_s + st * 2 * kTileBytes;
-        mbar_arrive_expect_tx(&bar.k_full[st], kTileBytes);
+        const int item = snake_item(round, blockIdx.x, gridDim.x);
+        if (item >= n_items) break;
+        const int h = item % a.H;
+        const int tile = a.tiles[item / a.H];
+        const int seq = tile >> 16, qt = tile & 0xFFFF;
+        const int s0 = a.seq_start[seq];
+        const int q0 = qt * kTile;
+        const int n_kv = qt + 1;  // causal: key tiles 0..qt
+        if (it > 0) mbar_wait(&bar.q_empty, (it - 1) & 1);  // the previous item's Q K^T are done
+        mbar_arrive_expect_tx(&bar.q_full, kTileBytes);
         for (int hh = 0; hh < 2; ++hh)
-          tma_load_2d(dst + hh * kHalfBytes, &tkv, &bar.k_full[st], (a.H + h) * 128 + hh * 64, s0 + j * kTile, pol_kv);
-      };
-      auto load_v = [&](int j) {
-        const int g = jg + j, st = g % kStages;
-        if (g >= kStages) mbar_wait(&bar.v_empty[st], ((g / kStages) - 1) & 1);
-        uint8_t* dst = kv_s + st * 2 * kTileBytes + kTileBytes;
-        mbar_arrive_expect_tx(&bar.v_full[st], kTileBytes);
-        for (int hh = 0; hh < 2; ++hh)
-          tma_load_2d(dst + hh * kHalfBytes, &tkv, &bar.v_full[st], (2 * a.H + h) * 128 + hh * 64, s0 + j * kTile,
-                      pol_kv);
-      };
-      auto issue_qk = [&](int j) {
-        const int g = jg + j, st = g % kStages, sb = g & 1;
-        mbar_wait(&bar.k_full[st], (g / kStages) & 1);
-        if (g >= 2) mbar_wait(&bar.s_empty[sb], ((g >> 1) - 1) & 1);
-        tc_fence_after();
-        const uint32_t k_addr = smem_u32(kv_s + st * 2 * kTileBytes);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-          umma_bf16(tmem + sb * kTile, umma_desc_sw128(q_addr + off), umma_desc_sw128(k_addr + off), idesc_qk,
-                    kk > 0 ? 1u : 0u);
+          tma_load_2d(q_s + hh * kHalfBytes, &tq, &bar.q_full, h * 128 + hh * 64, s0 + q0, pol_q);
+        // K and V of a tile have separate ring slots and barriers: K_j's slot
+        // frees when S_j = Q K_j^T completes (early), V_j's when P_j V_j does,
+        // so the next K load never waits behind a P V. g = global tile index.
+        auto load_k = [&](int j) {
+          const int g = jg + j, st = g % kStages;
+          if (g >= kStages) mbar_wait(&bar.k_empty[st], ((g / kStages) - 1) & 1);
+          uint8_t* dst = kv_s + st * 2 * kTileBytes;
+          mbar_arrive_expect_tx(&bar.k_full[st], kTileBytes);
+          for (int hh = 0; hh < 2; ++hh)
+            tma_load_2d(dst + hh * kHalfBytes, &tkv, &bar.k_full[st], (a.H + h) * 128 + hh * 64, s0 + j * kTile, pol_kv);
+        };
+        auto load_v = [&](int j) {
+          const int g = jg + j, st = g % kStages;
+          if (g >= kStages) mbar_wait(&bar.v_empty[st], ((g / kStages) - 1) & 1);
+          uint8_t* dst = kv_s + st * 2 * kTileBytes + kTileBytes;
+          mbar_arrive_expect_tx(&bar.v_full[st], kTileBytes);
+          for (int hh = 0; hh < 2; ++hh)
+            tma_load_2d(dst + hh * kHalfBytes, &tkv, &bar.v_full[st], (2 * a.H + h) * 128 + hh * 64, s0 + j * kTile,
+                        pol_kv);
+        };
+        auto issue_qk = [&](int j) {
+          const int g = jg + j, st = g % kStages, sb = g & 1;
+          mbar_wait(&bar.k_full[st], (g / kStages) & 1);
+          if (g >= 2) mbar_wait(&bar.s_empty[sb], ((g >> 1) - 1) & 1);
+          tc_fence_after();
+          const uint32_t k_addr = smem_u32(kv_s + st * 2 * kTileBytes);
+  #pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
+            umma_bf16(tmem + sb * kTile, umma_desc_sw128(q_addr + off), umma_desc_sw128(k_addr + off), idesc_qk,
+                      kk > 0 ? 1u : 0u);
+          }
+          umma_commit(&bar.s_full[sb]);
+          umma_commit(&bar.k_empty[st]);
+        };
+        load_k(0);
+        load_v(0);
+        if (n_kv > 1) {
+          load_k(1);
+          load_v(1);
         }
-        umma_commit(&bar.s_full[sb]);
-        umma_commit(&bar.k_empty[st]);
-      };
-      load_k(0);
-      load_v(0);
-      if (n_kv > 1) {
-        load_k(1);
-        load_v(1);
-      }
-      mbar_wait(&bar.q_full, it & 1);
-      issue_qk(0);
-      for (int j = 0; j < n_kv; ++j) {
-        const int g = jg + j;
-        if (j + 1 < n_kv) issue_qk(j + 1);
-        if (j + 1 == n_kv) umma_commit(&bar.q_empty);  // fires once this item's last Q K^T is done
-        // K_{j+2} goes into S_j's K slot as soon as S_j is done (issued one
-        // iteration ago): a full iteration ahead of Q K_{j+2}^T.
-        if (j + kStages < n_kv) load_k(j + kStages);
-        if (j + 1 < n_kv && j + 1 >= kStages) load_v(j + 1);  // waits for P_{j-1} V_{j-1}
-        // the previous item's O must have been read before P_0 V_0 overwrites it
-        if (j == 0 && it > 0) mbar_wait(&bar.o_empty, (it - 1) & 1);
-        // O_j = P_j V_j once the softmax has written P_j
-        mbar_wait(&bar.p_full, g & 1);
-        const int st = g % kStages;
-        mbar_wait(&bar.v_full[st], (g / kStages) & 1);
-        tc_fence_after();
-        const uint32_t v_addr = smem_u32(kv_s + st * 2 * kTileBytes + kTileBytes);
-#pragma unroll
-        for (int kk = 0; kk < 8; ++kk) {
-          umma_bf16(tmem + 2 * kTile, umma_desc_sw128(p_addr + (kk >> 2) * kHalfBytes + (kk & 3) * 32),
-                    umma_desc_sw128_mn(v_addr + kk * 2048), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+        mbar_wait(&bar.q_full, it & 1);
+        issue_qk(0);
+        for (int j = 0; j < n_kv; ++j) {
+          const int g = jg + j;
+          if (j + 1 < n_kv) issue_qk(j + 1);
+          if (j + 1 == n_kv) umma_commit(&bar.q_empty);  // fires once this item's last Q K^T is done
+          // K_{j+2} goes into S_j's K slot as soon as S_j is done (issued one
+          // iteration ago): a full iteration ahead of Q K_{j+2}^T.
+          if (j + kStages < n_kv) load_k(j + kStages);
+          if (j + 1 < n_kv && j + 1 >= kStages) load_v(j + 1);  // waits for P_{j-1} V_{j-1}
+          // the previous item's O must have been read before P_0 V_0 overwrites it
+          if (j == 0 && it > 0) mbar_wait(&bar.o_empty, (it - 1) & 1);
+          // O_j = P_j V_j once the softmax has written P_j
+          mbar_wait(&bar.p_full, g & 1);
+          const int st = g % kStages;
+          mbar_wait(&bar.v_full[st], (g / kStages) & 1);
+          tc_fence_after();
+          const uint32_t v_addr = smem_u32(kv_s + st * 2 * kTileBytes + kTileBytes);
+  #pragma unroll
+          for (int kk = 0; kk < 8; ++kk) {
+            umma_bf16(tmem + 2 * kTile, umma_desc_sw128(p_addr + (kk >> 2) * kHalfBytes + (kk & 3) * 32),
+                      umma_desc_sw128_mn(v_addr + kk * 2048), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+          }
+          umma_commit(&bar.o_full);
+          umma_commit(&bar.v_empty[st]);
         }
-        umma_commit(&bar.o_full);
-        umma_commit(&bar.v_empty[st]);
-      }
-      jg += n_kv;
+        jg += n_kv;
       }
     }
     __syncwarp();
@@ -233,133 +233,133 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
     const uint32_t o_addr = tmem + lane_base + 2 * kTile + hf * 64;
     int jg = 0;
     for (int round = 0;; ++round) {
-    const int item = snake_item(round, blockIdx.x, gridDim.x);
-    if (item >= n_items) break;
-    const int h = item % a.H;
-    const int tile = a.tiles[item / a.H];
-    const int seq = tile >> 16, qt = tile & 0xFFFF;
-    const int s0 = a.seq_start[seq];
-    const int len = a.seq_start[seq + 1] - s0;
-    const int q0 = qt * kTile;
-    const int n_kv = qt + 1;
-    const int qi = q0 + row;               // sequence-local query index
-    float m_run = -INFINITY, l_run = 0.f;
-    for (int j = 0; j < n_kv; ++j) {
-      const int g = jg + j;
-      const int sb = g & 1;
-      mbar_wait(&bar.s_full[sb], (g >> 1) & 1);
-      tc_fence_after();
-      const uint32_t s_addr = tmem + lane_base + sb * kTile + hf * 64;
-      const int kmax = min(qi, len - 1) - j * kTile - hf * 64;  // keys [0, kmax] of this half are visible
-      // S read once (64 keys of this half into registers); the S buffer is
-      // handed back right away so Q K_{j+2}^T can start.
-      float v[64];
-      tmem_ld_32x32b_x32(s_addr, *reinterpret_cast<float(*)[32]>(v));
-      tmem_ld_32x32b_x32(s_addr + 32, *reinterpret_cast<float(*)[32]>(v + 32));
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar.s_empty[sb]);
-      // partial row max over this half, exchanged with the partner warp
-      // Tiles below the diagonal and inside the sequence need no masking:
-      // the fast path is 3-input max, paired FMA, bare MUFU.EX2, paired add.
-      const bool full = kmax >= 63;
-      float mx = -INFINITY;
-      if (full) {
-#pragma unroll
-        for (int i = 0; i < 64; i += 2) mx = fmax3(mx, v[i], v[i + 1]);
-      } else {
-#pragma unroll
-        for (int i = 0; i < 64; ++i)
-          if (i <= kmax) mx = fmaxf(mx, v[i]);
-      }
-      bar.mx[g & 1][hf][row] = mx;
-      asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
-      mx = fmaxf(mx, bar.mx[g & 1][hf ^ 1][row]);
-      // Lazy rescaling: the running max only moves (and O is rescaled) when
-      // the tile's max exceeds it by more than 2^8; otherwise P = exp2(s - m)
-      // stays <= 256 under the stale max, and l / O share that max, so the
-      // final O / l is unchanged.
-      const float m_tile = mx * a.scale_log2;
-      const bool move = m_tile > m_run + 8.f;
-      const float m_new = move ? m_tile : m_run;
-      const float m_use = m_new == -INFINITY ? 0.f : m_new;
-      const float alpha = move ? exp2f(m_run - m_use) : 1.f;
-      // P = exp2(s - m) -> packed bf16 in registers while P_{j-1} V_{j-1} runs
-      float psum = 0.f;
-      uint32_t pk[32];
-      if (full) {
-        float s0 = 0.f, s1 = 0.f;
-#pragma unroll
-        for (int i = 0; i < 64; i += 2) {
-          float x0, x1;
-          ffma2(x0, x1, v[i], v[i + 1], a.scale_log2, a.scale_log2, -m_use, -m_use);
-          const float p0 = ex2_ftz(x0), p1 = ex2_ftz(x1);
-          fadd2(s0, s1, p0, p1);
-          pk[i >> 1] = pack_bf16(p0, p1);
-        }
-        psum = s0 + s1;
-      } else {
-#pragma unroll
-        for (int i = 0; i < 64; i += 2) {
-          const float p0 = i <= kmax ? exp2f(fmaf(v[i], a.scale_log2, -m_use)) : 0.f;
-          const float p1 = i + 1 <= kmax ? exp2f(fmaf(v[i + 1], a.scale_log2, -m_use)) : 0.f;
-          psum += p0 + p1;
-          pk[i >> 1] = pack_bf16(p0, p1);
-        }
-      }
-      if (g > 0) {
-        // the previous P V (this item's or the previous item's last) is
-        // complete: the P buffer is free and O may be rescaled
-        mbar_wait(&bar.o_full, (g - 1) & 1);
+      const int item = snake_item(round, blockIdx.x, gridDim.x);
+      if (item >= n_items) break;
+      const int h = item % a.H;
+      const int tile = a.tiles[item / a.H];
+      const int seq = tile >> 16, qt = tile & 0xFFFF;
+      const int s0 = a.seq_start[seq];
+      const int len = a.seq_start[seq + 1] - s0;
+      const int q0 = qt * kTile;
+      const int n_kv = qt + 1;
+      const int qi = q0 + row;               // sequence-local query index
+      float m_run = -INFINITY, l_run = 0.f;
+      for (int j = 0; j < n_kv; ++j) {
+        const int g = jg + j;
+        const int sb = g & 1;
+        mbar_wait(&bar.s_full[sb], (g >> 1) & 1);
         tc_fence_after();
+        const uint32_t s_addr = tmem + lane_base + sb * kTile + hf * 64;
+        const int kmax = min(qi, len - 1) - j * kTile - hf * 64;  // keys [0, kmax] of this half are visible
+        // S read once (64 keys of this half into registers); the S buffer is
+        // handed back right away so Q K_{j+2}^T can start.
+        float v[64];
+        tmem_ld_32x32b_x32(s_addr, *reinterpret_cast<float(*)[32]>(v));
+        tmem_ld_32x32b_x32(s_addr + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+        tc_fence_before();
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar.s_empty[sb]);
+        // partial row max over this half, exchanged with the partner warp
+        // Tiles below the diagonal and inside the sequence need no masking:
+        // the fast path is 3-input max, paired FMA, bare MUFU.EX2, paired add.
+        const bool full = kmax >= 63;
+        float mx = -INFINITY;
+        if (full) {
+  #pragma unroll
+          for (int i = 0; i < 64; i += 2) mx = fmax3(mx, v[i], v[i + 1]);
+        } else {
+  #pragma unroll
+          for (int i = 0; i < 64; ++i)
+            if (i <= kmax) mx = fmaxf(mx, v[i]);
+        }
+        bar.mx[g & 1][hf][row] = mx;
+        asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
+        mx = fmaxf(mx, bar.mx[g & 1][hf ^ 1][row]);
+        // Lazy rescaling: the running max only moves (and O is rescaled) when
+        // the tile's max exceeds it by more than 2^8; otherwise P = exp2(s - m)
+        // stays <= 256 under the stale max, and l / O share that max, so the
+        // final O / l is unchanged.
+        const float m_tile = mx * a.scale_log2;
+        const bool move = m_tile > m_run + 8.f;
+        const float m_new = move ? m_tile : m_run;
+        const float m_use = m_new == -INFINITY ? 0.f : m_new;
+        const float alpha = move ? exp2f(m_run - m_use) : 1.f;
+        // P = exp2(s - m) -> packed bf16 in registers while P_{j-1} V_{j-1} runs
+        float psum = 0.f;
+        uint32_t pk[32];
+        if (full) {
+          float s0 = 0.f, s1 = 0.f;
+  #pragma unroll
+          for (int i = 0; i < 64; i += 2) {
+            float x0, x1;
+            ffma2(x0, x1, v[i], v[i + 1], a.scale_log2, a.scale_log2, -m_use, -m_use);
+            const float p0 = ex2_ftz(x0), p1 = ex2_ftz(x1);
+            fadd2(s0, s1, p0, p1);
+            pk[i >> 1] = pack_bf16(p0, p1);
+          }
+          psum = s0 + s1;
+        } else {
+  #pragma unroll
+          for (int i = 0; i < 64; i += 2) {
+            const float p0 = i <= kmax ? exp2f(fmaf(v[i], a.scale_log2, -m_use)) : 0.f;
+            const float p1 = i + 1 <= kmax ? exp2f(fmaf(v[i + 1], a.scale_log2, -m_use)) : 0.f;
+            psum += p0 + p1;
+            pk[i >> 1] = pack_bf16(p0, p1);
+          }
+        }
+        if (g > 0) {
+          // the previous P V (this item's or the previous item's last) is
+          // complete: the P buffer is free and O may be rescaled
+          mbar_wait(&bar.o_full, (g - 1) & 1);
+          tc_fence_after();
+        }
+        // keys [64hf + 8chunk, +8) in the SW128 K-major image of this half's row
+  #pragma unroll
+        for (int chunk = 0; chunk < 8; ++chunk)
+          *reinterpret_cast<uint4*>(p_row + ((chunk ^ (row & 7)) << 4)) =
+              make_uint4(pk[4 * chunk], pk[4 * chunk + 1], pk[4 * chunk + 2], pk[4 * chunk + 3]);
+        if (j > 0 && __any_sync(0xffffffffu, move)) {
+  #pragma unroll 1
+          for (int c = 0; c < 2; ++c) {
+            float o[32];
+            tmem_ld_32x32b_x32(o_addr + c * 32, o);
+  #pragma unroll
+            for (int i = 0; i < 32; ++i) o[i] *= alpha;
+            tmem_st_32x32b_x32(o_addr + c * 32, o);
+          }
+        }
+        l_run = l_run * alpha + psum;
+        m_run = m_new;
+        tc_fence_before();
+        fence_async_smem();  // P (generic writes) -> the tensor core (async proxy)
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&bar.p_full);
       }
-      // keys [64hf + 8chunk, +8) in the SW128 K-major image of this half's row
-#pragma unroll
-      for (int chunk = 0; chunk < 8; ++chunk)
-        *reinterpret_cast<uint4*>(p_row + ((chunk ^ (row & 7)) << 4)) =
-            make_uint4(pk[4 * chunk], pk[4 * chunk + 1], pk[4 * chunk + 2], pk[4 * chunk + 3]);
-      if (j > 0 && __any_sync(0xffffffffu, move)) {
-#pragma unroll 1
-        for (int c = 0; c < 2; ++c) {
-          float o[32];
-          tmem_ld_32x32b_x32(o_addr + c * 32, o);
-#pragma unroll
-          for (int i = 0; i < 32; ++i) o[i] *= alpha;
-          tmem_st_32x32b_x32(o_addr + c * 32, o);
+      bar.ls[hf][row] = l_run;
+      asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
+      const float l_tot = l_run + bar.ls[hf ^ 1][row];
+      mbar_wait(&bar.o_full, (jg + n_kv - 1) & 1);
+      tc_fence_after();
+      const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
+      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) +
+                                            (static_cast<int64_t>(s0 + qi) * a.H + h) * 128 + hf * 64);
+  #pragma unroll
+      for (int c = 0; c < 2; ++c) {
+        float v[32];
+        tmem_ld_32x32b_x32(o_addr + c * 32, v);  // all lanes: .sync.aligned
+        if (qi < len) {
+  #pragma unroll
+          for (int u = 0; u < 4; ++u)
+            dst[c * 4 + u] = make_uint4(pack_bf16(v[8 * u] * inv, v[8 * u + 1] * inv),
+                                        pack_bf16(v[8 * u + 2] * inv, v[8 * u + 3] * inv),
+                                        pack_bf16(v[8 * u + 4] * inv, v[8 * u + 5] * inv),
+                                        pack_bf16(v[8 * u + 6] * inv, v[8 * u + 7] * inv));
         }
       }
-      l_run = l_run * alpha + psum;
-      m_run = m_new;
-      tc_fence_before();
-      fence_async_smem();  // P (generic writes) -> the tensor core (async proxy)
+      tc_fence_before();  // O read: the next item's P_0 V_0 may overwrite it
       __syncwarp();
-      if (lane == 0) mbar_arrive(&bar.p_full);
-    }
-    bar.ls[hf][row] = l_run;
-    asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
-    const float l_tot = l_run + bar.ls[hf ^ 1][row];
-    mbar_wait(&bar.o_full, (jg + n_kv - 1) & 1);
-    tc_fence_after();
-    const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
-    uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) +
-                                          (static_cast<int64_t>(s0 + qi) * a.H + h) * 128 + hf * 64);
-#pragma unroll
-    for (int c = 0; c < 2; ++c) {
-      float v[32];
-      tmem_ld_32x32b_x32(o_addr + c * 32, v);  // all lanes: .sync.aligned
-      if (qi < len) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u)
-          dst[c * 4 + u] = make_uint4(pack_bf16(v[8 * u] * inv, v[8 * u + 1] * inv),
-                                      pack_bf16(v[8 * u + 2] * inv, v[8 * u + 3] * inv),
-                                      pack_bf16(v[8 * u + 4] * inv, v[8 * u + 5] * inv),
-                                      pack_bf16(v[8 * u + 6] * inv, v[8 * u + 7] * inv));
-      }
-    }
-    tc_fence_before();  // O read: the next item's P_0 V_0 may overwrite it
-    __syncwarp();
-    if (lane == 0) mbar_arrive(&bar.o_empty);
-    jg += n_kv;
+      if (lane == 0) mbar_arrive(&bar.o_empty);
+      jg += n_kv;
     }
   }
   tc_fence_before();
