@@ -62,6 +62,37 @@ def tiny_unit(cuda):
     unit.close()
 
 
+@pytest.mark.parametrize("llm", [0, 1])
+def test_long_prefill_matches_oracle(tiny_unit, llm):
+    """Prefill of 1-4 long prompts (up to 1300 tokens, several 128-query
+    tiles per prompt): the persistent K3 walks many (tile, head) items per
+    CTA and the projections run on CTA pairs (M > 256); first tokens and a
+    few decode steps against the oracle."""
+    unit, specs, refs = tiny_unit
+    rng = np.random.default_rng(40 + llm)
+    lens = [1300, 700, 129, 3]
+    rids = [5000 + 100 * llm + i for i in range(len(lens))]
+    for rid, n in zip(rids, lens):
+        assert unit.pool.admit(llm, rid, n, n + 4).ok
+    prompts = [rng.integers(0, specs[llm].vocab, n).astype(np.int32) for n in lens]
+    first = np.zeros(len(lens), np.int32)
+    unit.prefill(llm, rids, np.concatenate(prompts), first, partition=0)
+    unit.sync()
+    gen = [[int(t)] for t in first]
+    out = np.zeros(len(lens), np.int32)
+    for _ in range(3):
+        for rid in rids:
+            assert unit.pool.alloc(llm, rid, 1, False).ok
+        unit.decode(llm, rids, out=out, partition=1)
+        unit.sync()
+        for i, t in enumerate(out):
+            gen[i].append(int(t))
+    for i in range(len(lens)):
+        check_tokens(refs[llm], prompts[i], gen[i])
+    for rid in rids:
+        unit.pool.free_request(llm, rid)
+
+
 def test_weights_round_trip(tiny_unit):
     unit, specs, _ = tiny_unit
     s = specs[0]
