@@ -262,7 +262,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       // Weights do not depend on earlier kernels: warp 0 starts streaming
       // them while the predecessor drains (PDL); activations must wait.
       if (!is_a) grid_dep_wait();
-      if (!is_a && r.dbg_nomma >= 2) return;  // debug: weights only
+      if (!is_a && r.dbg_nomma == 2) return;  // debug: weights only
       const uint64_t pol = is_a ? policy_evict_first()   // weights: streamed once per step
                                 : policy_evict_last();   // activations: re-read by every CTA
       const int SS = is_a ? SA : SB;
@@ -335,7 +335,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       for (int kbi = kb0; kbi < kb1; ++kbi, ++i) {
         mbar_wait(&full_a[sa], ra & 1);
         if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 64 + 4] = gtimer();
-        if (r.dbg_nomma < 2 && !(r.dbg_bres && rb > 0)) mbar_wait(&full_b[sb], rb & 1);
+        if (r.dbg_nomma != 2 && !(r.dbg_bres && rb > 0)) mbar_wait(&full_b[sb], rb & 1);
         if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 64 + 5] = gtimer();
         tc_fence_after();
         if (elect_one()) {
@@ -343,12 +343,13 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           const uint32_t b_addr = smem_u32(b_st + sb * b_stage_bytes);
 #pragma unroll
           for (int kk = 0; kk < kBK / 16; ++kk) {
-            if (r.dbg_nomma) break;
+            if (r.dbg_nomma == 1 || r.dbg_nomma == 2) break;
+            if (r.dbg_nomma == 3 && (kbi & 1)) break;  // debug: MMAs on every other stage only
             // Advance along K inside the swizzle atom: 16 bf16 = 32 bytes.
             umma_bf16(acc, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
                       (kbi != kb0 || kk != 0) ? 1u : 0u);
           }
-          if (r.dbg_nomma) {  // debug: pure streaming rate (results are garbage)
+          if (r.dbg_nomma == 1 || r.dbg_nomma == 2) {  // debug: pure streaming rate (results are garbage)
             mbar_arrive(&empty_a[sa]);
             if (r.dbg_nomma < 2) mbar_arrive(&empty_b[sb]);
             if (kbi == kb1 - 1) mbar_arrive(&tm_full[b]);
