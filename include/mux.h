@@ -136,6 +136,11 @@ typedef struct {
   int64_t token_budget;
   int block_tokens;
   double warmup_s, decode_sm, prefill_min_sm, activation_reserve_frac, quota_floor_frac;
+  /* NULL: the reference's decode cost form. Else 4 doubles {decode_fixed_ms,
+   * decode_row_ms, decode_bctx_ms, decode_sm_exponent}: the HBM-bound form
+   * (B200 extension,
+   * LatencyProfile::decode_form 1; DESIGN §4 "measured latency profile"). */
+  const double* decode_hbm;
 } mux_sim_config;
 
 typedef struct {
@@ -330,8 +335,17 @@ MUX_API int64_t mux_unit_launches(mux_unit* unit);
  * "chain" (decode layers as one fused persistent layer-chain launch plus
  * K1, default 0 = one launch per projection / element-wise step);
  * "fuse_qkv" (RoPE + KV append in the QKV GEMM epilogue, default 0: the
- * epilogue on the critical path costs more than the separate kv_append). */
+ * epilogue on the critical path costs more than the separate kv_append);
+ * "prefill_on_partition" (prefill jobs on their model's partition);
+ * "pass_green" (partitions = [whole GPU | a whole-GPU stream per model |
+ * a green partition per model]; decode jobs use the green partitions only in
+ * passes holding decode jobs of two or more models). */
 MUX_API int mux_unit_set_option(mux_unit* unit, const char* key, int64_t value);
+/* Scheduling passes of the last lockstep / measured run, and how many of
+ * them put their decode jobs on green partitions (option "pass_green":
+ * decode jobs of two or more models in one pass). Replaces nothing in the
+ * reference: its launch (sim_engine.cpp:308-330) prices sm_demand shares. */
+MUX_API int mux_unit_pass_stats(mux_unit* unit, int64_t* passes, int64_t* green_passes);
 
 /* Lockstep run: the engine's decisions are those of mux_simulate (oracle
  * timing), and every launched job executes on the unit's GPU. Synthetic

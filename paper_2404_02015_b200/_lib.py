@@ -58,7 +58,7 @@ class SimConfig(C.Structure):
                 ("kappa", f64), ("quota_period_s", f64), ("token_budget", i64),
                 ("block_tokens", C.c_int), ("warmup_s", f64), ("decode_sm", f64),
                 ("prefill_min_sm", f64), ("activation_reserve_frac", f64),
-                ("quota_floor_frac", f64)]
+                ("quota_floor_frac", f64), ("decode_hbm", P(f64))]
 
 
 class Request(C.Structure):
@@ -155,6 +155,7 @@ _SIGS = {
     "mux_unit_attn_timing": (C.c_int, [vp, C.c_int]),
     "mux_unit_attn_time": (C.c_int, [vp, P(f64), P(i64), P(f64)]),
     "mux_unit_launches": (i64, [vp]),
+    "mux_unit_pass_stats": (C.c_int, [vp, C.POINTER(i64), C.POINTER(i64)]),
     "mux_unit_last_stats": (C.c_int, [vp, P(vp)]),
     "mux_unit_run_lockstep": (C.c_int, [vp, P(SimConfig), C.c_int, P(LlmEntry), C.c_int,
                                         P(Request), u64, P(Record), P(i32)]),

@@ -17,6 +17,18 @@ framework's priced engine -- run on B200 costs:
 
     python -m paper_2404_02015_b200.calibrate -o b200_profile.json
 
+The reference's decode form is not how a B200 decode step behaves: the step
+streams the weights once plus every member's K/V, so its time is linear in
+batch x context, and a partial SM share slows it as f^-0.6, not flat then
+1/f. fit_profile() therefore also fits the HBM-bound form
+(LatencyProfile::decode_form 1, a B200 extension; csrc/host/spec.cpp):
+
+    decode   = (decode_fixed_ms + decode_row_ms * b + decode_bctx_ms * b * ctx)
+               * scale * f^-decode_sm_exponent / tp_speedup
+
+and adds its three keys to the profile (wire.HBM_KEYS); a config holding
+them prices decode that way, one without them is the reference's model.
+
 The output's "profile" object drops into a reference config unchanged
 (config.cpp "profile" section; wire.load_config reads it too). tp_efficiency
 needs a multi-GPU mesh and keeps its default on a one-GPU box (stated in the
@@ -101,6 +113,59 @@ def fit_sm_saturation(points):
     return best
 
 
+def _lstsq(rows, ys, ws):
+    """Weighted least squares y ~ rows . coef (normal equations, Gaussian
+    elimination with partial pivoting); returns coef."""
+    n = len(rows[0])
+    a = [[sum(w * r[i] * r[j] for r, w in zip(rows, ws)) for j in range(n)] for i in range(n)]
+    v = [sum(w * r[i] * y for r, y, w in zip(rows, ys, ws)) for i in range(n)]
+    for c in range(n):
+        piv = max(range(c, n), key=lambda i: abs(a[i][c]))
+        a[c], a[piv], v[c], v[piv] = a[piv], a[c], v[piv], v[c]
+        if abs(a[c][c]) < 1e-300:
+            raise ValueError("singular least-squares system")
+        for i in range(c + 1, n):
+            f = a[i][c] / a[c][c]
+            a[i] = [x - f * y for x, y in zip(a[i], a[c])]
+            v[i] -= f * v[c]
+    coef = [0.0] * n
+    for i in reversed(range(n)):
+        coef[i] = (v[i] - sum(a[i][j] * coef[j] for j in range(i + 1, n))) / a[i][i]
+    return coef
+
+
+def fit_decode_hbm(points, scale):
+    """points: [(batch, ctx, ms)] -> (decode_fixed_ms, decode_row_ms,
+    decode_bctx_ms, rel_rms) of the HBM-bound form: ms = (fixed + row * b +
+    bctx * b * ctx) * scale, relative-error weighted. A negative per-row
+    term (too few batch sizes to separate it) is dropped to 0 and refit."""
+    ys = [ms for _, _, ms in points]
+    ws = [1.0 / (y * y) for y in ys]
+    base, row, bctx = _lstsq([(1.0, b, b * c) for b, c, _ in points], ys, ws)
+    if row < 0:
+        row = 0.0
+        base, bctx = _lstsq([(1.0, b * c) for b, c, _ in points], ys, ws)
+    if base <= 0 or bctx <= 0:
+        raise ValueError("HBM decode fit failed (non-positive coefficients)")
+    err = math.sqrt(sum(((base + row * b + bctx * b * c) / ms - 1.0) ** 2 for b, c, ms in points) / len(points))
+    return base / scale, row / scale, bctx / scale, err
+
+
+def fit_sm_exponent(points):
+    """points: [(f, ms)] with a full-GPU point -> (exponent, rel_rms) of
+    ms = t(1) * f^-exponent (log-log least squares through t(1)), clamped to
+    [0, 1]."""
+    t1 = [ms for f, ms in points if f >= 0.999]
+    if not t1:
+        raise ValueError("need a full-GPU point")
+    t1 = t1[0]
+    xs = [(-math.log(f), math.log(ms / t1)) for f, ms in points if f < 0.999]
+    e = sum(x * y for x, y in xs) / sum(x * x for x, _ in xs) if xs else 0.0
+    e = min(1.0, max(0.0, e))
+    err = math.sqrt(sum((t1 * f ** -e / ms - 1.0) ** 2 for f, ms in points) / len(points))
+    return e, err
+
+
 def fit_profile(prefill_pts, decode_pts, sm_pts, num_layers, hidden):
     """All measurements of one model -> the LatencyProfile dict + fit report."""
     scale = model_scale(num_layers, hidden)
@@ -111,7 +176,16 @@ def fit_profile(prefill_pts, decode_pts, sm_pts, num_layers, hidden):
     prof.update({"prefill_ms_per_token": pf, "decode_base_ms": base, "decode_ctx_ms_per_token": ctx,
                  "batch_knee": knee, "sm_saturation_point": fsat})
     perr = math.sqrt(sum((pf * scale * t / ms - 1.0) ** 2 for t, ms in prefill_pts) / len(prefill_pts))
-    return prof, {"prefill_rel_rms": perr, "decode_rel_rms": derr, "sm_rel_rms": serr}
+    err = {"prefill_rel_rms": perr, "decode_rel_rms": derr, "sm_rel_rms": serr}
+    try:
+        hbase, hrow, hbctx, herr = fit_decode_hbm(decode_pts, scale)
+    except ValueError:
+        return prof, err  # reference form only
+    sexp, sexp_err = fit_sm_exponent(sm_pts) if sm_pts else (0.6, None)
+    prof.update({"decode_fixed_ms": hbase, "decode_row_ms": hrow, "decode_bctx_ms": hbctx,
+                 "decode_sm_exponent": sexp})
+    err.update({"decode_hbm_rel_rms": herr, "sm_exponent_rel_rms": sexp_err})
+    return prof, err
 
 
 # ------------------------------------------------------------------- GPU side

@@ -179,6 +179,13 @@ SimInputs build_inputs(const mux_sim_config* c, int n_entries, const mux_llm_ent
     in.prof.batch_knee = p[5];
     in.prof.reference_scale = p[6];
   }
+  if (c->decode_hbm) {
+    in.prof.decode_form = 1;
+    in.prof.decode_fixed_ms = c->decode_hbm[0];
+    in.prof.decode_row_ms = c->decode_hbm[1];
+    in.prof.decode_bctx_ms = c->decode_hbm[2];
+    in.prof.decode_sm_exponent = c->decode_hbm[3];
+  }
   in.params.scheduler = static_cast<muxsim::SchedKind>(c->scheduler);
   in.params.kappa = c->kappa;
   in.params.quota_period_s = c->quota_period_s;
@@ -222,6 +229,11 @@ struct mux_sim_stats {
 struct mux_unit {
   std::unique_ptr<mux_sim_stats> last_stats;  // of the last lockstep / measured run
   bool prefill_on_partition = false;          // option: prefill jobs on their model's partition
+  // option pass_green: partitions are [whole GPU | one whole-GPU stream per
+  // model | one green partition per model]; a pass's decode jobs take the
+  // green partitions only when decode jobs of two or more models share it.
+  bool pass_green = false;
+  int64_t passes = 0, green_passes = 0;  // of the last lockstep / measured run
   std::unique_ptr<mux::Runtime> rt;
   std::deque<muxsim::LLMSpec> specs;
   std::vector<std::unique_ptr<mux::Llama>> models;
@@ -305,6 +317,16 @@ class GpuExecutor : public muxsim::JobExecutor {
     for (size_t p = 1; p < u_->streams.size(); ++p) check(cudaStreamWaitEvent(u_->streams[p], tables_ready_, 0));
   }
 
+  void plan_pass(int, const std::vector<muxsim::JobPlan>& plans) override {
+    std::vector<char> decodes(u_->models.size(), 0);
+    int n = 0;
+    for (const muxsim::JobPlan& p : plans)
+      if (p.kind == muxsim::JobKind::Decode && !decodes[p.llm]) decodes[p.llm] = 1, ++n;
+    green_pass_ = n >= 2;
+    u_->green_passes += green_pass_ ? 1 : 0;
+    ++u_->passes;
+  }
+
   void launch(const muxsim::JobLaunch& j) override {
     const muxsim::UnitState& st = *j.state;
     const int P = static_cast<int>(u_->streams.size());
@@ -313,7 +335,16 @@ class GpuExecutor : public muxsim::JobExecutor {
     // every job of a model stays inside its green partition (stream 0's
     // kernels may otherwise occupy the SMs of the other model's partition).
     const bool own = j.kind != muxsim::JobKind::Prefill || u_->prefill_on_partition;
-    const int part = !own || P == 1 ? 0 : 1 + (j.llm % (P - 1));
+    int part = !own || P == 1 ? 0 : 1 + (j.llm % (P - 1));
+    if (u_->pass_green) {
+      // Per-pass choice: a decode job alone in its pass gets the whole GPU
+      // (a green share would leave the other SMs idle); decode jobs of
+      // several models split the SMs by their green partitions. Prefill
+      // follows its model's decode placement when prefill_on_partition.
+      const int n = static_cast<int>(u_->models.size());
+      if (P != 1 + 2 * n) throw std::invalid_argument("pass_green: the unit needs 1 + 2 x models partitions");
+      part = !own ? 0 : (green_pass_ ? 1 + n + j.llm : 1 + j.llm);
+    }
     cudaStream_t s = u_->streams[part];
     mux::Llama& m = *u_->models[j.llm];
     mux::Workspace& ws = *u_->ws[part];
@@ -387,6 +418,7 @@ class GpuExecutor : public muxsim::JobExecutor {
   std::vector<std::vector<int32_t>> tokens_;
   std::unordered_map<int64_t, Job> jobs_;
   cudaEvent_t tables_ready_ = nullptr;
+  bool green_pass_ = false;  // this pass's decode jobs run on green partitions
 };
 
 }  // namespace
@@ -1031,6 +1063,14 @@ int mux_unit_attn_time(mux_unit* u, double* total_ms, int64_t* launches, double*
 
 int64_t mux_unit_launches(mux_unit* u) { return u ? u->rt->launches() : -1; }
 
+int mux_unit_pass_stats(mux_unit* u, int64_t* passes, int64_t* green_passes) {
+  return guarded([&] {
+    if (u == nullptr) throw std::invalid_argument("null unit");
+    if (passes) *passes = u->passes;
+    if (green_passes) *green_passes = u->green_passes;
+  });
+}
+
 int mux_unit_tp_mailbox(mux_unit* u, int partition, void** dev_ptr, void* ipc_handle) {
   return guarded([&] {
     u->stream(partition);
@@ -1112,6 +1152,7 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
     else if (k == "fuse_qkv") u->rt->set_fuse_qkv(value != 0);
     else if (k == "l2_next") u->rt->set_l2_next(static_cast<int>(value));
     else if (k == "prefill_on_partition") u->prefill_on_partition = value != 0;
+    else if (k == "pass_green") u->pass_green = value != 0;
     else if (k == "fuse_norm") u->rt->set_fuse_norm(value != 0);
     else if (k == "fuse_k2") u->rt->set_fuse_k2(value != 0);
     else throw std::invalid_argument("unknown option: " + k);
@@ -1126,6 +1167,7 @@ int run_unit(mux_unit* u, const mux_sim_config* cfg, int n_entries, const mux_ll
     require(cfg->n_units == 1, "lockstep: single-unit placements only");
     require(n_entries == static_cast<int>(u->models.size()), "lockstep: entries must describe the unit's models");
     SimInputs in = build_inputs(cfg, n_entries, entries, n_requests, trace);
+    u->passes = u->green_passes = 0;
     GpuExecutor exec(u, prompt_seed, in.trace, measured);
     muxsim::SimResult res =
         muxsim::run_simulation(in.cluster, in.placement, in.entries, in.trace, in.prof, in.params, &exec);

@@ -98,6 +98,9 @@ class JobExecutor {
   virtual void attach_unit(int unit, const std::vector<const LLMSpec*>& specs, BlockPool& pool) = 0;
   // After one scheduling pass, before its launches: upload new block-table rows.
   virtual void begin_pass(int unit, BlockPool& pool) = 0;
+  // The pass's plans, before begin_pass: lets an executor place the jobs as a
+  // set (e.g. SM partitions only when several models' decode jobs share it).
+  virtual void plan_pass(int unit, const std::vector<JobPlan>& plans) { (void)unit; (void)plans; }
   virtual void launch(const JobLaunch& job) = 0;
   // The engine is about to retire job_id (free its requests' blocks): the
   // executor must make sure the job's device work has finished.

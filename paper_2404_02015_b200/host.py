@@ -274,12 +274,18 @@ def _build_config(gpu_memory_bytes: int, num_gpus: int, placement: Placement, pa
     placed_list = [PlacedLlm(u, e, placement.mesh_sizes[u], placement.num_sm)
                    for u, mem in enumerate(placement.members) for e in mem]
     placed = (PlacedLlm * max(len(placed_list), 1))(*placed_list)
-    prof = None if profile is None else (C.c_double * 7)(*profile)
-    keep += [sizes, placed, prof]
+    # profile: the reference's 7 LatencyProfile doubles, optionally followed
+    # by the HBM decode form's 4 (decode_fixed_ms, decode_row_ms,
+    # decode_bctx_ms, decode_sm_exponent; LatencyProfile::decode_form 1)
+    if profile is not None and len(profile) not in (7, 11):
+        raise ValueError("profile: 7 reference values, or 7 + 4 HBM decode-form values")
+    prof = None if profile is None else (C.c_double * 7)(*profile[:7])
+    hbm = None if profile is None or len(profile) == 7 else (C.c_double * 4)(*profile[7:])
+    keep += [sizes, placed, prof, hbm]
     cfg = SimConfig(1, num_gpus, gpu_memory_bytes, len(placement.mesh_sizes), sizes, len(placed_list),
                     placed, prof, params.scheduler, params.kappa, params.quota_period_s,
                     params.token_budget, params.block_tokens, params.warmup_s, params.decode_sm,
-                    params.prefill_min_sm, params.activation_reserve_frac, params.quota_floor_frac)
+                    params.prefill_min_sm, params.activation_reserve_frac, params.quota_floor_frac, hbm)
     return _Built(cfg, keep)
 
 
@@ -361,7 +367,7 @@ def slo_reference_latency_ms(s: LLMSpec, profile: Sequence[float] | None, tp_deg
     """metrics.cpp:21-27 (cost model in libmux.so)."""
     keep = []
     e = _c_entry(s, keep=keep)
-    prof = None if profile is None else (C.c_double * 7)(*profile)
+    prof = None if profile is None else (C.c_double * 7)(*profile[:7])  # SLO reference: reference form
     out = C.c_double()
     check(lib.mux_slo_reference_latency_ms(C.byref(e), prof, tp_degree, prompt_len, output_len, C.byref(out)))
     return out.value
@@ -528,6 +534,12 @@ class Unit:
 
     def set_option(self, key: str, value: int):
         check(lib.mux_unit_set_option(self._h, key.encode(), value))
+
+    def pass_stats(self) -> tuple[int, int]:
+        """(passes, green passes) of the last lockstep / measured run."""
+        a, b = C.c_int64(), C.c_int64()
+        check(lib.mux_unit_pass_stats(self._h, C.byref(a), C.byref(b)))
+        return a.value, b.value
 
     def run_lockstep(self, entries: Sequence[Entry], trace: Sequence[TraceRequest],
                      gpu_memory_bytes: int, params: EngineParams | None = None,

@@ -30,6 +30,10 @@ GIB = 1 << 30
 PROFILE_KEYS = ["prefill_ms_per_token", "decode_base_ms", "decode_ctx_ms_per_token", "tp_efficiency",
                 "sm_saturation_point", "batch_knee", "reference_scale"]
 PROFILE_DEFAULTS = [0.25, 12.0, 0.005, 0.9, 0.5, 16.0, 32.0 * 4096.0]
+# B200 extension: the HBM-bound decode form (LatencyProfile::decode_form 1,
+# DESIGN §4). A profile block holding all three keys selects it; the
+# reference's configs never carry them, so their parsing is unchanged.
+HBM_KEYS = ["decode_fixed_ms", "decode_row_ms", "decode_bctx_ms", "decode_sm_exponent"]
 SCHEDULERS = {"adbs": 0, "fcfs": 1, "round_robin": 2, "rr": 2}
 
 
@@ -107,10 +111,18 @@ def load_config(path: str, catalog: dict[str, LLMSpec] | None = None) -> Experim
                              rate, _mean_len(m.get("prompt_len", {"kind": "constant", "value": 1}), "prompt_len"),
                              _mean_len(m.get("output_len", {"kind": "constant", "value": 1}), "output_len")))
     prof = list(PROFILE_DEFAULTS)
+    hbm = {}
     for k, v in (root.get("profile") or {}).items():
+        if k in HBM_KEYS:
+            hbm[k] = float(v)
+            continue
         if k not in PROFILE_KEYS:
             raise ConfigError(f"profile: unknown key '{k}'")
         prof[PROFILE_KEYS.index(k)] = float(v)
+    if hbm:
+        if len(hbm) != len(HBM_KEYS):
+            raise ConfigError("profile: the HBM decode form needs " + ", ".join(HBM_KEYS))
+        prof += [hbm[k] for k in HBM_KEYS]
     p = EngineParams()
     sim = root.get("sim") or {}
     if "scheduler" in sim:

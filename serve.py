@@ -51,8 +51,11 @@ def make_trace(models, rates, horizon_s, seed, max_len=2048):
 
 
 def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, device=0, partition_sms=None,
-          scheduler="adbs", gpu_memory_gib=180.0, lengths=None, prefill_on_partition=False):
-    """lengths: optional per-model (prompt, output) constants (contention runs)."""
+          scheduler="adbs", gpu_memory_gib=180.0, lengths=None, prefill_on_partition=False, pass_green=None):
+    """lengths: optional per-model (prompt, output) constants (contention runs).
+    partition_sms: [0, sms of model 0's partition, ...] (static partitions).
+    pass_green: per-model green partition SMs, used only by passes holding
+    decode jobs of two or more models (whole-GPU streams otherwise)."""
     import paper_2404_02015_b200 as mux
     specs = [mux.spec(m, f"{m}.{i}") for i, m in enumerate(model_names)]  # distinct names per unit
     raw = make_trace(specs, rates, horizon_s, seed)
@@ -67,16 +70,23 @@ def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, 
     params = mux.EngineParams(scheduler={"adbs": 0, "fcfs": 1, "rr": 2}[scheduler])
     weights = sum(s.weight_bytes for s in specs)
     logical = (gpu_mem - weights - round(0.1 * gpu_mem)) // 4096
+    n_parts = len(specs) + 1
+    if pass_green is not None:
+        if partition_sms is not None or len(pass_green) != len(specs):
+            raise ValueError("pass_green takes one SM count per model and excludes partition_sms")
+        n_parts, partition_sms = 2 * len(specs) + 1, [0] * (len(specs) + 1) + list(pass_green)
     unit = mux.Unit(specs, pool_blocks=logical, device=device, device_pool_blocks=min(logical, 20_000_000),
                     max_batch=512, max_prefill_tokens=4096, max_ctx=2048 + 64, max_slots=len(trace) + 8,
-                    init_seed=1, init_std=0.02, partitions=len(specs) + 1,
+                    init_seed=1, init_std=0.02, partitions=n_parts,
                     partition_sms=partition_sms)
     try:
         unit.set_option("prefill_on_partition", int(prefill_on_partition))
+        unit.set_option("pass_green", int(pass_green is not None))
         unit.init_kv(seed=5, std=1.0)
         t0 = time.perf_counter()
         recs, _ = unit.run_lockstep(entries, trace, gpu_mem, params, measured=True)
         wall = time.perf_counter() - t0
+        passes, green_passes = unit.pass_stats()
     finally:
         unit.close()
     out_tokens = sum(r.output_len for r in trace)
@@ -95,7 +105,9 @@ def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, 
         "workload": {"models": list(model_names), "rates_rps": list(rates), "horizon_s": horizon_s, "seed": seed,
                      "lengths": "ShareGPT lognormal 161/338 sigma 0.8" if lengths is None else lengths,
                      "scheduler": scheduler, "gpu_memory_gib": gpu_memory_gib,
-                     "partition_sms": partition_sms, "prefill_on_partition": prefill_on_partition},
+                     "partition_sms": partition_sms, "prefill_on_partition": prefill_on_partition,
+                     "pass_green": pass_green},
+        "passes": passes, "green_passes": green_passes,
         "host_wall_s": round(wall, 2),
     }
 
@@ -109,6 +121,8 @@ def main():
     ap.add_argument("--partition-sms", type=lambda s: [int(x) for x in s.split(",")], default=None)
     ap.add_argument("--prefill-on-partition", type=int, default=0,
                     help="run each model's prefill jobs on its own green partition too")
+    ap.add_argument("--pass-green", type=lambda s: [int(x) for x in s.split(",")], default=None,
+                    help="per-model green partition SMs, used per pass (decode jobs of >= 2 models)")
     ap.add_argument("--scheduler", choices=["adbs", "fcfs", "rr"], default="adbs")
     ap.add_argument("--gpu-memory-gib", type=float, default=180.0)
     ap.add_argument("--lengths", default=None, help="per-model constant prompt:output, e.g. 128:384,64:64")
@@ -119,7 +133,8 @@ def main():
     lengths = None if args.lengths is None else [tuple(int(x) for x in m.split(":")) for m in args.lengths.split(",")]
     print(json.dumps(serve(models, rates, args.horizon, args.seed, partition_sms=psms, scheduler=args.scheduler,
                            gpu_memory_gib=args.gpu_memory_gib, lengths=lengths,
-                           prefill_on_partition=bool(args.prefill_on_partition))), flush=True)
+                           prefill_on_partition=bool(args.prefill_on_partition),
+                           pass_green=args.pass_green)), flush=True)
 
 
 if __name__ == "__main__":

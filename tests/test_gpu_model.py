@@ -390,6 +390,41 @@ def test_measured_engine_runs_config1_on_device_time(tiny_unit):
         check_tokens(refs[r.llm], prompt, toks)
 
 
+def test_measured_engine_chooses_green_partitions_per_pass(cuda):
+    """Option "pass_green" (serving): partitions are [whole GPU |
+    a whole-GPU stream per model | a green partition per model]. A pass whose
+    decode jobs belong to two or more models runs them on the green
+    partitions; a pass with one model's decode job gives it the whole GPU.
+    Config 1 in measured mode: both kinds of pass occur, every request
+    finishes, and the tokens pass the oracle check."""
+    specs = [mux.spec("tiny-a"), mux.spec("tiny-b")]
+    unit = mux.Unit(specs, pool_blocks=232999, device_pool_blocks=232999, max_batch=64,
+                    max_prefill_tokens=1024, max_ctx=1024, partitions=5, partition_sms=[0, 0, 0, 72, 64])
+    try:
+        assert unit.partition_sms(1) == unit.partition_sms(0) and unit.partition_sms(3) >= 72
+        weights = [load_weights(unit, i, s, 300 + i) for i, s in enumerate(specs)]
+        rope = llama_ref.rope_table(1024 + 16)
+        refs = [llama_ref.RefLlama(dims_of(s), w, rope) for s, w in zip(specs, weights)]
+        unit.set_option("pass_green", 1)
+        with open(os.path.join(GOLDEN, "sim_cfg1_tiny.json")) as f:
+            g = json.load(f)
+        names = [s.name for s in specs]
+        entries = [mux.Entry(specs[names.index(n)], rate, mp, mo) for (n, L, H, hid, wb, rate, mp, mo) in g["entries"]]
+        trace = [mux.TraceRequest(i, names.index(llm), a, p, min(o, 24)) for (i, llm, a, p, o) in g["trace"]
+                 if a < 10.0]
+        recs, tokens = unit.run_lockstep(entries, trace, g["gpu_memory_bytes"], prompt_seed=11, measured=True)
+        passes, green = unit.pass_stats()
+        assert 0 < green < passes
+        assert len(recs) == len(trace)
+        assert all(r.arrival_s <= r.first_token_s <= r.done_s for r in recs)
+        assert all(len(t) == r.output_len for t, r in zip(tokens, trace))
+        for llm in (0, 1):
+            for r, toks in [(r, t) for r, t in zip(trace, tokens) if r.llm == llm][:5]:
+                check_tokens(refs[llm], lockstep_prompt(11, r.id, r.prompt_len, specs[llm].vocab), toks)
+    finally:
+        unit.close()
+
+
 @pytest.mark.parametrize("option", ["fuse_qkv", "fuse_k2"])
 def test_fused_qkv_epilogue_is_bit_identical_to_kv_append(tiny_unit, option):
     """K2 fused into the QKV GEMM epilogue (option "fuse_qkv") or into the
