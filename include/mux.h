@@ -368,6 +368,17 @@ MUX_API int mux_unit_last_stats(mux_unit* unit, mux_sim_stats** out);
 MUX_API int mux_unit_run_measured(mux_unit* unit, const mux_sim_config* cfg, int n_entries,
                                   const mux_llm_entry* entries, int n_requests, const mux_request* trace,
                                   uint64_t prompt_seed, mux_record* records_out, int32_t* tokens_out);
+/* Real-time run ("CUDA-event-driven completions, measured
+ * interference instead of kappa"): jobs are launched asynchronously and
+ * overlap on the device across scheduling passes, as in the deployed system;
+ * the engine's clock is the device's (CUDA events from one origin), each
+ * completion is processed when its event fires, and idle gaps before the
+ * next arrival are skipped rather than waited out. Replaces the priced
+ * completion of UnitSim::launch (sim_engine.cpp:308-330). Same arguments and
+ * outputs as mux_unit_run_measured. */
+MUX_API int mux_unit_run_realtime(mux_unit* unit, const mux_sim_config* cfg, int n_entries,
+                                  const mux_llm_entry* entries, int n_requests, const mux_request* trace,
+                                  uint64_t prompt_seed, mux_record* records_out, int32_t* tokens_out);
 
 #ifdef __cplusplus
 }

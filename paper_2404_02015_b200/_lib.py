@@ -161,6 +161,8 @@ _SIGS = {
                                         P(Request), u64, P(Record), P(i32)]),
     "mux_unit_run_measured": (C.c_int, [vp, P(SimConfig), C.c_int, P(LlmEntry), C.c_int,
                                         P(Request), u64, P(Record), P(i32)]),
+    "mux_unit_run_realtime": (C.c_int, [vp, P(SimConfig), C.c_int, P(LlmEntry), C.c_int,
+                                        P(Request), u64, P(Record), P(i32)]),
 }
 
 

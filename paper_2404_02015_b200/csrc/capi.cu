@@ -6,6 +6,8 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <chrono>
+#include <thread>
 #include <cstring>
 #include <deque>
 #include <memory>
@@ -272,20 +274,66 @@ namespace {
 // the unit's GPU; completion is consumed only after the device finished.
 class GpuExecutor : public muxsim::JobExecutor {
  public:
-  GpuExecutor(mux_unit* u, uint64_t prompt_seed, const std::vector<muxsim::Request>& trace, bool measured = false)
-      : u_(u), seed_(prompt_seed), measured_(measured) {
+  GpuExecutor(mux_unit* u, uint64_t prompt_seed, const std::vector<muxsim::Request>& trace, bool measured = false,
+              bool realtime = false)
+      : u_(u), seed_(prompt_seed), measured_(measured || realtime), realtime_(realtime) {
     for (size_t i = 0; i < trace.size(); ++i) row_of_id_[trace[i].id] = static_cast<int>(i);
     tokens_.resize(trace.size());
     check(cudaEventCreateWithFlags(&tables_ready_, cudaEventDisableTiming));
     check(cudaEventCreate(&pass_start_));
+    check(cudaEventCreate(&t0_ev_));
   }
   ~GpuExecutor() override {
     for (auto& kv : jobs_) cudaEventDestroy(kv.second.done);
     cudaEventDestroy(tables_ready_);
     cudaEventDestroy(pass_start_);
+    cudaEventDestroy(t0_ev_);
+    if (upload_) {
+      cudaStreamSynchronize(upload_);
+      cudaStreamDestroy(upload_);
+    }
   }
 
-  bool measured() const override { return measured_; }
+  bool measured() const override { return measured_ && !realtime_; }
+  bool realtime() const override { return realtime_; }
+
+  // Real-time clock: host steady clock since the run started plus the idle
+  // time skipped by advance_to; job completions are device-event times on
+  // the same origin (t0 recorded with the device idle).
+  double clock_ms() const {
+    return std::chrono::duration<double, std::milli>(std::chrono::steady_clock::now() - t0_host_).count() +
+           skipped_ms_;
+  }
+
+  void advance_to(int, double t_ms) override {
+    const double c = clock_ms();
+    if (t_ms > c) skipped_ms_ += t_ms - c;
+  }
+
+  bool poll_done(int, double until_ms, std::int64_t* job_id, double* t_ms) override {
+    for (;;) {
+      // the earliest completed in-flight job (device time)
+      std::int64_t best = -1;
+      double best_t = 0.0;
+      for (std::int64_t id : inflight_) {
+        cudaError_t q = cudaEventQuery(jobs_.at(id).done);
+        if (q == cudaErrorNotReady) continue;
+        check(q);
+        float ms = 0.f;
+        check(cudaEventElapsedTime(&ms, t0_ev_, jobs_.at(id).done));
+        const double t = static_cast<double>(ms) + jobs_.at(id).skipped_ms;
+        if (best < 0 || t < best_t) best = id, best_t = t;
+      }
+      if (best >= 0 && best_t <= until_ms) {
+        inflight_.erase(std::find(inflight_.begin(), inflight_.end(), best));
+        *job_id = best;
+        *t_ms = best_t;
+        return true;
+      }
+      if (clock_ms() >= until_ms) return false;
+      std::this_thread::sleep_for(std::chrono::microseconds(20));
+    }
+  }
 
   // Device time from the start of the pass (its block-table upload included)
   // to the end of this job, waiting for it.
@@ -306,9 +354,24 @@ class GpuExecutor : public muxsim::JobExecutor {
         throw std::invalid_argument("lockstep: model " + specs[i]->name + " does not match the unit");
     }
     if (pool.total_blocks() > INT32_MAX) throw std::invalid_argument("lockstep: pool too large");
+    if (realtime_) {
+      // table uploads on their own stream: stream 0 may be running a prefill
+      check(cudaStreamCreateWithFlags(&upload_, cudaStreamNonBlocking));
+      check(cudaDeviceSynchronize());
+      check(cudaEventRecord(t0_ev_, upload_));
+      check(cudaEventSynchronize(t0_ev_));
+      t0_host_ = std::chrono::steady_clock::now();
+    }
   }
 
   void begin_pass(int, BlockPool& pool) override {
+    if (realtime_) {
+      for (int i = 0; i < static_cast<int>(u_->models.size()); ++i)
+        u_->rt->upload_rows(pool, i, *u_->models[i], upload_);
+      check(cudaEventRecord(tables_ready_, upload_));
+      for (cudaStream_t s : u_->streams) check(cudaStreamWaitEvent(s, tables_ready_, 0));
+      return;
+    }
     cudaStream_t s0 = u_->streams[0];
     if (measured_) check(cudaEventRecord(pass_start_, s0));
     for (int i = 0; i < static_cast<int>(u_->models.size()); ++i)
@@ -351,7 +414,15 @@ class GpuExecutor : public muxsim::JobExecutor {
     const int n = static_cast<int>(j.members->size());
     Job job;
     job.members = *j.members;
-    job.out = std::make_unique<mux::PinnedMem>(static_cast<size_t>(n) * 4);
+    // pinned result buffers are recycled: cudaFreeHost synchronises the
+    // device, which would serialise the real-time mode's overlapping jobs
+    for (auto it = spare_out_.begin(); it != spare_out_.end(); ++it)
+      if ((*it)->bytes >= static_cast<size_t>(n) * 4) {
+        job.out = std::move(*it);
+        spare_out_.erase(it);
+        break;
+      }
+    if (!job.out) job.out = std::make_unique<mux::PinnedMem>(std::max<size_t>(static_cast<size_t>(n) * 4, 1024));
     std::vector<int32_t> slots(n), aux(n);
     for (int i = 0; i < n; ++i) {
       const int rid = (*j.members)[i];
@@ -378,6 +449,10 @@ class GpuExecutor : public muxsim::JobExecutor {
     check(cudaEventCreateWithFlags(&job.done, measured_ ? cudaEventDefault : cudaEventDisableTiming));
     check(cudaEventRecord(job.done, s));
     job.llm = j.llm;
+    if (realtime_) {
+      job.skipped_ms = skipped_ms_;  // nothing in flight skips time, so this is fixed for the job
+      inflight_.push_back(j.job_id);
+    }
     job.global_ids.resize(n);
     for (int i = 0; i < n; ++i) job.global_ids[i] = st.requests[(*j.members)[i]].global_id;
     jobs_.emplace(j.job_id, std::move(job));
@@ -394,6 +469,7 @@ class GpuExecutor : public muxsim::JobExecutor {
       if (r != row_of_id_.end()) tokens_[r->second].push_back(out[i]);
     }
     cudaEventDestroy(job.done);
+    spare_out_.push_back(std::move(job.out));
     jobs_.erase(it);
   }
 
@@ -408,6 +484,7 @@ class GpuExecutor : public muxsim::JobExecutor {
     std::vector<int64_t> global_ids;
     std::unique_ptr<mux::PinnedMem> out;
     cudaEvent_t done = nullptr;
+    double skipped_ms = 0.0;  // real-time mode: idle time skipped before the launch
   };
   static void check(cudaError_t e) { mux::check_cuda(e, "lockstep executor"); }
   mux_unit* u_;
@@ -419,6 +496,14 @@ class GpuExecutor : public muxsim::JobExecutor {
   std::unordered_map<int64_t, Job> jobs_;
   cudaEvent_t tables_ready_ = nullptr;
   bool green_pass_ = false;  // this pass's decode jobs run on green partitions
+  // real-time mode
+  bool realtime_ = false;
+  cudaStream_t upload_ = nullptr;
+  cudaEvent_t t0_ev_ = nullptr;
+  std::chrono::steady_clock::time_point t0_host_{};
+  double skipped_ms_ = 0.0;
+  std::vector<int64_t> inflight_;
+  std::vector<std::unique_ptr<mux::PinnedMem>> spare_out_;
 };
 
 }  // namespace
@@ -1162,13 +1247,13 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
 namespace {
 int run_unit(mux_unit* u, const mux_sim_config* cfg, int n_entries, const mux_llm_entry* entries, int n_requests,
              const mux_request* trace, uint64_t prompt_seed, mux_record* records_out, int32_t* tokens_out,
-             bool measured) {
+             bool measured, bool realtime = false) {
   return guarded([&] {
     require(cfg->n_units == 1, "lockstep: single-unit placements only");
     require(n_entries == static_cast<int>(u->models.size()), "lockstep: entries must describe the unit's models");
     SimInputs in = build_inputs(cfg, n_entries, entries, n_requests, trace);
     u->passes = u->green_passes = 0;
-    GpuExecutor exec(u, prompt_seed, in.trace, measured);
+    GpuExecutor exec(u, prompt_seed, in.trace, measured, realtime);
     muxsim::SimResult res =
         muxsim::run_simulation(in.cluster, in.placement, in.entries, in.trace, in.prof, in.params, &exec);
     export_records(res, in, records_out);
@@ -1200,6 +1285,12 @@ int mux_unit_run_measured(mux_unit* u, const mux_sim_config* cfg, int n_entries,
                           int n_requests, const mux_request* trace, uint64_t prompt_seed, mux_record* records_out,
                           int32_t* tokens_out) {
   return run_unit(u, cfg, n_entries, entries, n_requests, trace, prompt_seed, records_out, tokens_out, true);
+}
+
+int mux_unit_run_realtime(mux_unit* u, const mux_sim_config* cfg, int n_entries, const mux_llm_entry* entries,
+                          int n_requests, const mux_request* trace, uint64_t prompt_seed, mux_record* records_out,
+                          int32_t* tokens_out) {
+  return run_unit(u, cfg, n_entries, entries, n_requests, trace, prompt_seed, records_out, tokens_out, false, true);
 }
 
 int mux_unit_last_stats(mux_unit* u, mux_sim_stats** out) {

@@ -111,6 +111,20 @@ class JobExecutor {
   // asks for each job's measured milliseconds (the executor waits for it).
   virtual bool measured() const { return false; }
   virtual double measure(int unit, std::int64_t job_id) { (void)unit; (void)job_id; return 0.0; }
+  // Real-time mode ("CUDA-event-driven completions"): jobs of
+  // different passes overlap on the device as they do in the deployed
+  // system, and the engine's clock is the device's. After launching, the
+  // engine polls: poll_done returns the in-flight job that completed first
+  // if it did so by `until_ms` (its device completion time in *t_ms), else
+  // false once the clock reaches until_ms. With nothing in flight the engine
+  // fast-forwards the clock to its next event (advance_to): idle time is not
+  // waited out. Contention between concurrent jobs is measured, not priced.
+  virtual bool realtime() const { return false; }
+  virtual bool poll_done(int unit, double until_ms, std::int64_t* job_id, double* t_ms) {
+    (void)unit; (void)until_ms; (void)job_id; (void)t_ms;
+    return false;
+  }
+  virtual void advance_to(int unit, double t_ms) { (void)unit; (void)t_ms; }
 };
 
 SimResult run_simulation(const Cluster& cluster, const PlacementResult& placement,

@@ -543,9 +543,12 @@ class Unit:
 
     def run_lockstep(self, entries: Sequence[Entry], trace: Sequence[TraceRequest],
                      gpu_memory_bytes: int, params: EngineParams | None = None,
-                     prompt_seed: int = 11, num_sm: float = 0.5, profile=None, measured: bool = False):
+                     prompt_seed: int = 11, num_sm: float = 0.5, profile=None, measured: bool = False,
+                     realtime: bool = False):
         """Engine decisions priced by the oracle model, every job run on this GPU
-        (measured=True: job durations are the measured device times instead).
+        (measured=True: job durations are the measured device times instead;
+        realtime=True: jobs overlap across passes and complete when their
+        device events fire, mux_unit_run_realtime).
         Returns (records, tokens) with tokens[i] the output of trace[i]."""
         params = params or EngineParams()
         placement = Placement([1], [list(range(len(entries)))], num_sm)
@@ -554,7 +557,8 @@ class Unit:
         recs = (Record * max(len(trace), 1))()
         total = sum(r.output_len for r in trace)
         toks = (C.c_int32 * max(total, 1))()
-        fn = lib.mux_unit_run_measured if measured else lib.mux_unit_run_lockstep
+        fn = (lib.mux_unit_run_realtime if realtime else
+              lib.mux_unit_run_measured if measured else lib.mux_unit_run_lockstep)
         check(fn(self._h, C.byref(b.cfg), len(entries), ents, len(trace), _c_trace(trace), prompt_seed, recs, toks))
         out, off = [], 0
         for r in trace:
