@@ -339,7 +339,10 @@ MUX_API int64_t mux_unit_launches(mux_unit* unit);
  * "prefill_on_partition" (prefill jobs on their model's partition);
  * "pass_green" (partitions = [whole GPU | a whole-GPU stream per model |
  * a green partition per model]; decode jobs use the green partitions only in
- * passes holding decode jobs of two or more models). */
+ * passes holding decode jobs of two or more models);
+ * "align_decode" (real-time runs: a decode job is held off the device until
+ * the other models' decode jobs already running have been retired, so the
+ * colocated models' steps start together and run in rounds). */
 MUX_API int mux_unit_set_option(mux_unit* unit, const char* key, int64_t value);
 /* Scheduling passes of the last lockstep / measured run, and how many of
  * them put their decode jobs on green partitions (option "pass_green":

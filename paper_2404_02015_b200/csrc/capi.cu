@@ -235,6 +235,7 @@ struct mux_unit {
   // model | one green partition per model]; a pass's decode jobs take the
   // green partitions only when decode jobs of two or more models share it.
   bool pass_green = false;
+  bool align_decode = false;  // option align_decode (real-time mode): colocated decode steps in rounds
   int64_t passes = 0, green_passes = 0;  // of the last lockstep / measured run
   std::unique_ptr<mux::Runtime> rt;
   std::deque<muxsim::LLMSpec> specs;
@@ -311,11 +312,13 @@ class GpuExecutor : public muxsim::JobExecutor {
   }
 
   bool poll_done(int, double until_ms, std::int64_t* job_id, double* t_ms) override {
+    release_held();
     for (;;) {
       // the earliest completed in-flight job (device time)
       std::int64_t best = -1;
       double best_t = 0.0;
       for (std::int64_t id : inflight_) {
+        if (jobs_.at(id).held) continue;
         cudaError_t q = cudaEventQuery(jobs_.at(id).done);
         if (q == cudaErrorNotReady) continue;
         check(q);
@@ -442,12 +445,29 @@ class GpuExecutor : public muxsim::JobExecutor {
                                               static_cast<uint64_t>(m.dims().vocab)));
       }
       u_->rt->prefill(m, ws, n, slots.data(), aux.data(), toks.data(), job.out->as<int32_t>(), s);
+    } else if (realtime_ && u_->align_decode) {
+      // Aligned decode rounds (option align_decode): a decode job waits,
+      // unlaunched, for the other models' decode jobs already on the device;
+      // it is enqueued once the engine has retired them, i.e. right after
+      // their models' next steps were launched, so colocated decode steps
+      // start together and share the GPU in rounds, as in bench.py.
+      for (int64_t id : inflight_) {
+        const Job& o = jobs_.at(id);
+        if (!o.held && o.decode && o.llm != j.llm) job.wait_for.push_back(id);
+      }
+      job.part = part;
+      job.slots = slots;
+      job.aux = aux;
+      job.held = !job.wait_for.empty();
+      if (!job.held)
+        u_->rt->decode(m, ws, n, slots.data(), aux.data(), nullptr, job.out->as<int32_t>(), s, nullptr);
     } else {
       u_->rt->decode(m, ws, n, slots.data(), aux.data(), nullptr, job.out->as<int32_t>(), s,
                      u_->timing ? &u_->timer : nullptr);
     }
+    job.decode = j.kind != muxsim::JobKind::Prefill;
     check(cudaEventCreateWithFlags(&job.done, measured_ ? cudaEventDefault : cudaEventDisableTiming));
-    check(cudaEventRecord(job.done, s));
+    if (!job.held) check(cudaEventRecord(job.done, s));
     job.llm = j.llm;
     if (realtime_) {
       job.skipped_ms = skipped_ms_;  // nothing in flight skips time, so this is fixed for the job
@@ -485,7 +505,29 @@ class GpuExecutor : public muxsim::JobExecutor {
     std::unique_ptr<mux::PinnedMem> out;
     cudaEvent_t done = nullptr;
     double skipped_ms = 0.0;  // real-time mode: idle time skipped before the launch
+    // align_decode: a held decode job (not yet on the device), the jobs it
+    // waits for, and what its enqueue needs
+    bool decode = false, held = false;
+    int part = 0;
+    std::vector<int64_t> wait_for;
+    std::vector<int32_t> slots, aux;
   };
+
+  // Enqueue the held decode jobs whose awaited jobs the engine has retired.
+  void release_held() {
+    for (int64_t id : inflight_) {
+      Job& jb = jobs_.at(id);
+      if (!jb.held) continue;
+      bool ready = true;
+      for (int64_t w : jb.wait_for) ready = ready && jobs_.find(w) == jobs_.end();
+      if (!ready) continue;
+      cudaStream_t s = u_->streams[jb.part];
+      u_->rt->decode(*u_->models[jb.llm], *u_->ws[jb.part], static_cast<int>(jb.slots.size()), jb.slots.data(),
+                     jb.aux.data(), nullptr, jb.out->as<int32_t>(), s, nullptr);
+      check(cudaEventRecord(jb.done, s));
+      jb.held = false;
+    }
+  }
   static void check(cudaError_t e) { mux::check_cuda(e, "lockstep executor"); }
   mux_unit* u_;
   uint64_t seed_;
@@ -1238,6 +1280,7 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
     else if (k == "l2_next") u->rt->set_l2_next(static_cast<int>(value));
     else if (k == "prefill_on_partition") u->prefill_on_partition = value != 0;
     else if (k == "pass_green") u->pass_green = value != 0;
+    else if (k == "align_decode") u->align_decode = value != 0;
     else if (k == "fuse_norm") u->rt->set_fuse_norm(value != 0);
     else if (k == "fuse_k2") u->rt->set_fuse_k2(value != 0);
     else throw std::invalid_argument("unknown option: " + k);

@@ -52,7 +52,7 @@ def make_trace(models, rates, horizon_s, seed, max_len=2048):
 
 def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, device=0, partition_sms=None,
           scheduler="adbs", gpu_memory_gib=180.0, lengths=None, prefill_on_partition=False, pass_green=None,
-          realtime=False):
+          realtime=False, align_decode=False):
     """lengths: optional per-model (prompt, output) constants (contention runs).
     partition_sms: [0, sms of model 0's partition, ...] (static partitions).
     pass_green: per-model green partition SMs, used only by passes holding
@@ -86,6 +86,7 @@ def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, 
     try:
         unit.set_option("prefill_on_partition", int(prefill_on_partition))
         unit.set_option("pass_green", int(pass_green is not None))
+        unit.set_option("align_decode", int(align_decode))
         unit.init_kv(seed=5, std=1.0)
         t0 = time.perf_counter()
         recs, _ = unit.run_lockstep(entries, trace, gpu_mem, params, measured=not realtime, realtime=realtime)
@@ -110,7 +111,8 @@ def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, 
                      "lengths": "ShareGPT lognormal 161/338 sigma 0.8" if lengths is None else lengths,
                      "scheduler": scheduler, "gpu_memory_gib": gpu_memory_gib,
                      "partition_sms": partition_sms, "prefill_on_partition": prefill_on_partition,
-                     "pass_green": pass_green, "engine": "realtime" if realtime else "measured"},
+                     "pass_green": pass_green, "engine": "realtime" if realtime else "measured",
+                     "align_decode": align_decode},
         "passes": passes, "green_passes": green_passes,
         "host_wall_s": round(wall, 2),
     }
@@ -129,6 +131,8 @@ def main():
                     help="per-model green partition SMs, used per pass (decode jobs of >= 2 models)")
     ap.add_argument("--realtime", action="store_true",
                     help="jobs overlap across passes, completions from device events (mux_unit_run_realtime)")
+    ap.add_argument("--align-decode", action="store_true",
+                    help="real-time: colocated models' decode steps start together (rounds)")
     ap.add_argument("--scheduler", choices=["adbs", "fcfs", "rr"], default="adbs")
     ap.add_argument("--gpu-memory-gib", type=float, default=180.0)
     ap.add_argument("--lengths", default=None, help="per-model constant prompt:output, e.g. 128:384,64:64")
@@ -140,7 +144,8 @@ def main():
     print(json.dumps(serve(models, rates, args.horizon, args.seed, partition_sms=psms, scheduler=args.scheduler,
                            gpu_memory_gib=args.gpu_memory_gib, lengths=lengths,
                            prefill_on_partition=bool(args.prefill_on_partition),
-                           pass_green=args.pass_green, realtime=args.realtime)), flush=True)
+                           pass_green=args.pass_green, realtime=args.realtime,
+                           align_decode=args.align_decode)), flush=True)
 
 
 if __name__ == "__main__":

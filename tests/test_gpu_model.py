@@ -390,12 +390,14 @@ def test_measured_engine_runs_config1_on_device_time(tiny_unit):
         check_tokens(refs[r.llm], prompt, toks)
 
 
-def test_realtime_engine_overlaps_jobs_across_passes(tiny_unit):
+@pytest.mark.parametrize("align", [0, 1])
+def test_realtime_engine_overlaps_jobs_across_passes(tiny_unit, align):
     """Real-time mode (mux_unit_run_realtime): jobs launched in
     different scheduling passes overlap on the device and complete when
     their CUDA events fire. Config 1: every request finishes with
     output_len tokens, timestamps are ordered and device-timed, the pool is
-    conserved (the engine checks it), and the tokens pass the oracle check."""
+    conserved (the engine checks it), and the tokens pass the oracle check;
+    align=1 holds each decode job until the other model's running step retires."""
     unit, specs, refs = tiny_unit
     with open(os.path.join(GOLDEN, "sim_cfg1_tiny.json")) as f:
         g = json.load(f)
@@ -403,7 +405,11 @@ def test_realtime_engine_overlaps_jobs_across_passes(tiny_unit):
     entries = [mux.Entry(specs[names.index(n)], rate, mp, mo) for (n, L, H, hid, wb, rate, mp, mo) in g["entries"]]
     trace = [mux.TraceRequest(i, names.index(llm), a, p, min(o, 24)) for (i, llm, a, p, o) in g["trace"]
              if a < 10.0]
-    recs, tokens = unit.run_lockstep(entries, trace, g["gpu_memory_bytes"], prompt_seed=11, realtime=True)
+    unit.set_option("align_decode", align)
+    try:
+        recs, tokens = unit.run_lockstep(entries, trace, g["gpu_memory_bytes"], prompt_seed=11, realtime=True)
+    finally:
+        unit.set_option("align_decode", 0)
     assert len(recs) == len(trace)
     assert all(r.arrival_s <= r.first_token_s <= r.done_s for r in recs)
     assert all(len(t) == r.output_len for t, r in zip(tokens, trace))
