@@ -8,10 +8,13 @@
 #include <algorithm>
 #include <chrono>
 #include <thread>
+#include <cstdio>
+#include <cstdlib>
 #include <cstring>
 #include <deque>
 #include <memory>
 #include <stdexcept>
+#include <sstream>
 #include <string>
 #include <unordered_map>
 #include <vector>
@@ -417,6 +420,10 @@ class GpuExecutor : public muxsim::JobExecutor {
     const int n = static_cast<int>(j.members->size());
     Job job;
     job.members = *j.members;
+    if (realtime_ && trace_) {
+      check(cudaEventCreate(&job.start));
+      check(cudaEventRecord(job.start, s));  // held jobs re-record at release
+    }
     // pinned result buffers are recycled: cudaFreeHost synchronises the
     // device, which would serialise the real-time mode's overlapping jobs
     for (auto it = spare_out_.begin(); it != spare_out_.end(); ++it)
@@ -488,12 +495,30 @@ class GpuExecutor : public muxsim::JobExecutor {
       auto r = row_of_id_.find(job.global_ids[i]);
       if (r != row_of_id_.end()) tokens_[r->second].push_back(out[i]);
     }
+    if (job.start) {
+      float a = 0.f, b = 0.f;
+      check(cudaEventElapsedTime(&a, t0_ev_, job.start));
+      check(cudaEventElapsedTime(&b, t0_ev_, job.done));
+      timeline_ << job.llm << ',' << (job.decode ? "decode" : "prefill") << ',' << job.global_ids.size() << ','
+                << a + job.skipped_ms << ',' << b + job.skipped_ms << '\n';
+      cudaEventDestroy(job.start);
+    }
     cudaEventDestroy(job.done);
     spare_out_.push_back(std::move(job.out));
     jobs_.erase(it);
   }
 
-  void detach_unit(int) override { check(cudaDeviceSynchronize()); }
+  void detach_unit(int) override {
+    check(cudaDeviceSynchronize());
+    if (trace_) {
+      std::FILE* f = std::fopen(std::getenv("MUX_RT_TIMELINE"), "w");
+      if (f) {
+        std::fputs("llm,kind,batch,start_ms,end_ms\n", f);
+        std::fputs(timeline_.str().c_str(), f);
+        std::fclose(f);
+      }
+    }
+  }
 
   const std::vector<std::vector<int32_t>>& tokens() const { return tokens_; }
 
@@ -505,6 +530,7 @@ class GpuExecutor : public muxsim::JobExecutor {
     std::unique_ptr<mux::PinnedMem> out;
     cudaEvent_t done = nullptr;
     double skipped_ms = 0.0;  // real-time mode: idle time skipped before the launch
+    cudaEvent_t start = nullptr;  // MUX_RT_TIMELINE: when the job's stream reached it
     // align_decode: a held decode job (not yet on the device), the jobs it
     // waits for, and what its enqueue needs
     bool decode = false, held = false;
@@ -522,6 +548,7 @@ class GpuExecutor : public muxsim::JobExecutor {
       for (int64_t w : jb.wait_for) ready = ready && jobs_.find(w) == jobs_.end();
       if (!ready) continue;
       cudaStream_t s = u_->streams[jb.part];
+      if (jb.start) check(cudaEventRecord(jb.start, s));
       u_->rt->decode(*u_->models[jb.llm], *u_->ws[jb.part], static_cast<int>(jb.slots.size()), jb.slots.data(),
                      jb.aux.data(), nullptr, jb.out->as<int32_t>(), s, nullptr);
       check(cudaEventRecord(jb.done, s));
@@ -546,6 +573,10 @@ class GpuExecutor : public muxsim::JobExecutor {
   double skipped_ms_ = 0.0;
   std::vector<int64_t> inflight_;
   std::vector<std::unique_ptr<mux::PinnedMem>> spare_out_;
+  // debug: MUX_RT_TIMELINE=<csv> writes every real-time job's device
+  // start / end (ms from the run's origin) at detach
+  bool trace_ = std::getenv("MUX_RT_TIMELINE") != nullptr;
+  std::ostringstream timeline_;
 };
 
 }  // namespace
