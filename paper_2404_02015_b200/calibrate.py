@@ -26,8 +26,10 @@ batch x context, and a partial SM share slows it as f^-0.6, not flat then
     decode   = (decode_fixed_ms + decode_row_ms * b + decode_bctx_ms * b * ctx)
                * scale * f^-decode_sm_exponent / tp_speedup
 
-and adds its three keys to the profile (wire.HBM_KEYS); a config holding
-them prices decode that way, one without them is the reference's model.
+and, with hbm=True, adds its four keys (wire.HBM_KEYS). main() writes them
+as a separate "profile_hbm" object: the reference's config.cpp rejects
+unknown profile keys, so "profile" stays a reference block; merged into
+"profile" for this framework's CLI (wire.load_config), they select the form.
 
 The output's "profile" object drops into a reference config unchanged
 (config.cpp "profile" section; wire.load_config reads it too). tp_efficiency
@@ -166,8 +168,9 @@ def fit_sm_exponent(points):
     return e, err
 
 
-def fit_profile(prefill_pts, decode_pts, sm_pts, num_layers, hidden):
-    """All measurements of one model -> the LatencyProfile dict + fit report."""
+def fit_profile(prefill_pts, decode_pts, sm_pts, num_layers, hidden, hbm=False):
+    """All measurements of one model -> the LatencyProfile dict + fit report
+    (hbm=True: plus the HBM-bound decode form's keys and fit errors)."""
     scale = model_scale(num_layers, hidden)
     pf = fit_prefill(prefill_pts, scale)
     base, ctx, knee, derr = fit_decode(decode_pts, scale)
@@ -177,6 +180,8 @@ def fit_profile(prefill_pts, decode_pts, sm_pts, num_layers, hidden):
                  "batch_knee": knee, "sm_saturation_point": fsat})
     perr = math.sqrt(sum((pf * scale * t / ms - 1.0) ** 2 for t, ms in prefill_pts) / len(prefill_pts))
     err = {"prefill_rel_rms": perr, "decode_rel_rms": derr, "sm_rel_rms": serr}
+    if not hbm:
+        return prof, err
     try:
         hbase, hrow, hbctx, herr = fit_decode_hbm(decode_pts, scale)
     except ValueError:
@@ -295,8 +300,10 @@ def main(argv=None) -> int:
     ap.add_argument("-o", "--output", default="b200_profile.json")
     a = ap.parse_args(argv)
     m = measure(a.model)
-    prof, err = fit_profile(m["prefill"], m["decode"], m["sm_share"], m["num_layers"], m["hidden"])
-    out = {"profile": prof, "fit": err, "measurements": m,
+    prof, err = fit_profile(m["prefill"], m["decode"], m["sm_share"], m["num_layers"], m["hidden"], hbm=True)
+    from .wire import HBM_KEYS
+    prof_hbm = {k: prof.pop(k) for k in HBM_KEYS if k in prof}
+    out = {"profile": prof, "profile_hbm": prof_hbm, "fit": err, "measurements": m,
            "notes": {"tp_efficiency": "default 0.9: needs a multi-GPU mesh (one-GPU box)",
                      "method": "CUDA events around back-to-back jobs on one stream; decode KV random, "
                                "prefill single request of N tokens; SM share = green-context partition"}}

@@ -1,7 +1,7 @@
 """`muxsim simulate` drop-in:
 
     python -m paper_2404_02015_b200.muxsim_cli -c cfg.json -p plan.json -t trace.csv -o out/ \\
-        [--engine priced|lockstep|measured]
+        [--engine priced|lockstep|measured|realtime]
 
 Reads the reference's config / plan.json / trace.csv and writes records.csv,
 metrics.json and poolstats.json in the reference's formats
@@ -12,6 +12,8 @@ Engines:
   lockstep  the same decisions, every job executed on this GPU (random-init
             weights, synthetic prompt tokens); records identical to priced
   measured  job completions at measured device time (real serving latencies)
+  realtime  jobs overlap across passes, completions when their device events
+            fire (mux_unit_run_realtime; concurrency and contention measured)
 The GPU engines serve single-unit, single-GPU plans (one B200).
 Exit codes follow the reference CLI (muxsim.cpp:51-63): 1 config error,
 2 infeasible, 3 anything else.
@@ -47,7 +49,7 @@ def run(cfg_path: str, plan_path: str, trace_path: str, out_dir: str, engine: st
         try:
             recs, _ = unit.run_lockstep([exp.entries[i] for i in placement.members[0]], trace,
                                         exp.gpu_memory_bytes, exp.params, profile=exp.profile,
-                                        measured=engine == "measured")
+                                        measured=engine == "measured", realtime=engine == "realtime")
             units = unit.last_stats()
             mem = placement.members[0]  # unit-local entry index -> config entry index
             for u in units:
@@ -72,7 +74,7 @@ def main(argv=None) -> int:
     ap.add_argument("-p", "--plan", required=True)
     ap.add_argument("-t", "--trace", required=True)
     ap.add_argument("-o", "--output", default="out")
-    ap.add_argument("--engine", choices=["priced", "lockstep", "measured"], default="priced")
+    ap.add_argument("--engine", choices=["priced", "lockstep", "measured", "realtime"], default="priced")
     a = ap.parse_args(argv)
     try:
         recs = run(a.config, a.plan, a.trace, a.output, a.engine)

@@ -47,7 +47,8 @@ def main():
     ap.add_argument("--measured-from", default=None,
                     help="FILE:KEY of an earlier output whose measured_b200 summary (same trace) is reused")
     a = ap.parse_args()
-    prof = json.load(open(a.profile))["profile"]
+    pj = json.load(open(a.profile))
+    prof = dict(pj["profile"], **pj.get("profile_hbm", {}))
     prof_list = [prof[k] for k in wire.PROFILE_KEYS]
     models = a.models.split(",")
     rates = [float(x) for x in a.rates.split(",")]
