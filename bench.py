@@ -182,6 +182,8 @@ def run_ours(args, rank, world, local_rank):
     unit.set_option("l2_next", args.l2_next)
     unit.set_option("fuse_norm", args.fuse_norm)
     unit.set_option("fuse_k2", args.fuse_k2)
+    if args.gemm_min_iters > 0:
+        unit.set_option("gemm_min_iters", args.gemm_min_iters)
     unit.init_kv(seed=7 + rank, std=1.0)
     pool = unit.pool
     ids = []
@@ -308,6 +310,8 @@ def main():
                     help="RMSNorm fused into the residual GEMMs on green partitions (grid barrier)")
     ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch between job kernels")
     ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg (profiling runs)")
+    ap.add_argument("--gemm-min-iters", type=int, default=0,
+                    help="decode GEMM k-blocks-per-CTA floor (0 = the runtime default)")
     args = ap.parse_args()
 
     rank = int(os.environ.get("RANK", "0"))

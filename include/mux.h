@@ -330,7 +330,7 @@ MUX_API int mux_unit_partition_sms(mux_unit* unit, int partition, int* sms);
 MUX_API int mux_unit_probe_smids(mux_unit* unit, int partition, int blocks, int* out);
 /* Kernel launches issued by this unit so far (all libmux kernels). */
 MUX_API int64_t mux_unit_launches(mux_unit* unit);
-/* Tuning knobs: "gemm_min_iters" (k-blocks per GEMM CTA, default 24);
+/* Tuning knobs: "gemm_min_iters" (k-blocks per GEMM CTA floor, default 8);
  * "pdl" (programmatic dependent launch between job kernels, default 1);
  * "chain" (decode layers as one fused persistent layer-chain launch plus
  * K1, default 0 = one launch per projection / element-wise step);

@@ -229,7 +229,7 @@ class Runtime {
   int64_t pool_blocks_;
   int max_pos_;
   int64_t launches_ = 0;
-  int gemm_min_iters_ = 24;
+  int gemm_min_iters_ = 8;  // scripts/min_iters_sweep.py: 8 is never slower on the whole GPU, -6..-11% at batch 128
   bool chain_enabled_ = false;
   bool fuse_qkv_ = false;  // K2 in the QKV GEMM epilogue (kQkvRope): measured slower than kv_append
   int l2_next_ = 0;        // tiles per CTA of the next decode GEMM prefetched into L2 (0 = off)
