@@ -521,3 +521,8 @@ def test_muxsim_cli_lockstep_on_gpu_matches_reference_outputs(cuda, tmp_path):
     exp = wire.load_config(os.path.join(g, "cfg_pair.json"))
     assert len((tmp_path / "m" / "records.csv").read_text().splitlines()) == 41
     assert exp.names == ["chat-7b", "chat-13b"]
+    # real-time engine: same files and schema, every request recorded
+    assert muxsim_cli.main(args + ["-o", str(tmp_path / "rt"), "--engine", "realtime"]) == 0
+    rj = json.loads((tmp_path / "rt" / "metrics.json").read_text())
+    assert list(rj) == list(mj) and [m["name"] for m in rj["models"]] == ["chat-7b", "chat-13b"]
+    assert len((tmp_path / "rt" / "records.csv").read_text().splitlines()) == 41
