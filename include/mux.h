@@ -141,6 +141,10 @@ typedef struct {
    * (B200 extension,
    * LatencyProfile::decode_form 1; DESIGN §4 "measured latency profile"). */
   const double* decode_hbm;
+  /* NULL: QuotaAdaptParams defaults. Else 3 doubles {low_mark, high_mark,
+   * step_frac} (kv_manager.hpp QuotaAdaptParams; config keys
+   * sim.quota_low_mark / quota_high_mark / quota_step_frac, config.cpp:242-244). */
+  const double* quota_adapt;
 } mux_sim_config;
 
 typedef struct {

@@ -14,7 +14,9 @@
  * and the physical table layout of this repo's pool (csrc/include/mux/kv.hpp):
  *   rowlist[slot][row] -> row record; rowrec[rec][(layer*H + head)*2 + kv].
  *
- * Build: gcc -O3 -ffast-math -march=x86-64-v3 -shared -fPIC -pthread numerics_ref.c -o _build/libnumerics_ref.so
+ * Build: gcc -O3 -march=x86-64-v3 -shared -fPIC -pthread numerics_ref.c -o _build/libnumerics_ref.so
+ * (no -ffast-math: the attention restatement relies on IEEE -INFINITY / exp
+ * semantics, and the summation orders below are the ones written).
  */
 #include <math.h>
 #include <pthread.h>
@@ -125,11 +127,17 @@ typedef struct {
   int B, N, K, next; pthread_mutex_t mu;
 } gemv_job;
 
-/* fp32 dot product; -ffast-math lets the compiler vectorise the reduction. */
+/* fp32 dot product over 16 independent lane sums (a fixed order the
+ * compiler can vectorise without -ffast-math), then a fixed lane reduction. */
 static float dot_f32(const float* a, const float* b, int n) {
-  float acc = 0.f;
-  for (int i = 0; i < n; ++i) acc += a[i] * b[i];
-  return acc;
+  float acc[16] = {0};
+  int i = 0;
+  for (; i + 16 <= n; i += 16)
+    for (int l = 0; l < 16; ++l) acc[l] += a[i + l] * b[i + l];
+  for (; i < n; ++i) acc[i & 15] += a[i] * b[i];
+  float s = 0.f;
+  for (int l = 0; l < 16; ++l) s += acc[l];
+  return s;
 }
 
 static void* gemv_worker(void* arg) {

@@ -15,7 +15,7 @@ def build_numerics() -> str:
     src = os.path.join(HERE, "numerics_ref.c")
     if not os.path.exists(NUMERICS_SO) or os.path.getmtime(NUMERICS_SO) < os.path.getmtime(src):
         os.makedirs(BUILD, exist_ok=True)
-        subprocess.check_call(["gcc", "-O3", "-ffast-math", "-march=x86-64-v3", "-shared", "-fPIC", "-pthread", src,
+        subprocess.check_call(["gcc", "-O3", "-march=x86-64-v3", "-shared", "-fPIC", "-pthread", src,
                                "-o", NUMERICS_SO, "-lm"])
     return NUMERICS_SO
 

@@ -58,7 +58,8 @@ class SimConfig(C.Structure):
                 ("kappa", f64), ("quota_period_s", f64), ("token_budget", i64),
                 ("block_tokens", C.c_int), ("warmup_s", f64), ("decode_sm", f64),
                 ("prefill_min_sm", f64), ("activation_reserve_frac", f64),
-                ("quota_floor_frac", f64), ("decode_hbm", P(f64))]
+                ("quota_floor_frac", f64), ("decode_hbm", P(f64)),
+                ("quota_adapt", P(f64))]
 
 
 class Request(C.Structure):

@@ -12,6 +12,8 @@
 #include <cstdlib>
 #include <cstring>
 #include <deque>
+#include <map>
+#include <mutex>
 #include <memory>
 #include <stdexcept>
 #include <sstream>
@@ -201,6 +203,11 @@ SimInputs build_inputs(const mux_sim_config* c, int n_entries, const mux_llm_ent
   in.params.prefill_min_sm = c->prefill_min_sm;
   in.params.activation_reserve_frac = c->activation_reserve_frac;
   in.params.quota_floor_frac = c->quota_floor_frac;
+  if (c->quota_adapt) {
+    in.params.adapt.low_mark = c->quota_adapt[0];
+    in.params.adapt.high_mark = c->quota_adapt[1];
+    in.params.adapt.step_frac = c->quota_adapt[2];
+  }
   return in;
 }
 
@@ -930,19 +937,31 @@ int mux_gemm_bf16(const void* x, const void* w, int w_tiled, int M, int N, int K
     require(M > 0 && N > 0 && K > 0 && K % 8 == 0 && N % 8 == 0, "gemm: bad shape");
     require(epilogue >= 0 && epilogue <= 3, "gemm: bad epilogue");
     require(epilogue != 2 || N % 16 == 0, "gemm: SiLU epilogue needs N % 16 == 0");
-    // Process-wide stream-K scratch for direct calls (tests); the runtime
-    // gives every partition its own.
-    static float* partials = nullptr;
-    static int* flags = nullptr;
-    static int epoch = 0;
+    // Stream-K scratch for direct calls (tests), one set per device (the
+    // runtime gives every partition its own). Calls on one device are
+    // serialised by the caller's stream order, as with any shared scratch.
+    struct Scratch {
+      float* partials = nullptr;
+      int* flags = nullptr;
+      int epoch = 0;
+    };
+    static std::mutex mu;
+    static std::map<int, Scratch> per_dev;
     constexpr int kMaxGrid = 1024;
-    if (partials == nullptr) {
-      mux::check_cuda(cudaMalloc(&partials, mux::gemm_partials_floats(kMaxGrid) * 4), "gemm scratch");
-      mux::check_cuda(cudaMalloc(&flags, kMaxGrid * 4), "gemm flags");
-      mux::check_cuda(cudaMemset(flags, 0, kMaxGrid * 4), "gemm flags");
+    int dev = 0;
+    mux::check_cuda(cudaGetDevice(&dev), "gemm device");
+    std::lock_guard<std::mutex> lk(mu);
+    Scratch& sc = per_dev[dev];
+    if (sc.partials == nullptr) {
+      mux::check_cuda(cudaMalloc(&sc.partials, mux::gemm_partials_floats(kMaxGrid) * 4), "gemm scratch");
+      mux::check_cuda(cudaMalloc(&sc.flags, kMaxGrid * 4), "gemm flags");
+      mux::check_cuda(cudaMemset(sc.flags, 0, kMaxGrid * 4), "gemm flags");
     }
+    float* partials = sc.partials;
+    int* flags = sc.flags;
+    int& epoch = sc.epoch;
     int sms = 148;
-    cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, 0);
+    mux::check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "gemm SM count");
     alignas(64) unsigned char tw[128], tx[128], to[128], tx128[128];
     const int n_tile = mux::gemm_pick_n_tile(M);
     if ((!w_tiled && !mux::make_tmap_bf16(tw, w, N, K, static_cast<uint64_t>(K) * 2, 128)) ||
@@ -991,6 +1010,8 @@ int mux_unit_create(const mux_unit_config* cfg, mux_unit** out) {
     for (int i = 0; i < cfg->n_llms; ++i) {
       const mux_llm_entry& e = cfg->llms[i];
       // the reference planner never checks head divisibility.
+      require(e.head_dim == 128 && e.bytes_per_element == 2,
+              "unit: the kernels serve head_dim 128, bf16 (4 KiB head-blocks of 16 tokens)");
       require(e.num_heads % tp == 0 && e.ffn % tp == 0,
               "unit: heads and ffn must be divisible by tp_size (reference planner emits e.g. 30b at tp 8)");
       u->specs.push_back(spec_of(e));
@@ -1324,6 +1345,10 @@ int run_unit(mux_unit* u, const mux_sim_config* cfg, int n_entries, const mux_ll
              bool measured, bool realtime = false) {
   return guarded([&] {
     require(cfg->n_units == 1, "lockstep: single-unit placements only");
+    // The kernels address 16-token head-blocks of 128 bf16 dims (4 KiB,
+    // kv_manager.cpp:37-40 at the catalog's geometry); the host pool must
+    // build rows of the same size.
+    require(cfg->block_tokens == 16, "GPU engines: block_tokens must be 16 (the kernels' head-block geometry)");
     require(n_entries == static_cast<int>(u->models.size()), "lockstep: entries must describe the unit's models");
     SimInputs in = build_inputs(cfg, n_entries, entries, n_requests, trace);
     u->passes = u->green_passes = 0;

@@ -231,7 +231,7 @@ bool Llama::get_tensor(const std::string& name, int layer, void* host, size_t by
 
 Workspace::Workspace(int max_tok, int max_batch_rows, int hidden, int qkv_cols, int ffn, int vocab,
                      int heads, int max_decode_batch, int grid)
-    : max_tokens(max_tok), max_hidden(hidden), max_qkv(qkv_cols), max_ffn(ffn), max_vocab(vocab),
+    : max_tokens(max_tok), max_decode(max_decode_batch), max_hidden(hidden), max_qkv(qkv_cols), max_ffn(ffn), max_vocab(vocab),
       max_heads(heads) {
   const size_t T = std::max(max_tok, 16);
   // Activation buffers get >= 256 rows so any n_tile box stays in bounds.
@@ -255,7 +255,7 @@ Workspace::Workspace(int max_tok, int max_batch_rows, int hidden, int qkv_cols, 
   const size_t rows_out = std::max<size_t>(max_batch_rows, 256);
   logits = DevMem(rows_out * vocab * 4);
   xlast = DevMem(rows_out * hidden * 2);
-  const size_t kv_splits = 16;
+  const size_t kv_splits = kMaxKvSplits;
   attn_part_o = DevMem(static_cast<size_t>(max_decode_batch) * heads * kv_splits * 128 * 4);
   attn_part_ml = DevMem(static_cast<size_t>(max_decode_batch) * heads * kv_splits * 2 * 4);
   attn_split_count = DevMem(static_cast<size_t>(max_decode_batch) * heads * 4);
@@ -486,6 +486,7 @@ void Runtime::row_parallel_norm(const void* w_tiled, const void* x, int M, int N
 }
 
 void Runtime::upload_rows(muxsim::BlockPool& bp, int llm, Llama& m, cudaStream_t stream) {
+  check_cuda(cudaSetDevice(device_), "cudaSetDevice");  // units of one process may sit on different GPUs
   std::vector<muxsim::RowDelta>& pend = bp.pending_rows(llm);
   if (pend.empty()) return;
   const int W = m.row_width();
@@ -543,7 +544,10 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
                      const int32_t* tokens_host, int32_t* out_host, cudaStream_t stream,
                      AttnTimer* timer) {
   if (n <= 0) return;
-  if (n > ws.max_tokens) throw std::invalid_argument("decode: batch exceeds workspace");
+  check_cuda(cudaSetDevice(device_), "cudaSetDevice");  // units of one process may sit on different GPUs
+  if (n > ws.max_tokens || n > ws.max_decode)
+    throw std::invalid_argument("decode: batch of " + std::to_string(n) + " exceeds the unit's max_batch " +
+                                std::to_string(ws.max_decode));
   const ModelDims& d = m.dims();
   const int T = std::max(ws.max_tokens, 16);
   int32_t* h = ws.stage_begin();
@@ -598,8 +602,12 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   // KV splits: enough CTAs to fill the GPU a few times over.
   int splits = 1;
   // (the last split merges in-kernel, so small batches can afford ~2 rows per split)
-  while (splits < 16 && n * H * splits < 4 * ws.sms && (max_rows_req + splits * 2 - 1) / (splits * 2) >= 2) splits *= 2;
+  while (splits < kMaxKvSplits && n * H * splits < 4 * ws.sms && (max_rows_req + splits * 2 - 1) / (splits * 2) >= 2)
+    splits *= 2;
   while ((max_rows_req + splits - 1) / splits > decode_attention_max_rows_per_split()) splits *= 2;
+  if (splits > kMaxKvSplits)  // the split scratch holds kMaxKvSplits per (member, head)
+    throw std::invalid_argument("decode: context of " + std::to_string(max_ctx) + " tokens exceeds K1's " +
+                                std::to_string(kMaxKvSplits * decode_attention_max_rows_per_split() * 16));
   at.splits = splits;
   at.rows_per_split = std::max(1, (max_rows_req + splits - 1) / splits);
   at.scale_log2 = 1.4426950408889634f / std::sqrt(128.f);
@@ -777,6 +785,7 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
 void Runtime::prefill(Llama& m, Workspace& ws, int n, const int32_t* slots_host, const int32_t* lens_host,
                       const int32_t* tokens_host, int32_t* out_host, cudaStream_t stream) {
   if (n <= 0) return;
+  check_cuda(cudaSetDevice(device_), "cudaSetDevice");  // units of one process may sit on different GPUs
   const ModelDims& d = m.dims();
   int T = 0;
   for (int i = 0; i < n; ++i) T += lens_host[i];

@@ -130,6 +130,7 @@ struct TpLink {
 // Per-partition scratch for one running job.
 struct Workspace {
   int max_tokens = 0;    // prefill token budget or max decode batch
+  int max_decode = 0;    // decode members the K1 split scratch is sized for
   int max_hidden = 0, max_qkv = 0, max_ffn = 0, max_vocab = 0, max_heads = 0;
   DevMem resid, xn, qkv, q, attn, act, logits, ints, attn_part_o, attn_part_ml, attn_split_count, xlast;
   DevMem gemm_partials, gemm_flags;  // stream-K fixup scratch of this partition's GEMMs

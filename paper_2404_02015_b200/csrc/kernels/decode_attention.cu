@@ -403,14 +403,12 @@ __global__ void __launch_bounds__(128) decode_attention_combine(const DecodeAttn
 template <int S, typename OutT>
 cudaError_t launch_decode(const DecodeAttnArgs& a, cudaStream_t stream) {
   const size_t smem = sizeof(AttnSmem<S>);
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(decode_attention_kernel<S, OutT>,
-                                         cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(smem));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static PerDeviceOnce configured;
+  cudaError_t ce = configured.run([&] {
+    return cudaFuncSetAttribute(decode_attention_kernel<S, OutT>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(smem));
+  });
+  if (ce != cudaSuccess) return ce;
   dim3 grid(a.splits, a.H, a.B);
   cudaError_t e = launch(decode_attention_kernel<S, OutT>, grid, dim3(kThreads), smem, stream, a);
   if (e == cudaSuccess && a.splits > 1 && a.split_count == nullptr)

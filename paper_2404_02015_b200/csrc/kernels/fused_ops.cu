@@ -99,6 +99,8 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_rows_kernel(const float* 
   }
 }
 
+constexpr unsigned long long kTpSpinTimeoutNs = 20ull * 1000 * 1000 * 1000;  // 20 s
+
 template <int kVec>
 __global__ void __launch_bounds__(kRowThreads) rmsnorm_tp_kernel(float* resid, const float* parts, int64_t part_stride,
                                                                  int tp, const int* counter, uint32_t expected,
@@ -107,12 +109,20 @@ __global__ void __launch_bounds__(kRowThreads) rmsnorm_tp_kernel(float* resid, c
   __shared__ float scratch[32];
   grid_dep_wait();
   if (threadIdx.x == 0) {
-    // every rank's GEMM CTAs have stored their partials and signalled
+    // every rank's GEMM CTAs have stored their partials and signalled; a
+    // peer that never signals (dead rank, mismatched launch) aborts the
+    // kernel after kTpSpinTimeoutNs instead of hanging the GPU: __trap()
+    // turns it into a launch failure the host reports.
+    unsigned long long t0;
+    asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t0));
     for (;;) {
       uint32_t v;
       asm volatile("ld.acquire.sys.global.u32 %0, [%1];" : "=r"(v) : "l"(counter) : "memory");
       if (static_cast<int32_t>(v - expected) >= 0) break;
       __nanosleep(64);
+      unsigned long long t;
+      asm volatile("mov.u64 %0, %globaltimer;" : "=l"(t));
+      if (t - t0 > kTpSpinTimeoutNs) __trap();
     }
   }
   __syncthreads();

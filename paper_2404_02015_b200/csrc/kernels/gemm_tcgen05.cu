@@ -895,12 +895,10 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
     r.norm_target = a.norm_base + static_cast<unsigned>(grid);
     r.norm_eps = a.norm_eps;
   }
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static PerDeviceOnce configured;
+  cudaError_t ce = configured.run(
+      [] { return cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448); });
+  if (ce != cudaSuccess) return ce;
   r.n_peers = a.n_peers;
   r.n_signal = a.n_signal;
   for (int d = 0; d < kMaxTp; ++d) r.signal[d] = a.signal[d];

@@ -66,6 +66,7 @@ cudaError_t table_update(const TableUpdateArgs& a, cudaStream_t stream);
 // Weight-stationary tiling: every CTA owns 128 rows of W (one UMMA M=128
 // tile) and up to 256 activation rows (UMMA N), so decode batches (M <= 256)
 // stream each weight byte exactly once.
+constexpr int kMaxKvSplits = 16;  // K1 context splits per (member, head): the workspace's split scratch
 constexpr int kMaxTp = 8;  // tensor-parallel ranks of one mesh (node-local)
 
 enum class Epilogue : int {

@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <mutex>
 #include <utility>
 
 namespace mux {
@@ -23,6 +24,29 @@ inline cudaError_t preload(K... kernels) {
   ((err = err == cudaSuccess ? cudaFuncGetAttributes(&attr, reinterpret_cast<const void*>(kernels)) : err), ...);
   return err;
 }
+
+// Kernel attributes (cudaFuncSetAttribute) are per device: a process that
+// drives units on several GPUs must set them once on EACH device it launches
+// on. Returns the first error of f() on the current device.
+class PerDeviceOnce {
+ public:
+  template <typename F>
+  cudaError_t run(F&& f) {
+    int dev = 0;
+    cudaError_t e = cudaGetDevice(&dev);
+    if (e != cudaSuccess) return e;
+    if (dev < 0 || dev >= 64) return cudaErrorInvalidDevice;
+    std::lock_guard<std::mutex> lk(mu_);
+    if (done_ & (1ull << dev)) return cudaSuccess;
+    e = f();
+    if (e == cudaSuccess) done_ |= 1ull << dev;
+    return e;
+  }
+
+ private:
+  std::mutex mu_;
+  unsigned long long done_ = 0;
+};
 
 template <typename... P, typename... A>
 inline cudaError_t launch(void (*kernel)(P...), dim3 grid, dim3 block, size_t smem, cudaStream_t stream,

@@ -378,13 +378,12 @@ cudaError_t preload_prefill_attention() { return preload(prefill_attention_kerne
 
 cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
   if (a.T <= 0 || a.n_tiles <= 0) return cudaSuccess;
-  static bool configured = false;
-  if (!configured) {
-    cudaError_t e = cudaFuncSetAttribute(prefill_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmemBytes));
-    if (e != cudaSuccess) return e;
-    configured = true;
-  }
+  static PerDeviceOnce configured;
+  cudaError_t ce = configured.run([] {
+    return cudaFuncSetAttribute(prefill_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kSmemBytes));
+  });
+  if (ce != cudaSuccess) return ce;
   CUtensorMap tq, tkv;
   std::memcpy(&tq, a.tmap_q, sizeof(CUtensorMap));
   std::memcpy(&tkv, a.tmap_qkv, sizeof(CUtensorMap));

@@ -242,6 +242,11 @@ class EngineParams:
     prefill_min_sm: float = 0.3
     activation_reserve_frac: float = 0.1
     quota_floor_frac: float = 0.02
+    # QuotaAdaptParams (kv_manager.hpp; config sim.quota_low_mark /
+    # quota_high_mark / quota_step_frac, config.cpp:242-244)
+    quota_low_mark: float = 0.5
+    quota_high_mark: float = 0.9
+    quota_step_frac: float = 0.1
 
 
 @dataclass
@@ -281,11 +286,13 @@ def _build_config(gpu_memory_bytes: int, num_gpus: int, placement: Placement, pa
         raise ValueError("profile: 7 reference values, or 7 + 4 HBM decode-form values")
     prof = None if profile is None else (C.c_double * 7)(*profile[:7])
     hbm = None if profile is None or len(profile) == 7 else (C.c_double * 4)(*profile[7:])
-    keep += [sizes, placed, prof, hbm]
+    adapt = (C.c_double * 3)(params.quota_low_mark, params.quota_high_mark, params.quota_step_frac)
+    keep += [sizes, placed, prof, hbm, adapt]
     cfg = SimConfig(1, num_gpus, gpu_memory_bytes, len(placement.mesh_sizes), sizes, len(placed_list),
                     placed, prof, params.scheduler, params.kappa, params.quota_period_s,
                     params.token_budget, params.block_tokens, params.warmup_s, params.decode_sm,
-                    params.prefill_min_sm, params.activation_reserve_frac, params.quota_floor_frac, hbm)
+                    params.prefill_min_sm, params.activation_reserve_frac, params.quota_floor_frac, hbm,
+                    adapt)
     return _Built(cfg, keep)
 
 

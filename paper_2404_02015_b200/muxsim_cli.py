@@ -41,9 +41,12 @@ def run(cfg_path: str, plan_path: str, trace_path: str, out_dir: str, engine: st
             raise wire.ConfigError("GPU engines serve a single-unit, single-GPU plan")
         specs = [exp.entries[i].spec for i in placement.members[0]]
         weights = sum(s.weight_bytes for s in specs)
-        logical = (exp.gpu_memory_bytes - weights - round(exp.params.activation_reserve_frac * exp.gpu_memory_bytes)) // 4096
+        if exp.params.block_tokens != 16:
+            raise wire.ConfigError("GPU engines: sim.block_tokens must be 16 (the kernels' 4 KiB head-blocks)")
+        block_bytes = 128 * exp.params.block_tokens * 2  # head_dim * block_tokens * bpe (kv_manager.cpp:37-40)
+        logical = (exp.gpu_memory_bytes - weights - round(exp.params.activation_reserve_frac * exp.gpu_memory_bytes)) // block_bytes
         longest = max((r.prompt_len + r.output_len for r in trace), default=16)
-        unit = Unit(specs, pool_blocks=logical, device_pool_blocks=min(logical, 20_000_000), max_batch=512,
+        unit = Unit(specs, pool_blocks=logical, device_pool_blocks=logical, max_batch=512,
                     max_prefill_tokens=max(exp.params.token_budget, longest), max_ctx=longest + 16,
                     max_slots=len(trace) + 8, init_seed=1, init_std=0.02, partitions=len(specs) + 1)
         try:

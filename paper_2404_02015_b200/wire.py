@@ -57,17 +57,100 @@ class Experiment:
     slo_reference_tp_one: bool = False                                           # config.hpp:60
 
 
-def _mean_len(d, what):
-    kind = d.get("kind")
+def _fail(msg):
+    raise ConfigError("config: " + msg)
+
+
+def _check_keys(obj, ctx, allowed):
+    """config.cpp:28-39: unknown keys are errors."""
+    for k in obj:
+        if k not in allowed:
+            _fail(f"unknown key '{k}' in {ctx}")
+
+
+def _is_num(v):
+    return isinstance(v, (int, float)) and not isinstance(v, bool)
+
+
+def _num(obj, ctx, key, default=None, required=False):
+    if key not in obj:
+        if required:
+            _fail(f"{ctx} is missing required key '{key}'")
+        return default
+    v = obj[key]
+    if not _is_num(v):
+        _fail(f"{ctx}.{key} must be a number")
+    return float(v)
+
+
+def _int(obj, ctx, key, default=None, required=False):
+    if key not in obj:
+        if required:
+            _fail(f"{ctx} is missing required key '{key}'")
+        return default
+    v = obj[key]
+    if not isinstance(v, int) or isinstance(v, bool):
+        _fail(f"{ctx}.{key} must be an integer")
+    return int(v)
+
+
+def _num_list(v, where):
+    if not isinstance(v, list):
+        _fail(f"{where} must be an array of numbers")
+    for e in v:
+        if not _is_num(e):
+            _fail(f"{where} element must be a number")
+    return [float(e) for e in v]
+
+
+def _mean_len(d, ctx):
+    """parse_dist (config.cpp:106-125) + LengthDist::mean (workload.cpp:66-76):
+    the empirical mean is weighted."""
+    if not isinstance(d, dict):
+        _fail(f"{ctx} must be an object with a 'kind'")
+    if "kind" not in d:
+        _fail(f"{ctx} is missing required key 'kind'")
+    kind = d["kind"]
+    if not isinstance(kind, str):
+        _fail(f"{ctx}.kind must be a string")
     if kind == "constant":
-        return float(d["value"])
-    if kind in ("lognormal", "empirical"):
-        if "mean" in d:
-            return float(d["mean"])
-        vals = d.get("values") or []
-        if vals:
-            return sum(vals) / len(vals)
-    raise ConfigError(f"{what}: unsupported length distribution {d!r}")
+        _check_keys(d, ctx, ("kind", "value"))
+        v = _num(d, ctx, "value", required=True)
+        if not v >= 1.0:
+            raise ConfigError("length dist: constant value must be >= 1")
+        return v
+    if kind == "lognormal":
+        _check_keys(d, ctx, ("kind", "mean", "sigma"))
+        mean = _num(d, ctx, "mean", required=True)
+        sigma = _num(d, ctx, "sigma", 0.8)
+        if not mean >= 1.0:
+            raise ConfigError("length dist: lognormal mean must be >= 1")
+        if not sigma >= 0.0:
+            raise ConfigError("length dist: sigma must be >= 0")
+        return mean
+    if kind == "empirical":
+        _check_keys(d, ctx, ("kind", "values", "weights"))
+        if "values" not in d:
+            _fail(f"{ctx} is missing required key 'values'")
+        if "weights" not in d:
+            _fail(f"{ctx} is missing required key 'weights'")
+        vals = _num_list(d["values"], ctx + ".values")
+        ws = _num_list(d["weights"], ctx + ".weights")
+        if not vals or len(vals) != len(ws):
+            raise ConfigError("length dist: empirical values/weights must be non-empty and equal length")
+        total = acc = 0.0
+        for v, w in zip(vals, ws):
+            if not v >= 1.0:
+                raise ConfigError("length dist: empirical values must be >= 1")
+            if not w >= 0.0:
+                raise ConfigError("length dist: empirical weights must be >= 0")
+        for v, w in zip(vals, ws):  # workload.cpp:70-75, same summation order
+            total += w
+            acc += v * w
+        if not total > 0.0:
+            raise ConfigError("length dist: empirical weights must not all be zero")
+        return acc / total
+    _fail(f"{ctx}.kind must be constant, lognormal, or empirical")
 
 
 def gen_rates(n, alpha, max_rate):
@@ -78,76 +161,207 @@ def gen_rates(n, alpha, max_rate):
 
 
 def load_config(path: str, catalog: dict[str, LLMSpec] | None = None) -> Experiment:
+    """parse_config (config.cpp:260-321) over the keys the engine consumes,
+    with the reference's key, type and range checks (ConfigError = CLI exit 1)."""
     catalog = catalog or CATALOG
-    with open(path) as f:
-        try:
-            root = json.load(f)
-        except json.JSONDecodeError as e:
-            raise ConfigError(f"config: invalid JSON: {e}") from None
-    cl = root.get("cluster") or {}
     try:
-        num_nodes, gpn = int(cl["num_nodes"]), int(cl["gpus_per_node"])
-        mem = int(round(float(cl["gpu_memory_gb"]) * GIB))  # GiB (config.cpp:141)
-    except KeyError as e:
-        raise ConfigError(f"cluster: missing {e}") from None
-    llms = root.get("llms") or []
-    if not llms:
-        raise ConfigError("config: 'llms' must be a non-empty array")
-    wl = root.get("workload") or {}
-    rates = [float(m.get("rate_rps", 0.0)) for m in llms]
-    if "power_law" in wl:
-        pl = wl["power_law"]
-        rates = gen_rates(len(llms), float(pl["alpha"]), float(pl["max_rate_rps"]))
-    names, entries = [], []
-    for m, rate in zip(llms, rates):
-        model = m.get("model")
+        with open(path) as f:
+            text = f.read()
+    except OSError:
+        _fail(f"cannot open '{path}'")
+    try:
+        root = json.loads(text)
+    except json.JSONDecodeError as e:
+        _fail(f"invalid JSON: {e}")
+    if not isinstance(root, dict):
+        _fail("top level must be an object")
+    _check_keys(root, "config", ("cluster", "llms", "workload", "placement", "profile", "sim", "metrics",
+                                 "ablate", "outputs"))
+    if "cluster" not in root:
+        _fail("config is missing required key 'cluster'")
+    cl = root["cluster"]
+    if not isinstance(cl, dict):
+        _fail("cluster must be an object")
+    _check_keys(cl, "cluster", ("num_nodes", "gpus_per_node", "gpu_memory_gb"))
+    num_nodes = _int(cl, "cluster", "num_nodes", required=True)
+    gpn = _int(cl, "cluster", "gpus_per_node", required=True)
+    gb = _num(cl, "cluster", "gpu_memory_gb", required=True)
+    if gb <= 0.0:
+        _fail("cluster.gpu_memory_gb must be positive")
+    if num_nodes < 1 or gpn < 1:
+        _fail("cluster: num_nodes and gpus_per_node must be >= 1")
+    mem = int(round(gb * GIB))  # llround(gb * 2^30) (config.cpp:141)
+    if "llms" not in root:
+        _fail("config is missing required key 'llms'")
+    llms = root["llms"]
+    if not isinstance(llms, list) or not llms:
+        _fail("llms must be a non-empty array")
+    names, entries, seen = [], [], set()
+    for i, m in enumerate(llms):
+        ctx = f"llms[{i}]"
+        if not isinstance(m, dict):
+            _fail(ctx + " must be an object")
+        _check_keys(m, ctx, ("name", "model", "rate_rps", "prompt_len", "output_len"))
+        for k in ("name", "model"):
+            if k not in m:
+                _fail(f"{ctx} is missing required key '{k}'")
+            if not isinstance(m[k], str):
+                _fail(f"{ctx}.{k} must be a string")
+        name, model = m["name"], m["model"]
+        if not name or "," in name:
+            _fail(ctx + ".name must be non-empty and comma-free")
+        if name in seen:
+            _fail(f"duplicate model name '{name}'")
+        seen.add(name)
         if model not in catalog:
-            raise ConfigError(f"llm '{m.get('name')}': unknown model '{model}'")
+            _fail(f"{ctx}.model '{model}' is not in the catalog ({', '.join(catalog)})")
+        rate = _num(m, ctx, "rate_rps", 0.0)
+        if rate < 0.0:
+            _fail(ctx + ".rate_rps must be >= 0")
         spec = catalog[model]
-        name = m.get("name", model)
         names.append(name)
+        # LlmConfig defaults: constant 128 prompt / 64 output (config.hpp:26-27)
+        mp = _mean_len(m["prompt_len"], ctx + ".prompt_len") if "prompt_len" in m else 128.0
+        mo = _mean_len(m["output_len"], ctx + ".output_len") if "output_len" in m else 64.0
         entries.append(Entry(LLMSpec(name, spec.num_layers, spec.num_heads, spec.head_dim, spec.hidden_size,
                                      spec.weight_bytes, spec.bytes_per_element, spec.ffn, spec.vocab),
-                             rate, _mean_len(m.get("prompt_len", {"kind": "constant", "value": 1}), "prompt_len"),
-                             _mean_len(m.get("output_len", {"kind": "constant", "value": 1}), "output_len")))
+                             rate, mp, mo))
+    horizon, seed = 60.0, 0
+    wl = root.get("workload")
+    if wl is not None:
+        if not isinstance(wl, dict):
+            _fail("workload must be an object")
+        _check_keys(wl, "workload", ("horizon_s", "seed", "power_law"))
+        horizon = _num(wl, "workload", "horizon_s", horizon)
+        if horizon <= 0.0:
+            _fail("workload.horizon_s must be positive")
+        seed = _int(wl, "workload", "seed", 0)
+        if seed < 0:
+            _fail("workload.seed must be >= 0")
+        if "power_law" in wl:
+            pl = wl["power_law"]
+            if not isinstance(pl, dict):
+                _fail("workload.power_law must be an object")
+            _check_keys(pl, "workload.power_law", ("alpha", "max_rate_rps"))
+            alpha = _num(pl, "workload.power_law", "alpha", required=True)
+            mx = _num(pl, "workload.power_law", "max_rate_rps", required=True)
+            if alpha < 0.0:
+                _fail("workload.power_law.alpha must be >= 0")
+            if mx <= 0.0:
+                _fail("workload.power_law.max_rate_rps must be positive")
+            for e, r in zip(entries, gen_rates(len(entries), alpha, mx)):
+                e.rate = r
+    pc = root.get("placement")
+    if pc is not None:
+        if not isinstance(pc, dict):
+            _fail("placement must be an object")
+        _check_keys(pc, "placement", ("backend", "sm_list", "tp_list", "max_batch", "max_ilp_dims"))
+        if pc.get("backend", "greedy") not in ("greedy", "ilp"):
+            _fail("placement.backend must be greedy or ilp")
     prof = list(PROFILE_DEFAULTS)
     hbm = {}
-    for k, v in (root.get("profile") or {}).items():
-        if k in HBM_KEYS:
-            hbm[k] = float(v)
-            continue
-        if k not in PROFILE_KEYS:
-            raise ConfigError(f"profile: unknown key '{k}'")
-        prof[PROFILE_KEYS.index(k)] = float(v)
+    pr = root.get("profile")
+    if pr is not None:
+        if not isinstance(pr, dict):
+            _fail("profile must be an object")
+        _check_keys(pr, "profile", PROFILE_KEYS + HBM_KEYS)
+        for k in pr:
+            v = _num(pr, "profile", k)
+            if k in HBM_KEYS:
+                hbm[k] = v
+            else:
+                prof[PROFILE_KEYS.index(k)] = v
     if hbm:
         if len(hbm) != len(HBM_KEYS):
             raise ConfigError("profile: the HBM decode form needs " + ", ".join(HBM_KEYS))
         prof += [hbm[k] for k in HBM_KEYS]
+    # LatencyProfile::validate (cost_model.cpp:49-59), reported as ConfigError
+    pp, db, dc, tpe, sat, knee, rs = prof[:7]
+    if not (pp > 0.0 and db > 0.0 and dc >= 0.0):
+        _fail("latency profile: coefficients must be positive")
+    if not (tpe > 0.5 and tpe <= 1.0):
+        _fail("latency profile: tp_efficiency must be in (0.5, 1]")
+    if not (sat > 0.0 and sat <= 1.0):
+        _fail("latency profile: sm_saturation_point must be in (0, 1]")
+    if not knee >= 1.0:
+        _fail("latency profile: batch_knee must be >= 1")
+    if not rs > 0.0:
+        _fail("latency profile: reference_scale must be positive")
     p = EngineParams()
-    sim = root.get("sim") or {}
-    if "scheduler" in sim:
-        if sim["scheduler"] not in SCHEDULERS:
-            raise ConfigError(f"sim.scheduler: unknown '{sim['scheduler']}'")
-        p.scheduler = SCHEDULERS[sim["scheduler"]]
-    for k in ("kappa", "quota_period_s", "warmup_s", "decode_sm", "prefill_min_sm", "activation_reserve_frac",
-              "quota_floor_frac"):
-        if k in sim:
-            setattr(p, k, float(sim[k]))
-    for k in ("token_budget", "block_tokens"):
-        if k in sim:
-            setattr(p, k, int(sim[k]))
-    if "decode_sm" not in sim:
+    sim = root.get("sim")
+    decode_sm_set = False
+    tp_one = False
+    if sim is not None:
+        if not isinstance(sim, dict):
+            _fail("sim must be an object")
+        _check_keys(sim, "sim", ("scheduler", "kappa", "quota_period_s", "token_budget", "block_tokens",
+                                 "warmup_s", "decode_sm", "prefill_min_sm", "activation_reserve_frac",
+                                 "quota_floor_frac", "quota_low_mark", "quota_high_mark", "quota_step_frac",
+                                 "slo_reference_tp_one"))
+        if "scheduler" in sim:
+            sched = sim["scheduler"]
+            if sched not in ("adbs", "fcfs", "round_robin"):
+                _fail("sim.scheduler must be adbs, fcfs, or round_robin")
+            p.scheduler = SCHEDULERS[sched]
+        for k in ("kappa", "quota_period_s", "warmup_s", "decode_sm", "prefill_min_sm", "activation_reserve_frac",
+                  "quota_floor_frac"):
+            setattr(p, k, _num(sim, "sim", k, getattr(p, k)))
+        p.quota_low_mark = _num(sim, "sim", "quota_low_mark", p.quota_low_mark)
+        p.quota_high_mark = _num(sim, "sim", "quota_high_mark", p.quota_high_mark)
+        p.quota_step_frac = _num(sim, "sim", "quota_step_frac", p.quota_step_frac)
+        for k in ("token_budget", "block_tokens"):
+            setattr(p, k, _int(sim, "sim", k, getattr(p, k)))
+        decode_sm_set = "decode_sm" in sim
+        if "slo_reference_tp_one" in sim:
+            if not isinstance(sim["slo_reference_tp_one"], bool):
+                _fail("sim.slo_reference_tp_one must be a boolean")
+            tp_one = sim["slo_reference_tp_one"]
+        if p.kappa < 0.0:
+            _fail("sim.kappa must be >= 0")
+        if p.quota_period_s <= 0.0:
+            _fail("sim.quota_period_s must be positive")
+        if p.token_budget < 1:
+            _fail("sim.token_budget must be >= 1")
+        if p.block_tokens < 1:
+            _fail("sim.block_tokens must be >= 1")
+        if p.warmup_s < 0.0:
+            _fail("sim.warmup_s must be >= 0")
+        if p.decode_sm <= 0.0 or p.decode_sm > 1.0:
+            _fail("sim.decode_sm must be in (0, 1]")
+        if p.prefill_min_sm <= 0.0 or p.prefill_min_sm > 1.0:
+            _fail("sim.prefill_min_sm must be in (0, 1]")
+        if p.activation_reserve_frac < 0.0 or p.activation_reserve_frac >= 1.0:
+            _fail("sim.activation_reserve_frac must be in [0, 1)")
+    if not decode_sm_set:
         p.decode_sm = prof[PROFILE_KEYS.index("sm_saturation_point")]
-    exp = Experiment(num_nodes, gpn, mem, names, entries, p, prof, float(wl.get("horizon_s", 60.0)),
-                     int(wl.get("seed", 0)), {"root": root})
-    if exp.horizon_s <= 0.0:
-        raise ConfigError("workload.horizon_s must be positive")
-    scales = (root.get("metrics") or {}).get("slo_scales")
-    if scales is not None:
-        if not isinstance(scales, list) or not scales or any(float(x) <= 0.0 for x in scales):
-            raise ConfigError("metrics.slo_scales must be a non-empty list of positive numbers")
-        exp.slo_scales = [float(x) for x in scales]
-    exp.slo_reference_tp_one = bool(sim.get("slo_reference_tp_one", False))
+    exp = Experiment(num_nodes, gpn, mem, names, entries, p, prof, horizon, seed, {"root": root})
+    met = root.get("metrics")
+    if met is not None:
+        if not isinstance(met, dict):
+            _fail("metrics must be an object")
+        _check_keys(met, "metrics", ("slo_scales",))
+        if "slo_scales" in met:
+            scales = _num_list(met["slo_scales"], "metrics.slo_scales")
+            if not scales:
+                _fail("metrics.slo_scales must be non-empty")
+            if any(x <= 0.0 for x in scales):
+                _fail("metrics.slo_scales entries must be positive")
+            exp.slo_scales = scales
+    ab = root.get("ablate")
+    if ab is not None:
+        if not isinstance(ab, dict):
+            _fail("ablate must be an object")
+        _check_keys(ab, "ablate", ("rate_scales",))
+        if "rate_scales" in ab:
+            rsc = _num_list(ab["rate_scales"], "ablate.rate_scales")
+            if not rsc or any(x <= 0.0 for x in rsc):
+                _fail("ablate.rate_scales must be non-empty with positive entries")
+    out = root.get("outputs")
+    if out is not None:
+        if not isinstance(out, dict):
+            _fail("outputs must be an object")
+        _check_keys(out, "outputs", ("trace", "plan", "dir", "sweep"))
+    exp.slo_reference_tp_one = bool(tp_one)
     return exp
 
 

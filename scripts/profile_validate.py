@@ -84,7 +84,7 @@ def main():
     else:
         weights = sum(s.weight_bytes for s in specs)
         logical = (gpu_mem - weights - round(0.1 * gpu_mem)) // 4096
-        unit = mux.Unit(specs, pool_blocks=logical, device_pool_blocks=min(logical, 20_000_000), max_batch=512,
+        unit = mux.Unit(specs, pool_blocks=logical, device_pool_blocks=logical, max_batch=512,
                         max_prefill_tokens=4096, max_ctx=2048 + 64, max_slots=len(trace) + 8, init_seed=1,
                         init_std=0.02, partitions=len(specs) + 1)
         try:

@@ -79,7 +79,7 @@ def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, 
         if partition_sms is not None or len(pass_green) != len(specs):
             raise ValueError("pass_green takes one SM count per model and excludes partition_sms")
         n_parts, partition_sms = 2 * len(specs) + 1, [0] * (len(specs) + 1) + list(pass_green)
-    unit = mux.Unit(specs, pool_blocks=logical, device=device, device_pool_blocks=min(logical, 20_000_000),
+    unit = mux.Unit(specs, pool_blocks=logical, device=device, device_pool_blocks=logical,
                     max_batch=512, max_prefill_tokens=4096, max_ctx=2048 + 64, max_slots=len(trace) + 8,
                     init_seed=1, init_std=0.02, partitions=n_parts,
                     partition_sms=partition_sms)

@@ -9,7 +9,7 @@ MUX=../../../oracle/_ref/muxsim
 # (profiles/r01_b200_profile_7b.json); its plan comes from the reference's own planner.
 $MUX plan -c cfg_b200prof.json -o plan_b200prof.json > /dev/null
 cp trace_pair.csv trace_b200prof.csv
-for c in pair mesh b200prof; do
+for c in pair mesh b200prof empq; do
   [ $c = b200prof ] || $MUX gen-workload -c cfg_$c.json -o trace_$c.csv > /dev/null
   rm -rf out_$c
   $MUX simulate -c cfg_$c.json -p plan_$c.json -t trace_$c.csv -o out_$c > /dev/null

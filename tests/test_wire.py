@@ -11,7 +11,7 @@ from paper_2404_02015_b200 import muxsim_cli as simulate, wire
 G = os.path.join(os.path.dirname(__file__), "golden", "wire")
 
 
-@pytest.mark.parametrize("case", ["pair", "mesh", "b200prof"])
+@pytest.mark.parametrize("case", ["pair", "mesh", "b200prof", "empq"])
 def test_priced_outputs_byte_identical_to_reference(case, tmp_path):
     out = tmp_path / "out"
     rc = simulate.main(["-c", os.path.join(G, f"cfg_{case}.json"), "-p", os.path.join(G, f"plan_{case}.json"),
@@ -60,3 +60,34 @@ def test_config_errors_map_to_exit_code_1(tmp_path):
 
 def test_power_law_rates():
     assert wire.gen_rates(3, 1.0, 6.0) == [6.0, 3.0, 2.0]
+
+
+def test_config_validation_matches_reference(tmp_path):
+    """config.cpp:28-39 check_keys + range checks: typos and bad values are
+    ConfigErrors (exit 1), as in the reference CLI."""
+    base = {"cluster": {"num_nodes": 1, "gpus_per_node": 1, "gpu_memory_gb": 80},
+            "llms": [{"name": "x", "model": "7b"}]}
+    import copy
+    import json as _json
+    bad = []
+    c = copy.deepcopy(base); c["sim"] = {"quota_low_mrk": 0.3}; bad.append(c)          # typo
+    c = copy.deepcopy(base); c["sim"] = {"decode_sm": 1.5}; bad.append(c)              # range
+    c = copy.deepcopy(base); c["sim"] = {"token_budget": 7.5}; bad.append(c)           # type
+    c = copy.deepcopy(base); c["llms"][0]["prompt_len"] = {"kind": "empirical", "values": [1, 2],
+                                                           "weights": [1]}; bad.append(c)
+    c = copy.deepcopy(base); c["llms"].append({"name": "x", "model": "13b"}); bad.append(c)  # duplicate
+    c = copy.deepcopy(base); c["profile"] = {"tp_efficiency": 0.2}; bad.append(c)
+    for i, cfg in enumerate(bad):
+        p = tmp_path / f"bad{i}.json"
+        p.write_text(_json.dumps(cfg))
+        with pytest.raises(wire.ConfigError):
+            wire.load_config(str(p))
+    ok = copy.deepcopy(base)
+    ok["sim"] = {"quota_low_mark": 0.3, "quota_high_mark": 0.6, "quota_step_frac": 0.25}
+    ok["llms"][0]["prompt_len"] = {"kind": "empirical", "values": [10, 100], "weights": [3, 1]}
+    p = tmp_path / "ok.json"
+    p.write_text(_json.dumps(ok))
+    exp = wire.load_config(str(p))
+    assert (exp.params.quota_low_mark, exp.params.quota_high_mark, exp.params.quota_step_frac) == (0.3, 0.6, 0.25)
+    assert exp.entries[0].mean_prompt_tokens == (10 * 3 + 100 * 1) / 4  # weighted (workload.cpp:66-76)
+    assert exp.entries[0].mean_output_tokens == 64.0                     # LlmConfig default (config.hpp:27)
