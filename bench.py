@@ -18,9 +18,10 @@ N GPUs (torchrun): every rank serves its own independent 7B+13B unit (units
 share nothing, sim_engine.hpp:74-80) -> weak scaling, no collective on the
 data path; timing is the max over ranks.
 
---impl reference: the CPU port of the same decode step (oracle/numerics_ref.c:
-bf16 GEMVs + paged attention, all host threads) on a bounded sample (one layer
-of each model, scaled to the full step), printed as the reference arm.
+--impl reference: the CPU restatement of the same decode round (bench_cpu.py:
+oracle/llama_ref.decode_batch + oracle/numerics_ref.c attention, all host
+threads), every step a full round of both models timed end to end, on this
+arm's config; it never imports the product package.
 """
 from __future__ import annotations
 
@@ -58,10 +59,30 @@ def k1_traffic():
         return None
 
 
-def pool_blocks(specs):
-    weights = sum(s.weight_bytes for s in specs)
+# LLMSpec.weight_bytes of the reference catalog (config.cpp:15-18)
+WEIGHT_BYTES = {"7b": int(13.5e9), "13b": int(26e9), "30b": int(65e9), "65b": int(130e9)}
+
+
+def pool_blocks(models):
+    """UnitSim::pool_blocks (sim_engine.cpp:172-186) on one 180 GiB GPU."""
+    weights = sum(WEIGHT_BYTES[m] for m in models)
     reserve = round(RESERVE * MESH_BYTES)
     return (MESH_BYTES - weights - reserve) // 4096
+
+
+def workload_config(args, world):
+    """The config dict both arms print (identical, so the driver's
+    ours-vs-reference ratio compares the same workload)."""
+    models = args.models.split(",")
+    return {
+        "workload": "cfg2: LLaMA-7B + LLaMA-13B colocated per B200, one ADBS decode round per step",
+        "models": args.models, "decode_batch_per_model": args.batch,
+        "contexts": "ShareGPT lognormal prompt 161 / output 338 (sigma 0.8), members mid-generation, "
+                    "seed 1000 + rank (bench.sample_batch)",
+        "pool_blocks": pool_blocks(models),
+        "l2": "inputs larger than L2 (39.5 GB weights + KV per step)",
+        "parallelism": f"{world} independent units (dp{world})",
+    }
 
 
 def sample_batch(rng, B, extra_steps):
@@ -159,7 +180,7 @@ def run_ours(args, rank, world, local_rank):
     for s, reqs in zip(specs, batches):
         for p, o, d in reqs:
             need += mux.blocks_for_tokens(s, 16, p + d + steps_total + 1)
-    logical = pool_blocks(specs)
+    logical = pool_blocks(args.models.split(","))
     assert need <= logical, "batch exceeds the unified pool"
     max_ctx = max(p + d + steps_total + 1 for reqs in batches for p, o, d in reqs)
     if args.partition_sms == "auto" and len(specs) == 1:
@@ -322,7 +343,7 @@ def main():
         if rank != 0:
             return
         from bench_cpu import reference_arm
-        print(json.dumps(reference_arm(args)), flush=True)
+        print(json.dumps(reference_arm(args, workload_config(args, world))), flush=True)
         return
 
     import torch
@@ -377,15 +398,8 @@ def main():
             "vs_baseline": None,
             "dtype": "bf16",
             "data": "synthetic (random-init weights, ShareGPT-shaped lognormal lengths, random KV)",
-            "config": {
-                "workload": "cfg2: LLaMA-7B + LLaMA-13B colocated per B200, one ADBS decode round per step",
-                "models": args.models, "decode_batch_per_model": args.batch,
-                "pool_blocks": pool_blocks([__import__("paper_2404_02015_b200").spec(m) for m in args.models.split(",")]),
-                "l2": "inputs larger than L2 (39.5 GB weights + KV per step)",
-                "parallelism": f"{world} independent units (dp{world})",
-                "partition_sms": r["partition_sms"],
-                "job_ms_per_step": r["job_ms_per_step"],
-            },
+            "config": workload_config(args, world),
+            "run": {"partition_sms": r["partition_sms"], "job_ms_per_step": r["job_ms_per_step"]},
             "e2e": {"value": round(per_step_tokens / (e2e_ms / 1e3), 1) if e2e_ms else None,
                     "unit": "tokens/s", "h2d_bytes_per_step": int(per_step_tokens * 4),
                     "d2h_bytes_per_step": int(per_step_tokens * 4)},

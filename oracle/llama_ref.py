@@ -30,11 +30,14 @@ def bf16_to_f32(u16: np.ndarray) -> np.ndarray:
 
 def f32_to_bf16(x: np.ndarray) -> np.ndarray:
     """Round-to-nearest-even fp32 -> bf16 (as uint16)."""
-    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32).astype(np.uint64)
-    r = (u + 0x7FFF + ((u >> 16) & 1)) >> 16
-    nan = (u & 0x7F800000) == 0x7F800000
-    quiet = np.where((u & 0xFFFF) != 0, np.uint64(0x40), np.uint64(0))
-    r = np.where(nan, (u >> 16) | quiet, r)
+    u = np.ascontiguousarray(x, dtype=np.float32).view(np.uint32)
+    # uint32 arithmetic: only NaN/Inf patterns (exponent all ones) can carry
+    # out of 32 bits, and those take the branch below
+    r = (u + np.uint32(0x7FFF) + ((u >> np.uint32(16)) & np.uint32(1))) >> np.uint32(16)
+    nan = (u & np.uint32(0x7F800000)) == np.uint32(0x7F800000)
+    if nan.any():
+        quiet = np.where((u & np.uint32(0xFFFF)) != 0, np.uint32(0x40), np.uint32(0))
+        r = np.where(nan, (u >> np.uint32(16)) | quiet, r)
     return r.astype(np.uint16)
 
 
@@ -166,6 +169,35 @@ class RefLlama:
             nw = self.attn_norm[l + 1] if l + 1 < d.layers else self.final_norm
             xn = rmsnorm_bf16(x, nw)
         return (xn[-1] @ self.lm_head.T).astype(np.float32)
+
+
+def decode_batch(ref: "RefLlama", tokens: np.ndarray, positions: np.ndarray, attend) -> np.ndarray:
+    """One decode step of a whole batch (the decode job of
+    csrc/device/runtime.cu Runtime::decode): member i feeds tokens[i] at
+    position positions[i] (its context minus one, scheduler.cpp:107).
+    attend(layer, q, k, v) receives the rotated bf16 q / k and v [B, H, 128]
+    (float32 holding bf16 values), appends k / v to each member's cache and
+    returns attention over the whole context [B, H, 128] (float32). Same
+    rounding points as RefLlama.forward; returns fp32 logits [B, vocab]."""
+    d = ref.d
+    B = len(tokens)
+    pos = np.asarray(positions)
+    x = ref.embed[np.asarray(tokens)].astype(np.float32)
+    xn = rmsnorm_bf16(x, ref.attn_norm[0])
+    for l in range(d.layers):
+        qkv = round_bf16(xn @ ref.wqkv[l].T).reshape(B, 3, d.heads, 128)
+        q = round_bf16(rope_rotate(qkv[:, 0], pos[:, None], ref.rope))
+        k = round_bf16(rope_rotate(qkv[:, 1], pos[:, None], ref.rope))
+        att = round_bf16(attend(l, q, k, qkv[:, 2])).reshape(B, d.heads * 128)
+        x = x + (att @ ref.wo[l].T).astype(np.float32)
+        xn = rmsnorm_bf16(x, ref.ffn_norm[l])
+        g = (xn @ ref.wg[l].T).astype(np.float32)
+        u = (xn @ ref.wu[l].T).astype(np.float32)
+        act = round_bf16((g / (1.0 + np.exp(-g))) * u)
+        x = x + (act @ ref.wdown[l].T).astype(np.float32)
+        nw = ref.attn_norm[l + 1] if l + 1 < d.layers else ref.final_norm
+        xn = rmsnorm_bf16(x, nw)
+    return (xn @ ref.lm_head.T).astype(np.float32)
 
 
 def prefill_attention_ref(q, k, v, seq_lens):

@@ -1,0 +1,307 @@
+"""Parity at the headline configuration: the unit bench.py times (BASELINE
+config 2, LLaMA-7B + LLaMA-13B colocated on one B200).
+
+What bench.py runs, and what is checked here at the same shapes:
+  * real 7B / 13B widths (hidden 4096 / 5120, heads 32 / 40, FFN 11008 /
+    13824, vocab 32000; config.cpp:15-18 + LLaMA-1), truncated to 2 layers so
+    the numpy oracle holds the weights in fp32;
+  * decode batch 128 per model with ShareGPT-shaped contexts caught
+    mid-generation (bench.sample_batch, same seed as bench rank 0);
+  * the two decode jobs run concurrently on green-context partitions of
+    56 + 92 SMs (the bench's byte_share_partitions split);
+  * one unified pool of 3 M head-blocks (12.3 GB) whose first 1.2 M blocks are
+    held by a filler request, so every K/V byte these jobs touch sits beyond
+    4 GiB of the pool base (64-bit block offsets).
+
+Checks:
+  1. teacher-forced greedy tokens over 4 decode steps against the oracle
+     (oracle/llama_ref.decode_batch + the C attention restatement over the
+     same head-block tables): exact-argmax rate >= 99%, and a non-argmax token
+     only where the oracle's own top-2 margin is under TOL (bf16 near-tie);
+  2. K1 on the unit's own pool and device tables, fp32 out, per element
+     |got - want| <= 1e-4 |want| + 1e-6 (north_star: fp32 within 1e-4
+     relative), bf16 out within 1e-2;
+  3. every 7B / 13B projection shape (K 4096 / 5120 / 11008 / 13824, N 4096 /
+     5120 / 12288 / 15360 / 22016 / 27648 / 32000) with its runtime epilogue,
+     at serving and headline batch sizes and on partition-sized grids,
+     against a torch fp32 matmul of the same bf16 operands.
+Geometry follows the reference: kv_manager.cpp:25-40 (head-blocks),
+scheduler.cpp:107 (context = prompt + 1 + steps).
+"""
+import numpy as np
+import pytest
+
+import bench
+import paper_2404_02015_b200 as mux
+from oracle import llama_ref, refs
+
+pytestmark = pytest.mark.gpu
+
+B = 128
+STEPS = 4
+TOL = 2e-2          # top-2 logit margin (x max|logit|) under which bf16 may pick either token
+POOL = 3_000_000    # head-blocks (12.3 GB)
+FILLER = 1_200_000  # blocks held first: K/V offsets start beyond 4.9 GB
+PARTS = [0, 56, 92]
+
+
+def two_layer(name):
+    s = mux.spec(name)
+    return mux.LLMSpec(f"{name}-2L", 2, s.num_heads, 128, s.hidden_size, s.weight_bytes, 2, s.ffn, s.vocab)
+
+
+class _DevBlocks:
+    """Zero-copy torch view of the unit's device pool ([blocks][2048] bf16 bits)."""
+
+    def __init__(self, ptr, n):
+        self.__cuda_array_interface__ = {"shape": (n, 2048), "typestr": "<i2", "data": (ptr, False),
+                                         "version": 3, "strides": None}
+
+
+def make_weights(d, seed, std=0.02):
+    """llama_ref.make_weights' layout, generated on the GPU (1.6 G parameters)."""
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(seed)
+
+    def w(*shape):
+        t = (torch.randn(*shape, generator=g, device="cuda") * std).to(torch.bfloat16)
+        return t.view(torch.int16).cpu().numpy().view(np.uint16)
+
+    rng = np.random.default_rng(seed)
+    out = {"embed": w(d.vocab, d.hidden), "lm_head": w(d.vocab, d.hidden),
+           "final_norm": (1.0 + 0.1 * rng.standard_normal(d.hidden)).astype(np.float32)}
+    for l in range(d.layers):
+        out[("wqkv", l)] = w(3 * d.heads * 128, d.hidden)
+        out[("wo", l)] = w(d.hidden, d.heads * 128)
+        out[("wgu", l)] = w(2 * d.ffn, d.hidden)
+        out[("wdown", l)] = w(d.hidden, d.ffn)
+        out[("attn_norm", l)] = (1.0 + 0.1 * rng.standard_normal(d.hidden)).astype(np.float32)
+        out[("ffn_norm", l)] = (1.0 + 0.1 * rng.standard_normal(d.hidden)).astype(np.float32)
+    return out
+
+
+class HostCache:
+    """The oracle's copy of one model's K/V: the head-blocks of every member
+    gathered from the device pool once (random K/V, as in the bench), then
+    extended by the oracle's OWN appended K/V (never re-read from the GPU)."""
+
+    def __init__(self, pool_view, unit, llm, spec, rids):
+        import torch
+        self.pool_view, self.unit, self.llm, self.rids = pool_view, unit, llm, rids
+        self.L, self.H = spec.num_layers, spec.num_heads
+        self.W = 2 * self.L * self.H
+        self.rows = [[] for _ in rids]   # per member: compact rowrec index per row
+        self.rowrec = np.zeros((0, self.W), np.int32)
+        self.blocks = np.zeros((0, 2048), np.uint16)
+        self.sync_rows(gather=True)
+
+    def sync_rows(self, gather=False):
+        """Pick up rows the host pool allocated since the last call; their
+        contents come from the device (gather=True) or start zeroed."""
+        import torch
+        new_ids = []
+        for i, rid in enumerate(self.rids):
+            t = np.asarray(self.unit.pool.block_table(self.llm, rid), np.int32).reshape(-1, self.W)
+            for r in range(len(self.rows[i]), t.shape[0]):
+                self.rows[i].append(self.rowrec.shape[0] + len(new_ids))
+                new_ids.append(t[r])
+        if not new_ids:
+            return
+        ids = np.stack(new_ids)
+        base = self.blocks.shape[0]
+        if gather:
+            idx = torch.from_numpy(ids.reshape(-1).astype(np.int64)).cuda()
+            blk = self.pool_view.index_select(0, idx).cpu().numpy().view(np.uint16)
+        else:
+            blk = np.zeros((ids.size, 2048), np.uint16)
+        self.blocks = np.concatenate([self.blocks, blk])
+        self.rowrec = np.concatenate([self.rowrec, (base + np.arange(ids.size, dtype=np.int32)).reshape(ids.shape)])
+
+    def tables(self):
+        max_rows = max(len(r) for r in self.rows)
+        rowlist = np.zeros((len(self.rids), max_rows), np.int32)
+        for i, r in enumerate(self.rows):
+            rowlist[i, :len(r)] = r
+        return rowlist, max_rows
+
+    def append(self, layer, k, v, pos):
+        """k / v [B, H, 128] (bf16 values as f32) at positions pos [B]."""
+        kb, vb = llama_ref.f32_to_bf16(k), llama_ref.f32_to_bf16(v)
+        for i in range(len(self.rids)):
+            rec = self.rows[i][pos[i] // 16]
+            cols = (layer * self.H + np.arange(self.H)) * 2
+            blk = self.blocks.reshape(-1, 16, 128)
+            blk[self.rowrec[rec, cols], pos[i] % 16] = kb[i]
+            blk[self.rowrec[rec, cols + 1], pos[i] % 16] = vb[i]
+
+    def attend(self, layer, q, ctx):
+        rowlist, max_rows = self.tables()
+        return refs.decode_attention(llama_ref.f32_to_bf16(q), self.blocks, self.rowrec, rowlist,
+                                     np.arange(len(self.rids), dtype=np.int32), np.asarray(ctx, np.int32),
+                                     self.L, layer, max_rows, nthreads=16)
+
+
+@pytest.fixture(scope="module")
+def headline(cuda):
+    import torch
+    specs = [two_layer("7b"), two_layer("13b"), mux.spec("tiny-b")]
+    rng = np.random.default_rng(1000)  # bench.py rank 0
+    batches = [bench.sample_batch(rng, B, STEPS + 2) for _ in range(2)]
+    max_ctx = max(p + d for bt in batches for p, o, d in bt) + STEPS + 16
+    unit = mux.Unit(specs, pool_blocks=POOL, device_pool_blocks=POOL, max_batch=B, max_prefill_tokens=256,
+                    max_ctx=max_ctx, max_slots=2 * B + 16, partitions=3, partition_sms=PARTS)
+    weights = []
+    for li in range(2):
+        s = specs[li]
+        w = make_weights(llama_ref.Dims(s.num_layers, s.num_heads, s.hidden_size, s.ffn, s.vocab), 11 + li)
+        for key, arr in w.items():
+            name, layer = (key, 0) if isinstance(key, str) else key
+            unit.set_tensor(li, name, layer, np.ascontiguousarray(arr))
+        weights.append(w)
+    unit.init_kv(seed=7, std=1.0)
+    pool = unit.pool
+    # filler: the lowest FILLER ids (a fresh pool hands ids out ascending)
+    assert pool.admit(2, 1, FILLER, FILLER).ok
+    assert min(pool.block_table(2, 1)) == 0 and max(pool.block_table(2, 1)) == FILLER - 1
+    rids = []
+    for li, bt in enumerate(batches):
+        r = []
+        for k, (p, o, d) in enumerate(bt):
+            rid = 10_000 * li + k
+            assert pool.admit(li, rid, p, p + o - 1).ok
+            if d:
+                assert pool.alloc(li, rid, d, False).ok
+            r.append(rid)
+        rids.append(r)
+    assert min(min(pool.block_table(li, r)) for li in range(2) for r in rids[li]) >= FILLER
+    ptr = unit.device_ptrs(0)[0]
+    pool_view = torch.as_tensor(_DevBlocks(ptr, POOL), device="cuda")
+    caches = [HostCache(pool_view, unit, li, specs[li], rids[li]) for li in range(2)]
+    rope = llama_ref.rope_table(max_ctx + 16)
+    models = [llama_ref.RefLlama(llama_ref.Dims(s.num_layers, s.num_heads, s.hidden_size, s.ffn, s.vocab), w, rope)
+              for s, w in zip(specs[:2], weights)]
+    yield unit, specs, rids, caches, models, pool_view
+    unit.close()
+
+
+def test_headline_decode_tokens_match_oracle(headline):
+    unit, specs, rids, caches, models, _ = headline
+    pool = unit.pool
+    rng = np.random.default_rng(5)
+    tokens = [rng.integers(0, s.vocab, B).astype(np.int32) for s in specs[:2]]
+    exact = total = 0
+    worst = 0.0
+    for step in range(STEPS):
+        ctx = []
+        for li in range(2):
+            assert all(r.ok for r in pool.alloc_n(li, rids[li], 1, False))
+            ctx.append(np.array([pool.request_tokens(li, r) for r in rids[li]], np.int32))
+            caches[li].sync_rows(gather=False)  # new rows: the oracle writes its own K/V
+        outs = [np.zeros(B, np.int32) for _ in range(2)]
+        for li in range(2):  # both jobs in flight at once, each on its green partition
+            unit.decode(li, rids[li], tokens=tokens[li], out=outs[li], partition=1 + li)
+        unit.sync()
+        for li in range(2):
+            c = caches[li]
+            pos = ctx[li] - 1
+
+            def attend(layer, q, k, v, c=c, pos=pos, cl=ctx[li]):
+                c.append(layer, k, v, pos)
+                return c.attend(layer, q, cl)
+
+            logits = llama_ref.decode_batch(models[li], tokens[li], pos, attend)
+            top = logits.max(axis=1)
+            got = logits[np.arange(B), outs[li]]
+            order = np.sort(logits, axis=1)
+            margin = order[:, -1] - order[:, -2]
+            scale = np.maximum(1.0, np.abs(logits).max(axis=1))
+            hit = outs[li] == logits.argmax(axis=1)
+            exact += int(hit.sum())
+            total += B
+            for i in np.nonzero(~hit)[0]:
+                # a different token is a bf16 near-tie of the oracle's top two
+                assert top[i] - got[i] <= TOL * scale[i] and margin[i] <= TOL * scale[i], \
+                    (specs[li].name, step, int(i), int(outs[li][i]), int(logits[i].argmax()), float(top[i] - got[i]))
+                worst = max(worst, float((top[i] - got[i]) / scale[i]))
+            tokens[li] = outs[li].copy()  # teacher forcing on the GPU's own history
+    rate = exact / total
+    print(f"headline greedy parity: {exact}/{total} exact argmax ({rate:.4f}), worst near-tie gap {worst:.2e}")
+    assert rate >= 0.99, rate
+
+
+def test_headline_k1_per_element_on_unit_pool(headline):
+    import torch
+    unit, specs, rids, _, _, pool_view = headline
+    pool = unit.pool
+    for li in range(2):
+        s = specs[li]
+        H, L = s.num_heads, s.num_layers
+        pool_ptr, rowrec_ptr, rowlist_ptr, max_rows, _ = unit.device_ptrs(li)
+        slots = torch.tensor([pool.slot(li, r) for r in rids[li]], dtype=torch.int32, device="cuda")
+        ctx_h = np.array([pool.request_tokens(li, r) for r in rids[li]], np.int32)
+        ctx = torch.from_numpy(ctx_h).cuda()
+        g = torch.Generator(device="cuda").manual_seed(20 + li)
+        q = torch.randn(B, H, 128, generator=g, device="cuda").to(torch.bfloat16)
+        ws = torch.empty(B * H * 16 * 130, dtype=torch.float32, device="cuda")
+        fresh = HostCache(pool_view, unit, li, s, rids[li])  # the GPU's K/V as it is now
+        rowlist, mr = fresh.tables()
+        want = refs.decode_attention(q.view(torch.int16).cpu().numpy().view(np.uint16), fresh.blocks,
+                                     fresh.rowrec, rowlist, np.arange(B, dtype=np.int32), ctx_h, L, L - 1, mr,
+                                     nthreads=16)
+        for splits in (0, 4):
+            out32 = torch.empty(B, H, 128, dtype=torch.float32, device="cuda")
+            mux.decode_attention_headwise(q, pool_ptr, rowrec_ptr, rowlist_ptr, slots, ctx, L, L - 1, max_rows,
+                                          int(ctx_h.max()), out32, kv_splits=splits, workspace=ws)
+            out16 = torch.empty(B, H, 128, dtype=torch.bfloat16, device="cuda")
+            mux.decode_attention_headwise(q, pool_ptr, rowrec_ptr, rowlist_ptr, slots, ctx, L, L - 1, max_rows,
+                                          int(ctx_h.max()), out16, kv_splits=splits, workspace=ws)
+            torch.cuda.synchronize()
+            got = out32.cpu().numpy()
+            err = np.abs(got - want)
+            bound = 1e-4 * np.abs(want) + 1e-6
+            assert (err <= bound).all(), (s.name, splits, float((err / (np.abs(want) + 1e-6)).max()))
+            got16 = out16.float().cpu().numpy()
+            assert (np.abs(got16 - want) <= 1e-2 * np.abs(want) + 1e-2 * 2 ** -8 * np.abs(want).max()).all()
+
+
+# (N, K, epilogue) of every decode projection: 0 bf16 store (QKV), 1 fp32
+# residual add (O, down), 2 SiLU(gate)*up (gate-up), 3 fp32 store (LM head)
+SHAPES = {
+    "7b": [(12288, 4096, 0), (4096, 4096, 1), (22016, 4096, 2), (4096, 11008, 1), (32000, 4096, 3)],
+    "13b": [(15360, 5120, 0), (5120, 5120, 1), (27648, 5120, 2), (5120, 13824, 1), (32000, 5120, 3)],
+}
+
+
+@pytest.mark.parametrize("model", ["7b", "13b"])
+@pytest.mark.parametrize("M,grid", [(8, 56), (32, 92), (128, 56), (128, 92), (128, 0)])
+def test_headline_projection_shapes(cuda, model, M, grid):
+    import torch
+    g = torch.Generator(device="cuda").manual_seed(M * 7 + grid)
+    for N, K, epi in SHAPES[model]:
+        x = (torch.randn(M, K, generator=g, device="cuda")).to(torch.bfloat16)
+        w = (torch.randn(N, K, generator=g, device="cuda") * 0.02).to(torch.bfloat16)
+        wt = mux.weight_tile(w)
+        ref = x.float() @ w.float().T
+        absdot = x.float().abs() @ w.float().abs().T
+        if epi == 0:
+            out = torch.empty(M, N, dtype=torch.bfloat16, device="cuda")
+        elif epi == 1:
+            out = torch.randn(M, N, generator=g, device="cuda")
+            base = out.clone()
+            ref = ref + base
+        elif epi == 2:
+            out = torch.empty(M, N // 2, dtype=torch.bfloat16, device="cuda")
+            gate, up = ref[:, 0::2], ref[:, 1::2]
+            absdot = absdot[:, 0::2] * up.abs() + absdot[:, 1::2] * gate.abs()
+            ref = gate * torch.sigmoid(gate) * up
+        else:
+            out = torch.empty(M, N, dtype=torch.float32, device="cuda")
+        mux.gemm_bf16(x, w, out, epilogue=epi, grid=grid, w_tiled=wt)
+        torch.cuda.synchronize()
+        got = out.float()
+        # fp32 accumulation order (1e-4 of the sum of |terms|; 2x through
+        # SiLU's slope), then the bf16 rounding of stored outputs
+        bound = (2e-4 if epi == 2 else 1e-4) * absdot + (2.0 ** -8 * ref.abs() if epi in (0, 2) else 0.0) + 1e-6
+        bad = (got - ref).abs() > bound
+        assert not bool(bad.any()), (model, N, K, epi, M, grid, int(bad.sum()),
+                                     float(((got - ref).abs() / (absdot + 1e-6)).max()))
