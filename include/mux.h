@@ -328,6 +328,24 @@ MUX_API int mux_unit_tp_connect(mux_unit* unit, int partition, int peer_rank, co
  * (out[4] = counter0, counter1, expected0, expected1), read on a side stream. */
 MUX_API int mux_unit_tp_debug(mux_unit* unit, int partition, uint32_t* out);
 /* SMs of a partition (its green context's, or the device's). */
+/* SM routing (option "sm_route"): every ADBS job runs on a green context
+ * whose SMs are sized by its JobPlan.sm_demand (scheduler.cpp:50-54, :95;
+ * priced by sim_engine.cpp:16-18, 308-330). One record per routed job of the
+ * last engine run: the scheduling pass, the SM run [first_unit, +units) of
+ * the device's green-context units, its SM count and the workspace used
+ * (first_unit -1: no free SMs were left, the job shared the whole device). */
+typedef struct {
+  int64_t pass, job;
+  int llm, kind;               /* kind: 0 prefill, 1 decode */
+  double sm_demand;
+  int first_unit, units, sms, workspace;
+  uint64_t busy_units;         /* bit k: unit k held by another in-flight job */
+} mux_route_record;
+MUX_API int mux_unit_route_log(mux_unit* unit, mux_route_record* out, int64_t cap, int64_t* n_out);
+/* The device's green-context units (8-SM granules, remainder last). */
+MUX_API int mux_unit_route_units(mux_unit* unit, int* n_units, int* unit_sms, int cap);
+/* %smid of `blocks` CTAs launched on the green context of one SM run. */
+MUX_API int mux_unit_probe_route(mux_unit* unit, int first_unit, int units, int blocks, int* out);
 MUX_API int mux_unit_partition_sms(mux_unit* unit, int partition, int* sms);
 /* Debug: launch `blocks` CTAs on a partition and record each CTA's %smid
  * into out (host, [blocks]); synchronises. Proves partition disjointness. */

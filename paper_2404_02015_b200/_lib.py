@@ -62,6 +62,12 @@ class SimConfig(C.Structure):
                 ("quota_adapt", P(f64))]
 
 
+class RouteRecord(C.Structure):
+    _fields_ = [("pass_", i64), ("job", i64), ("llm", C.c_int), ("kind", C.c_int), ("sm_demand", f64),
+                ("first_unit", C.c_int), ("units", C.c_int), ("sms", C.c_int), ("workspace", C.c_int),
+                ("busy_units", u64)]
+
+
 class Request(C.Structure):
     _fields_ = [("id", i64), ("llm", C.c_int), ("arrival_s", f64), ("prompt_len", C.c_int),
                 ("output_len", C.c_int)]
@@ -137,6 +143,9 @@ _SIGS = {
     "mux_unit_tp_debug": (C.c_int, [vp, C.c_int, P(C.c_uint32)]),
     "mux_unit_partition_sms": (C.c_int, [vp, C.c_int, P(C.c_int)]),
     "mux_unit_probe_smids": (C.c_int, [vp, C.c_int, C.c_int, P(C.c_int)]),
+    "mux_unit_route_log": (C.c_int, [vp, vp, i64, P(i64)]),
+    "mux_unit_route_units": (C.c_int, [vp, P(C.c_int), P(C.c_int), C.c_int]),
+    "mux_unit_probe_route": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, P(C.c_int)]),
     "mux_unit_set_option": (C.c_int, [vp, C.c_char_p, i64]),
     "mux_debug_gemm_timing": (None, [vp]),
     "mux_debug_chain_timing": (None, [vp]),

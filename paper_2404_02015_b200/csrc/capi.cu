@@ -230,6 +230,110 @@ uint64_t mix64(uint64_t x) {
 
 }  // namespace
 
+// SM routing of ADBS jobs (option sm_route): every job runs on a green
+// context whose SM set is sized by its JobPlan.sm_demand (scheduler.cpp:50-54
+// prefill, :95 decode) -- the spatial share the reference prices with
+// sm_scaling_* and interference_adjust (sim_engine.cpp:16-18, 308-330). The
+// device's SMs are split once into green-context granules (8-SM groups; the
+// remainder outside them is the last unit); a job takes the first free
+// contiguous run of units whose SM count reaches round(sm_demand x SMs), or
+// the largest free run when rounding leaves less. ADBS keeps the demands of
+// concurrent jobs <= 1, so concurrent jobs land on disjoint SM sets. The green
+// context of each (first unit, units) run is created on first use and cached.
+struct SmRouter {
+  struct Part {
+    CUgreenCtx g = nullptr;
+    cudaStream_t s = nullptr;
+    int sms = 0;
+  };
+  bool ready = false;
+  int device = 0;
+  int total_sms = 0;
+  std::vector<CUdevResource> units;
+  std::vector<int> unit_sms;
+  std::vector<int64_t> owner;  // job holding each unit, -1 = free
+  std::map<std::pair<int, int>, Part> parts;
+
+  void init(int dev) {
+    if (ready) return;
+    GreenApi& ga = green_api();
+    device = dev;
+    CUdevice d = 0;
+    check_cu(ga.device_get(&d, dev), "cuDeviceGet");
+    CUdevResource all{};
+    check_cu(ga.get_resource(d, &all, CU_DEV_RESOURCE_TYPE_SM), "cuDeviceGetDevResource");
+    unsigned int nb = 0;
+    check_cu(ga.split(nullptr, &nb, &all, nullptr, 0, 8), "cuDevSmResourceSplitByCount(query)");
+    units.resize(nb);
+    CUdevResource rem{};
+    check_cu(ga.split(units.data(), &nb, &all, &rem, 0, 8), "cuDevSmResourceSplitByCount");
+    units.resize(nb);
+    if (rem.sm.smCount > 0) units.push_back(rem);
+    total_sms = 0;
+    for (const CUdevResource& r : units) {
+      unit_sms.push_back(static_cast<int>(r.sm.smCount));
+      total_sms += static_cast<int>(r.sm.smCount);
+    }
+    owner.assign(units.size(), -1);
+    ready = true;
+  }
+  // (first unit, units) for a demand; (-1, 0) when every unit is taken.
+  std::pair<int, int> pick(double demand) const {
+    const int want = std::max(1, static_cast<int>(std::lround(demand * total_sms)));
+    const int n = static_cast<int>(units.size());
+    int best_start = -1, best_len = 0, best_sms = 0;
+    for (int i = 0; i < n; ++i) {
+      if (owner[i] >= 0) continue;
+      int sms = 0, j = i;
+      while (j < n && owner[j] < 0 && sms < want) sms += unit_sms[j++];
+      if (sms >= want) return {i, j - i};
+      if (sms > best_sms) best_start = i, best_len = j - i, best_sms = sms;
+      i = j - 1;
+    }
+    return {best_start, best_len};
+  }
+  Part& part(int start, int len) {
+    auto key = std::make_pair(start, len);
+    auto it = parts.find(key);
+    if (it != parts.end()) return it->second;
+    GreenApi& ga = green_api();
+    Part p;
+    CUdevResourceDesc desc;
+    std::vector<CUdevResource> rs(units.begin() + start, units.begin() + start + len);
+    check_cu(ga.gen_desc(&desc, rs.data(), static_cast<unsigned>(rs.size())), "cuDevResourceGenerateDesc");
+    CUdevice d = 0;
+    check_cu(ga.device_get(&d, device), "cuDeviceGet");
+    check_cu(ga.create(&p.g, desc, d, CU_GREEN_CTX_DEFAULT_STREAM), "cuGreenCtxCreate");
+    CUstream cs;
+    check_cu(ga.stream_create(&cs, p.g, CU_STREAM_NON_BLOCKING, 0), "cuGreenCtxStreamCreate");
+    p.s = reinterpret_cast<cudaStream_t>(cs);
+    for (int k = start; k < start + len; ++k) p.sms += unit_sms[k];
+    return parts.emplace(key, p).first->second;
+  }
+  void take(int start, int len, int64_t job) {
+    for (int k = start; k < start + len; ++k) owner[k] = job;
+  }
+  void release(int64_t job) {
+    for (int64_t& o : owner)
+      if (o == job) o = -1;
+  }
+  ~SmRouter() {
+    for (auto& kv : parts) {
+      if (kv.second.s) cudaStreamDestroy(kv.second.s);
+      if (kv.second.g) green_api().destroy(kv.second.g);
+    }
+  }
+};
+
+// One routed job, for mux_unit_route_log (tests, serving analysis).
+struct RouteRecord {
+  int64_t pass, job;
+  int llm, kind;  // kind: 0 prefill, 1 decode
+  double sm_demand;
+  int first_unit, units, sms, workspace;
+  uint64_t busy_units;  // units held by other in-flight jobs at this launch
+};
+
 // Pool statistics of a run (SimResult.units) behind poolstats.json.
 struct mux_sim_stats {
   std::vector<muxsim::UnitStats> units;
@@ -246,6 +350,10 @@ struct mux_unit {
   // green partitions only when decode jobs of two or more models share it.
   bool pass_green = false;
   bool align_decode = false;  // option align_decode (real-time mode): colocated decode steps in rounds
+  bool sm_route = false;      // option sm_route: every job on an SM run sized by its sm_demand
+  SmRouter router;
+  std::vector<int64_t> ws_owner;   // sm_route: job holding each workspace (-1 free)
+  std::vector<RouteRecord> route_log;
   int64_t passes = 0, green_passes = 0;  // of the last lockstep / measured run
   std::unique_ptr<mux::Runtime> rt;
   std::deque<muxsim::LLMSpec> specs;
@@ -422,8 +530,38 @@ class GpuExecutor : public muxsim::JobExecutor {
       part = !own ? 0 : (green_pass_ ? 1 + n + j.llm : 1 + j.llm);
     }
     cudaStream_t s = u_->streams[part];
+    mux::Workspace* wsp = u_->ws[part].get();
+    if (u_->sm_route) {
+      // the job's own SM run, sized by its sm_demand, and a free workspace
+      SmRouter& R = u_->router;
+      R.init(u_->rt->device());
+      int w = 0;
+      while (w < static_cast<int>(u_->ws_owner.size()) && u_->ws_owner[w] >= 0) ++w;
+      if (w == static_cast<int>(u_->ws_owner.size()))
+        throw std::logic_error("sm_route: more concurrent jobs than workspaces (create the unit with models + 1 partitions)");
+      uint64_t busy = 0;
+      for (size_t k = 0; k < R.owner.size() && k < 64; ++k)
+        if (R.owner[k] >= 0) busy |= 1ull << k;
+      const std::pair<int, int> run = R.pick(j.sm_demand);
+      int sms = u_->rt->num_sms();
+      if (run.first >= 0) {
+        SmRouter::Part& pt = R.part(run.first, run.second);
+        R.take(run.first, run.second, j.job_id);
+        s = pt.s;
+        sms = pt.sms;
+      } else {
+        s = u_->streams[0];  // every unit taken by rounding: share the whole device
+      }
+      u_->ws_owner[w] = j.job_id;
+      wsp = u_->ws[w].get();
+      wsp->sms = sms;
+      wsp->exclusive = run.first >= 0;
+      check(cudaStreamWaitEvent(s, tables_ready_, 0));
+      u_->route_log.push_back({u_->passes, j.job_id, j.llm, j.kind == muxsim::JobKind::Prefill ? 0 : 1, j.sm_demand,
+                               run.first, run.second, sms, w, busy});
+    }
     mux::Llama& m = *u_->models[j.llm];
-    mux::Workspace& ws = *u_->ws[part];
+    mux::Workspace& ws = *wsp;
     const int n = static_cast<int>(j.members->size());
     Job job;
     job.members = *j.members;
@@ -497,6 +635,11 @@ class GpuExecutor : public muxsim::JobExecutor {
     if (it == jobs_.end()) throw std::logic_error("lockstep: retire of unknown job");
     Job& job = it->second;
     check(cudaEventSynchronize(job.done));
+    if (u_->sm_route) {
+      u_->router.release(job_id);
+      for (int64_t& o : u_->ws_owner)
+        if (o == job_id) o = -1;
+    }
     const int32_t* out = job.out->as<int32_t>();
     for (size_t i = 0; i < job.global_ids.size(); ++i) {
       auto r = row_of_id_.find(job.global_ids[i]);
@@ -1303,6 +1446,41 @@ int mux_unit_tp_debug(mux_unit* u, int partition, uint32_t* out) {
   });
 }
 
+int mux_unit_route_log(mux_unit* u, mux_route_record* out, int64_t cap, int64_t* n_out) {
+  return guarded([&] {
+    require(n_out != nullptr, "route log: null count");
+    *n_out = static_cast<int64_t>(u->route_log.size());
+    for (int64_t i = 0; out && i < std::min<int64_t>(cap, *n_out); ++i) {
+      const RouteRecord& r = u->route_log[i];
+      out[i] = mux_route_record{r.pass, r.job, r.llm, r.kind, r.sm_demand, r.first_unit, r.units, r.sms, r.workspace,
+                                r.busy_units};
+    }
+  });
+}
+
+int mux_unit_route_units(mux_unit* u, int* n_units, int* unit_sms, int cap) {
+  return guarded([&] {
+    u->router.init(u->rt->device());
+    *n_units = static_cast<int>(u->router.units.size());
+    for (int i = 0; unit_sms && i < std::min(cap, *n_units); ++i) unit_sms[i] = u->router.unit_sms[i];
+  });
+}
+
+int mux_unit_probe_route(mux_unit* u, int first_unit, int units, int blocks, int* out) {
+  return guarded([&] {
+    require(blocks > 0, "probe: blocks must be positive");
+    u->router.init(u->rt->device());
+    require(first_unit >= 0 && units > 0 && first_unit + units <= static_cast<int>(u->router.units.size()),
+            "probe: bad SM run");
+    cudaStream_t s = u->router.part(first_unit, units).s;
+    mux::DevMem d(static_cast<size_t>(blocks) * 4);
+    probe_smid_kernel<<<blocks, 32, 0, s>>>(d.as<int>());
+    mux::check_cuda(cudaGetLastError(), "probe");
+    mux::check_cuda(cudaMemcpyAsync(out, d.p, static_cast<size_t>(blocks) * 4, cudaMemcpyDeviceToHost, s), "probe copy");
+    mux::check_cuda(cudaStreamSynchronize(s), "probe sync");
+  });
+}
+
 int mux_unit_partition_sms(mux_unit* u, int partition, int* sms) {
   return guarded([&] {
     u->stream(partition);
@@ -1333,6 +1511,11 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
     else if (k == "prefill_on_partition") u->prefill_on_partition = value != 0;
     else if (k == "pass_green") u->pass_green = value != 0;
     else if (k == "align_decode") u->align_decode = value != 0;
+    else if (k == "sm_route") {
+      require(!u->pass_green && !u->align_decode, "sm_route excludes pass_green and align_decode");
+      u->sm_route = value != 0;
+      u->ws_owner.assign(u->ws.size(), -1);
+    }
     else if (k == "fuse_norm") u->rt->set_fuse_norm(value != 0);
     else if (k == "fuse_k2") u->rt->set_fuse_k2(value != 0);
     else throw std::invalid_argument("unknown option: " + k);
@@ -1352,6 +1535,12 @@ int run_unit(mux_unit* u, const mux_sim_config* cfg, int n_entries, const mux_ll
     require(n_entries == static_cast<int>(u->models.size()), "lockstep: entries must describe the unit's models");
     SimInputs in = build_inputs(cfg, n_entries, entries, n_requests, trace);
     u->passes = u->green_passes = 0;
+    u->route_log.clear();
+    if (u->sm_route) {
+      require(u->ws.size() >= u->models.size() + 1, "sm_route: the unit needs models + 1 partitions (workspaces)");
+      u->ws_owner.assign(u->ws.size(), -1);
+      if (u->router.ready) u->router.owner.assign(u->router.owner.size(), -1);
+    }
     GpuExecutor exec(u, prompt_seed, in.trace, measured, realtime);
     muxsim::SimResult res =
         muxsim::run_simulation(in.cluster, in.placement, in.entries, in.trace, in.prof, in.params, &exec);

@@ -505,8 +505,8 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
 #pragma unroll
           for (int q2 = 0; q2 < 8; ++q2) {
             const float4 gu = sf4[q2];  // gate, up, gate, up
-            const float s0 = gu.x * rcp_approx(1.f + __expf(-gu.x));
-            const float s1 = gu.z * rcp_approx(1.f + __expf(-gu.z));
+            const float s0 = gu.x / (1.f + expf(-gu.x));
+            const float s1 = gu.z / (1.f + expf(-gu.z));
             packed[q2] = pack_bf16(s0 * gu.y, s1 * gu.w);
           }
           epi_bar(eg);

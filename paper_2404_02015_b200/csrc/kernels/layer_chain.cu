@@ -165,8 +165,8 @@ __device__ void post_silu(const ChainPost& p, int c, int G, int M) {
       if (e < n) {
         gu[e] = make_float4(0.f, 0.f, 0.f, 0.f);
         const float g0 = bf16_round(v[u].x), u0 = bf16_round(v[u].y), g1 = bf16_round(v[u].z), u1 = bf16_round(v[u].w);
-        const float s0 = g0 * rcp_approx(1.f + __expf(-g0));
-        const float s1 = g1 * rcp_approx(1.f + __expf(-g1));
+        const float s0 = g0 / (1.f + expf(-g0));
+        const float s1 = g1 / (1.f + expf(-g1));
         act[e] = pack_bf16(s0 * u0, s1 * u1);
       }
     }

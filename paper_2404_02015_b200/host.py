@@ -15,6 +15,7 @@ from typing import Iterable, Sequence
 
 from ._lib import (ALLOC_OK, ALLOC_POOL, ALLOC_QUOTA, LlmEntry as _CEntry, PlacedLlm, Record,
                    Request as _CRequest, SimConfig, UnitConfig, check, lib)
+from ._lib import RouteRecord as _RouteRecord
 from ._lib import PoolSample as _PoolSample, UnitLlmStats as _UnitLlmStats, UnitStats as _UnitStats
 
 # ----------------------------------------------------------------- model specs
@@ -534,6 +535,30 @@ class Unit:
     def probe_smids(self, partition: int, blocks: int):
         out = (C.c_int * blocks)()
         check(lib.mux_unit_probe_smids(self._h, partition, blocks, out))
+        return list(out)
+
+    def route_log(self) -> list[dict]:
+        """Jobs of the last engine run with option sm_route: pass, job, llm,
+        kind (0 prefill / 1 decode), sm_demand, SM run and its SM count."""
+        n = C.c_int64()
+        check(lib.mux_unit_route_log(self._h, None, 0, C.byref(n)))
+        buf = (_RouteRecord * max(n.value, 1))()
+        check(lib.mux_unit_route_log(self._h, buf, n.value, C.byref(n)))
+        return [{"pass": r.pass_, "job": r.job, "llm": r.llm, "kind": r.kind, "sm_demand": r.sm_demand,
+                 "first_unit": r.first_unit, "units": r.units, "sms": r.sms, "workspace": r.workspace,
+                 "busy_units": r.busy_units}
+                for r in buf[:n.value]]
+
+    def route_units(self) -> list[int]:
+        """SMs of each green-context unit of the device (sm_route's granules)."""
+        n = C.c_int()
+        buf = (C.c_int * 64)()
+        check(lib.mux_unit_route_units(self._h, C.byref(n), buf, 64))
+        return list(buf[:n.value])
+
+    def probe_route(self, first_unit: int, units: int, blocks: int) -> list[int]:
+        out = (C.c_int * blocks)()
+        check(lib.mux_unit_probe_route(self._h, first_unit, units, blocks, out))
         return list(out)
 
     def launches(self) -> int:

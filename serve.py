@@ -52,7 +52,7 @@ def make_trace(models, rates, horizon_s, seed, max_len=2048):
 
 def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, device=0, partition_sms=None,
           scheduler="adbs", gpu_memory_gib=180.0, lengths=None, prefill_on_partition=False, pass_green=None,
-          realtime=False, align_decode=False):
+          realtime=False, align_decode=False, sm_route=False):
     """lengths: optional per-model (prompt, output) constants (contention runs).
     partition_sms: [0, sms of model 0's partition, ...] (static partitions).
     pass_green: per-model green partition SMs, used only by passes holding
@@ -87,6 +87,8 @@ def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, 
         unit.set_option("prefill_on_partition", int(prefill_on_partition))
         unit.set_option("pass_green", int(pass_green is not None))
         unit.set_option("align_decode", int(align_decode))
+        if sm_route:  # every job on a green context sized by its ADBS sm_demand
+            unit.set_option("sm_route", 1)
         unit.init_kv(seed=5, std=1.0)
         t0 = time.perf_counter()
         recs, _ = unit.run_lockstep(entries, trace, gpu_mem, params, measured=not realtime, realtime=realtime)
@@ -112,7 +114,7 @@ def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, 
                      "scheduler": scheduler, "gpu_memory_gib": gpu_memory_gib,
                      "partition_sms": partition_sms, "prefill_on_partition": prefill_on_partition,
                      "pass_green": pass_green, "engine": "realtime" if realtime else "measured",
-                     "align_decode": align_decode},
+                     "align_decode": align_decode, "sm_route": sm_route},
         "passes": passes, "green_passes": green_passes,
         "host_wall_s": round(wall, 2),
     }
@@ -136,6 +138,8 @@ def main():
     ap.add_argument("--scheduler", choices=["adbs", "fcfs", "rr"], default="adbs")
     ap.add_argument("--gpu-memory-gib", type=float, default=180.0)
     ap.add_argument("--lengths", default=None, help="per-model constant prompt:output, e.g. 128:384,64:64")
+    ap.add_argument("--sm-route", action="store_true",
+                    help="run every ADBS job on a green context sized by its sm_demand (option sm_route)")
     args = ap.parse_args()
     models = args.models.split(",")
     rates = [float(x) for x in args.rates.split(",")]
@@ -145,7 +149,7 @@ def main():
                            gpu_memory_gib=args.gpu_memory_gib, lengths=lengths,
                            prefill_on_partition=bool(args.prefill_on_partition),
                            pass_green=args.pass_green, realtime=args.realtime,
-                           align_decode=args.align_decode)), flush=True)
+                           align_decode=args.align_decode, sm_route=args.sm_route)), flush=True)
 
 
 if __name__ == "__main__":

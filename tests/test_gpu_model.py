@@ -526,3 +526,62 @@ def test_muxsim_cli_lockstep_on_gpu_matches_reference_outputs(cuda, tmp_path):
     rj = json.loads((tmp_path / "rt" / "metrics.json").read_text())
     assert list(rj) == list(mj) and [m["name"] for m in rj["models"]] == ["chat-7b", "chat-13b"]
     assert len((tmp_path / "rt" / "records.csv").read_text().splitlines()) == 41
+
+
+@pytest.mark.parametrize("measured", [False, True])
+def test_sm_route_runs_each_job_on_its_sm_demand(cuda, measured):
+    """Option sm_route (ADBS sm_demand -> SM groups, scheduler.cpp:50-54,95):
+    config 1 through the engine with every job on a green context sized by
+    its JobPlan.sm_demand. Checks: a job's SM run is disjoint from the units
+    held by every other in-flight job; its size is round(sm_demand x SMs) or
+    the largest free run; the units are disjoint SM sets on the hardware
+    (%smid probe); records equal the priced engine's (lockstep) and tokens
+    pass the oracle."""
+    specs = [mux.spec("tiny-a"), mux.spec("tiny-b")]
+    unit = mux.Unit(specs, pool_blocks=232999, device_pool_blocks=232999, max_batch=64,
+                    max_prefill_tokens=4096, max_ctx=4096, partitions=3)
+    try:
+        weights = [load_weights(unit, i, s, 400 + i) for i, s in enumerate(specs)]
+        rope = llama_ref.rope_table(4096 + 16)
+        refs = [llama_ref.RefLlama(dims_of(s), w, rope) for s, w in zip(specs, weights)]
+        unit.set_option("sm_route", 1)
+        with open(os.path.join(GOLDEN, "sim_cfg1_tiny.json")) as f:
+            g = json.load(f)
+        names = [s.name for s in specs]
+        entries = [mux.Entry(specs[names.index(n)], rate, mp, mo) for (n, L, H, hid, wb, rate, mp, mo) in g["entries"]]
+        trace = [mux.TraceRequest(i, names.index(llm), a, p, min(o, 24)) for (i, llm, a, p, o) in g["trace"]
+                 if a < 10.0]
+        params = mux.EngineParams(decode_sm=0.4, prefill_min_sm=0.3)
+        recs, tokens = unit.run_lockstep(entries, trace, g["gpu_memory_bytes"], params=params, prompt_seed=11,
+                                         measured=measured)
+        if not measured:
+            want = mux.simulate(entries, trace, mux.Placement([1], [[0, 1]]), g["gpu_memory_bytes"], params)
+            assert [(r.id, r.first_token_s, r.done_s) for r in recs] == [(r.id, r.first_token_s, r.done_s) for r in want]
+        assert all(len(t) == r.output_len for t, r in zip(tokens, trace))
+        log = unit.route_log()
+        usms = unit.route_units()
+        total = sum(usms)
+        assert len(log) > 10 and {r["kind"] for r in log} == {0, 1}
+        for r in log:
+            assert r["first_unit"] >= 0, r
+            run = sum(1 << k for k in range(r["first_unit"], r["first_unit"] + r["units"]))
+            assert run & r["busy_units"] == 0, r                      # disjoint from in-flight jobs
+            assert r["sms"] == sum(usms[r["first_unit"]:r["first_unit"] + r["units"]])
+            want_sms = max(1, round(r["sm_demand"] * total))
+            if r["sms"] < want_sms:  # only when no free run was long enough
+                free = [k for k in range(len(usms)) if not (r["busy_units"] >> k) & 1]
+                assert all(sum(usms[i:j]) <= r["sms"] for i in free for j in range(i + 1, len(usms) + 1)
+                           if all(not (r["busy_units"] >> k) & 1 for k in range(i, j))), r
+            else:  # the shortest prefix reaching the demand
+                assert r["sms"] - usms[r["first_unit"] + r["units"] - 1] < want_sms, r
+        # the units are disjoint SM sets on the device
+        ids = [set(unit.probe_route(k, 1, 4 * n)) for k, n in enumerate(usms)]
+        for a in range(len(ids)):
+            assert len(ids[a]) <= usms[a]
+            for b in range(a + 1, len(ids)):
+                assert ids[a].isdisjoint(ids[b]), (a, b)
+        for llm in (0, 1):
+            for r, toks in [(r, t) for r, t in zip(trace, tokens) if r.llm == llm][:5]:
+                check_tokens(refs[llm], lockstep_prompt(11, r.id, r.prompt_len, specs[llm].vocab), toks)
+    finally:
+        unit.close()
