@@ -69,7 +69,9 @@ MUX_API int mux_adapt_quota(int n, const double* utilizations, const int64_t* qu
 typedef struct mux_pool mux_pool;
 
 /* BlockPool(total_blocks) (kv_manager.hpp:50). physical != 0 also assigns
- * physical 4 KiB head-block ids (the B200 extension). */
+ * physical 4 KiB head-block ids (the B200 extension); physical = k > 1 shards
+ * them head-wise over k tensor-parallel ranks, each rank's ids in
+ * [0, total_blocks / k) (a TP mesh's per-GPU pool slices). */
 MUX_API int mux_pool_create(int64_t total_blocks, int physical, mux_pool** out);
 MUX_API void mux_pool_destroy(mux_pool* pool);
 /* register_llm (kv_manager.hpp:53). */

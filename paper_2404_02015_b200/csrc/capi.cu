@@ -414,6 +414,7 @@ class GpuExecutor : public muxsim::JobExecutor {
   }
 
   bool measured() const override { return measured_ && !realtime_; }
+  int physical_shards() const override { return u_->models.empty() ? 1 : u_->models[0]->dims().tp_size; }
   bool realtime() const override { return realtime_; }
 
   // Real-time clock: host steady clock since the run started plus the idle
@@ -471,7 +472,7 @@ class GpuExecutor : public muxsim::JobExecutor {
     if (specs.size() != u_->models.size()) throw std::invalid_argument("lockstep: model count mismatch");
     for (size_t i = 0; i < specs.size(); ++i) {
       const mux::ModelDims& d = u_->models[i]->dims();
-      if (specs[i]->num_layers != d.layers || specs[i]->num_heads != d.heads)
+      if (specs[i]->num_layers != d.layers || specs[i]->num_heads != d.heads * d.tp_size)
         throw std::invalid_argument("lockstep: model " + specs[i]->name + " does not match the unit");
     }
     if (pool.total_blocks() > INT32_MAX) throw std::invalid_argument("lockstep: pool too large");
@@ -770,7 +771,7 @@ int mux_pool_create(int64_t total_blocks, int physical, mux_pool** out) {
     auto p = std::make_unique<mux_pool>();
     p->owned = std::make_unique<BlockPool>(total_blocks);
     p->bp = p->owned.get();
-    if (physical) p->bp->enable_physical();
+    if (physical) p->bp->enable_physical(physical);  // physical > 1: ids sharded over that many TP ranks
     *out = p.release();
   });
 }
@@ -1528,6 +1529,12 @@ int run_unit(mux_unit* u, const mux_sim_config* cfg, int n_entries, const mux_ll
              bool measured, bool realtime = false) {
   return guarded([&] {
     require(cfg->n_units == 1, "lockstep: single-unit placements only");
+    const int tp = u->models.empty() ? 1 : u->models[0]->dims().tp_size;
+    require(cfg->unit_mesh_size != nullptr && cfg->unit_mesh_size[0] == tp,
+            "GPU engines: the unit's mesh size must equal the unit's tensor-parallel size");
+    // every rank of a mesh must take the same decisions: priced durations
+    // (lockstep) are rank-independent, measured device times are not
+    require(tp == 1 || (!measured && !realtime), "tensor-parallel units run the lockstep engine only");
     // The kernels address 16-token head-blocks of 128 bf16 dims (4 KiB,
     // kv_manager.cpp:37-40 at the catalog's geometry); the host pool must
     // build rows of the same size.

@@ -489,8 +489,13 @@ void Runtime::upload_rows(muxsim::BlockPool& bp, int llm, Llama& m, cudaStream_t
   check_cuda(cudaSetDevice(device_), "cudaSetDevice");  // units of one process may sit on different GPUs
   std::vector<muxsim::RowDelta>& pend = bp.pending_rows(llm);
   if (pend.empty()) return;
+  // A tensor-parallel rank holds heads [r*H/tp, (r+1)*H/tp) of every row:
+  // its columns (layer, local head, kv) of the mesh-wide row record, whose
+  // ids are already rank-local (BlockPool::enable_physical(tp)).
   const int W = m.row_width();
-  if (W != bp.row_width(llm)) throw std::logic_error("upload_rows: row width mismatch");
+  const int tp = m.dims().tp_size, rank = m.dims().tp_rank, hl = m.dims().heads;
+  if (W * tp != bp.row_width(llm)) throw std::logic_error("upload_rows: row width mismatch");
+  if (tp > 1 && bp.shards() != tp) throw std::logic_error("upload_rows: pool ids are not sharded over the TP ranks");
   const size_t n = pend.size();
   const size_t meta_ints = (3 * n + 3) & ~size_t(3);  // keep the id block 16-byte aligned
   const size_t need = (meta_ints + n * static_cast<size_t>(W)) * 4;
@@ -521,8 +526,11 @@ void Runtime::upload_rows(muxsim::BlockPool& bp, int llm, Llama& m, cudaStream_t
     meta[3 * i + 2] = d.rowrec;
     const int32_t* src = bp.row_ids(llm, d.rowrec);
     for (int j = 0; j < W; ++j) {
-      if (src[j] >= pool_blocks_) throw std::runtime_error("upload_rows: block id beyond the device pool");
-      ids[i * W + j] = src[j];
+      // local column (l*hl + h)*2 + kv  <-  mesh column (l*hl*tp + rank*hl + h)*2 + kv
+      const int lh = j >> 1, l = lh / hl, h = lh - l * hl;
+      const int32_t id = tp == 1 ? src[j] : src[((l * hl * tp + rank * hl + h) << 1) | (j & 1)];
+      if (id >= pool_blocks_) throw std::runtime_error("upload_rows: block id beyond the device pool");
+      ids[i * W + j] = id;
     }
   }
   check_cuda(cudaMemcpyAsync(slot.dev.p, slot.host->p, need, cudaMemcpyHostToDevice, stream), "stage copy");

@@ -95,6 +95,9 @@ class JobExecutor {
   virtual ~JobExecutor() = default;
   // Physical head-block ids are needed by any executor that touches KV.
   virtual bool wants_physical() const { return true; }
+  // Tensor-parallel ranks the physical ids are sharded over (head-wise,
+  // BlockPool::enable_physical); 1 = one device pool for the whole unit.
+  virtual int physical_shards() const { return 1; }
   virtual void attach_unit(int unit, const std::vector<const LLMSpec*>& specs, BlockPool& pool) = 0;
   // After one scheduling pass, before its launches: upload new block-table rows.
   virtual void begin_pass(int unit, BlockPool& pool) = 0;

@@ -78,7 +78,14 @@ class BlockPool {
   // Turn on physical id assignment. Must be called before any allocation.
   // Ids are int32 in [0, total_blocks). Every registered model gets a slot
   // space (one device block-table row list per live request).
-  void enable_physical();
+  // shards > 1 (a tensor-parallel mesh): the pool is head-sharded
+  // over `shards` ranks, each holding floor(total / shards) blocks of its own
+  // device memory. A row's column (layer, head, kv) takes a rank-local id
+  // from the free stack of rank head / (H / shards); every row costs
+  // 2*L*H / shards blocks per rank, so the mesh-wide count check (the
+  // reference's decisions, unchanged) implies every rank's stack has room.
+  void enable_physical(int shards = 1);
+  int shards() const { return shards_; }
   bool physical() const { return physical_; }
   int rows_of(int llm, std::int64_t request_id) const;
   int slot_of(int llm, std::int64_t request_id) const;
@@ -94,7 +101,9 @@ class BlockPool {
   std::vector<RowDelta>& pending_rows(int llm);
   // Physical block table of one request, [rows][layer][head][kv] flattened.
   std::vector<std::int32_t> block_table(int llm, std::int64_t request_id) const;
-  std::int64_t physical_free() const { return static_cast<std::int64_t>(free_ids_.size()); }
+  std::int64_t physical_free() const;
+  // Shard (tensor-parallel rank) of column j of a row of `llm`.
+  int shard_of_column(int llm, int j) const;
 
  private:
   struct Req {
@@ -144,7 +153,8 @@ class BlockPool {
   std::int64_t committed_total_ = 0;
   std::vector<Model> llms_;
   bool physical_ = false;
-  std::vector<std::int32_t> free_ids_;  // LIFO; back() is the next id handed out
+  int shards_ = 1;
+  std::vector<std::vector<std::int32_t>> free_ids_;  // per shard, LIFO; back() is the next id handed out
 };
 
 struct QuotaInput {

@@ -123,11 +123,12 @@ _ERR = {ALLOC_OK: "none", ALLOC_POOL: "pool", ALLOC_QUOTA: "quota"}
 class BlockPool:
     """kv_manager.hpp:48-105 over the C ABI, with physical head-block ids."""
 
-    def __init__(self, total_blocks: int, physical: bool = True, _handle=None):
+    def __init__(self, total_blocks: int, physical: bool = True, _handle=None, shards: int = 1):
+        """shards > 1: physical ids sharded head-wise over that many TP ranks."""
         self._owned = _handle is None
         if _handle is None:
             h = C.c_void_p()
-            check(lib.mux_pool_create(total_blocks, 1 if physical else 0, C.byref(h)))
+            check(lib.mux_pool_create(total_blocks, (shards if shards > 1 else 1) if physical else 0, C.byref(h)))
             _handle = h.value
         self._h = _handle
 
@@ -265,6 +266,7 @@ class Placement:
     members: list[list[int]]                 # per unit: entry indices
     num_sm: float = 0.5
     tp_degree: dict = field(default_factory=dict)  # entry index -> plan tp_degree (metrics' placed_tp)
+    gpu_ids: list = field(default_factory=list)    # per unit: the plan's gpu_ids (empty: consecutive)
 
 
 @dataclass
@@ -576,15 +578,17 @@ class Unit:
     def run_lockstep(self, entries: Sequence[Entry], trace: Sequence[TraceRequest],
                      gpu_memory_bytes: int, params: EngineParams | None = None,
                      prompt_seed: int = 11, num_sm: float = 0.5, profile=None, measured: bool = False,
-                     realtime: bool = False):
+                     realtime: bool = False, mesh_size: int = 1):
         """Engine decisions priced by the oracle model, every job run on this GPU
+        (mesh_size > 1: this unit is one rank of a tensor-parallel mesh of that
+        many GPUs, created with tp_size = mesh_size; lockstep only)
         (measured=True: job durations are the measured device times instead;
         realtime=True: jobs overlap across passes and complete when their
         device events fire, mux_unit_run_realtime).
         Returns (records, tokens) with tokens[i] the output of trace[i]."""
         params = params or EngineParams()
-        placement = Placement([1], [list(range(len(entries)))], num_sm)
-        b = _build_config(gpu_memory_bytes, 1, placement, params, profile)
+        placement = Placement([mesh_size], [list(range(len(entries)))], num_sm)
+        b = _build_config(gpu_memory_bytes, mesh_size, placement, params, profile)
         ents = _c_entries(entries, b.keep)
         recs = (Record * max(len(trace), 1))()
         total = sum(r.output_len for r in trace)

@@ -14,7 +14,9 @@ Engines:
   measured  job completions at measured device time (real serving latencies)
   realtime  jobs overlap across passes, completions when their device events
             fire (mux_unit_run_realtime; concurrency and contention measured)
-The GPU engines serve single-unit, single-GPU plans (one B200).
+The GPU engines run any plan: every unit on its own GPU mesh, one process
+per tensor-parallel rank (cluster.run_plan; tp > 1 units in lockstep mode).
+A box with fewer GPUs than the plan names runs the units one after another.
 Exit codes follow the reference CLI (muxsim.cpp:51-63): 1 config error,
 2 infeasible, 3 anything else.
 """
@@ -24,9 +26,32 @@ import argparse
 import os
 import sys
 
-from . import wire
+from . import cluster, wire
 from ._lib import Infeasible, InvalidArgument
 from .host import Unit, simulate
+
+
+def _run_single(exp, placement, trace, engine):
+    """A one-GPU plan, in this process."""
+    specs = [exp.entries[i].spec for i in placement.members[0]]
+    logical = cluster.unit_pool_blocks(specs, 1, exp.gpu_memory_bytes, exp.params.activation_reserve_frac)
+    longest = max((r.prompt_len + r.output_len for r in trace), default=16)
+    unit = Unit(specs, pool_blocks=logical, device_pool_blocks=logical, max_batch=512,
+                max_prefill_tokens=max(exp.params.token_budget, longest), max_ctx=longest + 16,
+                max_slots=len(trace) + 8, init_seed=1, init_std=0.02, partitions=len(specs) + 1)
+    try:
+        recs, _ = unit.run_lockstep([exp.entries[i] for i in placement.members[0]], trace,
+                                    exp.gpu_memory_bytes, exp.params, profile=exp.profile,
+                                    measured=engine == "measured", realtime=engine == "realtime")
+        units = unit.last_stats()
+        mem = placement.members[0]  # unit-local entry index -> config entry index
+        for u in units:
+            for m in u.llms:
+                m.llm = mem[m.llm]
+            u.samples = [(t, mem[li], used, q) for t, li, used, q in u.samples]
+    finally:
+        unit.close()
+    return recs, units
 
 
 def run(cfg_path: str, plan_path: str, trace_path: str, out_dir: str, engine: str = "priced") -> list:
@@ -37,30 +62,16 @@ def run(cfg_path: str, plan_path: str, trace_path: str, out_dir: str, engine: st
         recs, units = simulate(exp.entries, trace, placement, exp.gpu_memory_bytes, exp.params, exp.profile,
                                stats=True)
     else:
-        if len(placement.mesh_sizes) != 1 or placement.mesh_sizes[0] != 1:
-            raise wire.ConfigError("GPU engines serve a single-unit, single-GPU plan")
-        specs = [exp.entries[i].spec for i in placement.members[0]]
-        weights = sum(s.weight_bytes for s in specs)
         if exp.params.block_tokens != 16:
             raise wire.ConfigError("GPU engines: sim.block_tokens must be 16 (the kernels' 4 KiB head-blocks)")
-        block_bytes = 128 * exp.params.block_tokens * 2  # head_dim * block_tokens * bpe (kv_manager.cpp:37-40)
-        logical = (exp.gpu_memory_bytes - weights - round(exp.params.activation_reserve_frac * exp.gpu_memory_bytes)) // block_bytes
-        longest = max((r.prompt_len + r.output_len for r in trace), default=16)
-        unit = Unit(specs, pool_blocks=logical, device_pool_blocks=logical, max_batch=512,
-                    max_prefill_tokens=max(exp.params.token_budget, longest), max_ctx=longest + 16,
-                    max_slots=len(trace) + 8, init_seed=1, init_std=0.02, partitions=len(specs) + 1)
-        try:
-            recs, _ = unit.run_lockstep([exp.entries[i] for i in placement.members[0]], trace,
-                                        exp.gpu_memory_bytes, exp.params, profile=exp.profile,
-                                        measured=engine == "measured", realtime=engine == "realtime")
-            units = unit.last_stats()
-            mem = placement.members[0]  # unit-local entry index -> config entry index
-            for u in units:
-                for m in u.llms:
-                    m.llm = mem[m.llm]
-                u.samples = [(t, mem[li], used, q) for t, li, used, q in u.samples]
-        finally:
-            unit.close()
+        if len(placement.mesh_sizes) == 1 and placement.mesh_sizes[0] == 1:
+            recs, units = _run_single(exp, placement, trace, engine)
+        else:  # every unit on its own GPU mesh, one process per rank (cluster.run_plan)
+            try:
+                recs, units, _ = cluster.run_plan(exp.entries, trace, placement, exp.gpu_memory_bytes, exp.params,
+                                                  exp.profile, engine)
+            except ValueError as e:
+                raise wire.ConfigError(str(e)) from None
     report = wire.compute_metrics(recs, exp, placement)
     os.makedirs(out_dir, exist_ok=True)
     wire.write_records_csv(os.path.join(out_dir, "records.csv"), recs, exp.names)

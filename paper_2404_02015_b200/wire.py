@@ -374,11 +374,12 @@ def load_plan(path: str, names: list[str]) -> Placement:
             raise ConfigError(f"plan: invalid JSON: {e}") from None
     if not isinstance(root, dict) or not isinstance(root.get("units"), list):
         raise ConfigError("plan: expected an object with a 'units' array")
-    sizes, members, tp = [], [], {}
+    sizes, members, tp, gpus = [], [], {}, []
     for u in root["units"]:
         if not isinstance(u, dict) or not isinstance(u.get("gpu_ids"), list):
             raise ConfigError("plan: each unit needs a gpu_ids array")
         sizes.append(len(u["gpu_ids"]))
+        gpus.append([int(g) for g in u["gpu_ids"]])
         mem = []
         for m in u.get("models", []):
             if m.get("name") not in names:
@@ -386,7 +387,7 @@ def load_plan(path: str, names: list[str]) -> Placement:
             mem.append(names.index(m["name"]))
             tp[names.index(m["name"])] = int(m.get("tp_degree", len(u["gpu_ids"])))  # commands.cpp:205
         members.append(mem)
-    return Placement(sizes, members, tp_degree=tp)
+    return Placement(sizes, members, tp_degree=tp, gpu_ids=gpus)
 
 
 def load_trace(path: str, names: list[str]) -> list[TraceRequest]:

@@ -125,3 +125,51 @@ def test_tp_spec_rejects_unrealizable_widths():
     with pytest.raises(ValueError):
         mesh.tp_spec(mux.spec("30b"), 8)  # 52 heads, the reference planner's tp=8
     assert mesh.tp_spec(mux.spec("13b"), 2).num_heads == 20
+
+
+@pytest.mark.parametrize("tp", [2, 4])
+def test_sharded_physical_ids_keep_mesh_decisions(tp):
+    """BlockPool.enable_physical(tp) (a TP mesh's pool): the
+    mesh-wide count decisions are the reference's, unchanged; every column
+    (layer, head, kv) of a row gets a rank-local id of rank head / (H / tp)
+    in [0, total / tp); live ids are unique per rank; conservation holds."""
+    specs = [mux.spec("7b"), mux.spec("13b")]
+    total = 4 * 3200 * 40 + 3  # not a multiple of tp: the tail is never materialised
+    sharded = mux.BlockPool(total, physical=True, shards=tp)
+    count = mux.BlockPool(total, physical=False)
+    for p in (sharded, count):
+        for i, s in enumerate(specs):
+            p.register_llm(i, s)
+            p.set_quota(i, total // 2)
+    rng = random.Random(tp)
+    live = []
+    for k in range(3000):
+        op = rng.random()
+        if op < 0.45 or not live:
+            llm, n = rng.randrange(2), rng.randrange(1, 300)
+            extra = rng.randrange(0, 300)
+            a, b = sharded.admit(llm, k, n, n + extra), count.admit(llm, k, n, n + extra)
+            assert (a.ok, a.error) == (b.ok, b.error)
+            if a.ok:
+                live.append((llm, k))
+        elif op < 0.85:
+            llm, rid = rng.choice(live)
+            add = rng.randrange(1, 40)
+            a, b = sharded.alloc(llm, rid, add, True), count.alloc(llm, rid, add, True)
+            assert (a.ok, a.error) == (b.ok, b.error)
+        else:
+            llm, rid = live.pop(rng.randrange(len(live)))
+            sharded.free_request(llm, rid)
+            count.free_request(llm, rid)
+        sharded.check_conservation()
+        if k % 500 == 0 or k == 2999:
+            seen = [set() for _ in range(tp)]
+            for llm, rid in live:
+                H = specs[llm].num_heads
+                ids = sharded.block_table(llm, rid)
+                for j, bid in enumerate(ids):
+                    rank = ((j % (2 * specs[llm].num_layers * H)) // 2 % H) // (H // tp)
+                    assert 0 <= bid < total // tp
+                    assert bid not in seen[rank]
+                    seen[rank].add(bid)
+    assert sharded.free_blocks() == count.free_blocks()

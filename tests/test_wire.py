@@ -91,3 +91,30 @@ def test_config_validation_matches_reference(tmp_path):
     assert (exp.params.quota_low_mark, exp.params.quota_high_mark, exp.params.quota_step_frac) == (0.3, 0.6, 0.25)
     assert exp.entries[0].mean_prompt_tokens == (10 * 3 + 100 * 1) / 4  # weighted (workload.cpp:66-76)
     assert exp.entries[0].mean_output_tokens == 64.0                     # LlmConfig default (config.hpp:27)
+
+
+def test_plan_split_and_unit_pools_match_reference():
+    """cluster.split_plan routes each request to its model's unit
+    (run_simulation, sim_engine.cpp:370-413) and unit_pool_blocks is
+    UnitSim::pool_blocks (sim_engine.cpp:172-186): the reference CLI's
+    poolstats total_blocks for the 2-unit tp=2 mesh golden."""
+    import json as _json
+
+    from paper_2404_02015_b200 import cluster
+    exp = wire.load_config(os.path.join(G, "cfg_mesh.json"))
+    placement = wire.load_plan(os.path.join(G, "plan_mesh.json"), exp.names)
+    trace = wire.load_trace(os.path.join(G, "trace_mesh.csv"), exp.names)
+    assert placement.gpu_ids == [[0, 1], [2, 3]]
+    jobs = cluster.split_plan(exp.entries, trace, placement, exp.gpu_memory_bytes, exp.params, exp.profile,
+                              "lockstep")
+    assert [j.unit for j in jobs] == [0, 1] and [j.gpu_ids for j in jobs] == [[0, 1], [2, 3]]
+    assert sorted(r.id for j in jobs for r in j.trace) == sorted(r.id for r in trace)
+    for j in jobs:
+        for r in j.trace:
+            orig = next(t for t in trace if t.id == r.id)
+            assert j.members[r.llm] == orig.llm
+    with open(os.path.join(G, "poolstats_mesh.json")) as f:
+        want = [u["total_blocks"] for u in _json.load(f)["units"]]
+    got = [cluster.unit_pool_blocks([e.spec for e in j.entries], len(j.gpu_ids), exp.gpu_memory_bytes,
+                                    exp.params.activation_reserve_frac) for j in jobs]
+    assert got == want
