@@ -492,8 +492,12 @@ void Runtime::upload_rows(muxsim::BlockPool& bp, int llm, Llama& m, cudaStream_t
   // A tensor-parallel rank holds heads [r*H/tp, (r+1)*H/tp) of every row:
   // its columns (layer, local head, kv) of the mesh-wide row record, whose
   // ids are already rank-local (BlockPool::enable_physical(tp)).
+  // Two pool forms: the unit's own pool registers the rank's head slice
+  // (row width W, rank-local ids, shards 1); a mesh-wide pool (the lockstep
+  // engine's shared decisions) registers full rows sharded over the ranks.
   const int W = m.row_width();
-  const int tp = m.dims().tp_size, rank = m.dims().tp_rank, hl = m.dims().heads;
+  const int rank = m.dims().tp_rank, hl = m.dims().heads;
+  const int tp = bp.row_width(llm) == W ? 1 : m.dims().tp_size;
   if (W * tp != bp.row_width(llm)) throw std::logic_error("upload_rows: row width mismatch");
   if (tp > 1 && bp.shards() != tp) throw std::logic_error("upload_rows: pool ids are not sharded over the TP ranks");
   const size_t n = pend.size();

@@ -255,14 +255,17 @@ def test_headline_decode_tokens_match_oracle(headline):
             # Layer 0 sees the same embedding, so they differ only where the
             # QKV GEMM's bf16 rounding of an fp32 sum fell the other way
             # (then RoPE mixes two such values); deeper layers also carry the
-            # upstream bf16 noise of the residual stream.
+            # upstream bf16 noise of the residual stream. Bound for layer 0:
+            # each RoPE input off by one bf16 ulp (<= 2^-7 of its magnitude),
+            # |cos| + |sin| <= sqrt(2), plus one ulp of the output's own
+            # rounding: < 2^-6 of the row's largest value.
             want_kv = c.token_kv(pos, from_device=False)  # [B, L*H*2, 128]
             got_kv = c.token_kv(pos, from_device=True)
             wf, gf = llama_ref.bf16_to_f32(want_kv), llama_ref.bf16_to_f32(got_kv)
             rowmax = np.maximum(np.abs(wf).max(axis=2, keepdims=True), 1e-30)
             err = np.abs(wf - gf) / rowmax
             l0 = slice(0, 2 * specs[li].num_heads)
-            assert err[:, l0].max() <= 2.0 ** -7, (specs[li].name, step, float(err[:, l0].max()))
+            assert err[:, l0].max() <= 2.0 ** -6, (specs[li].name, step, float(err[:, l0].max()))
             assert np.mean(want_kv[:, l0] == got_kv[:, l0]) >= 0.95
             assert err.max() <= 2.0 ** -5, (specs[li].name, step, float(err.max()))
             # teacher forcing: the next step starts from the GPU's own history,
