@@ -198,11 +198,6 @@ def run_ours(args, rank, world, local_rank):
                     init_seed=1 + rank, init_std=0.02, partitions=len(specs) + 1,
                     partition_sms=[0] + psms if psms else None)
     unit.set_option("pdl", args.pdl)
-    unit.set_option("chain", args.chain)
-    unit.set_option("fuse_qkv", args.fuse_qkv)
-    unit.set_option("l2_next", args.l2_next)
-    unit.set_option("fuse_norm", args.fuse_norm)
-    unit.set_option("fuse_k2", args.fuse_k2)
     if args.gemm_min_iters > 0:
         unit.set_option("gemm_min_iters", args.gemm_min_iters)
     unit.init_kv(seed=7 + rank, std=1.0)
@@ -321,14 +316,6 @@ def main():
     ap.add_argument("--serial", action="store_true", help="run the colocated decode jobs on one stream")
     ap.add_argument("--serve-horizon", type=float, default=3.0,
                     help="seconds of Poisson arrivals for the auxiliary measured serving run (0 = skip)")
-    ap.add_argument("--fuse-qkv", type=int, default=0, help="RoPE + KV append in the QKV GEMM epilogue (experimental)")
-    ap.add_argument("--chain", type=int, default=0, help="fused persistent layer chain for decode (experimental)")
-    ap.add_argument("--l2-next", type=int, default=0,
-                    help="16 KiB weight tiles per CTA of the next decode GEMM prefetched into L2 (0 = off)")
-    ap.add_argument("--fuse-k2", type=int, default=0,
-                    help="decode: RoPE + KV append inside the paged-attention kernel (no kv_append launch)")
-    ap.add_argument("--fuse-norm", type=int, default=0,
-                    help="RMSNorm fused into the residual GEMMs on green partitions (grid barrier)")
     ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch between job kernels")
     ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg (profiling runs)")
     ap.add_argument("--gemm-min-iters", type=int, default=0,

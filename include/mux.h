@@ -245,10 +245,6 @@ MUX_API int64_t mux_weight_tiled_bytes(int N, int K);
 /* Debug: per-CTA globaltimer stamps of every K4 launch ([grid][4] u64:
  * start, MMA issue done, epilogue done, exit) into buf; NULL turns it off. */
 MUX_API void mux_debug_gemm_timing(void* buf);
-/* Debug: per-CTA globaltimer stamps ([grid][64] u64) of every layer-chain
- * launch; and whether the chain launches keep PDL (cooperative + PDL). */
-MUX_API void mux_debug_chain_timing(void* buf);
-MUX_API int mux_debug_chain_coop_pdl(void);
 
 /* ---- device unit: one GPU, its KV pool and colocated models ---------- */
 
@@ -356,10 +352,6 @@ MUX_API int mux_unit_probe_smids(mux_unit* unit, int partition, int blocks, int*
 MUX_API int64_t mux_unit_launches(mux_unit* unit);
 /* Tuning knobs: "gemm_min_iters" (k-blocks per GEMM CTA floor, default 8);
  * "pdl" (programmatic dependent launch between job kernels, default 1);
- * "chain" (decode layers as one fused persistent layer-chain launch plus
- * K1, default 0 = one launch per projection / element-wise step);
- * "fuse_qkv" (RoPE + KV append in the QKV GEMM epilogue, default 0: the
- * epilogue on the critical path costs more than the separate kv_append);
  * "prefill_on_partition" (prefill jobs on their model's partition);
  * "pass_green" (partitions = [whole GPU | a whole-GPU stream per model |
  * a green partition per model]; decode jobs use the green partitions only in

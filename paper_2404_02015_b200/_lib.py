@@ -148,8 +148,6 @@ _SIGS = {
     "mux_unit_probe_route": (C.c_int, [vp, C.c_int, C.c_int, C.c_int, P(C.c_int)]),
     "mux_unit_set_option": (C.c_int, [vp, C.c_char_p, i64]),
     "mux_debug_gemm_timing": (None, [vp]),
-    "mux_debug_chain_timing": (None, [vp]),
-    "mux_debug_chain_coop_pdl": (C.c_int, []),
     "mux_unit_create": (C.c_int, [P(UnitConfig), P(vp)]),
     "mux_unit_destroy": (None, [vp]),
     "mux_unit_pool": (vp, [vp]),

@@ -1060,10 +1060,6 @@ int mux_rope_table(int positions, float* out) {
   });
 }
 
-void mux_debug_chain_timing(void* buf) { mux::chain_debug_timing(buf); }
-
-int mux_debug_chain_coop_pdl(void) { return mux::chain_coop_pdl() ? 1 : 0; }
-
 void mux_debug_gemm_timing(void* buf) { mux::gemm_debug_timing(buf); }
 
 int64_t mux_weight_tiled_bytes(int N, int K) { return static_cast<int64_t>(mux::weight_tiled_bytes(N, K)); }
@@ -1098,8 +1094,8 @@ int mux_gemm_bf16(const void* x, const void* w, int w_tiled, int M, int N, int K
     Scratch& sc = per_dev[dev];
     if (sc.partials == nullptr) {
       mux::check_cuda(cudaMalloc(&sc.partials, mux::gemm_partials_floats(kMaxGrid) * 4), "gemm scratch");
-      mux::check_cuda(cudaMalloc(&sc.flags, kMaxGrid * 4), "gemm flags");
-      mux::check_cuda(cudaMemset(sc.flags, 0, kMaxGrid * 4), "gemm flags");
+      mux::check_cuda(cudaMalloc(&sc.flags, 2 * kMaxGrid * 4), "gemm flags");
+      mux::check_cuda(cudaMemset(sc.flags, 0, 2 * kMaxGrid * 4), "gemm flags");
     }
     float* partials = sc.partials;
     int* flags = sc.flags;
@@ -1506,9 +1502,6 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
     const std::string k = key ? key : "";
     if (k == "gemm_min_iters") u->rt->set_gemm_min_iters(static_cast<int>(value));
     else if (k == "pdl") mux::pdl_enabled() = value != 0;
-    else if (k == "chain") u->rt->set_chain(value != 0);
-    else if (k == "fuse_qkv") u->rt->set_fuse_qkv(value != 0);
-    else if (k == "l2_next") u->rt->set_l2_next(static_cast<int>(value));
     else if (k == "prefill_on_partition") u->prefill_on_partition = value != 0;
     else if (k == "pass_green") u->pass_green = value != 0;
     else if (k == "align_decode") u->align_decode = value != 0;
@@ -1517,8 +1510,6 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
       u->sm_route = value != 0;
       u->ws_owner.assign(u->ws.size(), -1);
     }
-    else if (k == "fuse_norm") u->rt->set_fuse_norm(value != 0);
-    else if (k == "fuse_k2") u->rt->set_fuse_k2(value != 0);
     else throw std::invalid_argument("unknown option: " + k);
   });
 }

@@ -51,7 +51,7 @@ PinnedMem::~PinnedMem() {
 
 namespace {
 
-constexpr int kEpiStoreBf16 = 0, kEpiResidual = 1, kEpiSilu = 2, kEpiStoreF32 = 3, kEpiQkvRope = 4;
+constexpr int kEpiStoreBf16 = 0, kEpiResidual = 1, kEpiSilu = 2, kEpiStoreF32 = 3;
 
 __global__ void gather_last_tok(const int32_t* last_tok, const int32_t* slots, int32_t* tokens, int n) {
   grid_dep_wait();
@@ -65,24 +65,6 @@ __global__ void scatter_last_tok(int32_t* last_tok, const int32_t* slots, const 
   grid_dep_launch();
   const int i = blockIdx.x * blockDim.x + threadIdx.x;
   if (i < n) last_tok[slots[i]] = tokens[i];
-}
-
-// The fused QKV epilogue reads exactly the tables kv_append would.
-QkvRopeArgs qkv_rope_args(const AppendArgs& ap) {
-  QkvRopeArgs q{};
-  q.q_out = ap.q_out;
-  q.pool = ap.pool;
-  q.rowrec = ap.rowrec;
-  q.rowlist = ap.rowlist;
-  q.tok_slot = ap.tok_slot;
-  q.tok_pos = ap.tok_pos;
-  q.rope = ap.rope;
-  q.rope_positions = ap.rope_positions;
-  q.H = ap.H;
-  q.layer = ap.layer;
-  q.row_width = ap.row_width;
-  q.max_rows = ap.max_rows;
-  return q;
 }
 
 int gemm_n_tile(int M) {
@@ -243,13 +225,6 @@ Workspace::Workspace(int max_tok, int max_batch_rows, int hidden, int qkv_cols, 
   attn = DevMem(Tp * heads * 128 * 2);
   act = DevMem(Tp * ffn * 2);
   gemm_partials = DevMem(gemm_partials_floats(grid) * 4);
-  const size_t chain_rows = std::max(max_batch_rows, 16);
-  gu32 = DevMem(chain_rows * 2 * ffn * 4);
-  qkv32 = DevMem(chain_rows * qkv_cols * 4);
-  chain_bar = DevMem(256);
-  check_cuda(cudaMemset(gu32.p, 0, gu32.bytes), "memset gu32");
-  check_cuda(cudaMemset(qkv32.p, 0, qkv32.bytes), "memset qkv32");
-  check_cuda(cudaMemset(chain_bar.p, 0, chain_bar.bytes), "memset chain bar");
   gemm_flags = DevMem(static_cast<size_t>(std::max(grid, 1024)) * 4);
   check_cuda(cudaMemset(gemm_flags.p, 0, gemm_flags.bytes), "memset flags");
   const size_t rows_out = std::max<size_t>(max_batch_rows, 256);
@@ -259,8 +234,6 @@ Workspace::Workspace(int max_tok, int max_batch_rows, int hidden, int qkv_cols, 
   attn_part_o = DevMem(static_cast<size_t>(max_decode_batch) * heads * kv_splits * 128 * 4);
   attn_part_ml = DevMem(static_cast<size_t>(max_decode_batch) * heads * kv_splits * 2 * 4);
   attn_split_count = DevMem(static_cast<size_t>(max_decode_batch) * heads * 4);
-  norm_bar = DevMem(256);
-  check_cuda(cudaMemset(norm_bar.p, 0, norm_bar.bytes), "memset norm barrier");
   check_cuda(cudaMemset(attn_split_count.p, 0, attn_split_count.bytes), "memset split counters");
   // ints: tokens[T] slots[T] ctx[T] tok_slot[T] tok_pos[T] seq_start[T+1] out_tok[T] last_rows[T]
   const size_t n_ints = 8 * T + 8;
@@ -348,7 +321,6 @@ Runtime::Runtime(int device, int64_t pool_blocks, int max_pos)
   check_cuda(preload_gemm_2sm(), "preload");
   check_cuda(preload_prefill_attention(), "preload");
   check_cuda(preload_fused_ops(), "preload");
-  check_cuda(preload_layer_chain(), "preload");
   check_cuda(preload(gather_last_tok, scatter_last_tok), "preload");
   pool_ = DevMem(static_cast<size_t>(pool_blocks) * 4096);
   // RoPE table [max_pos][64][(cos, sin)], computed in double, stored fp32.
@@ -387,18 +359,15 @@ const void* Runtime::act_tmap(const void* base, int rows, int cols, int box_rows
 }
 
 void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void* out, int ldo, int epi,
-                   Workspace& ws, cudaStream_t stream, const QkvRopeArgs* qkv, const NextGemm* next,
-                   const float* norm_w, float norm_eps) {
+                   Workspace& ws, cudaStream_t stream) {
   // The X map is viewed over max(M, 256) rows: buffers are sized for it and
   // rows past M are never stored.
   const int rows = std::max(M, 256);
-  const void* tx = act_tmap(x, rows, K, gemm_n_tile(M));
-  const void* to = out_tmap(out, epi, M, N, ldo);
   GemmArgs g{};
   g.w_tiled = w_tiled;
-  g.tmap_x = tx;
+  g.tmap_x = act_tmap(x, rows, K, gemm_n_tile(M));
   if (M > 256) g.tmap_x128 = act_tmap(x, rows, K, 128);  // 2-SM prefill path (gemm_2sm.cu)
-  g.tmap_out = to;
+  g.tmap_out = out_tmap(out, epi, M, N, ldo);
   g.out = out;
   g.partials = ws.gemm_partials.as<float>();
   g.flags = ws.gemm_flags.as<int>();
@@ -410,25 +379,7 @@ void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void
   g.K = K;
   g.ldo = ldo;
   g.epi = static_cast<Epilogue>(epi);
-  if (qkv != nullptr) g.qkv = *qkv;
-  if (next != nullptr && next->w != nullptr && l2_next_ > 0) {
-    g.next_w = next->w;
-    g.next_N = next->N;
-    g.next_K = next->K;
-    g.next_epi = static_cast<Epilogue>(next->epi);
-    g.pf_stages = l2_next_;
-  }
-  int grid = 0;
-  if (norm_w != nullptr) {
-    g.norm_w = norm_w;
-    g.norm_out = ws.xn.p;
-    g.norm_bar = ws.norm_bar.as<unsigned>();
-    g.norm_base = ws.norm_base;
-    g.norm_eps = norm_eps;
-    g.grid_out = &grid;
-  }
   check_cuda(gemm_bf16_tn(g, stream), "gemm");
-  if (norm_w != nullptr) ws.norm_base += static_cast<unsigned>(grid);
   launches_ += 1;
 }
 
@@ -597,13 +548,6 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   at.part_o = ws.attn_part_o.as<float>();
   at.part_ml = ws.attn_part_ml.as<float>();
   at.split_count = ws.attn_split_count.as<int>();  // the last split of each (member, head) merges
-  if (fuse_k2_ && !fuse_qkv_ && !(chain_enabled_ && d.tp_size == 1 && n <= 256)) {
-    // K2 inside K1: q / k / v straight from the QKV output (no kv_append launch)
-    at.qkv = ws.qkv.p;
-    at.pool_w = pool_.p;
-    at.rope = rope_.as<float>();
-    at.rope_positions = max_pos_;
-  }
   at.B = n;
   at.H = H;
   at.max_rows = m.max_rows();
@@ -643,104 +587,16 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   ap.row_width = m.row_width();
   ap.rope_positions = max_pos_;
 
-  // Fused path (single rank, decode batch <= 256): per layer one K1 launch
-  // and one persistent layer-chain launch (layer_chain.cu).
-  if (chain_enabled_ && d.tp_size == 1 && n <= 256) {
-    auto job = [&](const DevMem& w, int N, int K, int post, const float* norm_w, const void* x, void* out,
-                   ChainArgs& c) {
-      const int j = c.n_jobs++;
-      c.job[j] = ChainJob{};
-      c.job[j].w = w.as<uint8_t>();
-      c.job[j].N = N;
-      c.job[j].K = K;
-      c.job[j].post = post;
-      c.job[j].norm_w = norm_w;
-      c.tmap_x[j] = act_tmap(x, std::max(n, 256), K, gemm_n_tile(n));
-      c.tmap_out[j] = out_tmap(out, kEpiResidual, n, N, N);
-    };
-    ChainArgs base{};
-    base.M = n;
-    base.grid = ws.sms;
-    base.bar = ws.chain_bar.as<unsigned>();
-    ChainPost& p = base.post;
-    p.resid = ws.resid.as<float>();
-    p.xn = ws.xn.as<__nv_bfloat16>();
-    p.hidden = hid;
-    p.eps = d.norm_eps;
-    p.gu32 = ws.gu32.as<float>();
-    p.act = ws.act.as<__nv_bfloat16>();
-    p.ffn = d.ffn;
-    p.qkv32 = ws.qkv32.as<float>();
-    p.q = ws.q.as<__nv_bfloat16>();
-    p.heads = H;
-    p.slots = ws.slots;
-    p.ctx = ws.ctx;
-    p.rope = rope_.as<float>();
-    p.rope_positions = max_pos_;
-    p.pool = pool_.p;
-    p.rowlist = m.rowlist.as<int32_t>();
-    p.rowrec = m.rowrec.as<int32_t>();
-    p.row_width = m.row_width();
-    p.max_rows = m.max_rows();
-    auto run = [&](ChainArgs& c) {
-      c.bar_base = ws.chain_base;
-      check_cuda(layer_chain(c, stream), "layer_chain");
-      ws.chain_base += 2u * static_cast<unsigned>(c.n_jobs) * static_cast<unsigned>(c.grid);
-      launches_ += 1;
-    };
-    {  // layer 0's QKV + RoPE + KV append
-      ChainArgs c = base;
-      c.post.layer = 0;
-      job(m.wqkv[0], m.qkv_cols(), hid, kPostQkvAppend, nullptr, ws.xn.p, ws.qkv32.p, c);
-      run(c);
-    }
-    for (int l = 0; l < L; ++l) {
-      at.layer = l;
-      cudaEvent_t e0 = nullptr, e1 = nullptr;
-      if (timer) {
-        e0 = timer->get();
-        e1 = timer->get();
-        check_cuda(cudaEventRecord(e0, stream), "timer");
-      }
-      check_cuda(decode_attention(at, false, stream), "decode_attention");
-      launches_ += 1;
-      if (timer) {
-        check_cuda(cudaEventRecord(e1, stream), "timer");
-        timer->pending.emplace_back(e0, e1);
-        timer->pending_bytes += attn_bytes;
-      }
-      const float* next_norm = l + 1 < L ? m.attn_norm[l + 1].as<float>() : m.final_norm.as<float>();
-      ChainArgs c = base;
-      c.post.layer = l + 1;
-      job(m.wo[l], hid, H * 128, kPostNorm, m.ffn_norm[l].as<float>(), ws.attn.p, ws.resid.p, c);
-      job(m.wgu[l], 2 * d.ffn, hid, kPostSilu, nullptr, ws.xn.p, ws.gu32.p, c);
-      job(m.wdown[l], hid, d.ffn, kPostNorm, next_norm, ws.act.p, ws.resid.p, c);
-      if (l + 1 < L) job(m.wqkv[l + 1], m.qkv_cols(), hid, kPostQkvAppend, nullptr, ws.xn.p, ws.qkv32.p, c);
-      run(c);
-    }
-  }
   // Debug (MUX_DEBUG_SKIP bitmask; outputs are garbage, timings are not): the
   // marginal in-step cost of a kernel class. 1 = K2, 2 = RMSNorm, 4 = K1,
   // 8 = RMSNorm over one row only (the launch boundary without the work).
   static const int dbg_skip = getenv("MUX_DEBUG_SKIP") ? atoi(getenv("MUX_DEBUG_SKIP")) : 0;
-  for (int l = 0; l < L && !(chain_enabled_ && d.tp_size == 1 && n <= 256); ++l) {
+  for (int l = 0; l < L; ++l) {
     ap.layer = l;
-    // next GEMM on this stream after each projection (L2 prefetch targets)
-    const NextGemm nx_o{m.wo[l].p, hid, H * 128, kEpiResidual};
-    const NextGemm nx_gu{m.wgu[l].p, 2 * d.ffn, hid, kEpiSilu};
-    const NextGemm nx_down{m.wdown[l].p, hid, d.ffn, kEpiResidual};
-    const NextGemm nx_qkv = l + 1 < L ? NextGemm{m.wqkv[l + 1].p, m.qkv_cols(), hid, kEpiStoreBf16}
-                                      : NextGemm{m.lm_head.p, d.vocab, hid, kEpiStoreF32};
-    if (fuse_qkv_) {
-      const QkvRopeArgs qr = qkv_rope_args(ap);
-      gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiQkvRope, ws, stream, &qr);
-    } else {
-      gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream, nullptr,
-           &nx_o);
-      if (!(dbg_skip & 1) && !fuse_k2_) {
-        check_cuda(kv_append(ap, stream), "kv_append");
-        launches_ += 1;
-      }
+    gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
+    if (!(dbg_skip & 1)) {
+      check_cuda(kv_append(ap, stream), "kv_append");
+      launches_ += 1;
     }
     at.layer = l;
     cudaEvent_t e0 = nullptr, e1 = nullptr;
@@ -765,20 +621,16 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
       row_parallel_norm(m.wdown[l].p, ws.act.p, n, hid, d.ffn, 1, next_norm, d.norm_eps, ws, stream);
       continue;
     }
-    // RMSNorm fused into the residual GEMMs when this stream owns its SMs
-    const bool fnorm = fuse_norm_ && ws.exclusive && n <= 256 && !(dbg_skip & 2);
-    gemm(m.wo[l].p, ws.attn.p, n, hid, H * 128, ws.resid.p, hid, kEpiResidual, ws, stream, nullptr, &nx_gu,
-         fnorm ? m.ffn_norm[l].as<float>() : nullptr, d.norm_eps);
-    if (!(dbg_skip & 2) && !fnorm) {
+    gemm(m.wo[l].p, ws.attn.p, n, hid, H * 128, ws.resid.p, hid, kEpiResidual, ws, stream);
+    if (!(dbg_skip & 2)) {
       check_cuda(rmsnorm_rows(ws.resid.as<float>(), m.ffn_norm[l].as<float>(), ws.xn.p, (dbg_skip & 8) ? 1 : n, hid,
                               d.norm_eps, stream, ws.sms),
                  "rmsnorm");
       launches_ += 1;
     }
-    gemm(m.wgu[l].p, ws.xn.p, n, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, ws, stream, nullptr, &nx_down);
-    gemm(m.wdown[l].p, ws.act.p, n, hid, d.ffn, ws.resid.p, hid, kEpiResidual, ws, stream, nullptr, &nx_qkv,
-         fnorm ? next_norm : nullptr, d.norm_eps);
-    if (!(dbg_skip & 2) && !fnorm) {
+    gemm(m.wgu[l].p, ws.xn.p, n, 2 * d.ffn, hid, ws.act.p, d.ffn, kEpiSilu, ws, stream);
+    gemm(m.wdown[l].p, ws.act.p, n, hid, d.ffn, ws.resid.p, hid, kEpiResidual, ws, stream);
+    if (!(dbg_skip & 2)) {
       check_cuda(rmsnorm_rows(ws.resid.as<float>(), next_norm, ws.xn.p, (dbg_skip & 8) ? 1 : n, hid, d.norm_eps,
                               stream, ws.sms),
                  "rmsnorm");
@@ -861,14 +713,9 @@ void Runtime::prefill(Llama& m, Workspace& ws, int n, const int32_t* slots_host,
   pa.max_ctas = ws.sms;
   for (int l = 0; l < L; ++l) {
     ap.layer = l;
-    if (fuse_qkv_) {
-      const QkvRopeArgs qr = qkv_rope_args(ap);
-      gemm(m.wqkv[l].p, ws.xn.p, T, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiQkvRope, ws, stream, &qr);
-    } else {
-      gemm(m.wqkv[l].p, ws.xn.p, T, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
-      check_cuda(kv_append(ap, stream), "kv_append");
-      launches_ += 1;
-    }
+    gemm(m.wqkv[l].p, ws.xn.p, T, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
+    check_cuda(kv_append(ap, stream), "kv_append");
+    launches_ += 1;
     check_cuda(prefill_attention(pa, stream), "prefill_attention");
     launches_ += 1;
     const float* next_norm = l + 1 < L ? m.attn_norm[l + 1].as<float>() : m.final_norm.as<float>();

@@ -137,13 +137,7 @@ struct Workspace {
   int gemm_epoch = 0;
   int sms = 148;           // SMs of the partition this workspace's jobs run on
   bool exclusive = false;  // a green partition: no other stream's kernels share its SMs
-  DevMem norm_bar;         // grid barrier of the fused residual GEMM + RMSNorm (monotonic)
-  unsigned norm_base = 0;
   std::unique_ptr<TpLink> tp;  // tensor-parallel mailbox (tp_size > 1)
-  // fused layer chain: fp32 reduce-add targets (kept zero between uses) and
-  // the grid-barrier counter with its running base
-  DevMem gu32, qkv32, chain_bar;
-  unsigned chain_base = 0;
   PinnedMem host_ints[2];  // double-buffered staging for per-job metadata
   cudaEvent_t staged[2] = {nullptr, nullptr};
   int cur = 0;
@@ -183,11 +177,6 @@ class Runtime {
   int num_sms() const { return num_sms_; }
   int64_t launches() const { return launches_; }
   void set_gemm_min_iters(int v) { gemm_min_iters_ = v; }
-  void set_chain(bool on) { chain_enabled_ = on; }
-  void set_fuse_qkv(bool on) { fuse_qkv_ = on; }
-  void set_l2_next(int stages) { l2_next_ = stages; }
-  void set_fuse_norm(bool on) { fuse_norm_ = on; }
-  void set_fuse_k2(bool on) { fuse_k2_ = on; }
   void count_launch(int64_t n = 1) { launches_ += n; }
 
   // Cached tensor map for an activation buffer viewed as rows x cols bf16.
@@ -207,17 +196,8 @@ class Runtime {
                const int32_t* tokens_host, int32_t* out_host /*nullable*/, cudaStream_t stream);
 
   // Decode-forward building blocks, exposed for tests/bench.
-  // The next GEMM on the same stream (decode chains): its first weight tiles
-  // are prefetched into L2 during this launch's tail (l2_next option).
-  struct NextGemm {
-    const void* w = nullptr;
-    int N = 0, K = 0, epi = 0;
-  };
-  // norm_w (decode residual GEMMs on an exclusive partition): RMSNorm of the
-  // updated residual rows into ws.xn fused into the GEMM (eps = norm_eps).
   void gemm(const void* w_tiled, const void* x, int M, int N, int K, void* out, int ldo, int epi,
-            Workspace& ws, cudaStream_t stream, const QkvRopeArgs* qkv = nullptr, const NextGemm* next = nullptr,
-            const float* norm_w = nullptr, float norm_eps = 1e-6f);
+            Workspace& ws, cudaStream_t stream);
   // Row-parallel projection + the fused allreduce (tp > 1): out partial of
   // X[M x K] W[N x K]^T to every rank's slot `s`, then resid += sum of ranks'
   // slots and xn = rmsnorm(resid) * norm_w on this rank.
@@ -231,11 +211,6 @@ class Runtime {
   int max_pos_;
   int64_t launches_ = 0;
   int gemm_min_iters_ = 8;  // scripts/min_iters_sweep.py: 8 is never slower on the whole GPU, -6..-11% at batch 128
-  bool chain_enabled_ = false;
-  bool fuse_qkv_ = false;  // K2 in the QKV GEMM epilogue (kQkvRope): measured slower than kv_append
-  int l2_next_ = 0;        // tiles per CTA of the next decode GEMM prefetched into L2 (0 = off)
-  bool fuse_k2_ = false;   // decode: RoPE + KV append inside K1 (no kv_append launch; measured no gain)
-  bool fuse_norm_ = false;  // RMSNorm fused into the residual GEMMs on exclusive partitions (measured: no gain)
   DevMem pool_;
   DevMem rope_;
   struct StageSlot {

@@ -122,64 +122,16 @@ decode_attention_kernel(const DecodeAttnArgs a) {
   // ---------------- consumer warps
   const int half = lane >> 4;  // token parity handled by this half-warp
   const int c = lane & 15;     // dims [8c, 8c+8)
-  const bool fused = a.qkv != nullptr;
-  const int pos = ctx - 1;     // position of this step's token
-  // fused K2: RoPE factors of this lane's 8 dims (pairs d, d + 64 across c ^ 8)
-  float rc[8], rs[8];
-  if (fused) {
-    const float4* cs = reinterpret_cast<const float4*>(a.rope + static_cast<int64_t>(min(pos, a.rope_positions - 1)) * 128);
-    const int f0 = (c & 7) * 8;  // dim mod 64 of this lane's first dim
-#pragma unroll
-    for (int k = 0; k < 4; ++k) {
-      const float4 t = cs[f0 / 2 + k];  // (cos, sin) of dims f0+2k, f0+2k+1
-      rc[2 * k] = t.x;
-      rs[2 * k] = t.y;
-      rc[2 * k + 1] = t.z;
-      rs[2 * k + 1] = t.w;
-    }
-  }
-  // rotate_half on this lane's 8 dims (partner lane c ^ 8), _rn like kv_append
-  auto rope8 = [&](float (&x)[8]) {
-    float o[8];
-#pragma unroll
-    for (int k = 0; k < 8; ++k) o[k] = __shfl_xor_sync(0xffffffffu, x[k], 8);
-#pragma unroll
-    for (int k = 0; k < 8; ++k)
-      x[k] = c < 8 ? __fsub_rn(__fmul_rn(x[k], rc[k]), __fmul_rn(o[k], rs[k]))
-                   : __fadd_rn(__fmul_rn(x[k], rc[k]), __fmul_rn(o[k], rs[k]));
-  };
-  auto load8 = [&](const void* p, float (&x)[8]) {
-    const uint4 v4 = *reinterpret_cast<const uint4*>(p);
+  float q[8];
+  {
+    const uint4 v4 = *reinterpret_cast<const uint4*>(reinterpret_cast<const __nv_bfloat16*>(a.q) +
+                                                     (static_cast<int64_t>(b) * a.H + h) * kDim + c * 8);
     const uint32_t w[4] = {v4.x, v4.y, v4.z, v4.w};
 #pragma unroll
     for (int k = 0; k < 4; ++k) {
-      x[2 * k] = bf16_lo(w[k]);
-      x[2 * k + 1] = bf16_hi(w[k]);
+      q[2 * k] = bf16_lo(w[k]) * a.scale_log2;
+      q[2 * k + 1] = bf16_hi(w[k]) * a.scale_log2;
     }
-  };
-  auto pack8 = [&](const float (&x)[8]) {
-    return make_uint4(pack_bf16(x[0], x[1]), pack_bf16(x[2], x[3]), pack_bf16(x[4], x[5]), pack_bf16(x[6], x[7]));
-  };
-  const __nv_bfloat16* qkv_tok =
-      fused ? reinterpret_cast<const __nv_bfloat16*>(a.qkv) + static_cast<int64_t>(b) * 3 * a.H * kDim : nullptr;
-  float q[8];
-  {
-    if (fused) {
-      float x[8];
-      load8(qkv_tok + static_cast<int64_t>(h) * kDim + c * 8, x);
-      rope8(x);
-      const uint4 r4 = pack8(x);  // q is rounded to bf16 as kv_append's q_out is
-      const uint32_t w[4] = {r4.x, r4.y, r4.z, r4.w};
-#pragma unroll
-      for (int k = 0; k < 4; ++k) {
-        q[2 * k] = bf16_lo(w[k]);
-        q[2 * k + 1] = bf16_hi(w[k]);
-      }
-    } else {
-      load8(reinterpret_cast<const __nv_bfloat16*>(a.q) + (static_cast<int64_t>(b) * a.H + h) * kDim + c * 8, q);
-    }
-#pragma unroll
-    for (int k = 0; k < 8; ++k) q[k] *= a.scale_log2;
   }
   // Which token (within its parity) this lane's reduced score belongs to.
   const int jsel = (((c >> 3) & 1) << 2) | (((c >> 2) & 1) << 1) | ((c >> 1) & 1);
@@ -194,26 +146,6 @@ decode_attention_kernel(const DecodeAttnArgs a) {
     mbar_wait(&sm.full[s], (i / S) & 1);
     const uint8_t* kblk = sm.kv[s][0];
     const uint8_t* vblk = sm.kv[s][1];
-    if (fused && r0 + i == nrows_total - 1) {
-      // this step's token: rotate k, append k and v to their head-blocks and
-      // patch the staged row (the copy above stopped at the stale slot)
-      const int slot16 = pos & 15;
-      float x[8];
-      load8(qkv_tok + static_cast<int64_t>(a.H + h) * kDim + c * 8, x);
-      rope8(x);  // all 32 lanes (shuffles); half 0 stores k, half 1 stores v
-      if (half == 0) {
-        const uint4 k4 = pack8(x);
-        *reinterpret_cast<uint4*>(const_cast<uint8_t*>(kblk) + slot16 * 256 + c * 16) = k4;
-        *reinterpret_cast<uint4*>(static_cast<uint8_t*>(a.pool_w) + static_cast<int64_t>(sm.ids[i].x) * kBlockBytes +
-                                  slot16 * 256 + c * 16) = k4;
-      } else {
-        const uint4 v4 = *reinterpret_cast<const uint4*>(qkv_tok + static_cast<int64_t>(2 * a.H + h) * kDim + c * 8);
-        *reinterpret_cast<uint4*>(const_cast<uint8_t*>(vblk) + slot16 * 256 + c * 16) = v4;
-        *reinterpret_cast<uint4*>(static_cast<uint8_t*>(a.pool_w) + static_cast<int64_t>(sm.ids[i].y) * kBlockBytes +
-                                  slot16 * 256 + c * 16) = v4;
-      }
-      __syncwarp();
-    }
     const int valid = min(kBlockTok, ctx - (r0 + i) * kBlockTok);
 
     // q . k for the 8 tokens of this lane's parity, 8 dims each.

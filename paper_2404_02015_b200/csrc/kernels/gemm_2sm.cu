@@ -289,7 +289,7 @@ bool gemm_2sm_eligible(const GemmArgs& a) {
   const int rounds = (tiles + pairs - 1) / pairs;
   if (10 * tiles < 7 * rounds * pairs) return false;
   return env != 0 && a.tmap_x128 != nullptr && a.w_tiled != nullptr &&
-         a.K % 64 == 0 && a.n_peers == 0 && a.n_signal == 0 && a.norm_w == nullptr &&
+         a.K % 64 == 0 && a.n_peers == 0 && a.n_signal == 0 &&
          (a.epi == Epilogue::kStoreBf16 || a.epi == Epilogue::kSiluMulBf16 || a.epi == Epilogue::kResidualAddF32 ||
           a.epi == Epilogue::kStoreF32) &&
          (a.grid <= 0 || a.grid >= 2);

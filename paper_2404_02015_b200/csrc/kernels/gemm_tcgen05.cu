@@ -56,6 +56,7 @@ constexpr int kEpiThreads = 128;            // one epilogue group: a warp per TM
 constexpr int kEpiGroups = 2;
 constexpr int kChunkBytes = 32 * kBM * 4;  // one epilogue chunk: 32 tokens x 128 fp32
 constexpr int kSmemBudget = 224 * 1024;     // A ring + B ring + 2 staging chunks
+constexpr int kPreIssue = 2;                // weight stages issued before the block barrier
 
 struct PeerMaps {
   CUtensorMap m[kMaxTp - 1];
@@ -64,8 +65,8 @@ struct PeerMaps {
 struct GemmRun {
   const uint8_t* w_tiled;  // pre-tiled weights (weight_tile), or null -> TMA map
   void* out;
-  float* partials;  // [grid][n_tile][128] fp32
-  int* flags;       // [grid]
+  float* partials;  // [grid][2 slots][8 chunks][32 x 128] fp32
+  int* flags;       // [grid][2 slots]
   int epoch;
   int M, N, K, ldo;
   int n_tile, stages_a, stages_b;
@@ -81,33 +82,15 @@ struct GemmRun {
   int64_t sk_iters;
   int epi;
   uint32_t tmem_cols;
-  unsigned long long* timing;  // debug: [grid][4] globaltimer stamps, or null
+  unsigned long long* timing;  // debug: [grid][64] globaltimer stamps, or null
+  int dbg_nomma;    // debug (MUX_GEMM_NOMMA=1): stream operands without MMAs
   // Tensor-parallel fan-out (kStoreF32 only): every finished tile is also
   // stored through peers.m[0..n_peers) (the same slot on the other ranks of
   // the mesh, NVLink peer memory), and once all of a CTA's stores have landed
   // it adds 1 to signal[0..n_signal) (this rank's and every peer's counter).
-  QkvRopeArgs qr;   // kQkvRope
-  int a_split;      // bulk copies per weight stage (1, 2, 4)
-  int n_stg;        // epilogue staging buffers (1 or 2)
-  int dbg_nomma;    // debug (MUX_GEMM_NOMMA): stream operands without MMAs
-  int dbg_bres;     // debug (MUX_GEMM_BRES): load only the first SB activation stages, reuse them
   int n_peers;
   int n_signal;
   int* signal[kMaxTp];
-  // Cross-launch L2 prefetch: once this CTA has issued its last weight load,
-  // it prefetches the first pf_stages tiles of its range in the NEXT decode
-  // GEMM of the chain (same flattened [m][kb] tile layout, contiguous), so
-  // HBM keeps streaming through this launch's tail and the next one's head.
-  const uint8_t* next_w;
-  int next_grid;
-  int pf_stages;
-  int64_t next_iters;
-  // fused RMSNorm of the residual rows (see GemmArgs::norm_w)
-  const float* norm_w;
-  __nv_bfloat16* norm_out;
-  unsigned* norm_bar;
-  unsigned norm_target;
-  float norm_eps;
 };
 
 __device__ __forceinline__ unsigned long long gtimer() {
@@ -123,14 +106,45 @@ __device__ __forceinline__ int64_t range_begin(int64_t iters, int c, int grid) {
   return static_cast<int64_t>(static_cast<uint32_t>(iters) * static_cast<uint32_t>(c) / static_cast<uint32_t>(grid));
 }
 
+// The CTA whose stream-K range holds iteration `it` (ranges are contiguous
+// and ascending; start the search at a CTA known to be close).
+__device__ __forceinline__ int cta_of(int64_t iters, int64_t it, int hint, int G) {
+  int a = hint;
+  while (a > 0 && range_begin(iters, a, G) > it) --a;
+  while (a + 1 < G && range_begin(iters, a + 1, G) <= it) ++a;
+  return a;
+}
+
 // The work of one CTA as a sequence of segments: (tile, k-block range); the
 // same sequence is walked by the producers, the MMA issuer and the epilogue.
+//
+// Stream-K pieces and who finishes a cut tile. A tile cut into P pieces
+// (CTAs a..b, P = b - a + 1) is finished by one "fixer": a for P = 2 (the
+// tile's first piece is a's LAST segment, so a reaches it last and its
+// partner b published the tile's end as b's FIRST segment), a + 1 for P >= 3
+// (a middle CTA whose whole range lies inside the tile: it has nothing else
+// to do, so it should not be the one others wait for). For P >= 3 the first
+// piece is again a's last segment; a walks it FIRST (rot_lo / rot_hi) so
+// that partial is published early too. Partners publish into slot 1 (a's
+// rotated first piece) or slot 0 (the piece at the start of their range):
+// every publish precedes every wait inside a CTA, and a CTA waits only as
+// the fixer of its last segment, so no cycle can form.
 struct SegGen {
-  int64_t sk, sk_end;
+  int64_t sk, sk_end;      // stream-K iterations walked in order
+  int64_t rot_lo, rot_hi;  // walked first when rot_lo < rot_hi
   int j;
   __device__ SegGen(const GemmRun& r, int c, int G)
-      : sk(range_begin(r.sk_iters, c, G)), sk_end(range_begin(r.sk_iters, c + 1, G)), j(0) {}
-  // tile (m, nt), k-blocks [kb0, kb1); sk: stream-K piece of the tile whose
+      : sk(range_begin(r.sk_iters, c, G)), sk_end(range_begin(r.sk_iters, c + 1, G)), rot_lo(0), rot_hi(0), j(0) {
+    if (r.epi != static_cast<int>(Epilogue::kResidualAddF32) && sk_end > sk && c + 2 <= G) {
+      const int64_t last_lo = static_cast<int64_t>(static_cast<uint32_t>(sk_end - 1) / static_cast<uint32_t>(r.kb)) * r.kb;
+      if (last_lo > sk && sk_end < last_lo + r.kb && range_begin(r.sk_iters, c + 2, G) < last_lo + r.kb) {
+        rot_lo = last_lo;
+        rot_hi = sk_end;
+        sk_end = last_lo;
+      }
+    }
+  }
+  // tile (m, nt), k-blocks [kb0, kb1); skp: stream-K piece of the tile whose
   // stream-K iterations are [lo, lo + kb)
   __device__ bool next(const GemmRun& r, int c, int G, int& m, int& nt, int& kb0, int& kb1, bool& skp, int64_t& lo) {
     int64_t tile;
@@ -142,13 +156,22 @@ struct SegGen {
       skp = false;
       lo = 0;
     } else {
-      if (sk >= sk_end) return false;
-      const int64_t st = static_cast<uint32_t>(sk) / static_cast<uint32_t>(r.kb);
+      int64_t s0, e;
+      if (rot_lo < rot_hi) {
+        s0 = rot_lo;
+        e = rot_hi;
+        rot_hi = rot_lo;  // consumed
+      } else {
+        if (sk >= sk_end) return false;
+        s0 = sk;
+        const int64_t t0 = static_cast<int64_t>(static_cast<uint32_t>(s0) / static_cast<uint32_t>(r.kb)) * r.kb;
+        e = min(sk_end, t0 + r.kb);
+        sk = e;
+      }
+      const int64_t st = static_cast<uint32_t>(s0) / static_cast<uint32_t>(r.kb);
       lo = st * r.kb;
-      kb0 = static_cast<int>(sk - lo);
-      const int64_t e = min(sk_end, lo + r.kb);
+      kb0 = static_cast<int>(s0 - lo);
       kb1 = static_cast<int>(e - lo);
-      sk = e;
       skp = true;
       tile = static_cast<int64_t>(r.n_dp) * G + st;
     }
@@ -166,11 +189,8 @@ struct SegGen {
     }
     return true;
   }
+  __device__ bool has_more(const GemmRun& r) const { return j < r.n_dp || rot_lo < rot_hi || sk < sk_end; }
 };
-
-__device__ __forceinline__ bool sg_has_more(const SegGen& sg, const GemmRun& r) {
-  return sg.j < r.n_dp || sg.sk < sg.sk_end;
-}
 
 __device__ __forceinline__ int ld_acquire(const int* p) {
   int v;
@@ -193,6 +213,9 @@ __device__ __forceinline__ void epi_bar_all() {
   asm volatile("bar.sync 3, %0;" ::"n"(kEpiGroups * kEpiThreads) : "memory");
 }
 
+#define STAMP(cond, slot) \
+  do { if (r.timing != nullptr && (cond)) r.timing[c * 64 + (slot)] = gtimer(); } while (0)
+
 __global__ void __launch_bounds__(kThreads, 1)
 gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
                const __grid_constant__ CUtensorMap tout, const GemmRun r, const __grid_constant__ PeerMaps peers) {
@@ -208,7 +231,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   uint8_t* a_st = base;
   uint8_t* b_st = base + SA * kAStageBytes;
   uint8_t* stage_out = b_st + SB * b_stage_bytes;  // 2 x 16 KiB epilogue staging
-  uint64_t* full_a = reinterpret_cast<uint64_t*>(stage_out + r.n_stg * kChunkBytes);
+  uint64_t* full_a = reinterpret_cast<uint64_t*>(stage_out + kEpiGroups * kChunkBytes);
   uint64_t* empty_a = full_a + SA;
   uint64_t* full_b = empty_a + SA;
   uint64_t* empty_b = full_b + SB;
@@ -216,108 +239,108 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   uint64_t* tm_empty = tm_full + 2;  // [2]
   uint64_t* pbar = tm_empty + 2;     // fixer's partial prefetch
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(pbar + 1);
-  int* meta_pos = reinterpret_cast<int*>(tmem_slot + 4);  // kQkvRope: [256] token positions
-  int* meta_id = meta_pos + 256;                          //            [256] K or V block ids
-  float* norm_red = reinterpret_cast<float*>(meta_pos);   // fused RMSNorm (never with kQkvRope): [8]
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
   const int c = blockIdx.x;
   const int G = gridDim.x;
-  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 64 + 0] = gtimer();
+  STAMP(threadIdx.x == 0, 0);
 
-  if (warp == 0 && lane == 0) {
-    if (r.w_tiled == nullptr) prefetch_tmap(&tw);
-    prefetch_tmap(&tx);
-    prefetch_tmap(&tout);
-    for (int s = 0; s < SA; ++s) {
-      mbar_init(&full_a[s], 1);
-      mbar_init(&empty_a[s], 1);
+  // Weight producer state (warp 0, lane 0). Weights do not depend on earlier
+  // kernels, so the first stages are issued right after the barriers are
+  // initialised -- beside TMEM allocation, before the block barrier -- and
+  // under PDL while the predecessor drains (only kPreIssue: every issue
+  // costs ~0.2 us, which the rest of the CTA would wait for at the barrier).
+  SegGen pg(r, c, G);
+  int pm = 0, pkb = 0, pkb1 = 0, ps = 0, pround = 0;
+  bool pvalid = false;
+  uint64_t wpol = 0;
+  auto a_next = [&]() -> bool {
+    if (pvalid && ++pkb < pkb1) return true;
+    int nt, kb0;
+    bool skp;
+    int64_t lo;
+    pvalid = pg.next(r, c, G, pm, nt, kb0, pkb1, skp, lo);
+    pkb = kb0;
+    return pvalid;
+  };
+  auto a_issue = [&]() {
+    if (pround > 0) mbar_wait(&empty_a[ps], (pround - 1) & 1);
+    mbar_arrive_expect_tx(&full_a[ps], kAStageBytes);
+    if (r.w_tiled != nullptr)  // one contiguous, pre-swizzled 16 KiB UMMA tile
+      bulk_g2s_stream(a_st + ps * kAStageBytes, r.w_tiled + (static_cast<int64_t>(pm) * r.kb + pkb) * kAStageBytes,
+                      kAStageBytes, &full_a[ps], wpol);
+    else
+      tma_load_2d(a_st + ps * kAStageBytes, &tw, &full_a[ps], pkb * kBK, pm * kBM, wpol);
+    if (++ps == SA) {
+      ps = 0;
+      ++pround;
     }
-    for (int s = 0; s < SB; ++s) {
-      mbar_init(&full_b[s], 1);
-      mbar_init(&empty_b[s], 1);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {
+      for (int s = 0; s < SA; ++s) {
+        mbar_init(&full_a[s], 1);
+        mbar_init(&empty_a[s], 1);
+      }
+      for (int s = 0; s < SB; ++s) {
+        mbar_init(&full_b[s], 1);
+        mbar_init(&empty_b[s], 1);
+      }
+      for (int b = 0; b < 2; ++b) {
+        mbar_init(&tm_full[b], 1);
+        mbar_init(&tm_empty[b], kEpiGroups * kEpiThreads / 32);
+      }
+      mbar_init(pbar, 1);
+      fence_barrier_init();
+      wpol = policy_evict_first();  // weights: streamed once per step
+      STAMP(true, 32);
+      for (int k = 0; k < kPreIssue && a_next(); ++k) a_issue();
+      STAMP(true, 19);
+      if (r.w_tiled == nullptr) prefetch_tmap(&tw);
+      prefetch_tmap(&tx);
+      prefetch_tmap(&tout);
     }
-    for (int b = 0; b < 2; ++b) {
-      mbar_init(&tm_full[b], 1);
-      mbar_init(&tm_empty[b], kEpiGroups * kEpiThreads / 32);
-    }
-    mbar_init(pbar, 1);
-    fence_barrier_init();
+    __syncwarp();
   }
   if (warp == 2) tmem_alloc_dyn(tmem_slot, r.tmem_cols);
   tc_fence_before();
   __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
-  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 64 + 15] = gtimer();
+  STAMP(threadIdx.x == 0, 15);
   if (threadIdx.x == 0) grid_dep_launch();
 
-  if (warp == 0 || warp == 3) {
-    // ------------------------------------------------ TMA producers
-    // warp 0 streams the weight tiles, warp 3 the activation tiles.
+  if (warp == 0) {
+    // ------------------------------------------------ weight producer
+    if (lane == 0)
+      while (a_next()) a_issue();
+    __syncwarp();
+  } else if (warp == 3) {
+    // -------------------------------------------- activation producer
     if (elect_one()) {
-      const bool is_a = warp == 0;
-      if (is_a && r.timing != nullptr) r.timing[c * 64 + 32] = gtimer();
-      // Weights do not depend on earlier kernels: warp 0 starts streaming
-      // them while the predecessor drains (PDL); activations must wait.
-      if (!is_a) grid_dep_wait();
-      if (!is_a && r.dbg_nomma == 2) return;  // debug: weights only
-      const uint64_t pol = is_a ? policy_evict_first()   // weights: streamed once per step
-                                : policy_evict_last();   // activations: re-read by every CTA
-      const int SS = is_a ? SA : SB;
-      uint64_t* fb = is_a ? full_a : full_b;
-      uint64_t* eb = is_a ? empty_a : empty_b;
-      const uint32_t bytes = is_a ? kAStageBytes : b_stage_bytes;
-      // Segments (tile, k-block range) with incremental stage counters: no
-      // 64-bit division in the issue loop.
-      if (is_a && r.timing != nullptr) r.timing[c * 64 + 33] = gtimer();
+      grid_dep_wait();  // activations come from the predecessor
+      const uint64_t pol = policy_evict_last();  // re-read by every CTA
+      const uint32_t bytes = static_cast<uint32_t>(b_stage_bytes);
       SegGen sg(r, c, G);
       int m, nt, kb0, kb1;
       bool skp;
       int64_t lo;
       int s = 0, round = 0;
-      if (is_a && r.timing != nullptr) r.timing[c * 64 + 34] = gtimer();
-      int64_t issued = 0, pf_at = -1;
-      if (is_a && r.next_w != nullptr && c < r.next_grid) {
-        // start the prefetch when ~SA stages of this range remain
-        const int64_t mine = range_begin(r.sk_iters, c + 1, G) - range_begin(r.sk_iters, c, G) +
-                             static_cast<int64_t>(r.n_dp) * r.kb;
-        pf_at = mine > SA ? mine - SA : 0;
-      }
       while (sg.next(r, c, G, m, nt, kb0, kb1, skp, lo)) {
         for (int kbi = kb0; kbi < kb1; ++kbi) {
-          if (!is_a && r.dbg_bres && round > 0) break;  // debug: resident activations
-          if (round > 0) mbar_wait(&eb[s], (round - 1) & 1);
-          if (is_a && round == 0 && s == 0 && r.timing != nullptr) r.timing[c * 64 + 35] = gtimer();
-          mbar_arrive_expect_tx(&fb[s], bytes);
-          if (is_a && round == 0 && s == 0 && r.timing != nullptr) r.timing[c * 64 + 36] = gtimer();
-          if (is_a) {
-            if (r.w_tiled != nullptr) {
-              // one contiguous, pre-swizzled 16 KiB UMMA tile: a_split bulk copies
-              const uint8_t* src = r.w_tiled + (static_cast<int64_t>(m) * r.kb + kbi) * kAStageBytes;
-              const uint32_t piece = kAStageBytes / r.a_split;
-              for (int pc = 0; pc < r.a_split; ++pc)
-                bulk_g2s_stream(a_st + s * kAStageBytes + pc * piece, src + pc * piece, piece, &fb[s], pol);
-            } else {
-              tma_load_2d(a_st + s * kAStageBytes, &tw, &fb[s], kbi * kBK, m * kBM, pol);
-            }
-          } else {
-            tma_load_2d(b_st + s * b_stage_bytes, &tx, &fb[s], kbi * kBK, nt * r.n_tile, pol);
-          }
-          if (is_a && round == 0 && s == 0 && r.timing != nullptr) r.timing[c * 64 + 19] = gtimer();
-          if (issued++ == pf_at) {
-            const int64_t b0 = range_begin(r.next_iters, c, r.next_grid);
-            const int64_t b1 = min(range_begin(r.next_iters, c + 1, r.next_grid), b0 + r.pf_stages);
-            for (int64_t t = b0; t < b1; ++t) prefetch_l2(r.next_w + t * kAStageBytes, kAStageBytes);
-          }
-          if (++s == SS) {
+          if (round > 0) mbar_wait(&empty_b[s], (round - 1) & 1);
+          mbar_arrive_expect_tx(&full_b[s], bytes);
+          tma_load_2d(b_st + s * b_stage_bytes, &tx, &full_b[s], kbi * kBK, nt * r.n_tile, pol);
+          if (++s == SB) {
             s = 0;
             ++round;
           }
         }
       }
     }
+    __syncwarp();
   } else if (warp == 1) {
     // ------------------------------------------------------ MMA issuer
     const uint32_t idesc = umma_idesc_bf16(kBM, r.n_tile);
@@ -334,28 +357,24 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       const uint32_t acc = tmem + static_cast<uint32_t>(b * r.n_tile);
       for (int kbi = kb0; kbi < kb1; ++kbi, ++i) {
         mbar_wait(&full_a[sa], ra & 1);
-        if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 64 + 4] = gtimer();
-        if (r.dbg_nomma != 2 && !(r.dbg_bres && rb > 0)) mbar_wait(&full_b[sb], rb & 1);
-        if (i == 0 && r.timing != nullptr && lane == 0) r.timing[c * 64 + 5] = gtimer();
+        STAMP(i == 0 && lane == 0, 4);
+        mbar_wait(&full_b[sb], rb & 1);
+        STAMP(i == 0 && lane == 0, 5);
         tc_fence_after();
         if (elect_one()) {
           const uint32_t a_addr = smem_u32(a_st + sa * kAStageBytes);
           const uint32_t b_addr = smem_u32(b_st + sb * b_stage_bytes);
-#pragma unroll
-          for (int kk = 0; kk < kBK / 16; ++kk) {
-            if (r.dbg_nomma == 1 || r.dbg_nomma == 2) break;
-            if (r.dbg_nomma == 3 && (kbi & 1)) break;  // debug: MMAs on every other stage only
-            // Advance along K inside the swizzle atom: 16 bf16 = 32 bytes.
-            umma_bf16(acc, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
-                      (kbi != kb0 || kk != 0) ? 1u : 0u);
-          }
-          if (r.dbg_nomma == 1 || r.dbg_nomma == 2) {  // debug: pure streaming rate (results are garbage)
+          if (r.dbg_nomma) {  // debug: pure streaming rate (results are garbage)
             mbar_arrive(&empty_a[sa]);
-            if (r.dbg_nomma < 2) mbar_arrive(&empty_b[sb]);
+            mbar_arrive(&empty_b[sb]);
             if (kbi == kb1 - 1) mbar_arrive(&tm_full[b]);
           } else {
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk)  // along K inside the swizzle atom: 16 bf16 = 32 bytes
+              umma_bf16(acc, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
+                        (kbi != kb0 || kk != 0) ? 1u : 0u);
             umma_commit(&empty_a[sa]);
-            if (!r.dbg_bres) umma_commit(&empty_b[sb]);
+            umma_commit(&empty_b[sb]);
             if (kbi == kb1 - 1) umma_commit(&tm_full[b]);
           }
         }
@@ -371,7 +390,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       }
       ++seg;
     }
-    if (r.timing != nullptr && lane == 0) r.timing[c * 64 + 1] = gtimer();
+    STAMP(lane == 0, 1);
   } else if (warp >= 4) {
     // ------------------------------------------------------ epilogue
     // Each chunk (32 tokens of the tile) goes TMEM -> registers -> a 16 KiB
@@ -389,6 +408,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     const bool leader = etid == 0;
     const bool lead0 = leader && eg == 0;
     const bool residual = r.epi == static_cast<int>(Epilogue::kResidualAddF32);
+    const bool silu = r.epi == static_cast<int>(Epilogue::kSiluMulBf16);
     int seg = 0;
     uint32_t pphase = 0;
     SegGen sg(r, c, G);
@@ -396,79 +416,64 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     bool skp;
     int64_t tile_lo;
     uint8_t* st = stage_out + eg * kChunkBytes;  // this group's staging buffer
+    const float* pstage = reinterpret_cast<const float*>(a_st);  // fixer: the idle A ring at its last segment
     while (sg.next(r, c, G, m, nt, kb0, kb1, skp, tile_lo)) {
-      const int64_t tile_hi = tile_lo + r.kb;  // stream-K iterations of this tile (skp)
-      const bool seg_last = !sg_has_more(sg, r);
-      // Whole (data-parallel) tiles need no fixup; residual adds neither:
-      // every piece reduce-adds into the fp32 residual stream (order of the
-      // <= few pieces is not fixed). Other epilogues are nonlinear or
-      // rounding, so stream-K pieces are summed first.
-      const bool first = residual || !skp || kb0 == 0;
-      const bool last = residual || !skp || kb1 == r.kb;
+      const bool seg_last = !sg.has_more(r);
+      // Role of this piece. Residual epilogues reduce-add every piece into
+      // the fp32 residual stream (order of the <= few pieces is not fixed);
+      // the others are nonlinear or rounding, so the pieces are summed in a
+      // fixed order by the tile's fixer (see SegGen).
+      int pa = c, pb = c, fix = c;
+      if (skp && !residual) {
+        pa = kb0 == 0 ? c : cta_of(r.sk_iters, tile_lo, c, G);
+        pb = kb1 == r.kb ? c : cta_of(r.sk_iters, tile_lo + r.kb - 1, c, G);
+        fix = pb - pa <= 1 ? pa : pa + 1;  // pa == pb: the whole tile in one piece
+      }
+      const bool partner = c != fix;
+      const int n_part = partner ? 0 : pb - pa;
       const int b = seg & 1;
       const int tok0 = nt * r.n_tile;
       const int nchunk = (r.n_tile + 31) / 32;
-      int n_part = 0;
-      const float* pstage = reinterpret_cast<const float*>(a_st);  // idle A ring at the last segment
-      if (first && !last) {
-        // Fixer (always this CTA's last segment): wait for the partners of
-        // this tile, then bulk-prefetch all their chunks into the A ring.
-        int p_hi = c + 1;
-        while (p_hi < G && range_begin(r.sk_iters, p_hi, G) < tile_hi) ++p_hi;
-        n_part = p_hi - (c + 1);
-        if (lead0)
-          for (int p = c + 1; p < p_hi; ++p)
-            while (ld_acquire(r.flags + p) != r.epoch) __nanosleep(32);
-        if (lead0 && r.timing != nullptr) r.timing[c * 64 + 6] = gtimer();
-      }
-      const bool rope = first && r.epi == static_cast<int>(Epilogue::kQkvRope);
-      const int part = m / max(1, r.qr.H), head = m % max(1, r.qr.H);  // kQkvRope: q/k/v and head of the tile
-      if (rope) {
-        // token positions and K/V block ids of this tile's tokens, fetched
-        // while the MMAs still run (read after the staging barrier below);
-        // both groups must have left the previous segment's tables first
-        epi_bar_all();
-        for (int i = etid; i < r.n_tile; i += kEpiThreads) {
-          const int tt = tok0 + i;
-          if (tt < r.M) {
-            const int pos = r.qr.tok_pos[tt];
-            meta_pos[i] = pos;
-            if (part > 0) {
-              const int rr = r.qr.rowlist[static_cast<int64_t>(r.qr.tok_slot[tt]) * r.qr.max_rows + (pos >> 4)];
-              meta_id[i] = r.qr.rowrec[static_cast<int64_t>(rr) * r.qr.row_width + (r.qr.layer * r.qr.H + head) * 2 +
-                                       (part - 1)];
-            }
-          }
-        }
+      if (n_part > 0 && lead0) {
+        for (int p = pa; p <= pb; ++p)
+          if (p != fix)
+            while (ld_acquire(r.flags + 2 * p + (p == pa ? 1 : 0)) != r.epoch) __nanosleep(32);
+        STAMP(true, 6);
       }
       mbar_wait(&tm_full[b], (seg >> 1) & 1);
       tc_fence_after();
-      if (lead0 && r.timing != nullptr && seg < 4) r.timing[c * 64 + 9 + seg] = gtimer();
+      STAMP(lead0 && seg < 4, 9 + seg);
       if (eg >= nchunk) {  // no chunk for this group (n_tile <= 32): hand TMEM back now
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&tm_empty[b]);
       }
       if (n_part > 0) {
-        // All MMAs of this CTA are complete, so the A ring is idle now.
+        // All MMAs of this CTA are complete (this is its last segment), so
+        // the A ring is idle: bulk-prefetch every partner chunk into it.
         if (lead0) {
           asm volatile("fence.proxy.async.global;" ::: "memory");
           mbar_arrive_expect_tx(pbar, static_cast<uint32_t>(n_part * nchunk * kChunkBytes));
-          for (int pi = 0; pi < n_part; ++pi)
+          int pi = 0;
+          for (int p = pa; p <= pb; ++p) {
+            if (p == fix) continue;
+            const float* src = r.partials + (static_cast<int64_t>(2 * p + (p == pa ? 1 : 0)) * 8) * (kChunkBytes / 4);
             for (int k = 0; k < nchunk; ++k)
-              bulk_g2s(a_st + (pi * nchunk + k) * kChunkBytes,
-                       r.partials + (static_cast<int64_t>(c + 1 + pi) * 8 + k) * (kChunkBytes / 4), kChunkBytes, pbar);
+              bulk_g2s(a_st + (pi * nchunk + k) * kChunkBytes, src + k * (kChunkBytes / 4), kChunkBytes, pbar);
+            ++pi;
+          }
         }
         mbar_wait(pbar, pphase);
         pphase ^= 1;
-        if (lead0 && r.timing != nullptr) r.timing[c * 64 + 7] = gtimer();
+        STAMP(lead0, 7);
       }
+      const int slot = c == pa ? 1 : 0;  // partner: where this piece is published
       const uint32_t acc = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * r.n_tile);
       for (int k = eg; k < nchunk; k += kEpiGroups) {
         const int cc = k * 32;
+        const bool stamp = r.timing != nullptr && lead0 && seg_last && k < 4;
         float v[32];
         tmem_ld_32x32b_x32(acc + cc, v);
-        const bool stamp = lead0 && r.timing != nullptr && seg_last && k < 4;
         if (stamp) r.timing[c * 64 + 20 + k] = gtimer();
         if (k + kEpiGroups >= nchunk) {  // this group's accumulators consumed: hand TMEM back
           tc_fence_before();
@@ -484,86 +489,35 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         if (leader) bulk_wait_read<0>();
         epi_bar(eg);
         if (stamp) r.timing[c * 64 + 24 + k] = gtimer();
-        const bool silu = first && r.epi == static_cast<int>(Epilogue::kSiluMulBf16);
-        const bool fp32_rows = !first || residual || silu || r.epi == static_cast<int>(Epilogue::kStoreF32);
-        if (fp32_rows) {
-          float* sf = reinterpret_cast<float*>(st);
+        if (partner || residual || r.epi == static_cast<int>(Epilogue::kStoreF32)) {
+          float* sf = reinterpret_cast<float*>(st);  // [32 tokens][128 features] fp32
 #pragma unroll
           for (int j = 0; j < 32; ++j) sf[j * kBM + fl] = v[j];
-        } else {  // kStoreBf16
+        } else if (silu) {
+          // Feature rows come in (gate_i, up_i) pairs on adjacent lanes: the
+          // even lane finishes tokens 0..15 of the chunk, the odd lane tokens
+          // 16..31, one shuffle per token. Output act [32 tokens][64] bf16.
+          const bool odd = lane & 1;
+          __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(st) + (odd ? 16 * (kBM / 2) : 0) + (fl >> 1);
+#pragma unroll
+          for (int j = 0; j < 16; ++j) {
+            const float recv = __shfl_xor_sync(0xffffffffu, odd ? v[j] : v[16 + j], 1);
+            const float g = odd ? recv : v[j];
+            const float u = odd ? v[16 + j] : recv;
+            // ex2.approx + rcp.approx: within 2 fp32 ulp of the IEEE
+            // g / (1 + expf(-g)), far below the bf16 rounding of the output
+            sh[j * (kBM / 2)] = __float2bfloat16_rn(g * rcp_approx(1.f + __expf(-g)) * u);
+          }
+        } else {  // kStoreBf16: [32 tokens][128 features] bf16
           __nv_bfloat16* sh = reinterpret_cast<__nv_bfloat16*>(st);
 #pragma unroll
           for (int j = 0; j < 32; ++j) sh[j * kBM + fl] = __float2bfloat16_rn(v[j]);
         }
-        if (silu) {
-          // kSiluMulBf16: feature rows come in (gate_i, up_i) pairs. The fp32
-          // chunk is staged first; each thread then turns 16 adjacent pairs of
-          // one token into 16 bf16 act[token][i] (no shuffles, all ILP).
-          epi_bar(eg);
-          const float4* sf4 = reinterpret_cast<const float4*>(st) + (etid >> 2) * (kBM / 4) + (etid & 3) * 8;
-          uint32_t packed[8];
-#pragma unroll
-          for (int q2 = 0; q2 < 8; ++q2) {
-            const float4 gu = sf4[q2];  // gate, up, gate, up
-            const float s0 = gu.x / (1.f + expf(-gu.x));
-            const float s1 = gu.z / (1.f + expf(-gu.z));
-            packed[q2] = pack_bf16(s0 * gu.y, s1 * gu.w);
-          }
-          epi_bar(eg);
-          uint4* dst = reinterpret_cast<uint4*>(st + (etid >> 2) * kBM + (etid & 3) * 32);
-          dst[0] = make_uint4(packed[0], packed[1], packed[2], packed[3]);
-          dst[1] = make_uint4(packed[4], packed[5], packed[6], packed[7]);
-        }
-        if (rope) {
-          // K2 fused: thread = (token jj of the chunk, dims [d0, d0+16) and
-          // their rotate_half partners d0+64..); the same _rn arithmetic as
-          // kv_append, on the same bf16-rounded values.
-          epi_bar(eg);
-          const int jj = etid >> 2, d0 = (etid & 3) * 16;
-          const int tt = tok0 + cc + jj;
-          if (tt < r.M) {
-            __nv_bfloat16* rowp = reinterpret_cast<__nv_bfloat16*>(st) + jj * kBM;
-            uint4 lo4[2] = {reinterpret_cast<uint4*>(rowp + d0)[0], reinterpret_cast<uint4*>(rowp + d0)[1]};
-            uint4 hi4[2] = {reinterpret_cast<uint4*>(rowp + 64 + d0)[0], reinterpret_cast<uint4*>(rowp + 64 + d0)[1]};
-            const int pos = meta_pos[cc + jj];
-            if (part < 2) {
-              const float* cs = r.qr.rope + static_cast<int64_t>(min(pos, r.qr.rope_positions - 1)) * 128;
-              uint32_t* lw = reinterpret_cast<uint32_t*>(lo4);
-              uint32_t* hw = reinterpret_cast<uint32_t*>(hi4);
-#pragma unroll
-              for (int i = 0; i < 8; ++i) {
-                const float l0 = bf16_lo(lw[i]), l1 = bf16_hi(lw[i]), h0 = bf16_lo(hw[i]), h1 = bf16_hi(hw[i]);
-                const float c0 = cs[2 * (d0 + 2 * i)], s0 = cs[2 * (d0 + 2 * i) + 1];
-                const float c1 = cs[2 * (d0 + 2 * i + 1)], s1 = cs[2 * (d0 + 2 * i + 1) + 1];
-                lw[i] = pack_bf16(__fsub_rn(__fmul_rn(l0, c0), __fmul_rn(h0, s0)),
-                                  __fsub_rn(__fmul_rn(l1, c1), __fmul_rn(h1, s1)));
-                hw[i] = pack_bf16(__fadd_rn(__fmul_rn(h0, c0), __fmul_rn(l0, s0)),
-                                  __fadd_rn(__fmul_rn(h1, c1), __fmul_rn(l1, s1)));
-              }
-              reinterpret_cast<uint4*>(rowp + d0)[0] = lo4[0];
-              reinterpret_cast<uint4*>(rowp + d0)[1] = lo4[1];
-              reinterpret_cast<uint4*>(rowp + 64 + d0)[0] = hi4[0];
-              reinterpret_cast<uint4*>(rowp + 64 + d0)[1] = hi4[1];
-            }
-            __nv_bfloat16* dst;
-            if (part == 0) {
-              dst = reinterpret_cast<__nv_bfloat16*>(r.qr.q_out) + (static_cast<int64_t>(tt) * r.qr.H + head) * 128;
-            } else {
-              dst = reinterpret_cast<__nv_bfloat16*>(static_cast<uint8_t*>(r.qr.pool) +
-                                                     static_cast<int64_t>(meta_id[cc + jj]) * 4096 + (pos & 15) * 256);
-            }
-            reinterpret_cast<uint4*>(dst + d0)[0] = lo4[0];
-            reinterpret_cast<uint4*>(dst + d0)[1] = lo4[1];
-            reinterpret_cast<uint4*>(dst + 64 + d0)[0] = hi4[0];
-            reinterpret_cast<uint4*>(dst + 64 + d0)[1] = hi4[1];
-          }
-        }
         fence_async_smem();
         epi_bar(eg);
         if (leader) {
-          if (!first) {
-            // partner: publish the whole chunk (fixed slot of this CTA)
-            bulk_s2g(r.partials + (static_cast<int64_t>(c) * 8 + k) * (kChunkBytes / 4), st, kChunkBytes);
+          if (partner) {
+            bulk_s2g(r.partials + (static_cast<int64_t>(2 * c + slot) * 8 + k) * (kChunkBytes / 4), st, kChunkBytes);
           } else if (residual) {
             tma_reduce_add_2d(&tout, st, m * kBM, tok0 + cc);  // rows >= M are clipped by TMA
           } else if (silu) {
@@ -576,16 +530,16 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           if (stamp) r.timing[c * 64 + 28 + k] = gtimer();
         }
       }
-      if (!first) {  // publish: both groups' partial bulk writes complete, then the flag
+      if (partner) {  // publish: both groups' partial bulk writes complete, then the flag
         if (leader) bulk_wait<0>();
         epi_bar_all();
         if (lead0) {
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          st_release(r.flags + c, r.epoch);
-          if (r.timing != nullptr) r.timing[c * 64 + 8] = gtimer();
+          st_release(r.flags + 2 * c + slot, r.epoch);
+          STAMP(true, 8);
         }
       }
-      if (lead0 && r.timing != nullptr && seg < 4) r.timing[c * 64 + 16 + seg] = gtimer();
+      STAMP(lead0 && seg < 4, 16 + seg);
       ++seg;
     }
     // Staging smem must outlive the bulk stores' reads of it; completion of
@@ -595,59 +549,17 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       if (r.n_signal > 0) bulk_wait<0>();
       else bulk_wait_read<0>();
     }
-    if (r.n_signal > 0) epi_bar_all();  // both groups' stores have landed
-    if (r.norm_w != nullptr) {
-      // Fused RMSNorm: wait until every CTA's reduce-adds into the residual
-      // have landed (grid barrier: all CTAs are co-resident on an exclusive
-      // partition), then normalise this CTA's share of the token rows.
-      if (leader) bulk_wait<0>();
-      epi_bar_all();
+    if (r.n_signal > 0) {
+      epi_bar_all();  // both groups' stores have landed
       if (lead0) {
-        asm volatile("fence.acq_rel.gpu;" ::: "memory");
-        atomicAdd(r.norm_bar, 1u);
-        while (static_cast<int>(static_cast<unsigned>(ld_acquire(reinterpret_cast<const int*>(r.norm_bar))) -
-                                r.norm_target) < 0)
-          __nanosleep(64);
-      }
-      epi_bar_all();
-      const int nt4 = r.N / 4;  // float4s per row (N = hidden)
-      const int t0 = static_cast<int>(static_cast<int64_t>(r.M) * c / G);
-      const int t1 = static_cast<int>(static_cast<int64_t>(r.M) * (c + 1) / G);
-      const int et = threadIdx.x - 128;  // 0..255 over both groups
-      for (int t = t0; t < t1; ++t) {
-        const float4* x = reinterpret_cast<const float4*>(static_cast<const float*>(r.out) +
-                                                          static_cast<int64_t>(t) * r.ldo);
-        float ss = 0.f;
-        for (int i = et; i < nt4; i += kEpiGroups * kEpiThreads) {
-          const float4 v = __ldcg(x + i);
-          ss = fmaf(v.x, v.x, fmaf(v.y, v.y, fmaf(v.z, v.z, fmaf(v.w, v.w, ss))));
-        }
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) ss += __shfl_xor_sync(0xffffffffu, ss, o);
-        if (lane == 0) norm_red[warp - 4] = ss;
-        epi_bar_all();
-        float tot = 0.f;
-#pragma unroll
-        for (int w = 0; w < kEpiGroups * kEpiThreads / 32; ++w) tot += norm_red[w];
-        const float inv = rsqrtf(tot / static_cast<float>(r.N) + r.norm_eps);
-        uint2* y = reinterpret_cast<uint2*>(r.norm_out + static_cast<int64_t>(t) * r.N);
-        const float4* g = reinterpret_cast<const float4*>(r.norm_w);
-        for (int i = et; i < nt4; i += kEpiGroups * kEpiThreads) {
-          const float4 v = __ldcg(x + i);
-          const float4 gw = g[i];
-          y[i] = make_uint2(pack_bf16(v.x * inv * gw.x, v.y * inv * gw.y), pack_bf16(v.z * inv * gw.z, v.w * inv * gw.w));
-        }
-        epi_bar_all();  // norm_red is reused by the next row
+        // every store of this CTA (local + peers) has completed: publish
+        asm volatile("fence.proxy.async.global;" ::: "memory");
+        asm volatile("fence.acq_rel.sys;" ::: "memory");
+        for (int d = 0; d < r.n_signal; ++d)
+          asm volatile("red.release.sys.global.add.s32 [%0], 1;" ::"l"(r.signal[d]) : "memory");
       }
     }
-    if (lead0 && r.n_signal > 0) {
-      // every store of this CTA (local + peers) has completed: publish
-      asm volatile("fence.proxy.async.global;" ::: "memory");
-      asm volatile("fence.acq_rel.sys;" ::: "memory");
-      for (int d = 0; d < r.n_signal; ++d)
-        asm volatile("red.release.sys.global.add.s32 [%0], 1;" ::"l"(r.signal[d]) : "memory");
-    }
-    if (r.timing != nullptr && threadIdx.x == 128) r.timing[c * 64 + 2] = gtimer();
+    STAMP(threadIdx.x == 128, 2);
   }
   // Reconverge the role warps (elected producer / MMA lanes) before the
   // block barrier: a diverged warp would arrive early and let warp 2 free
@@ -655,9 +567,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   __syncwarp();
   tc_fence_before();
   __syncthreads();
-  if (r.timing != nullptr && threadIdx.x == 0) r.timing[c * 64 + 3] = gtimer();
-  if (r.timing != nullptr && threadIdx.x == 128) r.timing[c * 64 + 13] = gtimer();
-  if (r.timing != nullptr && threadIdx.x == 32) r.timing[c * 64 + 14] = gtimer();
+  STAMP(threadIdx.x == 0, 3);
   if (warp == 2) {
     tc_fence_after();
     tmem_dealloc(tmem, r.tmem_cols);
@@ -756,7 +666,7 @@ int gemm_pick_n_tile(int M) {
   return n;
 }
 
-size_t gemm_partials_floats(int max_grid) { return static_cast<size_t>(max_grid) * 8 * (kChunkBytes / 4); }
+size_t gemm_partials_floats(int max_grid) { return static_cast<size_t>(max_grid) * 2 * 8 * (kChunkBytes / 4); }
 
 size_t weight_tiled_bytes(int N, int K) {
   return static_cast<size_t>((N + kBM - 1) / kBM) * ((K + kBK - 1) / kBK) * kAStageBytes;
@@ -800,27 +710,17 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   static const int env_sb = getenv("MUX_GEMM_SB") ? atoi(getenv("MUX_GEMM_SB")) : 0;
   static const int env_sa = getenv("MUX_GEMM_SA") ? atoi(getenv("MUX_GEMM_SA")) : 0;
   if (env_sb > 0) r.stages_b = env_sb;
-  static const int env_split = getenv("MUX_GEMM_ASPLIT") ? atoi(getenv("MUX_GEMM_ASPLIT")) : 1;
-  r.a_split = (env_split == 2 || env_split == 4 || env_split == 8) ? env_split : 1;
   static const int env_nomma = getenv("MUX_GEMM_NOMMA") ? atoi(getenv("MUX_GEMM_NOMMA")) : 0;
-  r.dbg_nomma = env_nomma;
-  static const int env_bres = getenv("MUX_GEMM_BRES") ? atoi(getenv("MUX_GEMM_BRES")) : 0;
-  r.dbg_bres = env_bres;
-  const int meta_bytes = a.epi == Epilogue::kQkvRope ? 2 * 256 * 4 : 0;  // token positions + block ids
-  static const int env_stg = getenv("MUX_GEMM_STG") ? atoi(getenv("MUX_GEMM_STG")) : 2;
+  r.dbg_nomma = env_nomma != 0;
   static const int env_budget = getenv("MUX_GEMM_SMEM_KB") ? atoi(getenv("MUX_GEMM_SMEM_KB")) * 1024 : kSmemBudget;
-  r.n_stg = 2;  // one staging buffer per epilogue group
-  (void)env_stg;
-  r.stages_a = (env_budget - meta_bytes - r.stages_b * b_stage - r.n_stg * kChunkBytes) / kAStageBytes;
+  r.stages_a = (env_budget - r.stages_b * b_stage - kEpiGroups * kChunkBytes) / kAStageBytes;
   if (env_sa > 0) r.stages_a = std::min(env_sa, r.stages_a);
   else if (r.stages_a > 10) r.stages_a = 10;
-  // The fixer prefetches up to 2 partners x ceil(n_tile/32) chunks into the A ring.
   r.kb = (a.K + kBK - 1) / kBK;
   r.m_tiles = (a.N + kBM - 1) / kBM;
   const int n_tiles_tok = (a.M + r.n_tile - 1) / r.n_tile;
   r.iters = static_cast<int64_t>(r.m_tiles) * n_tiles_tok * r.kb;
   r.epi = static_cast<int>(a.epi);
-  r.qr = a.qkv;
   r.n_tok_tiles = n_tiles_tok;
   r.tmem_cols = pow2_cols(r.n_tile + (r.n_tile > 32 ? r.n_tile : 32));
   int grid = a.grid > 0 ? a.grid : 148;
@@ -832,8 +732,8 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   static const int env_rmin = getenv("MUX_GEMM_RES_MIN_ITERS") ? atoi(getenv("MUX_GEMM_RES_MIN_ITERS")) : 8;
   if (a.epi == Epilogue::kResidualAddF32) min_iters = std::min<int64_t>(min_iters, env_rmin);
   if (static_cast<int64_t>(grid) * min_iters > r.iters) grid = static_cast<int>(std::max<int64_t>(1, r.iters / min_iters));
-  // Non-residual epilogues sum pieces in a fixer: keep every tile in <= 3
-  // pieces (<= 2 partners) so their chunks fit the idle A ring.
+  // Non-residual epilogues sum pieces in a fixer: keep every tile in few
+  // enough pieces that the partners' chunks fit the fixer's idle A ring.
   if (r.epi != static_cast<int>(Epilogue::kResidualAddF32)) {
     const int nchunk = (r.n_tile + 31) / 32;
     const int max_partners = (r.stages_a * kAStageBytes) / (nchunk * kChunkBytes);
@@ -843,7 +743,7 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   }
   // Schedule: decode (one token tile) = pure stream-K; prefill = grouped
   // data-parallel rounds + stream-K over the last 1-2 waves of tiles (so
-  // every stream-K range spans >= one tile's k-blocks: <= 2 partners).
+  // every stream-K range spans >= one tile's k-blocks: <= 2 pieces).
   static const int env_group = getenv("MUX_GEMM_GROUP_M") ? atoi(getenv("MUX_GEMM_GROUP_M")) : 8;
   const int64_t tiles = static_cast<int64_t>(r.m_tiles) * n_tiles_tok;
   if (n_tiles_tok > 1 && env_group > 0) {
@@ -855,7 +755,7 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   }
   r.sk_iters = (tiles - static_cast<int64_t>(r.n_dp) * grid) * r.kb;
   smem_out = 1024 + static_cast<size_t>(r.stages_a) * kAStageBytes + static_cast<size_t>(r.stages_b) * b_stage +
-             r.n_stg * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16 + std::max(meta_bytes, 64);
+             kEpiGroups * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16;
   grid_out = grid;
 }
 
@@ -869,32 +769,6 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   plan(a, r, grid, smem);
   // device index math is 32-bit (range_begin): iters * (grid + 1) must fit
   if (static_cast<uint64_t>(r.iters) * static_cast<uint64_t>(grid + 1) >= (1ull << 32)) return cudaErrorInvalidValue;
-  if (a.next_w != nullptr && a.pf_stages > 0 && r.n_tok_tiles == 1) {
-    // the next decode GEMM of the chain: same tokens, same partition
-    GemmArgs na = a;
-    na.N = a.next_N;
-    na.K = a.next_K;
-    na.epi = a.next_epi;
-    GemmRun nr{};
-    int ngrid = 0;
-    size_t nsmem = 0;
-    plan(na, nr, ngrid, nsmem);
-    if (static_cast<uint64_t>(nr.iters) * static_cast<uint64_t>(ngrid + 1) >= (1ull << 32)) return cudaErrorInvalidValue;
-    r.next_w = static_cast<const uint8_t*>(a.next_w);
-    r.next_grid = ngrid;
-    r.next_iters = nr.sk_iters;
-    r.pf_stages = a.pf_stages;
-  }
-  if (a.norm_w != nullptr) {
-    // decode residual GEMMs only: one token tile, the whole grid co-resident
-    if (a.epi != Epilogue::kResidualAddF32 || r.n_tok_tiles != 1 || a.norm_bar == nullptr || a.N % 4 != 0)
-      return cudaErrorInvalidValue;
-    r.norm_w = a.norm_w;
-    r.norm_out = static_cast<__nv_bfloat16*>(a.norm_out);
-    r.norm_bar = a.norm_bar;
-    r.norm_target = a.norm_base + static_cast<unsigned>(grid);
-    r.norm_eps = a.norm_eps;
-  }
   static PerDeviceOnce configured;
   cudaError_t ce = configured.run(
       [] { return cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448); });

@@ -20,15 +20,6 @@ struct DecodeAttnArgs {
   float* part_o;            // [B][H][splits][128] (splits > 1)
   float* part_ml;           // [B][H][splits][2]   (splits > 1)
   int* split_count;         // [B][H] zeroed: the last split CTA merges in-kernel (null: combine launch)
-  // Decode with K2 fused (qkv != null): q, k, v of the step's token come
-  // straight from the QKV GEMM output [B][3][H][128] (not rotated); every
-  // CTA rotates q itself (RoPE at position ctx-1, the _rn arithmetic of
-  // kv_append), the CTA holding the member's last row rotates k, writes k and
-  // v into their head-blocks (pool_w) and patches its staged copy of the row.
-  const void* qkv;
-  void* pool_w;
-  const float* rope;        // [rope_positions][64][2] (cos, sin)
-  int rope_positions;
   int B, H, layer, max_rows, row_width;
   int splits, rows_per_split;
   float scale_log2;         // log2(e) / sqrt(128)
@@ -74,19 +65,6 @@ enum class Epilogue : int {
   kResidualAddF32 = 1, // out fp32 [M][ldo] += D (the residual stream; single owner per element)
   kSiluMulBf16 = 2,    // W rows interleaved (gate, up) pairs: out bf16 [M][N/2]
   kStoreF32 = 3,       // out fp32 [M][ldo]
-  kQkvRope = 4,        // K2 fused into the QKV projection: out bf16 [M][3][H][128] with q and k
-                       // rotated (RoPE), rotated q -> q_out, the token's K/V -> its head-blocks
-};
-// Tables of the fused QKV epilogue (kQkvRope): what kv_append would read.
-struct QkvRopeArgs {
-  void* q_out;              // [M][H][128] bf16 rotated q
-  void* pool;               // [n_blocks][16][128] bf16
-  const int32_t* rowrec;
-  const int32_t* rowlist;
-  const int32_t* tok_slot;  // [M] table slot of each token's request
-  const int32_t* tok_pos;   // [M] position of the token in its request
-  const float* rope;        // [rope_positions][64][2]
-  int rope_positions, H, layer, row_width, max_rows;
 };
 struct GemmArgs {
   const void* w_tiled;      // weights in weight_tile() layout (preferred), or null
@@ -103,7 +81,6 @@ struct GemmArgs {
   int M, N, K;
   int ldo;
   Epilogue epi;
-  QkvRopeArgs qkv;          // kQkvRope only
   // Tensor parallelism (kStoreF32): also store every tile through these
   // maps (host CUtensorMap*, peer ranks' slots) and signal the counters
   // once per CTA when its stores have landed. grid_out receives the grid.
@@ -112,24 +89,6 @@ struct GemmArgs {
   int n_signal = 0;
   int* signal[kMaxTp] = {};
   int* grid_out = nullptr;
-  // Decode chains: the weights (weight_tile layout) and shape of the NEXT
-  // GEMM on this stream; each CTA prefetches the first pf_stages 16 KiB tiles
-  // of its range there into L2 once its own weight loads are issued.
-  const void* next_w = nullptr;
-  int next_N = 0, next_K = 0;
-  Epilogue next_epi = Epilogue::kStoreBf16;
-  int pf_stages = 0;
-  // kResidualAddF32 decode only: after every CTA's reduce-adds have landed
-  // (grid barrier on norm_bar: count reaches norm_target), the CTAs normalise
-  // the residual rows (RMSNorm with norm_w, eps) into norm_out bf16 [M][N]:
-  // the RMSNorm launch between two GEMMs disappears. All CTAs of the grid
-  // must be co-resident with no other stream sharing their SMs (a green
-  // partition); norm_target is set from the launch grid (grid_out).
-  const float* norm_w = nullptr;
-  void* norm_out = nullptr;
-  unsigned* norm_bar = nullptr;
-  unsigned norm_base = 0;
-  float norm_eps = 1e-6f;
 };
 cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream);
 // Prefill GEMMs on CTA pairs (tcgen05 cta_group::2, gemm_2sm.cu); gemm_bf16_tn
@@ -153,42 +112,6 @@ bool make_tmap_2d(void* tmap_out, const void* base, bool fp32, uint64_t rows, ui
                   uint64_t row_stride_bytes, uint32_t box_rows, uint32_t box_cols);
 bool make_tmap_bf16(void* tmap_out, const void* base, uint64_t rows, uint64_t cols,
                     uint64_t row_stride_bytes, uint32_t box_rows);
-
-// ---- fused decode layer chain (layer_chain.cu) -----------------------------
-// The projections of a decode layer between two attention launches in one
-// persistent cooperative tcgen05 kernel; every job reduce-adds fp32 into its
-// output, then an element-wise step runs on all CTAs after a grid barrier.
-constexpr int kChainMaxJobs = 6;
-enum ChainPostKind : int { kPostNone = 0, kPostNorm = 1, kPostSilu = 2, kPostQkvAppend = 3 };
-struct ChainJob {
-  const uint8_t* w;        // weights in weight_tile() layout
-  int N, K;                // D[M x N] += X[M x K] W[N x K]^T
-  int post;                // ChainPostKind, run after this job
-  const float* norm_w;     // kPostNorm: RMSNorm weight
-  int kb, m_tiles;         // filled by layer_chain()
-  int64_t iters;
-};
-struct ChainPost {
-  float* resid; __nv_bfloat16* xn; int hidden; float eps;   // norm: resid -> xn
-  float* gu32; __nv_bfloat16* act; int ffn;                  // silu: gu32 [M][2ffn] -> act [M][ffn]
-  float* qkv32; __nv_bfloat16* q; int heads;                 // qkv: qkv32 [M][3][H][128] -> q, pool
-  const int32_t* slots; const int32_t* ctx;                  // per member: table slot, ctx incl. new token
-  const float* rope; int rope_positions;
-  void* pool; const int32_t* rowlist; const int32_t* rowrec; int row_width, max_rows, layer;
-};
-struct ChainArgs {
-  int n_jobs;
-  ChainJob job[kChainMaxJobs];
-  const void* tmap_x[kChainMaxJobs];    // B operand maps (bf16, box rows = gemm_pick_n_tile(M))
-  const void* tmap_out[kChainMaxJobs];  // fp32 reduce-add maps (make_tmap_gemm_out, residual epilogue)
-  int M, grid;
-  unsigned* bar;                        // grid-barrier counter (monotonic)
-  unsigned bar_base;                    // its value before this launch; the launch adds 2 * n_jobs * grid
-  ChainPost post;
-};
-cudaError_t layer_chain(const ChainArgs& a, cudaStream_t stream);
-void chain_debug_timing(void* buf);  // [grid][64] u64 globaltimer stamps of every launch, null = off
-bool chain_coop_pdl();               // false once the driver refused cooperative + PDL together
 
 // ---- K5 small fused ops ---------------------------------------------------
 cudaError_t embed_rmsnorm(const void* emb, const int32_t* tokens, const float* norm_w,
@@ -234,6 +157,5 @@ cudaError_t preload_kv_append();
 cudaError_t preload_gemm();
 cudaError_t preload_prefill_attention();
 cudaError_t preload_fused_ops();
-cudaError_t preload_layer_chain();
 
 }  // namespace mux

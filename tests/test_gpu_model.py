@@ -226,15 +226,11 @@ def test_green_partitions_are_disjoint_sm_sets(green_unit):
     assert len(set(unit.probe_smids(0, 4 * unit.partition_sms(0)))) > s1  # partition 0 spans the device
 
 
-@pytest.mark.parametrize("fuse_norm", [0, 1])
-def test_colocated_decode_on_green_partitions(green_unit, fuse_norm):
+def test_colocated_decode_on_green_partitions(green_unit):
     """Both models prefill and decode concurrently, each on its own SM
-    partition (spatial multiplexing, PAPER §4); tokens match the oracle.
-    fuse_norm=1: the RMSNorm runs inside the residual GEMMs after a grid
-    barrier (exclusive partitions only)."""
+    partition (spatial multiplexing, PAPER §4); tokens match the oracle."""
     unit, specs, refs = green_unit
-    unit.set_option("fuse_norm", fuse_norm)
-    rng = np.random.default_rng(11 + fuse_norm)
+    rng = np.random.default_rng(11)
     jobs = []
     for llm in (0, 1):
         rids = [70000 + 100 * llm + i for i in range(6)]
@@ -262,7 +258,6 @@ def test_colocated_decode_on_green_partitions(green_unit, fuse_norm):
             check_tokens(refs[llm], prompts[i], gen[i])
         for rid in rids:
             unit.pool.free_request(llm, rid)
-    unit.set_option("fuse_norm", 0)
 
 
 def _pinned_i32(n):
@@ -326,41 +321,6 @@ def test_tensor_parallel_tp2_fused_allreduce(cuda):
     finally:
         for u in units:
             u.close()
-
-
-def test_decode_fused_layer_chain_matches_oracle(tiny_unit):
-    """The experimental fused decode path (one persistent cooperative
-    layer-chain launch per layer: O, gate-up, down, next QKV with RMSNorm,
-    SiLU and RoPE + KV append between grid barriers) keeps greedy-token
-    parity with the oracle."""
-    unit, specs, refs = tiny_unit
-    unit.set_option("chain", 1)
-    try:
-        for llm in (0, 1):
-            rng = np.random.default_rng(40 + llm)
-            lens = [3, 16, 33, 90]
-            rids = [30000 + 100 * llm + i for i in range(len(lens))]
-            for rid, n in zip(rids, lens):
-                assert unit.pool.admit(llm, rid, n, n + 12).ok
-            prompts = [rng.integers(0, specs[llm].vocab, n).astype(np.int32) for n in lens]
-            first = np.zeros(len(lens), np.int32)
-            unit.prefill(llm, rids, np.concatenate(prompts), first, partition=0)
-            unit.sync()
-            gen = [[int(t)] for t in first]
-            out = np.zeros(len(lens), np.int32)
-            for _ in range(12):
-                for rid in rids:
-                    assert unit.pool.alloc(llm, rid, 1, False).ok
-                unit.decode(llm, rids, out=out, partition=1)
-                unit.sync()
-                for i, t in enumerate(out):
-                    gen[i].append(int(t))
-            for i in range(len(lens)):
-                check_tokens(refs[llm], prompts[i], gen[i])
-            for rid in rids:
-                unit.pool.free_request(llm, rid)
-    finally:
-        unit.set_option("chain", 0)
 
 
 def test_measured_engine_runs_config1_on_device_time(tiny_unit):
@@ -454,45 +414,6 @@ def test_measured_engine_chooses_green_partitions_per_pass(cuda):
                 check_tokens(refs[llm], lockstep_prompt(11, r.id, r.prompt_len, specs[llm].vocab), toks)
     finally:
         unit.close()
-
-
-@pytest.mark.parametrize("option", ["fuse_qkv", "fuse_k2"])
-def test_fused_qkv_epilogue_is_bit_identical_to_kv_append(tiny_unit, option):
-    """K2 fused into the QKV GEMM epilogue (option "fuse_qkv") or into the
-    decode attention K1 (option "fuse_k2") against the separate
-    kv_append kernel: same bf16 rounding and _rn RoPE arithmetic, so the same
-    prefill + decode produce identical tokens."""
-    unit, specs, refs = tiny_unit
-    rng = np.random.default_rng(77)
-    lens = [1, 15, 16, 17, 64, 200]
-    prompts = [rng.integers(0, specs[0].vocab, n).astype(np.int32) for n in lens]
-    runs = []
-    unit.set_option("fuse_k2", 0)
-    for fused, base in ((1, 61000), (0, 62000)):
-        unit.set_option(option, fused)
-        rids = [base + i for i in range(len(lens))]
-        for rid, n in zip(rids, lens):
-            assert unit.pool.admit(0, rid, n, n + 10).ok
-        first = np.zeros(len(lens), np.int32)
-        unit.prefill(0, rids, np.concatenate(prompts), first, partition=0)
-        unit.sync()
-        gen = [[int(t)] for t in first]
-        out = np.zeros(len(lens), np.int32)
-        for _ in range(10):
-            for rid in rids:
-                assert unit.pool.alloc(0, rid, 1, False).ok
-            unit.decode(0, rids, out=out, partition=1)
-            unit.sync()
-            for i, t in enumerate(out):
-                gen[i].append(int(t))
-        for rid in rids:
-            unit.pool.free_request(0, rid)
-        runs.append(gen)
-    unit.set_option("fuse_qkv", 0)
-    unit.set_option("fuse_k2", 0)
-    assert runs[0] == runs[1]
-    for i in range(len(lens)):
-        check_tokens(refs[0], prompts[i], runs[0][i])
 
 
 @pytest.mark.timeout(600)
