@@ -313,6 +313,9 @@ MUX_API int mux_unit_elapsed(mux_unit* unit, int slot_a, int slot_b, float* ms);
  * enable, then read the summed kernel milliseconds and launch count. */
 MUX_API int mux_unit_attn_timing(mux_unit* unit, int enable);
 MUX_API int mux_unit_attn_time(mux_unit* unit, double* total_ms, int64_t* launches, double* bytes);
+/* The decode GEMMs (M <= 256) timed while mux_unit_attn_timing is on: event
+ * pairs around every launch, bytes = the weights each streams (N*K*2). */
+MUX_API int mux_unit_gemm_time(mux_unit* unit, double* total_ms, int64_t* launches, double* bytes);
 /* Tensor-parallel mailbox of a partition (the fused row-parallel GEMM ->
  * allreduce): its device pointer and a CUDA IPC handle (64 bytes) that the
  * other ranks of the mesh open with mux_unit_tp_connect. Replaces the
@@ -352,6 +355,7 @@ MUX_API int mux_unit_probe_smids(mux_unit* unit, int partition, int blocks, int*
 MUX_API int64_t mux_unit_launches(mux_unit* unit);
 /* Tuning knobs: "gemm_min_iters" (k-blocks per GEMM CTA floor, default 8);
  * "pdl" (programmatic dependent launch between job kernels, default 1);
+ * "graphs" (decode jobs replayed from cached CUDA graphs, default 1);
  * "prefill_on_partition" (prefill jobs on their model's partition);
  * "pass_green" (partitions = [whole GPU | a whole-GPU stream per model |
  * a green partition per model]; decode jobs use the green partitions only in

@@ -162,6 +162,7 @@ _SIGS = {
     "mux_unit_elapsed": (C.c_int, [vp, C.c_int, C.c_int, P(f32)]),
     "mux_unit_attn_timing": (C.c_int, [vp, C.c_int]),
     "mux_unit_attn_time": (C.c_int, [vp, P(f64), P(i64), P(f64)]),
+    "mux_unit_gemm_time": (C.c_int, [vp, P(f64), P(i64), P(f64)]),
     "mux_unit_launches": (i64, [vp]),
     "mux_unit_pass_stats": (C.c_int, [vp, C.POINTER(i64), C.POINTER(i64)]),
     "mux_unit_last_stats": (C.c_int, [vp, P(vp)]),

@@ -366,6 +366,7 @@ struct mux_unit {
   cudaEvent_t ev[64] = {};
   bool timing = false;
   mux::AttnTimer timer;
+  mux::AttnTimer gemm_timer;  // decode GEMM launches while timing is on
   int max_batch = 0;
   int max_prefill = 0;
   ~mux_unit() {
@@ -1364,10 +1365,23 @@ int mux_unit_elapsed(mux_unit* u, int a, int b, float* ms) {
 int mux_unit_attn_timing(mux_unit* u, int enable) {
   return guarded([&] {
     u->timer.harvest();
+    u->gemm_timer.harvest();
     u->timing = enable != 0;
-    u->timer.total_ms = 0.0;
-    u->timer.bytes = 0.0;
-    u->timer.launches = 0;
+    u->rt->set_gemm_timer(u->timing ? &u->gemm_timer : nullptr);
+    for (mux::AttnTimer* t : {&u->timer, &u->gemm_timer}) {
+      t->total_ms = 0.0;
+      t->bytes = 0.0;
+      t->launches = 0;
+    }
+  });
+}
+
+int mux_unit_gemm_time(mux_unit* u, double* total_ms, int64_t* launches, double* bytes) {
+  return guarded([&] {
+    u->gemm_timer.harvest();
+    if (total_ms) *total_ms = u->gemm_timer.total_ms;
+    if (launches) *launches = u->gemm_timer.launches;
+    if (bytes) *bytes = u->gemm_timer.bytes;
   });
 }
 
@@ -1502,6 +1516,7 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
     const std::string k = key ? key : "";
     if (k == "gemm_min_iters") u->rt->set_gemm_min_iters(static_cast<int>(value));
     else if (k == "pdl") mux::pdl_enabled() = value != 0;
+    else if (k == "graphs") u->rt->set_graphs(value != 0);
     else if (k == "prefill_on_partition") u->prefill_on_partition = value != 0;
     else if (k == "pass_green") u->pass_green = value != 0;
     else if (k == "align_decode") u->align_decode = value != 0;

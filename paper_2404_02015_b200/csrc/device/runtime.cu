@@ -322,6 +322,7 @@ Runtime::Runtime(int device, int64_t pool_blocks, int max_pos)
   check_cuda(preload_prefill_attention(), "preload");
   check_cuda(preload_fused_ops(), "preload");
   check_cuda(preload(gather_last_tok, scatter_last_tok), "preload");
+  if (const char* g = getenv("MUX_GRAPHS")) use_graphs_ = atoi(g) != 0;  // A/B switch (option "graphs")
   pool_ = DevMem(static_cast<size_t>(pool_blocks) * 4096);
   // RoPE table [max_pos][64][(cos, sin)], computed in double, stored fp32.
   std::vector<float> tab(static_cast<size_t>(max_pos) * 128);
@@ -340,6 +341,7 @@ Runtime::Runtime(int device, int64_t pool_blocks, int max_pos)
 Runtime::~Runtime() {
   for (StageSlot& s : ring_)
     if (s.done) cudaEventDestroy(s.done);
+  for (auto& g : graphs_) cudaGraphExecDestroy(g.second.exec);
 }
 
 const void* Runtime::act_tmap(const void* base, int rows, int cols, int box_rows) {
@@ -379,7 +381,19 @@ void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void
   g.K = K;
   g.ldo = ldo;
   g.epi = static_cast<Epilogue>(epi);
+  cudaEvent_t e0 = nullptr, e1 = nullptr;
+  const bool timed = gemm_timer_ != nullptr && M <= 256;
+  if (timed) {
+    e0 = gemm_timer_->get();
+    e1 = gemm_timer_->get();
+    check_cuda(cudaEventRecord(e0, stream), "timer");
+  }
   check_cuda(gemm_bf16_tn(g, stream), "gemm");
+  if (timed) {
+    check_cuda(cudaEventRecord(e1, stream), "timer");
+    gemm_timer_->pending.emplace_back(e0, e1);
+    gemm_timer_->pending_bytes += static_cast<double>(N) * K * 2;  // decode: the weights, streamed once
+  }
   launches_ += 1;
 }
 
@@ -525,14 +539,32 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   int32_t* order = h + 3 * T;
   for (int i = 0; i < n; ++i) order[i] = i;
   std::stable_sort(order, order + n, [&](int32_t x, int32_t y) { return ctx_host[x] > ctx_host[y]; });
-  ws.stage_commit(5 * static_cast<size_t>(T), stream);
+  const int hid = d.hidden, H = d.heads, L = d.layers;
+  int max_ctx = 0;
+  for (int i = 0; i < n; ++i) max_ctx = std::max(max_ctx, ctx_host[i]);
+  const int max_rows_req = (max_ctx + 15) / 16;
+  // KV splits: enough CTAs to fill the GPU a few times over.
+  int splits = 1;
+  // (the last split merges in-kernel, so small batches can afford ~2 rows per split)
+  while (splits < kMaxKvSplits && n * H * splits < 4 * ws.sms && (max_rows_req + splits * 2 - 1) / (splits * 2) >= 2)
+    splits *= 2;
+  while ((max_rows_req + splits - 1) / splits > decode_attention_max_rows_per_split()) splits *= 2;
+  if (splits > kMaxKvSplits)  // the split scratch holds kMaxKvSplits per (member, head)
+    throw std::invalid_argument("decode: context of " + std::to_string(max_ctx) + " tokens exceeds K1's " +
+                                std::to_string(kMaxKvSplits * decode_attention_max_rows_per_split() * 16));
+  h[5 * T] = std::max(1, (max_rows_req + splits - 1) / splits);  // K1 rows per split (seq_start[0])
+  ws.stage_commit(5 * static_cast<size_t>(T) + 1, stream);
+
+  // Everything below is a pure function of (model, workspace, n, splits,
+  // whether tokens are staged): it is enqueued directly, or captured once
+  // into a CUDA graph and replayed (per-step data all comes through the
+  // staged metadata and device tables).
+  auto enqueue = [&]() {
   if (!tokens_host) {
     check_cuda(launch(gather_last_tok, dim3((n + 127) / 128), dim3(128), 0, stream, m.last_tok.as<int32_t>(),
                       ws.slots, ws.tokens, n), "gather_last_tok");
     launches_ += 1;
   }
-
-  const int hid = d.hidden, H = d.heads, L = d.layers;
   check_cuda(embed_rmsnorm(m.embed.p, ws.tokens, m.attn_norm[0].as<float>(), ws.resid.as<float>(), ws.xn.p,
                            n, hid, d.norm_eps, stream), "embed");
   launches_ += 1;
@@ -552,20 +584,9 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   at.H = H;
   at.max_rows = m.max_rows();
   at.row_width = m.row_width();
-  int max_ctx = 0;
-  for (int i = 0; i < n; ++i) max_ctx = std::max(max_ctx, ctx_host[i]);
-  const int max_rows_req = (max_ctx + 15) / 16;
-  // KV splits: enough CTAs to fill the GPU a few times over.
-  int splits = 1;
-  // (the last split merges in-kernel, so small batches can afford ~2 rows per split)
-  while (splits < kMaxKvSplits && n * H * splits < 4 * ws.sms && (max_rows_req + splits * 2 - 1) / (splits * 2) >= 2)
-    splits *= 2;
-  while ((max_rows_req + splits - 1) / splits > decode_attention_max_rows_per_split()) splits *= 2;
-  if (splits > kMaxKvSplits)  // the split scratch holds kMaxKvSplits per (member, head)
-    throw std::invalid_argument("decode: context of " + std::to_string(max_ctx) + " tokens exceeds K1's " +
-                                std::to_string(kMaxKvSplits * decode_attention_max_rows_per_split() * 16));
   at.splits = splits;
-  at.rows_per_split = std::max(1, (max_rows_req + splits - 1) / splits);
+  at.rows_per_split = decode_attention_max_rows_per_split();  // bound; the value is staged
+  at.rows_per_split_dev = ws.seq_start;
   at.scale_log2 = 1.4426950408889634f / std::sqrt(128.f);
   // Algorithmic bytes of one K1 launch: K+V of every cached token, q in, o out.
   double attn_bytes = 0.0;
@@ -642,6 +663,53 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   check_cuda(launch(scatter_last_tok, dim3((n + 127) / 128), dim3(128), 0, stream, m.last_tok.as<int32_t>(),
                     ws.slots, ws.out_tok, n), "scatter_last_tok");
   launches_ += 2;
+  };
+  // Graphs: single-rank decode without per-launch timing (the TP path's
+  // mailbox counters advance per call; timers record events per launch).
+  if (use_graphs_ && timer == nullptr && gemm_timer_ == nullptr && d.tp_size == 1) {
+    const GraphKey key{&m, &ws, n, splits, tokens_host != nullptr};
+    auto it = graphs_.find(key);
+    // capture on a key's second use: a batch size seen once (serving under
+    // churn) is cheaper to enqueue than to capture and instantiate
+    const bool capture = it == graphs_.end() && ++graph_seen_[key] >= 2;
+    if (it == graphs_.end() && !capture) {
+      enqueue();
+    } else {
+    if (it == graphs_.end()) {
+      if (graphs_.size() >= kMaxGraphs) {  // bounded cache: drop the least recently used
+        auto lru = graphs_.begin();
+        for (auto g = graphs_.begin(); g != graphs_.end(); ++g)
+          if (g->second.used < lru->second.used) lru = g;
+        cudaGraphExecDestroy(lru->second.exec);
+        graph_seen_.erase(lru->first);
+        graphs_.erase(lru);
+      }
+      const int64_t l0 = launches_;
+      check_cuda(cudaStreamBeginCapture(stream, cudaStreamCaptureModeThreadLocal), "graph capture");
+      cudaGraph_t graph = nullptr;
+      try {
+        enqueue();
+      } catch (...) {
+        cudaStreamEndCapture(stream, &graph);
+        if (graph) cudaGraphDestroy(graph);
+        throw;
+      }
+      check_cuda(cudaStreamEndCapture(stream, &graph), "graph capture end");
+      cudaGraphExec_t exec = nullptr;
+      const cudaError_t ie = cudaGraphInstantiate(&exec, graph, 0);
+      cudaGraphDestroy(graph);
+      check_cuda(ie, "graph instantiate");
+      it = graphs_.emplace(key, GraphEntry{exec, launches_ - l0, 0}).first;
+      launches_ = l0;
+      graph_captures_ += 1;
+    }
+    it->second.used = ++graph_clock_;
+    check_cuda(cudaGraphLaunch(it->second.exec, stream), "graph launch");
+    launches_ += it->second.kernels;
+    }
+  } else {
+    enqueue();
+  }
   if (out_host)
     check_cuda(cudaMemcpyAsync(out_host, ws.out_tok, n * 4, cudaMemcpyDeviceToHost, stream), "out copy");
 }

@@ -178,6 +178,13 @@ class Runtime {
   int64_t launches() const { return launches_; }
   void set_gemm_min_iters(int v) { gemm_min_iters_ = v; }
   void count_launch(int64_t n = 1) { launches_ += n; }
+  // Per-launch CUDA events around every decode GEMM (M <= 256) on its
+  // stream, accumulating the weight bytes it streams (null = off).
+  void set_gemm_timer(AttnTimer* t) { gemm_timer_ = t; }
+  // CUDA graphs for decode jobs: one capture per (model, workspace, batch,
+  // K1 splits, tokens staged or gathered), replayed on later calls.
+  void set_graphs(bool on) { use_graphs_ = on; }
+  int64_t graph_captures() const { return graph_captures_; }
 
   // Cached tensor map for an activation buffer viewed as rows x cols bf16.
   const void* act_tmap(const void* base, int rows, int cols, int box_rows);
@@ -210,6 +217,27 @@ class Runtime {
   int64_t pool_blocks_;
   int max_pos_;
   int64_t launches_ = 0;
+  AttnTimer* gemm_timer_ = nullptr;
+  struct GraphKey {
+    const void* model;
+    const void* ws;
+    int n, splits;
+    bool tokens;
+    bool operator<(const GraphKey& o) const {
+      return std::tie(model, ws, n, splits, tokens) < std::tie(o.model, o.ws, o.n, o.splits, o.tokens);
+    }
+  };
+  struct GraphEntry {
+    cudaGraphExec_t exec;
+    int64_t kernels;  // kernels per replay (launch accounting)
+    uint64_t used;    // LRU clock
+  };
+  static constexpr size_t kMaxGraphs = 384;
+  bool use_graphs_ = true;
+  std::map<GraphKey, GraphEntry> graphs_;
+  std::map<GraphKey, int> graph_seen_;
+  uint64_t graph_clock_ = 0;
+  int64_t graph_captures_ = 0;
   int gemm_min_iters_ = 8;  // scripts/min_iters_sweep.py: 8 is never slower on the whole GPU, -6..-11% at batch 128
   DevMem pool_;
   DevMem rope_;

@@ -64,8 +64,9 @@ decode_attention_kernel(const DecodeAttnArgs a) {
 
   const int ctx = a.ctx[b];
   const int nrows_total = (ctx + kBlockTok - 1) / kBlockTok;
-  const int r0 = split * a.rows_per_split;
-  const int r1 = min(nrows_total, r0 + a.rows_per_split);
+  const int rps = a.rows_per_split_dev != nullptr ? *a.rows_per_split_dev : a.rows_per_split;
+  const int r0 = split * rps;
+  const int r1 = min(nrows_total, r0 + rps);
   const int n = max(0, r1 - r0);
 
   if (threadIdx.x == 0) {
@@ -353,8 +354,15 @@ cudaError_t launch_decode(const DecodeAttnArgs& a, cudaStream_t stream) {
 int decode_attention_max_rows_per_split() { return kMaxIdsPerSplit; }
 
 cudaError_t preload_decode_attention() {
-  return preload(decode_attention_kernel<4, float>, decode_attention_kernel<4, __nv_bfloat16>,
-                 decode_attention_combine<float>, decode_attention_combine<__nv_bfloat16>);
+  cudaError_t e = preload(decode_attention_kernel<4, float>, decode_attention_kernel<4, __nv_bfloat16>,
+                          decode_attention_combine<float>, decode_attention_combine<__nv_bfloat16>);
+  // attributes set at unit creation: no first launch inside a graph capture
+  if (e != cudaSuccess) return e;
+  e = cudaFuncSetAttribute(decode_attention_kernel<4, float>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                           static_cast<int>(sizeof(AttnSmem<4>)));
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(decode_attention_kernel<4, __nv_bfloat16>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                              static_cast<int>(sizeof(AttnSmem<4>)));
 }
 
 cudaError_t decode_attention(const DecodeAttnArgs& a, bool fp32_out, cudaStream_t stream) {

@@ -51,11 +51,17 @@ namespace {
 constexpr int kBM = 128;  // W rows per tile (UMMA M)
 constexpr int kBK = 64;   // K per stage (one 128-byte swizzle atom)
 constexpr int kAStageBytes = kBM * kBK * 2;
-constexpr int kThreads = 384;               // warps 0-3 roles, warps 4-11 two epilogue groups
+// Warps 0-3: roles; then EG epilogue groups of four warps. EG = 2 (one CTA
+// per SM, the big ring) for decode batches above 64 tokens; EG = 1 with a
+// <= 113 KB ring for smaller batches, so TWO GEMM CTAs fit one SM: under PDL
+// the next projection's CTAs start streaming their weights while this one
+// drains, and colocated models' GEMMs on different streams co-reside.
+template <int EG>
+constexpr int threads_of() { return 128 + EG * 128; }
 constexpr int kEpiThreads = 128;            // one epilogue group: a warp per TMEM lane quarter
-constexpr int kEpiGroups = 2;
 constexpr int kChunkBytes = 32 * kBM * 4;  // one epilogue chunk: 32 tokens x 128 fp32
 constexpr int kSmemBudget = 224 * 1024;     // A ring + B ring + 2 staging chunks
+constexpr int kDualSmemBudget = 110 * 1024;  // EG = 1: rings + staging of one of two CTAs per SM
 constexpr int kPreIssue = 2;                // weight stages issued before the block barrier
 
 struct PeerMaps {
@@ -84,6 +90,7 @@ struct GemmRun {
   uint32_t tmem_cols;
   unsigned long long* timing;  // debug: [grid][64] globaltimer stamps, or null
   int dbg_nomma;    // debug (MUX_GEMM_NOMMA=1): stream operands without MMAs
+  int eg;           // epilogue groups of the instantiation (template EG)
   // Tensor-parallel fan-out (kStoreF32 only): every finished tile is also
   // stored through peers.m[0..n_peers) (the same slot on the other ranks of
   // the mesh, NVLink peer memory), and once all of a CTA's stores have landed
@@ -209,14 +216,17 @@ __device__ __forceinline__ void epi_bar(int g) {
   if (g == 0) asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
   else asm volatile("bar.sync 2, %0;" ::"n"(kEpiThreads) : "memory");
 }
+template <int EG>
 __device__ __forceinline__ void epi_bar_all() {
-  asm volatile("bar.sync 3, %0;" ::"n"(kEpiGroups * kEpiThreads) : "memory");
+  if constexpr (EG == 1) asm volatile("bar.sync 1, %0;" ::"n"(kEpiThreads) : "memory");
+  else asm volatile("bar.sync 3, %0;" ::"n"(2 * kEpiThreads) : "memory");
 }
 
 #define STAMP(cond, slot) \
   do { if (r.timing != nullptr && (cond)) r.timing[c * 64 + (slot)] = gtimer(); } while (0)
 
-__global__ void __launch_bounds__(kThreads, 1)
+template <int EG>
+__global__ void __launch_bounds__(threads_of<EG>(), 3 - EG)
 gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
                const __grid_constant__ CUtensorMap tout, const GemmRun r, const __grid_constant__ PeerMaps peers) {
   extern __shared__ __align__(1024) uint8_t smem_raw[];
@@ -231,6 +241,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   uint8_t* a_st = base;
   uint8_t* b_st = base + SA * kAStageBytes;
   uint8_t* stage_out = b_st + SB * b_stage_bytes;  // 2 x 16 KiB epilogue staging
+  constexpr int kEpiGroups = EG;
   uint64_t* full_a = reinterpret_cast<uint64_t*>(stage_out + kEpiGroups * kChunkBytes);
   uint64_t* empty_a = full_a + SA;
   uint64_t* full_b = empty_a + SA;
@@ -435,9 +446,14 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       const int tok0 = nt * r.n_tile;
       const int nchunk = (r.n_tile + 31) / 32;
       if (n_part > 0 && lead0) {
-        for (int p = pa; p <= pb; ++p)
-          if (p != fix)
-            while (ld_acquire(r.flags + 2 * p + (p == pa ? 1 : 0)) != r.epoch) __nanosleep(32);
+        for (int p = pa; p <= pb; ++p) {
+          if (p == fix) continue;
+          int* f = r.flags + 2 * p + (p == pa ? 1 : 0);
+          while (ld_acquire(f) != r.epoch) __nanosleep(32);
+          // every published flag has exactly one reader: clear it, so a
+          // replay of the same launch (CUDA graph, same epoch) waits again
+          *f = 0;
+        }
         STAMP(true, 6);
       }
       mbar_wait(&tm_full[b], (seg >> 1) & 1);
@@ -532,7 +548,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       }
       if (partner) {  // publish: both groups' partial bulk writes complete, then the flag
         if (leader) bulk_wait<0>();
-        epi_bar_all();
+        epi_bar_all<EG>();
         if (lead0) {
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
           st_release(r.flags + 2 * c + slot, r.epoch);
@@ -550,7 +566,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       else bulk_wait_read<0>();
     }
     if (r.n_signal > 0) {
-      epi_bar_all();  // both groups' stores have landed
+      epi_bar_all<EG>();  // both groups' stores have landed
       if (lead0) {
         // every store of this CTA (local + peers) has completed: publish
         asm volatile("fence.proxy.async.global;" ::: "memory");
@@ -686,7 +702,18 @@ cudaError_t weight_tile(const void* src, int N, int K, void* dst, bool inverse, 
   return cudaGetLastError();
 }
 
-cudaError_t preload_gemm() { return preload(gemm_tn_kernel, weight_tile_kernel); }
+// Attributes are set here too (per device, at unit creation), so no launch
+// inside a CUDA-graph capture is the first one on its device.
+static cudaError_t configure_gemm() {
+  cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  if (e != cudaSuccess) return e;
+  return cudaFuncSetAttribute(gemm_tn_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 116 * 1024);
+}
+
+cudaError_t preload_gemm() {
+  cudaError_t e = preload(gemm_tn_kernel<1>, gemm_tn_kernel<2>, weight_tile_kernel);
+  return e != cudaSuccess ? e : configure_gemm();
+}
 
 static unsigned long long* g_debug_timing = nullptr;
 void gemm_debug_timing(void* buf) { g_debug_timing = static_cast<unsigned long long*>(buf); }
@@ -705,6 +732,8 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   r.ldo = a.ldo;
   r.n_tile = gemm_pick_n_tile(a.M);
   const int b_stage = r.n_tile * kBK * 2;
+  static const int env_dual = getenv("MUX_GEMM_DUAL") ? atoi(getenv("MUX_GEMM_DUAL")) : 1;
+  r.eg = (env_dual && r.n_tile <= 64) ? 1 : 2;
   r.stages_b = r.n_tile > 128 ? 2 : 3;
   // Debug overrides for pipeline-depth sweeps (scripts/gemm_micro.py).
   static const int env_sb = getenv("MUX_GEMM_SB") ? atoi(getenv("MUX_GEMM_SB")) : 0;
@@ -713,7 +742,9 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   static const int env_nomma = getenv("MUX_GEMM_NOMMA") ? atoi(getenv("MUX_GEMM_NOMMA")) : 0;
   r.dbg_nomma = env_nomma != 0;
   static const int env_budget = getenv("MUX_GEMM_SMEM_KB") ? atoi(getenv("MUX_GEMM_SMEM_KB")) * 1024 : kSmemBudget;
-  r.stages_a = (env_budget - r.stages_b * b_stage - kEpiGroups * kChunkBytes) / kAStageBytes;
+  // two co-resident CTAs: (228 KB - 2 x 1 KB reserved) / 2 minus alignment slack
+  const int budget = r.eg == 1 ? kDualSmemBudget : env_budget;
+  r.stages_a = (budget - r.stages_b * b_stage - r.eg * kChunkBytes) / kAStageBytes;
   if (env_sa > 0) r.stages_a = std::min(env_sa, r.stages_a);
   else if (r.stages_a > 10) r.stages_a = 10;
   r.kb = (a.K + kBK - 1) / kBK;
@@ -755,7 +786,7 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   }
   r.sk_iters = (tiles - static_cast<int64_t>(r.n_dp) * grid) * r.kb;
   smem_out = 1024 + static_cast<size_t>(r.stages_a) * kAStageBytes + static_cast<size_t>(r.stages_b) * b_stage +
-             kEpiGroups * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16;
+             r.eg * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16;
   grid_out = grid;
 }
 
@@ -770,8 +801,7 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   // device index math is 32-bit (range_begin): iters * (grid + 1) must fit
   if (static_cast<uint64_t>(r.iters) * static_cast<uint64_t>(grid + 1) >= (1ull << 32)) return cudaErrorInvalidValue;
   static PerDeviceOnce configured;
-  cudaError_t ce = configured.run(
-      [] { return cudaFuncSetAttribute(gemm_tn_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448); });
+  cudaError_t ce = configured.run(configure_gemm);
   if (ce != cudaSuccess) return ce;
   r.n_peers = a.n_peers;
   r.n_signal = a.n_signal;
@@ -785,7 +815,8 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   std::memcpy(&tx, a.tmap_x, sizeof(CUtensorMap));
   std::memcpy(&to, a.tmap_out, sizeof(CUtensorMap));
   if (a.grid_out != nullptr) *a.grid_out = grid;
-  return launch(gemm_tn_kernel, dim3(grid), dim3(kThreads), smem, stream, tw, tx, to, r, pm);
+  if (r.eg == 1) return launch(gemm_tn_kernel<1>, dim3(grid), dim3(threads_of<1>()), smem, stream, tw, tx, to, r, pm);
+  return launch(gemm_tn_kernel<2>, dim3(grid), dim3(threads_of<2>()), smem, stream, tw, tx, to, r, pm);
 }
 
 }  // namespace mux

@@ -22,6 +22,9 @@ struct DecodeAttnArgs {
   int* split_count;         // [B][H] zeroed: the last split CTA merges in-kernel (null: combine launch)
   int B, H, layer, max_rows, row_width;
   int splits, rows_per_split;
+  // Rows per split from device memory (staged with the job's metadata), so
+  // one CUDA-graph capture serves every context length; null: rows_per_split.
+  const int32_t* rows_per_split_dev;
   float scale_log2;         // log2(e) / sqrt(128)
 };
 cudaError_t decode_attention(const DecodeAttnArgs& a, bool fp32_out, cudaStream_t stream);

@@ -511,6 +511,13 @@ class Unit:
         check(lib.mux_unit_attn_time(self._h, C.byref(ms), C.byref(n), C.byref(by)))
         return ms.value, n.value, by.value
 
+    def gemm_time(self):
+        """(total ms, launches, weight bytes) of the decode GEMMs timed while
+        attn_timing is on."""
+        ms, n, by = C.c_double(), C.c_int64(), C.c_double()
+        check(lib.mux_unit_gemm_time(self._h, C.byref(ms), C.byref(n), C.byref(by)))
+        return ms.value, n.value, by.value
+
     def tp_mailbox(self, partition: int):
         """(device pointer, 64-byte CUDA IPC handle) of a partition's TP mailbox."""
         ptr = C.c_void_p()
