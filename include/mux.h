@@ -147,6 +147,11 @@ typedef struct {
    * step_frac} (kv_manager.hpp QuotaAdaptParams; config keys
    * sim.quota_low_mark / quota_high_mark / quota_step_frac, config.cpp:242-244). */
   const double* quota_adapt;
+  /* NULL: the reference's tp_speedup = eta * tp (cost_model.cpp:43-47). Else
+   * 2 doubles {allreduce_alpha_ms, allreduce_ms_per_mib}: a tp > 1 job costs
+   * t(1)/tp + 2 * num_layers * (alpha + per_mib * tokens * hidden * 4 B / MiB)
+   * (B200 extension, LatencyProfile::tp_scaled; DESIGN §4 "f1"). */
+  const double* tp_allreduce;
 } mux_sim_config;
 
 typedef struct {
@@ -196,6 +201,27 @@ MUX_API int mux_sim_stats_unit(const mux_sim_stats* stats, int unit, mux_unit_st
 MUX_API int mux_sim_stats_llms(const mux_sim_stats* stats, int unit, mux_unit_llm_stats* out /* [n_llms] */);
 MUX_API int mux_sim_stats_samples(const mux_sim_stats* stats, int unit, mux_pool_sample* out /* [n_samples] */);
 MUX_API void mux_sim_stats_destroy(mux_sim_stats* stats);
+
+/* Realizable parallel candidates (llm_parallel_candidates,
+ * placement.cpp:57-103, plus the engine's shardability filter: tp must divide
+ * num_heads and, when entry.ffn > 0, the FFN width). One
+ * candidate per (model, realizable tp in tp_list) in entry order; llm = entry
+ * index. Profile blocks as in mux_sim_config (NULL = defaults). sm_list NULL
+ * or n_sm 0 = {0.1, ..., 1.0}. MUX_EINFEAS (reference InfeasibleError) when a
+ * model has no width that both fits and shards. */
+typedef struct {
+  int llm;
+  int tp_degree;
+  double num_sm;
+  int batch;
+  double est_tpt;
+  int saturated;
+} mux_candidate;
+MUX_API int mux_parallel_candidates(int n_entries, const mux_llm_entry* entries, int num_nodes, int gpus_per_node,
+                                    int64_t gpu_memory_bytes, const double* profile, const double* decode_hbm,
+                                    const double* tp_allreduce, int n_tp, const int* tp_list, int n_sm,
+                                    const double* sm_list, double activation_reserve_frac, int max_batch,
+                                    mux_candidate* out, int capacity, int* n_out);
 
 /* slo_reference_latency_ms (metrics.cpp:21-27): the unloaded latency a
  * request's SLO is a multiple of. profile: 7 doubles or NULL (defaults). */

@@ -4,9 +4,9 @@ pool, with sm_100a kernels for decode attention, KV append and tcgen05 GEMMs.
 Everything runs in libmux.so (csrc/); this package is the ctypes mirror of the
 reference's C++ API (see host.py and include/mux.h).
 """
-from ._lib import LIB_PATH, MuxError, header_symbols, lib  # noqa: F401
+from ._lib import LIB_PATH, Infeasible, InvalidArgument, LogicError, MuxError, header_symbols, lib  # noqa: F401
 from .host import (CATALOG, AllocResult, BlockPool, EngineParams, Entry, LLMSpec, Placement,  # noqa: F401
-                   QuotaInput, TraceRequest, Unit, adapt_quota, blocks_for_tokens, blocks_per_token, byte_share_partitions,
+                   ParallelCandidate, QuotaInput, TraceRequest, parallel_candidates, Unit, adapt_quota, blocks_for_tokens, blocks_per_token, byte_share_partitions,
                    decode_attention_headwise, gemm_bf16, init_token_block_quota, kv_append,
                    prefill_attention,
                    rope_table, simulate, spec, weight_tile)

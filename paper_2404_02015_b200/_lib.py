@@ -59,7 +59,12 @@ class SimConfig(C.Structure):
                 ("block_tokens", C.c_int), ("warmup_s", f64), ("decode_sm", f64),
                 ("prefill_min_sm", f64), ("activation_reserve_frac", f64),
                 ("quota_floor_frac", f64), ("decode_hbm", P(f64)),
-                ("quota_adapt", P(f64))]
+                ("quota_adapt", P(f64)), ("tp_allreduce", P(f64))]
+
+
+class Candidate(C.Structure):
+    _fields_ = [("llm", C.c_int), ("tp_degree", C.c_int), ("num_sm", f64), ("batch", C.c_int),
+                ("est_tpt", f64), ("saturated", C.c_int)]
 
 
 class RouteRecord(C.Structure):
@@ -127,6 +132,9 @@ _SIGS = {
     "mux_sim_stats_llms": (C.c_int, [vp, C.c_int, P(UnitLlmStats)]),
     "mux_sim_stats_samples": (C.c_int, [vp, C.c_int, P(PoolSample)]),
     "mux_sim_stats_destroy": (None, [vp]),
+    "mux_parallel_candidates": (C.c_int, [C.c_int, P(LlmEntry), C.c_int, C.c_int, i64, P(f64), P(f64), P(f64),
+                                          C.c_int, P(C.c_int), C.c_int, P(f64), f64, C.c_int, P(Candidate),
+                                          C.c_int, P(C.c_int)]),
     "mux_slo_reference_latency_ms": (C.c_int, [P(LlmEntry), P(f64), C.c_int, C.c_int, C.c_int, P(f64)]),
     "mux_decode_attention_headwise": (C.c_int, [vp, vp, vp, vp, vp, vp, C.c_int, C.c_int, C.c_int,
                                                 C.c_int, C.c_int, C.c_int, vp, C.c_int, C.c_int,

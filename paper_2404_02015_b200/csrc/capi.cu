@@ -24,6 +24,7 @@
 #include "device/runtime.h"
 #include "kernels/kernels.h"
 #include "kernels/launch.cuh"
+#include "mux/planner.hpp"
 #include "mux/engine.hpp"
 #include "mux/kv.hpp"
 
@@ -134,6 +135,34 @@ struct SimInputs {
   muxsim::EngineParams params;
 };
 
+// LatencyProfile from the ABI's optional blocks: the reference's 7 fields
+// (cost_model.hpp:33-40), the HBM decode form and the measured TP allreduce
+// terms (B200 extensions; NULL = the reference's defaults / forms).
+muxsim::LatencyProfile profile_of(const double* p, const double* decode_hbm, const double* tp_allreduce) {
+  muxsim::LatencyProfile prof;
+  if (p) {
+    prof.prefill_ms_per_token = p[0];
+    prof.decode_base_ms = p[1];
+    prof.decode_ctx_ms_per_token = p[2];
+    prof.tp_efficiency = p[3];
+    prof.sm_saturation_point = p[4];
+    prof.batch_knee = p[5];
+    prof.reference_scale = p[6];
+  }
+  if (decode_hbm) {
+    prof.decode_form = 1;
+    prof.decode_fixed_ms = decode_hbm[0];
+    prof.decode_row_ms = decode_hbm[1];
+    prof.decode_bctx_ms = decode_hbm[2];
+    prof.decode_sm_exponent = decode_hbm[3];
+  }
+  if (tp_allreduce) {
+    prof.allreduce_alpha_ms = tp_allreduce[0];
+    prof.allreduce_ms_per_mib = tp_allreduce[1];
+  }
+  return prof;
+}
+
 SimInputs build_inputs(const mux_sim_config* c, int n_entries, const mux_llm_entry* entries, int n_req,
                        const mux_request* trace) {
   require(c != nullptr && entries != nullptr && (n_req == 0 || trace != nullptr), "null argument");
@@ -176,23 +205,7 @@ SimInputs build_inputs(const mux_sim_config* c, int n_entries, const mux_llm_ent
     r.output_len = trace[i].output_len;
     in.trace.push_back(r);
   }
-  if (c->profile) {
-    const double* p = c->profile;
-    in.prof.prefill_ms_per_token = p[0];
-    in.prof.decode_base_ms = p[1];
-    in.prof.decode_ctx_ms_per_token = p[2];
-    in.prof.tp_efficiency = p[3];
-    in.prof.sm_saturation_point = p[4];
-    in.prof.batch_knee = p[5];
-    in.prof.reference_scale = p[6];
-  }
-  if (c->decode_hbm) {
-    in.prof.decode_form = 1;
-    in.prof.decode_fixed_ms = c->decode_hbm[0];
-    in.prof.decode_row_ms = c->decode_hbm[1];
-    in.prof.decode_bctx_ms = c->decode_hbm[2];
-    in.prof.decode_sm_exponent = c->decode_hbm[3];
-  }
+  in.prof = profile_of(c->profile, c->decode_hbm, c->tp_allreduce);
   in.params.scheduler = static_cast<muxsim::SchedKind>(c->scheduler);
   in.params.kappa = c->kappa;
   in.params.quota_period_s = c->quota_period_s;
@@ -920,6 +933,47 @@ int mux_sim_stats_samples(const mux_sim_stats* st, int u, mux_pool_sample* out) 
       const muxsim::PoolSample& p = us.samples[i];
       out[i] = {p.t_s, st->idx.at(p.llm), p.used_blocks, p.quota_blocks};
     }
+  });
+}
+
+int mux_parallel_candidates(int n_entries, const mux_llm_entry* entries, int num_nodes, int gpus_per_node,
+                            int64_t gpu_memory_bytes, const double* profile, const double* decode_hbm,
+                            const double* tp_allreduce, int n_tp, const int* tp_list, int n_sm,
+                            const double* sm_list, double activation_reserve_frac, int max_batch,
+                            mux_candidate* out, int capacity, int* n_out) {
+  return guarded([&] {
+    require(n_entries >= 0 && (n_entries == 0 || entries != nullptr) && n_out != nullptr, "null argument");
+    require(n_tp >= 0 && (n_tp == 0 || tp_list != nullptr) && n_sm >= 0 && (n_sm == 0 || sm_list != nullptr),
+            "null argument");
+    std::vector<muxsim::LlmEntry> llms;
+    std::vector<int> ffn;
+    for (int i = 0; i < n_entries; ++i) {
+      muxsim::LlmEntry e;
+      e.spec = spec_of(entries[i]);
+      e.rate = entries[i].rate;
+      e.mean_prompt_tokens = entries[i].mean_prompt_tokens;
+      e.mean_output_tokens = entries[i].mean_output_tokens;
+      llms.push_back(e);
+      ffn.push_back(entries[i].ffn);
+    }
+    muxsim::Cluster cl;
+    cl.num_nodes = num_nodes;
+    cl.gpus_per_node = gpus_per_node;
+    cl.gpu_memory_bytes = gpu_memory_bytes;
+    muxsim::CandidateParams cp;
+    if (n_tp) cp.tp_list.assign(tp_list, tp_list + n_tp);
+    if (n_sm) cp.sm_list.assign(sm_list, sm_list + n_sm);
+    cp.activation_reserve_frac = activation_reserve_frac;
+    cp.max_batch = max_batch;
+    auto cands = muxsim::realizable_parallel_candidates(llms, cl, profile_of(profile, decode_hbm, tp_allreduce), cp, ffn);
+    int n = 0;
+    for (size_t i = 0; i < cands.size(); ++i)
+      for (const auto& c : cands[i]) {
+        if (out != nullptr && n < capacity)
+          out[n] = {static_cast<int>(i), c.tp_degree, c.num_sm, c.batch, c.est_tpt, c.saturated ? 1 : 0};
+        ++n;
+      }
+    *n_out = n;
   });
 }
 

@@ -15,7 +15,7 @@ from typing import Iterable, Sequence
 
 from ._lib import (ALLOC_OK, ALLOC_POOL, ALLOC_QUOTA, LlmEntry as _CEntry, PlacedLlm, Record,
                    Request as _CRequest, SimConfig, UnitConfig, check, lib)
-from ._lib import RouteRecord as _RouteRecord
+from ._lib import Candidate as _Candidate, RouteRecord as _RouteRecord
 from ._lib import PoolSample as _PoolSample, UnitLlmStats as _UnitLlmStats, UnitStats as _UnitStats
 
 # ----------------------------------------------------------------- model specs
@@ -275,6 +275,24 @@ class _Built:
     keep: list = field(default_factory=list)
 
 
+def _profile_blocks(profile: Sequence[float] | None):
+    """The ABI's profile blocks from a flat list: the reference's 7
+    LatencyProfile doubles (cost_model.hpp:33-40), optionally followed by the
+    HBM decode form's 4 (decode_fixed_ms, decode_row_ms, decode_bctx_ms,
+    decode_sm_exponent; LatencyProfile::decode_form 1) and/or the measured TP
+    allreduce's 2 (allreduce_alpha_ms, allreduce_ms_per_mib): lengths 7, 9
+    (+TP), 11 (+HBM) or 13 (+HBM +TP)."""
+    if profile is None:
+        return None, None, None
+    n = len(profile)
+    if n not in (7, 9, 11, 13):
+        raise ValueError("profile: 7 reference values, + 4 HBM decode-form values and/or + 2 TP allreduce values")
+    prof = (C.c_double * 7)(*profile[:7])
+    hbm = (C.c_double * 4)(*profile[7:11]) if n >= 11 else None
+    tpar = (C.c_double * 2)(*profile[-2:]) if n in (9, 13) else None
+    return prof, hbm, tpar
+
+
 def _build_config(gpu_memory_bytes: int, num_gpus: int, placement: Placement, params: EngineParams,
                   profile: Sequence[float] | None) -> _Built:
     keep = []
@@ -282,20 +300,14 @@ def _build_config(gpu_memory_bytes: int, num_gpus: int, placement: Placement, pa
     placed_list = [PlacedLlm(u, e, placement.mesh_sizes[u], placement.num_sm)
                    for u, mem in enumerate(placement.members) for e in mem]
     placed = (PlacedLlm * max(len(placed_list), 1))(*placed_list)
-    # profile: the reference's 7 LatencyProfile doubles, optionally followed
-    # by the HBM decode form's 4 (decode_fixed_ms, decode_row_ms,
-    # decode_bctx_ms, decode_sm_exponent; LatencyProfile::decode_form 1)
-    if profile is not None and len(profile) not in (7, 11):
-        raise ValueError("profile: 7 reference values, or 7 + 4 HBM decode-form values")
-    prof = None if profile is None else (C.c_double * 7)(*profile[:7])
-    hbm = None if profile is None or len(profile) == 7 else (C.c_double * 4)(*profile[7:])
+    prof, hbm, tpar = _profile_blocks(profile)
     adapt = (C.c_double * 3)(params.quota_low_mark, params.quota_high_mark, params.quota_step_frac)
-    keep += [sizes, placed, prof, hbm, adapt]
+    keep += [sizes, placed, prof, hbm, tpar, adapt]
     cfg = SimConfig(1, num_gpus, gpu_memory_bytes, len(placement.mesh_sizes), sizes, len(placed_list),
                     placed, prof, params.scheduler, params.kappa, params.quota_period_s,
                     params.token_budget, params.block_tokens, params.warmup_s, params.decode_sm,
                     params.prefill_min_sm, params.activation_reserve_frac, params.quota_floor_frac, hbm,
-                    adapt)
+                    adapt, tpar)
     return _Built(cfg, keep)
 
 
@@ -381,6 +393,40 @@ def slo_reference_latency_ms(s: LLMSpec, profile: Sequence[float] | None, tp_deg
     out = C.c_double()
     check(lib.mux_slo_reference_latency_ms(C.byref(e), prof, tp_degree, prompt_len, output_len, C.byref(out)))
     return out.value
+
+
+@dataclass
+class ParallelCandidate:
+    """ParallelCandidate (placement.hpp:45-52)."""
+    tp_degree: int
+    num_sm: float
+    batch: int
+    est_tpt: float
+    saturated: bool
+
+
+def parallel_candidates(entries: Sequence[Entry], gpus_per_node: int, gpu_memory_bytes: int, num_nodes: int = 1,
+                        profile: Sequence[float] | None = None, tp_list: Sequence[int] = (1, 2, 4, 8),
+                        sm_list: Sequence[float] | None = None, activation_reserve_frac: float = 0.1,
+                        max_batch: int = 256) -> list[list[ParallelCandidate]]:
+    """llm_parallel_candidates (placement.cpp:57-103) restricted to tp widths
+    the engine can shard (tp | num_heads, tp | ffn): one list per entry,
+    ascending in tp_list order. Raises Infeasible when a model has none."""
+    keep = []
+    ents = _c_entries(entries, keep)
+    prof, hbm, tpar = _profile_blocks(profile)
+    tps = (C.c_int * max(1, len(tp_list)))(*tp_list)
+    sms = (C.c_double * max(1, len(sm_list or ())))(*(sm_list or ()))
+    cap = max(1, len(entries) * len(tp_list))
+    out = (_Candidate * cap)()
+    n = C.c_int()
+    check(lib.mux_parallel_candidates(len(entries), ents, num_nodes, gpus_per_node, gpu_memory_bytes, prof, hbm, tpar,
+                                      len(tp_list), tps, len(sm_list or ()), sms, activation_reserve_frac, max_batch,
+                                      out, cap, C.byref(n)))
+    res = [[] for _ in entries]
+    for c in out[:n.value]:
+        res[c.llm].append(ParallelCandidate(c.tp_degree, c.num_sm, c.batch, c.est_tpt, bool(c.saturated)))
+    return res
 
 
 # ---------------------------------------------------------------------- Unit

@@ -34,6 +34,9 @@ PROFILE_DEFAULTS = [0.25, 12.0, 0.005, 0.9, 0.5, 16.0, 32.0 * 4096.0]
 # DESIGN §4). A profile block holding all three keys selects it; the
 # reference's configs never carry them, so their parsing is unchanged.
 HBM_KEYS = ["decode_fixed_ms", "decode_row_ms", "decode_bctx_ms", "decode_sm_exponent"]
+# B200 extension: the measured tensor-parallel allreduce in place of
+# tp_speedup = eta * tp (LatencyProfile::tp_scaled, f1). Both keys or none.
+TP_KEYS = ["allreduce_alpha_ms", "allreduce_ms_per_mib"]
 SCHEDULERS = {"adbs": 0, "fcfs": 1, "round_robin": 2, "rr": 2}
 
 
@@ -259,22 +262,30 @@ def load_config(path: str, catalog: dict[str, LLMSpec] | None = None) -> Experim
         if pc.get("backend", "greedy") not in ("greedy", "ilp"):
             _fail("placement.backend must be greedy or ilp")
     prof = list(PROFILE_DEFAULTS)
-    hbm = {}
+    hbm, tpk = {}, {}
     pr = root.get("profile")
     if pr is not None:
         if not isinstance(pr, dict):
             _fail("profile must be an object")
-        _check_keys(pr, "profile", PROFILE_KEYS + HBM_KEYS)
+        _check_keys(pr, "profile", PROFILE_KEYS + HBM_KEYS + TP_KEYS)
         for k in pr:
             v = _num(pr, "profile", k)
             if k in HBM_KEYS:
                 hbm[k] = v
+            elif k in TP_KEYS:
+                tpk[k] = v
             else:
                 prof[PROFILE_KEYS.index(k)] = v
     if hbm:
         if len(hbm) != len(HBM_KEYS):
             raise ConfigError("profile: the HBM decode form needs " + ", ".join(HBM_KEYS))
         prof += [hbm[k] for k in HBM_KEYS]
+    if tpk:
+        if len(tpk) != len(TP_KEYS):
+            raise ConfigError("profile: the measured TP allreduce needs " + ", ".join(TP_KEYS))
+        if min(tpk.values()) < 0.0:
+            _fail("latency profile: allreduce terms must be >= 0")
+        prof += [tpk[k] for k in TP_KEYS]
     # LatencyProfile::validate (cost_model.cpp:49-59), reported as ConfigError
     pp, db, dc, tpe, sat, knee, rs = prof[:7]
     if not (pp > 0.0 and db > 0.0 and dc >= 0.0):

@@ -2,6 +2,7 @@
 plan.json / trace.csv in, records.csv / metrics.json / poolstats.json out,
 byte-identical to the unmodified reference CLI on the same inputs (goldens in
 tests/golden/wire, made by make_wire_golden.sh with oracle/_ref/muxsim)."""
+import json
 import os
 
 import pytest
@@ -118,3 +119,23 @@ def test_plan_split_and_unit_pools_match_reference():
     got = [cluster.unit_pool_blocks([e.spec for e in j.entries], len(j.gpu_ids), exp.gpu_memory_bytes,
                                     exp.params.activation_reserve_frac) for j in jobs]
     assert got == want
+
+
+def test_profile_tp_allreduce_keys(tmp_path):
+    """B200 extension keys (wire.TP_KEYS): both or none, non-negative; they
+    append after the reference's 7 (and the HBM form's 4) profile values."""
+    from paper_2404_02015_b200 import wire
+    base = json.load(open(os.path.join(G, "cfg_b200prof.json")))
+    cfg = dict(base, profile=dict(base["profile"], allreduce_alpha_ms=0.02, allreduce_ms_per_mib=0.004))
+    p = tmp_path / "c.json"
+    p.write_text(json.dumps(cfg))
+    exp = wire.load_config(str(p))
+    assert len(exp.profile) == 9 and exp.profile[-2:] == [0.02, 0.004]
+    cfg["profile"].pop("allreduce_ms_per_mib")
+    p.write_text(json.dumps(cfg))
+    with pytest.raises(wire.ConfigError):
+        wire.load_config(str(p))
+    cfg["profile"].update(allreduce_ms_per_mib=-1.0)
+    p.write_text(json.dumps(cfg))
+    with pytest.raises(wire.ConfigError):
+        wire.load_config(str(p))
