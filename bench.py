@@ -83,6 +83,17 @@ def workload_config(args, world):
     """The config dict both arms print (identical, so the driver's
     ours-vs-reference ratio compares the same workload)."""
     models = args.models.split(",")
+    if args.placement and world > 1:
+        units = placement_plan(args.placement, world)
+        return {
+            "workload": f"cfg4 placement ({args.placement}/plan_g{world}.json, unmodified reference planner): "
+                        "one unit per rank, one ADBS decode round of every colocated model per step",
+            "units": [",".join(u) for u in units], "decode_batch_per_model": f"<= {args.batch} (fits the unit pool)",
+            "contexts": "ShareGPT lognormal prompt 161 / output 338 (sigma 0.8), members mid-generation, "
+                        "seed 1000 + rank (bench.sample_batch)",
+            "l2": "inputs larger than L2 (weights + KV per step)",
+            "parallelism": f"{world} placed units (one per GPU, no data-path collective)",
+        }
     return {
         "workload": "cfg2: LLaMA-7B + LLaMA-13B colocated per B200, one ADBS decode round per step",
         "models": args.models, "decode_batch_per_model": args.batch,
@@ -92,6 +103,49 @@ def workload_config(args, world):
         "l2": "inputs larger than L2 (39.5 GB weights + KV per step)",
         "parallelism": f"{world} independent units (dp{world})",
     }
+
+
+def placement_plan(name, world):
+    """A committed placement for a box of `world` GPUs
+    (scripts/<name>/plan_g<world>.json, made by the unmodified reference
+    planner) as the model-catalog names each rank (GPU) serves: its tp = 1
+    unit's models, or none for a GPU of an empty mesh."""
+    with open(os.path.join(ROOT, "scripts", name, f"cfg_g{world}.json")) as f:
+        cfg = json.load(f)
+    with open(os.path.join(ROOT, "scripts", name, f"plan_g{world}.json")) as f:
+        plan = json.load(f)
+    model_of = {e["name"]: e["model"] for e in cfg["llms"]}
+    ranks = [None] * world
+    for u in plan["units"]:
+        models = [model_of[m["name"]] for m in u["models"]]
+        if models and len(u["gpu_ids"]) != 1:
+            raise ValueError("bench --placement runs tp = 1 units (one per rank)")
+        for g in u["gpu_ids"]:  # an empty mesh idles all of its GPUs
+            if not 0 <= g < world or ranks[g] is not None:
+                raise ValueError(f"plan maps GPU {g} twice or outside the box")
+            ranks[g] = models
+    if any(r is None for r in ranks):
+        raise ValueError("plan leaves a GPU of the box unmapped")
+    return ranks
+
+
+def unit_models(args, rank, world):
+    """The models this rank's unit serves: --models (every rank its own
+    copy, the default), or unit `rank` of a committed placement."""
+    if args.placement and world > 1:
+        return placement_plan(args.placement, world)[rank]
+    return args.models.split(",")
+
+
+def idle_result(args, world):
+    """A rank whose mesh holds no model: it only joins the barriers."""
+    import torch
+    if world > 1:
+        torch.distributed.barrier()
+    return {"ms": 0.0, "tokens": 0, "launches": 0, "attn_ms": 0.0, "attn_n": 0, "attn_bytes": 0.0,
+            "clocks": {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["idle rank"]}, "gemm_ms": 0.0, "gemm_n": 0,
+            "gemm_bytes": 0.0, "e2e_ms": 0.0, "bytes_step": 0.0, "partition_sms": None, "job_ms_per_step": [],
+            "models": [], "batch": 0}
 
 
 def sample_batch(rng, B, extra_steps):
@@ -180,16 +234,21 @@ def run_ours(args, rank, world, local_rank):
     device = local_rank if torch.cuda.device_count() > local_rank else 0
     torch.cuda.set_device(device)
     local_rank = device
-    specs = [mux.spec(m) for m in args.models.split(",")]
-    B = args.batch
+    models = unit_models(args, rank, world)
+    if not models:  # an empty mesh of the placement: this rank serves nothing
+        return idle_result(args, world)
+    specs = [mux.spec(m) for m in models]
     steps_total = 2 * args.warmup + args.steps + args.e2e_steps + args.attn_steps + 2
-    rng = np.random.default_rng(1000 + rank)
-    batches = [sample_batch(rng, B, steps_total) for _ in specs]
-    need = 0
-    for s, reqs in zip(specs, batches):
-        for p, o, d in reqs:
-            need += mux.blocks_for_tokens(s, 16, p + d + steps_total + 1)
-    logical = pool_blocks(args.models.split(","))
+    logical = pool_blocks(models)
+    B = args.batch
+    while True:  # the largest batch <= --batch whose members fit the unified pool
+        rng = np.random.default_rng(1000 + rank)
+        batches = [sample_batch(rng, B, steps_total) for _ in specs]
+        need = sum(mux.blocks_for_tokens(s, 16, p + d + steps_total + 1)
+                   for s, reqs in zip(specs, batches) for p, o, d in reqs)
+        if need <= logical or B == 1:
+            break
+        B = max(1, B * 3 // 4)
     assert need <= logical, "batch exceeds the unified pool"
     max_ctx = max(p + d + steps_total + 1 for reqs in batches for p, o, d in reqs)
     if args.partition_sms == "auto" and len(specs) == 1:
@@ -203,7 +262,7 @@ def run_ours(args, rank, world, local_rank):
         psms = [int(x) for x in args.partition_sms.split(",")]
     args.partition_resolved = psms
     unit = mux.Unit(specs, pool_blocks=logical, device=local_rank, device_pool_blocks=need + 4096,
-                    max_batch=B, max_prefill_tokens=256, max_ctx=max_ctx + 16, max_slots=2 * B + 16,
+                    max_batch=B, max_prefill_tokens=256, max_ctx=max_ctx + 16, max_slots=len(specs) * B + 16,
                     init_seed=1 + rank, init_std=0.02, partitions=len(specs) + 1,
                     partition_sms=[0] + psms if psms else None)
     unit.set_option("pdl", args.pdl)
@@ -309,7 +368,7 @@ def run_ours(args, rank, world, local_rank):
         "ms": ms, "tokens": len(specs) * B * args.steps, "launches": launches,
         "attn_ms": attn_ms, "attn_n": attn_n, "attn_bytes": attn_bytes, "clocks": clk,
         "gemm_ms": gemm_ms, "gemm_n": gemm_n, "gemm_bytes": gemm_bytes,
-        "e2e_ms": e2e_ms, "bytes_step": bytes_step,
+        "e2e_ms": e2e_ms, "bytes_step": bytes_step, "models": models, "batch": B,
         "partition_sms": [unit_sms[li] for li in range(len(specs))] if psms else None,
         "job_ms_per_step": [round(x / args.steps, 3) for x in part_ms],
     }
@@ -324,6 +383,9 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--batch", type=int, default=128, help="decode members per model")
     ap.add_argument("--models", default="7b,13b")
+    ap.add_argument("--placement", default="",
+                    help="N > 1: run unit `rank` of the committed placement scripts/<name>/plan_g<N>.json "
+                         "(e.g. c4: BASELINE config 4) instead of N copies of --models")
     ap.add_argument("--e2e-steps", type=int, default=10)
     ap.add_argument("--attn-steps", type=int, default=2, help="steps with per-launch K1 events")
     ap.add_argument("--partition-sms", default="auto",
@@ -358,9 +420,16 @@ def main():
             torch.cuda.set_device(local_rank)
         torch.distributed.init_process_group(backend)
     r = run_ours(args, rank, world, local_rank)
-    tokens = r["tokens"] * world
     from paper_2404_02015_b200 import mesh
-    ms, e2e_ms = mesh.max_over_ranks([r["ms"], r["e2e_ms"]])  # the job ends with its slowest rank
+    ms, e2e_ms, max_bytes_step = mesh.max_over_ranks([r["ms"], r["e2e_ms"], r["bytes_step"]])  # slowest rank
+    # every rank's own unit: tokens, launches and the kernel timings add up
+    # (ranks of a placement serve different models; idle ranks add zero)
+    keys = ["tokens", "launches", "attn_ms", "attn_n", "attn_bytes", "gemm_ms", "gemm_n", "gemm_bytes"]
+    tot = dict(zip(keys, mesh.sum_over_ranks([float(r[k]) for k in keys])))
+    unit_models_all = mesh.gather_objects({"models": r["models"], "batch": r["batch"]})
+    tokens = tot["tokens"]
+    if rank == 0:
+        r = dict(r, **tot, bytes_step=max_bytes_step)
     hbm, peak_kind = peaks()
     achieved = r["attn_bytes"] / (r["attn_ms"] / 1e3) / 1e9 if r["attn_ms"] > 0 else 0.0
     value = tokens / (ms / 1e3)
@@ -403,7 +472,8 @@ def main():
                                "events, timed alone on the whole GPU; algorithmic bytes = the weights, N*K*2)",
                      "peak_source": peak_kind, "launches_timed": r["gemm_n"], "device_ms": round(r["gemm_ms"], 3),
                      "bytes_per_launch": round(r["gemm_bytes"] / max(1, r["gemm_n"]))}
-        # whole-job roofline: every rank streams its own weights + KV per step
+        # whole-job roofline: every rank streams its own weights + KV per step,
+        # the step lasts as long as the rank with the most bytes
         step_roof = per_step_tokens / (r["bytes_step"] / (hbm * 1e9)) if r["bytes_step"] else None
         line = {
             "metric": "aggregate decode tokens/s across colocated LLMs; paged-attn HBM GB/s vs peak",
@@ -419,7 +489,8 @@ def main():
             "dtype": "bf16",
             "data": "synthetic (random-init weights, ShareGPT-shaped lognormal lengths, random KV)",
             "config": workload_config(args, world),
-            "run": {"partition_sms": r["partition_sms"], "job_ms_per_step": r["job_ms_per_step"]},
+            "run": {"partition_sms": r["partition_sms"], "job_ms_per_step": r["job_ms_per_step"],
+                    "units": unit_models_all},
             "e2e": {"value": round(per_step_tokens / (e2e_ms / 1e3), 1) if e2e_ms else None,
                     "unit": "tokens/s", "h2d_bytes_per_step": int(per_step_tokens * 4),
                     "d2h_bytes_per_step": int(per_step_tokens * 4)},
@@ -432,7 +503,7 @@ def main():
                               "frac_nominal_8tbs": round(value / (step_roof * 8000.0 / hbm), 4) if step_roof else None},
             "cpu_baseline": cpu,
             "serving": serving,
-            "gpu_launches": r["launches"] * world,
+            "gpu_launches": int(r["launches"]),
             "clocks": r["clocks"],
         }
         print(json.dumps(line), flush=True)

@@ -41,6 +41,30 @@ def max_over_ranks(values: Sequence[float]) -> list[float]:
     return t.tolist()
 
 
+def sum_over_ranks(values: Sequence[float]) -> list[float]:
+    """Element-wise sum over ranks (tokens and kernel time of every unit)."""
+    import torch
+    import torch.distributed as dist
+    _, world = rank_world()
+    if world == 1:
+        return list(values)
+    dev = "cuda" if dist.get_backend() == "nccl" else "cpu"
+    t = torch.tensor(list(values), dtype=torch.float64, device=dev)
+    dist.all_reduce(t, op=dist.ReduceOp.SUM)
+    return t.tolist()
+
+
+def gather_objects(obj) -> list:
+    """Every rank's picklable `obj`, in rank order (plumbing only)."""
+    import torch.distributed as dist
+    _, world = rank_world()
+    if world == 1:
+        return [obj]
+    out: list = [None] * world
+    dist.all_gather_object(out, obj)
+    return out
+
+
 def tp_pool_blocks(total_blocks: int, tp: int) -> int:
     """KV head-blocks of one rank's pool slice: the mesh-wide
     pool of sim_engine.cpp:172-186 split by head, floor(total / tp)."""
