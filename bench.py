@@ -392,7 +392,7 @@ def main():
                     help="green-context SMs of each model's decode partition: 'auto' (shares of the per-round "
                          "HBM bytes, byte_share_partitions), 'none' (every job on the whole GPU), or e.g. 56,88")
     ap.add_argument("--serial", action="store_true", help="run the colocated decode jobs on one stream")
-    ap.add_argument("--serve-horizon", type=float, default=3.0,
+    ap.add_argument("--serve-horizon", type=float, default=6.0,
                     help="seconds of Poisson arrivals for the auxiliary measured serving run (0 = skip)")
     ap.add_argument("--pdl", type=int, default=1, help="programmatic dependent launch between job kernels")
     ap.add_argument("--skip-cpu", action="store_true", help="omit the cpu_baseline leg (profiling runs)")

@@ -69,6 +69,7 @@ def main():
             units = make_units(spec, tp, b, ctx)
             rids = list(range(1000, 1000 + b))
             for u in units:
+                u.pool.set_quota(0, u.pool.total_blocks())
                 for r in rids:
                     assert u.pool.admit(0, r, ctx, ctx + 64).ok
             try:

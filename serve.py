@@ -50,6 +50,21 @@ def make_trace(models, rates, horizon_s, seed, max_len=2048):
     return reqs
 
 
+def arrival_window_throughput(timeline_csv, horizon_s):
+    """Tokens/s produced by real-time jobs ending in [horizon/2, horizon]
+    (device ms from the run's origin; one token per member per job)."""
+    import csv
+    lo, hi = 500.0 * horizon_s, 1000.0 * horizon_s
+    tok = {"decode": 0, "prefill": 0}
+    with open(timeline_csv) as f:
+        for r in csv.DictReader(f):
+            if lo <= float(r["end_ms"]) < hi:
+                tok[r["kind"]] += int(r["batch"])
+    return {"tok_s": round((tok["decode"] + tok["prefill"]) / (0.5 * horizon_s), 1),
+            "decode_tok_s": round(tok["decode"] / (0.5 * horizon_s), 1),
+            "window_s": [0.5 * horizon_s, horizon_s]}
+
+
 def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, device=0, partition_sms=None,
           scheduler="adbs", gpu_memory_gib=180.0, lengths=None, prefill_on_partition=False, pass_green=None,
           realtime=False, align_decode=False, sm_route=False):
@@ -90,12 +105,24 @@ def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, 
         if sm_route:  # every job on a green context sized by its ADBS sm_demand
             unit.set_option("sm_route", 1)
         unit.init_kv(seed=5, std=1.0)
+        # real-time runs: the device timeline of every job (MUX_RT_TIMELINE)
+        # gives the tokens produced while arrivals are still coming in
+        own_tl = None
+        if realtime and not os.environ.get("MUX_RT_TIMELINE"):
+            import tempfile
+            own_tl = os.environ["MUX_RT_TIMELINE"] = os.path.join(tempfile.mkdtemp(), "timeline.csv")
         t0 = time.perf_counter()
         recs, _ = unit.run_lockstep(entries, trace, gpu_mem, params, measured=not realtime, realtime=realtime)
         wall = time.perf_counter() - t0
         passes, green_passes = unit.pass_stats()
     finally:
         unit.close()
+    window = None
+    tl = os.environ.get("MUX_RT_TIMELINE") if realtime else None
+    if tl and os.path.exists(tl):
+        window = arrival_window_throughput(tl, horizon_s)
+    if own_tl:
+        del os.environ["MUX_RT_TIMELINE"]
     out_tokens = sum(r.output_len for r in trace)
     first = min(r.arrival_s for r in recs)
     makespan = max(r.done_s for r in recs) - first
@@ -116,6 +143,11 @@ def serve(model_names=("7b", "13b"), rates=(20.0, 10.0), horizon_s=8.0, seed=3, 
                      "pass_green": pass_green, "engine": "realtime" if realtime else "measured",
                      "align_decode": align_decode, "sm_route": sm_route},
         "passes": passes, "green_passes": green_passes,
+        # tokens produced (decode jobs' batches, prefills' first tokens) by
+        # jobs ending in the second half of the arrival period, per second:
+        # the engine's throughput under the offered load, before the drain
+        # (the tail of long outputs at shrinking batch) that `value` includes
+        "arrival_window": window,
         "host_wall_s": round(wall, 2),
     }
 

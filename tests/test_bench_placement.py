@@ -47,3 +47,19 @@ def test_bench_placement_two_ranks_on_one_gpu(tmp_path):
     assert line["n_gpus"] == 2 and line["value"] > 0
     assert [u["models"] for u in line["run"]["units"]] == bench.placement_plan("c4", 2)
     assert line["config"]["units"] == [",".join(u) for u in bench.placement_plan("c4", 2)]
+
+
+@pytest.mark.parametrize("rate", [5, 10, 20, 40])
+def test_c5_sweep_inputs_are_consistent(rate):
+    """scripts/c5 (config 5, 19 LLMs): every model placed exactly once on a
+    tp = 1 unit that fits one GPU, and every trace row names a config model."""
+    from paper_2404_02015_b200 import wire
+    d = os.path.join(ROOT, "scripts", "c5")
+    exp = wire.load_config(os.path.join(d, f"cfg_r{rate}.json"))
+    plan = json.load(open(os.path.join(d, f"plan_r{rate}.json")))
+    placed = [m["name"] for u in plan["units"] for m in u["models"]]
+    assert sorted(placed) == sorted(exp.names) and len(exp.names) == 19
+    for u in plan["units"]:  # empty meshes may be wider: they idle
+        assert not u["models"] or (len(u["gpu_ids"]) == 1 and all(m["tp_degree"] == 1 for m in u["models"]))
+    trace = wire.load_trace(os.path.join(d, f"trace_r{rate}.csv"), exp.names)
+    assert trace and all(0 <= r.llm < 19 for r in trace)
