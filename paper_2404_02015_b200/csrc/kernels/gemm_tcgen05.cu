@@ -77,7 +77,8 @@ struct GemmRun {
   int M, N, K, ldo;
   int n_tile, stages_a, stages_b;
   int kb;           // k-blocks per tile
-  int m_tiles;      // ceil(N / 128)
+  int m_tiles;      // ceil(N / 128) / st: weight units along N
+  int st;           // 128-row weight tiles per unit (2: one activation stage feeds two MMAs)
   int64_t iters;    // tiles * kb
   // Prefill schedule (several token tiles): n_dp data-parallel rounds of
   // whole tiles (tile j*G + c), raster-grouped group_m weight tiles wide so
@@ -239,7 +240,8 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   const int SA = r.stages_a, SB = r.stages_b;
   const int b_stage_bytes = r.n_tile * kBK * 2;
   uint8_t* a_st = base;
-  uint8_t* b_st = base + SA * kAStageBytes;
+  const int a_stage_bytes = r.st * kAStageBytes;  // st weight tiles of one k-block
+  uint8_t* b_st = base + SA * a_stage_bytes;
   uint8_t* stage_out = b_st + SB * b_stage_bytes;  // 2 x 16 KiB epilogue staging
   constexpr int kEpiGroups = EG;
   uint64_t* full_a = reinterpret_cast<uint64_t*>(stage_out + kEpiGroups * kChunkBytes);
@@ -277,12 +279,16 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   };
   auto a_issue = [&]() {
     if (pround > 0) mbar_wait(&empty_a[ps], (pround - 1) & 1);
-    mbar_arrive_expect_tx(&full_a[ps], kAStageBytes);
-    if (r.w_tiled != nullptr)  // one contiguous, pre-swizzled 16 KiB UMMA tile
-      bulk_g2s_stream(a_st + ps * kAStageBytes, r.w_tiled + (static_cast<int64_t>(pm) * r.kb + pkb) * kAStageBytes,
-                      kAStageBytes, &full_a[ps], wpol);
-    else
-      tma_load_2d(a_st + ps * kAStageBytes, &tw, &full_a[ps], pkb * kBK, pm * kBM, wpol);
+    mbar_arrive_expect_tx(&full_a[ps], static_cast<uint32_t>(a_stage_bytes));
+    for (int j = 0; j < r.st; ++j) {
+      const int mt = pm * r.st + j;  // 128-row weight tile
+      uint8_t* dst = a_st + ps * a_stage_bytes + j * kAStageBytes;
+      if (r.w_tiled != nullptr)  // one contiguous, pre-swizzled 16 KiB UMMA tile
+        bulk_g2s_stream(dst, r.w_tiled + (static_cast<int64_t>(mt) * r.kb + pkb) * kAStageBytes, kAStageBytes,
+                        &full_a[ps], wpol);
+      else
+        tma_load_2d(dst, &tw, &full_a[ps], pkb * kBK, mt * kBM, wpol);
+    }
     if (++ps == SA) {
       ps = 0;
       ++pround;
@@ -365,7 +371,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       const int b = seg & 1;
       if (seg >= 2) mbar_wait(&tm_empty[b], ((seg >> 1) - 1) & 1);
       tc_fence_after();
-      const uint32_t acc = tmem + static_cast<uint32_t>(b * r.n_tile);
+      const uint32_t acc = tmem + static_cast<uint32_t>(b * r.st * r.n_tile);
       for (int kbi = kb0; kbi < kb1; ++kbi, ++i) {
         mbar_wait(&full_a[sa], ra & 1);
         STAMP(i == 0 && lane == 0, 4);
@@ -373,17 +379,18 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         STAMP(i == 0 && lane == 0, 5);
         tc_fence_after();
         if (elect_one()) {
-          const uint32_t a_addr = smem_u32(a_st + sa * kAStageBytes);
+          const uint32_t a_addr = smem_u32(a_st + sa * a_stage_bytes);
           const uint32_t b_addr = smem_u32(b_st + sb * b_stage_bytes);
           if (r.dbg_nomma) {  // debug: pure streaming rate (results are garbage)
             mbar_arrive(&empty_a[sa]);
             mbar_arrive(&empty_b[sb]);
             if (kbi == kb1 - 1) mbar_arrive(&tm_full[b]);
           } else {
+            for (int j = 0; j < r.st; ++j)  // st weight tiles share this activation stage
 #pragma unroll
-            for (int kk = 0; kk < kBK / 16; ++kk)  // along K inside the swizzle atom: 16 bf16 = 32 bytes
-              umma_bf16(acc, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
-                        (kbi != kb0 || kk != 0) ? 1u : 0u);
+              for (int kk = 0; kk < kBK / 16; ++kk)  // along K inside the swizzle atom: 16 bf16 = 32 bytes
+                umma_bf16(acc + static_cast<uint32_t>(j * r.n_tile), umma_desc_sw128(a_addr + j * kAStageBytes + kk * 32),
+                          umma_desc_sw128(b_addr + kk * 32), idesc, (kbi != kb0 || kk != 0) ? 1u : 0u);
             umma_commit(&empty_a[sa]);
             umma_commit(&empty_b[sb]);
             if (kbi == kb1 - 1) umma_commit(&tm_full[b]);
@@ -444,7 +451,8 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       const int n_part = partner ? 0 : pb - pa;
       const int b = seg & 1;
       const int tok0 = nt * r.n_tile;
-      const int nchunk = (r.n_tile + 31) / 32;
+      const int nct = (r.n_tile + 31) / 32;  // 32-token chunks of one 128-row tile
+      const int nchunk = r.st * nct;          // chunks of the unit (tile j = k / nct)
       if (n_part > 0 && lead0) {
         for (int p = pa; p <= pb; ++p) {
           if (p == fix) continue;
@@ -484,12 +492,14 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         STAMP(lead0, 7);
       }
       const int slot = c == pa ? 1 : 0;  // partner: where this piece is published
-      const uint32_t acc = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * r.n_tile);
+      const uint32_t acc = tmem + (static_cast<uint32_t>(q * 32) << 16) + static_cast<uint32_t>(b * r.st * r.n_tile);
       for (int k = eg; k < nchunk; k += kEpiGroups) {
-        const int cc = k * 32;
+        const int tj = k / nct;                  // weight tile of the unit
+        const int cc = (k - tj * nct) * 32;      // token offset inside the tile
+        const int mrow = m * r.st + tj;          // 128-row output tile
         const bool stamp = r.timing != nullptr && lead0 && seg_last && k < 4;
         float v[32];
-        tmem_ld_32x32b_x32(acc + cc, v);
+        tmem_ld_32x32b_x32(acc + tj * r.n_tile + cc, v);
         if (stamp) r.timing[c * 64 + 20 + k] = gtimer();
         if (k + kEpiGroups >= nchunk) {  // this group's accumulators consumed: hand TMEM back
           tc_fence_before();
@@ -535,12 +545,12 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           if (partner) {
             bulk_s2g(r.partials + (static_cast<int64_t>(2 * c + slot) * 8 + k) * (kChunkBytes / 4), st, kChunkBytes);
           } else if (residual) {
-            tma_reduce_add_2d(&tout, st, m * kBM, tok0 + cc);  // rows >= M are clipped by TMA
+            tma_reduce_add_2d(&tout, st, mrow * kBM, tok0 + cc);  // rows >= M are clipped by TMA
           } else if (silu) {
-            tma_store_2d(&tout, st, m * (kBM / 2), tok0 + cc);
+            tma_store_2d(&tout, st, mrow * (kBM / 2), tok0 + cc);
           } else {
-            tma_store_2d(&tout, st, m * kBM, tok0 + cc);
-            for (int pr = 0; pr < r.n_peers; ++pr) tma_store_2d(&peers.m[pr], st, m * kBM, tok0 + cc);
+            tma_store_2d(&tout, st, mrow * kBM, tok0 + cc);
+            for (int pr = 0; pr < r.n_peers; ++pr) tma_store_2d(&peers.m[pr], st, mrow * kBM, tok0 + cc);
           }
           bulk_commit();
           if (stamp) r.timing[c * 64 + 28 + k] = gtimer();
@@ -744,16 +754,23 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   static const int env_budget = getenv("MUX_GEMM_SMEM_KB") ? atoi(getenv("MUX_GEMM_SMEM_KB")) * 1024 : kSmemBudget;
   // two co-resident CTAs: (228 KB - 2 x 1 KB reserved) / 2 minus alignment slack
   const int budget = r.eg == 1 ? kDualSmemBudget : env_budget;
-  r.stages_a = (budget - r.stages_b * b_stage - r.eg * kChunkBytes) / kAStageBytes;
+  // Two 128-row weight tiles per unit (st = 2): each activation stage feeds
+  // two MMAs, halving the activation bytes re-read from L2 and staged per
+  // weight byte. Decode only (one token tile of <= 128), an even number of
+  // weight tiles, one CTA per SM (the dual ring is too small for 32 KiB stages).
+  static const int env_st = getenv("MUX_GEMM_ST") ? atoi(getenv("MUX_GEMM_ST")) : 1;
+  const int w_tiles = (a.N + kBM - 1) / kBM;
+  r.st = (env_st == 2 && r.eg == 2 && a.M <= 128 && w_tiles % 2 == 0) ? 2 : 1;
+  r.stages_a = (budget - r.stages_b * b_stage - r.eg * kChunkBytes) / (r.st * kAStageBytes);
   if (env_sa > 0) r.stages_a = std::min(env_sa, r.stages_a);
-  else if (r.stages_a > 10) r.stages_a = 10;
+  else if (r.stages_a > 10 / r.st) r.stages_a = 10 / r.st;
   r.kb = (a.K + kBK - 1) / kBK;
-  r.m_tiles = (a.N + kBM - 1) / kBM;
+  r.m_tiles = w_tiles / r.st;
   const int n_tiles_tok = (a.M + r.n_tile - 1) / r.n_tile;
   r.iters = static_cast<int64_t>(r.m_tiles) * n_tiles_tok * r.kb;
   r.epi = static_cast<int>(a.epi);
   r.n_tok_tiles = n_tiles_tok;
-  r.tmem_cols = pow2_cols(r.n_tile + (r.n_tile > 32 ? r.n_tile : 32));
+  r.tmem_cols = pow2_cols(r.st * r.n_tile + (r.st * r.n_tile > 32 ? r.st * r.n_tile : 32));
   int grid = a.grid > 0 ? a.grid : 148;
   // Enough k-blocks per CTA that the fixed per-CTA cost and the fixup
   // partials stay small next to the weight bytes it streams.
@@ -766,8 +783,8 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   // Non-residual epilogues sum pieces in a fixer: keep every tile in few
   // enough pieces that the partners' chunks fit the fixer's idle A ring.
   if (r.epi != static_cast<int>(Epilogue::kResidualAddF32)) {
-    const int nchunk = (r.n_tile + 31) / 32;
-    const int max_partners = (r.stages_a * kAStageBytes) / (nchunk * kChunkBytes);
+    const int nchunk = r.st * ((r.n_tile + 31) / 32);
+    const int max_partners = (r.stages_a * r.st * kAStageBytes) / (nchunk * kChunkBytes);
     // a range of R iterations lets a tile meet at most ceil(kb / R) + 1 ranges
     const int64_t need_r = (r.kb + max_partners - 1) / std::max(1, max_partners);
     if (static_cast<int64_t>(grid) * need_r > r.iters) grid = static_cast<int>(std::max<int64_t>(1, r.iters / need_r));
@@ -785,7 +802,7 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
     r.group_m = 0;
   }
   r.sk_iters = (tiles - static_cast<int64_t>(r.n_dp) * grid) * r.kb;
-  smem_out = 1024 + static_cast<size_t>(r.stages_a) * kAStageBytes + static_cast<size_t>(r.stages_b) * b_stage +
+  smem_out = 1024 + static_cast<size_t>(r.stages_a) * r.st * kAStageBytes + static_cast<size_t>(r.stages_b) * b_stage +
              r.eg * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16;
   grid_out = grid;
 }
