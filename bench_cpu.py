@@ -147,7 +147,7 @@ def _ref_sim():
 
 def _steps_total(args):
     # bench.run_ours draws its members with the same extra-steps margin
-    return args.warmup + args.steps + args.e2e_steps + args.attn_steps + 2
+    return 2 * args.warmup + args.steps + args.e2e_steps + args.attn_steps + 2
 
 
 def _sample_text(unit, n_steps, wall):

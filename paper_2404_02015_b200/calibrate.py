@@ -298,13 +298,23 @@ def main(argv=None) -> int:
     ap = argparse.ArgumentParser(description=__doc__.split("\n")[0])
     ap.add_argument("--model", default="7b")
     ap.add_argument("-o", "--output", default="b200_profile.json")
+    ap.add_argument("--tp-allreduce", default=None,
+                    help="JSON from scripts/tp_allreduce_cost.py: adds its allreduce_alpha_ms / "
+                         "allreduce_ms_per_mib (wire.TP_KEYS) as the profile_tp block")
     a = ap.parse_args(argv)
     m = measure(a.model)
     prof, err = fit_profile(m["prefill"], m["decode"], m["sm_share"], m["num_layers"], m["hidden"], hbm=True)
     from .wire import HBM_KEYS
     prof_hbm = {k: prof.pop(k) for k in HBM_KEYS if k in prof}
-    out = {"profile": prof, "profile_hbm": prof_hbm, "fit": err, "measurements": m,
-           "notes": {"tp_efficiency": "default 0.9: needs a multi-GPU mesh (one-GPU box)",
+    prof_tp = None
+    if a.tp_allreduce:
+        from .wire import TP_KEYS
+        with open(a.tp_allreduce) as f:
+            tpm = json.load(f)
+        prof_tp = {k: float(tpm[k]) for k in TP_KEYS}
+    out = {"profile": prof, "profile_hbm": prof_hbm, "profile_tp": prof_tp, "fit": err, "measurements": m,
+           "notes": {"tp_efficiency": "default 0.9: needs a multi-GPU mesh (one-GPU box); profile_tp, when "
+                                      "present, replaces eta * tp by the measured allreduce (LatencyProfile::tp_scaled)",
                      "method": "CUDA events around back-to-back jobs on one stream; decode KV random, "
                                "prefill single request of N tokens; SM share = green-context partition"}}
     with open(a.output, "w") as f:

@@ -761,6 +761,9 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   static const int env_st = getenv("MUX_GEMM_ST") ? atoi(getenv("MUX_GEMM_ST")) : 1;
   const int w_tiles = (a.N + kBM - 1) / kBM;
   r.st = (env_st == 2 && r.eg == 2 && a.M <= 128 && w_tiles % 2 == 0) ? 2 : 1;
+  // one activation stage now covers twice the weight bytes: two stages keep
+  // the same activation lead, and the freed 16 KiB buys a fifth weight stage
+  if (r.st == 2 && env_sb <= 0) r.stages_b = 2;
   r.stages_a = (budget - r.stages_b * b_stage - r.eg * kChunkBytes) / (r.st * kAStageBytes);
   if (env_sa > 0) r.stages_a = std::min(env_sa, r.stages_a);
   else if (r.stages_a > 10 / r.st) r.stages_a = 10 / r.st;

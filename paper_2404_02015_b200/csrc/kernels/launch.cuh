@@ -6,6 +6,7 @@
 
 #include <cuda_runtime.h>
 
+#include <cstdlib>
 #include <mutex>
 #include <utility>
 
@@ -17,11 +18,31 @@ bool& pdl_enabled();
 // Force-load kernels now (CUDA lazy loading would otherwise load a kernel at
 // its first launch, which can wait for the device to idle -- a deadlock when
 // an earlier kernel of the same process spins on a tensor-parallel peer).
+//
+// Every job kernel also asks for the maximum shared-memory carveout (option
+// MUX_CARVEOUT, default on): an SM runs CTAs of one L1/shared split at a
+// time, so a kernel with a smaller preferred carveout between two GEMMs
+// (228 KB) would make the SM drain and reconfigure at each boundary, and
+// under PDL the next kernel's CTAs could not join the previous one's.
+inline bool max_carveout_enabled() {
+  static const bool on = [] {
+    const char* e = std::getenv("MUX_CARVEOUT");
+    return e == nullptr || std::atoi(e) != 0;
+  }();
+  return on;
+}
+
 template <typename... K>
 inline cudaError_t preload(K... kernels) {
   cudaError_t err = cudaSuccess;
   cudaFuncAttributes attr;
   ((err = err == cudaSuccess ? cudaFuncGetAttributes(&attr, reinterpret_cast<const void*>(kernels)) : err), ...);
+  if (err == cudaSuccess && max_carveout_enabled())
+    ((err = err == cudaSuccess ? cudaFuncSetAttribute(reinterpret_cast<const void*>(kernels),
+                                                      cudaFuncAttributePreferredSharedMemoryCarveout,
+                                                      cudaSharedmemCarveoutMaxShared)
+                               : err),
+     ...);
   return err;
 }
 
