@@ -21,3 +21,4 @@ for st in 2 1; do
 done
 done
 tail -3 $out/tests_st2.log; cat $out/rounds.jsonl; for f in $out/micro*; do echo $f; cat $f | awk '{print $2, $5, $6, $7}'; done
+timeout 900 python scripts/tp_allreduce_cost.py $out/tp_allreduce.json > $out/tp_allreduce.log 2>&1; tail -8 $out/tp_allreduce.log

@@ -27,7 +27,7 @@ import paper_2404_02015_b200 as mux  # noqa: E402
 
 
 def make_units(spec, tp, max_batch, ctx):
-    total = 2_000_000
+    total = 12_000_000  # head-blocks (49 GB): batch 128 x 564 tokens at tp 1
     units = [mux.Unit([spec], pool_blocks=total // tp, device_pool_blocks=total // tp, max_batch=max_batch,
                       max_prefill_tokens=256, max_ctx=ctx + 64, max_slots=max_batch + 8, init_seed=1, init_std=0.02,
                       partitions=2, tp_rank=r, tp_size=tp) for r in range(tp)]
@@ -71,7 +71,8 @@ def main():
             for u in units:
                 u.pool.set_quota(0, u.pool.total_blocks())
                 for r in rids:
-                    assert u.pool.admit(0, r, ctx, ctx + 64).ok
+                    res = u.pool.admit(0, r, ctx, ctx + 64)
+                    assert res.ok, (tp, b, res)
             try:
                 t[tp] = step_ms(units, rids)
             finally:
