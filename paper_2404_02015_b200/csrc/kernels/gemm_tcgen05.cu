@@ -758,9 +758,22 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   // two MMAs, halving the activation bytes re-read from L2 and staged per
   // weight byte. Decode only (one token tile of <= 128), an even number of
   // weight tiles, one CTA per SM (the dual ring is too small for 32 KiB stages).
-  static const int env_st = getenv("MUX_GEMM_ST") ? atoi(getenv("MUX_GEMM_ST")) : 1;
+  // Pays when every CTA streams many units; with few units per CTA the
+  // doubled unit size lengthens the stream-K fixup (the fixer sums partners'
+  // 8-chunk partials) and the last epilogue. Measured on the 9 decode shapes
+  // of 7B/13B at M = 128 (profiles/r02_gemm_st.txt): LM head +12%, gate-up 13B
+  // +6%, down +3-7%; QKV -36-45%, O -5-15%, gate-up 7B -11%. Auto (default):
+  // on when a CTA's range holds >= 16 two-tile units (residual epilogue: no
+  // fixup) or >= 48 (fixup epilogues). MUX_GEMM_ST=1 off, =2 forced.
+  static const int env_st = getenv("MUX_GEMM_ST") ? atoi(getenv("MUX_GEMM_ST")) : 0;
   const int w_tiles = (a.N + kBM - 1) / kBM;
-  r.st = (env_st == 2 && r.eg == 2 && a.M <= 128 && w_tiles % 2 == 0) ? 2 : 1;
+  const bool st_ok = r.eg == 2 && a.M <= 128 && w_tiles % 2 == 0;
+  bool st2 = env_st == 2;
+  if (env_st == 0 && st_ok) {
+    const int64_t per_cta = static_cast<int64_t>(w_tiles / 2) * ((a.K + kBK - 1) / kBK) / std::max(1, a.grid > 0 ? a.grid : 148);
+    st2 = per_cta >= (a.epi == Epilogue::kResidualAddF32 ? 16 : 48);
+  }
+  r.st = (st2 && st_ok) ? 2 : 1;
   // one activation stage now covers twice the weight bytes: two stages keep
   // the same activation lead, and the freed 16 KiB buys a fifth weight stage
   if (r.st == 2 && env_sb <= 0) r.stages_b = 2;

@@ -19,15 +19,14 @@ bool& pdl_enabled();
 // its first launch, which can wait for the device to idle -- a deadlock when
 // an earlier kernel of the same process spins on a tensor-parallel peer).
 //
-// Every job kernel also asks for the maximum shared-memory carveout (option
-// MUX_CARVEOUT, default on): an SM runs CTAs of one L1/shared split at a
-// time, so a kernel with a smaller preferred carveout between two GEMMs
-// (228 KB) would make the SM drain and reconfigure at each boundary, and
-// under PDL the next kernel's CTAs could not join the previous one's.
+// Debug (MUX_CARVEOUT=1): every job kernel prefers the maximum shared-memory
+// carveout, so no L1/shared reconfiguration can sit between a GEMM and its
+// neighbours. Measured: no change in decode rounds (profiles/r02_gemm_st.txt),
+// so it is off by default.
 inline bool max_carveout_enabled() {
   static const bool on = [] {
     const char* e = std::getenv("MUX_CARVEOUT");
-    return e == nullptr || std::atoi(e) != 0;
+    return e != nullptr && std::atoi(e) != 0;
   }();
   return on;
 }
