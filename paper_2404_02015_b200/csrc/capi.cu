@@ -1157,7 +1157,7 @@ int mux_gemm_bf16(const void* x, const void* w, int w_tiled, int M, int N, int K
     int& epoch = sc.epoch;
     int sms = 148;
     mux::check_cuda(cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev), "gemm SM count");
-    alignas(64) unsigned char tw[128], tx[128], to[128], tx128[128];
+    alignas(64) unsigned char tw[128], tx[128], to[128], tx128[128], txh[128], twr[128];
     const int n_tile = mux::gemm_pick_n_tile(M);
     if ((!w_tiled && !mux::make_tmap_bf16(tw, w, N, K, static_cast<uint64_t>(K) * 2, 128)) ||
         !mux::make_tmap_bf16(tx, x, M, K, static_cast<uint64_t>(K) * 2, n_tile))
@@ -1171,6 +1171,13 @@ int mux_gemm_bf16(const void* x, const void* w, int w_tiled, int M, int N, int K
     g.tmap_x = tx;
     // prefill shapes with tiled weights may run on CTA pairs (gemm_2sm.cu)
     if (w_tiled && M > 256 && mux::make_tmap_bf16(tx128, x, M, K, static_cast<uint64_t>(K) * 2, 128)) g.tmap_x128 = tx128;
+    // decode shapes with tiled weights may run on CTA pairs (MUX_GEMM_PAIR)
+    if (w_tiled && M <= 256 && n_tile > 64 &&
+        mux::make_tmap_bf16(txh, x, M, K, static_cast<uint64_t>(K) * 2, n_tile / 2) &&
+        mux::make_tmap_w_rows(twr, w, N, K)) {
+      g.tmap_x_half = txh;
+      g.tmap_w_rows = twr;
+    }
     g.out = out;
     g.partials = partials;
     g.flags = flags;

@@ -369,6 +369,10 @@ void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void
   g.w_tiled = w_tiled;
   g.tmap_x = act_tmap(x, rows, K, gemm_n_tile(M));
   if (M > 256) g.tmap_x128 = act_tmap(x, rows, K, 128);  // 2-SM prefill path (gemm_2sm.cu)
+  if (M <= 256 && gemm_n_tile(M) > 64 && w_tiled != nullptr) {  // decode CTA-pair mode (MUX_GEMM_PAIR)
+    g.tmap_x_half = act_tmap(x, rows, K, gemm_n_tile(M) / 2);
+    g.tmap_w_rows = w_rows_tmap(w_tiled, N, K);
+  }
   g.tmap_out = out_tmap(out, epi, M, N, ldo);
   g.out = out;
   g.partials = ws.gemm_partials.as<float>();
@@ -395,6 +399,18 @@ void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void
     gemm_timer_->pending_bytes += static_cast<double>(N) * K * 2;  // decode: the weights, streamed once
   }
   launches_ += 1;
+}
+
+const void* Runtime::w_rows_tmap(const void* w_tiled, int N, int K) {
+  auto key = std::make_tuple(w_tiled, N, K, -1);
+  auto it = tmaps_.find(key);
+  if (it != tmaps_.end()) return it->second.data();
+  std::vector<unsigned char> raw(128 + 64);
+  unsigned char* aligned = reinterpret_cast<unsigned char*>(
+      (reinterpret_cast<uintptr_t>(raw.data()) + 63) & ~uintptr_t(63));
+  if (!make_tmap_w_rows(aligned, w_tiled, N, K)) throw std::runtime_error("weight-row tensor map encode failed");
+  auto ins = tmaps_.emplace(key, std::vector<unsigned char>(aligned, aligned + 128));
+  return ins.first->second.data();
 }
 
 const void* Runtime::out_tmap(const void* out, int epi, int M, int N, int ldo) {

@@ -188,6 +188,7 @@ class Runtime {
 
   // Cached tensor map for an activation buffer viewed as rows x cols bf16.
   const void* act_tmap(const void* base, int rows, int cols, int box_rows);
+  const void* w_rows_tmap(const void* w_tiled, int N, int K);  // make_tmap_w_rows, cached
   // Cached store map of a GEMM output (exact M rows: TMA clips the tail).
   const void* out_tmap(const void* out, int epi, int M, int N, int ldo);
 

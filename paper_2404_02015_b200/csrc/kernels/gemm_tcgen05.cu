@@ -92,6 +92,7 @@ struct GemmRun {
   unsigned long long* timing;  // debug: [grid][64] globaltimer stamps, or null
   int dbg_nomma;    // debug (MUX_GEMM_NOMMA=1): stream operands without MMAs
   int eg;           // epilogue groups of the instantiation (template EG)
+  int pair;         // CTA-pair mode (template PAIR): 256-row units, cta_group::2 MMAs
   // Tensor-parallel fan-out (kStoreF32 only): every finished tile is also
   // stored through peers.m[0..n_peers) (the same slot on the other ranks of
   // the mesh, NVLink peer memory), and once all of a CTA's stores have landed
@@ -226,7 +227,15 @@ __device__ __forceinline__ void epi_bar_all() {
 #define STAMP(cond, slot) \
   do { if (r.timing != nullptr && (cond)) r.timing[c * 64 + (slot)] = gtimer(); } while (0)
 
-template <int EG>
+// PAIR: the CTAs of a cluster pair (one TPC) share each 256-row weight unit:
+// each stages its own 128 weight rows and HALF of the token tile, and the
+// leader's single tcgen05.mma.cta_group::2 (M = 256) reads the token operand
+// from both CTAs' shared memory. Per SM that stages and reads half the
+// activation bytes of the single-CTA form: 48 instead of 64 KiB of shared-
+// memory traffic per 16 KiB of weights (the MMAs' operand reads stall the
+// weight stream near the 128 B/clk port limit at 128 tokens). Stream-K runs
+// over pairs; each rank fixes up / publishes its own 128-row half.
+template <int EG, bool PAIR>
 __global__ void __launch_bounds__(threads_of<EG>(), 3 - EG)
 gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ CUtensorMap tx,
                const __grid_constant__ CUtensorMap tout, const GemmRun r, const __grid_constant__ PeerMaps peers) {
@@ -238,7 +247,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   // L2-resident activation tiles (B) only SB, so more weight bytes are in
   // flight per SM than a shared ring of the same smem would allow.
   const int SA = r.stages_a, SB = r.stages_b;
-  const int b_stage_bytes = r.n_tile * kBK * 2;
+  const int b_stage_bytes = (PAIR ? r.n_tile / 2 : r.n_tile) * kBK * 2;  // pair: this CTA's token half
   uint8_t* a_st = base;
   const int a_stage_bytes = r.st * kAStageBytes;  // st weight tiles of one k-block
   uint8_t* b_st = base + SA * a_stage_bytes;
@@ -255,8 +264,13 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
 
   const int warp = threadIdx.x >> 5;
   const int lane = threadIdx.x & 31;
-  const int c = blockIdx.x;
-  const int G = gridDim.x;
+  // stream-K participant: the CTA, or the CTA pair in PAIR mode
+  const int rank = PAIR ? static_cast<int>(cluster_rank()) : 0;
+  const int c = PAIR ? static_cast<int>(blockIdx.x >> 1) : static_cast<int>(blockIdx.x);
+  const int G = PAIR ? static_cast<int>(gridDim.x >> 1) : static_cast<int>(gridDim.x);
+  // flags / partials slot of participant p's CTA of this rank
+  auto pid = [&](int p) { return PAIR ? 2 * p + rank : p; };
+  const int me = pid(c);
   STAMP(threadIdx.x == 0, 0);
 
   // Weight producer state (warp 0, lane 0). Weights do not depend on earlier
@@ -279,6 +293,19 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   };
   auto a_issue = [&]() {
     if (pround > 0) mbar_wait(&empty_a[ps], (pround - 1) & 1);
+    if constexpr (PAIR) {
+      // both CTAs' 16 KiB count on the leader's barrier; the tiled weights
+      // are a [tiles * 128][64] tensor (rows already in the SW128 image)
+      if (rank == 0) mbar_arrive_expect_tx(&full_a[ps], 2u * kAStageBytes);
+      const int mt = 2 * pm + rank;
+      tma_load_2d_pair(a_st + ps * kAStageBytes, &tw, map_to_rank(smem_u32(&full_a[ps]), 0), 0,
+                       (mt * r.kb + pkb) * kBM, wpol);
+      if (++ps == SA) {
+        ps = 0;
+        ++pround;
+      }
+      return;
+    }
     mbar_arrive_expect_tx(&full_a[ps], static_cast<uint32_t>(a_stage_bytes));
     for (int j = 0; j < r.st; ++j) {
       const int mt = pm * r.st + j;  // 128-row weight tile
@@ -307,13 +334,17 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       }
       for (int b = 0; b < 2; ++b) {
         mbar_init(&tm_full[b], 1);
-        mbar_init(&tm_empty[b], kEpiGroups * kEpiThreads / 32);
+        // the leader's counts both CTAs' epilogue warps in PAIR mode
+        mbar_init(&tm_empty[b], (PAIR ? 2 : 1) * kEpiGroups * kEpiThreads / 32);
       }
       mbar_init(pbar, 1);
       fence_barrier_init();
       wpol = policy_evict_first();  // weights: streamed once per step
       STAMP(true, 32);
-      for (int k = 0; k < kPreIssue && a_next(); ++k) a_issue();
+      // (PAIR: the peer's copies complete on the leader's barriers, so none
+      // is issued before the cluster barrier below)
+      if constexpr (!PAIR)
+        for (int k = 0; k < kPreIssue && a_next(); ++k) a_issue();
       STAMP(true, 19);
       if (r.w_tiled == nullptr) prefetch_tmap(&tw);
       prefetch_tmap(&tx);
@@ -321,9 +352,19 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     }
     __syncwarp();
   }
-  if (warp == 2) tmem_alloc_dyn(tmem_slot, r.tmem_cols);
+  if (warp == 2) {
+    if constexpr (PAIR) {
+      asm volatile("tcgen05.alloc.cta_group::2.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                   "r"(r.tmem_cols)
+                   : "memory");
+      asm volatile("tcgen05.relinquish_alloc_permit.cta_group::2.sync.aligned;" ::: "memory");
+    } else {
+      tmem_alloc_dyn(tmem_slot, r.tmem_cols);
+    }
+  }
   tc_fence_before();
-  __syncthreads();
+  if constexpr (PAIR) cluster_sync_all();  // both CTAs' barriers initialised, TMEM allocated
+  else __syncthreads();
   tc_fence_after();
   const uint32_t tmem = *tmem_slot;
   STAMP(threadIdx.x == 0, 15);
@@ -340,6 +381,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       grid_dep_wait();  // activations come from the predecessor
       const uint64_t pol = policy_evict_last();  // re-read by every CTA
       const uint32_t bytes = static_cast<uint32_t>(b_stage_bytes);
+      const uint32_t full_b_leader = PAIR ? map_to_rank(smem_u32(full_b), 0) : 0u;
       SegGen sg(r, c, G);
       int m, nt, kb0, kb1;
       bool skp;
@@ -348,8 +390,14 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       while (sg.next(r, c, G, m, nt, kb0, kb1, skp, lo)) {
         for (int kbi = kb0; kbi < kb1; ++kbi) {
           if (round > 0) mbar_wait(&empty_b[s], (round - 1) & 1);
-          mbar_arrive_expect_tx(&full_b[s], bytes);
-          tma_load_2d(b_st + s * b_stage_bytes, &tx, &full_b[s], kbi * kBK, nt * r.n_tile, pol);
+          if constexpr (PAIR) {
+            if (rank == 0) mbar_arrive_expect_tx(&full_b[s], 2 * bytes);
+            tma_load_2d_pair(b_st + s * b_stage_bytes, &tx, full_b_leader + s * 8, kbi * kBK,
+                             nt * r.n_tile + rank * (r.n_tile / 2), pol);
+          } else {
+            mbar_arrive_expect_tx(&full_b[s], bytes);
+            tma_load_2d(b_st + s * b_stage_bytes, &tx, &full_b[s], kbi * kBK, nt * r.n_tile, pol);
+          }
           if (++s == SB) {
             s = 0;
             ++round;
@@ -358,9 +406,10 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       }
     }
     __syncwarp();
-  } else if (warp == 1) {
+  } else if (warp == 1 && (!PAIR || rank == 0)) {
     // ------------------------------------------------------ MMA issuer
-    const uint32_t idesc = umma_idesc_bf16(kBM, r.n_tile);
+    // (PAIR: the leader issues one M = 256 MMA for both CTAs)
+    const uint32_t idesc = umma_idesc_bf16(PAIR ? 2 * kBM : kBM, r.n_tile);
     int i = 0, seg = 0;
     int sa = 0, ra = 0, sb = 0, rb = 0;  // ring slots and their round parities
     SegGen sg(r, c, G);
@@ -381,7 +430,15 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         if (elect_one()) {
           const uint32_t a_addr = smem_u32(a_st + sa * a_stage_bytes);
           const uint32_t b_addr = smem_u32(b_st + sb * b_stage_bytes);
-          if (r.dbg_nomma) {  // debug: pure streaming rate (results are garbage)
+          if constexpr (PAIR) {
+#pragma unroll
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              umma2_bf16(acc, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
+                         (kbi != kb0 || kk != 0) ? 1u : 0u);
+            umma2_commit_both(&empty_a[sa]);
+            umma2_commit_both(&empty_b[sb]);
+            if (kbi == kb1 - 1) umma2_commit_both(&tm_full[b]);
+          } else if (r.dbg_nomma) {  // debug: pure streaming rate (results are garbage)
             mbar_arrive(&empty_a[sa]);
             mbar_arrive(&empty_b[sb]);
             if (kbi == kb1 - 1) mbar_arrive(&tm_full[b]);
@@ -456,7 +513,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       if (n_part > 0 && lead0) {
         for (int p = pa; p <= pb; ++p) {
           if (p == fix) continue;
-          int* f = r.flags + 2 * p + (p == pa ? 1 : 0);
+          int* f = r.flags + 2 * pid(p) + (p == pa ? 1 : 0);
           while (ld_acquire(f) != r.epoch) __nanosleep(32);
           // every published flag has exactly one reader: clear it, so a
           // replay of the same launch (CUDA graph, same epoch) waits again
@@ -470,7 +527,10 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       if (eg >= nchunk) {  // no chunk for this group (n_tile <= 32): hand TMEM back now
         tc_fence_before();
         __syncwarp();
-        if (lane == 0) mbar_arrive(&tm_empty[b]);
+        if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_cluster(map_to_rank(smem_u32(&tm_empty[b]), 0));
+          else mbar_arrive(&tm_empty[b]);
+        }
       }
       if (n_part > 0) {
         // All MMAs of this CTA are complete (this is its last segment), so
@@ -481,7 +541,8 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           int pi = 0;
           for (int p = pa; p <= pb; ++p) {
             if (p == fix) continue;
-            const float* src = r.partials + (static_cast<int64_t>(2 * p + (p == pa ? 1 : 0)) * 8) * (kChunkBytes / 4);
+            const float* src =
+                r.partials + (static_cast<int64_t>(2 * pid(p) + (p == pa ? 1 : 0)) * 8) * (kChunkBytes / 4);
             for (int k = 0; k < nchunk; ++k)
               bulk_g2s(a_st + (pi * nchunk + k) * kChunkBytes, src + k * (kChunkBytes / 4), kChunkBytes, pbar);
             ++pi;
@@ -496,7 +557,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       for (int k = eg; k < nchunk; k += kEpiGroups) {
         const int tj = k / nct;                  // weight tile of the unit
         const int cc = (k - tj * nct) * 32;      // token offset inside the tile
-        const int mrow = m * r.st + tj;          // 128-row output tile
+        const int mrow = PAIR ? 2 * m + rank : m * r.st + tj;  // 128-row output tile
         const bool stamp = r.timing != nullptr && lead0 && seg_last && k < 4;
         float v[32];
         tmem_ld_32x32b_x32(acc + tj * r.n_tile + cc, v);
@@ -504,7 +565,10 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         if (k + kEpiGroups >= nchunk) {  // this group's accumulators consumed: hand TMEM back
           tc_fence_before();
           __syncwarp();
-          if (lane == 0) mbar_arrive(&tm_empty[b]);
+          if (lane == 0) {
+          if constexpr (PAIR) mbar_arrive_cluster(map_to_rank(smem_u32(&tm_empty[b]), 0));
+          else mbar_arrive(&tm_empty[b]);
+        }
         }
         for (int pi = 0; pi < n_part; ++pi) {  // partner order = CTA order: deterministic
           const float* src = pstage + (pi * nchunk + k) * (kChunkBytes / 4) + fl;
@@ -543,7 +607,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         epi_bar(eg);
         if (leader) {
           if (partner) {
-            bulk_s2g(r.partials + (static_cast<int64_t>(2 * c + slot) * 8 + k) * (kChunkBytes / 4), st, kChunkBytes);
+            bulk_s2g(r.partials + (static_cast<int64_t>(2 * me + slot) * 8 + k) * (kChunkBytes / 4), st, kChunkBytes);
           } else if (residual) {
             tma_reduce_add_2d(&tout, st, mrow * kBM, tok0 + cc);  // rows >= M are clipped by TMA
           } else if (silu) {
@@ -561,7 +625,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
         epi_bar_all<EG>();
         if (lead0) {
           asm volatile("fence.acq_rel.gpu;" ::: "memory");
-          st_release(r.flags + 2 * c + slot, r.epoch);
+          st_release(r.flags + 2 * me + slot, r.epoch);
           STAMP(true, 8);
         }
       }
@@ -593,10 +657,16 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
   __syncwarp();
   tc_fence_before();
   __syncthreads();
+  // PAIR: the peer's epilogue arrivals on this CTA's barriers and the
+  // leader's MMAs into this CTA's TMEM are done before either deallocates
+  if constexpr (PAIR) cluster_sync_all();
   STAMP(threadIdx.x == 0, 3);
   if (warp == 2) {
     tc_fence_after();
-    tmem_dealloc(tmem, r.tmem_cols);
+    if constexpr (PAIR)
+      asm volatile("tcgen05.dealloc.cta_group::2.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(r.tmem_cols) : "memory");
+    else
+      tmem_dealloc(tmem, r.tmem_cols);
   }
 }
 
@@ -677,6 +747,11 @@ bool make_tmap_2d(void* tmap_out, const void* base, bool fp32, uint64_t rows, ui
   return res == CUDA_SUCCESS;
 }
 
+bool make_tmap_w_rows(void* tmap_out, const void* w_tiled, int N, int K) {
+  const uint64_t rows = static_cast<uint64_t>((N + kBM - 1) / kBM) * ((K + kBK - 1) / kBK) * kBM;
+  return make_tmap_2d(tmap_out, w_tiled, false, rows, kBK, kBK * 2, kBM, kBK);
+}
+
 bool make_tmap_gemm_out(void* tmap_out, const void* out, int epi, int M, int N, int ldo) {
   const bool fp32 = epi == static_cast<int>(Epilogue::kResidualAddF32) || epi == static_cast<int>(Epilogue::kStoreF32);
   const bool silu = epi == static_cast<int>(Epilogue::kSiluMulBf16);
@@ -715,13 +790,15 @@ cudaError_t weight_tile(const void* src, int N, int K, void* dst, bool inverse, 
 // Attributes are set here too (per device, at unit creation), so no launch
 // inside a CUDA-graph capture is the first one on its device.
 static cudaError_t configure_gemm() {
-  cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<2>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  cudaError_t e = cudaFuncSetAttribute(gemm_tn_kernel<2, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
+  if (e == cudaSuccess)
+    e = cudaFuncSetAttribute(gemm_tn_kernel<2, true>, cudaFuncAttributeMaxDynamicSharedMemorySize, 232448);
   if (e != cudaSuccess) return e;
-  return cudaFuncSetAttribute(gemm_tn_kernel<1>, cudaFuncAttributeMaxDynamicSharedMemorySize, 116 * 1024);
+  return cudaFuncSetAttribute(gemm_tn_kernel<1, false>, cudaFuncAttributeMaxDynamicSharedMemorySize, 116 * 1024);
 }
 
 cudaError_t preload_gemm() {
-  cudaError_t e = preload(gemm_tn_kernel<1>, gemm_tn_kernel<2>, weight_tile_kernel);
+  cudaError_t e = preload(gemm_tn_kernel<1, false>, gemm_tn_kernel<2, false>, gemm_tn_kernel<2, true>, weight_tile_kernel);
   return e != cudaSuccess ? e : configure_gemm();
 }
 
@@ -741,10 +818,19 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   r.K = a.K;
   r.ldo = a.ldo;
   r.n_tile = gemm_pick_n_tile(a.M);
-  const int b_stage = r.n_tile * kBK * 2;
+  // CTA pairs (PAIR instantiation, MUX_GEMM_PAIR=1): decode token tiles of
+  // 65..256 (one CTA per SM), an even number of 128-row weight tiles, the
+  // half-box activation map and the row view of the tiled weights given.
+  static const int env_pair = getenv("MUX_GEMM_PAIR") ? atoi(getenv("MUX_GEMM_PAIR")) : 0;
+  const int w_tiles0 = (a.N + kBM - 1) / kBM;
+  r.pair = env_pair != 0 && r.n_tile > 64 && a.M <= 256 && w_tiles0 % 2 == 0 && a.tmap_x_half != nullptr &&
+                   a.tmap_w_rows != nullptr && a.n_peers == 0 && a.n_signal == 0 && (a.grid <= 0 || a.grid >= 2)
+               ? 1
+               : 0;
+  const int b_stage = (r.pair ? r.n_tile / 2 : r.n_tile) * kBK * 2;
   static const int env_dual = getenv("MUX_GEMM_DUAL") ? atoi(getenv("MUX_GEMM_DUAL")) : 1;
   r.eg = (env_dual && r.n_tile <= 64) ? 1 : 2;
-  r.stages_b = r.n_tile > 128 ? 2 : 3;
+  r.stages_b = r.pair ? 4 : (r.n_tile > 128 ? 2 : 3);
   // Debug overrides for pipeline-depth sweeps (scripts/gemm_micro.py).
   static const int env_sb = getenv("MUX_GEMM_SB") ? atoi(getenv("MUX_GEMM_SB")) : 0;
   static const int env_sa = getenv("MUX_GEMM_SA") ? atoi(getenv("MUX_GEMM_SA")) : 0;
@@ -767,7 +853,7 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   // fixup) or >= 48 (fixup epilogues). MUX_GEMM_ST=1 off, =2 forced.
   static const int env_st = getenv("MUX_GEMM_ST") ? atoi(getenv("MUX_GEMM_ST")) : 0;
   const int w_tiles = (a.N + kBM - 1) / kBM;
-  const bool st_ok = r.eg == 2 && a.M <= 128 && w_tiles % 2 == 0;
+  const bool st_ok = !r.pair && r.eg == 2 && a.M <= 128 && w_tiles % 2 == 0;
   bool st2 = env_st == 2;
   if (env_st == 0 && st_ok) {
     const int64_t per_cta = static_cast<int64_t>(w_tiles / 2) * ((a.K + kBK - 1) / kBK) / std::max(1, a.grid > 0 ? a.grid : 148);
@@ -781,13 +867,15 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   if (env_sa > 0) r.stages_a = std::min(env_sa, r.stages_a);
   else if (r.stages_a > 10 / r.st) r.stages_a = 10 / r.st;
   r.kb = (a.K + kBK - 1) / kBK;
-  r.m_tiles = w_tiles / r.st;
+  r.m_tiles = w_tiles / (r.pair ? 2 : r.st);  // units along N
   const int n_tiles_tok = (a.M + r.n_tile - 1) / r.n_tile;
   r.iters = static_cast<int64_t>(r.m_tiles) * n_tiles_tok * r.kb;
   r.epi = static_cast<int>(a.epi);
   r.n_tok_tiles = n_tiles_tok;
   r.tmem_cols = pow2_cols(r.st * r.n_tile + (r.st * r.n_tile > 32 ? r.st * r.n_tile : 32));
+  // grid = stream-K participants: CTAs, or CTA pairs (launched as 2 x grid)
   int grid = a.grid > 0 ? a.grid : 148;
+  if (r.pair) grid /= 2;
   // Enough k-blocks per CTA that the fixed per-CTA cost and the fixup
   // partials stay small next to the weight bytes it streams.
   int64_t min_iters = a.min_iters > 0 ? a.min_iters : 1;
@@ -820,7 +908,7 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   r.sk_iters = (tiles - static_cast<int64_t>(r.n_dp) * grid) * r.kb;
   smem_out = 1024 + static_cast<size_t>(r.stages_a) * r.st * kAStageBytes + static_cast<size_t>(r.stages_b) * b_stage +
              r.eg * kChunkBytes + (2 * (r.stages_a + r.stages_b) + 6) * 8 + 16;
-  grid_out = grid;
+  grid_out = r.pair ? 2 * grid : grid;
 }
 
 cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
@@ -848,8 +936,28 @@ cudaError_t gemm_bf16_tn(const GemmArgs& a, cudaStream_t stream) {
   std::memcpy(&tx, a.tmap_x, sizeof(CUtensorMap));
   std::memcpy(&to, a.tmap_out, sizeof(CUtensorMap));
   if (a.grid_out != nullptr) *a.grid_out = grid;
-  if (r.eg == 1) return launch(gemm_tn_kernel<1>, dim3(grid), dim3(threads_of<1>()), smem, stream, tw, tx, to, r, pm);
-  return launch(gemm_tn_kernel<2>, dim3(grid), dim3(threads_of<2>()), smem, stream, tw, tx, to, r, pm);
+  if (r.pair) {
+    // clusters of two CTAs (one TPC) + programmatic dependent launch
+    std::memcpy(&tw, a.tmap_w_rows, sizeof(CUtensorMap));
+    std::memcpy(&tx, a.tmap_x_half, sizeof(CUtensorMap));
+    cudaLaunchAttribute attr[2];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = 2;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    attr[1].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    attr[1].val.programmaticStreamSerializationAllowed = 1;
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = dim3(grid);
+    cfg.blockDim = dim3(threads_of<2>());
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = pdl_enabled() ? 2 : 1;
+    return cudaLaunchKernelEx(&cfg, gemm_tn_kernel<2, true>, tw, tx, to, r, pm);
+  }
+  if (r.eg == 1) return launch(gemm_tn_kernel<1, false>, dim3(grid), dim3(threads_of<1>()), smem, stream, tw, tx, to, r, pm);
+  return launch(gemm_tn_kernel<2, false>, dim3(grid), dim3(threads_of<2>()), smem, stream, tw, tx, to, r, pm);
 }
 
 }  // namespace mux

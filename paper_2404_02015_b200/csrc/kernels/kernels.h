@@ -74,6 +74,11 @@ struct GemmArgs {
   const void* tmap_w;       // else: CUtensorMap* over row-major W (host memory)
   const void* tmap_x;       // box rows must equal gemm_pick_n_tile(M)
   const void* tmap_x128 = nullptr;  // same tensor, box 128 rows: enables the 2-SM prefill path (M > 256)
+  // Decode CTA-pair mode (MUX_GEMM_PAIR): the activations with box rows =
+  // gemm_pick_n_tile(M) / 2, and the tiled weights as a [tiles * 128][64]
+  // bf16 tensor (make_tmap_w_rows).
+  const void* tmap_x_half = nullptr;
+  const void* tmap_w_rows = nullptr;
   const void* tmap_out;     // make_tmap_gemm_out(): box 32 tokens x 128 (SiLU: 64) features
   void* out;
   float* partials;          // stream-K fixup scratch: gemm_partials_floats(grid) floats
@@ -101,6 +106,9 @@ bool gemm_2sm_eligible(const GemmArgs& a);
 cudaError_t gemm_2sm(const GemmArgs& a, cudaStream_t stream);
 cudaError_t preload_gemm_2sm();
 int gemm_pick_n_tile(int M);
+// The tiled weights (weight_tile layout) as a [ceil(N/128) * ceil(K/64) * 128][64]
+// bf16 tensor, box 128 x 64, no swizzle (the bytes already hold the SW128 image).
+bool make_tmap_w_rows(void* tmap_out, const void* w_tiled, int N, int K);
 bool make_tmap_gemm_out(void* tmap_out, const void* out, int epi, int M, int N, int ldo);
 // B200 weight layout: [ceil(N/128)][ceil(K/64)] contiguous 16 KiB UMMA tiles,
 // pre-swizzled (SWIZZLE_128B), zero-padded. inverse=true converts back.
