@@ -179,7 +179,8 @@ def test_gemm_tcgen05(cuda, M, N, K):
 @pytest.mark.parametrize("M,N,K", [(1, 256, 512), (64, 384, 200), (128, 1000, 576), (300, 640, 1024)])
 def test_gemm_tiled_weights(cuda, M, N, K):
     """Weights in the B200 tile layout (bulk-copied 16 KiB UMMA tiles) give the
-    same result as the TMA path; the tile transform round-trips exactly."""
+    same result as the TMA path (up to fp32 summation order); the tile
+    transform round-trips exactly."""
     import torch
     g = torch.Generator(device="cuda").manual_seed(M + N + K)
     x = torch.randn(M, K, generator=g, device="cuda").to(torch.bfloat16)
@@ -193,7 +194,9 @@ def test_gemm_tiled_weights(cuda, M, N, K):
     mux.gemm_bf16(x, w, b, epilogue=3, w_tiled=wt)
     torch.cuda.synchronize()
     assert torch.equal(back, w)
-    assert torch.equal(a, b)
+    # same products; the tiled path may split K differently across CTAs (CTA
+    # pairs for decode shapes), so only the fp32 summation order may differ
+    assert (a - b).abs().max().item() <= 1e-5 * a.abs().max().item() + 1e-6
 
 
 @pytest.mark.parametrize("M,N,K", [(300, 512, 576), (1000, 1024, 1024), (4096, 512, 256), (257, 768, 320)])
