@@ -818,10 +818,10 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   r.K = a.K;
   r.ldo = a.ldo;
   r.n_tile = gemm_pick_n_tile(a.M);
-  // CTA pairs (PAIR instantiation, MUX_GEMM_PAIR=1): decode token tiles of
+  // CTA pairs (PAIR instantiation; default, MUX_GEMM_PAIR=0 off): decode token tiles of
   // 65..256 (one CTA per SM), an even number of 128-row weight tiles, the
   // half-box activation map and the row view of the tiled weights given.
-  static const int env_pair = getenv("MUX_GEMM_PAIR") ? atoi(getenv("MUX_GEMM_PAIR")) : 0;
+  static const int env_pair = getenv("MUX_GEMM_PAIR") ? atoi(getenv("MUX_GEMM_PAIR")) : 1;
   const int w_tiles0 = (a.N + kBM - 1) / kBM;
   r.pair = env_pair != 0 && r.n_tile > 64 && a.M <= 256 && w_tiles0 % 2 == 0 && a.tmap_x_half != nullptr &&
                    a.tmap_w_rows != nullptr && a.n_peers == 0 && a.n_signal == 0 && (a.grid <= 0 || a.grid >= 2)
