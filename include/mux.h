@@ -382,6 +382,8 @@ MUX_API int64_t mux_unit_launches(mux_unit* unit);
 /* Tuning knobs: "gemm_min_iters" (k-blocks per GEMM CTA floor, default 8);
  * "pdl" (programmatic dependent launch between job kernels, default 1);
  * "graphs" (decode jobs replayed from cached CUDA graphs, default 1);
+ * "debug_skip" (measurement: decode jobs skip kernel classes, bitmask 1 K2,
+ * 2 RMSNorm, 4 K1; outputs are garbage; bench.py times the GEMM stream so);
  * "prefill_on_partition" (prefill jobs on their model's partition);
  * "pass_green" (partitions = [whole GPU | a whole-GPU stream per model |
  * a green partition per model]; decode jobs use the green partitions only in

@@ -323,6 +323,7 @@ Runtime::Runtime(int device, int64_t pool_blocks, int max_pos)
   check_cuda(preload_fused_ops(), "preload");
   check_cuda(preload(gather_last_tok, scatter_last_tok), "preload");
   if (const char* g = getenv("MUX_GRAPHS")) use_graphs_ = atoi(g) != 0;  // A/B switch (option "graphs")
+  if (const char* k = getenv("MUX_DEBUG_SKIP")) dbg_skip_ = atoi(k);   // option "debug_skip"
   pool_ = DevMem(static_cast<size_t>(pool_blocks) * 4096);
   // RoPE table [max_pos][64][(cos, sin)], computed in double, stored fp32.
   std::vector<float> tab(static_cast<size_t>(max_pos) * 128);
@@ -627,7 +628,7 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   // Debug (MUX_DEBUG_SKIP bitmask; outputs are garbage, timings are not): the
   // marginal in-step cost of a kernel class. 1 = K2, 2 = RMSNorm, 4 = K1,
   // 8 = RMSNorm over one row only (the launch boundary without the work).
-  static const int dbg_skip = getenv("MUX_DEBUG_SKIP") ? atoi(getenv("MUX_DEBUG_SKIP")) : 0;
+  const int dbg_skip = dbg_skip_;
   for (int l = 0; l < L; ++l) {
     ap.layer = l;
     gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
@@ -682,7 +683,7 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   };
   // Graphs: single-rank decode without per-launch timing (the TP path's
   // mailbox counters advance per call; timers record events per launch).
-  if (use_graphs_ && timer == nullptr && gemm_timer_ == nullptr && d.tp_size == 1) {
+  if (use_graphs_ && timer == nullptr && gemm_timer_ == nullptr && d.tp_size == 1 && dbg_skip_ == 0) {
     const GraphKey key{&m, &ws, n, splits, tokens_host != nullptr};
     auto it = graphs_.find(key);
     // capture on a key's second use: a batch size seen once (serving under

@@ -184,6 +184,11 @@ class Runtime {
   // CUDA graphs for decode jobs: one capture per (model, workspace, batch,
   // K1 splits, tokens staged or gathered), replayed on later calls.
   void set_graphs(bool on) { use_graphs_ = on; }
+  // Debug / measurement (MUX_DEBUG_SKIP, option "debug_skip"): decode jobs
+  // skip kernel classes (1 K2, 2 RMSNorm, 4 K1, 8 RMSNorm over one row);
+  // outputs are garbage, the remaining kernels' timings are not. Never
+  // captured into graphs.
+  void set_debug_skip(int mask) { dbg_skip_ = mask; }
   int64_t graph_captures() const { return graph_captures_; }
 
   // Cached tensor map for an activation buffer viewed as rows x cols bf16.
@@ -235,6 +240,7 @@ class Runtime {
   };
   static constexpr size_t kMaxGraphs = 384;
   bool use_graphs_ = true;
+  int dbg_skip_ = 0;
   std::map<GraphKey, GraphEntry> graphs_;
   std::map<GraphKey, int> graph_seen_;
   uint64_t graph_clock_ = 0;
