@@ -87,7 +87,7 @@ __device__ __forceinline__ int snake_item(int r, int c, int G) { return r * G + 
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv,
                          const PrefillAttnArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
+  extern __shared__ __align__(16) uint8_t smem_raw[];  // aligned below (a 1 KiB-aligned declaration costs 1 KiB of static smem)
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* q_s = base;
   uint8_t* kv_s = q_s + kTileBytes;                 // [stage][K|V][2 halves]
@@ -390,18 +390,21 @@ struct Bars2 {
   uint64_t s_full[2], s_empty[2], p_full[2], o_full[2];
   uint32_t tmem;
   uint32_t pad;
-  float ml[2][2][128];  // [group][m | l][row]: the epilogue's exchange
 };
-// Q + 2 stages of K and V + P0, P1 (the dynamic window starts 1 KiB-aligned
-// after the 1 KiB the driver reserves per CTA; checked in the kernel)
+// Q + 2 stages of K and V + P0, P1 + barriers: 224.2 KiB of the 227 KiB a
+// CTA may hold (the dynamic window starts 1 KiB-aligned after the 1 KiB the
+// driver reserves; checked in the kernel). The epilogue's (m, l) exchange
+// lives in the P buffers, idle once the item's P V are done.
 constexpr size_t kSmem2 = kTileBytes + kStages * 2 * kTileBytes + 2 * kTileBytes + sizeof(Bars2);
 
 __global__ void __maxnreg__(224)
 prefill_attention_split_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv,
                                const PrefillAttnArgs a) {
-  extern __shared__ __align__(1024) uint8_t smem_raw[];
-  if ((smem_u32(smem_raw) & 1023u) != 0) __trap();  // SW128 images need 1 KiB alignment
-  uint8_t* q_s = smem_raw;
+  // no __align__(1024) on the declaration: it costs 1 KiB of static shared
+  // memory, and Q + K/V + P + barriers need all but ~850 B of the 227 KiB
+  extern __shared__ __align__(16) uint8_t smem_split[];
+  if ((smem_u32(smem_split) & 1023u) != 0) __trap();  // SW128 images need 1 KiB alignment
+  uint8_t* q_s = smem_split;
   uint8_t* kv_s = q_s + kTileBytes;                 // [stage][K|V][2 halves]
   uint8_t* p_s = kv_s + kStages * 2 * kTileBytes;   // [group][2 halves][128 rows][128 B]
   Bars2& bar = *reinterpret_cast<Bars2*>(p_s + 2 * kTileBytes);
@@ -622,15 +625,19 @@ prefill_attention_split_kernel(const __grid_constant__ CUtensorMap tq, const __g
       }
       // ---- epilogue: merge the two groups; group g writes dims [64g, 64g + 64)
       const int n0 = (n_kv + 1) / 2, n1 = n_kv / 2;  // tiles of group 0 / 1 in this item
-      bar.ml[grp][0][row] = m_run;
-      bar.ml[grp][1][row] = l_run;
-      asm volatile("bar.sync 1, %0;" ::"n"(2 * kGroupWarps * 32) : "memory");
-      const float m0 = bar.ml[0][0][row], l0 = bar.ml[0][1][row];
-      const float m1 = bar.ml[1][0][row], l1 = bar.ml[1][1][row];
-      asm volatile("bar.sync 1, %0;" ::"n"(2 * kGroupWarps * 32) : "memory");  // exchange read: reusable
+      // every P V of the item is done: O final, both P buffers idle
       mbar_wait(&bar.o_full[0], (cnt0 + n0 - 1) & 1);
       if (n1 > 0) mbar_wait(&bar.o_full[1], (cnt1 + n1 - 1) & 1);
       tc_fence_after();
+      float* ml_mine = reinterpret_cast<float*>(p_s + grp * kTileBytes);
+      const float* ml_other = reinterpret_cast<const float*>(p_s + (grp ^ 1) * kTileBytes);
+      ml_mine[row] = m_run;
+      ml_mine[128 + row] = l_run;
+      asm volatile("bar.sync 1, %0;" ::"n"(2 * kGroupWarps * 32) : "memory");
+      const float mo = ml_other[row], lo = ml_other[128 + row];
+      asm volatile("bar.sync 1, %0;" ::"n"(2 * kGroupWarps * 32) : "memory");  // read: P buffers reusable
+      const float m0 = grp ? mo : m_run, l0 = grp ? lo : l_run;
+      const float m1 = grp ? m_run : mo, l1 = grp ? l_run : lo;
       const float m = fmaxf(m0, m1);
       const float a0 = l0 > 0.f ? exp2f(m0 - m) : 0.f;
       const float a1 = l1 > 0.f ? exp2f(m1 - m) : 0.f;
