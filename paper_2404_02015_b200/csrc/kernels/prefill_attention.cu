@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 
@@ -397,7 +398,7 @@ struct Bars2 {
 // lives in the P buffers, idle once the item's P V are done.
 constexpr size_t kSmem2 = kTileBytes + kStages * 2 * kTileBytes + 2 * kTileBytes + sizeof(Bars2);
 
-__global__ void __maxnreg__(224)
+__global__ void __launch_bounds__(kThreads2, 1)
 prefill_attention_split_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv,
                                const PrefillAttnArgs a) {
   // no __align__(1024) on the declaration: it costs 1 KiB of static shared
@@ -571,41 +572,49 @@ prefill_attention_split_kernel(const __grid_constant__ CUtensorMap tq, const __g
         const float m_new = move ? m_tile : m_run;
         const float m_use = m_new == -INFINITY ? 0.f : m_new;
         const float alpha = move ? exp2f(m_run - m_use) : 1.f;
-        float psum = 0.f;
-        uint32_t pk[64];
-        if (full) {
-          float sa = 0.f, sb = 0.f;
-  #pragma unroll
-          for (int i = 0; i < 128; i += 2) {
-            float x0, x1;
-            ffma2(x0, x1, v[i], v[i + 1], a.scale_log2, a.scale_log2, -m_use, -m_use);
-            const float p0 = ex2_ftz(x0), p1 = ex2_ftz(x1);
-            fadd2(sa, sb, p0, p1);
-            pk[i >> 1] = pack_bf16(p0, p1);
-          }
-          psum = sa + sb;
-        } else {
-  #pragma unroll
-          for (int i = 0; i < 128; i += 2) {
-            const float p0 = i <= kmax ? exp2f(fmaf(v[i], a.scale_log2, -m_use)) : 0.f;
-            const float p1 = i + 1 <= kmax ? exp2f(fmaf(v[i + 1], a.scale_log2, -m_use)) : 0.f;
-            psum += p0 + p1;
-            pk[i >> 1] = pack_bf16(p0, p1);
-          }
-        }
         // the group's previous P V (this item's or an earlier item's) is done:
-        // its P buffer is free and O_g may be rescaled
+        // its P buffer is free and O_g may be rescaled. Waiting here (not
+        // after the exps) lets each 8-key chunk of P go to smem as soon as it
+        // is computed, so no packed copy of the row is held in registers.
         if (u >= 1) {
           mbar_wait(&bar.o_full[grp], (u - 1) & 1);
           tc_fence_after();
         }
+        float psum = 0.f;
+        if (full) {
+          float sa = 0.f, sb = 0.f;
   #pragma unroll
-        for (int hf = 0; hf < 2; ++hf)
+          for (int c8 = 0; c8 < 16; ++c8) {
+            uint32_t pk[4];
   #pragma unroll
-          for (int chunk = 0; chunk < 8; ++chunk)
-            *reinterpret_cast<uint4*>(p_row + hf * kHalfBytes + ((chunk ^ (row & 7)) << 4)) =
-                make_uint4(pk[32 * hf + 4 * chunk], pk[32 * hf + 4 * chunk + 1], pk[32 * hf + 4 * chunk + 2],
-                           pk[32 * hf + 4 * chunk + 3]);
+            for (int e = 0; e < 4; ++e) {
+              const int i = 8 * c8 + 2 * e;
+              float x0, x1;
+              ffma2(x0, x1, v[i], v[i + 1], a.scale_log2, a.scale_log2, -m_use, -m_use);
+              const float p0 = ex2_ftz(x0), p1 = ex2_ftz(x1);
+              fadd2(sa, sb, p0, p1);
+              pk[e] = pack_bf16(p0, p1);
+            }
+            *reinterpret_cast<uint4*>(p_row + (c8 >> 3) * kHalfBytes + (((c8 & 7) ^ (row & 7)) << 4)) =
+                make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+          psum = sa + sb;
+        } else {
+  #pragma unroll
+          for (int c8 = 0; c8 < 16; ++c8) {
+            uint32_t pk[4];
+  #pragma unroll
+            for (int e = 0; e < 4; ++e) {
+              const int i = 8 * c8 + 2 * e;
+              const float p0 = i <= kmax ? exp2f(fmaf(v[i], a.scale_log2, -m_use)) : 0.f;
+              const float p1 = i + 1 <= kmax ? exp2f(fmaf(v[i + 1], a.scale_log2, -m_use)) : 0.f;
+              psum += p0 + p1;
+              pk[e] = pack_bf16(p0, p1);
+            }
+            *reinterpret_cast<uint4*>(p_row + (c8 >> 3) * kHalfBytes + (((c8 & 7) ^ (row & 7)) << 4)) =
+                make_uint4(pk[0], pk[1], pk[2], pk[3]);
+          }
+        }
         if (t > 0 && __any_sync(0xffffffffu, move)) {
   #pragma unroll 1
           for (int c = 0; c < 4; ++c) {
@@ -705,8 +714,20 @@ cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
   std::memcpy(&tkv, a.tmap_qkv, sizeof(CUtensorMap));
   const int n_items = a.n_tiles * a.H;
   const int grid = std::max(1, std::min(n_items, a.max_ctas > 0 ? a.max_ctas : 148));
-  if (env_k3 == 2)
-    return launch(prefill_attention_split_kernel, dim3(grid), dim3(kThreads2), kSmem2, stream, tq, tkv, a);
+  if (env_k3 == 2) {
+    cudaError_t e = launch(prefill_attention_split_kernel, dim3(grid), dim3(kThreads2), kSmem2, stream, tq, tkv, a);
+    if (e == cudaErrorLaunchOutOfResources) {  // diagnostics for the resource budget of this form
+      cudaFuncAttributes fa{};
+      cudaFuncGetAttributes(&fa, reinterpret_cast<const void*>(prefill_attention_split_kernel));
+      int optin = 0, dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev);
+      std::fprintf(stderr, "K3 split: regs %d maxThreads %d static smem %zu maxDyn %d requested dyn %zu optin %d threads %d\n",
+                   fa.numRegs, fa.maxThreadsPerBlock, fa.sharedSizeBytes, fa.maxDynamicSharedSizeBytes, kSmem2, optin,
+                   kThreads2);
+    }
+    return e;
+  }
   return launch(prefill_attention_kernel, dim3(grid), dim3(kThreads), kSmemBytes, stream, tq, tkv, a);
 }
 
