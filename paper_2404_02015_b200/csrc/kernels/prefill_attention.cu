@@ -699,7 +699,7 @@ cudaError_t preload_prefill_attention() { return preload(prefill_attention_kerne
 
 cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
   if (a.T <= 0 || a.n_tiles <= 0) return cudaSuccess;
-  static const int env_k3 = getenv("MUX_K3") ? atoi(getenv("MUX_K3")) : 1;
+  static const int env_k3 = getenv("MUX_K3") ? atoi(getenv("MUX_K3")) : 2;  // 1: the one-group form
   static PerDeviceOnce configured;
   cudaError_t ce = configured.run([] {
     cudaError_t e = cudaFuncSetAttribute(prefill_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
