@@ -42,11 +42,19 @@ constexpr int kTile = 128;                   // queries per CTA, keys per KV til
 constexpr int kHalfBytes = kTile * 64 * 2;   // one 64-dim SW128 half of a tile: 16 KiB
 constexpr int kTileBytes = 2 * kHalfBytes;   // 128 x 128 bf16
 constexpr int kStages = 2;
-constexpr int kSoftmaxWarps = 8;             // 2 per TMEM lane quarter: each owns 64 of a row's 128 keys
+// kParts softmax warps per TMEM lane quarter, each owning kKeys of a row's
+// 128 keys (and 128 / kParts of its output dims): more warps per SMSP hide
+// the exp / TMEM-load latencies the one-row-per-thread chain exposes.
+#ifndef MUX_K3_PARTS
+#define MUX_K3_PARTS 4
+#endif
+constexpr int kParts = MUX_K3_PARTS;
+constexpr int kKeys = kTile / kParts;
+constexpr int kSoftmaxWarps = 4 * kParts;
 constexpr int kThreads = (kSoftmaxWarps + 1) * 32;  // + 1 TMA/MMA warp
 constexpr uint32_t kTmemCols = 512;          // S0 [0,128) S1 [128,256) O [256,384)
 constexpr size_t kSmemBytes = 1024 + kTileBytes /*Q*/ + kStages * 2 * kTileBytes /*K,V*/ +
-                              kTileBytes /*P*/ + 256 /*barriers*/ + 4 * 2 * 128 * 4 /*row exchange*/;
+                              kTileBytes /*P*/ + 256 /*barriers*/ + 3 * kParts * 128 * 4 /*row exchange*/;
 
 struct Bars {
   uint64_t q_full;
@@ -62,8 +70,8 @@ struct Bars {
   uint64_t o_empty;  // persistent: the softmax warps have read the item's O
   uint32_t tmem;
   uint32_t pad[3];
-  float mx[2][2][128];  // [tile parity][key half][row]: partial row maxima
-  float ls[2][128];     // [key half][row]: partial row sums (end)
+  float mx[2][kParts][128];  // [tile parity][key part][row]: partial row maxima
+  float ls[kParts][128];     // [key part][row]: partial row sums (end)
 };
 
 // MN-major SW128 descriptor (B = V: N = head dims contiguous, K = keys):
@@ -221,16 +229,19 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
     }
     __syncwarp();
   } else {
-    // ---------------- softmax warps: thread = (query row, key half)
-    // Warps w and w+4 share TMEM lane quarter w%4 (rows 32*(w%4)..+31) and
-    // split the 128 keys of a tile (and the 128 output dims) in halves; the
-    // row max is exchanged through smem once per tile (double-buffered by
-    // tile parity, so one barrier per tile), the row sums once at the end.
-    const int quarter = warp & 3, hf = warp >> 2;
+    // ---------------- softmax warps: thread = (query row, key part)
+    // Warps w, w+4, w+8, ... share TMEM lane quarter w%4 (rows 32*(w%4)..+31)
+    // and split the 128 keys of a tile (and the 128 output dims) into kParts
+    // parts of kKeys; the row max is exchanged through smem once per tile
+    // (double-buffered by tile parity, so one barrier per tile), the row sums
+    // once at the end.
+    const int quarter = warp & 3, part = warp >> 2;
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    uint8_t* p_row = p_s + hf * kHalfBytes + row * 128;
-    const uint32_t o_addr = tmem + lane_base + 2 * kTile + hf * 64;
+    // this part's keys in P's SW128 K-major image: half (part*kKeys)/64, 16-B chunks from (part*kKeys%64)/8
+    uint8_t* p_row = p_s + ((part * kKeys) / 64) * kHalfBytes + row * 128;
+    const int chunk0 = ((part * kKeys) % 64) / 8;
+    const uint32_t o_addr = tmem + lane_base + 2 * kTile + part * kKeys;
     int jg = 0;
     for (int round = 0;; ++round) {
       const int item = snake_item(round, blockIdx.x, gridDim.x);
@@ -249,32 +260,35 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         const int sb = g & 1;
         mbar_wait(&bar.s_full[sb], (g >> 1) & 1);
         tc_fence_after();
-        const uint32_t s_addr = tmem + lane_base + sb * kTile + hf * 64;
-        const int kmax = min(qi, len - 1) - j * kTile - hf * 64;  // keys [0, kmax] of this half are visible
-        // S read once (64 keys of this half into registers); the S buffer is
+        const uint32_t s_addr = tmem + lane_base + sb * kTile + part * kKeys;
+        const int kmax = min(qi, len - 1) - j * kTile - part * kKeys;  // keys [0, kmax] of this part are visible
+        // S read once (this part's keys into registers); the S buffer is
         // handed back right away so Q K_{j+2}^T can start.
-        float v[64];
-        tmem_ld_32x32b_x32(s_addr, *reinterpret_cast<float(*)[32]>(v));
-        tmem_ld_32x32b_x32(s_addr + 32, *reinterpret_cast<float(*)[32]>(v + 32));
+        float v[kKeys];
+  #pragma unroll
+        for (int c = 0; c < kKeys / 32; ++c) tmem_ld_32x32b_x32(s_addr + c * 32, *reinterpret_cast<float(*)[32]>(v + 32 * c));
         tc_fence_before();
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar.s_empty[sb]);
-        // partial row max over this half, exchanged with the partner warp
-        // Tiles below the diagonal and inside the sequence need no masking:
-        // the fast path is 3-input max, paired FMA, bare MUFU.EX2, paired add.
-        const bool full = kmax >= 63;
+        // partial row max over this part, exchanged with the quarter's other
+        // warps. Tiles below the diagonal and inside the sequence need no
+        // masking: the fast path is 3-input max, paired FMA, bare MUFU.EX2,
+        // paired add.
+        const bool full = kmax >= kKeys - 1;
         float mx = -INFINITY;
         if (full) {
   #pragma unroll
-          for (int i = 0; i < 64; i += 2) mx = fmax3(mx, v[i], v[i + 1]);
+          for (int i = 0; i < kKeys; i += 2) mx = fmax3(mx, v[i], v[i + 1]);
         } else {
   #pragma unroll
-          for (int i = 0; i < 64; ++i)
+          for (int i = 0; i < kKeys; ++i)
             if (i <= kmax) mx = fmaxf(mx, v[i]);
         }
-        bar.mx[g & 1][hf][row] = mx;
+        bar.mx[g & 1][part][row] = mx;
         asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
-        mx = fmaxf(mx, bar.mx[g & 1][hf ^ 1][row]);
+  #pragma unroll
+        for (int o = 0; o < kParts; ++o)
+          if (o != part) mx = fmaxf(mx, bar.mx[g & 1][o][row]);
         // Lazy rescaling: the running max only moves (and O is rescaled) when
         // the tile's max exceeds it by more than 2^8; otherwise P = exp2(s - m)
         // stays <= 256 under the stale max, and l / O share that max, so the
@@ -286,11 +300,11 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         const float alpha = move ? exp2f(m_run - m_use) : 1.f;
         // P = exp2(s - m) -> packed bf16 in registers while P_{j-1} V_{j-1} runs
         float psum = 0.f;
-        uint32_t pk[32];
+        uint32_t pk[kKeys / 2];
         if (full) {
           float s0 = 0.f, s1 = 0.f;
   #pragma unroll
-          for (int i = 0; i < 64; i += 2) {
+          for (int i = 0; i < kKeys; i += 2) {
             float x0, x1;
             ffma2(x0, x1, v[i], v[i + 1], a.scale_log2, a.scale_log2, -m_use, -m_use);
             const float p0 = ex2_ftz(x0), p1 = ex2_ftz(x1);
@@ -300,7 +314,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
           psum = s0 + s1;
         } else {
   #pragma unroll
-          for (int i = 0; i < 64; i += 2) {
+          for (int i = 0; i < kKeys; i += 2) {
             const float p0 = i <= kmax ? exp2f(fmaf(v[i], a.scale_log2, -m_use)) : 0.f;
             const float p1 = i + 1 <= kmax ? exp2f(fmaf(v[i + 1], a.scale_log2, -m_use)) : 0.f;
             psum += p0 + p1;
@@ -313,14 +327,14 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
           mbar_wait(&bar.o_full, (g - 1) & 1);
           tc_fence_after();
         }
-        // keys [64hf + 8chunk, +8) in the SW128 K-major image of this half's row
+        // this part's keys [part*kKeys + 8c, +8) in the SW128 K-major image of its row
   #pragma unroll
-        for (int chunk = 0; chunk < 8; ++chunk)
-          *reinterpret_cast<uint4*>(p_row + ((chunk ^ (row & 7)) << 4)) =
-              make_uint4(pk[4 * chunk], pk[4 * chunk + 1], pk[4 * chunk + 2], pk[4 * chunk + 3]);
+        for (int c = 0; c < kKeys / 8; ++c)
+          *reinterpret_cast<uint4*>(p_row + (((chunk0 + c) ^ (row & 7)) << 4)) =
+              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
         if (j > 0 && __any_sync(0xffffffffu, move)) {
   #pragma unroll 1
-          for (int c = 0; c < 2; ++c) {
+          for (int c = 0; c < kKeys / 32; ++c) {
             float o[32];
             tmem_ld_32x32b_x32(o_addr + c * 32, o);
   #pragma unroll
@@ -335,16 +349,18 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar.p_full);
       }
-      bar.ls[hf][row] = l_run;
+      bar.ls[part][row] = l_run;
       asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
-      const float l_tot = l_run + bar.ls[hf ^ 1][row];
+      float l_tot = 0.f;
+  #pragma unroll
+      for (int o = 0; o < kParts; ++o) l_tot += bar.ls[o][row];
       mbar_wait(&bar.o_full, (jg + n_kv - 1) & 1);
       tc_fence_after();
       const float inv = l_tot > 0.f ? 1.f / l_tot : 0.f;
       uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) +
-                                            (static_cast<int64_t>(s0 + qi) * a.H + h) * 128 + hf * 64);
+                                            (static_cast<int64_t>(s0 + qi) * a.H + h) * 128 + part * kKeys);
   #pragma unroll
-      for (int c = 0; c < 2; ++c) {
+      for (int c = 0; c < kKeys / 32; ++c) {
         float v[32];
         tmem_ld_32x32b_x32(o_addr + c * 32, v);  // all lanes: .sync.aligned
         if (qi < len) {
