@@ -384,8 +384,6 @@ MUX_API int64_t mux_unit_launches(mux_unit* unit);
  * "graphs" (decode jobs replayed from cached CUDA graphs, default 1);
  * "debug_skip" (measurement: decode jobs skip kernel classes, bitmask 1 K2,
  * 2 RMSNorm, 4 K1; outputs are garbage; bench.py times the GEMM stream so);
- * "qkv_f32" (decode QKV as fp32 sums through the GEMM's reduce-add epilogue,
- * no stream-K fixup; K2 rounds them to bf16 and clears them, default 1);
  * "prefill_on_partition" (prefill jobs on their model's partition);
  * "pass_green" (partitions = [whole GPU | a whole-GPU stream per model |
  * a green partition per model]; decode jobs use the green partitions only in

@@ -1579,7 +1579,6 @@ int mux_unit_set_option(mux_unit* u, const char* key, int64_t value) {
     else if (k == "pdl") mux::pdl_enabled() = value != 0;
     else if (k == "graphs") u->rt->set_graphs(value != 0);
     else if (k == "debug_skip") u->rt->set_debug_skip(static_cast<int>(value));
-    else if (k == "qkv_f32") u->rt->set_qkv_f32(value != 0);
     else if (k == "prefill_on_partition") u->prefill_on_partition = value != 0;
     else if (k == "pass_green") u->pass_green = value != 0;
     else if (k == "align_decode") u->align_decode = value != 0;

@@ -225,8 +225,6 @@ Workspace::Workspace(int max_tok, int max_batch_rows, int hidden, int qkv_cols, 
   attn = DevMem(Tp * heads * 128 * 2);
   act = DevMem(Tp * ffn * 2);
   gemm_partials = DevMem(gemm_partials_floats(grid) * 4);
-  qkv_f32 = DevMem(static_cast<size_t>(std::max(max_decode_batch, 1)) * qkv_cols * 4);
-  check_cuda(cudaMemset(qkv_f32.p, 0, qkv_f32.bytes), "memset qkv_f32");
   gemm_flags = DevMem(static_cast<size_t>(std::max(grid, 1024)) * 4);
   check_cuda(cudaMemset(gemm_flags.p, 0, gemm_flags.bytes), "memset flags");
   const size_t rows_out = std::max<size_t>(max_batch_rows, 256);
@@ -326,7 +324,6 @@ Runtime::Runtime(int device, int64_t pool_blocks, int max_pos)
   check_cuda(preload(gather_last_tok, scatter_last_tok), "preload");
   if (const char* g = getenv("MUX_GRAPHS")) use_graphs_ = atoi(g) != 0;  // A/B switch (option "graphs")
   if (const char* k = getenv("MUX_DEBUG_SKIP")) dbg_skip_ = atoi(k);   // option "debug_skip"
-  if (const char* k = getenv("MUX_QKV_F32")) qkv_f32_ = atoi(k) != 0;  // option "qkv_f32"
   pool_ = DevMem(static_cast<size_t>(pool_blocks) * 4096);
   // RoPE table [max_pos][64][(cos, sin)], computed in double, stored fp32.
   std::vector<float> tab(static_cast<size_t>(max_pos) * 128);
@@ -346,12 +343,6 @@ Runtime::~Runtime() {
   for (StageSlot& s : ring_)
     if (s.done) cudaEventDestroy(s.done);
   for (auto& g : graphs_) cudaGraphExecDestroy(g.second.exec);
-}
-
-void Runtime::clear_graphs() {
-  for (auto& g : graphs_) cudaGraphExecDestroy(g.second.exec);
-  graphs_.clear();
-  graph_seen_.clear();
 }
 
 const void* Runtime::act_tmap(const void* base, int rows, int cols, int box_rows) {
@@ -552,13 +543,6 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
     throw std::invalid_argument("decode: batch of " + std::to_string(n) + " exceeds the unit's max_batch " +
                                 std::to_string(ws.max_decode));
   const ModelDims& d = m.dims();
-  // fp32 QKV sums: the buffer must be zero before the first layer's reduce-add
-  const bool qkv32 = qkv_f32_ && d.tp_size == 1 && ws.qkv_f32.bytes >= static_cast<size_t>(n) * m.qkv_cols() * 4;
-  if (qkv32 && ws.qkv_dirty && !(dbg_skip_ & 1)) {
-    check_cuda(cudaMemsetAsync(ws.qkv_f32.p, 0, ws.qkv_f32.bytes, stream), "clear qkv_f32");
-    ws.qkv_dirty = false;
-  }
-  if (qkv32 && (dbg_skip_ & 1)) ws.qkv_dirty = true;  // K2 skipped: the sums are not cleared
   const int T = std::max(ws.max_tokens, 16);
   int32_t* h = ws.stage_begin();
   for (int i = 0; i < n; ++i) {
@@ -628,7 +612,6 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
 
   AppendArgs ap{};
   ap.qkv = ws.qkv.p;
-  ap.qkv_f32 = qkv32 ? ws.qkv_f32.as<float>() : nullptr;
   ap.q_out = ws.q.p;
   ap.pool = pool_.p;
   ap.rowrec = m.rowrec.as<int32_t>();
@@ -648,10 +631,7 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   const int dbg_skip = dbg_skip_;
   for (int l = 0; l < L; ++l) {
     ap.layer = l;
-    if (qkv32)  // fp32 sums, pieces reduce-added: no stream-K fixup
-      gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv_f32.p, m.qkv_cols(), kEpiResidual, ws, stream);
-    else
-      gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
+    gemm(m.wqkv[l].p, ws.xn.p, n, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);
     if (!(dbg_skip & 1)) {
       check_cuda(kv_append(ap, stream), "kv_append");
       launches_ += 1;

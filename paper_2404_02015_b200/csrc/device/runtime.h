@@ -134,10 +134,6 @@ struct Workspace {
   int max_hidden = 0, max_qkv = 0, max_ffn = 0, max_vocab = 0, max_heads = 0;
   DevMem resid, xn, qkv, q, attn, act, logits, ints, attn_part_o, attn_part_ml, attn_split_count, xlast;
   DevMem gemm_partials, gemm_flags;  // stream-K fixup scratch of this partition's GEMMs
-  // decode QKV as fp32 sums (option qkv_f32): [max_decode][qkv] fp32, zero
-  // between layers (K2 consumes and clears); dirty after K2-skipping debug jobs
-  DevMem qkv_f32;
-  bool qkv_dirty = false;
   int gemm_epoch = 0;
   int sms = 148;           // SMs of the partition this workspace's jobs run on
   bool exclusive = false;  // a green partition: no other stream's kernels share its SMs
@@ -193,13 +189,6 @@ class Runtime {
   // outputs are garbage, the remaining kernels' timings are not. Never
   // captured into graphs.
   void set_debug_skip(int mask) { dbg_skip_ = mask; }
-  // Decode QKV through the GEMM's fp32 reduce-add epilogue into
-  // Workspace::qkv_f32 (no stream-K fixup tail); K2 rounds to bf16 and clears.
-  void set_qkv_f32(bool on) {
-    if (on != qkv_f32_) clear_graphs();
-    qkv_f32_ = on;
-  }
-  void clear_graphs();
   int64_t graph_captures() const { return graph_captures_; }
 
   // Cached tensor map for an activation buffer viewed as rows x cols bf16.
@@ -252,7 +241,6 @@ class Runtime {
   static constexpr size_t kMaxGraphs = 384;
   bool use_graphs_ = true;
   int dbg_skip_ = 0;
-  bool qkv_f32_ = true;
   std::map<GraphKey, GraphEntry> graphs_;
   std::map<GraphKey, int> graph_seen_;
   uint64_t graph_clock_ = 0;

@@ -42,11 +42,6 @@ struct AppendArgs {
   const float* rope;        // [max_pos][64][2] (cos, sin)
   int T, H, layer, max_rows, row_width;
   int rope_positions;
-  // Decode (option qkv_f32): q | k | v come as fp32 sums [T][3][H][128]
-  // (the QKV GEMM's reduce-add epilogue, no stream-K fixup); they are rounded
-  // to bf16 as the store epilogue would, and the rows are zeroed again for the
-  // next layer's reduce-add. qkv is then unused.
-  float* qkv_f32 = nullptr;
 };
 cudaError_t kv_append(const AppendArgs& a, cudaStream_t stream);
 

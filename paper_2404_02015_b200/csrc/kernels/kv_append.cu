@@ -52,22 +52,9 @@ __global__ void __launch_bounds__(256) kv_append_kernel(const AppendArgs a) {
 
   const int64_t tok_base = static_cast<int64_t>(t) * 3 * a.H * kDim;
   const __nv_bfloat16* qkv = reinterpret_cast<const __nv_bfloat16*>(a.qkv);
-  uint2 qv, kv, vv;
-  if (a.qkv_f32 != nullptr) {
-    // fp32 sums -> bf16 (round to nearest, as the bf16 store epilogue), then
-    // zero them for the next layer's reduce-add
-    float4* src = reinterpret_cast<float4*>(a.qkv_f32 + tok_base + h * kDim + lane * 4);
-    const int64_t part = static_cast<int64_t>(a.H) * kDim / 4;  // q -> k -> v, in float4
-    const float4 fq = src[0], fk = src[part], fv = src[2 * part];
-    src[0] = src[part] = src[2 * part] = make_float4(0.f, 0.f, 0.f, 0.f);
-    qv = make_uint2(pack_bf16(fq.x, fq.y), pack_bf16(fq.z, fq.w));
-    kv = make_uint2(pack_bf16(fk.x, fk.y), pack_bf16(fk.z, fk.w));
-    vv = make_uint2(pack_bf16(fv.x, fv.y), pack_bf16(fv.z, fv.w));
-  } else {
-    qv = *reinterpret_cast<const uint2*>(qkv + tok_base + (0 * a.H + h) * kDim + lane * 4);
-    kv = *reinterpret_cast<const uint2*>(qkv + tok_base + (1 * a.H + h) * kDim + lane * 4);
-    vv = *reinterpret_cast<const uint2*>(qkv + tok_base + (2 * a.H + h) * kDim + lane * 4);
-  }
+  const uint2 qv = *reinterpret_cast<const uint2*>(qkv + tok_base + (0 * a.H + h) * kDim + lane * 4);
+  const uint2 kv = *reinterpret_cast<const uint2*>(qkv + tok_base + (1 * a.H + h) * kDim + lane * 4);
+  const uint2 vv = *reinterpret_cast<const uint2*>(qkv + tok_base + (2 * a.H + h) * kDim + lane * 4);
   float q[4], k[4];
   unpack4(qv, q);
   unpack4(kv, k);
@@ -78,10 +65,8 @@ __global__ void __launch_bounds__(256) kv_append_kernel(const AppendArgs a) {
     __nv_bfloat16* qo = reinterpret_cast<__nv_bfloat16*>(a.q_out);
     *reinterpret_cast<uint2*>(qo + (static_cast<int64_t>(t) * a.H + h) * kDim + lane * 4) = pack4(q);
     // Rotated k back in place too, for the prefill attention that reads it.
-    if (a.qkv_f32 == nullptr) {
-      __nv_bfloat16* qkv_w = const_cast<__nv_bfloat16*>(qkv);
-      *reinterpret_cast<uint2*>(qkv_w + tok_base + (1 * a.H + h) * kDim + lane * 4) = kr;
-    }
+    __nv_bfloat16* qkv_w = const_cast<__nv_bfloat16*>(qkv);
+    *reinterpret_cast<uint2*>(qkv_w + tok_base + (1 * a.H + h) * kDim + lane * 4) = kr;
   }
   uint8_t* pool = reinterpret_cast<uint8_t*>(a.pool);
   const int64_t off = static_cast<int64_t>(pos & 15) * 256 + lane * 8;
