@@ -43,10 +43,11 @@ constexpr int kHalfBytes = kTile * 64 * 2;   // one 64-dim SW128 half of a tile:
 constexpr int kTileBytes = 2 * kHalfBytes;   // 128 x 128 bf16
 constexpr int kStages = 2;
 // kParts softmax warps per TMEM lane quarter, each owning kKeys of a row's
-// 128 keys (and 128 / kParts of its output dims): more warps per SMSP hide
-// the exp / TMEM-load latencies the one-row-per-thread chain exposes.
+// 128 keys (and 128 / kParts of its output dims). 2 (8 softmax warps) is
+// the measured best: 4 parts (16 warps) ran 4096 tokens x 40 heads in 263
+// instead of 245 us (profiles/r02_k3_parts.txt).
 #ifndef MUX_K3_PARTS
-#define MUX_K3_PARTS 4
+#define MUX_K3_PARTS 2
 #endif
 constexpr int kParts = MUX_K3_PARTS;
 constexpr int kKeys = kTile / kParts;
