@@ -29,6 +29,7 @@
 
 #include <algorithm>
 #include <cstdint>
+#include <cstdlib>
 #include <cstring>
 
 #include "kernels.h"
@@ -53,7 +54,8 @@ constexpr int kParts = MUX_K3_PARTS;
 constexpr int kKeys = kTile / kParts;
 constexpr int kSoftmaxWarps = 4 * kParts;
 constexpr int kThreads = (kSoftmaxWarps + 1) * 32;  // + 1 TMA/MMA warp
-constexpr uint32_t kTmemCols = 512;          // S0 [0,128) S1 [128,256) O [256,384)
+constexpr uint32_t kTmemCols = 512;          // S0 [0,128) S1 [128,256) O [256,384) P [384,448)
+constexpr uint32_t kPCol = 384;              // P (bf16 pairs) when it goes through TMEM (args.p_tmem)
 constexpr size_t kSmemBytes = 1024 + kTileBytes /*Q*/ + kStages * 2 * kTileBytes /*K,V*/ +
                               kTileBytes /*P*/ + 256 /*barriers*/ + 3 * kParts * 128 * 4 /*row exchange*/;
 
@@ -219,8 +221,12 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
           const uint32_t v_addr = smem_u32(kv_s + st * 2 * kTileBytes + kTileBytes);
   #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            umma_bf16(tmem + 2 * kTile, umma_desc_sw128(p_addr + (kk >> 2) * kHalfBytes + (kk & 3) * 32),
-                      umma_desc_sw128_mn(v_addr + kk * 2048), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+            if (a.p_tmem)
+              umma_ts_bf16(tmem + 2 * kTile, tmem + kPCol + kk * 8, umma_desc_sw128_mn(v_addr + kk * 2048), idesc_pv,
+                           (j > 0 || kk > 0) ? 1u : 0u);
+            else
+              umma_bf16(tmem + 2 * kTile, umma_desc_sw128(p_addr + (kk >> 2) * kHalfBytes + (kk & 3) * 32),
+                        umma_desc_sw128_mn(v_addr + kk * 2048), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
           }
           umma_commit(&bar.o_full);
           umma_commit(&bar.v_empty[st]);
@@ -328,11 +334,19 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
           mbar_wait(&bar.o_full, (g - 1) & 1);
           tc_fence_after();
         }
-        // this part's keys [part*kKeys + 8c, +8) in the SW128 K-major image of its row
+        if (a.p_tmem) {
+          // this part's keys as bf16 pairs in its row's lane, columns [kPCol + part*kKeys/2, +kKeys/2)
   #pragma unroll
-        for (int c = 0; c < kKeys / 8; ++c)
-          *reinterpret_cast<uint4*>(p_row + (((chunk0 + c) ^ (row & 7)) << 4)) =
-              make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+          for (int c = 0; c < kKeys / 64; ++c)
+            tmem_st_32x32b_x32(tmem + lane_base + kPCol + part * (kKeys / 2) + c * 32,
+                               *reinterpret_cast<const float(*)[32]>(pk + 32 * c));
+        } else {
+          // this part's keys [part*kKeys + 8c, +8) in the SW128 K-major image of its row
+  #pragma unroll
+          for (int c = 0; c < kKeys / 8; ++c)
+            *reinterpret_cast<uint4*>(p_row + (((chunk0 + c) ^ (row & 7)) << 4)) =
+                make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
+        }
         if (j > 0 && __any_sync(0xffffffffu, move)) {
   #pragma unroll 1
           for (int c = 0; c < kKeys / 32; ++c) {
@@ -406,7 +420,10 @@ cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
   std::memcpy(&tkv, a.tmap_qkv, sizeof(CUtensorMap));
   const int n_items = a.n_tiles * a.H;
   const int grid = std::max(1, std::min(n_items, a.max_ctas > 0 ? a.max_ctas : 148));
-  return launch(prefill_attention_kernel, dim3(grid), dim3(kThreads), kSmemBytes, stream, tq, tkv, a);
+  PrefillAttnArgs args = a;
+  static const int env_pt = getenv("MUX_K3_PTMEM") ? atoi(getenv("MUX_K3_PTMEM")) : 0;
+  args.p_tmem = env_pt;
+  return launch(prefill_attention_kernel, dim3(grid), dim3(kThreads), kSmemBytes, stream, tq, tkv, args);
 }
 
 }  // namespace mux
