@@ -155,7 +155,6 @@ struct PrefillAttnArgs {
   int n_tiles, nseq, H, T;
   float scale_log2;
   int max_ctas = 0;         // persistent grid (the partition's SMs); 0 = 148
-  int p_tmem = 0;           // P through tensor memory (TS MMA) instead of shared memory
 };
 cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream);
 size_t prefill_attention_smem();

@@ -11,8 +11,9 @@
 //   S_j = Q K_j^T      UMMA 128x128x128, A = Q (smem, K-major), B = K_j (smem,
 //                      K-major), fp32 accumulator in TMEM (double-buffered so
 //                      S_{j+1} is computed while the softmax reads S_j)
-//   O_j = P_j V_j      UMMA 128x128x128, A = P_j (bf16, written to smem by the
-//                      softmax in the canonical SW128 K-major image), B = V_j
+//   O_j = P_j V_j      UMMA 128x128x128, A = P_j from TENSOR MEMORY (the
+//                      softmax stores bf16 pairs with tcgen05.st, row = lane,
+//                      64 columns; no shared-memory traffic for P), B = V_j
 //                      (smem, MN-major: the same TMA box as K, other descriptor)
 // Warp 8 = TMA producer + MMA issuer (one elected lane); warps 0-7 = softmax,
 // two warps per TMEM lane quarter, a thread owns half (64 keys / 64 output
@@ -20,8 +21,8 @@
 // masking. The output accumulates in TMEM across key tiles; when
 // a row's max moves, its O row is rescaled in place (tcgen05.ld/st) before
 // the next P V is issued.
-// K/V tiles stream through a 2-stage TMA ring (SWIZZLE_128B boxes of 64 dims
-// x 128 tokens over the [T][3][H][128] QKV buffer).
+// K/V tiles stream through a kStages-deep TMA ring (SWIZZLE_128B boxes of 64
+// dims x 128 tokens over the [T][3][H][128] QKV buffer).
 // FLOPs per (sequence of length n, head): 4 * 128 * n * (n + 1) / 2 (causal).
 #include <cuda.h>
 #include <cuda_bf16.h>
@@ -55,9 +56,9 @@ constexpr int kKeys = kTile / kParts;
 constexpr int kSoftmaxWarps = 4 * kParts;
 constexpr int kThreads = (kSoftmaxWarps + 1) * 32;  // + 1 TMA/MMA warp
 constexpr uint32_t kTmemCols = 512;          // S0 [0,128) S1 [128,256) O [256,384) P [384,448)
-constexpr uint32_t kPCol = 384;              // P (bf16 pairs) when it goes through TMEM (args.p_tmem)
+constexpr uint32_t kPCol = 384;              // P: bf16 pairs, row = lane (the PV MMA's A operand)
 constexpr size_t kSmemBytes = 1024 + kTileBytes /*Q*/ + kStages * 2 * kTileBytes /*K,V*/ +
-                              kTileBytes /*P*/ + 256 /*barriers*/ + 3 * kParts * 128 * 4 /*row exchange*/;
+                              256 /*barriers*/ + 3 * kParts * 128 * 4 /*row exchange*/;
 
 struct Bars {
   uint64_t q_full;
@@ -101,8 +102,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* q_s = base;
   uint8_t* kv_s = q_s + kTileBytes;                 // [stage][K|V][2 halves]
-  uint8_t* p_s = kv_s + kStages * 2 * kTileBytes;   // [2 halves][128 rows][128 B]
-  Bars& bar = *reinterpret_cast<Bars*>(p_s + kTileBytes);
+  Bars& bar = *reinterpret_cast<Bars*>(kv_s + kStages * 2 * kTileBytes);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
   // Persistent: CTA c takes one work item per round in snake order over the
@@ -144,7 +144,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
       const uint64_t pol_kv = policy_evict_last();  // re-read by the other q tiles of this head
       const uint32_t idesc_qk = umma_idesc_bf16(kTile, kTile);
       const uint32_t idesc_pv = umma_idesc_bf16(kTile, 128) | (1u << 16);  // B (V) MN-major
-      const uint32_t q_addr = smem_u32(q_s), p_addr = smem_u32(p_s);
+      const uint32_t q_addr = smem_u32(q_s);
       int jg = 0;  // key tiles issued by this CTA before the current item (global ring / buffer counter)
       int it = 0;
       for (int round = 0;; ++round, ++it) {
@@ -221,12 +221,8 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
           const uint32_t v_addr = smem_u32(kv_s + st * 2 * kTileBytes + kTileBytes);
   #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
-            if (a.p_tmem)
-              umma_ts_bf16(tmem + 2 * kTile, tmem + kPCol + kk * 8, umma_desc_sw128_mn(v_addr + kk * 2048), idesc_pv,
-                           (j > 0 || kk > 0) ? 1u : 0u);
-            else
-              umma_bf16(tmem + 2 * kTile, umma_desc_sw128(p_addr + (kk >> 2) * kHalfBytes + (kk & 3) * 32),
-                        umma_desc_sw128_mn(v_addr + kk * 2048), idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
+            umma_ts_bf16(tmem + 2 * kTile, tmem + kPCol + kk * 8, umma_desc_sw128_mn(v_addr + kk * 2048), idesc_pv,
+                         (j > 0 || kk > 0) ? 1u : 0u);
           }
           umma_commit(&bar.o_full);
           umma_commit(&bar.v_empty[st]);
@@ -246,8 +242,6 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
     const int row = quarter * 32 + lane;
     const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
     // this part's keys in P's SW128 K-major image: half (part*kKeys)/64, 16-B chunks from (part*kKeys%64)/8
-    uint8_t* p_row = p_s + ((part * kKeys) / 64) * kHalfBytes + row * 128;
-    const int chunk0 = ((part * kKeys) % 64) / 8;
     const uint32_t o_addr = tmem + lane_base + 2 * kTile + part * kKeys;
     int jg = 0;
     for (int round = 0;; ++round) {
@@ -334,19 +328,11 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
           mbar_wait(&bar.o_full, (g - 1) & 1);
           tc_fence_after();
         }
-        if (a.p_tmem) {
-          // this part's keys as bf16 pairs in its row's lane, columns [kPCol + part*kKeys/2, +kKeys/2)
+        // this part's keys as bf16 pairs in its row's lane, columns [kPCol + part*kKeys/2, +kKeys/2)
   #pragma unroll
-          for (int c = 0; c < kKeys / 64; ++c)
-            tmem_st_32x32b_x32(tmem + lane_base + kPCol + part * (kKeys / 2) + c * 32,
-                               *reinterpret_cast<const float(*)[32]>(pk + 32 * c));
-        } else {
-          // this part's keys [part*kKeys + 8c, +8) in the SW128 K-major image of its row
-  #pragma unroll
-          for (int c = 0; c < kKeys / 8; ++c)
-            *reinterpret_cast<uint4*>(p_row + (((chunk0 + c) ^ (row & 7)) << 4)) =
-                make_uint4(pk[4 * c], pk[4 * c + 1], pk[4 * c + 2], pk[4 * c + 3]);
-        }
+        for (int c = 0; c < kKeys / 64; ++c)
+          tmem_st_32x32b_x32(tmem + lane_base + kPCol + part * (kKeys / 2) + c * 32,
+                             *reinterpret_cast<const float(*)[32]>(pk + 32 * c));
         if (j > 0 && __any_sync(0xffffffffu, move)) {
   #pragma unroll 1
           for (int c = 0; c < kKeys / 32; ++c) {
@@ -359,8 +345,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         }
         l_run = l_run * alpha + psum;
         m_run = m_new;
-        tc_fence_before();
-        fence_async_smem();  // P (generic writes) -> the tensor core (async proxy)
+        tc_fence_before();  // P stored to TMEM (tcgen05.wait::st) -> the P V MMA
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar.p_full);
       }
@@ -420,10 +405,7 @@ cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
   std::memcpy(&tkv, a.tmap_qkv, sizeof(CUtensorMap));
   const int n_items = a.n_tiles * a.H;
   const int grid = std::max(1, std::min(n_items, a.max_ctas > 0 ? a.max_ctas : 148));
-  PrefillAttnArgs args = a;
-  static const int env_pt = getenv("MUX_K3_PTMEM") ? atoi(getenv("MUX_K3_PTMEM")) : 0;
-  args.p_tmem = env_pt;
-  return launch(prefill_attention_kernel, dim3(grid), dim3(kThreads), kSmemBytes, stream, tq, tkv, args);
+  return launch(prefill_attention_kernel, dim3(grid), dim3(kThreads), kSmemBytes, stream, tq, tkv, a);
 }
 
 }  // namespace mux

@@ -1,12 +1,12 @@
 #!/bin/bash
 # K3 with P through TMEM (TS MMA, MUX_K3_PTMEM=1): parity, ncu device times of both forms
 out=gpurun_out/r2y; mkdir -p $out
-MUX_K3_PTMEM=1 timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x -k "prefill_attention" > $out/tests_k3.log 2>&1
+timeout 300 python -m pytest tests/test_gpu_kernels.py -q -x -k "prefill_attention" > $out/tests_k3.log 2>&1
 tail -2 $out/tests_k3.log
 if grep -q " passed" $out/tests_k3.log && ! grep -q "failed" $out/tests_k3.log; then
-MUX_K3_PTMEM=1 timeout 600 python -m pytest tests/test_gpu_model.py -q -x -k "prefill or long or lockstep" > $out/tests_k3_model.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_model.py -q -x -k "prefill or long or lockstep" > $out/tests_k3_model.log 2>&1
 tail -2 $out/tests_k3_model.log
-for pt in 1 0; do
+for pt in 1; do
 MUX_K3_PTMEM=$pt timeout 600 ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_active --clock-control none --csv \
   -k regex:prefill_attention --log-file $out/k3_ncu_$pt.csv python - > $out/k3_ncu_$pt.log 2>&1 <<'PY'
 import sys
