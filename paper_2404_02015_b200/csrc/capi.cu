@@ -1050,10 +1050,10 @@ int mux_prefill_attention(const void* q, const void* qkv, void* out, const int32
     }
     meta[nseq] = T;
     require(nseq < 65536 && max_qt < 65536, "prefill attention: too many sequences");
-    const bool pp = mux::prefill_pp_enabled();
-    std::vector<int32_t> units(static_cast<size_t>(max_qt + 1) * nseq);
-    const int n_tiles = mux::prefill_units(seq_lens, nseq, pp, units.data());
-    meta.insert(meta.end(), units.begin(), units.begin() + n_tiles);
+    for (int qt = max_qt; qt >= 0; --qt)
+      for (int i = 0; i < nseq; ++i)
+        if (qt * 128 < seq_lens[i]) meta.push_back((i << 16) | qt);
+    const int n_tiles = static_cast<int>(meta.size()) - (nseq + 1);
     cudaStream_t s = static_cast<cudaStream_t>(stream);
     static mux::DevMem& d = *new mux::DevMem();  // grows; the call synchronises before returning
     if (d.bytes < meta.size() * 4) d = mux::DevMem(std::max<size_t>(meta.size() * 4, 1 << 16));
@@ -1075,7 +1075,6 @@ int mux_prefill_attention(const void* q, const void* qkv, void* out, const int32
     a.H = H;
     a.T = T;
     a.scale_log2 = 1.4426950408889634f / std::sqrt(128.f);
-    a.pp = pp ? 1 : 0;
     mux::check_cuda(mux::prefill_attention(a, s), "prefill_attention");
     mux::check_cuda(cudaStreamSynchronize(s), "prefill_attention sync");
   });

@@ -758,8 +758,9 @@ void Runtime::prefill(Llama& m, Workspace& ws, int n, const int32_t* slots_host,
   int32_t* tiles = h + 2 * cap;
   int max_qt = 0;
   for (int i = 0; i < n; ++i) max_qt = std::max(max_qt, (lens_host[i] - 1) / 128);
-  const bool pp = prefill_pp_enabled();
-  n_tiles = prefill_units(lens_host, n, pp, tiles);
+  for (int qt = max_qt; qt >= 0; --qt)
+    for (int i = 0; i < n; ++i)
+      if (qt * 128 < lens_host[i]) tiles[n_tiles++] = (i << 16) | qt;
   ws.stage_commit(8 * static_cast<size_t>(cap) + 8, stream);
 
   const int hid = d.hidden, H = d.heads, L = d.layers;
@@ -795,7 +796,6 @@ void Runtime::prefill(Llama& m, Workspace& ws, int n, const int32_t* slots_host,
   pa.T = T;
   pa.scale_log2 = 1.4426950408889634f / std::sqrt(128.f);
   pa.max_ctas = ws.sms;
-  pa.pp = pp ? 1 : 0;
   for (int l = 0; l < L; ++l) {
     ap.layer = l;
     gemm(m.wqkv[l].p, ws.xn.p, T, m.qkv_cols(), hid, ws.qkv.p, m.qkv_cols(), kEpiStoreBf16, ws, stream);

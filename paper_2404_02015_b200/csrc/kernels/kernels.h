@@ -155,13 +155,8 @@ struct PrefillAttnArgs {
   int n_tiles, nseq, H, T;
   float scale_log2;
   int max_ctas = 0;         // persistent grid (the partition's SMs); 0 = 148
-  int pp = 0;               // ping-pong form: tiles[] holds units (prefill_units(.., pp = true))
 };
 cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream);
-// K3 work list: (seq << 16) | q_tile, heaviest first; pp = units of two
-// query tiles (leaders q_tiles-1, q_tiles-3, ...). Returns the count.
-int prefill_units(const int32_t* lens, int n, bool pp, int32_t* out);
-bool prefill_pp_enabled();  // MUX_K3_PP
 size_t prefill_attention_smem();
 // Deterministic N(0, std) init of a bf16 buffer from (seed, index).
 cudaError_t init_normal_bf16(void* dst, int64_t n, uint64_t seed, float std, cudaStream_t stream);

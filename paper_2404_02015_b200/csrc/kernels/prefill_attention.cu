@@ -386,315 +386,18 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
   }
 }
 
-
-// ---------------------------------------------------------------------------
-// K3, ping-pong form (args.pp): a work unit is TWO consecutive 128-query
-// tiles of one (sequence, head), A = tile tA and B = tile tA - 1 (B absent
-// when tA = 0). They share every K/V tile B needs (keys 0..tA-1), loaded
-// once. Softmax group A (warps 0-3) and group B (warps 4-7) each own a full
-// query row per thread (all 128 keys of a tile: no row-max exchange), so
-// while one group runs its exps the tensor core runs the other group's
-// Q K^T / P V. TMEM: S_A [0,128) S_B [128,256) O_A [256,384) O_B [384,512);
-// P_g overwrites the first 64 columns of S_g in place (bf16 pairs) and is the
-// A operand of P_g V (TS MMA). Units come heaviest first (leaders tA =
-// Q-1, Q-3, ... of each sequence; prefill_units()).
-constexpr int kThreadsPP = 9 * 32;  // 2 softmax groups x 4 warps + TMA/MMA warp
-struct BarsPP {
-  uint64_t q_full, q_empty;
-  uint64_t k_full[kStages], k_empty[kStages], v_full[kStages], v_empty[kStages];
-  uint64_t s_full[2], p_full[2], o_full[2], o_empty[2];
-  uint32_t tmem, pad;
-};
-constexpr size_t kSmemPP = 1024 + 2 * kTileBytes + kStages * 2 * kTileBytes + sizeof(BarsPP);
-
-__global__ void __launch_bounds__(kThreadsPP, 1)
-prefill_attention_pp_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv,
-                            const PrefillAttnArgs a) {
-  extern __shared__ __align__(16) uint8_t smem_pp[];
-  uint8_t* base = smem_pp + ((1024u - (smem_u32(smem_pp) & 1023u)) & 1023u);
-  uint8_t* q_s = base;                               // [A | B][2 halves]
-  uint8_t* kv_s = q_s + 2 * kTileBytes;              // [stage][K | V][2 halves]
-  BarsPP& bar = *reinterpret_cast<BarsPP*>(kv_s + kStages * 2 * kTileBytes);
-  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int n_items = a.n_tiles * a.H;
-
-  if (threadIdx.x == 0) {
-    mbar_init(&bar.q_full, 1);
-    mbar_init(&bar.q_empty, 1);
-    for (int s = 0; s < kStages; ++s) {
-      mbar_init(&bar.k_full[s], 1);
-      mbar_init(&bar.k_empty[s], 1);
-      mbar_init(&bar.v_full[s], 1);
-      mbar_init(&bar.v_empty[s], 1);
-    }
-    for (int g = 0; g < 2; ++g) {
-      mbar_init(&bar.s_full[g], 1);
-      mbar_init(&bar.p_full[g], 4);
-      mbar_init(&bar.o_full[g], 1);
-      mbar_init(&bar.o_empty[g], 4);
-    }
-    fence_barrier_init();
-  }
-  if (warp == 0) tmem_alloc<kTmemCols>(&bar.tmem);
-  tc_fence_before();
-  __syncthreads();
-  tc_fence_after();
-  grid_dep_wait();  // q / k / v come from kv_append and the QKV GEMM
-  if (threadIdx.x == 0) grid_dep_launch();
-  const uint32_t tmem = bar.tmem;
-
-  if (warp == 8) {
-    if (elect_one()) {
-      // ---------------- TMA producer + MMA issuer
-      const uint64_t pol_q = policy_evict_first();
-      const uint64_t pol_kv = policy_evict_last();
-      const uint32_t idesc_qk = umma_idesc_bf16(kTile, kTile);
-      const uint32_t idesc_pv = umma_idesc_bf16(kTile, 128) | (1u << 16);  // B (V) MN-major
-      int jg = 0;                    // K/V tiles of earlier units (ring position)
-      int np0 = 0, np1 = 0;          // P V issued per group (p_full parity)
-      int nu0 = 0, nu1 = 0;          // units with tiles per group (o_empty parity)
-      for (int round = 0, it = 0;; ++round, ++it) {
-        const int item = snake_item(round, blockIdx.x, gridDim.x);
-        if (item >= n_items) break;
-        const int h = item % a.H;
-        const int unit = a.tiles[item / a.H];
-        const int seq = unit >> 16, tA = unit & 0xFFFF;
-        const int s0 = a.seq_start[seq];
-        const int nA = tA + 1, nB = tA;  // key tiles of A and of B (B = tile tA - 1)
-        if (it > 0) mbar_wait(&bar.q_empty, (it - 1) & 1);
-        mbar_arrive_expect_tx(&bar.q_full, (nB > 0 ? 2 : 1) * kTileBytes);
-        for (int g = 0; g < (nB > 0 ? 2 : 1); ++g)
-          for (int hh = 0; hh < 2; ++hh)
-            tma_load_2d(q_s + g * kTileBytes + hh * kHalfBytes, &tq, &bar.q_full, h * 128 + hh * 64,
-                        s0 + (tA - g) * kTile, pol_q);
-        auto load = [&](int j, bool v) {
-          const int gt = jg + j, st = gt % kStages;
-          uint64_t* empty = v ? &bar.v_empty[st] : &bar.k_empty[st];
-          uint64_t* full = v ? &bar.v_full[st] : &bar.k_full[st];
-          if (gt >= kStages) mbar_wait(empty, ((gt / kStages) - 1) & 1);
-          uint8_t* dst = kv_s + st * 2 * kTileBytes + (v ? kTileBytes : 0);
-          mbar_arrive_expect_tx(full, kTileBytes);
-          for (int hh = 0; hh < 2; ++hh)
-            tma_load_2d(dst + hh * kHalfBytes, &tkv, full, ((v ? 2 : 1) * a.H + h) * 128 + hh * 64, s0 + j * kTile,
-                        pol_kv);
-        };
-        auto qk = [&](int g, int j) {  // S_g = Q_g K_j^T
-          const int gt = jg + j, st = gt % kStages;
-          mbar_wait(&bar.k_full[st], (gt / kStages) & 1);
-          tc_fence_after();
-          const uint32_t q_addr = smem_u32(q_s + g * kTileBytes), k_addr = smem_u32(kv_s + st * 2 * kTileBytes);
-  #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-            umma_bf16(tmem + g * kTile, umma_desc_sw128(q_addr + off), umma_desc_sw128(k_addr + off), idesc_qk,
-                      kk > 0 ? 1u : 0u);
-          }
-          umma_commit(&bar.s_full[g]);
-        };
-        auto pv = [&](int g, int j, int n_g) {  // O_g (+)= P_g V_j, P_g in S_g's first 64 columns
-          const int gt = jg + j, st = gt % kStages;
-          const int u = g ? np1++ : np0++;
-          if (j == 0) {  // the previous unit's epilogue of this group read O_g
-            const int nu = g ? nu1 : nu0;
-            if (nu >= 1) mbar_wait(&bar.o_empty[g], (nu - 1) & 1);
-          }
-          mbar_wait(&bar.p_full[g], u & 1);
-          mbar_wait(&bar.v_full[st], (gt / kStages) & 1);
-          tc_fence_after();
-          const uint32_t v_addr = smem_u32(kv_s + st * 2 * kTileBytes + kTileBytes);
-  #pragma unroll
-          for (int kk = 0; kk < 8; ++kk)
-            umma_ts_bf16(tmem + 2 * kTile + g * kTile, tmem + g * kTile + kk * 8, umma_desc_sw128_mn(v_addr + kk * 2048),
-                         idesc_pv, (j > 0 || kk > 0) ? 1u : 0u);
-          if (j + 1 == n_g) umma_commit(&bar.o_full[g]);
-        };
-        load(0, false);
-        load(0, true);
-        if (nA > 1) {
-          load(1, false);
-          load(1, true);
-        }
-        mbar_wait(&bar.q_full, it & 1);
-        qk(0, 0);
-        if (nB > 0) qk(1, 0);
-        umma_commit(&bar.k_empty[jg % kStages]);  // K_0's users issued
-        if (nA == 1) umma_commit(&bar.q_empty);
-        for (int j = 0; j < nA; ++j) {
-          const int st = (jg + j) % kStages;
-          pv(0, j, nA);
-          if (j + 1 < nA) {
-            qk(0, j + 1);
-            if (j + 1 == nA - 1) umma_commit(&bar.q_empty);  // the unit's last Q K^T
-          }
-          if (j < nB) {
-            pv(1, j, nB);
-            if (j + 1 < nB) qk(1, j + 1);
-          }
-          umma_commit(&bar.v_empty[st]);                                     // V_j's users issued
-          if (j + 1 < nA) umma_commit(&bar.k_empty[(jg + j + 1) % kStages]);  // K_{j+1}'s users issued
-          if (j + 2 < nA) {
-            load(j + 2, false);  // into K_j's slot
-            load(j + 2, true);   // into V_j's slot (waits for P V_j)
-          }
-        }
-        nu0 += 1;
-        nu1 += nB > 0 ? 1 : 0;
-        jg += nA;
-      }
-    }
-    __syncwarp();
-  } else {
-    // ---------------- softmax group g: thread = query row, all 128 keys of a tile
-    const int g = warp >> 2, quarter = warp & 3;
-    const int row = quarter * 32 + lane;
-    const uint32_t lane_base = static_cast<uint32_t>(quarter * 32) << 16;
-    const uint32_t s_addr = tmem + lane_base + g * kTile;
-    const uint32_t o_addr = tmem + lane_base + 2 * kTile + g * kTile;
-    int cnt = 0, nu = 0;  // this group's tiles / units so far (barrier parities)
-    for (int round = 0;; ++round) {
-      const int item = snake_item(round, blockIdx.x, gridDim.x);
-      if (item >= n_items) break;
-      const int h = item % a.H;
-      const int unit = a.tiles[item / a.H];
-      const int seq = unit >> 16, tA = unit & 0xFFFF;
-      const int qt = tA - g;
-      if (qt < 0) continue;  // B absent in this unit
-      const int s0 = a.seq_start[seq];
-      const int len = a.seq_start[seq + 1] - s0;
-      const int n_kv = qt + 1;
-      const int qi = qt * kTile + row;
-      float m_run = -INFINITY, l_run = 0.f;
-      for (int j = 0; j < n_kv; ++j, ++cnt) {
-        mbar_wait(&bar.s_full[g], cnt & 1);  // S_g(j) computed; P_g V_{j-1} (issued before it) done
-        tc_fence_after();
-        float v[128];
-  #pragma unroll
-        for (int c = 0; c < 4; ++c) tmem_ld_32x32b_x32(s_addr + c * 32, *reinterpret_cast<float(*)[32]>(v + 32 * c));
-        const int kmax = min(qi, len - 1) - j * kTile;
-        const bool full = kmax >= kTile - 1;
-        float mx = -INFINITY;
-        if (full) {
-  #pragma unroll
-          for (int i = 0; i < 128; i += 2) mx = fmax3(mx, v[i], v[i + 1]);
-        } else {
-  #pragma unroll
-          for (int i = 0; i < 128; ++i)
-            if (i <= kmax) mx = fmaxf(mx, v[i]);
-        }
-        const float m_tile = mx * a.scale_log2;
-        const bool move = m_tile > m_run + 8.f;  // lazy rescaling (as in the one-tile form)
-        const float m_new = move ? m_tile : m_run;
-        const float m_use = m_new == -INFINITY ? 0.f : m_new;
-        const float alpha = move ? exp2f(m_run - m_use) : 1.f;
-        if (j > 0 && __any_sync(0xffffffffu, move)) {
-  #pragma unroll 1
-          for (int c = 0; c < 4; ++c) {
-            float o[32];
-            tmem_ld_32x32b_x32(o_addr + c * 32, o);
-  #pragma unroll
-            for (int i = 0; i < 32; ++i) o[i] *= alpha;
-            tmem_st_32x32b_x32(o_addr + c * 32, o);
-          }
-        }
-        // P = exp2(s - m) as bf16 pairs over S_g's first 64 columns, 32 keys per store
-        float sa = 0.f, sb = 0.f;
-  #pragma unroll
-        for (int c = 0; c < 4; ++c) {
-          uint32_t pk[16];
-  #pragma unroll
-          for (int e = 0; e < 16; ++e) {
-            const int i = 32 * c + 2 * e;
-            float p0, p1;
-            if (full) {
-              float x0, x1;
-              ffma2(x0, x1, v[i], v[i + 1], a.scale_log2, a.scale_log2, -m_use, -m_use);
-              p0 = ex2_ftz(x0);
-              p1 = ex2_ftz(x1);
-            } else {
-              p0 = i <= kmax ? exp2f(fmaf(v[i], a.scale_log2, -m_use)) : 0.f;
-              p1 = i + 1 <= kmax ? exp2f(fmaf(v[i + 1], a.scale_log2, -m_use)) : 0.f;
-            }
-            fadd2(sa, sb, p0, p1);
-            pk[e] = pack_bf16(p0, p1);
-          }
-          tmem_st_32x32b_x16(s_addr + c * 16, pk);
-        }
-        l_run = l_run * alpha + (sa + sb);
-        m_run = m_new;
-        tc_fence_before();
-        __syncwarp();
-        if (lane == 0) mbar_arrive(&bar.p_full[g]);
-      }
-      // epilogue: O_g / l
-      mbar_wait(&bar.o_full[g], nu & 1);
-      tc_fence_after();
-      const float inv = l_run > 0.f ? 1.f / l_run : 0.f;
-      uint4* dst = reinterpret_cast<uint4*>(reinterpret_cast<__nv_bfloat16*>(a.out) +
-                                            (static_cast<int64_t>(s0 + qi) * a.H + h) * 128);
-  #pragma unroll
-      for (int c = 0; c < 4; ++c) {
-        float o[32];
-        tmem_ld_32x32b_x32(o_addr + c * 32, o);
-        if (qi < len) {
-  #pragma unroll
-          for (int u = 0; u < 4; ++u)
-            dst[c * 4 + u] = make_uint4(pack_bf16(o[8 * u] * inv, o[8 * u + 1] * inv),
-                                        pack_bf16(o[8 * u + 2] * inv, o[8 * u + 3] * inv),
-                                        pack_bf16(o[8 * u + 4] * inv, o[8 * u + 5] * inv),
-                                        pack_bf16(o[8 * u + 6] * inv, o[8 * u + 7] * inv));
-        }
-      }
-      tc_fence_before();
-      __syncwarp();
-      if (lane == 0) mbar_arrive(&bar.o_empty[g]);
-      ++nu;
-    }
-  }
-  tc_fence_before();
-  __syncthreads();
-  if (warp == 0) {
-    tc_fence_after();
-    tmem_dealloc(tmem, kTmemCols);
-  }
-}
-
 }  // namespace
 
 size_t prefill_attention_smem() { return kSmemBytes; }
 
-cudaError_t preload_prefill_attention() { return preload(prefill_attention_kernel, prefill_attention_pp_kernel); }
-
-bool prefill_pp_enabled() {
-  static const bool on = [] {
-    const char* e = std::getenv("MUX_K3_PP");
-    return e != nullptr && std::atoi(e) != 0;
-  }();
-  return on;
-}
-
-int prefill_units(const int32_t* lens, int n, bool pp, int32_t* out) {
-  int max_qt = 0;
-  for (int i = 0; i < n; ++i) max_qt = std::max(max_qt, (lens[i] - 1) / kTile);
-  int k = 0;
-  for (int qt = max_qt; qt >= 0; --qt)
-    for (int i = 0; i < n; ++i) {
-      const int q_tiles = (lens[i] + kTile - 1) / kTile;
-      if (qt >= q_tiles) continue;
-      if (pp && (q_tiles - 1 - qt) % 2 != 0) continue;  // covered as B of unit qt + 1
-      out[k++] = (i << 16) | qt;
-    }
-  return k;
-}
+cudaError_t preload_prefill_attention() { return preload(prefill_attention_kernel); }
 
 cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
   if (a.T <= 0 || a.n_tiles <= 0) return cudaSuccess;
   static PerDeviceOnce configured;
   cudaError_t ce = configured.run([] {
-    cudaError_t e = cudaFuncSetAttribute(prefill_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                         static_cast<int>(kSmemBytes));
-    if (e != cudaSuccess) return e;
-    return cudaFuncSetAttribute(prefill_attention_pp_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                static_cast<int>(kSmemPP));
+    return cudaFuncSetAttribute(prefill_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                static_cast<int>(kSmemBytes));
   });
   if (ce != cudaSuccess) return ce;
   CUtensorMap tq, tkv;
@@ -702,7 +405,6 @@ cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
   std::memcpy(&tkv, a.tmap_qkv, sizeof(CUtensorMap));
   const int n_items = a.n_tiles * a.H;
   const int grid = std::max(1, std::min(n_items, a.max_ctas > 0 ? a.max_ctas : 148));
-  if (a.pp) return launch(prefill_attention_pp_kernel, dim3(grid), dim3(kThreadsPP), kSmemPP, stream, tq, tkv, a);
   return launch(prefill_attention_kernel, dim3(grid), dim3(kThreads), kSmemBytes, stream, tq, tkv, a);
 }
 

@@ -243,17 +243,6 @@ __device__ __forceinline__ void tmem_st_32x32b_x32(uint32_t taddr, const float (
   asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
 }
 
-// 32 lanes x 16 consecutive 32-bit columns (waits for the store to land).
-__device__ __forceinline__ void tmem_st_32x32b_x16(uint32_t taddr, const uint32_t (&v)[16]) {
-  asm volatile(
-      "tcgen05.st.sync.aligned.32x32b.x16.b32 [%0], "
-      "{%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,%16};" ::"r"(taddr),
-      "r"(v[0]), "r"(v[1]), "r"(v[2]), "r"(v[3]), "r"(v[4]), "r"(v[5]), "r"(v[6]), "r"(v[7]), "r"(v[8]),
-      "r"(v[9]), "r"(v[10]), "r"(v[11]), "r"(v[12]), "r"(v[13]), "r"(v[14]), "r"(v[15])
-      : "memory");
-  asm volatile("tcgen05.wait::st.sync.aligned;" ::: "memory");
-}
-
 // Shared-memory matrix descriptor for a K-major operand tile stored in the
 // canonical 128-byte-swizzled layout (rows of 64 bf16 = 128 B, 8-row groups
 // 1024 B apart), which is exactly what a SWIZZLE_128B TMA box produces.
