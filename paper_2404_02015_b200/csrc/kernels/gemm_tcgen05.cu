@@ -24,6 +24,13 @@
 // higher index that never wait on it, so the scheme cannot deadlock even
 // when the grid is not fully co-resident.
 //
+// Decode forms (plan()): token tiles of 65..256 run on CTA PAIRS (template
+// PAIR: clusters of two, one tcgen05.mma.cta_group::2 of M = 256 per
+// k-block, each CTA staging its 128 weight rows and half the token tile);
+// single-CTA launches with many units per CTA stage two 128-row weight tiles
+// per activation stage (st = 2); token tiles of <= 64 run two CTAs per SM
+// (EG = 1) so the next projection's CTAs stream under PDL.
+//
 // Warp roles: warp 0 = TMA producer, warp 1 = MMA issuer (one elected lane),
 // warp 2 = TMEM allocator, warps 4..7 = epilogue. Accumulators are double
 // buffered in TMEM so the epilogue of one segment overlaps the MMAs of the
