@@ -67,10 +67,7 @@ __global__ void scatter_last_tok(int32_t* last_tok, const int32_t* slots, const 
   if (i < n) last_tok[slots[i]] = tokens[i];
 }
 
-int gemm_n_tile(int M) {
-  int n = ((M + 15) / 16) * 16;
-  return std::max(16, std::min(256, n));
-}
+int gemm_n_tile(int M) { return gemm_pick_n_tile(M); }
 
 }  // namespace
 
@@ -370,7 +367,7 @@ void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void
   g.w_tiled = w_tiled;
   g.tmap_x = act_tmap(x, rows, K, gemm_n_tile(M));
   if (M > 256) g.tmap_x128 = act_tmap(x, rows, K, 128);  // 2-SM prefill path (gemm_2sm.cu)
-  if (M <= 256 && gemm_n_tile(M) > 64 && w_tiled != nullptr) {  // decode CTA-pair mode (MUX_GEMM_PAIR)
+  if (gemm_n_tile(M) > 64 && w_tiled != nullptr) {  // CTA-pair mode (MUX_GEMM_PAIR)
     g.tmap_x_half = act_tmap(x, rows, K, gemm_n_tile(M) / 2);
     g.tmap_w_rows = w_rows_tmap(w_tiled, N, K);
   }

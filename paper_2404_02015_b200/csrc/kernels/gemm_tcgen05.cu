@@ -767,8 +767,11 @@ bool make_tmap_gemm_out(void* tmap_out, const void* out, int epi, int M, int N, 
   return make_tmap_2d(tmap_out, out, fp32, static_cast<uint64_t>(M), cols, stride, 32, silu ? kBM / 2 : kBM);
 }
 
+// Token-tile rows: one tile up to 256 tokens; beyond, the fewest tiles of
+// <= 256 with the tokens split evenly (322 -> 2 x 176, not 256 + 66).
 int gemm_pick_n_tile(int M) {
-  int n = ((M + 15) / 16) * 16;
+  const int tiles = std::max(1, (M + 255) / 256);
+  int n = (((M + tiles - 1) / tiles + 15) / 16) * 16;
   if (n > 256) n = 256;
   if (n < 16) n = 16;
   return n;
@@ -825,12 +828,14 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   r.K = a.K;
   r.ldo = a.ldo;
   r.n_tile = gemm_pick_n_tile(a.M);
-  // CTA pairs (PAIR instantiation; default, MUX_GEMM_PAIR=0 off): decode token tiles of
-  // 65..256 (one CTA per SM), an even number of 128-row weight tiles, the
-  // half-box activation map and the row view of the tiled weights given.
+  // CTA pairs (PAIR instantiation; default, MUX_GEMM_PAIR=0 off): token
+  // tiles of 65..256 rows (one CTA per SM; several token tiles for prefill
+  // shapes the 256 x 256 pair tiles of gemm_2sm would leave unbalanced), an
+  // even number of 128-row weight tiles, the half-box activation map and the
+  // row view of the tiled weights given.
   static const int env_pair = getenv("MUX_GEMM_PAIR") ? atoi(getenv("MUX_GEMM_PAIR")) : 1;
   const int w_tiles0 = (a.N + kBM - 1) / kBM;
-  r.pair = env_pair != 0 && r.n_tile > 64 && a.M <= 256 && w_tiles0 % 2 == 0 && a.tmap_x_half != nullptr &&
+  r.pair = env_pair != 0 && r.n_tile > 64 && w_tiles0 % 2 == 0 && a.tmap_x_half != nullptr &&
                    a.tmap_w_rows != nullptr && a.n_peers == 0 && a.n_signal == 0 && (a.grid <= 0 || a.grid >= 2)
                ? 1
                : 0;
