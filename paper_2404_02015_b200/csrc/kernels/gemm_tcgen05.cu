@@ -767,11 +767,14 @@ bool make_tmap_gemm_out(void* tmap_out, const void* out, int epi, int M, int N, 
   return make_tmap_2d(tmap_out, out, fp32, static_cast<uint64_t>(M), cols, stride, 32, silu ? kBM / 2 : kBM);
 }
 
-// Token-tile rows: one tile up to 256 tokens; beyond, the fewest tiles of
-// <= 256 with the tokens split evenly (322 -> 2 x 176, not 256 + 66).
+// Token-tile rows: one tile up to 256 tokens (a multiple of 16); beyond, the
+// fewest tiles of <= 256 with the tokens split evenly, in multiples of 32 --
+// the epilogue's chunk -- so no chunk crosses into the next token tile
+// (322 -> 2 x 192 instead of 256 + 66).
 int gemm_pick_n_tile(int M) {
   const int tiles = std::max(1, (M + 255) / 256);
-  int n = (((M + tiles - 1) / tiles + 15) / 16) * 16;
+  const int per = (M + tiles - 1) / tiles;
+  int n = tiles == 1 ? ((per + 15) / 16) * 16 : ((per + 31) / 32) * 32;
   if (n > 256) n = 256;
   if (n < 16) n = 16;
   return n;
