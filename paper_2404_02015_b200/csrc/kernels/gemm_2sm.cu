@@ -236,8 +236,9 @@ bool gemm_2sm_eligible(const GemmArgs& a) {
   static const int env = getenv("MUX_GEMM_2SM") ? atoi(getenv("MUX_GEMM_2SM")) : 1;
   // Below min_m tokens the stream-K CTA-pair path of gemm_tcgen05.cu (token
   // tiles split evenly, every SM busy) wins over data-parallel 256 x 256 pair
-  // tiles, whose count is too small to balance (MUX_GEMM_2SM_MIN_M).
-  static const int min_m = getenv("MUX_GEMM_2SM_MIN_M") ? atoi(getenv("MUX_GEMM_2SM_MIN_M")) : 512;
+  // tiles, whose count is too small to balance (MUX_GEMM_2SM_MIN_M; measured
+  // crossover ~1000 tokens on the 7B/13B shapes, profiles/r02_gemm_2sm_min_m.txt).
+  static const int min_m = getenv("MUX_GEMM_2SM_MIN_M") ? atoi(getenv("MUX_GEMM_2SM_MIN_M")) : 1000;
   if (a.N % 256 != 0 || a.M <= std::max(256, min_m)) return false;
   // Data-parallel pair tiles: when the last round would leave most pairs idle
   // (e.g. 80 tiles on 74 pairs), the single-SM stream-K path balances better.
