@@ -46,6 +46,19 @@ def test_max_over_ranks_gloo():
     _run(_max_body, 2)
 
 
+def _sum_gather_body(rank, world):
+    # bench.py --placement: every rank's unit adds its tokens / kernel time,
+    # an idle rank adds zeros, and rank 0 lists every rank's models
+    got = mesh.sum_over_ranks([float(10 * rank), 0.5])
+    assert got == [float(10 * sum(range(world))), 0.5 * world]
+    units = mesh.gather_objects({"models": ["7b"] * rank, "batch": 8 * rank})
+    assert units == [{"models": ["7b"] * r, "batch": 8 * r} for r in range(world)]
+
+
+def test_sum_and_gather_over_ranks_gloo():
+    _run(_sum_gather_body, 2)
+
+
 class _FakeUnit:
     def __init__(self, rank):
         self.rank = rank
