@@ -838,13 +838,16 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   // row view of the tiled weights given.
   static const int env_pair = getenv("MUX_GEMM_PAIR") ? atoi(getenv("MUX_GEMM_PAIR")) : 1;
   const int w_tiles0 = (a.N + kBM - 1) / kBM;
-  r.pair = env_pair != 0 && r.n_tile > 64 && w_tiles0 % 2 == 0 && a.tmap_x_half != nullptr &&
+  // (MUX_GEMM_PAIR_MIN_TILE: smallest token tile run on pairs; below it the
+  // two-CTAs-per-SM form keeps the next projection streaming under PDL)
+  static const int env_pair_min = getenv("MUX_GEMM_PAIR_MIN_TILE") ? atoi(getenv("MUX_GEMM_PAIR_MIN_TILE")) : 80;
+  r.pair = env_pair != 0 && r.n_tile >= std::max(32, env_pair_min) && w_tiles0 % 2 == 0 && a.tmap_x_half != nullptr &&
                    a.tmap_w_rows != nullptr && a.n_peers == 0 && a.n_signal == 0 && (a.grid <= 0 || a.grid >= 2)
                ? 1
                : 0;
   const int b_stage = (r.pair ? r.n_tile / 2 : r.n_tile) * kBK * 2;
   static const int env_dual = getenv("MUX_GEMM_DUAL") ? atoi(getenv("MUX_GEMM_DUAL")) : 1;
-  r.eg = (env_dual && r.n_tile <= 64) ? 1 : 2;
+  r.eg = (env_dual && r.n_tile <= 64 && !r.pair) ? 1 : 2;
   r.stages_b = r.pair ? 4 : (r.n_tile > 128 ? 2 : 3);
   // Debug overrides for pipeline-depth sweeps (scripts/gemm_micro.py).
   static const int env_sb = getenv("MUX_GEMM_SB") ? atoi(getenv("MUX_GEMM_SB")) : 0;
