@@ -1172,7 +1172,7 @@ int mux_gemm_bf16(const void* x, const void* w, int w_tiled, int M, int N, int K
     // prefill shapes with tiled weights may run on CTA pairs (gemm_2sm.cu)
     if (w_tiled && M > 256 && mux::make_tmap_bf16(tx128, x, M, K, static_cast<uint64_t>(K) * 2, 128)) g.tmap_x128 = tx128;
     // decode shapes with tiled weights may run on CTA pairs (MUX_GEMM_PAIR)
-    if (w_tiled && n_tile >= 32 &&
+    if (w_tiled && n_tile >= 16 &&
         mux::make_tmap_bf16(txh, x, M, K, static_cast<uint64_t>(K) * 2, n_tile / 2) &&
         mux::make_tmap_w_rows(twr, w, N, K)) {
       g.tmap_x_half = txh;

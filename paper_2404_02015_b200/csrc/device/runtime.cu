@@ -370,7 +370,7 @@ void Runtime::gemm(const void* w_tiled, const void* x, int M, int N, int K, void
   // CTA-pair mode (MUX_GEMM_PAIR). Not for tensor-parallel units: when the
   // ranks of a mesh share one GPU (the tests), a rank's rmsnorm_tp spinners
   // can leave no TPC with two free SMs for the peer's cluster launches.
-  if (gemm_n_tile(M) >= 32 && w_tiled != nullptr && !ws.tp) {
+  if (gemm_n_tile(M) >= 16 && w_tiled != nullptr && !ws.tp) {
     g.tmap_x_half = act_tmap(x, rows, K, gemm_n_tile(M) / 2);
     g.tmap_w_rows = w_rows_tmap(w_tiled, N, K);
   }

@@ -838,10 +838,11 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   // row view of the tiled weights given.
   static const int env_pair = getenv("MUX_GEMM_PAIR") ? atoi(getenv("MUX_GEMM_PAIR")) : 1;
   const int w_tiles0 = (a.N + kBM - 1) / kBM;
-  // (MUX_GEMM_PAIR_MIN_TILE: smallest token tile run on pairs; below it the
-  // two-CTAs-per-SM form keeps the next projection streaming under PDL)
-  static const int env_pair_min = getenv("MUX_GEMM_PAIR_MIN_TILE") ? atoi(getenv("MUX_GEMM_PAIR_MIN_TILE")) : 80;
-  r.pair = env_pair != 0 && r.n_tile >= std::max(32, env_pair_min) && w_tiles0 % 2 == 0 && a.tmap_x_half != nullptr &&
+  // (MUX_GEMM_PAIR_MIN_TILE: smallest token tile run on pairs, default 32:
+  // decode rounds at batch 32 / 64 run 11% faster on pairs than in the
+  // two-CTAs-per-SM form, profiles/r02_gemm_pair_small.txt)
+  static const int env_pair_min = getenv("MUX_GEMM_PAIR_MIN_TILE") ? atoi(getenv("MUX_GEMM_PAIR_MIN_TILE")) : 32;
+  r.pair = env_pair != 0 && r.n_tile >= std::max(16, env_pair_min) && w_tiles0 % 2 == 0 && a.tmap_x_half != nullptr &&
                    a.tmap_w_rows != nullptr && a.n_peers == 0 && a.n_signal == 0 && (a.grid <= 0 || a.grid >= 2)
                ? 1
                : 0;
