@@ -24,12 +24,12 @@
 // higher index that never wait on it, so the scheme cannot deadlock even
 // when the grid is not fully co-resident.
 //
-// Decode forms (plan()): token tiles of 65..256 run on CTA PAIRS (template
+// Decode forms (plan()): token tiles of 16..256 run on CTA PAIRS (template
 // PAIR: clusters of two, one tcgen05.mma.cta_group::2 of M = 256 per
 // k-block, each CTA staging its 128 weight rows and half the token tile);
 // single-CTA launches with many units per CTA stage two 128-row weight tiles
-// per activation stage (st = 2); token tiles of <= 64 run two CTAs per SM
-// (EG = 1) so the next projection's CTAs stream under PDL.
+// per activation stage (st = 2); token tiles of <= 64 that pairs cannot take
+// run two CTAs per SM (EG = 1) so the next projection's CTAs stream under PDL.
 //
 // Warp roles: warp 0 = TMA producer, warp 1 = MMA issuer (one elected lane),
 // warp 2 = TMEM allocator, warps 4..7 = epilogue. Accumulators are double
@@ -838,10 +838,12 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   // row view of the tiled weights given.
   static const int env_pair = getenv("MUX_GEMM_PAIR") ? atoi(getenv("MUX_GEMM_PAIR")) : 1;
   const int w_tiles0 = (a.N + kBM - 1) / kBM;
-  // (MUX_GEMM_PAIR_MIN_TILE: smallest token tile run on pairs, default 32:
-  // decode rounds at batch 32 / 64 run 11% faster on pairs than in the
-  // two-CTAs-per-SM form, profiles/r02_gemm_pair_small.txt)
-  static const int env_pair_min = getenv("MUX_GEMM_PAIR_MIN_TILE") ? atoi(getenv("MUX_GEMM_PAIR_MIN_TILE")) : 32;
+  // (MUX_GEMM_PAIR_MIN_TILE: smallest token tile run on pairs, default 16 =
+  // every decode tile: decode rounds at batch 8-64 run 11-14% faster on pairs
+  // than in the two-CTAs-per-SM form, profiles/r02_gemm_pair_small.txt; that
+  // form remains for launches pairs cannot take: odd weight-tile counts,
+  // tensor-parallel units, weights without the tiled layout)
+  static const int env_pair_min = getenv("MUX_GEMM_PAIR_MIN_TILE") ? atoi(getenv("MUX_GEMM_PAIR_MIN_TILE")) : 16;
   r.pair = env_pair != 0 && r.n_tile >= std::max(16, env_pair_min) && w_tiles0 % 2 == 0 && a.tmap_x_half != nullptr &&
                    a.tmap_w_rows != nullptr && a.n_peers == 0 && a.n_signal == 0 && (a.grid <= 0 || a.grid >= 2)
                ? 1
