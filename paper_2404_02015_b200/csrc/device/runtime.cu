@@ -560,12 +560,10 @@ void Runtime::decode(Llama& m, Workspace& ws, int n, const int32_t* slots_host, 
   int max_ctx = 0;
   for (int i = 0; i < n; ++i) max_ctx = std::max(max_ctx, ctx_host[i]);
   const int max_rows_req = (max_ctx + 15) / 16;
-  // KV splits: enough CTAs to fill the GPU a few times over (MUX_K1_FILL
-  // CTAs per SM, default 4).
-  static const int k1_fill = getenv("MUX_K1_FILL") ? std::max(1, atoi(getenv("MUX_K1_FILL"))) : 4;
+  // KV splits: enough CTAs to fill the GPU a few times over.
   int splits = 1;
   // (the last split merges in-kernel, so small batches can afford ~2 rows per split)
-  while (splits < kMaxKvSplits && n * H * splits < k1_fill * ws.sms && (max_rows_req + splits * 2 - 1) / (splits * 2) >= 2)
+  while (splits < kMaxKvSplits && n * H * splits < 4 * ws.sms && (max_rows_req + splits * 2 - 1) / (splits * 2) >= 2)
     splits *= 2;
   while ((max_rows_req + splits - 1) / splits > decode_attention_max_rows_per_split()) splits *= 2;
   if (splits > kMaxKvSplits)  // the split scratch holds kMaxKvSplits per (member, head)
