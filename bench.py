@@ -298,7 +298,7 @@ def run_ours(args, rank, world, local_rank):
     def step(tokens=None, outs=None, whole_gpu=False):
         # one ADBS decode round: +1 token per member (BlockPool), then the jobs
         for li in issue_order:
-            if not all(r.ok for r in pool.alloc_n(li, ids_c[li], 1, False)):
+            if not pool.alloc_n_ok(li, ids_c[li], 1, False):
                 raise RuntimeError("pool exhausted")
             unit.decode(li, ids[li], tokens=None if tokens is None else tokens[li],
                         out=None if outs is None else outs[li], partition=0 if whole_gpu else 1 + (0 if args.serial else li),

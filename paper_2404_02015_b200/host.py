@@ -161,6 +161,15 @@ class BlockPool:
         check(lib.mux_pool_alloc_n(self._h, llm, n, ids, add_tokens, 1 if enforce_quota else 0, res))
         return [AllocResult(r == ALLOC_OK, _ERR[r]) for r in res[:n]]
 
+    def alloc_n_ok(self, llm, request_ids, add_tokens, enforce_quota) -> bool:
+        """alloc_n() reporting only whether every member's allocation
+        succeeded (the decode round's hot path: no per-member result objects)."""
+        ids = request_ids if isinstance(request_ids, C.Array) else (C.c_int64 * len(request_ids))(*request_ids)
+        n = len(ids)
+        res = (C.c_int * max(n, 1))()
+        check(lib.mux_pool_alloc_n(self._h, llm, n, ids, add_tokens, 1 if enforce_quota else 0, res))
+        return not any(res[:n])
+
     def free_request(self, llm, request_id):
         check(lib.mux_pool_free_request(self._h, llm, request_id))
 
