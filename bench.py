@@ -295,14 +295,22 @@ def run_ours(args, rank, world, local_rank):
         p + d for p, o, d in batches[li]) * specs[li].kv_bytes_per_token()))
     ctx0 = [sum(pool.request_tokens(li, r) for r in ids[li]) for li in range(len(specs))]
 
-    def step(tokens=None, outs=None, whole_gpu=False):
-        # one ADBS decode round: +1 token per member (BlockPool), then the jobs
+    def alloc_round():
+        # one ADBS decode round's allocation: +1 token per member (BlockPool)
         for li in issue_order:
             if not pool.alloc_n_ok(li, ids_c[li], 1, False):
                 raise RuntimeError("pool exhausted")
+
+    def issue_round(tokens=None, outs=None, whole_gpu=False):
+        for li in issue_order:
             unit.decode(li, ids[li], tokens=None if tokens is None else tokens[li],
                         out=None if outs is None else outs[li], partition=0 if whole_gpu else 1 + (0 if args.serial else li),
                         ids_c=ids_c[li])
+
+    def step(tokens=None, outs=None, whole_gpu=False):
+        # one ADBS decode round: the allocation, then the jobs
+        alloc_round()
+        issue_round(tokens, outs, whole_gpu)
 
     # clocks are sampled from the warm-up on (the timed region alone is only
     # a few hundred ms): idle samples before the first step are dropped
@@ -379,8 +387,12 @@ def run_ours(args, rank, world, local_rank):
         unit.sync()
     unit.sync()
     t0 = time.perf_counter()
+    if args.e2e_steps:
+        alloc_round()
     for i in range(args.e2e_steps):
-        step(tokens=pinned_in, outs=pinned_out)
+        issue_round(tokens=pinned_in, outs=pinned_out)
+        if i + 1 < args.e2e_steps:
+            alloc_round()  # the next round's KV rows while this one runs (host state only)
         unit.sync()  # the step's result is on the host before the next step is issued
         for li in range(len(specs)):
             pinned_in[li][:] = pinned_out[li]
