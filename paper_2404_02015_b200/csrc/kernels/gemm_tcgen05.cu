@@ -303,14 +303,10 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
     if constexpr (PAIR) {
       // both CTAs' 16 KiB count on the leader's barrier; the tiled weights
       // are a [tiles * 128][64] tensor (rows already in the SW128 image)
-      // (st = 2: a 512-row unit; MMA j covers tiles 4u + 2j (rank 0) and
-      // 4u + 2j + 1 (rank 1), this CTA's slot j)
-      if (rank == 0) mbar_arrive_expect_tx(&full_a[ps], 2u * static_cast<uint32_t>(a_stage_bytes));
-      for (int j = 0; j < r.st; ++j) {
-        const int mt = 2 * (pm * r.st + j) + rank;
-        tma_load_2d_pair(a_st + ps * a_stage_bytes + j * kAStageBytes, &tw, map_to_rank(smem_u32(&full_a[ps]), 0), 0,
-                         (mt * r.kb + pkb) * kBM, wpol);
-      }
+      if (rank == 0) mbar_arrive_expect_tx(&full_a[ps], 2u * kAStageBytes);
+      const int mt = 2 * pm + rank;
+      tma_load_2d_pair(a_st + ps * kAStageBytes, &tw, map_to_rank(smem_u32(&full_a[ps]), 0), 0,
+                       (mt * r.kb + pkb) * kBM, wpol);
       if (++ps == SA) {
         ps = 0;
         ++pround;
@@ -442,11 +438,10 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
           const uint32_t a_addr = smem_u32(a_st + sa * a_stage_bytes);
           const uint32_t b_addr = smem_u32(b_st + sb * b_stage_bytes);
           if constexpr (PAIR) {
-            for (int j = 0; j < r.st; ++j)
 #pragma unroll
-              for (int kk = 0; kk < kBK / 16; ++kk)
-                umma2_bf16(acc + static_cast<uint32_t>(j * r.n_tile), umma_desc_sw128(a_addr + j * kAStageBytes + kk * 32),
-                           umma_desc_sw128(b_addr + kk * 32), idesc, (kbi != kb0 || kk != 0) ? 1u : 0u);
+            for (int kk = 0; kk < kBK / 16; ++kk)
+              umma2_bf16(acc, umma_desc_sw128(a_addr + kk * 32), umma_desc_sw128(b_addr + kk * 32), idesc,
+                         (kbi != kb0 || kk != 0) ? 1u : 0u);
             umma2_commit_both(&empty_a[sa]);
             umma2_commit_both(&empty_b[sb]);
             if (kbi == kb1 - 1) umma2_commit_both(&tm_full[b]);
@@ -569,7 +564,7 @@ gemm_tn_kernel(const __grid_constant__ CUtensorMap tw, const __grid_constant__ C
       for (int k = eg; k < nchunk; k += kEpiGroups) {
         const int tj = k / nct;                  // weight tile of the unit
         const int cc = (k - tj * nct) * 32;      // token offset inside the tile
-        const int mrow = PAIR ? 2 * (m * r.st + tj) + rank : m * r.st + tj;  // 128-row output tile
+        const int mrow = PAIR ? 2 * m + rank : m * r.st + tj;  // 128-row output tile
         const bool stamp = r.timing != nullptr && lead0 && seg_last && k < 4;
         float v[32];
         tmem_ld_32x32b_x32(acc + tj * r.n_tile + cc, v);
@@ -879,29 +874,21 @@ static void plan(const GemmArgs& a, GemmRun& r, int& grid_out, size_t& smem_out)
   // fixup) or >= 48 (fixup epilogues). MUX_GEMM_ST=1 off, =2 forced.
   static const int env_st = getenv("MUX_GEMM_ST") ? atoi(getenv("MUX_GEMM_ST")) : 0;
   const int w_tiles = (a.N + kBM - 1) / kBM;
-  // In pair mode a unit of two tiles per CTA is 512 rows (MUX_GEMM_PAIR_ST=1
-  // enables it; thresholds counted per pair).
-  static const int env_pair_st = getenv("MUX_GEMM_PAIR_ST") ? atoi(getenv("MUX_GEMM_PAIR_ST")) : 0;
-  // (pairs: residual epilogues only -- a fixer's A ring holds one partner's
-  // 8-chunk partial, which would cap the grid at one participant per unit)
-  const bool st_ok = r.eg == 2 && a.M <= 128 &&
-                     (r.pair ? (env_pair_st != 0 && w_tiles % 4 == 0 && a.epi == Epilogue::kResidualAddF32)
-                             : w_tiles % 2 == 0);
+  const bool st_ok = !r.pair && r.eg == 2 && a.M <= 128 && w_tiles % 2 == 0;
   bool st2 = env_st == 2;
   if (env_st == 0 && st_ok) {
-    const int parts = std::max(1, (a.grid > 0 ? a.grid : 148) / (r.pair ? 2 : 1));
-    const int64_t per_cta = static_cast<int64_t>(w_tiles / (r.pair ? 4 : 2)) * ((a.K + kBK - 1) / kBK) / parts;
+    const int64_t per_cta = static_cast<int64_t>(w_tiles / 2) * ((a.K + kBK - 1) / kBK) / std::max(1, a.grid > 0 ? a.grid : 148);
     st2 = per_cta >= (a.epi == Epilogue::kResidualAddF32 ? 16 : 48);
   }
   r.st = (st2 && st_ok) ? 2 : 1;
   // one activation stage now covers twice the weight bytes: two stages keep
   // the same activation lead, and the freed 16 KiB buys a fifth weight stage
-  if (r.st == 2 && env_sb <= 0 && !r.pair) r.stages_b = 2;
+  if (r.st == 2 && env_sb <= 0) r.stages_b = 2;
   r.stages_a = (budget - r.stages_b * b_stage - r.eg * kChunkBytes) / (r.st * kAStageBytes);
   if (env_sa > 0) r.stages_a = std::min(env_sa, r.stages_a);
   else if (r.stages_a > 10 / r.st) r.stages_a = 10 / r.st;
   r.kb = (a.K + kBK - 1) / kBK;
-  r.m_tiles = w_tiles / ((r.pair ? 2 : 1) * r.st);  // units along N
+  r.m_tiles = w_tiles / (r.pair ? 2 : r.st);  // units along N
   const int n_tiles_tok = (a.M + r.n_tile - 1) / r.n_tile;
   r.iters = static_cast<int64_t>(r.m_tiles) * n_tiles_tok * r.kb;
   r.epi = static_cast<int>(a.epi);
