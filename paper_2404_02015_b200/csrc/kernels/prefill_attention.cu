@@ -95,6 +95,32 @@ __device__ __forceinline__ uint64_t umma_desc_sw128_mn(uint32_t smem_addr) {
 // rows instead of the c-th heaviest of every round.
 __device__ __forceinline__ int snake_item(int r, int c, int G) { return r * G + ((r & 1) ? G - 1 - c : c); }
 
+// exp2(v * scale - m) of a thread's kKeys scores, packed to bf16 pairs;
+// returns the fp32 sum. kP of every 8 pairs use the FMA-pipe polynomial.
+template <int kP>
+__device__ __forceinline__ float exp_pack(const float (&v)[kKeys], float scale, float m, uint32_t (&pk)[kKeys / 2]) {
+  float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+  for (int i = 0; i < kKeys; i += 2) {
+    float x0, x1, p0, p1;
+    ffma2(x0, x1, v[i], v[i + 1], scale, scale, -m, -m);
+    if (((i >> 1) & 7) < kP) {
+      ex2_poly2(p0, p1, x0, x1);
+    } else {
+      p0 = ex2_ftz(x0);
+      p1 = ex2_ftz(x1);
+    }
+    fadd2(s0, s1, p0, p1);
+    pk[i >> 1] = pack_bf16(p0, p1);
+  }
+  return s0 + s1;
+}
+
+// kPoly of every 8 exp2 pairs of a full tile run as the FMA-pipe polynomial
+// (ex2_poly2) instead of MUFU.EX2. The back-to-back MUFU block held a third of
+// the softmax warps' stall samples (FMA pipe 9% busy); 3 of 8 pairs on the
+// FMA pipe: 4096 tokens x 40 heads 200.8 -> 195.9 us (4 of 8: no better).
+template <int kPoly>
 __global__ void __launch_bounds__(kThreads, 1)
 prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_constant__ CUtensorMap tkv,
                          const PrefillAttnArgs a) {
@@ -276,15 +302,15 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         // masking: the fast path is 3-input max, paired FMA, bare MUFU.EX2,
         // paired add.
         const bool full = kmax >= kKeys - 1;
-        float mx = -INFINITY;
-        if (full) {
-  #pragma unroll
-          for (int i = 0; i < kKeys; i += 2) mx = fmax3(mx, v[i], v[i + 1]);
-        } else {
+        if (!full) {
+          // masked keys -> -inf: MUFU.EX2 maps them to exactly +0 below
   #pragma unroll
           for (int i = 0; i < kKeys; ++i)
-            if (i <= kmax) mx = fmaxf(mx, v[i]);
+            if (i > kmax) v[i] = -INFINITY;
         }
+        float mx = -INFINITY;
+  #pragma unroll
+        for (int i = 0; i < kKeys; i += 2) mx = fmax3(mx, v[i], v[i + 1]);
         bar.mx[g & 1][part][row] = mx;
         asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
   #pragma unroll
@@ -299,29 +325,10 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         const float m_new = move ? m_tile : m_run;
         const float m_use = m_new == -INFINITY ? 0.f : m_new;
         const float alpha = move ? exp2f(m_run - m_use) : 1.f;
-        // P = exp2(s - m) -> packed bf16 in registers while P_{j-1} V_{j-1} runs
-        float psum = 0.f;
+        // P = exp2(s - m) -> packed bf16 in registers while P_{j-1} V_{j-1} runs;
+        // masked tiles keep every exponential on MUFU (exact zeros for -inf)
         uint32_t pk[kKeys / 2];
-        if (full) {
-          float s0 = 0.f, s1 = 0.f;
-  #pragma unroll
-          for (int i = 0; i < kKeys; i += 2) {
-            float x0, x1;
-            ffma2(x0, x1, v[i], v[i + 1], a.scale_log2, a.scale_log2, -m_use, -m_use);
-            const float p0 = ex2_ftz(x0), p1 = ex2_ftz(x1);
-            fadd2(s0, s1, p0, p1);
-            pk[i >> 1] = pack_bf16(p0, p1);
-          }
-          psum = s0 + s1;
-        } else {
-  #pragma unroll
-          for (int i = 0; i < kKeys; i += 2) {
-            const float p0 = i <= kmax ? exp2f(fmaf(v[i], a.scale_log2, -m_use)) : 0.f;
-            const float p1 = i + 1 <= kmax ? exp2f(fmaf(v[i + 1], a.scale_log2, -m_use)) : 0.f;
-            psum += p0 + p1;
-            pk[i >> 1] = pack_bf16(p0, p1);
-          }
-        }
+        const float psum = full ? exp_pack<kPoly>(v, a.scale_log2, m_use, pk) : exp_pack<0>(v, a.scale_log2, m_use, pk);
         if (g > 0) {
           // the previous P V (this item's or the previous item's last) is
           // complete: the P buffer is free and O may be rescaled
@@ -390,13 +397,25 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
 
 size_t prefill_attention_smem() { return kSmemBytes; }
 
-cudaError_t preload_prefill_attention() { return preload(prefill_attention_kernel); }
+// MUX_K3_POLY (0, 3 or 4; read once) picks how many of every 8 exp2 pairs run
+// on the FMA pipe. 3 is the measured best (profiles/r02_k3_exp_poly.txt).
+using PrefillKernel = void (*)(const CUtensorMap, const CUtensorMap, const PrefillAttnArgs);
+static PrefillKernel prefill_kernel_pick() {
+  static const int poly = getenv("MUX_K3_POLY") ? atoi(getenv("MUX_K3_POLY")) : 3;
+  switch (poly) {
+    case 0: return prefill_attention_kernel<0>;
+    case 4: return prefill_attention_kernel<4>;
+    default: return prefill_attention_kernel<3>;
+  }
+}
+
+cudaError_t preload_prefill_attention() { return preload(prefill_kernel_pick()); }
 
 cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
   if (a.T <= 0 || a.n_tiles <= 0) return cudaSuccess;
   static PerDeviceOnce configured;
   cudaError_t ce = configured.run([] {
-    return cudaFuncSetAttribute(prefill_attention_kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+    return cudaFuncSetAttribute(prefill_kernel_pick(), cudaFuncAttributeMaxDynamicSharedMemorySize,
                                 static_cast<int>(kSmemBytes));
   });
   if (ce != cudaSuccess) return ce;
@@ -405,7 +424,7 @@ cudaError_t prefill_attention(const PrefillAttnArgs& a, cudaStream_t stream) {
   std::memcpy(&tkv, a.tmap_qkv, sizeof(CUtensorMap));
   const int n_items = a.n_tiles * a.H;
   const int grid = std::max(1, std::min(n_items, a.max_ctas > 0 ? a.max_ctas : 148));
-  return launch(prefill_attention_kernel, dim3(grid), dim3(kThreads), kSmemBytes, stream, tq, tkv, a);
+  return launch(prefill_kernel_pick(), dim3(grid), dim3(kThreads), kSmemBytes, stream, tq, tkv, a);
 }
 
 }  // namespace mux
