@@ -57,11 +57,11 @@ constexpr int kSoftmaxWarps = 4 * kParts;
 constexpr int kThreads = (kSoftmaxWarps + 1) * 32;  // + 1 TMA/MMA warp
 constexpr uint32_t kTmemCols = 512;          // S0 [0,128) S1 [128,256) O [256,384) P [384,448)
 constexpr uint32_t kPCol = 384;              // P: bf16 pairs, row = lane (the PV MMA's A operand)
-constexpr size_t kSmemBytes = 1024 + kTileBytes /*Q*/ + kStages * 2 * kTileBytes /*K,V*/ +
+constexpr size_t kSmemBytes = 1024 + 2 * kTileBytes /*Q, double-buffered*/ + kStages * 2 * kTileBytes /*K,V*/ +
                               256 /*barriers*/ + 3 * kParts * 128 * 4 /*row exchange*/;
 
 struct Bars {
-  uint64_t q_full;
+  uint64_t q_full[2];  // per Q buffer (item parity)
   uint64_t k_full[kStages];
   uint64_t k_empty[kStages];
   uint64_t v_full[kStages];
@@ -70,7 +70,7 @@ struct Bars {
   uint64_t s_empty[2];
   uint64_t p_full;
   uint64_t o_full;
-  uint64_t q_empty;  // persistent: the item's last Q K^T done, Q buffer reusable
+  uint64_t q_empty[2];  // per Q buffer: the item's last Q K^T done, buffer reusable
   uint64_t o_empty;  // persistent: the softmax warps have read the item's O
   uint32_t tmem;
   uint32_t pad[3];
@@ -127,7 +127,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
   extern __shared__ __align__(1024) uint8_t smem_raw[];
   uint8_t* base = smem_raw + ((1024u - (smem_u32(smem_raw) & 1023u)) & 1023u);
   uint8_t* q_s = base;
-  uint8_t* kv_s = q_s + kTileBytes;                 // [stage][K|V][2 halves]
+  uint8_t* kv_s = q_s + 2 * kTileBytes;             // [stage][K|V][2 halves]
   Bars& bar = *reinterpret_cast<Bars*>(kv_s + kStages * 2 * kTileBytes);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -138,7 +138,10 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
   const int n_items = a.n_tiles * a.H;
 
   if (threadIdx.x == 0) {
-    mbar_init(&bar.q_full, 1);
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&bar.q_full[b], 1);
+      mbar_init(&bar.q_empty[b], 1);
+    }
     for (int s = 0; s < kStages; ++s) {
       mbar_init(&bar.k_full[s], 1);
       mbar_init(&bar.k_empty[s], 1);
@@ -151,7 +154,6 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
     }
     mbar_init(&bar.p_full, kSoftmaxWarps);
     mbar_init(&bar.o_full, 1);
-    mbar_init(&bar.q_empty, 1);
     mbar_init(&bar.o_empty, kSoftmaxWarps);
     fence_barrier_init();
   }
@@ -170,90 +172,120 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
       const uint64_t pol_kv = policy_evict_last();  // re-read by the other q tiles of this head
       const uint32_t idesc_qk = umma_idesc_bf16(kTile, kTile);
       const uint32_t idesc_pv = umma_idesc_bf16(kTile, 128) | (1u << 16);  // B (V) MN-major
-      const uint32_t q_addr = smem_u32(q_s);
-      int jg = 0;  // key tiles issued by this CTA before the current item (global ring / buffer counter)
-      int it = 0;
-      for (int round = 0;; ++round, ++it) {
-        const int item = snake_item(round, blockIdx.x, gridDim.x);
-        if (item >= n_items) break;
-        const int h = item % a.H;
+      // One flat stream of key tiles g over this CTA's items (rounds r), walked
+      // by four cursors: the K loads run two tiles ahead, V one, Q K^T one, and
+      // P V last. Q is double-buffered by item parity, so the next item's Q
+      // load and its first Q K^T are issued while the current item's last
+      // softmax and P V run (short prompts are one or two key tiles per item).
+      struct Cur {
+        int r, j, g, h, row0, q0, n_kv;
+        bool valid;
+      };
+      auto fetch = [&](Cur& c) {
+        const int item = snake_item(c.r, blockIdx.x, gridDim.x);
+        c.valid = item < n_items;
+        if (!c.valid) return;
+        c.h = item % a.H;
         const int tile = a.tiles[item / a.H];
         const int seq = tile >> 16, qt = tile & 0xFFFF;
-        const int s0 = a.seq_start[seq];
-        const int q0 = qt * kTile;
-        const int n_kv = qt + 1;  // causal: key tiles 0..qt
-        if (it > 0) mbar_wait(&bar.q_empty, (it - 1) & 1);  // the previous item's Q K^T are done
-        mbar_arrive_expect_tx(&bar.q_full, kTileBytes);
-        for (int hh = 0; hh < 2; ++hh)
-          tma_load_2d(q_s + hh * kHalfBytes, &tq, &bar.q_full, h * 128 + hh * 64, s0 + q0, pol_q);
-        // K and V of a tile have separate ring slots and barriers: K_j's slot
-        // frees when S_j = Q K_j^T completes (early), V_j's when P_j V_j does,
-        // so the next K load never waits behind a P V. g = global tile index.
-        auto load_k = [&](int j) {
-          const int g = jg + j, st = g % kStages;
-          if (g >= kStages) mbar_wait(&bar.k_empty[st], ((g / kStages) - 1) & 1);
-          uint8_t* dst = kv_s + st * 2 * kTileBytes;
-          mbar_arrive_expect_tx(&bar.k_full[st], kTileBytes);
-          for (int hh = 0; hh < 2; ++hh)
-            tma_load_2d(dst + hh * kHalfBytes, &tkv, &bar.k_full[st], (a.H + h) * 128 + hh * 64, s0 + j * kTile, pol_kv);
-        };
-        auto load_v = [&](int j) {
-          const int g = jg + j, st = g % kStages;
-          if (g >= kStages) mbar_wait(&bar.v_empty[st], ((g / kStages) - 1) & 1);
-          uint8_t* dst = kv_s + st * 2 * kTileBytes + kTileBytes;
-          mbar_arrive_expect_tx(&bar.v_full[st], kTileBytes);
-          for (int hh = 0; hh < 2; ++hh)
-            tma_load_2d(dst + hh * kHalfBytes, &tkv, &bar.v_full[st], (2 * a.H + h) * 128 + hh * 64, s0 + j * kTile,
-                        pol_kv);
-        };
-        auto issue_qk = [&](int j) {
-          const int g = jg + j, st = g % kStages, sb = g & 1;
-          mbar_wait(&bar.k_full[st], (g / kStages) & 1);
-          if (g >= 2) mbar_wait(&bar.s_empty[sb], ((g >> 1) - 1) & 1);
-          tc_fence_after();
-          const uint32_t k_addr = smem_u32(kv_s + st * 2 * kTileBytes);
-  #pragma unroll
-          for (int kk = 0; kk < 8; ++kk) {
-            const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
-            umma_bf16(tmem + sb * kTile, umma_desc_sw128(q_addr + off), umma_desc_sw128(k_addr + off), idesc_qk,
-                      kk > 0 ? 1u : 0u);
-          }
-          umma_commit(&bar.s_full[sb]);
-          umma_commit(&bar.k_empty[st]);
-        };
-        load_k(0);
-        load_v(0);
-        if (n_kv > 1) {
-          load_k(1);
-          load_v(1);
+        c.row0 = a.seq_start[seq];
+        c.q0 = qt * kTile;
+        c.n_kv = qt + 1;  // causal: key tiles 0..qt
+      };
+      auto advance = [&](Cur& c) {
+        ++c.g;
+        if (++c.j == c.n_kv) {
+          ++c.r;
+          c.j = 0;
+          fetch(c);
         }
-        mbar_wait(&bar.q_full, it & 1);
-        issue_qk(0);
-        for (int j = 0; j < n_kv; ++j) {
-          const int g = jg + j;
-          if (j + 1 < n_kv) issue_qk(j + 1);
-          if (j + 1 == n_kv) umma_commit(&bar.q_empty);  // fires once this item's last Q K^T is done
-          // K_{j+2} goes into S_j's K slot as soon as S_j is done (issued one
-          // iteration ago): a full iteration ahead of Q K_{j+2}^T.
-          if (j + kStages < n_kv) load_k(j + kStages);
-          if (j + 1 < n_kv && j + 1 >= kStages) load_v(j + 1);  // waits for P_{j-1} V_{j-1}
+      };
+      Cur start{0, 0, 0, 0, 0, 0, 0, false};
+      fetch(start);
+      auto load_q = [&](const Cur& c) {
+        const int b = c.r & 1;
+        if (c.r >= 2) mbar_wait(&bar.q_empty[b], ((c.r >> 1) - 1) & 1);  // item r-2's Q K^T are done
+        mbar_arrive_expect_tx(&bar.q_full[b], kTileBytes);
+        for (int hh = 0; hh < 2; ++hh)
+          tma_load_2d(q_s + b * kTileBytes + hh * kHalfBytes, &tq, &bar.q_full[b], c.h * 128 + hh * 64, c.row0 + c.q0,
+                      pol_q);
+      };
+      // K and V of a tile have separate ring slots and barriers: K_g's slot
+      // frees when S_g = Q K_g^T completes (early), V_g's when P_g V_g does,
+      // so the next K load never waits behind a P V.
+      auto load_k = [&](const Cur& c) {
+        if (c.j == 0) load_q(c);
+        const int st = c.g % kStages;
+        if (c.g >= kStages) mbar_wait(&bar.k_empty[st], ((c.g / kStages) - 1) & 1);
+        uint8_t* dst = kv_s + st * 2 * kTileBytes;
+        mbar_arrive_expect_tx(&bar.k_full[st], kTileBytes);
+        for (int hh = 0; hh < 2; ++hh)
+          tma_load_2d(dst + hh * kHalfBytes, &tkv, &bar.k_full[st], (a.H + c.h) * 128 + hh * 64, c.row0 + c.j * kTile,
+                      pol_kv);
+      };
+      auto load_v = [&](const Cur& c) {
+        const int st = c.g % kStages;
+        if (c.g >= kStages) mbar_wait(&bar.v_empty[st], ((c.g / kStages) - 1) & 1);
+        uint8_t* dst = kv_s + st * 2 * kTileBytes + kTileBytes;
+        mbar_arrive_expect_tx(&bar.v_full[st], kTileBytes);
+        for (int hh = 0; hh < 2; ++hh)
+          tma_load_2d(dst + hh * kHalfBytes, &tkv, &bar.v_full[st], (2 * a.H + c.h) * 128 + hh * 64,
+                      c.row0 + c.j * kTile, pol_kv);
+      };
+      auto issue_qk = [&](const Cur& c) {
+        const int st = c.g % kStages, sb = c.g & 1, b = c.r & 1;
+        mbar_wait(&bar.k_full[st], (c.g / kStages) & 1);
+        if (c.g >= 2) mbar_wait(&bar.s_empty[sb], ((c.g >> 1) - 1) & 1);
+        if (c.j == 0) mbar_wait(&bar.q_full[b], (c.r >> 1) & 1);
+        tc_fence_after();
+        const uint32_t q_addr = smem_u32(q_s + b * kTileBytes);
+        const uint32_t k_addr = smem_u32(kv_s + st * 2 * kTileBytes);
+  #pragma unroll
+        for (int kk = 0; kk < 8; ++kk) {
+          const uint32_t off = (kk >> 2) * kHalfBytes + (kk & 3) * 32;
+          umma_bf16(tmem + sb * kTile, umma_desc_sw128(q_addr + off), umma_desc_sw128(k_addr + off), idesc_qk,
+                    kk > 0 ? 1u : 0u);
+        }
+        umma_commit(&bar.s_full[sb]);
+        umma_commit(&bar.k_empty[st]);
+        if (c.j + 1 == c.n_kv) umma_commit(&bar.q_empty[b]);  // fires once the item's last Q K^T is done
+      };
+      if (start.valid) {
+        Cur kl = start, vl = start, qk = start, pv = start;
+        for (int n = 0; n < kStages && kl.valid; ++n, advance(kl)) load_k(kl);
+        for (int n = 0; n < kStages && vl.valid; ++n, advance(vl)) load_v(vl);
+        issue_qk(qk);
+        advance(qk);
+        while (pv.valid) {
+          if (qk.valid) {  // S_{g+1} (possibly the next item's first) while the softmax reads S_g
+            issue_qk(qk);
+            advance(qk);
+          }
+          if (kl.valid) {  // K_{g+2} into S_g's K slot as soon as S_g is done
+            load_k(kl);
+            advance(kl);
+          }
+          if (vl.valid && vl.g == pv.g + 1) {  // V_{g+1}: waits for P_{g-1} V_{g-1}
+            load_v(vl);
+            advance(vl);
+          }
           // the previous item's O must have been read before P_0 V_0 overwrites it
-          if (j == 0 && it > 0) mbar_wait(&bar.o_empty, (it - 1) & 1);
-          // O_j = P_j V_j once the softmax has written P_j
-          mbar_wait(&bar.p_full, g & 1);
-          const int st = g % kStages;
-          mbar_wait(&bar.v_full[st], (g / kStages) & 1);
+          if (pv.j == 0 && pv.r > 0) mbar_wait(&bar.o_empty, (pv.r - 1) & 1);
+          // O_g = P_g V_g once the softmax has written P_g
+          mbar_wait(&bar.p_full, pv.g & 1);
+          const int st = pv.g % kStages;
+          mbar_wait(&bar.v_full[st], (pv.g / kStages) & 1);
           tc_fence_after();
           const uint32_t v_addr = smem_u32(kv_s + st * 2 * kTileBytes + kTileBytes);
   #pragma unroll
           for (int kk = 0; kk < 8; ++kk) {
             umma_ts_bf16(tmem + 2 * kTile, tmem + kPCol + kk * 8, umma_desc_sw128_mn(v_addr + kk * 2048), idesc_pv,
-                         (j > 0 || kk > 0) ? 1u : 0u);
+                         (pv.j > 0 || kk > 0) ? 1u : 0u);
           }
           umma_commit(&bar.o_full);
           umma_commit(&bar.v_empty[st]);
+          advance(pv);
         }
-        jg += n_kv;
       }
     }
     __syncwarp();
