@@ -257,7 +257,10 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         issue_qk(qk);
         advance(qk);
         while (pv.valid) {
-          if (qk.valid) {  // S_{g+1} (possibly the next item's first) while the softmax reads S_g
+          // S_{g+1} while the softmax reads S_g; the next item's first S goes
+          // after this item's last P V, which the epilogue waits for
+          const bool qk_after = qk.valid && qk.r != pv.r;
+          if (qk.valid && !qk_after) {
             issue_qk(qk);
             advance(qk);
           }
@@ -284,6 +287,10 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
           }
           umma_commit(&bar.o_full);
           umma_commit(&bar.v_empty[st]);
+          if (qk_after) {
+            issue_qk(qk);
+            advance(qk);
+          }
           advance(pv);
         }
       }
