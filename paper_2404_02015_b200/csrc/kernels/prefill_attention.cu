@@ -74,6 +74,7 @@ struct Bars {
   uint64_t o_empty;  // persistent: the softmax warps have read the item's O
   uint32_t tmem;
   uint32_t pad[3];
+  int4 items[4];  // MMA thread: descriptor ring {h, row0, q0, n_kv} by round & 3
   float mx[2][kParts][128];  // [tile parity][key part][row]: partial row maxima
   float ls[kParts][128];     // [key part][row]: partial row sums (end)
 };
@@ -181,27 +182,42 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         int r, j, g, h, row0, q0, n_kv;
         bool valid;
       };
-      auto fetch = [&](Cur& c) {
-        const int item = snake_item(c.r, blockIdx.x, gridDim.x);
-        c.valid = item < n_items;
-        if (!c.valid) return;
-        c.h = item % a.H;
-        const int tile = a.tiles[item / a.H];
-        const int seq = tile >> 16, qt = tile & 0xFFFF;
-        c.row0 = a.seq_start[seq];
-        c.q0 = qt * kTile;
-        c.n_kv = qt + 1;  // causal: key tiles 0..qt
+      // Descriptors are loaded once per item by the leading (K-load) cursor
+      // into a 4-deep ring the trailing cursors read (they lag by at most
+      // three key tiles); the next item's tile word is prefetched a round
+      // ahead, so entering an item costs one global-load latency, not two.
+      int pf_tile = 0;
+      auto fill = [&](int r) {
+        const int item = snake_item(r, blockIdx.x, gridDim.x);
+        int4 d = make_int4(0, 0, 0, 0);  // n_kv = 0: past the last item
+        if (item < n_items) {
+          const int tile = r == 0 ? a.tiles[item / a.H] : pf_tile;
+          const int qt = tile & 0xFFFF;
+          d = make_int4(item % a.H, a.seq_start[tile >> 16], qt * kTile, qt + 1);  // causal: key tiles 0..qt
+          const int item_n = snake_item(r + 1, blockIdx.x, gridDim.x);
+          pf_tile = item_n < n_items ? a.tiles[item_n / a.H] : 0;
+        }
+        bar.items[r & 3] = d;
       };
-      auto advance = [&](Cur& c) {
+      auto fetch = [&](Cur& c, bool lead) {
+        if (lead) fill(c.r);
+        const int4 d = bar.items[c.r & 3];
+        c.valid = d.w > 0;
+        c.h = d.x;
+        c.row0 = d.y;
+        c.q0 = d.z;
+        c.n_kv = d.w;
+      };
+      auto advance = [&](Cur& c, bool lead = false) {
         ++c.g;
         if (++c.j == c.n_kv) {
           ++c.r;
           c.j = 0;
-          fetch(c);
+          fetch(c, lead);
         }
       };
       Cur start{0, 0, 0, 0, 0, 0, 0, false};
-      fetch(start);
+      fetch(start, true);
       auto load_q = [&](const Cur& c) {
         const int b = c.r & 1;
         if (c.r >= 2) mbar_wait(&bar.q_empty[b], ((c.r >> 1) - 1) & 1);  // item r-2's Q K^T are done
@@ -252,7 +268,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
       };
       if (start.valid) {
         Cur kl = start, vl = start, qk = start, pv = start;
-        for (int n = 0; n < kStages && kl.valid; ++n, advance(kl)) load_k(kl);
+        for (int n = 0; n < kStages && kl.valid; ++n, advance(kl, true)) load_k(kl);
         for (int n = 0; n < kStages && vl.valid; ++n, advance(vl)) load_v(vl);
         issue_qk(qk);
         advance(qk);
@@ -266,7 +282,7 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
           }
           if (kl.valid) {  // K_{g+2} into S_g's K slot as soon as S_g is done
             load_k(kl);
-            advance(kl);
+            advance(kl, true);
           }
           if (vl.valid && vl.g == pv.g + 1) {  // V_{g+1}: waits for P_{g-1} V_{g-1}
             load_v(vl);
@@ -309,14 +325,24 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
     // this part's keys in P's SW128 K-major image: half (part*kKeys)/64, 16-B chunks from (part*kKeys%64)/8
     const uint32_t o_addr = tmem + lane_base + 2 * kTile + part * kKeys;
     int jg = 0;
-    for (int round = 0;; ++round) {
-      const int item = snake_item(round, blockIdx.x, gridDim.x);
-      if (item >= n_items) break;
+    // Item descriptors are prefetched: the next item's tile word is loaded
+    // when an item starts, its sequence bounds before the epilogue, so no
+    // item begins on two dependent global loads (short prompts: 1-2 key tiles
+    // per item).
+    int item = snake_item(0, blockIdx.x, gridDim.x);
+    int tile_c = 0, s0_c = 0, s1_c = 0;
+    if (item < n_items) {
+      tile_c = a.tiles[item / a.H];
+      s0_c = a.seq_start[tile_c >> 16];
+      s1_c = a.seq_start[(tile_c >> 16) + 1];
+    }
+    for (int round = 0; item < n_items; ++round) {
       const int h = item % a.H;
-      const int tile = a.tiles[item / a.H];
-      const int seq = tile >> 16, qt = tile & 0xFFFF;
-      const int s0 = a.seq_start[seq];
-      const int len = a.seq_start[seq + 1] - s0;
+      const int qt = tile_c & 0xFFFF;
+      const int s0 = s0_c;
+      const int len = s1_c - s0_c;
+      const int item_n = snake_item(round + 1, blockIdx.x, gridDim.x);
+      const int tile_n = item_n < n_items ? a.tiles[item_n / a.H] : 0;
       const int q0 = qt * kTile;
       const int n_kv = qt + 1;
       const int qi = q0 + row;               // sequence-local query index
@@ -395,6 +421,10 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
         __syncwarp();
         if (lane == 0) mbar_arrive(&bar.p_full);
       }
+      if (item_n < n_items) {  // in flight during the epilogue
+        s0_c = a.seq_start[tile_n >> 16];
+        s1_c = a.seq_start[(tile_n >> 16) + 1];
+      }
       bar.ls[part][row] = l_run;
       asm volatile("bar.sync 1, %0;" ::"n"(kSoftmaxWarps * 32) : "memory");
       float l_tot = 0.f;
@@ -422,6 +452,8 @@ prefill_attention_kernel(const __grid_constant__ CUtensorMap tq, const __grid_co
       __syncwarp();
       if (lane == 0) mbar_arrive(&bar.o_empty);
       jg += n_kv;
+      item = item_n;
+      tile_c = tile_n;
     }
   }
   tc_fence_before();
