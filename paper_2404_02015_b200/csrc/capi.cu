@@ -1075,6 +1075,8 @@ int mux_prefill_attention(const void* q, const void* qkv, void* out, const int32
     a.H = H;
     a.T = T;
     a.scale_log2 = 1.4426950408889634f / std::sqrt(128.f);
+    // test hook: a small persistent grid puts many items on each CTA
+    if (const char* e = std::getenv("MUX_K3_CTAS")) a.max_ctas = std::atoi(e);
     mux::check_cuda(mux::prefill_attention(a, s), "prefill_attention");
     mux::check_cuda(cudaStreamSynchronize(s), "prefill_attention sync");
   });

@@ -290,3 +290,28 @@ def test_prefill_attention_tcgen05_matches_oracle(cuda, lens, H, seed):
                                           qkv[:, 2].float().numpy(), lens)
     err = np.abs(got - ref).max() / max(1e-6, np.abs(ref).max())
     assert err <= 1e-2, err
+
+
+@pytest.mark.parametrize("ctas", [1, 3, 7])
+def test_prefill_attention_many_items_per_cta(cuda, monkeypatch, ctas):
+    """K3's persistent schedule with a small grid (MUX_K3_CTAS): dozens of
+    items per CTA, mostly one key tile each, so the producer's cursors cross
+    items every tile (4-deep descriptor ring, Q buffers by item parity,
+    prefetched item descriptors) -- same oracle bound as above."""
+    import torch
+    monkeypatch.setenv("MUX_K3_CTAS", str(ctas))
+    rng = np.random.default_rng(10 + ctas)
+    lens = [int(x) for x in rng.integers(1, 140, size=23)] + [1, 128, 129, 300, 257]
+    H = 3
+    g = torch.Generator().manual_seed(ctas)
+    T = sum(lens)
+    qkv = (torch.randn(T, 3, H, 128, generator=g) * 2.0).to(torch.bfloat16)
+    q = (torch.randn(T, H, 128, generator=g) * 2.0).to(torch.bfloat16)
+    out = torch.zeros(T, H, 128, dtype=torch.bfloat16)
+    qd, qkvd, od = q.cuda(), qkv.cuda(), out.cuda()
+    mux.prefill_attention(qd, qkvd, od, lens)
+    got = od.float().cpu().numpy()
+    ref = llama_ref.prefill_attention_ref(q.float().numpy(), qkv[:, 1].float().numpy(),
+                                          qkv[:, 2].float().numpy(), lens)
+    err = np.abs(got - ref).max() / max(1e-6, np.abs(ref).max())
+    assert err <= 1e-2, err
