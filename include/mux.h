@@ -251,7 +251,8 @@ MUX_API int mux_kv_append(const void* qkv, void* q_out, void* pool, const int32_
 /* K3: causal varlen prefill attention (the attention term of prefill_latency,
  * cost_model.cpp:75-83) on tcgen05. q [T][H][128] bf16 (rotated), qkv
  * [T][3][H][128] bf16 (k rotated), out [T][H][128] bf16; seq_lens (host)
- * split the T tokens into nseq prompts. Synchronises the stream. */
+ * split the T tokens into nseq prompts. Synchronises the stream. Environment
+ * (read per call, tests only): MUX_K3_CTAS caps the persistent grid. */
 MUX_API int mux_prefill_attention(const void* q, const void* qkv, void* out, const int32_t* seq_lens, int nseq,
                                   int H, void* stream);
 /* RoPE table [positions][64][(cos,sin)] fp32, theta 10000, head_dim 128. */
