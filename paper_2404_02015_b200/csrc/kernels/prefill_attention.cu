@@ -6,8 +6,10 @@
 // kv_append has rotated q and k (RoPE) and written k/v into the head-blocks
 // (the K/V read here are the same bytes, straight from the QKV GEMM output).
 //
-// One CTA = (128-query tile of one sequence, head). Flash-attention over
-// 128-key tiles with both contractions on tcgen05:
+// Persistent: each CTA walks a list of items (128-query tile of one sequence,
+// head); its MMA warp streams the items' key tiles back to back, Q
+// double-buffered by item. Flash-attention over 128-key tiles with both
+// contractions on tcgen05:
 //   S_j = Q K_j^T      UMMA 128x128x128, A = Q (smem, K-major), B = K_j (smem,
 //                      K-major), fp32 accumulator in TMEM (double-buffered so
 //                      S_{j+1} is computed while the softmax reads S_j)
@@ -18,7 +20,8 @@
 // Warp 8 = TMA producer + MMA issuer (one elected lane); warps 0-7 = softmax,
 // two warps per TMEM lane quarter, a thread owns half (64 keys / 64 output
 // dims) of one query row: online max/sum in fp32, causal + sequence-end
-// masking. The output accumulates in TMEM across key tiles; when
+// masking (masked scores set to -inf), exp2 on MUFU for 5 of 8 pairs and as an
+// FMA-pipe polynomial for 3. The output accumulates in TMEM across key tiles; when
 // a row's max moves, its O row is rescaled in place (tcgen05.ld/st) before
 // the next P V is issued.
 // K/V tiles stream through a kStages-deep TMA ring (SWIZZLE_128B boxes of 64
