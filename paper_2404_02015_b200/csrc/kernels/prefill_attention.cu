@@ -20,7 +20,7 @@
 // Warp 8 = TMA producer + MMA issuer (one elected lane); warps 0-7 = softmax,
 // two warps per TMEM lane quarter, a thread owns half (64 keys / 64 output
 // dims) of one query row: online max/sum in fp32, causal + sequence-end
-// masking (masked scores set to -inf), exp2 on MUFU for 5 of 8 pairs and as an
+// masking (masked scores set to -inf); in full tiles exp2 runs on MUFU for 5 of 8 pairs and as an
 // FMA-pipe polynomial for 3. The output accumulates in TMEM across key tiles; when
 // a row's max moves, its O row is rescaled in place (tcgen05.ld/st) before
 // the next P V is issued.
