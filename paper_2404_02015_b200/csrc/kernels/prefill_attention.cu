@@ -56,6 +56,7 @@ constexpr int kStages = 2;
 #endif
 constexpr int kParts = MUX_K3_PARTS;
 constexpr int kKeys = kTile / kParts;
+static_assert(kKeys == 64, "P is written as one 32-column tcgen05.st of bf16 pairs per part: kParts must be 2");
 constexpr int kSoftmaxWarps = 4 * kParts;
 constexpr int kThreads = (kSoftmaxWarps + 1) * 32;  // + 1 TMA/MMA warp
 constexpr uint32_t kTmemCols = 512;          // S0 [0,128) S1 [128,256) O [256,384) P [384,448)
